@@ -1,0 +1,358 @@
+#!/usr/bin/env python
+"""Benchmark: pose hypotheses rendered+scored per second (BASELINE.json).
+
+Workload (N=1): configs[0], the configuration the metric is quoted on
+(120x160 = H x W): a 1,000-voxel blob, 1,024 6-DoF hypotheses per step
+(8x8x16 lattice zipped with vMF(kappa=1000) rotations), windowed likelihood
+r=5 mm, 3x3 window.  One step = score the batch on the GPU (pose grid
+generated on the device, fused raster + likelihood, rendered images never
+leave the SM) + the stage reduction (argmax, logsumexp, one categorical
+draw).  Weak scaling: at N GPUs each rank scores its own 1,024-hypothesis
+batch against the shared observation, scores are all-gathered over NCCL and
+every rank reduces the global array in one fixed order.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+--impl reference times the reference's algorithm on the host cores (the CPU
+oracle port; the reference itself cannot be compiled here).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "pose hypotheses rendered+scored/sec at 120x160 @1/2/4/8 B200; tracking FPS"
+UNIT = "hypotheses/s"
+BATCH = 1024
+
+
+def _ops_per_hyp(c: dict, n_sigma: int, n_noise: int, n: int) -> float:
+    """Algorithmic op count per hypothesis (BASELINE.md §3 / SURVEY.md 8d),
+    from the oracle's exact counters."""
+    return (18 * c["vertices"] + 45 * c["triangles"] + 18 * c["bbox_px"] + 10 * c["fragments"]
+            + 6 * c["rend_valid"] + (8 + 3 * n_sigma) * c["pairs"]
+            + 3 * n_noise * c["obs_valid"]) / n
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def build_workload_oracle(seed=0, shard=0):
+    from oracle import pyoracle as O
+    from paper_2312_08715_b200 import configs
+    rf = lambda k, v, t, p: O.render(k, [(v, t, p)])
+    return configs.cfg1(rf, O.voxel_to_mesh, seed=seed, shard=shard)
+
+
+def cpu_baseline(w, seconds=12.0, threads=None, counters=True):
+    """The oracle port (the reference's algorithm, scalar fp64) timed on this
+    host's cores over repeated passes of the 1,024-hypothesis batch."""
+    from oracle import pyoracle as O
+    threads = threads or cpu_threads()
+    poses = w.grid_poses()
+    done, t0, cnt = 0, time.perf_counter(), None
+    scores = None
+    while True:
+        if counters and cnt is None:
+            scores, _, cnt = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses,
+                                           w.noise, w.sigma_max, w.window, threads=threads,
+                                           counters=True)
+        else:
+            scores, _ = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
+                                      w.sigma_max, w.window, threads=threads)
+        done += poses.shape[0]
+        el = time.perf_counter() - t0
+        if el >= seconds or done >= 64 * poses.shape[0]:
+            break
+    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{done} hypotheses ({done // poses.shape[0]} passes of the cfg1 batch), "
+                      f"{el:.1f} s"}, cnt, scores
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm (oracle port) on host cores."""
+    if rank != 0:
+        return
+    w = build_workload_oracle()
+    from oracle import pyoracle as O
+    threads = cpu_threads()
+    poses = w.grid_poses()
+    for _ in range(args.warmup):
+        O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise, w.sigma_max,
+                      w.window, threads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        s, _ = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
+                             w.sigma_max, w.window, threads=threads)
+        probs, _ = O.normalize(s[:, 0])
+        O.argmax(s[:, 0])
+        O.sample_categorical(probs, O.rng_seed(7))
+    el = time.perf_counter() - t0
+    v = args.steps * BATCH / el
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded voxel blob, BASELINE cfg1)", "impl": "reference",
+            "config": {"workload": "configs[0]: single-object scoring 160x120 (WxH), 1,024 "
+                                   "hypotheses/step", "hypotheses_per_step": BATCH},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+                             "sample": f"{args.steps} steps x {BATCH} hypotheses (full batch)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return run_reference(args, rank, world)
+
+    import torch
+    import torch.distributed as dist
+    from paper_2312_08715_b200 import b3d, configs
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    stream = torch.cuda.current_stream(dev)
+    ctx = b3d.GpuContext(local)
+    ctx.set_stream(stream.cuda_stream)
+
+    def render_fn(k, v, t, p):
+        ctx.set_camera(b3d.Intrinsics(*k.as_tuple()))
+        mid = ctx.upload_mesh(v, t)
+        d, _ = ctx.render_poses(mid, np.asarray(p, dtype=np.float64)[None], with_ids=False)
+        return d[0]
+
+    w = configs.cfg1(render_fn, b3d.voxel_to_mesh, seed=0, shard=rank)
+    ctx.set_camera(b3d.Intrinsics(*w.k.as_tuple()))
+    mid = ctx.upload_mesh(w.vertices, w.triangles)
+    ctx.set_likelihood(w.noise, w.sigma_max, w.window)
+    n_all = BATCH * world
+
+    # ---- device-resident arm (value)
+    d_obs = torch.from_numpy(w.observed).to(dev)
+    ctx.set_observation(d_obs)
+    d_rot = torch.from_numpy(w.rotations).to(dev)
+    grid = ctx.make_grid(w.center, w.extent, w.count, d_rot, w.grid_mode)
+    d_scores = torch.zeros((BATCH, 1), dtype=torch.float64, device=dev)
+    d_status = torch.zeros(BATCH, dtype=torch.uint8, device=dev)
+    d_all = torch.zeros((n_all, 1), dtype=torch.float64, device=dev) if world > 1 else d_scores
+    d_rng = torch.from_numpy(b3d.rng_seed(7).view(np.int64)).to(dev)
+    d_res = torch.zeros(64, dtype=torch.uint8, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
+
+    def step(ev_k=None):
+        ctx.score_grid(mid, grid, d_scores, d_status)
+        if ev_k is not None:
+            ev_k.record(stream)
+        if world > 1:
+            dist.all_gather_into_tensor(d_all, d_scores)
+        ctx.stage_reduce(d_all, n=n_all, rng_state=d_rng, out=d_res)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True),
+            torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(local)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    time.sleep(0.3)
+    for i in range(args.steps):
+        flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
+        e0, ek, e1 = evs[i]
+        e0.record(stream)
+        step(ek)
+        e1.record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = [e0.elapsed_time(e1) for e0, _, e1 in evs]
+    kern_ms = [e0.elapsed_time(ek) for e0, ek, _ in evs]
+    total_ms = sum(step_ms)
+
+    # ---- end-to-end arm: public C ABI with pinned host buffers
+    ctx.set_stream(None)
+    h_obs = torch.from_numpy(w.observed).pin_memory().numpy()
+    h_poses = torch.from_numpy(w.grid_poses()).pin_memory().numpy()
+    h_scores = torch.zeros((BATCH, 1), dtype=torch.float64).pin_memory().numpy()
+    h_status = torch.zeros(BATCH, dtype=torch.uint8).pin_memory().numpy()
+    h_all = torch.zeros((n_all, 1), dtype=torch.float64).pin_memory().numpy()
+    h_rng = b3d.rng_seed(7)
+
+    def e2e_step():
+        ctx.set_observation(h_obs)
+        ctx.score_poses(mid, h_poses, h_scores, h_status)
+        if world > 1:
+            t = torch.from_numpy(h_scores).to(dev)
+            g = torch.empty((n_all, 1), dtype=torch.float64, device=dev)
+            dist.all_gather_into_tensor(g, t)
+            h_all[:] = g.cpu().numpy()
+            src = h_all
+        else:
+            src = h_scores
+        return ctx.stage_reduce(src, n=n_all, rng_state=h_rng)
+
+    for _ in range(args.warmup):
+        e2e_step()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e2e_ms = []
+    for i in range(args.steps):
+        flush.fill_(float(i))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e2e_step()
+        e2e_ms.append(1e3 * (time.perf_counter() - t0))
+    e2e_total = sum(e2e_ms)
+    clk = clocks.stop()
+
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_total = t.tolist()
+
+    if rank == 0:
+        value = args.steps * n_all / (total_ms * 1e-3)
+        e2e_value = args.steps * n_all / (e2e_total * 1e-3)
+        kern_avg = statistics.mean(kern_ms) * 1e-3
+        peaks = {}
+        try:
+            import ctypes
+            L = ctypes.CDLL(os.path.join(ROOT, "paper_2312_08715_b200", "_lib", "libb3d_peaks.so"))
+            r = ctypes.c_double()
+            L.b3d_bench_fp64_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+            if L.b3d_bench_fp64_rate(local, ctypes.byref(r)) == 0:
+                peaks["fp64_nofma_ops"] = r.value
+        except Exception as e:  # pragma: no cover
+            peaks["error"] = str(e)
+        cpu = None
+        cnt = None
+        if not args.no_cpu_baseline:
+            cpu, cnt, cpu_scores = cpu_baseline(w, seconds=args.cpu_seconds)
+        roof = None
+        if cnt is not None and "fp64_nofma_ops" in peaks:
+            ops = _ops_per_hyp(cnt, 1, 1, BATCH)
+            achieved = ops * BATCH / kern_avg
+            roof = {"bound": "sm_fp64", "achieved": achieved / 1e12,
+                    "peak": peaks["fp64_nofma_ops"] / 1e12, "unit": "Tops/s",
+                    "frac": achieved / peaks["fp64_nofma_ops"], "traffic": None,
+                    "ops_per_hypothesis": ops,
+                    "kernel_ms": kern_avg * 1e3,
+                    "peak_source": "measured in-run (non-FMA DMUL/DADD microbenchmark)"}
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded 1,000-voxel Eden blob, noisy rendered observation)",
+            "config": {"workload": "configs[0]: single-object scoring 160x120 (WxH), "
+                                   "1,024 hypotheses/step/GPU",
+                       "hypotheses_per_step": n_all, "image": "120x160", "window": "3x3",
+                       "triangles": int(w.triangles.shape[0]),
+                       "vertices": int(w.vertices.shape[0]),
+                       "l2": "flushed between timed steps (256 MB write)",
+                       "parallelism": f"dp{world} (hypothesis shards, NCCL score all-gather)"},
+            "gpu_launches": 2 * args.steps,
+            "e2e": {"value": e2e_value, "unit": UNIT,
+                    "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 8 * n_all + 40),
+                    "d2h_bytes_per_step": int(h_scores.nbytes + h_status.nbytes + 64 + 40),
+                    "ms_per_step": e2e_total / args.steps},
+            "clocks": clk,
+            "roofline": roof,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,189 @@
+/*
+ * b3d_b200.h -- C ABI of the B200-native pose-enumeration hot path.
+ *
+ * Drop-in boundary for the reference's C API (proj/include/b3d/b3d.h): same
+ * conventions -- opaque handles created by *_create and released by the
+ * matching *_destroy (b3d.h:4-7), every fallible call returns b3d_status
+ * (b3d.h:26-32) and leaves a message in the thread-local b3d_last_error()
+ * (b3d_capi.cpp:22,118), no exception crosses the ABI (guarded(),
+ * b3d_capi.cpp:33-48), caller-owned output buffers (b3d.h:130-131).
+ *
+ * Part 1 keeps the reference's on-path entry points with their exact
+ * signatures and semantics (GPU-backed).  Part 2 adds the batched entry
+ * points the reference's internal seams correspond to:
+ * render-many (render_batch, renderer.hpp:42-43), score-many
+ * (score_cells / windowed_log_likelihood_multi, inference.hpp:111-113,
+ * likelihood.hpp:65-69) and the enumerate/reduce/sample stage
+ * (coarse_to_fine_propose / sample_categorical, inference.hpp:136-138,
+ * inference.cpp:345-353).
+ *
+ * Memory: every pointer argument of part 2 may be a host pointer or a CUDA
+ * device pointer (detected with cudaPointerGetAttributes).  A call whose
+ * pointers are all device pointers is asynchronous on the context's stream;
+ * otherwise the call copies through the stream and returns when the results
+ * are in the caller's buffers.
+ */
+#ifndef B3D_B200_H
+#define B3D_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#define B3D_API __attribute__((visibility("default")))
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ===================== part 1: reference-compatible ===================== */
+
+/* b3d.h:26-32 */
+typedef enum b3d_status {
+  B3D_OK = 0,
+  B3D_ERROR = 1,
+  B3D_ERROR_CONFIG = 2,
+  B3D_ERROR_IO = 3,
+  B3D_ERROR_NUMERIC = 4
+} b3d_status;
+
+/* b3d.h:45-49 */
+typedef struct b3d_intrinsics {
+  double fx, fy, cx, cy;
+  uint32_t width, height;
+  double near_m, far_m;
+} b3d_intrinsics;
+
+/* b3d.h:52-55: unit quaternion (w, x, y, z) plus translation, meters. */
+typedef struct b3d_pose {
+  double qw, qx, qy, qz;
+  double tx, ty, tz;
+} b3d_pose;
+
+/* b3d.h:34,37 */
+B3D_API const char* b3d_version(void);
+B3D_API const char* b3d_last_error(void);
+
+/* b3d.h:39,59-68 (in-memory subset; SDPT file I/O is out of scope) */
+typedef struct b3d_depth_image b3d_depth_image;
+B3D_API b3d_status b3d_depth_image_create(uint32_t width, uint32_t height,
+                                          const float* depth, b3d_depth_image** out);
+B3D_API uint32_t b3d_depth_image_width(const b3d_depth_image* img);
+B3D_API uint32_t b3d_depth_image_height(const b3d_depth_image* img);
+B3D_API const float* b3d_depth_image_data(const b3d_depth_image* img);
+B3D_API void b3d_depth_image_destroy(b3d_depth_image* img);
+
+/* b3d.h:110-115 -- windowed depth likelihood; window < 0 selects the
+ * untruncated form.  Same semantics as the reference (b3d_capi.cpp:276-295),
+ * including B3D_ERROR for an all-sentinel rendered image; runs on GPU 0. */
+B3D_API b3d_status b3d_log_likelihood(const b3d_depth_image* observed,
+                                      const b3d_depth_image* rendered,
+                                      const b3d_intrinsics* k, double p_outlier,
+                                      double sigma_noise, double sigma_max,
+                                      int window, double* out);
+
+/* ===================== part 2: batched GPU entry points ================= */
+
+typedef struct b3d_gpu_context b3d_gpu_context;
+
+/* NoiseParams (likelihood.hpp:10-13) */
+typedef struct b3d_noise {
+  double p_outlier;
+  double sigma_noise;
+} b3d_noise;
+
+enum { B3D_PREFACTOR_PRINTED = 0, B3D_PREFACTOR_UNIFORM = 1 };
+enum { B3D_GRID_PRODUCT = 0, B3D_GRID_ZIP = 1 };
+enum { B3D_MAX_NOISE = 4 };
+
+/* 6-DoF hypothesis grid generated on the device.  Translation lattice per
+ * axis: center.t - extent + 2*extent*i/(n-1) (tracking.cpp:34-35); rotation
+ * q = normalized(center.q * dq[r]) for a table of unit quaternions dq
+ * (w,x,y,z).  PRODUCT: index = ((ix*ny + iy)*nz + iz)*n_rot + r.  ZIP:
+ * index i pairs translation i with rotation i (nx*ny*nz == n_rot). */
+typedef struct b3d_pose_grid {
+  b3d_pose center;
+  double extent[3];
+  uint32_t count[3];
+  const double* rotations; /* n_rot x 4 */
+  uint32_t n_rot;
+  uint32_t mode;
+} b3d_pose_grid;
+
+/* One stage's reduction: argmax (first index of the strict max), max,
+ * logsumexp, sum exp(x-max), and one categorical draw (u < running CDF,
+ * inference.cpp:345-353) with the stream's next uniform(). */
+typedef struct b3d_stage_result {
+  uint64_t argmax;
+  uint64_t sample;
+  double max_score;
+  double logsumexp;
+  double total;
+  double sample_logp;
+  uint32_t all_zero;
+  uint32_t n_nonfinite;
+  uint32_t sample_fallback;
+  uint32_t reserved;
+} b3d_stage_result;
+
+/* Context: device, stream, uploaded meshes, observation, likelihood config. */
+B3D_API b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out);
+B3D_API void b3d_gpu_context_destroy(b3d_gpu_context* ctx);
+/* Use an external cudaStream_t (NULL = the context's own stream). */
+B3D_API b3d_status b3d_gpu_set_stream(b3d_gpu_context* ctx, void* cuda_stream);
+B3D_API b3d_status b3d_gpu_synchronize(b3d_gpu_context* ctx);
+
+/* Intrinsics plus camera-to-world pose (NULL = identity). */
+B3D_API b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics* k,
+                                      const b3d_pose* camera);
+/* TriangleMesh (geometry.hpp:84-89): vertices n_vertices x 3 (fp64, model
+ * frame), triangles n_triangles x 3 (u32).  Triangle order = draw order. */
+B3D_API b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
+                                       uint64_t n_vertices, const uint32_t* triangles,
+                                       uint64_t n_triangles, int32_t* out_mesh_id);
+/* Observed depth image (W x H fp32, sentinel = (float)far). */
+B3D_API b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth);
+/* windowed_log_likelihood_multi settings (likelihood.hpp:65-69). */
+B3D_API b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
+                                          uint32_t n_noise, double sigma_max, int window,
+                                          int prefactor);
+
+/* score-many: scores[i*n_noise + e] = windowed log-likelihood of the
+ * observation given the render of mesh at poses[i] (model-to-world).
+ * status[i] = 1 marks an empty render (score -inf; the reference throws). */
+B3D_API b3d_status b3d_gpu_score_poses(b3d_gpu_context* ctx, int32_t mesh_id,
+                                       const b3d_pose* poses, uint64_t n, double* scores,
+                                       uint8_t* status);
+B3D_API b3d_status b3d_gpu_score_grid(b3d_gpu_context* ctx, int32_t mesh_id,
+                                      const b3d_pose_grid* grid, double* scores,
+                                      uint8_t* status);
+/* render-many: depth n x W x H (fp32, sentinel = far) and optional
+ * draw_index n x W x H (int32, triangle index in mesh order, -1 = none). */
+B3D_API b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id,
+                                        const b3d_pose* poses, uint64_t n, float* depth,
+                                        int32_t* draw_index);
+/* Stage reduction over scores[i*stride + col], i < n.  rng_state (5 x u64:
+ * seed, s0..s3 of the reference Rng) is advanced by one uniform() when not
+ * NULL; NULL skips the draw.  probs (optional, n) receives the normalised
+ * CellScores (inference.cpp:315-330). */
+B3D_API b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scores,
+                                        uint64_t n, uint32_t stride, uint32_t col,
+                                        uint64_t* rng_state, b3d_stage_result* out,
+                                        double* probs);
+
+/* Reference Rng seeding (rng.cpp:20-28), for building rng_state. */
+B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
+B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,
+                           uint64_t out[5]);
+
+/* voxel_to_mesh (geometry.cpp:142-177) on the host: exterior faces of the
+ * occupied voxels in stored order.  Capacities: vertices >= 24*n doubles,
+ * triangles >= 36*n u32. */
+B3D_API b3d_status b3d_voxel_to_mesh(const int32_t* voxels, uint64_t n, double resolution,
+                                     const double origin[3], double* vertices,
+                                     uint32_t* triangles, uint64_t* n_vertices,
+                                     uint64_t* n_triangles);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* B3D_B200_H */

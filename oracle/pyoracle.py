@@ -1,0 +1,323 @@
+"""ctypes binding of the CPU oracle (oracle/_build/libb3d_oracle.so).
+
+TEST INFRASTRUCTURE ONLY: imported by tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / --impl reference leg, as the checker -- never by
+the product package.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB = os.path.join(_HERE, "_build", "libb3d_oracle.so")
+REF_RNG = os.path.join(_HERE, "_ref", "libref_rng.so")
+
+
+class Intr(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_uint32), ("height", C.c_uint32),
+                ("near_m", C.c_double), ("far_m", C.c_double)]
+
+
+class Pose(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("qw", "qx", "qy", "qz", "tx", "ty", "tz")]
+
+
+class Noise(C.Structure):
+    _fields_ = [("p_outlier", C.c_double), ("sigma_noise", C.c_double)]
+
+
+class Instance(C.Structure):
+    _fields_ = [("vertices", C.c_void_p), ("triangles", C.c_void_p),
+                ("n_vertices", C.c_uint64), ("n_triangles", C.c_uint64),
+                ("model_to_world", Pose)]
+
+
+class Counters(C.Structure):
+    _fields_ = [(n, C.c_uint64) for n in ("vertices", "triangles", "bbox_px", "fragments",
+                                          "rend_valid", "obs_valid", "pairs")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+_lib = None
+
+
+def build():
+    subprocess.check_call(["make", "-s", "-C", _HERE])
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB):
+            build()
+        L = C.CDLL(LIB)
+        vp = C.c_void_p
+        d = C.c_double
+        L.orc_rng_uniform.restype = d
+        L.orc_rng_normal.restype = d
+        L.orc_rng_next_u64.restype = C.c_uint64
+        L.orc_rng_uniform_int.restype = C.c_uint64
+        L.orc_rng_uniform_int.argtypes = [vp, C.c_uint64]
+        L.orc_rng_seed.argtypes = [C.c_uint64, vp]
+        L.orc_rng_split.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]
+        L.orc_visible_volume.restype = d
+        L.orc_logsumexp.restype = d
+        L.orc_logsumexp.argtypes = [vp, C.c_size_t]
+        L.orc_sample_categorical.restype = C.c_size_t
+        L.orc_sample_categorical.argtypes = [vp, C.c_size_t, vp]
+        L.orc_argmax.restype = C.c_size_t
+        L.orc_argmax.argtypes = [vp, C.c_size_t]
+        L.orc_normalize.argtypes = [vp, C.c_size_t, vp]
+        L.orc_lattice.restype = d
+        L.orc_lattice.argtypes = [d, d, C.c_int, C.c_int]
+        L.orc_from_axis_angle.argtypes = [vp, d, vp]
+        L.orc_camera_pose_from_spherical.argtypes = [d, d, d, vp]
+        L.orc_contact_to_pose.argtypes = [d, d, vp, vp, C.c_int, d, d, d, vp]
+        L.orc_windowed_loglik_multi.argtypes = [vp, vp, vp, vp, C.c_size_t, d, d, C.c_int,
+                                                C.c_int, vp, vp]
+        L.orc_full_loglik.argtypes = [vp, vp, vp, vp, d, d, C.c_int, vp]
+        L.orc_raster_mesh.argtypes = [vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
+                                      C.c_uint32, vp]
+        L.orc_render_instances.argtypes = [vp, vp, vp, C.c_size_t, vp, vp, vp]
+        L.orc_score_poses.argtypes = [vp, vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
+                                      C.c_size_t, vp, C.c_size_t, d, C.c_int, C.c_int, vp, vp,
+                                      C.c_int, vp]
+        L.orc_voxel_to_mesh.argtypes = [vp, C.c_size_t, d, vp, vp, vp, vp, vp]
+        L.orc_compose.argtypes = [vp, vp, vp]
+        L.orc_inverse.argtypes = [vp, vp]
+        L.orc_rotation_matrix.argtypes = [vp, vp]
+        L.orc_rotated_bounds.argtypes = [vp, vp, C.c_int, vp, vp]
+        L.orc_box_mesh.argtypes = [vp, vp, vp, vp]
+        _lib = L
+    return _lib
+
+
+def intr(k) -> Intr:
+    t = k.as_tuple() if hasattr(k, "as_tuple") else tuple(k)
+    return Intr(*t)
+
+
+def pose(p) -> Pose:
+    return Pose(*np.asarray(p, dtype=np.float64).reshape(7).tolist())
+
+
+def _p(a):
+    return a.ctypes.data if a is not None else None
+
+
+# ---------------------------------------------------------------- wrappers
+def rng_seed(seed):
+    st = np.zeros(5, dtype=np.uint64)
+    lib().orc_rng_seed(seed, _p(st))
+    return st
+
+
+def rng_split(st, k0, k1=0, k2=0):
+    out = np.zeros(5, dtype=np.uint64)
+    lib().orc_rng_split(_p(st), k0, k1, k2, _p(out))
+    return out
+
+
+def rng_u64(st, n):
+    return np.array([lib().orc_rng_next_u64(_p(st)) for _ in range(n)], dtype=np.uint64)
+
+
+def rng_uniform(st):
+    return lib().orc_rng_uniform(_p(st))
+
+
+def voxel_to_mesh(voxels, resolution, origin):
+    v = np.ascontiguousarray(voxels, dtype=np.int32)
+    n = v.shape[0]
+    verts = np.zeros((8 * n, 3), dtype=np.float64)
+    tris = np.zeros((12 * n, 3), dtype=np.uint32)
+    nv, nt = C.c_size_t(), C.c_size_t()
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    rc = lib().orc_voxel_to_mesh(_p(v), n, resolution, _p(o), _p(verts), _p(tris), C.byref(nv),
+                                 C.byref(nt))
+    assert rc == 0
+    return verts[: nv.value].copy(), tris[: nt.value].copy()
+
+
+def box_mesh(lo, hi):
+    v = np.zeros((8, 3), dtype=np.float64)
+    t = np.zeros((12, 3), dtype=np.uint32)
+    lib().orc_box_mesh(_p(np.asarray(lo, dtype=np.float64)), _p(np.asarray(hi, dtype=np.float64)),
+                       _p(v), _p(t))
+    return v, t
+
+
+def compose(a, b):
+    out = Pose()
+    pa, pb = pose(a), pose(b)
+    lib().orc_compose(C.byref(pa), C.byref(pb), C.byref(out))
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def inverse(a):
+    out = Pose()
+    pa = pose(a)
+    lib().orc_inverse(C.byref(pa), C.byref(out))
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def rotation_matrix(a):
+    m = np.zeros(9, dtype=np.float64)
+    pa = pose(a)
+    lib().orc_rotation_matrix(C.byref(pa), _p(m))
+    return m.reshape(3, 3)
+
+
+def from_axis_angle(axis, angle, t=(0, 0, 0)):
+    out = Pose()
+    lib().orc_from_axis_angle(_p(np.asarray(axis, dtype=np.float64)), angle, C.byref(out))
+    p = np.array([getattr(out, n) for n, _ in Pose._fields_])
+    p[4:] = t
+    return p
+
+
+def camera_pose_from_spherical(d, az, alt):
+    out = Pose()
+    lib().orc_camera_pose_from_spherical(d, az, alt, C.byref(out))
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def contact_to_pose(table_w, table_h, aabb_min, aabb_max, face, dx, dy, dtheta):
+    out = Pose()
+    rc = lib().orc_contact_to_pose(table_w, table_h,
+                                   _p(np.asarray(aabb_min, dtype=np.float64)),
+                                   _p(np.asarray(aabb_max, dtype=np.float64)), face, dx, dy,
+                                   dtheta, C.byref(out))
+    if rc:
+        raise ValueError("contact params out of valid range")
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def rotated_bounds(aabb_min, aabb_max, face):
+    lo = np.zeros(3)
+    hi = np.zeros(3)
+    lib().orc_rotated_bounds(_p(np.asarray(aabb_min, dtype=np.float64)),
+                             _p(np.asarray(aabb_max, dtype=np.float64)), face, _p(lo), _p(hi))
+    return lo, hi
+
+
+def render(k, instances, camera=None, with_ids=False, counters=False):
+    """render_instances: instances = [(vertices, triangles, model_to_world)]."""
+    ki = intr(k)
+    W, H = ki.width, ki.height
+    keep = []
+    arr = (Instance * max(1, len(instances)))()
+    for i, (v, t, p) in enumerate(instances):
+        v = np.ascontiguousarray(v, dtype=np.float64)
+        t = np.ascontiguousarray(t, dtype=np.uint32)
+        keep += [v, t]
+        arr[i] = Instance(v.ctypes.data, t.ctypes.data, v.shape[0], t.shape[0], pose(p))
+    depth = np.zeros((H, W), dtype=np.float32)
+    ids = np.zeros((H, W), dtype=np.int32) if with_ids else None
+    cam = pose(camera if camera is not None else [1, 0, 0, 0, 0, 0, 0])
+    cnt = Counters()
+    lib().orc_render_instances(C.byref(ki), C.byref(cam), arr, len(instances), _p(depth),
+                               _p(ids), C.byref(cnt))
+    out = (depth, ids) if with_ids else depth
+    if counters:
+        return out, cnt.as_dict()
+    return out
+
+
+def windowed_loglik_multi(obs, rend, k, noise, sigma_max, window, prefactor=0, volume=None,
+                          counters=False):
+    ki = intr(k)
+    arr = (Noise * len(noise))(*[Noise(p, s) for p, s in noise])
+    out = np.zeros(len(noise), dtype=np.float64)
+    vol = lib().orc_visible_volume(C.byref(ki)) if volume is None else volume
+    cnt = Counters()
+    o = np.ascontiguousarray(obs, dtype=np.float32)
+    r = np.ascontiguousarray(rend, dtype=np.float32)
+    rc = lib().orc_windowed_loglik_multi(_p(o), _p(r), C.byref(ki), arr, len(noise), vol,
+                                         sigma_max, window, prefactor, _p(out), C.byref(cnt))
+    if rc:
+        raise ValueError("windowed likelihood: invalid argument or empty rendered cloud")
+    return (out, cnt.as_dict()) if counters else out
+
+
+def full_loglik(obs, rend, k, noise, sigma_max, prefactor=0, volume=None):
+    ki = intr(k)
+    np_ = Noise(*noise)
+    vol = lib().orc_visible_volume(C.byref(ki)) if volume is None else volume
+    out = C.c_double()
+    o = np.ascontiguousarray(obs, dtype=np.float32)
+    r = np.ascontiguousarray(rend, dtype=np.float32)
+    rc = lib().orc_full_loglik(_p(o), _p(r), C.byref(ki), C.byref(np_), vol, sigma_max,
+                               prefactor, C.byref(out))
+    if rc:
+        raise ValueError("full likelihood: invalid argument or empty rendered cloud")
+    return out.value
+
+
+def visible_volume(k):
+    ki = intr(k)
+    return lib().orc_visible_volume(C.byref(ki))
+
+
+def score_poses(k, observed, verts, tris, poses, noise, sigma_max, window, prefactor=0,
+                base_depth=None, camera=None, threads=0, counters=False):
+    ki = intr(k)
+    poses = np.ascontiguousarray(poses, dtype=np.float64)
+    n = poses.shape[0]
+    arr = (Noise * len(noise))(*[Noise(p, s) for p, s in noise])
+    scores = np.zeros((n, len(noise)), dtype=np.float64)
+    status = np.zeros(n, dtype=np.uint8)
+    v = np.ascontiguousarray(verts, dtype=np.float64)
+    t = np.ascontiguousarray(tris, dtype=np.uint32)
+    o = np.ascontiguousarray(observed, dtype=np.float32)
+    cam = pose(camera if camera is not None else [1, 0, 0, 0, 0, 0, 0])
+    cnt = Counters()
+    lib().orc_score_poses(C.byref(ki), C.byref(cam), _p(o), _p(base_depth), _p(v), v.shape[0],
+                          _p(t), t.shape[0], _p(poses), n, arr, len(noise), sigma_max, window,
+                          prefactor, _p(scores), _p(status), threads, C.byref(cnt))
+    if counters:
+        return scores, status, cnt.as_dict()
+    return scores, status
+
+
+def normalize(lt):
+    lt = np.ascontiguousarray(lt, dtype=np.float64)
+    p = np.zeros_like(lt)
+    az = lib().orc_normalize(_p(lt), lt.shape[0], _p(p))
+    return p, bool(az)
+
+
+def sample_categorical(probs, st):
+    probs = np.ascontiguousarray(probs, dtype=np.float64)
+    return int(lib().orc_sample_categorical(_p(probs), probs.shape[0], _p(st)))
+
+
+def argmax(xs):
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    return int(lib().orc_argmax(_p(xs), xs.shape[0]))
+
+
+def logsumexp(xs):
+    xs = np.ascontiguousarray(xs, dtype=np.float64)
+    return float(lib().orc_logsumexp(_p(xs), xs.shape[0]))
+
+
+# ------------------------------------------------ the reference's own RNG
+def ref_rng_available() -> bool:
+    return os.path.exists(REF_RNG)
+
+
+def ref_rng_draw(seed, split, k0, k1, k2, kind, m, n):
+    L = C.CDLL(REF_RNG)
+    out = np.zeros(n, dtype=np.uint64)
+    L.ref_rng_draw.argtypes = [C.c_uint64, C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int,
+                               C.c_uint64, C.c_void_p, C.c_size_t]
+    L.ref_rng_draw(seed, split, k0, k1, k2, kind, m, out.ctypes.data, n)
+    return out

@@ -1,0 +1,317 @@
+"""ctypes client of libb3d_b200.so (include/b3d_b200.h).
+
+The product is the C ABI + C++ host layer + sm_100a kernels in csrc/; this
+module only marshals arguments so tests and bench.py can drive the same
+entry points a foreign caller would bind.  There is no CPU
+fallback: if the shared library or a GPU is missing, calls fail loudly.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+from typing import Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_lib", "libb3d_b200.so")
+
+B3D_OK = 0
+PREFACTOR_PRINTED = 0
+PREFACTOR_UNIFORM = 1
+GRID_PRODUCT = 0
+GRID_ZIP = 1
+
+# b3d_pose as a numpy row: (qw, qx, qy, qz, tx, ty, tz)
+POSE_DTYPE = np.float64
+
+
+class B3DError(RuntimeError):
+    def __init__(self, status: int, message: str):
+        super().__init__(f"b3d status {status}: {message}")
+        self.status = status
+
+
+class Intrinsics(C.Structure):
+    _fields_ = [("fx", C.c_double), ("fy", C.c_double), ("cx", C.c_double), ("cy", C.c_double),
+                ("width", C.c_uint32), ("height", C.c_uint32),
+                ("near_m", C.c_double), ("far_m", C.c_double)]
+
+    @classmethod
+    def make(cls, fx, fy, cx, cy, width, height, near, far):
+        return cls(fx, fy, cx, cy, width, height, near, far)
+
+
+class Pose(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("qw", "qx", "qy", "qz", "tx", "ty", "tz")]
+
+
+class Noise(C.Structure):
+    _fields_ = [("p_outlier", C.c_double), ("sigma_noise", C.c_double)]
+
+
+class PoseGrid(C.Structure):
+    _fields_ = [("center", Pose), ("extent", C.c_double * 3), ("count", C.c_uint32 * 3),
+                ("rotations", C.c_void_p), ("n_rot", C.c_uint32), ("mode", C.c_uint32)]
+
+
+class StageResult(C.Structure):
+    _fields_ = [("argmax", C.c_uint64), ("sample", C.c_uint64), ("max_score", C.c_double),
+                ("logsumexp", C.c_double), ("total", C.c_double), ("sample_logp", C.c_double),
+                ("all_zero", C.c_uint32), ("n_nonfinite", C.c_uint32),
+                ("sample_fallback", C.c_uint32), ("reserved", C.c_uint32)]
+
+
+_lib = None
+
+
+def lib() -> C.CDLL:
+    """Loads libb3d_b200.so; raises if it has not been built."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} missing: run __graft_entry__.build() (no CPU fallback)")
+    L = C.CDLL(LIB_PATH)
+    vp, st, u64, i32, u32, dbl = C.c_void_p, C.c_int, C.c_uint64, C.c_int32, C.c_uint32, C.c_double
+    sig = {
+        "b3d_version": ([], C.c_char_p),
+        "b3d_last_error": ([], C.c_char_p),
+        "b3d_depth_image_create": ([u32, u32, vp, C.POINTER(vp)], st),
+        "b3d_depth_image_width": ([vp], u32),
+        "b3d_depth_image_height": ([vp], u32),
+        "b3d_depth_image_data": ([vp], vp),
+        "b3d_depth_image_destroy": ([vp], None),
+        "b3d_log_likelihood": ([vp, vp, C.POINTER(Intrinsics), dbl, dbl, dbl, st,
+                                C.POINTER(dbl)], st),
+        "b3d_gpu_context_create": ([st, C.POINTER(vp)], st),
+        "b3d_gpu_context_destroy": ([vp], None),
+        "b3d_gpu_set_stream": ([vp, vp], st),
+        "b3d_gpu_synchronize": ([vp], st),
+        "b3d_gpu_set_camera": ([vp, C.POINTER(Intrinsics), C.POINTER(Pose)], st),
+        "b3d_gpu_upload_mesh": ([vp, vp, u64, vp, u64, C.POINTER(i32)], st),
+        "b3d_gpu_set_observation": ([vp, vp], st),
+        "b3d_gpu_set_likelihood": ([vp, C.POINTER(Noise), u32, dbl, st, st], st),
+        "b3d_gpu_score_poses": ([vp, i32, vp, u64, vp, vp], st),
+        "b3d_gpu_score_grid": ([vp, i32, C.POINTER(PoseGrid), vp, vp], st),
+        "b3d_gpu_render_poses": ([vp, i32, vp, u64, vp, vp], st),
+        "b3d_gpu_stage_reduce": ([vp, vp, u64, u32, u32, vp, vp, vp], st),
+        "b3d_rng_seed": ([u64, vp], None),
+        "b3d_rng_split": ([vp, u64, u64, u64, vp], None),
+        "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
+    }
+    for name, (args, res) in sig.items():
+        f = getattr(L, name)
+        f.argtypes = args
+        f.restype = res
+    _lib = L
+    return L
+
+
+def exported_symbols() -> Sequence[str]:
+    """Every function include/b3d_b200.h declares (B3D_API)."""
+    import re
+    hdr = open(os.path.join(_HERE, os.pardir, "include", "b3d_b200.h")).read()
+    return re.findall(r"B3D_API[^;]*?\b(b3d_\w+)\s*\(", hdr, flags=re.S)
+
+
+def _check(status: int) -> None:
+    if status != B3D_OK:
+        raise B3DError(status, lib().b3d_last_error().decode())
+
+
+def _ptr(a) -> int:
+    """Raw address of a numpy array (host) or a torch tensor (host/device)."""
+    if a is None:
+        return None
+    if hasattr(a, "data_ptr"):
+        return a.data_ptr()
+    if isinstance(a, np.ndarray):
+        if not a.flags["C_CONTIGUOUS"]:
+            raise ValueError("arrays must be C-contiguous")
+        return a.ctypes.data
+    raise TypeError(f"unsupported buffer type {type(a)}")
+
+
+def _pose(p) -> Pose:
+    p = np.asarray(p, dtype=np.float64).reshape(7)
+    return Pose(*p.tolist())
+
+
+def rng_seed(seed: int) -> np.ndarray:
+    st = np.zeros(5, dtype=np.uint64)
+    lib().b3d_rng_seed(C.c_uint64(seed), st.ctypes.data)
+    return st
+
+
+def rng_split(state: np.ndarray, k0: int, k1: int = 0, k2: int = 0) -> np.ndarray:
+    out = np.zeros(5, dtype=np.uint64)
+    lib().b3d_rng_split(state.ctypes.data, k0, k1, k2, out.ctypes.data)
+    return out
+
+
+def voxel_to_mesh(voxels: np.ndarray, resolution: float, origin) -> tuple:
+    v = np.ascontiguousarray(voxels, dtype=np.int32)
+    n = v.shape[0]
+    verts = np.zeros((8 * n, 3), dtype=np.float64)
+    tris = np.zeros((12 * n, 3), dtype=np.uint32)
+    o = np.ascontiguousarray(origin, dtype=np.float64)
+    nv, nt = C.c_uint64(), C.c_uint64()
+    _check(lib().b3d_voxel_to_mesh(v.ctypes.data, n, resolution, o.ctypes.data,
+                                   verts.ctypes.data, tris.ctypes.data, C.byref(nv), C.byref(nt)))
+    return verts[: nv.value].copy(), tris[: nt.value].copy()
+
+
+def log_likelihood(observed: np.ndarray, rendered: np.ndarray, k: Intrinsics, p_outlier: float,
+                   sigma_noise: float, sigma_max: float, window: int) -> float:
+    """b3d_log_likelihood (reference b3d.h:110-115), GPU-backed."""
+    L = lib()
+    o, r = C.c_void_p(), C.c_void_p()
+    obs = np.ascontiguousarray(observed, dtype=np.float32)
+    ren = np.ascontiguousarray(rendered, dtype=np.float32)
+    _check(L.b3d_depth_image_create(obs.shape[1], obs.shape[0], obs.ctypes.data, C.byref(o)))
+    try:
+        _check(L.b3d_depth_image_create(ren.shape[1], ren.shape[0], ren.ctypes.data, C.byref(r)))
+        try:
+            out = C.c_double()
+            _check(L.b3d_log_likelihood(o, r, C.byref(k), p_outlier, sigma_noise, sigma_max,
+                                        window, C.byref(out)))
+            return out.value
+        finally:
+            L.b3d_depth_image_destroy(r)
+    finally:
+        L.b3d_depth_image_destroy(o)
+
+
+@dataclass
+class StageOut:
+    argmax: int
+    sample: int
+    max_score: float
+    logsumexp: float
+    total: float
+    sample_logp: float
+    all_zero: bool
+    n_nonfinite: int
+    sample_fallback: bool
+
+
+class GpuContext:
+    """Owns a b3d_gpu_context (device, stream, meshes, observation)."""
+
+    def __init__(self, device: int = 0):
+        self._L = lib()
+        h = C.c_void_p()
+        _check(self._L.b3d_gpu_context_create(device, C.byref(h)))
+        self.h = h
+        self.device = device
+        self.k: Optional[Intrinsics] = None
+        self.n_noise = 0
+
+    def close(self):
+        if self.h:
+            self._L.b3d_gpu_context_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_stream(self, stream_handle: int | None):
+        _check(self._L.b3d_gpu_set_stream(self.h, stream_handle))
+
+    def synchronize(self):
+        _check(self._L.b3d_gpu_synchronize(self.h))
+
+    def set_camera(self, k: Intrinsics, camera=None):
+        self.k = k
+        _check(self._L.b3d_gpu_set_camera(self.h, C.byref(k),
+                                          C.byref(_pose(camera)) if camera is not None else None))
+
+    def upload_mesh(self, vertices: np.ndarray, triangles: np.ndarray) -> int:
+        v = np.ascontiguousarray(vertices, dtype=np.float64)
+        t = np.ascontiguousarray(triangles, dtype=np.uint32)
+        mid = C.c_int32()
+        _check(self._L.b3d_gpu_upload_mesh(self.h, v.ctypes.data, v.shape[0], t.ctypes.data,
+                                           t.shape[0], C.byref(mid)))
+        return mid.value
+
+    def set_observation(self, depth):
+        if isinstance(depth, np.ndarray):
+            depth = np.ascontiguousarray(depth, dtype=np.float32)
+        _check(self._L.b3d_gpu_set_observation(self.h, _ptr(depth)))
+
+    def set_likelihood(self, noise: Sequence[tuple], sigma_max: float, window: int,
+                       prefactor: int = PREFACTOR_PRINTED):
+        arr = (Noise * len(noise))(*[Noise(p, s) for p, s in noise])
+        _check(self._L.b3d_gpu_set_likelihood(self.h, arr, len(noise), sigma_max, window,
+                                              prefactor))
+        self.n_noise = len(noise)
+
+    def score_poses(self, mesh: int, poses, scores=None, status=None):
+        """poses: (n,7) float64 numpy (host) or torch tensor (host/device)."""
+        n = poses.shape[0]
+        host = isinstance(poses, np.ndarray)
+        if host:
+            poses = np.ascontiguousarray(poses, dtype=np.float64)
+        if scores is None:
+            scores = np.zeros((n, self.n_noise), dtype=np.float64)
+            status = np.zeros(n, dtype=np.uint8) if status is None else status
+        _check(self._L.b3d_gpu_score_poses(self.h, mesh, _ptr(poses), n, _ptr(scores),
+                                           _ptr(status)))
+        return scores, status
+
+    def make_grid(self, center, extent, count, rotations, mode=GRID_ZIP) -> PoseGrid:
+        g = PoseGrid()
+        g.center = _pose(center)
+        for a in range(3):
+            g.extent[a] = float(extent[a])
+            g.count[a] = int(count[a])
+        g.rotations = _ptr(rotations)
+        g.n_rot = rotations.shape[0]
+        g.mode = mode
+        g._keep = rotations  # keep the buffer alive
+        return g
+
+    @staticmethod
+    def grid_size(g: PoseGrid) -> int:
+        nt = g.count[0] * g.count[1] * g.count[2]
+        return nt * g.n_rot if g.mode == GRID_PRODUCT else nt
+
+    def score_grid(self, mesh: int, grid: PoseGrid, scores=None, status=None):
+        n = self.grid_size(grid)
+        if scores is None:
+            scores = np.zeros((n, self.n_noise), dtype=np.float64)
+            status = np.zeros(n, dtype=np.uint8) if status is None else status
+        _check(self._L.b3d_gpu_score_grid(self.h, mesh, C.byref(grid), _ptr(scores),
+                                          _ptr(status)))
+        return scores, status
+
+    def render_poses(self, mesh: int, poses, with_ids: bool = True):
+        n = poses.shape[0]
+        poses = np.ascontiguousarray(poses, dtype=np.float64)
+        H, W = self.k.height, self.k.width
+        depth = np.zeros((n, H, W), dtype=np.float32)
+        ids = np.zeros((n, H, W), dtype=np.int32) if with_ids else None
+        _check(self._L.b3d_gpu_render_poses(self.h, mesh, poses.ctypes.data, n,
+                                            depth.ctypes.data, _ptr(ids)))
+        return depth, ids
+
+    def stage_reduce(self, scores, n=None, stride=1, col=0, rng_state=None, probs=None,
+                     out=None):
+        if n is None:
+            n = scores.shape[0]
+        if isinstance(scores, np.ndarray):
+            scores = np.ascontiguousarray(scores, dtype=np.float64)
+        res = StageResult() if out is None else None
+        _check(self._L.b3d_gpu_stage_reduce(self.h, _ptr(scores), n, stride, col,
+                                            _ptr(rng_state), _ptr(out) if out is not None
+                                            else C.addressof(res), _ptr(probs)))
+        if res is None:
+            return None
+        return StageOut(res.argmax, res.sample, res.max_score, res.logsumexp, res.total,
+                        res.sample_logp, bool(res.all_zero), res.n_nonfinite,
+                        bool(res.sample_fallback))

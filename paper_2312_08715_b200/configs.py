@@ -1,0 +1,144 @@
+"""BASELINE.json configs restated as concrete seeded workloads.
+
+Each builder returns a Workload holding the mesh, intrinsics, observation,
+hypothesis grid and likelihood settings.  The observation is rendered at the
+ground-truth pose by `render_fn(k, vertices, triangles, pose) -> depth`
+(the product renderer on a GPU box, or the CPU oracle in CPU-only tests; the
+two are bit-identical, which the parity suite checks) and then corrupted.
+Mapping of BASELINE terms onto the reference:
+r -> sigma_noise, f x f window -> window = (f-1)/2, sigma_max = 0.1,
+prefactor "printed".
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import synth
+
+RESOLUTION = 0.005  # 5 mm voxels
+
+
+@dataclass
+class Intr:
+    fx: float
+    fy: float
+    cx: float
+    cy: float
+    width: int
+    height: int
+    near: float
+    far: float
+
+    def as_tuple(self):
+        return (self.fx, self.fy, self.cx, self.cy, self.width, self.height, self.near, self.far)
+
+
+@dataclass
+class Workload:
+    name: str
+    k: Intr
+    voxels: np.ndarray
+    vertices: np.ndarray
+    triangles: np.ndarray
+    gt_pose: np.ndarray            # (7,) model-to-camera ground truth
+    observed: np.ndarray           # (H, W) float32
+    center: np.ndarray             # (7,) grid centre
+    extent: tuple
+    count: tuple
+    rotations: np.ndarray          # (n_rot, 4) perturbations dq
+    grid_mode: int
+    noise: List[tuple]             # [(p_outlier, sigma)]
+    window: int
+    sigma_max: float = 0.1
+    stages: Optional[list] = None  # coarse-to-fine schedule (cfg2/cfg4)
+    extra: dict = field(default_factory=dict)
+
+    @property
+    def n_hyp(self) -> int:
+        nt = self.count[0] * self.count[1] * self.count[2]
+        return nt * self.rotations.shape[0] if self.grid_mode == 0 else nt
+
+    def grid_poses(self) -> np.ndarray:
+        """All hypothesis poses on the host (same formulas as the device grid;
+        used for the explicit-pose API and the CPU oracle)."""
+        return _grid_poses_host(self.center, self.extent, self.count, self.rotations,
+                                self.grid_mode)
+
+
+def _grid_poses_host(center, extent, count, rotations, mode) -> np.ndarray:
+    """Host restatement of the device pose grid (posemath.cuh grid_pose):
+    tracking.cpp:34-35 lattice and q = normalized(center.q * dq), scalar
+    Eigen evaluation order, no FMA (numpy float64 ops are single-rounded)."""
+    nx, ny, nz = count
+    nt = nx * ny * nz
+    n_rot = rotations.shape[0]
+    n = nt * n_rot if mode == 0 else nt
+    idx = np.arange(n, dtype=np.int64)
+    ti = idx // n_rot if mode == 0 else idx
+    ri = idx % n_rot if mode == 0 else idx
+    iz = ti % nz
+    iy = (ti // nz) % ny
+    ix = ti // (nz * ny)
+
+    def lat(c, e, cnt, i):
+        if cnt == 1:
+            return np.full(i.shape, c, dtype=np.float64)
+        return (c - e) + ((2.0 * e) * i.astype(np.float64)) / float(cnt - 1)
+
+    aw, ax, ay, az = center[0], center[1], center[2], center[3]
+    d = rotations[ri]
+    bw, bx, by, bz = d[:, 0], d[:, 1], d[:, 2], d[:, 3]
+    w = ((aw * bw - ax * bx) - ay * by) - az * bz
+    x = ((aw * bx + ax * bw) + ay * bz) - az * by
+    y = ((aw * by + ay * bw) + az * bx) - ax * bz
+    z = ((aw * bz + az * bw) + ax * by) - ay * bx
+    n2 = (x * x + y * y) + (z * z + w * w)
+    nrm = np.sqrt(n2)
+    out = np.zeros((n, 7), dtype=np.float64)
+    out[:, 0] = w / nrm
+    out[:, 1] = x / nrm
+    out[:, 2] = y / nrm
+    out[:, 3] = z / nrm
+    out[:, 4] = lat(center[4], extent[0], nx, ix)
+    out[:, 5] = lat(center[5], extent[1], ny, iy)
+    out[:, 6] = lat(center[6], extent[2], nz, iz)
+    return out
+
+
+RenderFn = Callable[[Intr, np.ndarray, np.ndarray, np.ndarray], np.ndarray]
+
+
+def make_mesh(voxels: np.ndarray, mesh_fn) -> tuple:
+    origin = synth.centered_origin(voxels, RESOLUTION)
+    return mesh_fn(voxels, RESOLUTION, origin)
+
+
+def cfg1(render_fn: RenderFn, mesh_fn, seed: int = 0, blob: str = "eden",
+         shard: int = 0) -> Workload:
+    """configs[0]: single-object scoring at 160x120 (W x H).
+
+    1,000-voxel blob (5 mm), pinhole fx=fy=200, cx=80, cy=60, near 0.01,
+    far 10.  Observation: render at t=(0,0,0.6) with a uniform random
+    rotation, N(0, 2 mm) depth noise, 10% of pixels -> U[0.2, 1.5] m.
+    Hypotheses: 8x8x16 translation lattice over +-2 cm (16 along z) zipped
+    with 1,024 independent vMF(kappa=1000) rotation perturbations.
+    Likelihood r=5 mm, 3x3 window (w=1), outlier_prob 0.01.
+    `shard` selects an independent batch of rotation perturbations (weak
+    scaling: rank r scores batch r against the same observation).
+    """
+    rng = np.random.Generator(np.random.PCG64(1000 + seed))
+    rng_rot = np.random.Generator(np.random.PCG64([2000 + seed, shard]))
+    vox = synth.eden_blob(1000, seed) if blob == "eden" else synth.random_walk_blob(1000, seed)
+    verts, tris = make_mesh(vox, mesh_fn)
+    k = Intr(200.0, 200.0, 80.0, 60.0, 160, 120, 0.01, 10.0)
+    q = synth.uniform_quaternion(rng)
+    gt = np.array([q[0], q[1], q[2], q[3], 0.0, 0.0, 0.6])
+    depth = render_fn(k, verts, tris, gt)
+    obs = synth.noisy_observation(depth, k.far, 0.002, 0.10, 0.2, 1.5, rng, k.near)
+    count = (8, 8, 16)
+    rots = synth.vmf_quaternions(8 * 8 * 16, 1000.0, rng_rot)
+    return Workload("cfg1_single_object_160x120", k, vox, verts, tris, gt, obs, gt.copy(),
+                    (0.02, 0.02, 0.02), count, rots, 1, [(0.01, 0.005)], 1)

@@ -1,0 +1,853 @@
+// b3d_capi.cpp -- C++ host layer and C ABI (include/b3d_b200.h) of the
+// B200-native pose-enumeration hot path.
+//
+// Mirrors the reference's C API conventions (proj/src/capi/b3d_capi.cpp):
+// exceptions are converted to b3d_status by guarded() (b3d_capi.cpp:33-48),
+// the message goes to a thread-local string (b3d_capi.cpp:22,118), and the
+// argument checks reuse the reference's messages where one exists.
+#include "b3d_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "b3d_kernels.cuh"
+
+namespace b3d200 {
+
+// kernels (render_score.cu, stage.cu, image_score.cu)
+template <bool kIds, bool kScore, bool kOut>
+cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st);
+template <bool kIds, bool kScore, bool kOut>
+cudaError_t occupancy_render_score(int* blocks, size_t smem);
+cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
+                               float fcy, float inv_fx, float inv_fy, float4* out,
+                               int* count, cudaStream_t st);
+cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
+                                unsigned long long* rng_state, KStageResult* out,
+                                double* probs, cudaStream_t st);
+cudaError_t launch_select_center(const KGrid& g, const KStageResult* r, int use_sample,
+                                 KPose* center_out, cudaStream_t st);
+cudaError_t launch_image_loglik(const float* obs, const float* rend, int W, int H,
+                                double fx, double fy, double cx, double cy, float far_f,
+                                double p_outlier, double sigma, double sigma_max,
+                                double volume, int window, int prefactor,
+                                unsigned long long* d_acc, double* d_out, int* d_count,
+                                cudaStream_t st);
+
+// ------------------------------------------------------------------ errors
+enum class ErrorCode { invalid = 1, config = 2, io = 3, numeric = 4 };
+
+struct Error : std::runtime_error {
+  Error(ErrorCode c, const std::string& w) : std::runtime_error(w), code(c) {}
+  ErrorCode code;
+};
+
+[[noreturn]] inline void fail(ErrorCode c, const std::string& m) { throw Error(c, m); }
+inline void require(bool cond, ErrorCode c, const std::string& m) {
+  if (!cond) fail(c, m);
+}
+inline void check(bool cond, const char* msg) { require(cond, ErrorCode::invalid, msg); }
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    fail(ErrorCode::numeric, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// ------------------------------------------------------------- pose math
+// geometry.cpp:26-31 inverse (host side, once per call); the per-hypothesis
+// compose runs on the device (posemath.cuh).  Same scalar Eigen order.
+KPose pose_inverse(const KPose& p) {
+  double w = p.qw, x = -p.qx, y = -p.qy, z = -p.qz;
+  const double n2 = (x * x + y * y) + (z * z + w * w);
+  if (n2 > 0) {
+    const double n = std::sqrt(n2);
+    w /= n;
+    x /= n;
+    y /= n;
+    z /= n;
+  }
+  const double v[3] = {p.tx, p.ty, p.tz};
+  double uv0 = y * v[2] - z * v[1];
+  double uv1 = z * v[0] - x * v[2];
+  double uv2 = x * v[1] - y * v[0];
+  uv0 += uv0;
+  uv1 += uv1;
+  uv2 += uv2;
+  const double c0 = y * uv2 - z * uv1;
+  const double c1 = z * uv0 - x * uv2;
+  const double c2 = x * uv1 - y * uv0;
+  KPose o;
+  o.qw = w;
+  o.qx = x;
+  o.qy = y;
+  o.qz = z;
+  o.tx = -(v[0] + w * uv0 + c0);
+  o.ty = -(v[1] + w * uv1 + c1);
+  o.tz = -(v[2] + w * uv2 + c2);
+  return o;
+}
+
+// b3d_capi.cpp:66-74 (from_c(b3d_pose)): unit-norm check, then normalize
+KPose pose_from_c(const b3d_pose& p) {
+  const double n2 = (p.qx * p.qx + p.qy * p.qy) + (p.qz * p.qz + p.qw * p.qw);
+  check(std::abs(std::sqrt(n2) - 1.0) < 1e-6, "pose rotation must be a unit quaternion");
+  KPose o{p.qw, p.qx, p.qy, p.qz, p.tx, p.ty, p.tz};
+  const double n = std::sqrt(n2);
+  if (n2 > 0) {
+    o.qw /= n;
+    o.qx /= n;
+    o.qy /= n;
+    o.qz /= n;
+  }
+  return o;
+}
+
+// geometry.cpp:38-44
+void validate_intrinsics(const b3d_intrinsics& k) {
+  check(k.fx > 0 && k.fy > 0, "intrinsics: focal lengths must be positive");
+  check(k.width > 0 && k.height > 0, "intrinsics: image dimensions must be positive");
+  check(k.cx >= 0 && k.cx < k.width && k.cy >= 0 && k.cy < k.height,
+        "intrinsics: principal point outside image bounds");
+  check(k.near_m > 0 && k.near_m < k.far_m, "intrinsics: require 0 < near < far");
+}
+
+// likelihood.cpp:30-35
+double visible_volume(const b3d_intrinsics& k) {
+  const double di = (k.far_m * k.far_m * k.far_m - k.near_m * k.near_m * k.near_m) / 3.0;
+  return di * (k.width / k.fx) * (k.height / k.fy);
+}
+
+// ---------------------------------------------------------- device buffers
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cuda_check(cudaMalloc(&p, n), "cudaMalloc");
+    bytes = n;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
+bool is_device_ptr(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+struct Mesh {
+  DevBuf verts, tris;
+  int nv = 0, nt = 0;
+};
+
+}  // namespace b3d200
+
+using namespace b3d200;
+
+struct b3d_gpu_context {
+  int device = 0;
+  int sm_count = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  bool has_camera = false;
+  b3d_intrinsics k{};
+  KPose w2c{1, 0, 0, 0, 0, 0, 0};
+  std::vector<std::unique_ptr<Mesh>> meshes;
+  bool has_obs = false;
+  DevBuf obs_depth, obs_pts, obs_count;
+  bool has_lik = false;
+  KLik lik{};
+  DevBuf zscratch, vscratch;
+  DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
+};
+
+namespace {
+
+thread_local std::string g_last_error;
+
+b3d_status to_status(const Error& e) {
+  switch (e.code) {
+    case ErrorCode::config: return B3D_ERROR_CONFIG;
+    case ErrorCode::io: return B3D_ERROR_IO;
+    case ErrorCode::numeric: return B3D_ERROR_NUMERIC;
+    default: return B3D_ERROR;
+  }
+}
+
+template <typename F>
+b3d_status guarded(F&& fn) {
+  try {
+    fn();
+    return B3D_OK;
+  } catch (const Error& e) {
+    g_last_error = e.what();
+    return to_status(e);
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return B3D_ERROR;
+  } catch (...) {
+    g_last_error = "unknown error";
+    return B3D_ERROR;
+  }
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cuda_check(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void require_ready(const b3d_gpu_context* ctx, bool need_obs, bool need_lik) {
+  check(ctx != nullptr, "bad arguments");
+  require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
+  if (need_obs) require(ctx->has_obs, ErrorCode::invalid, "gpu context: observation not set");
+  if (need_lik)
+    require(ctx->has_lik, ErrorCode::invalid, "gpu context: likelihood settings not set");
+}
+
+const Mesh& get_mesh(const b3d_gpu_context* ctx, int32_t id) {
+  require(id >= 0 && static_cast<size_t>(id) < ctx->meshes.size(), ErrorCode::invalid,
+          "gpu context: unknown mesh id");
+  return *ctx->meshes[id];
+}
+
+// Copies `bytes` from a host pointer into the staging buffer (or passes a
+// device pointer through).
+const void* stage_in(b3d_gpu_context* ctx, DevBuf& buf, const void* src, size_t bytes,
+                     bool* was_host) {
+  if (is_device_ptr(src)) {
+    *was_host = false;
+    return src;
+  }
+  *was_host = true;
+  buf.ensure(bytes);
+  cuda_check(cudaMemcpyAsync(buf.p, src, bytes, cudaMemcpyHostToDevice, ctx->stream),
+             "cudaMemcpyAsync H2D");
+  return buf.p;
+}
+
+struct LaunchPlan {
+  int grid = 0;
+  size_t smem = 0;
+  int vcap = 0;
+  int zcap = 0;
+};
+
+template <bool kIds, bool kScore, bool kOut>
+LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n) {
+  LaunchPlan lp;
+  const size_t key = kIds ? 8 : 4;
+  const size_t budget = 110 * 1024;  // two resident CTAs per SM
+  const size_t vbytes = 24ull * m.nv;
+  lp.vcap = vbytes <= 64 * 1024 ? m.nv : 0;
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  size_t zcap = (budget - 24ull * lp.vcap) / key;
+  if (zcap > npx) zcap = npx;
+  lp.zcap = (int)zcap;
+  lp.smem = 24ull * lp.vcap + key * zcap;
+  int per_sm = 0;
+  cuda_check(occupancy_render_score<kIds, kScore, kOut>(&per_sm, lp.smem), "occupancy");
+  if (per_sm < 1) per_sm = 1;
+  long long grid = (long long)per_sm * ctx->sm_count;
+  if (grid > n) grid = n;
+  if (grid < 1) grid = 1;
+  lp.grid = (int)grid;
+  // overflow scratch for hypotheses whose region / mesh exceeds shared memory
+  ctx->zscratch.ensure((size_t)lp.grid * npx * 8);
+  if (lp.vcap < m.nv) ctx->vscratch.ensure((size_t)lp.grid * 24 * m.nv);
+  return lp;
+}
+
+KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
+  KParams p{};
+  const b3d_intrinsics& k = ctx->k;
+  p.fx = k.fx;
+  p.fy = k.fy;
+  p.cx = k.cx;
+  p.cy = k.cy;
+  p.near_m = k.near_m;
+  p.far_m = k.far_m;
+  p.near_lim = k.near_m * (1.0 - 1e-12);
+  p.far_f = static_cast<float>(k.far_m);
+  p.W = (int)k.width;
+  p.H = (int)k.height;
+  p.fcx = (float)k.cx;
+  p.fcy = (float)k.cy;
+  p.inv_fx = (float)(1.0 / k.fx);
+  p.inv_fy = (float)(1.0 / k.fy);
+  p.w2c = ctx->w2c;
+  p.verts = m.verts.as<double>();
+  p.tris = m.tris.as<uint32_t>();
+  p.nv = m.nv;
+  p.nt = m.nt;
+  p.draw_base = 0;
+  p.obs = ctx->obs_pts.as<float4>();
+  p.obs_count = ctx->obs_count.as<int>();
+  p.lik = ctx->lik;
+  p.zscratch = ctx->zscratch.as<unsigned long long>();
+  p.vscratch = ctx->vscratch.as<double>();
+  return p;
+}
+
+void finish_copy_out(b3d_gpu_context* ctx, void* dst, const void* src, size_t bytes) {
+  cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream),
+             "cudaMemcpyAsync D2H");
+}
+
+void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
+                  const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status) {
+  require_ready(ctx, true, true);
+  check(scores != nullptr, "bad arguments");
+  check(n > 0, "score_cells: no cells");
+  DeviceGuard dg(ctx->device);
+  const Mesh& m = get_mesh(ctx, mesh_id);
+  KParams p = base_params(ctx, m);
+  bool host_in = false;
+  if (poses) {
+    p.poses = static_cast<const KPose*>(
+        stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
+  } else {
+    check(grid != nullptr && grid->rotations && grid->n_rot > 0, "bad arguments");
+    const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
+    check(nt > 0, "pose grid: counts must be >= 1");
+    const uint64_t gn = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
+    check(grid->mode == B3D_GRID_PRODUCT || nt == grid->n_rot,
+          "pose grid: zip mode needs nx*ny*nz == n_rot");
+    check(gn == n, "pose grid: n does not match the grid size");
+    bool h2 = false;
+    p.poses = nullptr;
+    p.grid.center = pose_from_c(grid->center);
+    p.grid.center_dev = nullptr;
+    for (int a = 0; a < 3; ++a) {
+      p.grid.extent[a] = grid->extent[a];
+      p.grid.count[a] = (int)grid->count[a];
+    }
+    p.grid.rotations = static_cast<const double*>(
+        stage_in(ctx, ctx->rot_stage, grid->rotations, 32ull * grid->n_rot, &h2));
+    p.grid.n_rot = (int)grid->n_rot;
+    p.grid.mode = (int)grid->mode;
+    host_in = host_in || h2;
+  }
+  p.n_hyp = (long long)n;
+  const int nn = ctx->lik.n_noise;
+  const bool dev_scores = is_device_ptr(scores);
+  const bool dev_status = status && is_device_ptr(status);
+  if (dev_scores) {
+    p.scores = scores;
+  } else {
+    ctx->out_stage.ensure(sizeof(double) * n * nn);
+    p.scores = ctx->out_stage.as<double>();
+  }
+  if (status) {
+    if (dev_status) {
+      p.status = status;
+    } else {
+      ctx->out_stage2.ensure(n);
+      p.status = ctx->out_stage2.as<uint8_t>();
+    }
+  }
+  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n);
+  p.zscratch = ctx->zscratch.as<unsigned long long>();
+  p.vscratch = ctx->vscratch.as<double>();
+  p.vcap = lp.vcap;
+  p.zcap = lp.zcap;
+  cuda_check(launch_render_score<false, true, false>(p, lp.grid, lp.smem, ctx->stream),
+             "render_score launch");
+  bool sync = host_in;
+  if (!dev_scores) {
+    finish_copy_out(ctx, scores, p.scores, sizeof(double) * n * nn);
+    sync = true;
+  }
+  if (status && !dev_status) {
+    finish_copy_out(ctx, status, p.status, n);
+    sync = true;
+  }
+  if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "score_poses");
+}
+
+}  // namespace
+
+// =================================================================== C ABI
+extern "C" {
+
+const char* b3d_version(void) { return "0.1.0-b200"; }
+
+const char* b3d_last_error(void) { return g_last_error.c_str(); }
+
+struct b3d_depth_image {
+  uint32_t width = 0, height = 0;
+  std::vector<float> depth;
+};
+
+b3d_status b3d_depth_image_create(uint32_t width, uint32_t height, const float* depth,
+                                  b3d_depth_image** out) {
+  return guarded([&] {
+    check(out && depth && width > 0 && height > 0, "bad arguments");
+    auto h = std::make_unique<b3d_depth_image>();
+    h->width = width;
+    h->height = height;
+    h->depth.assign(depth, depth + static_cast<size_t>(width) * height);
+    *out = h.release();
+  });
+}
+
+uint32_t b3d_depth_image_width(const b3d_depth_image* img) { return img ? img->width : 0; }
+uint32_t b3d_depth_image_height(const b3d_depth_image* img) { return img ? img->height : 0; }
+const float* b3d_depth_image_data(const b3d_depth_image* img) {
+  return img ? img->depth.data() : nullptr;
+}
+void b3d_depth_image_destroy(b3d_depth_image* img) { delete img; }
+
+b3d_status b3d_log_likelihood(const b3d_depth_image* observed, const b3d_depth_image* rendered,
+                              const b3d_intrinsics* k, double p_outlier, double sigma_noise,
+                              double sigma_max, int window, double* out) {
+  return guarded([&] {
+    check(observed && rendered && k && out, "bad arguments");
+    validate_intrinsics(*k);
+    // likelihood.cpp:21-26 validate_noise
+    require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
+    require(sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
+    require(p_outlier >= 0 && p_outlier <= 1, ErrorCode::invalid,
+            "p_outlier must be in [0,1]");
+    if (window >= 0) {
+      require(observed->width == k->width && observed->height == k->height,
+              ErrorCode::invalid, "observation dimensions do not match intrinsics");
+      require(observed->width == rendered->width && observed->height == rendered->height,
+              ErrorCode::invalid, "windowed likelihood: image dimension mismatch");
+    } else {
+      require(observed->width == k->width && observed->height == k->height &&
+                  rendered->width == k->width && rendered->height == k->height,
+              ErrorCode::invalid, "depth_to_cloud: image dimensions do not match intrinsics");
+    }
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    const size_t npx = (size_t)k->width * k->height;
+    DevBuf d_obs, d_rend, d_acc, d_out, d_cnt;
+    d_obs.ensure(npx * 4);
+    d_rend.ensure(npx * 4);
+    d_acc.ensure(16);
+    d_out.ensure(8);
+    d_cnt.ensure(8);
+    cuda_check(cudaMemcpy(d_obs.p, observed->depth.data(), npx * 4, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    cuda_check(cudaMemcpy(d_rend.p, rendered->depth.data(), npx * 4, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    cuda_check(launch_image_loglik(d_obs.as<float>(), d_rend.as<float>(), (int)k->width,
+                                   (int)k->height, k->fx, k->fy, k->cx, k->cy,
+                                   static_cast<float>(k->far_m), p_outlier, sigma_noise,
+                                   sigma_max, visible_volume(*k), window, 0,
+                                   d_acc.as<unsigned long long>(), d_out.as<double>(),
+                                   d_cnt.as<int>(), nullptr),
+               "image_loglik launch");
+    int cnt = 0;
+    double v = 0;
+    cuda_check(cudaMemcpy(&cnt, d_cnt.p, 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    cuda_check(cudaMemcpy(&v, d_out.p, 8, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    if (window >= 0)
+      require(cnt > 0, ErrorCode::invalid, "windowed likelihood: empty rendered cloud");
+    else
+      require(cnt > 0, ErrorCode::invalid, "full_log_likelihood: empty rendered cloud");
+    *out = v;
+  });
+}
+
+b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
+  return guarded([&] {
+    check(out != nullptr, "bad arguments");
+    int n = 0;
+    cuda_check(cudaGetDeviceCount(&n), "cudaGetDeviceCount");
+    require(device >= 0 && device < n, ErrorCode::invalid, "gpu context: no such device");
+    DeviceGuard dg(device);
+    auto c = std::make_unique<b3d_gpu_context>();
+    c->device = device;
+    cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device),
+               "cudaDeviceGetAttribute");
+    cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    c->stream = c->own;
+    c->obs_count.ensure(sizeof(int));
+    c->result.ensure(sizeof(KStageResult));
+    c->rng.ensure(5 * sizeof(uint64_t));
+    *out = c.release();
+  });
+}
+
+void b3d_gpu_context_destroy(b3d_gpu_context* ctx) {
+  if (!ctx) return;
+  DeviceGuard dg(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  cudaStream_t own = ctx->own;
+  delete ctx;  // device buffers are released with the device current
+  if (own) cudaStreamDestroy(own);
+}
+
+b3d_status b3d_gpu_set_stream(b3d_gpu_context* ctx, void* cuda_stream) {
+  return guarded([&] {
+    check(ctx != nullptr, "bad arguments");
+    ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
+  });
+}
+
+b3d_status b3d_gpu_synchronize(b3d_gpu_context* ctx) {
+  return guarded([&] {
+    check(ctx != nullptr, "bad arguments");
+    DeviceGuard dg(ctx->device);
+    cuda_check(cudaStreamSynchronize(ctx->stream), "cudaStreamSynchronize");
+  });
+}
+
+b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics* k,
+                              const b3d_pose* camera) {
+  return guarded([&] {
+    check(ctx && k, "bad arguments");
+    validate_intrinsics(*k);
+    if (ctx->has_camera && (k->width != ctx->k.width || k->height != ctx->k.height))
+      ctx->has_obs = false;
+    ctx->k = *k;
+    const KPose cam = camera ? pose_from_c(*camera) : KPose{1, 0, 0, 0, 0, 0, 0};
+    ctx->w2c = pose_inverse(cam);
+    ctx->has_camera = true;
+  });
+}
+
+b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
+                               uint64_t n_vertices, const uint32_t* triangles,
+                               uint64_t n_triangles, int32_t* out_mesh_id) {
+  return guarded([&] {
+    check(ctx && vertices && triangles && out_mesh_id, "bad arguments");
+    check(n_vertices > 0 && n_triangles > 0, "mesh: empty");
+    check(n_vertices < (1u << 30) && n_triangles < (1u << 30), "mesh: too large");
+    for (uint64_t i = 0; i < 3 * n_triangles; ++i)
+      check(triangles[i] < n_vertices, "mesh: triangle index out of range");
+    DeviceGuard dg(ctx->device);
+    auto m = std::make_unique<Mesh>();
+    m->nv = (int)n_vertices;
+    m->nt = (int)n_triangles;
+    m->verts.ensure(24 * n_vertices);
+    m->tris.ensure(12 * n_triangles);
+    cuda_check(cudaMemcpy(m->verts.p, vertices, 24 * n_vertices, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    cuda_check(cudaMemcpy(m->tris.p, triangles, 12 * n_triangles, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    ctx->meshes.push_back(std::move(m));
+    *out_mesh_id = (int32_t)(ctx->meshes.size() - 1);
+  });
+}
+
+b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth) {
+  return guarded([&] {
+    check(ctx && depth, "bad arguments");
+    require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
+    DeviceGuard dg(ctx->device);
+    const b3d_intrinsics& k = ctx->k;
+    const size_t npx = (size_t)k.width * k.height;
+    bool host = false;
+    const float* d = static_cast<const float*>(stage_in(ctx, ctx->obs_depth, depth, npx * 4, &host));
+    ctx->obs_pts.ensure(npx * sizeof(float4));
+    cuda_check(launch_obs_prepare(d, (int)k.width, (int)k.height, static_cast<float>(k.far_m),
+                                  (float)k.cx, (float)k.cy, (float)(1.0 / k.fx),
+                                  (float)(1.0 / k.fy), ctx->obs_pts.as<float4>(),
+                                  ctx->obs_count.as<int>(), ctx->stream),
+               "obs_prepare launch");
+    if (host) cuda_check(cudaStreamSynchronize(ctx->stream), "set_observation");
+    ctx->has_obs = true;
+  });
+}
+
+b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
+                                  uint32_t n_noise, double sigma_max, int window,
+                                  int prefactor) {
+  return guarded([&] {
+    check(ctx && noise, "bad arguments");
+    require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
+    require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
+    require(n_noise <= (uint32_t)kMaxNoise, ErrorCode::invalid,
+            "gpu context: at most 4 noise settings per call");
+    require(window >= 0, ErrorCode::invalid, "window radius must be >= 0");
+    require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
+            ErrorCode::invalid, "unknown prefactor");
+    const double vol = visible_volume(ctx->k);
+    require(vol > 0, ErrorCode::invalid, "scene volume must be positive");
+    KLik L{};
+    L.n_noise = (int)n_noise;
+    L.window = window;
+    std::vector<double> slots;
+    for (uint32_t e = 0; e < n_noise; ++e) {
+      const b3d_noise& np = noise[e];
+      require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
+      require(np.sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
+      require(np.p_outlier >= 0 && np.p_outlier <= 1, ErrorCode::invalid,
+              "p_outlier must be in [0,1]");
+      require(np.p_outlier > 0, ErrorCode::invalid,
+              "gpu context: p_outlier must be > 0 on the fp32 likelihood path");
+      const double sigma2 = np.sigma_noise * np.sigma_noise;
+      L.one_minus_p[e] = 1.0 - np.p_outlier;
+      L.norm3[e] = std::pow(6.283185307179586476925287 * sigma2, -1.5);
+      L.floor_term[e] = np.p_outlier / vol;
+      L.log_floor[e] = std::log(L.floor_term[e]);
+      L.prefactor[e] = prefactor == B3D_PREFACTOR_PRINTED ? std::log(np.sigma_noise / sigma_max)
+                                                          : -std::log(sigma_max);
+      size_t s = 0;
+      while (s < slots.size() && slots[s] != np.sigma_noise) ++s;
+      if (s == slots.size()) slots.push_back(np.sigma_noise);
+      L.slot_of[e] = (int)s;
+    }
+    L.n_slots = (int)slots.size();
+    for (size_t s = 0; s < slots.size(); ++s)
+      L.slot_scale[s] = (float)(1.0 / (2.0 * slots[s] * slots[s]));
+    ctx->lik = L;
+    ctx->has_lik = true;
+  });
+}
+
+b3d_status b3d_gpu_score_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
+                               uint64_t n, double* scores, uint8_t* status) {
+  return guarded([&] {
+    check(poses != nullptr, "bad arguments");
+    score_common(ctx, mesh_id, poses, nullptr, n, scores, status);
+  });
+}
+
+b3d_status b3d_gpu_score_grid(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose_grid* grid,
+                              double* scores, uint8_t* status) {
+  return guarded([&] {
+    check(grid != nullptr, "bad arguments");
+    const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
+    const uint64_t n = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
+    score_common(ctx, mesh_id, nullptr, grid, n, scores, status);
+  });
+}
+
+b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
+                                uint64_t n, float* depth, int32_t* draw_index) {
+  return guarded([&] {
+    require_ready(ctx, false, false);
+    check(poses && depth && n > 0, "bad arguments");
+    DeviceGuard dg(ctx->device);
+    const Mesh& m = get_mesh(ctx, mesh_id);
+    KParams p = base_params(ctx, m);
+    bool host_in = false;
+    p.poses = static_cast<const KPose*>(
+        stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
+    p.n_hyp = (long long)n;
+    const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+    const bool dev_d = is_device_ptr(depth);
+    const bool dev_i = draw_index && is_device_ptr(draw_index);
+    if (dev_d) {
+      p.out_depth = depth;
+    } else {
+      ctx->out_stage.ensure(4 * npx * n);
+      p.out_depth = ctx->out_stage.as<float>();
+    }
+    if (draw_index) {
+      if (dev_i) {
+        p.out_ids = draw_index;
+      } else {
+        ctx->out_stage2.ensure(4 * npx * n);
+        p.out_ids = ctx->out_stage2.as<int32_t>();
+      }
+    }
+    bool sync = host_in;
+    if (draw_index) {
+      LaunchPlan lp = plan_launch<true, false, true>(ctx, m, (long long)n);
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      cuda_check(launch_render_score<true, false, true>(p, lp.grid, lp.smem, ctx->stream),
+                 "render launch");
+    } else {
+      LaunchPlan lp = plan_launch<false, false, true>(ctx, m, (long long)n);
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      cuda_check(launch_render_score<false, false, true>(p, lp.grid, lp.smem, ctx->stream),
+                 "render launch");
+    }
+    if (!dev_d) {
+      finish_copy_out(ctx, depth, p.out_depth, 4 * npx * n);
+      sync = true;
+    }
+    if (draw_index && !dev_i) {
+      finish_copy_out(ctx, draw_index, p.out_ids, 4 * npx * n);
+      sync = true;
+    }
+    if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "render_poses");
+  });
+}
+
+b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scores, uint64_t n,
+                                uint32_t stride, uint32_t col, uint64_t* rng_state,
+                                b3d_stage_result* out, double* probs) {
+  return guarded([&] {
+    check(ctx && scores && out && n > 0, "bad arguments");
+    check(stride >= 1 && col < stride, "stage_reduce: bad stride/column");
+    DeviceGuard dg(ctx->device);
+    bool host_in = false;
+    const double* d_scores = static_cast<const double*>(
+        stage_in(ctx, ctx->in_stage, scores, sizeof(double) * n * stride, &host_in));
+    unsigned long long* d_rng = nullptr;
+    const bool dev_rng = rng_state && is_device_ptr(rng_state);
+    if (rng_state) {
+      if (dev_rng) {
+        d_rng = reinterpret_cast<unsigned long long*>(rng_state);
+      } else {
+        cuda_check(cudaMemcpyAsync(ctx->rng.p, rng_state, 40, cudaMemcpyHostToDevice,
+                                   ctx->stream),
+                   "cudaMemcpyAsync");
+        d_rng = ctx->rng.as<unsigned long long>();
+        host_in = true;
+      }
+    }
+    const bool dev_out = is_device_ptr(out);
+    KStageResult* d_out = dev_out ? reinterpret_cast<KStageResult*>(out)
+                                  : ctx->result.as<KStageResult>();
+    const bool dev_probs = probs && is_device_ptr(probs);
+    double* d_probs = nullptr;
+    if (probs) {
+      if (dev_probs) {
+        d_probs = probs;
+      } else {
+        ctx->out_stage2.ensure(8 * n);
+        d_probs = ctx->out_stage2.as<double>();
+      }
+    }
+    cuda_check(launch_stage_reduce(d_scores, (long long)n, (int)stride, (int)col, d_rng, d_out,
+                                   d_probs, ctx->stream),
+               "stage_reduce launch");
+    bool sync = host_in;
+    if (!dev_out) {
+      finish_copy_out(ctx, out, d_out, sizeof(KStageResult));
+      sync = true;
+    }
+    if (rng_state && !dev_rng) finish_copy_out(ctx, rng_state, d_rng, 40);
+    if (probs && !dev_probs) {
+      finish_copy_out(ctx, probs, d_probs, 8 * n);
+      sync = true;
+    }
+    if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "stage_reduce");
+  });
+}
+
+// rng.hpp:8-13, rng.cpp:13-28
+static uint64_t splitmix64_next(uint64_t& s) {
+  uint64_t z = (s += 0x9e3779b97f4a7c15ull);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+  return z ^ (z >> 31);
+}
+
+void b3d_rng_seed(uint64_t seed, uint64_t state[5]) {
+  uint64_t s = seed;
+  state[0] = seed;
+  for (int i = 0; i < 4; ++i) state[1 + i] = splitmix64_next(s);
+}
+
+void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,
+                   uint64_t out[5]) {
+  auto mix = [](uint64_t a, uint64_t b) {
+    uint64_t s = a ^ (0x9e3779b97f4a7c15ull + (b << 6) + (b >> 2));
+    return splitmix64_next(s);
+  };
+  b3d_rng_seed(mix(mix(mix(state[0], k0), k1), k2), out);
+}
+
+b3d_status b3d_voxel_to_mesh(const int32_t* voxels, uint64_t n, double resolution,
+                             const double origin[3], double* vertices, uint32_t* triangles,
+                             uint64_t* n_vertices, uint64_t* n_triangles) {
+  return guarded([&] {
+    check(voxels && origin && vertices && triangles && n_vertices && n_triangles,
+          "bad arguments");
+    require(n > 0, ErrorCode::invalid, "voxel_to_mesh: empty grid");
+    // geometry.cpp:128-138
+    static const int kCorners[6][4][3] = {
+        {{0, 0, 0}, {0, 0, 1}, {0, 1, 1}, {0, 1, 0}},
+        {{1, 0, 0}, {1, 1, 0}, {1, 1, 1}, {1, 0, 1}},
+        {{0, 0, 0}, {1, 0, 0}, {1, 0, 1}, {0, 0, 1}},
+        {{0, 1, 0}, {0, 1, 1}, {1, 1, 1}, {1, 1, 0}},
+        {{0, 0, 0}, {0, 1, 0}, {1, 1, 0}, {1, 0, 0}},
+        {{0, 0, 1}, {1, 0, 1}, {1, 1, 1}, {0, 1, 1}},
+    };
+    static const int kOff[6][3] = {{-1, 0, 0}, {1, 0, 0},  {0, -1, 0},
+                                   {0, 1, 0},  {0, 0, -1}, {0, 0, 1}};
+    struct K3 {
+      int x, y, z;
+      bool operator==(const K3& o) const { return x == o.x && y == o.y && z == o.z; }
+    };
+    struct H3 {
+      size_t operator()(const K3& k) const {
+        uint64_t h = 1469598103934665603ull;
+        for (int v : {k.x, k.y, k.z}) {
+          h ^= (uint64_t)(uint32_t)v;
+          h *= 1099511628211ull;
+        }
+        return (size_t)h;
+      }
+    };
+    std::unordered_map<K3, uint8_t, H3> occ;
+    occ.reserve(2 * n);
+    for (uint64_t i = 0; i < n; ++i)
+      occ.emplace(K3{voxels[3 * i], voxels[3 * i + 1], voxels[3 * i + 2]}, 1);
+    std::unordered_map<K3, uint32_t, H3> corner;
+    uint64_t nv = 0, nt = 0;
+    for (uint64_t i = 0; i < n; ++i) {
+      const int* v = voxels + 3 * i;
+      for (int f = 0; f < 6; ++f) {
+        if (occ.count(K3{v[0] + kOff[f][0], v[1] + kOff[f][1], v[2] + kOff[f][2]})) continue;
+        uint32_t quad[4];
+        for (int c = 0; c < 4; ++c) {
+          const K3 cc{v[0] + kCorners[f][c][0], v[1] + kCorners[f][c][1],
+                      v[2] + kCorners[f][c][2]};
+          auto it = corner.find(cc);
+          if (it == corner.end()) {
+            it = corner.emplace(cc, (uint32_t)nv).first;
+            vertices[3 * nv + 0] = origin[0] + resolution * (double)cc.x;
+            vertices[3 * nv + 1] = origin[1] + resolution * (double)cc.y;
+            vertices[3 * nv + 2] = origin[2] + resolution * (double)cc.z;
+            ++nv;
+          }
+          quad[c] = it->second;
+        }
+        uint32_t* t = triangles + 3 * nt;
+        t[0] = quad[0];
+        t[1] = quad[1];
+        t[2] = quad[2];
+        t[3] = quad[0];
+        t[4] = quad[2];
+        t[5] = quad[3];
+        nt += 2;
+      }
+    }
+    *n_vertices = nv;
+    *n_triangles = nt;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,89 @@
+// b3d_kernels.cuh -- device-side data structures shared by the B200 kernels
+// and the C++ host layer.  No torch types: the host side is plain CUDA C++.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace b3d200 {
+
+// Same layout as b3d_pose (reference b3d.h:52-55).
+struct KPose {
+  double qw, qx, qy, qz;
+  double tx, ty, tz;
+};
+
+// BASELINE 6-DoF hypothesis grid (no reference equivalent):
+// translation lattice (tracking.cpp:27-37 formula) around the centre times a
+// table of rotation perturbations, q = normalized(center.q * dq[r]).
+struct KGrid {
+  KPose center;             // used when center_dev == nullptr
+  const KPose* center_dev;  // device-resident centre (stage chaining)
+  double extent[3];
+  int count[3];
+  const double* rotations;  // n_rot x 4 (w,x,y,z), device
+  int n_rot;
+  int mode;                 // 0 product, 1 zip
+};
+
+constexpr int kMaxNoise = 4;
+
+struct KLik {
+  int n_noise;
+  int n_slots;
+  int window;
+  int slot_of[kMaxNoise];
+  float slot_scale[kMaxNoise];   // 1/(2 sigma^2) per distinct sigma
+  double one_minus_p[kMaxNoise]; // 1 - p_outlier
+  double norm3[kMaxNoise];       // pow(2 pi sigma^2, -1.5)
+  double floor_term[kMaxNoise];  // p_outlier / V
+  double log_floor[kMaxNoise];   // log(floor_term)
+  double prefactor[kMaxNoise];   // log(sigma/sigma_max) or -log(sigma_max)
+};
+
+struct KParams {
+  // intrinsics (geometry.hpp:40-47)
+  double fx, fy, cx, cy, near_m, far_m, near_lim;
+  float far_f;
+  int W, H;
+  float fcx, fcy, inv_fx, inv_fy;  // fp32 back-projection for the likelihood
+  KPose w2c;                       // inverse(camera)
+  // mesh of the enumerated object
+  const double* verts;
+  const uint32_t* tris;
+  int nv, nt;
+  uint32_t draw_base;
+  // hypotheses
+  const KPose* poses;  // nullptr => grid
+  KGrid grid;
+  long long n_hyp;
+  // observation (per pixel: x, y, z, valid) + device count of valid pixels
+  const float4* obs;
+  const int* obs_count;
+  KLik lik;
+  // outputs
+  double* scores;     // n_hyp x n_noise
+  uint8_t* status;    // n_hyp (1 = empty render)
+  float* out_depth;   // n_hyp x W x H  (render mode)
+  int32_t* out_ids;   // n_hyp x W x H  (render mode, draw index or -1)
+  // per-CTA global scratch (used only when the on-chip buffers overflow)
+  unsigned long long* zscratch;  // gridDim x W*H keys
+  double* vscratch;              // gridDim x 3*nv
+  int vcap;                      // vertices cached in shared memory
+  int zcap;                      // z-buffer pixels in shared memory
+};
+
+struct KStageResult {
+  unsigned long long argmax;
+  unsigned long long sample;
+  double max_score;
+  double logsumexp;
+  double total;        // sum exp(x - max)
+  double sample_logp;  // x[sample] - logsumexp
+  unsigned int all_zero;
+  unsigned int n_nonfinite;
+  unsigned int sample_fallback;  // sequential CDF rescan was needed
+  unsigned int pad;
+};
+
+}  // namespace b3d200

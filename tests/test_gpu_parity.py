@@ -1,0 +1,236 @@
+"""GPU parity: the sm_100a product path (through the C ABI) against the CPU
+oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): per-pixel depth and triangle ids
+bit-exact (the kernels follow the oracle's fp64 operation order with no FMA;
+the north_star allows 1e-5 relative on depth, we require equality), log
+scores within 1e-4 relative (fp32 likelihood terms, fp64 accumulation), argmax
+identical unless the two top scores tie within that tolerance.
+"""
+import numpy as np
+import pytest
+
+from helpers import b3d_intr, cfg1_oracle, rel_err, square_k
+from paper_2312_08715_b200 import b3d, configs, synth
+
+pytestmark = pytest.mark.gpu
+
+SCORE_RTOL = 1e-4
+
+
+def _setup(ctx, w):
+    ctx.set_camera(b3d_intr(w.k))
+    mid = ctx.upload_mesh(w.vertices, w.triangles)
+    ctx.set_observation(w.observed)
+    ctx.set_likelihood(w.noise, w.sigma_max, w.window)
+    return mid
+
+
+def _render_parity(ctx, oracle, k, verts, tris, poses):
+    ctx.set_camera(b3d_intr(k))
+    mid = ctx.upload_mesh(verts, tris)
+    depth, ids = ctx.render_poses(mid, poses, with_ids=True)
+    for i in range(poses.shape[0]):
+        od, oi = oracle.render(k, [(verts, tris, poses[i])], with_ids=True)
+        np.testing.assert_array_equal(depth[i].view(np.uint32), od.view(np.uint32),
+                                      err_msg=f"depth bits differ, hypothesis {i}")
+        np.testing.assert_array_equal(ids[i], oi, err_msg=f"triangle ids differ, hypothesis {i}")
+    # depth-only render mode agrees with the id mode
+    d2, _ = ctx.render_poses(mid, poses, with_ids=False)
+    np.testing.assert_array_equal(d2.view(np.uint32), depth.view(np.uint32))
+    return depth, ids
+
+
+def test_render_parity_cfg1(gpu_ctx, oracle):
+    w = cfg1_oracle()
+    poses = w.grid_poses()[::16]
+    depth, ids = _render_parity(gpu_ctx, oracle, w.k, w.vertices, w.triangles, poses)
+    assert (ids >= 0).sum() > 1000
+
+
+def test_render_parity_random_walk_blob(gpu_ctx, oracle):
+    w = cfg1_oracle(seed=3, blob="random_walk")
+    _render_parity(gpu_ctx, oracle, w.k, w.vertices, w.triangles, w.grid_poses()[::64])
+
+
+def test_render_parity_near_clipping_and_overflow(gpu_ctx, oracle):
+    """Objects crossing z = near (renderer.cpp:127-141): the clipped fan path
+    and the full-image region that spills to global scratch."""
+    w = cfg1_oracle()
+    rng = np.random.Generator(np.random.PCG64(5))
+    poses = []
+    for i in range(12):
+        q = synth.uniform_quaternion(rng)
+        poses.append([q[0], q[1], q[2], q[3], rng.uniform(-0.01, 0.01),
+                      rng.uniform(-0.01, 0.01), rng.uniform(0.005, 0.05)])
+    poses = np.array(poses)
+    depth, ids = _render_parity(gpu_ctx, oracle, w.k, w.vertices, w.triangles, poses)
+    assert (ids >= 0).mean() > 0.2  # big on screen
+
+
+def test_render_parity_large_mesh_vertex_spill(gpu_ctx, oracle):
+    """A 4,000-voxel random-walk blob (>64 KB of projected vertices) uses the
+    global vertex scratch instead of shared memory."""
+    vox = synth.random_walk_blob(4000, 11)
+    verts, tris = configs.make_mesh(vox, oracle.voxel_to_mesh)
+    assert verts.shape[0] * 24 > 64 * 1024
+    k = configs.Intr(250.0, 250.0, 100.0, 100.0, 200, 200, 0.01, 10.0)
+    rng = np.random.Generator(np.random.PCG64(2))
+    poses = np.array([[*synth.uniform_quaternion(rng), 0.0, 0.0, 0.9] for _ in range(4)])
+    _render_parity(gpu_ctx, oracle, k, verts, tris, poses)
+
+
+def test_render_parity_table_box_scene(gpu_ctx, oracle):
+    """A box mesh (make_box_mesh) seen from a spherical camera, as in the
+    reference renderer tests (test_renderer.cpp:172-197)."""
+    k = square_k(32)
+    verts, tris = oracle.box_mesh([-0.05, -0.04, 0.0], [0.05, 0.04, 0.09])
+    cams = [oracle.camera_pose_from_spherical(0.5 + 0.1 * i, 0.7 * i, 0.5 + 0.05 * i)
+            for i in range(6)]
+    gpu_ctx.set_camera(b3d_intr(k))
+    mid = gpu_ctx.upload_mesh(verts, tris)
+    ident = np.array([[1, 0, 0, 0, 0, 0, 0.0]])
+    for cam in cams:
+        gpu_ctx.set_camera(b3d_intr(k), cam)
+        d, ids = gpu_ctx.render_poses(mid, ident)
+        od, oi = oracle.render(k, [(verts, tris, ident[0])], camera=cam, with_ids=True)
+        np.testing.assert_array_equal(d[0].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[0], oi)
+
+
+def test_score_parity_cfg1(gpu_ctx, oracle):
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    grid = gpu_ctx.make_grid(w.center, w.extent, w.count, w.rotations, w.grid_mode)
+    s_gpu, st_gpu = gpu_ctx.score_grid(mid, grid)
+    poses = w.grid_poses()
+    s_orc, st_orc = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
+                                       w.sigma_max, w.window)
+    np.testing.assert_array_equal(st_gpu, st_orc)
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+    # the fp32 likelihood terms are far tighter than the bar in practice
+    assert np.abs(s_gpu - s_orc).max() < 0.05
+    a_gpu, a_orc = int(np.argmax(s_gpu[:, 0])), oracle.argmax(s_orc[:, 0])
+    if a_gpu != a_orc:
+        assert abs(s_orc[a_gpu, 0] - s_orc[a_orc, 0]) <= SCORE_RTOL * abs(s_orc[a_orc, 0])
+    # explicit poses == device grid, bitwise
+    s_p, _ = gpu_ctx.score_poses(mid, poses)
+    np.testing.assert_array_equal(s_p, s_gpu)
+
+
+def test_score_parity_multi_noise(gpu_ctx, oracle):
+    w = cfg1_oracle(seed=1)
+    noise = [(0.01, 0.005), (0.3, 0.005), (0.05, 0.02), (0.8, 0.01)]
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    gpu_ctx.set_likelihood(noise, 0.1, 2)
+    poses = w.grid_poses()[::8]
+    s_gpu, _ = gpu_ctx.score_poses(mid, poses)
+    s_orc, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, noise, 0.1, 2)
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+
+
+def test_score_uniform_prefactor_and_windows(gpu_ctx, oracle):
+    w = cfg1_oracle(seed=2)
+    poses = w.grid_poses()[::32]
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    for window in (0, 1, 3, 5):
+        gpu_ctx.set_likelihood(w.noise, 0.1, window, b3d.PREFACTOR_UNIFORM)
+        s_gpu, _ = gpu_ctx.score_poses(mid, poses)
+        s_orc, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
+                                      0.1, window, prefactor=1)
+        assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL, window
+
+
+def test_empty_render_status(gpu_ctx, oracle):
+    """Hypotheses entirely behind the camera render nothing: the reference
+    throws (likelihood.cpp:159-160); batched scoring flags them and returns
+    -inf so the rest of the batch survives."""
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    poses = w.grid_poses()[:4].copy()
+    poses[1, 6] = -0.5
+    poses[3, 4] = 50.0
+    s, st = gpu_ctx.score_poses(mid, poses)
+    assert list(st) == [0, 1, 0, 1]
+    assert np.isneginf(s[1, 0]) and np.isneginf(s[3, 0])
+    assert np.isfinite(s[0, 0]) and np.isfinite(s[2, 0])
+
+
+def test_stage_reduce_matches_oracle(gpu_ctx, oracle):
+    rng = np.random.Generator(np.random.PCG64(9))
+    for n in (1, 7, 1024, 32768, 100003):
+        x = rng.normal(-2.0e4, 30.0, size=n)
+        if n > 10:
+            x[n // 3] = x.max() + 5.0
+            x[n // 2] = x[n // 3]  # tie: lowest index must win
+            x[5] = -np.inf
+        st_g = b3d.rng_seed(1234 + n)
+        st_o = oracle.rng_seed(1234 + n)
+        probs_g = np.zeros(n)
+        r = gpu_ctx.stage_reduce(x, rng_state=st_g, probs=probs_g)
+        probs_o, all_zero = oracle.normalize(x)
+        assert r.argmax == oracle.argmax(x)
+        assert not r.all_zero and not all_zero
+        assert abs(r.logsumexp - oracle.logsumexp(x)) <= 1e-12 * abs(oracle.logsumexp(x))
+        np.testing.assert_allclose(probs_g, probs_o, rtol=1e-12, atol=1e-300)
+        assert r.sample == oracle.sample_categorical(probs_o, st_o)
+        np.testing.assert_array_equal(st_g, st_o)  # stream advanced identically
+
+
+def test_stage_reduce_all_neg_inf(gpu_ctx, oracle):
+    x = np.full(1000, -np.inf)
+    st_g, st_o = b3d.rng_seed(5), oracle.rng_seed(5)
+    r = gpu_ctx.stage_reduce(x, rng_state=st_g)
+    probs_o, all_zero = oracle.normalize(x)
+    assert r.all_zero and all_zero and r.argmax == 0
+    assert r.sample == oracle.sample_categorical(probs_o, st_o)
+
+
+def test_log_likelihood_c_abi(oracle):
+    """b3d_log_likelihood keeps the reference signature and semantics."""
+    from helpers import make_k
+    k = make_k(16, 16, 20.0, 0.1, 5.0)
+    rng = np.random.Generator(np.random.PCG64(4))
+
+    def surf(sp):
+        img = np.full((16, 16), np.float32(5.0), dtype=np.float32)
+        m = rng.random((16, 16)) >= sp
+        img[m] = rng.uniform(0.5, 4.5, size=int(m.sum())).astype(np.float32)
+        return img
+
+    for trial in range(10):
+        obs, ren = surf(0.3), surf(0.3)
+        p, s = rng.uniform(0.05, 0.95), rng.uniform(0.01, 0.1)
+        for window in (0, 2, 16):
+            got = b3d.log_likelihood(obs, ren, b3d_intr(k), p, s, 0.1, window)
+            want = oracle.windowed_loglik_multi(obs, ren, k, [(p, s)], 0.1, window)[0]
+            assert abs(got - want) <= 1e-10 * abs(want)
+        got = b3d.log_likelihood(obs, ren, b3d_intr(k), p, s, 0.1, -1)
+        want = oracle.full_loglik(obs, ren, k, (p, s), 0.1)
+        assert abs(got - want) <= 1e-10 * abs(want)
+    empty = np.full((16, 16), np.float32(5.0), dtype=np.float32)
+    with pytest.raises(b3d.B3DError, match="empty rendered cloud"):
+        b3d.log_likelihood(surf(0.3), empty, b3d_intr(k), 0.5, 0.01, 0.1, 2)
+
+
+def test_device_pointers_async_path(gpu_ctx, oracle):
+    """Device-resident inputs/outputs (torch CUDA tensors) give the same bits
+    as the host-buffer path."""
+    import torch
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    poses = w.grid_poses()
+    s_host, _ = gpu_ctx.score_poses(mid, poses)
+    dp = torch.from_numpy(poses).cuda()
+    ds = torch.zeros((poses.shape[0], 1), dtype=torch.float64, device="cuda")
+    dst = torch.zeros(poses.shape[0], dtype=torch.uint8, device="cuda")
+    gpu_ctx.set_stream(torch.cuda.current_stream().cuda_stream)
+    gpu_ctx.set_observation(torch.from_numpy(w.observed).cuda())
+    gpu_ctx.score_poses(mid, dp, ds, dst)
+    torch.cuda.synchronize()
+    gpu_ctx.set_stream(None)
+    np.testing.assert_array_equal(ds.cpu().numpy(), s_host)
