@@ -197,7 +197,10 @@ def main():
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
-    stream = torch.cuda.current_stream(dev)
+    # a dedicated (non-default) stream shared by torch and the C ABI context,
+    # so the CUDA events below bracket exactly the work they time
+    stream = torch.cuda.Stream(dev)
+    torch.cuda.set_stream(stream)
     ctx = b3d.GpuContext(local)
     ctx.set_stream(stream.cuda_stream)
 

@@ -10,6 +10,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <stdexcept>
@@ -25,7 +27,10 @@ namespace b3d200 {
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st);
 template <bool kIds, bool kScore, bool kOut>
-cudaError_t occupancy_render_score(int* blocks, size_t smem);
+cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs);
+template <bool kIds, bool kScore, bool kOut>
+size_t static_smem_render_score();
+size_t render_score_staging_bytes(int nt);
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
@@ -177,6 +182,7 @@ struct b3d_gpu_context {
   DevBuf obs_depth, obs_pts, obs_count;
   bool has_lik = false;
   KLik lik{};
+  int cull = 0;  // B3D_OCCLUSION_CULL=1: exact two-pass back-face occlusion culling
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
 };
@@ -254,6 +260,7 @@ const void* stage_in(b3d_gpu_context* ctx, DevBuf& buf, const void* src, size_t 
 }
 
 struct LaunchPlan {
+  long long zstride = 0;
   int grid = 0;
   size_t smem = 0;
   int vcap = 0;
@@ -264,24 +271,47 @@ template <bool kIds, bool kScore, bool kOut>
 LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n) {
   LaunchPlan lp;
   const size_t key = kIds ? 8 : 4;
-  const size_t budget = 110 * 1024;  // two resident CTAs per SM
-  const size_t vbytes = 24ull * m.nv;
-  lp.vcap = vbytes <= 64 * 1024 ? m.nv : 0;
   const size_t npx = (size_t)ctx->k.width * ctx->k.height;
-  size_t zcap = (budget - 24ull * lp.vcap) / key;
-  if (zcap > npx) zcap = npx;
+  // largest CTAs/SM (3, 2, 1) whose shared memory holds the projected
+  // vertices plus a region z-buffer of at least 4,096 pixels; otherwise the
+  // vertices spill to the per-CTA global scratch
+  const size_t vbytes = 32ull * m.nv;  // u, v, 1/z (fp64) + packed int bbox
+  const size_t stage = render_score_staging_bytes(m.nt);
+  const size_t zmin = std::min<size_t>(2048, npx) * key;
+  // shared memory per SM is 228 KB (227 KB max per CTA), 1 KB reserved per
+  // CTA, plus the kernel's static shared memory
+  const size_t stat = static_smem_render_score<kIds, kScore, kOut>();
+  auto budget_for = [&](int b) {
+    size_t bud = 233472 / b - 1024 - stat;
+    return std::min<size_t>(bud, 232448 - stat);
+  };
+  size_t budget = 0;
+  lp.vcap = 0;
+  for (int b = 2; b >= 1; --b) {
+    budget = budget_for(b);
+    if (vbytes + stage + zmin <= budget) {
+      lp.vcap = m.nv;
+      break;
+    }
+  }
+  if (lp.vcap == 0) budget = budget_for(2);
+  size_t zcap = (budget - 32ull * lp.vcap - stage) / key;
+  if (zcap > npx + 8 * (ctx->k.width + ctx->k.height) + 64)
+    zcap = npx + 8 * (ctx->k.width + ctx->k.height) + 64;
   lp.zcap = (int)zcap;
-  lp.smem = 24ull * lp.vcap + key * zcap;
+  lp.smem = 32ull * lp.vcap + stage + key * zcap;
   int per_sm = 0;
-  cuda_check(occupancy_render_score<kIds, kScore, kOut>(&per_sm, lp.smem), "occupancy");
+  cuda_check(occupancy_render_score<kIds, kScore, kOut>(&per_sm, lp.smem, lp.vcap >= m.nv), "occupancy");
   if (per_sm < 1) per_sm = 1;
   long long grid = (long long)per_sm * ctx->sm_count;
   if (grid > n) grid = n;
   if (grid < 1) grid = 1;
   lp.grid = (int)grid;
   // overflow scratch for hypotheses whose region / mesh exceeds shared memory
-  ctx->zscratch.ensure((size_t)lp.grid * npx * 8);
-  if (lp.vcap < m.nv) ctx->vscratch.ensure((size_t)lp.grid * 24 * m.nv);
+  const int pad = kScore ? 2 * ctx->lik.window : 0;
+  lp.zstride = (long long)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
+  ctx->zscratch.ensure((size_t)lp.grid * lp.zstride * 8);
+  if (lp.vcap < m.nv) ctx->vscratch.ensure((size_t)lp.grid * 32 * m.nv);
   return lp;
 }
 
@@ -304,7 +334,7 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.inv_fy = (float)(1.0 / k.fy);
   p.w2c = ctx->w2c;
   p.verts = m.verts.as<double>();
-  p.tris = m.tris.as<uint32_t>();
+  p.tris = m.tris.as<uint4>();
   p.nv = m.nv;
   p.nt = m.nt;
   p.draw_base = 0;
@@ -313,6 +343,7 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.lik = ctx->lik;
   p.zscratch = ctx->zscratch.as<unsigned long long>();
   p.vscratch = ctx->vscratch.as<double>();
+  p.cull = ctx->cull;
   return p;
 }
 
@@ -378,6 +409,7 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   p.vscratch = ctx->vscratch.as<double>();
   p.vcap = lp.vcap;
   p.zcap = lp.zcap;
+  p.zstride = lp.zstride;
   cuda_check(launch_render_score<false, true, false>(p, lp.grid, lp.smem, ctx->stream),
              "render_score launch");
   bool sync = host_in;
@@ -491,6 +523,7 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
                "cudaDeviceGetAttribute");
     cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
+    if (const char* env = std::getenv("B3D_OCCLUSION_CULL")) c->cull = std::atoi(env) != 0;
     c->obs_count.ensure(sizeof(int));
     c->result.ensure(sizeof(KStageResult));
     c->rng.ensure(5 * sizeof(uint64_t));
@@ -527,6 +560,8 @@ b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics* k,
   return guarded([&] {
     check(ctx && k, "bad arguments");
     validate_intrinsics(*k);
+    require(k->width <= 16384 && k->height <= 16384, ErrorCode::invalid,
+            "gpu context: image dimensions above 16384 are not supported");
     if (ctx->has_camera && (k->width != ctx->k.width || k->height != ctx->k.height))
       ctx->has_obs = false;
     ctx->k = *k;
@@ -550,10 +585,14 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
     m->nv = (int)n_vertices;
     m->nt = (int)n_triangles;
     m->verts.ensure(24 * n_vertices);
-    m->tris.ensure(12 * n_triangles);
+    m->tris.ensure(16 * n_triangles);
+    // triangles padded to 16 bytes: one 128-bit load per triangle
+    std::vector<uint32_t> padded(4 * n_triangles, 0u);
+    for (uint64_t i = 0; i < n_triangles; ++i)
+      for (int j = 0; j < 3; ++j) padded[4 * i + j] = triangles[3 * i + j];
     cuda_check(cudaMemcpy(m->verts.p, vertices, 24 * n_vertices, cudaMemcpyHostToDevice),
                "cudaMemcpy");
-    cuda_check(cudaMemcpy(m->tris.p, triangles, 12 * n_triangles, cudaMemcpyHostToDevice),
+    cuda_check(cudaMemcpy(m->tris.p, padded.data(), 16 * n_triangles, cudaMemcpyHostToDevice),
                "cudaMemcpy");
     ctx->meshes.push_back(std::move(m));
     *out_mesh_id = (int32_t)(ctx->meshes.size() - 1);
@@ -620,7 +659,7 @@ b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
     }
     L.n_slots = (int)slots.size();
     for (size_t s = 0; s < slots.size(); ++s)
-      L.slot_scale[s] = (float)(1.0 / (2.0 * slots[s] * slots[s]));
+      L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
     ctx->lik = L;
     ctx->has_lik = true;
   });
@@ -680,6 +719,7 @@ b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d
       p.vscratch = ctx->vscratch.as<double>();
       p.vcap = lp.vcap;
       p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
       cuda_check(launch_render_score<true, false, true>(p, lp.grid, lp.smem, ctx->stream),
                  "render launch");
     } else {
@@ -688,6 +728,7 @@ b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d
       p.vscratch = ctx->vscratch.as<double>();
       p.vcap = lp.vcap;
       p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
       cuda_check(launch_render_score<false, false, true>(p, lp.grid, lp.smem, ctx->stream),
                  "render launch");
     }

@@ -33,7 +33,7 @@ struct KLik {
   int n_slots;
   int window;
   int slot_of[kMaxNoise];
-  float slot_scale[kMaxNoise];   // 1/(2 sigma^2) per distinct sigma
+  float slot_scale[kMaxNoise];   // log2(e)/(2 sigma^2) per distinct sigma (exp2 form)
   double one_minus_p[kMaxNoise]; // 1 - p_outlier
   double norm3[kMaxNoise];       // pow(2 pi sigma^2, -1.5)
   double floor_term[kMaxNoise];  // p_outlier / V
@@ -50,9 +50,10 @@ struct KParams {
   KPose w2c;                       // inverse(camera)
   // mesh of the enumerated object
   const double* verts;
-  const uint32_t* tris;
+  const uint4* tris;  // (i0, i1, i2, 0) per triangle
   int nv, nt;
   uint32_t draw_base;
+  int cull;  // two-pass conservative occlusion culling of back faces (exact)
   // hypotheses
   const KPose* poses;  // nullptr => grid
   KGrid grid;
@@ -67,7 +68,8 @@ struct KParams {
   float* out_depth;   // n_hyp x W x H  (render mode)
   int32_t* out_ids;   // n_hyp x W x H  (render mode, draw index or -1)
   // per-CTA global scratch (used only when the on-chip buffers overflow)
-  unsigned long long* zscratch;  // gridDim x W*H keys
+  unsigned long long* zscratch;  // gridDim x zstride keys
+  long long zstride;             // (W + 4w) * (H + 4w): padded full-image region
   double* vscratch;              // gridDim x 3*nv
   int vcap;                      // vertices cached in shared memory
   int zcap;                      // z-buffer pixels in shared memory

@@ -32,35 +32,27 @@ namespace {
 
 using namespace pm;
 
-// static_cast<int>(double) as the x86-64 reference build executes it
-// (cvttsd2si: out of range or NaN -> INT_MIN).
-__device__ __forceinline__ int to_int_x86(double x) {
-  if (!(x > -2147483649.0 && x < 2147483648.0)) return (int)0x80000000u;
-  return __double2int_rz(x);
-}
 
 struct SV {
   double u, v, iz;
 };
 
-// renderer.cpp:26-59, with the orientation sign folded into the canonical
-// deltas: sign*(cdx*A - cdy*B) == (sign*cdx)*A - (sign*cdy)*B bitwise for
-// sign = +-1 (round-to-nearest is symmetric; only the sign of an exact zero
-// can differ, which neither the fill rule nor the depth test observes).
+// renderer.cpp:26-59.  EdgeFn::eval is sign*(cdx*(py-oy) - cdy*(px-ox))
+// with (cdx, cdy) = hi - lo of the canonically ordered endpoints.  Since
+// sign*cdx == b.u - a.u bitwise (round-to-nearest is antisymmetric) and
+// sign*(X - Y) == (sign*X') - (sign*Y') with X' = cdx*A, the edge value is
+// (b.u-a.u)*(py-oy) - (b.v-a.v)*(px-ox) with the canonical origin o: the same
+// bits except possibly the sign of an exact zero, which neither the fill
+// rule (e > 0 / e < 0 / tie) nor the 1/z test (inv_z <= 0) can observe.
 struct Edge {
-  double ox, oy, scdx, scdy, dx, dy;
+  double ox, oy, dx, dy;
 };
 
 __device__ __forceinline__ Edge make_edge(const SV& a, const SV& b) {
   const bool canonical = a.u < b.u || (a.u == b.u && a.v < b.v);
-  const double lou = canonical ? a.u : b.u, lov = canonical ? a.v : b.v;
-  const double hiu = canonical ? b.u : a.u, hiv = canonical ? b.v : a.v;
   Edge e;
-  e.ox = lou;
-  e.oy = lov;
-  const double cdx = hiu - lou, cdy = hiv - lov;
-  e.scdx = canonical ? cdx : -cdx;
-  e.scdy = canonical ? cdy : -cdy;
+  e.ox = canonical ? a.u : b.u;
+  e.oy = canonical ? a.v : b.v;
   e.dx = b.u - a.u;
   e.dy = b.v - a.v;
   return e;
@@ -90,14 +82,19 @@ __device__ __forceinline__ void zmin(unsigned long long* p, unsigned long long v
   if (v < *p) atomicMin(p, v);
 }
 
+// Screen region of one hypothesis: interior [u0,u1]x[v0,v1] (clipped to the
+// image) that the object can touch, stored with a background halo of `pad`
+// pixels so the likelihood's window taps never need bounds checks.
+// Buffer index of pixel (u, v): (v - oy) * rw + (u - ox).
 struct Region {
-  int u0, v0, u1, v1, rw;
+  int u0, v0, u1, v1, ox, oy, rw, rh;
 };
 
-// renderer.cpp:61-103 -- one screen triangle into the region z-buffer.
+// renderer.cpp:63-102 for a triangle whose integer pixel bbox is known.
 template <bool kIds>
-__device__ void raster_tri(const KParams& p, typename KeyT<kIds>::T* zb, const Region& rg,
-                           SV a, SV b, SV c, uint32_t draw) {
+__device__ __forceinline__ void raster_tri_box(const KParams& p, typename KeyT<kIds>::T* zb,
+                                               const Region& rg, SV a, SV b, SV c, int u_min,
+                                               int u_max, int v_min, int v_max, uint32_t draw) {
   double area2 = (b.u - a.u) * (c.v - a.v) - (b.v - a.v) * (c.u - a.u);
   if (area2 == 0) return;
   if (area2 < 0) {
@@ -106,41 +103,21 @@ __device__ void raster_tri(const KParams& p, typename KeyT<kIds>::T* zb, const R
     c = t;
     area2 = -area2;
   }
-  double mnu = a.u, mxu = a.u, mnv = a.v, mxv = a.v;
-  if (b.u < mnu) mnu = b.u;
-  if (c.u < mnu) mnu = c.u;
-  if (mxu < b.u) mxu = b.u;
-  if (mxu < c.u) mxu = c.u;
-  if (b.v < mnv) mnv = b.v;
-  if (c.v < mnv) mnv = c.v;
-  if (mxv < b.v) mxv = b.v;
-  if (mxv < c.v) mxv = c.v;
-  int u_min = to_int_x86(ceil(mnu));
-  if (u_min < 0) u_min = 0;
-  int u_max = to_int_x86(floor(mxu));
-  if (u_max > p.W - 1) u_max = p.W - 1;
-  int v_min = to_int_x86(ceil(mnv));
-  if (v_min < 0) v_min = 0;
-  int v_max = to_int_x86(floor(mxv));
-  if (v_max > p.H - 1) v_max = p.H - 1;
-  if (u_min > u_max || v_min > v_max) return;
-
   const Edge ab = make_edge(a, b);
   const Edge bc = make_edge(b, c);
   const Edge ca = make_edge(c, a);
   const double inv_area2 = 1.0 / area2;
-
   for (int pv = v_min; pv <= v_max; ++pv) {
     const double py = pv;
-    const double r_ab = ab.scdx * (py - ab.oy);
-    const double r_bc = bc.scdx * (py - bc.oy);
-    const double r_ca = ca.scdx * (py - ca.oy);
-    typename KeyT<kIds>::T* row = zb + (pv - rg.v0) * rg.rw - rg.u0;
+    const double r_ab = ab.dx * (py - ab.oy);
+    const double r_bc = bc.dx * (py - bc.oy);
+    const double r_ca = ca.dx * (py - ca.oy);
+    typename KeyT<kIds>::T* row = zb + (pv - rg.oy) * rg.rw - rg.ox;
     for (int pu = u_min; pu <= u_max; ++pu) {
       const double px = pu;
-      const double e_ab = r_ab - ab.scdy * (px - ab.ox);
-      const double e_bc = r_bc - bc.scdy * (px - bc.ox);
-      const double e_ca = r_ca - ca.scdy * (px - ca.ox);
+      const double e_ab = r_ab - ab.dy * (px - ab.ox);
+      const double e_bc = r_bc - bc.dy * (px - bc.ox);
+      const double e_ca = r_ca - ca.dy * (px - ca.ox);
       if (!covers(ab, e_ab) || !covers(bc, e_bc) || !covers(ca, e_ca)) continue;
       const double inv_z = (e_bc * a.iz + e_ca * b.iz + e_ab * c.iz) * inv_area2;
       if (inv_z <= 0) continue;
@@ -159,6 +136,22 @@ __device__ void raster_tri(const KParams& p, typename KeyT<kIds>::T* zb, const R
   }
 }
 
+// renderer.cpp:61-103 -- one screen triangle into the region z-buffer
+// (clipped path: the bbox comes from the fp64 vertex coordinates).  The
+// bounds reproduce static_cast<int> on x86-64 exactly: a max u or v beyond
+// the int range converts to INT_MIN there and empties the bbox.
+template <bool kIds>
+__device__ __forceinline__ void raster_tri(const KParams& p, typename KeyT<kIds>::T* zb,
+                                           const Region& rg, SV a, SV b, SV c, uint32_t draw) {
+  const double mnu = fmin(fmin(a.u, b.u), c.u), mxu = fmax(fmax(a.u, b.u), c.u);
+  const double mnv = fmin(fmin(a.v, b.v), c.v), mxv = fmax(fmax(a.v, b.v), c.v);
+  if (!(mxu < 2147483648.0) || !(mxv < 2147483648.0)) return;
+  const double cu0 = fmax(ceil(mnu), 0.0), fu1 = fmin(floor(mxu), (double)(p.W - 1));
+  const double cv0 = fmax(ceil(mnv), 0.0), fv1 = fmin(floor(mxv), (double)(p.H - 1));
+  if (cu0 > fu1 || cv0 > fv1) return;
+  raster_tri_box<kIds>(p, zb, rg, a, b, c, (int)cu0, (int)fu1, (int)cv0, (int)fv1, draw);
+}
+
 __device__ __forceinline__ SV project(const KParams& p, double x, double y, double z) {
   const double iz = 1.0 / z;
   SV s;
@@ -174,6 +167,58 @@ __device__ __forceinline__ void cam_vertex(const double* R, const double* t, con
   o[0] = (R[0] * v[0] + (R[1] * v[1] + R[2] * v[2])) + t[0];
   o[1] = (R[3] * v[0] + (R[4] * v[1] + R[5] * v[2])) + t[1];
   o[2] = (R[6] * v[0] + (R[7] * v[1] + R[8] * v[2])) + t[2];
+}
+
+// Packed per-vertex integer bbox data (screen bounds of one vertex), used to
+// reject triangles and size their pixel bbox with integer min/max:
+//   x = ceil(u) clamped to [0, W], y = floor(u) clamped to [-1, W-1] or
+//   kOvf when u >= 2^31 (the reference's static_cast<int> then yields INT_MIN
+//   and an empty bbox, renderer.cpp:70-76), z/w the same for v;
+//   x = kClipV marks a vertex in front of z = near (clipped path).
+constexpr short kOvf = 32767;
+constexpr short kClipV = -32768;
+
+__device__ __forceinline__ short4 vertex_bbox(const KParams& p, double u, double v) {
+  short4 r;
+  r.x = (short)fmin(fmax(ceil(u), 0.0), (double)p.W);
+  r.y = u >= 2147483648.0 ? kOvf : (short)fmin(fmax(floor(u), -1.0), (double)(p.W - 1));
+  r.z = (short)fmin(fmax(ceil(v), 0.0), (double)p.H);
+  r.w = v >= 2147483648.0 ? kOvf : (short)fmin(fmax(floor(v), -1.0), (double)(p.H - 1));
+  return r;
+}
+
+// Per-warp triangle records (structure of arrays: a warp reading the
+// records of different triangles hits distinct banks).  Filled by the lane
+// that sets the triangle up, read by whichever lane owns a pixel of it.
+struct WarpRec {
+  double inv_area2[32];
+  uint32_t ia[32], ib[32], ic[32];  // vertex ids after the orientation swap
+  uint32_t tri[32];                 // triangle index (draw order)
+  int uv0[32];                      // u_min | v_min << 16
+  int bwf[32];                      // bbox width | edge flags << 16
+  float inv_bw[32];
+};
+
+// Edge flags: bit e = canonical origin is the edge's first vertex
+// (renderer.cpp:47), bit 3+e = pixels exactly on the edge are covered
+// (top-left rule, renderer.cpp:39-43).
+__device__ __forceinline__ int edge_flags(const SV& a, const SV& b, int e) {
+  const bool canonical = a.u < b.u || (a.u == b.u && a.v < b.v);
+  const double dx = b.u - a.u, dy = b.v - a.v;
+  const bool tie = dy < 0 || (dy == 0 && dx > 0);
+  return ((int)canonical << e) | ((int)tie << (3 + e));
+}
+
+// Edge value of the directed edge (a -> b) at (px, py) with the canonical
+// origin selected by `canon` -- bitwise the reference's EdgeFn::eval.
+__device__ __forceinline__ double edge_at(double2 a, double2 b, bool canon, double px,
+                                          double py) {
+  const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+  return (b.x - a.x) * (py - oy) - (b.y - a.y) * (px - ox);
+}
+
+__device__ __forceinline__ bool edge_covers(double e, bool tie) {
+  return e > 0 || (e == 0 && tie);
 }
 
 // renderer.cpp:124-150 for a triangle with a vertex in front of z = near.
@@ -225,43 +270,449 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
-constexpr int kThreads = 256;
+// sum over the (2w+1)^2 window of exp(-|o - r|^2 / (2 sigma^2)) per distinct
+// sigma (likelihood.cpp:198-214) in fp32: rendered points back-projected on
+// the fly from the region buffer, exp as ex2 with the scale pre-multiplied
+// by log2(e).  Background taps give d^2 >= (far - z_obs)^2 and an exact 0.
+template <bool kIds, int kW>
+__device__ __forceinline__ void window_sums_w(const KParams& p,
+                                              const typename KeyT<kIds>::T* zb,
+                                              const Region& rg, int u, int v, float4 o,
+                                              float S[kMaxNoise]) {
+#pragma unroll
+  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  const float cu0 = ((float)(u - kW) - p.fcx) * p.inv_fx;
+  const float cv0 = ((float)(v - kW) - p.fcy) * p.inv_fy;
+  const typename KeyT<kIds>::T* row0 = zb + (v - kW - rg.oy) * rg.rw + (u - kW - rg.ox);
+#pragma unroll
+  for (int j = 0; j < 2 * kW + 1; ++j) {
+    const float cv = cv0 + (float)j * p.inv_fy;
+#pragma unroll
+    for (int k = 0; k < 2 * kW + 1; ++k) {
+      const typename KeyT<kIds>::T key = row0[j * rg.rw + k];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+      const float cu = cu0 + (float)k * p.inv_fx;
+      const float dx = __fmaf_rn(-cu, z, o.x);
+      const float dy = __fmaf_rn(-cv, z, o.y);
+      const float dz = o.z - z;
+      const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
+#pragma unroll
+      for (int s = 0; s < kMaxNoise; ++s)
+        if (s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+    }
+  }
+}
+
+template <bool kIds>
+__device__ __forceinline__ void window_sums_any(const KParams& p,
+                                                const typename KeyT<kIds>::T* zb,
+                                                const Region& rg, int u, int v, float4 o,
+                                                float S[kMaxNoise]) {
+#pragma unroll
+  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  const int w = p.lik.window;
+  for (int rv = v - w; rv <= v + w; ++rv) {
+    const float cv = ((float)rv - p.fcy) * p.inv_fy;
+    for (int ru = u - w; ru <= u + w; ++ru) {
+      const typename KeyT<kIds>::T key = zb[(rv - rg.oy) * rg.rw + (ru - rg.ox)];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+      const float cu = ((float)ru - p.fcx) * p.inv_fx;
+      const float dx = __fmaf_rn(-cu, z, o.x);
+      const float dy = __fmaf_rn(-cv, z, o.y);
+      const float dz = o.z - z;
+      const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
+#pragma unroll
+      for (int s = 0; s < kMaxNoise; ++s)
+        if (s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+    }
+  }
+}
+
+template <bool kIds>
+__device__ __forceinline__ void window_sums(const KParams& p, const typename KeyT<kIds>::T* zb,
+                                            const Region& rg, int u, int v, float4 o,
+                                            float S[kMaxNoise]) {
+  switch (p.lik.window) {
+    case 0: window_sums_w<kIds, 0>(p, zb, rg, u, v, o, S); break;
+    case 1: window_sums_w<kIds, 1>(p, zb, rg, u, v, o, S); break;
+    case 2: window_sums_w<kIds, 2>(p, zb, rg, u, v, o, S); break;
+    case 3: window_sums_w<kIds, 3>(p, zb, rg, u, v, o, S); break;
+    default: window_sums_any<kIds>(p, zb, rg, u, v, o, S); break;
+  }
+}
+
+constexpr float kBgDepth = 1e30f;
+constexpr int kThreads = 384;
 constexpr int kWarps = kThreads / 32;
 
 }  // namespace
 
+// Shared state of one CTA while it processes one hypothesis.
+struct HypCtx {
+  const double* R;  // rotation (row-major) in shared memory
+  const double* t;
+  Region rg;
+  bool empty_region, clip;
+  int rpx;
+};
+
+// Work of one hypothesis after the vertex phase: z-buffer init, raster,
+// render-many output and/or likelihood.  Instantiated twice per kernel so
+// that the z-buffer accesses compile to shared-memory instructions (kZS) or
+// global ones (overflow scratch), never to generic ones.
+template <bool kIds, bool kScore, bool kOut, typename VS, typename Key>
+__device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
+                                         const VS& vs, WarpRec* const wrec,
+                                         uint32_t* const def_list, int* s_ndef,
+                                         int* s_count, double* s_coef,
+                                         double (*s_red)[kMaxNoise],
+                                         int (*s_redi)[kMaxNoise + 1], long long h) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Region& rg = hc.rg;
+  const double* const R = hc.R;
+  const double* const t = hc.t;
+  // background depth 1e30 (not the far sentinel) so window taps on empty
+  // pixels give d^2 = inf and an exact 0 term for any sigma; the z-test is
+  // unchanged because every fragment is also tested zf < (float)far.
+  const Key bg = kIds ? (Key)(((unsigned long long)__float_as_uint(kBgDepth) << 32) |
+                              0xffffffffull)
+                      : (Key)__float_as_uint(kBgDepth);
+  for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
+  if (tid == 0) *s_ndef = 0;
+  __syncthreads();
+
+  // ---- C: raster.  C1: lane = triangle (mesh order): integer bbox reject,
+  // orientation, edge flags and 1/area into the warp's records.  C2: the
+  // warp's bbox pixels are dealt out one per lane (owner found by a 5-step
+  // shuffle search over the exclusive scan of pixel counts), so lanes stay
+  // busy whatever the per-triangle pixel counts are.
+  //
+  // With p.cull set, two passes: each pixel's final key is the minimum over
+  // all fragments of (fp32 depth bits[, draw index]) -- exactly the
+  // reference's strict-less test in draw order (renderer.cpp:99-100) -- so
+  // triangles may be processed in any order and one that provably cannot
+  // lower any key may be skipped.  Pass 0 rasterizes front-facing triangles
+  // and defers back-facing ones; pass 1 skips a deferred triangle when its
+  // nearest possible depth (1/max vertex 1/z, minus a 1e-9 relative margin
+  // for interpolation rounding, rounded down) is strictly behind every
+  // current depth in its bbox, and rasterizes it exactly otherwise.
+  if (!hc.empty_region || hc.clip) {
+    WarpRec& wr = wrec[warp];
+    const int n_pass = p.cull ? 2 : 1;
+    for (int pass = 0; pass < n_pass; ++pass) {
+      if (pass == 1) __syncthreads();
+      const int n_items = pass == 0 ? p.nt : *s_ndef;
+      for (int base = warp * 32; base < n_items; base += kThreads) {
+        __syncwarp();
+        const int ti = base + lane < n_items
+                           ? (pass == 0 ? base + lane : (int)def_list[base + lane])
+                           : p.nt;
+        int cnt = 0;
+        bool deferred = false;
+        if (ti < p.nt) {
+          const uint4 tri = __ldg(p.tris + ti);
+          uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
+          const short4 A = vs.bb[ia], B = vs.bb[ib], C = vs.bb[ic];
+          if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
+            raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
+          } else {
+            const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
+            const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
+            if (u_max != kOvf && v_max != kOvf && u_min <= u_max && v_min <= v_max) {
+              const double2 PA = vs.uv[ia];
+              double2 PB = vs.uv[ib], PC = vs.uv[ic];
+              double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
+              bool skip = area2 == 0;
+              if (!skip && p.cull && pass == 0 && area2 > 0) {  // back-facing (y down)
+                deferred = true;
+                skip = true;
+              }
+              if (!skip && pass == 1) {  // conservative occlusion test
+                const double izm = fmax(fmax(vs.iz[ia], vs.iz[ib]), vs.iz[ic]);
+                const float zlo = __double2float_rd((1.0 / izm) * (1.0 - 1e-9));
+                float zcur = 0.f;
+                for (int pv = v_min; pv <= v_max; ++pv) {
+                  const Key* row = zb + (pv - rg.oy) * rg.rw - rg.ox;
+                  for (int pu = u_min; pu <= u_max; ++pu)
+                    zcur = fmaxf(zcur, __uint_as_float((unsigned int)(
+                                           kIds ? ((unsigned long long)row[pu] >> 32)
+                                                : (unsigned long long)row[pu])));
+                }
+                skip = zlo > zcur;
+              }
+              if (!skip) {
+                if (area2 < 0) {  // renderer.cpp:65-69
+                  const double2 T = PB;
+                  PB = PC;
+                  PC = T;
+                  const uint32_t tt = ib;
+                  ib = ic;
+                  ic = tt;
+                  area2 = -area2;
+                }
+                const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
+                const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+                const int bw = u_max - u_min + 1;
+                wr.inv_area2[lane] = 1.0 / area2;
+                wr.tri[lane] = (uint32_t)ti;
+                wr.ia[lane] = ia;
+                wr.ib[lane] = ib;
+                wr.ic[lane] = ic;
+                wr.uv0[lane] = u_min | (v_min << 16);
+                wr.bwf[lane] = bw | (fl << 16);
+                wr.inv_bw[lane] = 1.0f / (float)bw;
+                cnt = bw * (v_max - v_min + 1);
+              }
+            }
+          }
+        }
+        if (p.cull && pass == 0) {  // append deferred triangles to the pass-1 list
+          const unsigned m = __ballot_sync(0xffffffffu, deferred);
+          int pos0 = 0;
+          if (lane == 0 && m) pos0 = atomicAdd(s_ndef, __popc(m));
+          pos0 = __shfl_sync(0xffffffffu, pos0, 0);
+          if (deferred) def_list[pos0 + __popc(m & ((1u << lane) - 1u))] = (uint32_t)ti;
+        }
+        int incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const int y = __shfl_up_sync(0xffffffffu, incl, o);
+          if (lane >= o) incl += y;
+        }
+        const int start = incl - cnt;
+        const int total = __shfl_sync(0xffffffffu, incl, 31);
+        __syncwarp();
+        for (int c0 = 0; c0 < total; c0 += 32) {
+          const int item = c0 + lane;
+          int own = 0;  // last lane whose start <= item (never a zero-count lane)
+#pragma unroll
+          for (int step = 16; step > 0; step >>= 1) {
+            const int sp = __shfl_sync(0xffffffffu, start, own + step);
+            if (sp <= item) own += step;
+          }
+          const int st = __shfl_sync(0xffffffffu, start, own);
+          if (item < total) {
+            const int k = item - st;
+            const int bwf = wr.bwf[own], uv0 = wr.uv0[own];
+            const int bw = bwf & 0xffff, fl = bwf >> 16;
+            const int dv = (int)(((float)k + 0.5f) * wr.inv_bw[own]);
+            const int pu = (uv0 & 0xffff) + (k - dv * bw);
+            const int pv = (uv0 >> 16) + dv;
+            const uint32_t ia = wr.ia[own], ib = wr.ib[own], ic = wr.ic[own];
+            const double2 a = vs.uv[ia], b = vs.uv[ib], c = vs.uv[ic];
+            const double px = pu, py = pv;
+            const double e_ab = edge_at(a, b, fl & 1, px, py);
+            const double e_bc = edge_at(b, c, fl & 2, px, py);
+            const double e_ca = edge_at(c, a, fl & 4, px, py);
+            if (edge_covers(e_ab, fl & 8) && edge_covers(e_bc, fl & 16) &&
+                edge_covers(e_ca, fl & 32)) {
+              // renderer.cpp:94-100
+              const double inv_z =
+                  (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * wr.inv_area2[own];
+              if (inv_z > 0) {
+                const double z = 1.0 / inv_z;
+                if (!(z < p.near_lim || z > p.far_m)) {
+                  const float zf = __double2float_rn(z);
+                  if (zf < p.far_f) {
+                    Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+                    if (kIds)
+                      zmin((unsigned long long*)cell,
+                           ((unsigned long long)__float_as_uint(zf) << 32) |
+                               (unsigned long long)(p.draw_base + wr.tri[own]));
+                    else
+                      zmin((unsigned int*)cell, __float_as_uint(zf));
+                  }
+                }
+              }
+            }
+          }
+        }
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- render-many output (sentinel = (float)far, id -1 = background)
+  if (kOut) {
+    const size_t npx = (size_t)p.W * p.H;
+    float* od = p.out_depth + (size_t)h * npx;
+    int32_t* oi = p.out_ids ? p.out_ids + (size_t)h * npx : nullptr;
+    for (int i = tid; i < (int)npx; i += kThreads) {
+      const int u = i % p.W, v = i / p.W;
+      Key k = bg;
+      if (!hc.empty_region && u >= rg.u0 && u <= rg.u1 && v >= rg.v0 && v <= rg.v1)
+        k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
+      od[i] = z < p.far_f ? z : p.far_f;
+      if (kIds && oi) {
+        const unsigned int d = (unsigned int)((unsigned long long)k & 0xffffffffull);
+        oi[i] = d == 0xffffffffu ? -1 : (int32_t)d;
+      }
+    }
+  }
+
+  if (kScore) {
+    // ---- D1: |y| = number of valid rendered pixels (likelihood.cpp:144-158)
+    int cnt = 0;
+    if (!hc.empty_region)
+      for (int i = tid; i < hc.rpx; i += kThreads) {
+        const float z = __uint_as_float(
+            kIds ? (unsigned int)((unsigned long long)zb[i] >> 32) : (unsigned int)zb[i]);
+        cnt += z < p.far_f;
+      }
+    cnt = warp_sum_i(cnt);
+    if (lane == 0 && cnt) atomicAdd(s_count, cnt);
+    __syncthreads();
+    const int rend_count = *s_count;
+    if (rend_count == 0) {
+      // the reference throws (likelihood.cpp:159-160); batched callers get
+      // -inf and a status flag instead
+      if (tid == 0) {
+        for (int e = 0; e < p.lik.n_noise; ++e)
+          p.scores[h * p.lik.n_noise + e] = -__longlong_as_double(0x7ff0000000000000ll);
+        if (p.status) p.status[h] = 1;
+      }
+      return;
+    }
+    if (tid < p.lik.n_noise)  // likelihood.cpp:167 coefficient order
+      s_coef[tid] = p.lik.one_minus_p[tid] / (double)rend_count * p.lik.norm3[tid];
+    __syncthreads();
+    float coef_f[kMaxNoise], floor_f[kMaxNoise];
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      coef_f[e] = e < p.lik.n_noise ? (float)s_coef[e] : 0.f;
+      floor_f[e] = e < p.lik.n_noise ? (float)p.lik.floor_term[e] : 0.f;
+    }
+
+    // ---- D2: window sums over the dilated region.  Observed pixels whose
+    // window holds no valid rendered pixel contribute exactly log(floor)
+    // (likelihood.cpp:209-216 with an empty dist2 list); they are counted.
+    // Taps are unconditional: the halo and every non-rendered pixel hold the
+    // background depth, whose Gaussian term underflows to exactly 0.
+    const int w = p.lik.window;
+    const int du0 = max(rg.u0 - w, 0), du1 = min(rg.u1 + w, p.W - 1);
+    const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
+    const int dw = du1 - du0 + 1;
+    const int dpx = hc.empty_region ? 0 : dw * (dv1 - dv0 + 1);
+    double acc[kMaxNoise];
+    int npos[kMaxNoise];
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      acc[e] = 0.0;
+      npos[e] = 0;
+    }
+    for (int i = tid; i < dpx; i += kThreads) {
+      const int v = dv0 + i / dw;
+      const int u = du0 + (i - (v - dv0) * dw);
+      const float4 o = __ldg(p.obs + (size_t)v * p.W + u);
+      if (o.w == 0.f) continue;
+      float S[kMaxNoise];
+      window_sums<kIds>(p, zb, rg, u, v, o, S);
+#pragma unroll
+      for (int e = 0; e < kMaxNoise; ++e) {
+        if (e < p.lik.n_noise) {
+          const float Se = S[p.lik.slot_of[e]];
+          if (Se > 0.f) {
+            acc[e] += (double)__logf(floor_f[e] + coef_f[e] * Se);
+            npos[e] += 1;
+          }
+        }
+      }
+    }
+    // ---- D3: fp64 block reduction -> one score per noise entry
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      acc[e] = warp_sum(acc[e]);
+      npos[e] = warp_sum_i(npos[e]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int e = 0; e < kMaxNoise; ++e) {
+        s_red[warp][e] = acc[e];
+        s_redi[warp][e] = npos[e];
+      }
+    }
+    __syncthreads();
+    if (tid < p.lik.n_noise) {
+      const int e = tid;
+      double a = 0.0;
+      int np = 0;
+      for (int k = 0; k < kWarps; ++k) {
+        a += s_red[k][e];
+        np += s_redi[k][e];
+      }
+      const int m_zero = *p.obs_count - np;
+      double total = p.lik.prefactor[e] + a;
+      if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
+      p.scores[h * p.lik.n_noise + e] = total;
+    }
+    if (tid == 0 && p.status) p.status[h] = 0;
+  }
+}
+
+// Projected-vertex cache: (u, v) and 1/z in fp64 plus the packed integer
+// bbox, in shared memory (kVS) or in the CTA's global scratch.
+struct VertexCache {
+  double2* uv;
+  double* iz;
+  short4* bb;
+};
+
 // kIds: 64-bit (depth, draw) keys; kScore: run the likelihood epilogue;
-// kOut: write the full depth / id images to HBM (render-many).
-template <bool kIds, bool kScore, bool kOut>
-__global__ void __launch_bounds__(kThreads) render_score_kernel(const KParams p) {
+// kOut: write the full depth / id images to HBM (render-many); kVS: the
+// projected vertices fit in shared memory.
+template <bool kIds, bool kScore, bool kOut, bool kVS>
+__global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams p) {
   using Key = typename KeyT<kIds>::T;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  __shared__ double s_R[9], s_t[3];
+  __shared__ double s_pose[32][12];  // R (row-major) | t per upcoming hypothesis
   __shared__ int s_lo_u, s_hi_u, s_lo_v, s_hi_v, s_clip;
   __shared__ double s_red[kWarps][kMaxNoise];
   __shared__ int s_redi[kWarps][kMaxNoise + 1];
   __shared__ double s_coef[kMaxNoise];
   __shared__ int s_count;
+  __shared__ int s_ndef;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  double* const sv_u_s = reinterpret_cast<double*>(smem_raw);
-  const bool v_in_smem = p.nv <= p.vcap;
-  double* const vu = v_in_smem ? sv_u_s : p.vscratch + (size_t)blockIdx.x * 3 * p.nv;
-  const int vstride = v_in_smem ? p.vcap : p.nv;
-  double* const vv = vu + vstride;
-  double* const viz = vv + vstride;
-  Key* const zb_s = reinterpret_cast<Key*>(sv_u_s + 3 * (size_t)p.vcap);
+  // dynamic shared memory: [(u,v) | 1/z | packed bbox] x vcap vertices,
+  // per-warp triangle records, deferred-triangle list, region z-buffer
+  double* const sv_s = reinterpret_cast<double*>(smem_raw);
+  VertexCache vs;
+  if (kVS) {
+    vs.uv = reinterpret_cast<double2*>(sv_s);
+    vs.iz = sv_s + 2 * (size_t)p.vcap;
+    vs.bb = reinterpret_cast<short4*>(sv_s + 3 * (size_t)p.vcap);
+  } else {
+    double* const g = p.vscratch + (size_t)blockIdx.x * 4 * p.nv;
+    vs.uv = reinterpret_cast<double2*>(g);
+    vs.iz = g + 2 * (size_t)p.nv;
+    vs.bb = reinterpret_cast<short4*>(g + 3 * (size_t)p.nv);
+  }
+  const int vcap = kVS ? p.vcap : 0;
+  WarpRec* const wrec = reinterpret_cast<WarpRec*>(sv_s + 4 * (size_t)vcap);
+  uint32_t* const def_list = reinterpret_cast<uint32_t*>(wrec + kWarps);
+  Key* const zb_s = reinterpret_cast<Key*>(def_list + ((p.nt + 3) & ~3));
 
-  for (long long h = blockIdx.x; h < p.n_hyp; h += gridDim.x) {
-    // ---- A: pose
+  int kk = 0;  // hypotheses this CTA has processed
+  for (long long h = blockIdx.x; h < p.n_hyp; h += gridDim.x, ++kk) {
+    // ---- A: poses of this CTA's next 32 hypotheses, one per lane of warp 0
+    // (compose with inverse(camera) -> rotation matrix + translation)
+    if ((kk & 31) == 0 && warp == 0) {
+      const long long hh = h + (long long)lane * gridDim.x;
+      if (hh < p.n_hyp) {
+        KPose hp;
+        if (p.poses)
+          hp = p.poses[hh];
+        else
+          grid_pose(p.grid, hh, hp);
+        pose_to_rt(p.w2c, hp, s_pose[lane], s_pose[lane] + 9);
+      }
+    }
     if (tid == 0) {
-      KPose hp;
-      if (p.poses)
-        hp = p.poses[h];
-      else
-        grid_pose(p.grid, h, hp);
-      pose_to_rt(p.w2c, hp, s_R, s_t);
       s_lo_u = INT_MAX;
       s_lo_v = INT_MAX;
       s_hi_u = INT_MIN;
@@ -270,35 +721,29 @@ __global__ void __launch_bounds__(kThreads) render_score_kernel(const KParams p)
       s_count = 0;
     }
     __syncthreads();
-    double R[9], t[3];
-#pragma unroll
-    for (int i = 0; i < 9; ++i) R[i] = s_R[i];
-    t[0] = s_t[0];
-    t[1] = s_t[1];
-    t[2] = s_t[2];
+    HypCtx hc;
+    hc.R = s_pose[kk & 31];  // broadcast reads from shared memory
+    hc.t = hc.R + 9;
+    const double* const R = hc.R;
+    const double* const t = hc.t;
 
-    // ---- B: vertices -> (u, v, 1/z), region bounds
+    // ---- B: vertices -> (u, v, 1/z), packed bbox, region bounds
     int lo_u = INT_MAX, lo_v = INT_MAX, hi_u = INT_MIN, hi_v = INT_MIN, clip = 0;
     for (int i = tid; i < p.nv; i += kThreads) {
       double c[3];
       cam_vertex(R, t, p.verts + 3 * (size_t)i, c);
       if (c[2] >= p.near_m) {
         const SV s = project(p, c[0], c[1], c[2]);
-        vu[i] = s.u;
-        vv[i] = s.v;
-        viz[i] = s.iz;
-        // clamp before converting: the region only has to contain every
-        // triangle bbox (which raster_tri recomputes exactly)
-        const double cu = fmin(fmax(ceil(s.u), -1.0), (double)p.W);
-        const double fu = fmin(fmax(floor(s.u), -1.0), (double)p.W);
-        const double cv = fmin(fmax(ceil(s.v), -1.0), (double)p.H);
-        const double fv = fmin(fmax(floor(s.v), -1.0), (double)p.H);
-        lo_u = min(lo_u, (int)cu);
-        hi_u = max(hi_u, (int)fu);
-        lo_v = min(lo_v, (int)cv);
-        hi_v = max(hi_v, (int)fv);
+        vs.uv[i] = make_double2(s.u, s.v);
+        vs.iz[i] = s.iz;
+        const short4 bb = vertex_bbox(p, s.u, s.v);
+        vs.bb[i] = bb;
+        lo_u = min(lo_u, (int)bb.x);
+        hi_u = max(hi_u, bb.y == kOvf ? p.W - 1 : (int)bb.y);
+        lo_v = min(lo_v, (int)bb.z);
+        hi_v = max(hi_v, bb.w == kOvf ? p.H - 1 : (int)bb.w);
       } else {
-        vu[i] = __longlong_as_double(0x7ff8000000000000ll);  // NaN marks "clip"
+        vs.bb[i] = make_short4(kClipV, 0, 0, 0);
         clip = 1;
       }
     }
@@ -318,8 +763,9 @@ __global__ void __launch_bounds__(kThreads) render_score_kernel(const KParams p)
       if (clip) s_clip = 1;
     }
     __syncthreads();
-    Region rg;
-    if (s_clip) {
+    Region& rg = hc.rg;
+    hc.clip = s_clip != 0;
+    if (hc.clip) {
       rg.u0 = 0;
       rg.v0 = 0;
       rg.u1 = p.W - 1;
@@ -330,176 +776,24 @@ __global__ void __launch_bounds__(kThreads) render_score_kernel(const KParams p)
       rg.u1 = min(s_hi_u, p.W - 1);
       rg.v1 = min(s_hi_v, p.H - 1);
     }
-    const bool empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
-    if (empty_region) {  // keep one valid (unused) pixel so indexing stays sane
+    hc.empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
+    if (hc.empty_region) {  // keep one valid (unused) pixel so indexing stays sane
       rg.u1 = rg.u0 = min(max(rg.u0, 0), p.W - 1);
       rg.v1 = rg.v0 = min(max(rg.v0, 0), p.H - 1);
     }
-    rg.rw = rg.u1 - rg.u0 + 1;
-    const int rpx = rg.rw * (rg.v1 - rg.v0 + 1);
-    Key* const zb = rpx <= p.zcap ? zb_s
-                                  : reinterpret_cast<Key*>(p.zscratch +
-                                                           (size_t)blockIdx.x * p.W * p.H);
-    const Key bg = kIds ? (Key)(((unsigned long long)__float_as_uint(p.far_f) << 32) |
-                                0xffffffffull)
-                        : (Key)__float_as_uint(p.far_f);
-    for (int i = tid; i < rpx; i += kThreads) zb[i] = bg;
-    __syncthreads();
-
-    // ---- C: raster, thread per triangle in mesh order
-    if (!empty_region || s_clip) {
-      for (int ti = tid; ti < p.nt; ti += kThreads) {
-        const uint32_t i0 = __ldg(p.tris + 3 * ti), i1 = __ldg(p.tris + 3 * ti + 1),
-                       i2 = __ldg(p.tris + 3 * ti + 2);
-        const double au = vu[i0], bu = vu[i1], cu = vu[i2];
-        const uint32_t draw = p.draw_base + (uint32_t)ti;
-        if (isnan(au) || isnan(bu) || isnan(cu)) {
-          raster_clipped<kIds>(p, zb, rg, R, t, i0, i1, i2, draw);
-        } else {
-          raster_tri<kIds>(p, zb, rg, SV{au, vv[i0], viz[i0]}, SV{bu, vv[i1], viz[i1]},
-                           SV{cu, vv[i2], viz[i2]}, draw);
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- render-many output
-    if (kOut) {
-      const size_t npx = (size_t)p.W * p.H;
-      float* od = p.out_depth + (size_t)h * npx;
-      int32_t* oi = p.out_ids ? p.out_ids + (size_t)h * npx : nullptr;
-      for (int i = tid; i < (int)npx; i += kThreads) {
-        const int u = i % p.W, v = i / p.W;
-        Key k = bg;
-        if (!empty_region && u >= rg.u0 && u <= rg.u1 && v >= rg.v0 && v <= rg.v1)
-          k = zb[(v - rg.v0) * rg.rw + (u - rg.u0)];
-        if (kIds) {
-          od[i] = __uint_as_float((unsigned int)((unsigned long long)k >> 32));
-          if (oi) {
-            const unsigned int d = (unsigned int)((unsigned long long)k & 0xffffffffull);
-            oi[i] = d == 0xffffffffu ? -1 : (int32_t)d;
-          }
-        } else {
-          od[i] = __uint_as_float((unsigned int)k);
-        }
-      }
-    }
-
-    if (kScore) {
-      // ---- D1: |y| = number of valid rendered pixels (likelihood.cpp:144-158)
-      int cnt = 0;
-      if (!empty_region)
-        for (int i = tid; i < rpx; i += kThreads) {
-          const float z = __uint_as_float(
-              kIds ? (unsigned int)((unsigned long long)zb[i] >> 32) : (unsigned int)zb[i]);
-          cnt += z < p.far_f;
-        }
-      cnt = warp_sum_i(cnt);
-      if (lane == 0 && cnt) atomicAdd(&s_count, cnt);
-      __syncthreads();
-      const int rend_count = s_count;
-      if (rend_count == 0) {
-        // the reference throws (likelihood.cpp:159-160); batched callers get
-        // -inf and a status flag instead
-        if (tid == 0) {
-          for (int e = 0; e < p.lik.n_noise; ++e)
-            p.scores[h * p.lik.n_noise + e] = -__longlong_as_double(0x7ff0000000000000ll);
-          if (p.status) p.status[h] = 1;
-        }
-        __syncthreads();
-        continue;
-      }
-      if (tid < p.lik.n_noise)  // likelihood.cpp:167 coefficient order
-        s_coef[tid] = p.lik.one_minus_p[tid] / (double)rend_count * p.lik.norm3[tid];
-      __syncthreads();
-      float coef_f[kMaxNoise], floor_f[kMaxNoise];
-#pragma unroll
-      for (int e = 0; e < kMaxNoise; ++e) {
-        coef_f[e] = e < p.lik.n_noise ? (float)s_coef[e] : 0.f;
-        floor_f[e] = e < p.lik.n_noise ? (float)p.lik.floor_term[e] : 0.f;
-      }
-
-      // ---- D2: window sums over the dilated region.  Observed pixels whose
-      // window holds no valid rendered pixel contribute exactly log(floor)
-      // (likelihood.cpp:209-216 with an empty dist2 list); they are counted.
-      const int w = p.lik.window;
-      const int du0 = max(rg.u0 - w, 0), du1 = min(rg.u1 + w, p.W - 1);
-      const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
-      const int dw = du1 - du0 + 1;
-      const int dpx = dw * (dv1 - dv0 + 1);
-      double acc[kMaxNoise];
-      int npos[kMaxNoise];
-#pragma unroll
-      for (int e = 0; e < kMaxNoise; ++e) {
-        acc[e] = 0.0;
-        npos[e] = 0;
-      }
-      for (int i = tid; i < dpx; i += kThreads) {
-        const int u = du0 + i % dw, v = dv0 + i / dw;
-        const float4 o = __ldg(p.obs + (size_t)v * p.W + u);
-        if (o.w == 0.f) continue;
-        float S[kMaxNoise];
-#pragma unroll
-        for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
-        const int rv0 = max(v - w, rg.v0), rv1 = min(v + w, rg.v1);
-        const int ru0 = max(u - w, rg.u0), ru1 = min(u + w, rg.u1);
-        for (int rv = rv0; rv <= rv1; ++rv) {
-          const Key* row = zb + (rv - rg.v0) * rg.rw - rg.u0;
-          const float fyr = ((float)rv - p.fcy) * p.inv_fy;
-          for (int ru = ru0; ru <= ru1; ++ru) {
-            const Key k = row[ru];
-            const float z = __uint_as_float(
-                kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
-            if (!(z < p.far_f)) continue;
-            const float dx = o.x - ((float)ru - p.fcx) * p.inv_fx * z;
-            const float dy = o.y - fyr * z;
-            const float dz = o.z - z;
-            const float d2 = dx * dx + (dy * dy + dz * dz);
-#pragma unroll
-            for (int s = 0; s < kMaxNoise; ++s)
-              if (s < p.lik.n_slots) S[s] += __expf(-d2 * p.lik.slot_scale[s]);
-          }
-        }
-#pragma unroll
-        for (int e = 0; e < kMaxNoise; ++e) {
-          if (e < p.lik.n_noise) {
-            const float Se = S[p.lik.slot_of[e]];
-            if (Se > 0.f) {
-              acc[e] += (double)__logf(floor_f[e] + coef_f[e] * Se);
-              npos[e] += 1;
-            }
-          }
-        }
-      }
-      // ---- D3: fp64 block reduction -> one score per noise entry
-#pragma unroll
-      for (int e = 0; e < kMaxNoise; ++e) {
-        acc[e] = warp_sum(acc[e]);
-        npos[e] = warp_sum_i(npos[e]);
-      }
-      if (lane == 0) {
-#pragma unroll
-        for (int e = 0; e < kMaxNoise; ++e) {
-          s_red[warp][e] = acc[e];
-          s_redi[warp][e] = npos[e];
-        }
-      }
-      __syncthreads();
-      if (tid < p.lik.n_noise) {
-        const int e = tid;
-        double a = 0.0;
-        int np = 0;
-        for (int k = 0; k < kWarps; ++k) {
-          a += s_red[k][e];
-          np += s_redi[k][e];
-        }
-        const int m_zero = *p.obs_count - np;
-        double total = p.lik.prefactor[e] + a;
-        if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
-        p.scores[h * p.lik.n_noise + e] = total;
-      }
-      if (tid == 0 && p.status) p.status[h] = 0;
-    }
+    const int pad = kScore ? 2 * p.lik.window : 0;
+    rg.ox = rg.u0 - pad;
+    rg.oy = rg.v0 - pad;
+    rg.rw = rg.u1 - rg.u0 + 1 + 2 * pad;
+    rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
+    hc.rpx = rg.rw * rg.rh;
+    if (hc.rpx <= p.zcap)
+      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wrec, def_list, &s_ndef, &s_count, s_coef,
+                                   s_red, s_redi, h);
+    else
+      hyp_body<kIds, kScore, kOut>(
+          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wrec,
+          def_list, &s_ndef, &s_count, s_coef, s_red, s_redi, h);
     __syncthreads();
   }
 }
@@ -530,10 +824,16 @@ __global__ void obs_prepare_kernel(const float* depth, int W, int H, float far_f
   if (threadIdx.x == 0 && s_cnt) atomicAdd(count, s_cnt);
 }
 
-// Host-side launch helpers (declared in b3d_host.cpp).
+// Host-side launch helpers (declared in b3d_capi.cpp).
+template <bool kIds, bool kScore, bool kOut>
+static auto pick_kernel(bool vs) {
+  return vs ? render_score_kernel<kIds, kScore, kOut, true>
+            : render_score_kernel<kIds, kScore, kOut, false>;
+}
+
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = render_score_kernel<kIds, kScore, kOut>;
+  auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -542,23 +842,35 @@ cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStr
 }
 
 template <bool kIds, bool kScore, bool kOut>
-cudaError_t occupancy_render_score(int* blocks, size_t smem) {
-  auto kern = render_score_kernel<kIds, kScore, kOut>;
+cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs) {
+  auto kern = pick_kernel<kIds, kScore, kOut>(vs);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
   return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, kThreads, smem);
 }
 
-template cudaError_t launch_render_score<false, true, false>(const KParams&, int, size_t,
-                                                             cudaStream_t);
-template cudaError_t launch_render_score<true, false, true>(const KParams&, int, size_t,
-                                                            cudaStream_t);
-template cudaError_t launch_render_score<false, false, true>(const KParams&, int, size_t,
-                                                             cudaStream_t);
-template cudaError_t occupancy_render_score<false, true, false>(int*, size_t);
-template cudaError_t occupancy_render_score<true, false, true>(int*, size_t);
-template cudaError_t occupancy_render_score<false, false, true>(int*, size_t);
+template <bool kIds, bool kScore, bool kOut>
+size_t static_smem_render_score() {
+  size_t mx = 0;
+  for (int vs = 0; vs < 2; ++vs) {
+    cudaFuncAttributes a{};
+    if (cudaFuncGetAttributes(&a, pick_kernel<kIds, kScore, kOut>(vs)) != cudaSuccess)
+      return 8192;
+    if (a.sharedSizeBytes > mx) mx = a.sharedSizeBytes;
+  }
+  return mx;
+}
+
+#define B3D_INST(I, S, O)                                                                 \
+  template cudaError_t launch_render_score<I, S, O>(const KParams&, int, size_t,         \
+                                                    cudaStream_t);                       \
+  template cudaError_t occupancy_render_score<I, S, O>(int*, size_t, bool);              \
+  template size_t static_smem_render_score<I, S, O>();
+B3D_INST(false, true, false)
+B3D_INST(true, false, true)
+B3D_INST(false, false, true)
+#undef B3D_INST
 
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out, int* count,
@@ -574,5 +886,9 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
 }
 
 int render_score_threads() { return kThreads; }
+
+size_t render_score_staging_bytes(int nt) {
+  return sizeof(WarpRec) * kWarps + 4 * (size_t)((nt + 3) & ~3);
+}
 
 }  // namespace b3d200
