@@ -857,44 +857,33 @@ int orc_windowed_loglik_multi(const float* obs, const float* rend, const orc_int
   return rc;
 }
 
-/* likelihood.cpp:82-104 (clouds from depth_to_cloud, geometry.cpp:54-70) */
-int orc_full_loglik(const float* obs, const float* rend, const orc_intrinsics* k,
-                    const orc_noise* np, double volume, double sigma_max, int prefactor,
-                    double* out) {
-  if (!noise_ok(np, sigma_max) || !(volume > 0)) return 1;
-  const int w = (int)k->width, h = (int)k->height;
+/* geometry.cpp:54-70 */
+void orc_depth_to_cloud(const float* depth, const orc_intrinsics* k, double* out, size_t* n) {
   const float sentinel = (float)k->far_m;
-  const size_t npx = (size_t)w * h;
-  double* op = (double*)malloc(npx * 3 * sizeof(double));
-  double* rp = (double*)malloc(npx * 3 * sizeof(double));
-  size_t no = 0, nr = 0;
-  for (int v = 0; v < h; ++v)
-    for (int u = 0; u < w; ++u) {
-      const float zo = obs[(size_t)v * w + u], zr = rend[(size_t)v * w + u];
-      if (zo < sentinel) {
-        const double zd = zo;
-        op[3 * no] = (u - k->cx) * zd / k->fx;
-        op[3 * no + 1] = (v - k->cy) * zd / k->fy;
-        op[3 * no + 2] = zd;
-        ++no;
-      }
-      if (zr < sentinel) {
-        const double zd = zr;
-        rp[3 * nr] = (u - k->cx) * zd / k->fx;
-        rp[3 * nr + 1] = (v - k->cy) * zd / k->fy;
-        rp[3 * nr + 2] = zd;
-        ++nr;
-      }
+  size_t m = 0;
+  for (uint32_t v = 0; v < k->height; ++v)
+    for (uint32_t u = 0; u < k->width; ++u) {
+      const float z = depth[(size_t)v * k->width + u];
+      if (z >= sentinel) continue;
+      const double zd = z;
+      out[3 * m + 0] = (u - k->cx) * zd / k->fx;
+      out[3 * m + 1] = (v - k->cy) * zd / k->fy;
+      out[3 * m + 2] = zd;
+      ++m;
     }
-  if (nr == 0) {
-    free(op); free(rp);
-    return 1;
-  }
+  *n = m;
+}
+
+/* likelihood.cpp:82-104 */
+int orc_full_loglik_points(const double* op, size_t no, const double* rp, size_t nr,
+                           const orc_noise* np, double volume, double sigma_max, int prefactor,
+                           double* out) {
+  if (!noise_ok(np, sigma_max) || nr == 0 || !(volume > 0)) return 1;
   const double sigma2 = np->sigma_noise * np->sigma_noise;
   const double inv_two_sigma2 = 1.0 / (2.0 * sigma2);
   const double norm3 = pow(kTwoPi * sigma2, -1.5);
   const double coef = (1.0 - np->p_outlier) / nr * norm3;
-  const double floor_term = np->p_outlier / volume;
+  const double outlier_floor = np->p_outlier / volume;
   double total = log_prefactor(np, sigma_max, prefactor);
   for (size_t i = 0; i < no; ++i) {
     double s = 0.0;
@@ -903,11 +892,26 @@ int orc_full_loglik(const float* obs, const float* rend, const orc_intrinsics* k
                    dz = op[3 * i + 2] - rp[3 * j + 2];
       s += exp(-(dx * dx + (dy * dy + dz * dz)) * inv_two_sigma2);
     }
-    total += log(floor_term + coef * s);
+    total += log(outlier_floor + coef * s);
   }
-  free(op); free(rp);
   *out = total;
   return 0;
+}
+
+/* likelihood.cpp:82-104 over depth_to_cloud of both images */
+int orc_full_loglik(const float* obs, const float* rend, const orc_intrinsics* k,
+                    const orc_noise* np, double volume, double sigma_max, int prefactor,
+                    double* out) {
+  const size_t npx = (size_t)k->width * k->height;
+  double* op = (double*)malloc(npx * 3 * sizeof(double));
+  double* rp = (double*)malloc(npx * 3 * sizeof(double));
+  size_t no = 0, nr = 0;
+  orc_depth_to_cloud(obs, k, op, &no);
+  orc_depth_to_cloud(rend, k, rp, &nr);
+  const int rc = orc_full_loglik_points(op, no, rp, nr, np, volume, sigma_max, prefactor, out);
+  free(op);
+  free(rp);
+  return rc;
 }
 
 /* ------------------------------------------------------- batched scoring */

@@ -134,6 +134,14 @@ int orc_windowed_loglik_multi(const float* observed, const float* rendered,
                               size_t n_noise, double volume, double sigma_max,
                               int window, int prefactor, double* out,
                               orc_counters* counters);
+/* depth_to_cloud (geometry.cpp:54-70): non-sentinel pixels row-major,
+ * ((u-cx)z/fx, (v-cy)z/fy, z).  out: capacity W*H*3 doubles. */
+void orc_depth_to_cloud(const float* depth, const orc_intrinsics* k, double* out, size_t* n);
+/* full_log_likelihood over explicit point clouds (likelihood.cpp:82-104).
+ * Returns 1 for an empty rendered cloud / invalid noise. */
+int orc_full_loglik_points(const double* obs, size_t n_obs, const double* rend,
+                           size_t n_rend, const orc_noise* noise, double volume,
+                           double sigma_max, int prefactor, double* out);
 /* full_log_likelihood over the two depth images' clouds (likelihood.cpp:82-104). */
 int orc_full_loglik(const float* observed, const float* rendered,
                     const orc_intrinsics* k, const orc_noise* noise, double volume,

@@ -66,6 +66,9 @@ def lib():
         L.orc_rng_uniform_int.restype = C.c_uint64
         L.orc_rng_uniform_int.argtypes = [vp, C.c_uint64]
         L.orc_rng_seed.argtypes = [C.c_uint64, vp]
+        L.orc_rng_normal.argtypes = [vp]
+        L.orc_rng_uniform.argtypes = [vp]
+        L.orc_rng_next_u64.argtypes = [vp]
         L.orc_rng_split.argtypes = [vp, C.c_uint64, C.c_uint64, C.c_uint64, vp]
         L.orc_visible_volume.restype = d
         L.orc_logsumexp.restype = d
@@ -83,6 +86,9 @@ def lib():
         L.orc_windowed_loglik_multi.argtypes = [vp, vp, vp, vp, C.c_size_t, d, d, C.c_int,
                                                 C.c_int, vp, vp]
         L.orc_full_loglik.argtypes = [vp, vp, vp, vp, d, d, C.c_int, vp]
+        L.orc_full_loglik_points.argtypes = [vp, C.c_size_t, vp, C.c_size_t, vp, d, d, C.c_int,
+                                             vp]
+        L.orc_depth_to_cloud.argtypes = [vp, vp, vp, vp]
         L.orc_raster_mesh.argtypes = [vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
                                       C.c_uint32, vp]
         L.orc_render_instances.argtypes = [vp, vp, vp, C.c_size_t, vp, vp, vp]
@@ -133,6 +139,14 @@ def rng_uniform(st):
     return lib().orc_rng_uniform(_p(st))
 
 
+def rng_uniform_int(st, n):
+    return int(lib().orc_rng_uniform_int(_p(st), n))
+
+
+def rng_normal(st):
+    return lib().orc_rng_normal(_p(st))
+
+
 def voxel_to_mesh(voxels, resolution, origin):
     v = np.ascontiguousarray(voxels, dtype=np.int32)
     n = v.shape[0]
@@ -149,8 +163,9 @@ def voxel_to_mesh(voxels, resolution, origin):
 def box_mesh(lo, hi):
     v = np.zeros((8, 3), dtype=np.float64)
     t = np.zeros((12, 3), dtype=np.uint32)
-    lib().orc_box_mesh(_p(np.asarray(lo, dtype=np.float64)), _p(np.asarray(hi, dtype=np.float64)),
-                       _p(v), _p(t))
+    lo_a = np.ascontiguousarray(lo, dtype=np.float64)  # keep alive across the call
+    hi_a = np.ascontiguousarray(hi, dtype=np.float64)
+    lib().orc_box_mesh(_p(lo_a), _p(hi_a), _p(v), _p(t))
     return v, t
 
 
@@ -177,7 +192,8 @@ def rotation_matrix(a):
 
 def from_axis_angle(axis, angle, t=(0, 0, 0)):
     out = Pose()
-    lib().orc_from_axis_angle(_p(np.asarray(axis, dtype=np.float64)), angle, C.byref(out))
+    ax = np.ascontiguousarray(axis, dtype=np.float64)
+    lib().orc_from_axis_angle(_p(ax), angle, C.byref(out))
     p = np.array([getattr(out, n) for n, _ in Pose._fields_])
     p[4:] = t
     return p
@@ -191,10 +207,10 @@ def camera_pose_from_spherical(d, az, alt):
 
 def contact_to_pose(table_w, table_h, aabb_min, aabb_max, face, dx, dy, dtheta):
     out = Pose()
-    rc = lib().orc_contact_to_pose(table_w, table_h,
-                                   _p(np.asarray(aabb_min, dtype=np.float64)),
-                                   _p(np.asarray(aabb_max, dtype=np.float64)), face, dx, dy,
-                                   dtheta, C.byref(out))
+    lo_a = np.ascontiguousarray(aabb_min, dtype=np.float64)
+    hi_a = np.ascontiguousarray(aabb_max, dtype=np.float64)
+    rc = lib().orc_contact_to_pose(table_w, table_h, _p(lo_a), _p(hi_a), face, dx, dy, dtheta,
+                                   C.byref(out))
     if rc:
         raise ValueError("contact params out of valid range")
     return np.array([getattr(out, n) for n, _ in Pose._fields_])
@@ -203,8 +219,9 @@ def contact_to_pose(table_w, table_h, aabb_min, aabb_max, face, dx, dy, dtheta):
 def rotated_bounds(aabb_min, aabb_max, face):
     lo = np.zeros(3)
     hi = np.zeros(3)
-    lib().orc_rotated_bounds(_p(np.asarray(aabb_min, dtype=np.float64)),
-                             _p(np.asarray(aabb_max, dtype=np.float64)), face, _p(lo), _p(hi))
+    lo_a = np.ascontiguousarray(aabb_min, dtype=np.float64)
+    hi_a = np.ascontiguousarray(aabb_max, dtype=np.float64)
+    lib().orc_rotated_bounds(_p(lo_a), _p(hi_a), face, _p(lo), _p(hi))
     return lo, hi
 
 
@@ -259,6 +276,27 @@ def full_loglik(obs, rend, k, noise, sigma_max, prefactor=0, volume=None):
     if rc:
         raise ValueError("full likelihood: invalid argument or empty rendered cloud")
     return out.value
+
+
+def full_loglik_points(obs_pts, rend_pts, noise, volume, sigma_max, prefactor=0):
+    o = np.ascontiguousarray(obs_pts, dtype=np.float64).reshape(-1, 3)
+    r = np.ascontiguousarray(rend_pts, dtype=np.float64).reshape(-1, 3)
+    np_ = Noise(*noise)
+    out = C.c_double()
+    rc = lib().orc_full_loglik_points(_p(o), o.shape[0], _p(r), r.shape[0], C.byref(np_),
+                                      volume, sigma_max, prefactor, C.byref(out))
+    if rc:
+        raise ValueError("full_log_likelihood: empty rendered cloud or invalid noise")
+    return out.value
+
+
+def depth_to_cloud(depth, k):
+    ki = intr(k)
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    out = np.zeros((d.size, 3), dtype=np.float64)
+    n = C.c_size_t()
+    lib().orc_depth_to_cloud(_p(d), C.byref(ki), _p(out), C.byref(n))
+    return out[: n.value].copy()
 
 
 def visible_volume(k):

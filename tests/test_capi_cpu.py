@@ -1,0 +1,54 @@
+"""C ABI checks that need no GPU: the library loads, exports exactly what
+include/b3d_b200.h declares, host-side entry points work, and GPU entry points
+fail cleanly (status + thread-local message, no crash) without a device."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_2312_08715_b200 import b3d
+
+
+def test_library_exports_every_declared_symbol():
+    L = b3d.lib()
+    declared = b3d.exported_symbols()
+    assert len(declared) >= 20
+    for name in declared:
+        assert hasattr(L, name), name
+
+
+def test_version_and_depth_image_roundtrip():
+    L = b3d.lib()
+    assert L.b3d_version().decode().startswith("0.1")
+    img = np.arange(12, dtype=np.float32).reshape(3, 4)
+    h = C.c_void_p()
+    assert L.b3d_depth_image_create(4, 3, img.ctypes.data, C.byref(h)) == 0
+    assert L.b3d_depth_image_width(h) == 4 and L.b3d_depth_image_height(h) == 3
+    data = np.ctypeslib.as_array(C.cast(L.b3d_depth_image_data(h), C.POINTER(C.c_float)), (12,))
+    assert np.array_equal(data, img.ravel())
+    L.b3d_depth_image_destroy(h)
+    # bad arguments -> B3D_ERROR with the reference's message
+    assert L.b3d_depth_image_create(0, 3, img.ctypes.data, C.byref(h)) == 1
+    assert L.b3d_last_error().decode() == "bad arguments"
+
+
+def test_gpu_entry_points_fail_cleanly_without_device():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    L = b3d.lib()
+    h = C.c_void_p()
+    st = L.b3d_gpu_context_create(0, C.byref(h))
+    assert st != 0 and L.b3d_last_error()
+
+
+def test_voxel_to_mesh_errors():
+    L = b3d.lib()
+    nv, nt = C.c_uint64(), C.c_uint64()
+    o = np.zeros(3)
+    buf = np.zeros(24)
+    tb = np.zeros(36, dtype=np.uint32)
+    vox = np.zeros((0, 3), dtype=np.int32)
+    st = L.b3d_voxel_to_mesh(vox.ctypes.data, 0, 0.1, o.ctypes.data, buf.ctypes.data,
+                             tb.ctypes.data, C.byref(nv), C.byref(nt))
+    assert st == 1 and b"empty grid" in L.b3d_last_error()
