@@ -15,7 +15,7 @@ from typing import Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libb3d_b200.so")
+LIB_PATH = os.environ.get("B3D_LIB") or os.path.join(_HERE, "_lib", "libb3d_b200.so")
 
 B3D_OK = 0
 PREFACTOR_PRINTED = 0
