@@ -170,6 +170,35 @@ B3D_API b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scor
                                         uint64_t* rng_state, b3d_stage_result* out,
                                         double* probs);
 
+/* One stage of a device-resident enumeration schedule: a pose grid around
+ * the previous stage's chosen pose (the caller's centre for stage 0), its
+ * likelihood settings (sigma_max and prefactor come from the context), and
+ * how the next centre is chosen: B3D_SELECT_SAMPLE draws from the stage's
+ * categorical posterior (coarse_to_fine_propose, inference.cpp:357-396),
+ * B3D_SELECT_ARGMAX keeps the MAP pose (track_camera, tracking.cpp:132-138). */
+enum { B3D_SELECT_SAMPLE = 0, B3D_SELECT_ARGMAX = 1 };
+typedef struct b3d_stage_spec {
+  double extent[3];
+  uint32_t count[3];
+  const double* rotations; /* n_rot x 4 (w,x,y,z), host or device */
+  uint32_t n_rot;
+  uint32_t mode;
+  b3d_noise noise;
+  int32_t window;
+  uint32_t select;
+} b3d_stage_spec;
+
+/* Runs n_stages enumerate -> score -> reduce -> select stages back to back
+ * on the context's stream with no host round trip between stages.
+ * rng_state (5 x u64, advanced by one uniform() per SAMPLE stage), results
+ * (n_stages) and centers (n_stages + 1; centers[0] = *center) are caller
+ * buffers, host or device. */
+B3D_API b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id,
+                                          const b3d_pose* center,
+                                          const b3d_stage_spec* stages, uint32_t n_stages,
+                                          uint64_t* rng_state, b3d_stage_result* results,
+                                          b3d_pose* centers);
+
 /* Reference Rng seeding (rng.cpp:20-28), for building rng_state. */
 B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
 B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,

@@ -56,6 +56,16 @@ class PoseGrid(C.Structure):
                 ("rotations", C.c_void_p), ("n_rot", C.c_uint32), ("mode", C.c_uint32)]
 
 
+class StageSpec(C.Structure):
+    _fields_ = [("extent", C.c_double * 3), ("count", C.c_uint32 * 3), ("rotations", C.c_void_p),
+                ("n_rot", C.c_uint32), ("mode", C.c_uint32), ("noise", Noise),
+                ("window", C.c_int32), ("select", C.c_uint32)]
+
+
+SELECT_SAMPLE = 0
+SELECT_ARGMAX = 1
+
+
 class StageResult(C.Structure):
     _fields_ = [("argmax", C.c_uint64), ("sample", C.c_uint64), ("max_score", C.c_double),
                 ("logsumexp", C.c_double), ("total", C.c_double), ("sample_logp", C.c_double),
@@ -97,6 +107,7 @@ def lib() -> C.CDLL:
         "b3d_gpu_score_grid": ([vp, i32, C.POINTER(PoseGrid), vp, vp], st),
         "b3d_gpu_render_poses": ([vp, i32, vp, u64, vp, vp], st),
         "b3d_gpu_stage_reduce": ([vp, vp, u64, u32, u32, vp, vp, vp], st),
+        "b3d_gpu_coarse_to_fine": ([vp, i32, C.POINTER(Pose), vp, u32, vp, vp, vp], st),
         "b3d_rng_seed": ([u64, vp], None),
         "b3d_rng_split": ([vp, u64, u64, u64, vp], None),
         "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
@@ -315,3 +326,32 @@ class GpuContext:
         return StageOut(res.argmax, res.sample, res.max_score, res.logsumexp, res.total,
                         res.sample_logp, bool(res.all_zero), res.n_nonfinite,
                         bool(res.sample_fallback))
+
+    def coarse_to_fine(self, mesh: int, center, stages: Sequence[dict], rng_state=None):
+        """b3d_gpu_coarse_to_fine.  stages: dicts with extent, count,
+        rotations (n,4), mode, noise (p, sigma), window, select.
+        Returns (list of StageOut, centers (n_stages+1, 7))."""
+        specs = (StageSpec * len(stages))()
+        keep = []
+        for i, g in enumerate(stages):
+            rot = np.ascontiguousarray(g["rotations"], dtype=np.float64)
+            keep.append(rot)
+            sp = specs[i]
+            for a in range(3):
+                sp.extent[a] = float(g["extent"][a])
+                sp.count[a] = int(g["count"][a])
+            sp.rotations = rot.ctypes.data
+            sp.n_rot = rot.shape[0]
+            sp.mode = int(g.get("mode", GRID_PRODUCT))
+            sp.noise = Noise(*g["noise"])
+            sp.window = int(g["window"])
+            sp.select = int(g.get("select", SELECT_SAMPLE))
+        res = (StageResult * len(stages))()
+        centers = np.zeros((len(stages) + 1, 7), dtype=np.float64)
+        c = _pose(center)
+        _check(self._L.b3d_gpu_coarse_to_fine(self.h, mesh, C.byref(c), specs, len(stages),
+                                              _ptr(rng_state), C.addressof(res),
+                                              centers.ctypes.data))
+        outs = [StageOut(r.argmax, r.sample, r.max_score, r.logsumexp, r.total, r.sample_logp,
+                         bool(r.all_zero), r.n_nonfinite, bool(r.sample_fallback)) for r in res]
+        return outs, centers

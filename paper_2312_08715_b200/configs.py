@@ -142,3 +142,103 @@ def cfg1(render_fn: RenderFn, mesh_fn, seed: int = 0, blob: str = "eden",
     rots = synth.vmf_quaternions(8 * 8 * 16, 1000.0, rng_rot)
     return Workload("cfg1_single_object_160x120", k, vox, verts, tris, gt, obs, gt.copy(),
                     (0.02, 0.02, 0.02), count, rots, 1, [(0.01, 0.005)], 1)
+
+
+def grid_poses(center, extent, count, rotations, mode) -> np.ndarray:
+    """Host poses of a device pose grid (same arithmetic as posemath.cuh)."""
+    return _grid_poses_host(np.asarray(center, dtype=np.float64), extent, count,
+                            np.asarray(rotations, dtype=np.float64), mode)
+
+
+def _geom(a, b, n):
+    return [a * (b / a) ** (i / (n - 1)) for i in range(n)]
+
+
+def cfg2(render_fn: RenderFn, mesh_fn, seed: int = 0, n_stages: int = 5,
+         counts=(16, 16, 16), n_rot: int = 8) -> Workload:
+    """configs[1]: coarse-to-fine schedule, one object, 200x200, fx=fy=250.
+
+    3,000-voxel blob; observation as cfg1 (N(0, 2 mm), 10% outliers).  Five
+    stages of a 16x16x16 translation grid times 8 vMF rotations (PRODUCT,
+    32,768 hypotheses); translation width 4 -> 2 -> 1 -> 0.5 -> 0.2 cm
+    (extent = width / 2), kappa 50 -> 2000 and sigma 20 -> 2 mm geometric,
+    window 7,7,5,5,3 (w = 3,3,2,2,1).  Each stage's centre is drawn from the
+    previous stage's categorical posterior (seeded).  Stage 0 is centred on
+    the ground truth displaced by 1.5 cm and ~10 degrees.
+    """
+    rng = np.random.Generator(np.random.PCG64(3000 + seed))
+    vox = synth.eden_blob(3000, seed)
+    verts, tris = make_mesh(vox, mesh_fn)
+    k = Intr(250.0, 250.0, 100.0, 100.0, 200, 200, 0.01, 10.0)
+    q = synth.uniform_quaternion(rng)
+    gt = np.array([q[0], q[1], q[2], q[3], 0.0, 0.0, 0.6])
+    depth = render_fn(k, verts, tris, gt)
+    obs = synth.noisy_observation(depth, k.far, 0.002, 0.10, 0.2, 1.5, rng, k.near)
+    d = rng.standard_normal(3)
+    start = gt.copy()
+    start[4:] += 0.015 * d / np.linalg.norm(d)
+    dq = synth.vmf_quaternions(1, 300.0, rng)[0]
+    start[:4] = _qmul(gt[:4], dq)
+    widths = [0.04, 0.02, 0.01, 0.005, 0.002]
+    kappas = _geom(50.0, 2000.0, 5)
+    sigmas = _geom(0.02, 0.002, 5)
+    windows = [3, 3, 2, 2, 1]
+    stages = []
+    for s in range(n_stages):
+        stages.append({"extent": (widths[s] / 2,) * 3, "count": counts,
+                       "rotations": synth.vmf_quaternions(n_rot, kappas[s], rng), "mode": 0,
+                       "noise": (0.01, sigmas[s]), "window": windows[s], "select": 0})
+    w = Workload("cfg2_coarse_to_fine_200x200", k, vox, verts, tris, gt, obs, start,
+                 stages[0]["extent"], counts, stages[0]["rotations"], 0, [stages[0]["noise"]],
+                 windows[0], stages=stages)
+    return w
+
+
+def _qmul(a, b):
+    aw, ax, ay, az = a
+    bw, bx, by, bz = b
+    q = np.array([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
+                  aw * by + ay * bw + az * bx - ax * bz, aw * bz + az * bw + ax * by - ay * bx])
+    return q / np.linalg.norm(q)
+
+
+def _axis_angle_q(axis, angle):
+    axis = np.asarray(axis, dtype=np.float64)
+    axis = axis / np.linalg.norm(axis)
+    return np.concatenate([[np.cos(angle / 2)], np.sin(angle / 2) * axis])
+
+
+def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
+    """configs[3]: real-time tracking, 2,000-voxel blob, 240x320 (H x W),
+    fx=fy=400 (cfg1's field of view), cx=160, cy=120.  Ground truth: seeded
+    random walk, 1 cm translation and 5 degrees rotation per frame from
+    (0, 0, 0.6); observations with N(0, 2 mm) noise and 5% outliers.  Per
+    frame two stages of 16x16x4 translations x 8 rotations (8,192 each)
+    centred on the previous estimate, MAP (argmax) selection; likelihood
+    r = 5 mm, 5x5 window, outlier_prob 0.05."""
+    rng = np.random.Generator(np.random.PCG64(4000 + seed))
+    vox = synth.eden_blob(2000, seed)
+    verts, tris = make_mesh(vox, mesh_fn)
+    k = Intr(400.0, 400.0, 160.0, 120.0, 320, 240, 0.01, 10.0)
+    q = synth.uniform_quaternion(rng)
+    pose = np.array([q[0], q[1], q[2], q[3], 0.0, 0.0, 0.6])
+    gts, frames = [], []
+    for f in range(n_frames):
+        if f:
+            d = rng.standard_normal(3)
+            pose = pose.copy()
+            pose[4:] += 0.01 * d / np.linalg.norm(d)
+            pose[:4] = _qmul(_axis_angle_q(rng.standard_normal(3), np.deg2rad(5.0)), pose[:4])
+        gts.append(pose)
+        depth = render_fn(k, verts, tris, pose)
+        frames.append(synth.noisy_observation(depth, k.far, 0.002, 0.05, 0.2, 1.5, rng, k.near))
+    stages = [
+        {"extent": (0.02, 0.02, 0.02), "count": (16, 16, 4),
+         "rotations": np.vstack([[1.0, 0, 0, 0], synth.vmf_quaternions(7, 150.0, rng)]),
+         "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
+        {"extent": (0.004, 0.004, 0.004), "count": (16, 16, 4),
+         "rotations": np.vstack([[1.0, 0, 0, 0], synth.vmf_quaternions(7, 3000.0, rng)]),
+         "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
+    ]
+    return {"k": k, "vertices": verts, "triangles": tris, "voxels": vox, "gt": np.array(gts),
+            "frames": frames, "stages": stages, "name": "cfg4_tracking_240x320"}

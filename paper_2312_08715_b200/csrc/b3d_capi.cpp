@@ -182,9 +182,12 @@ struct b3d_gpu_context {
   DevBuf obs_depth, obs_pts, obs_count;
   bool has_lik = false;
   KLik lik{};
+  double sigma_max = 0.1;
+  int prefactor = B3D_PREFACTOR_PRINTED;
   int cull = 0;  // B3D_OCCLUSION_CULL=1: exact two-pass back-face occlusion culling
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
+  DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
 };
 
 namespace {
@@ -268,7 +271,7 @@ struct LaunchPlan {
 };
 
 template <bool kIds, bool kScore, bool kOut>
-LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n) {
+LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int window = -1) {
   LaunchPlan lp;
   const size_t key = kIds ? 8 : 4;
   const size_t npx = (size_t)ctx->k.width * ctx->k.height;
@@ -308,7 +311,7 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n) {
   if (grid < 1) grid = 1;
   lp.grid = (int)grid;
   // overflow scratch for hypotheses whose region / mesh exceeds shared memory
-  const int pad = kScore ? 2 * ctx->lik.window : 0;
+  const int pad = kScore ? 2 * (window >= 0 ? window : ctx->lik.window) : 0;
   lp.zstride = (long long)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
   ctx->zscratch.ensure((size_t)lp.grid * lp.zstride * 8);
   if (lp.vcap < m.nv) ctx->vscratch.ensure((size_t)lp.grid * 32 * m.nv);
@@ -350,6 +353,49 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
 void finish_copy_out(b3d_gpu_context* ctx, void* dst, const void* src, size_t bytes) {
   cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream),
              "cudaMemcpyAsync D2H");
+}
+
+// windowed_log_likelihood_multi settings (likelihood.cpp:14-26,162-186):
+// per-noise coefficients and the distinct-sigma slots, validated like the
+// reference (validate_noise).
+KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
+              double sigma_max, int window, int prefactor) {
+  require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
+  require(n_noise <= (uint32_t)kMaxNoise, ErrorCode::invalid,
+          "gpu context: at most 4 noise settings per call");
+  require(window >= 0, ErrorCode::invalid, "window radius must be >= 0");
+  require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
+          ErrorCode::invalid, "unknown prefactor");
+  const double vol = visible_volume(k);
+  require(vol > 0, ErrorCode::invalid, "scene volume must be positive");
+  KLik L{};
+  L.n_noise = (int)n_noise;
+  L.window = window;
+  std::vector<double> slots;
+  for (uint32_t e = 0; e < n_noise; ++e) {
+    const b3d_noise& np = noise[e];
+    require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
+    require(np.sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
+    require(np.p_outlier >= 0 && np.p_outlier <= 1, ErrorCode::invalid,
+            "p_outlier must be in [0,1]");
+    require(np.p_outlier > 0, ErrorCode::invalid,
+            "gpu context: p_outlier must be > 0 on the fp32 likelihood path");
+    const double sigma2 = np.sigma_noise * np.sigma_noise;
+    L.one_minus_p[e] = 1.0 - np.p_outlier;
+    L.norm3[e] = std::pow(6.283185307179586476925287 * sigma2, -1.5);
+    L.floor_term[e] = np.p_outlier / vol;
+    L.log_floor[e] = std::log(L.floor_term[e]);
+    L.prefactor[e] = prefactor == B3D_PREFACTOR_PRINTED ? std::log(np.sigma_noise / sigma_max)
+                                                        : -std::log(sigma_max);
+    size_t s = 0;
+    while (s < slots.size() && slots[s] != np.sigma_noise) ++s;
+    if (s == slots.size()) slots.push_back(np.sigma_noise);
+    L.slot_of[e] = (int)s;
+  }
+  L.n_slots = (int)slots.size();
+  for (size_t s = 0; s < slots.size(); ++s)
+    L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
+  return L;
 }
 
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
@@ -625,42 +671,9 @@ b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
   return guarded([&] {
     check(ctx && noise, "bad arguments");
     require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
-    require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
-    require(n_noise <= (uint32_t)kMaxNoise, ErrorCode::invalid,
-            "gpu context: at most 4 noise settings per call");
-    require(window >= 0, ErrorCode::invalid, "window radius must be >= 0");
-    require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
-            ErrorCode::invalid, "unknown prefactor");
-    const double vol = visible_volume(ctx->k);
-    require(vol > 0, ErrorCode::invalid, "scene volume must be positive");
-    KLik L{};
-    L.n_noise = (int)n_noise;
-    L.window = window;
-    std::vector<double> slots;
-    for (uint32_t e = 0; e < n_noise; ++e) {
-      const b3d_noise& np = noise[e];
-      require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
-      require(np.sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
-      require(np.p_outlier >= 0 && np.p_outlier <= 1, ErrorCode::invalid,
-              "p_outlier must be in [0,1]");
-      require(np.p_outlier > 0, ErrorCode::invalid,
-              "gpu context: p_outlier must be > 0 on the fp32 likelihood path");
-      const double sigma2 = np.sigma_noise * np.sigma_noise;
-      L.one_minus_p[e] = 1.0 - np.p_outlier;
-      L.norm3[e] = std::pow(6.283185307179586476925287 * sigma2, -1.5);
-      L.floor_term[e] = np.p_outlier / vol;
-      L.log_floor[e] = std::log(L.floor_term[e]);
-      L.prefactor[e] = prefactor == B3D_PREFACTOR_PRINTED ? std::log(np.sigma_noise / sigma_max)
-                                                          : -std::log(sigma_max);
-      size_t s = 0;
-      while (s < slots.size() && slots[s] != np.sigma_noise) ++s;
-      if (s == slots.size()) slots.push_back(np.sigma_noise);
-      L.slot_of[e] = (int)s;
-    }
-    L.n_slots = (int)slots.size();
-    for (size_t s = 0; s < slots.size(); ++s)
-      L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
-    ctx->lik = L;
+    ctx->lik = make_lik(ctx->k, noise, n_noise, sigma_max, window, prefactor);
+    ctx->sigma_max = sigma_max;
+    ctx->prefactor = prefactor;
     ctx->has_lik = true;
   });
 }
@@ -794,6 +807,113 @@ b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scores, uint
       sync = true;
     }
     if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "stage_reduce");
+  });
+}
+
+b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* center,
+                                  const b3d_stage_spec* stages, uint32_t n_stages,
+                                  uint64_t* rng_state, b3d_stage_result* results,
+                                  b3d_pose* centers) {
+  return guarded([&] {
+    require_ready(ctx, true, true);
+    check(center && stages && n_stages > 0 && results, "bad arguments");
+    DeviceGuard dg(ctx->device);
+    const Mesh& m = get_mesh(ctx, mesh_id);
+    // stage sizes, rotation tables (staged once), scratch sized for the
+    // largest stage / window
+    std::vector<uint64_t> n(n_stages), rot_off(n_stages);
+    uint64_t n_max = 0, rot_total = 0;
+    int w_max = 0;
+    bool any_sample = false;
+    for (uint32_t s = 0; s < n_stages; ++s) {
+      const b3d_stage_spec& g = stages[s];
+      check(g.rotations && g.n_rot > 0, "stage: rotation table required");
+      const uint64_t nt = (uint64_t)g.count[0] * g.count[1] * g.count[2];
+      check(nt > 0, "pose grid: counts must be >= 1");
+      check(g.mode == B3D_GRID_PRODUCT || nt == g.n_rot,
+            "pose grid: zip mode needs nx*ny*nz == n_rot");
+      n[s] = g.mode == B3D_GRID_PRODUCT ? nt * g.n_rot : nt;
+      n_max = std::max(n_max, n[s]);
+      w_max = std::max(w_max, (int)g.window);
+      rot_off[s] = rot_total;
+      rot_total += g.n_rot;
+      any_sample = any_sample || g.select == B3D_SELECT_SAMPLE;
+    }
+    if (any_sample) check(rng_state != nullptr, "stage: SAMPLE selection needs rng_state");
+    ctx->c2f_scores.ensure(8 * n_max);
+    ctx->c2f_rot.ensure(32 * rot_total);
+    ctx->c2f_centers.ensure(sizeof(KPose) * (n_stages + 1));
+    ctx->c2f_results.ensure(sizeof(KStageResult) * n_stages);
+    for (uint32_t s = 0; s < n_stages; ++s)
+      cuda_check(cudaMemcpyAsync(ctx->c2f_rot.as<double>() + 4 * rot_off[s], stages[s].rotations,
+                                 32ull * stages[s].n_rot, cudaMemcpyDefault, ctx->stream),
+                 "cudaMemcpyAsync rotations");
+    KPose* d_centers = ctx->c2f_centers.as<KPose>();
+    const KPose c0 = pose_from_c(*center);
+    cuda_check(cudaMemcpyAsync(d_centers, &c0, sizeof(KPose), cudaMemcpyHostToDevice,
+                               ctx->stream),
+               "cudaMemcpyAsync centre");
+    unsigned long long* d_rng = nullptr;
+    const bool dev_rng = rng_state && is_device_ptr(rng_state);
+    if (rng_state) {
+      if (dev_rng) {
+        d_rng = reinterpret_cast<unsigned long long*>(rng_state);
+      } else {
+        cuda_check(cudaMemcpyAsync(ctx->rng.p, rng_state, 40, cudaMemcpyHostToDevice,
+                                   ctx->stream),
+                   "cudaMemcpyAsync rng");
+        d_rng = ctx->rng.as<unsigned long long>();
+      }
+    }
+    KStageResult* d_res = ctx->c2f_results.as<KStageResult>();
+    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n_max, w_max);
+    for (uint32_t s = 0; s < n_stages; ++s) {
+      const b3d_stage_spec& g = stages[s];
+      KParams p = base_params(ctx, m);
+      p.lik = make_lik(ctx->k, &g.noise, 1, ctx->sigma_max, g.window, ctx->prefactor);
+      p.poses = nullptr;
+      p.grid.center_dev = d_centers + s;
+      for (int a = 0; a < 3; ++a) {
+        p.grid.extent[a] = g.extent[a];
+        p.grid.count[a] = (int)g.count[a];
+      }
+      p.grid.rotations = ctx->c2f_rot.as<double>() + 4 * rot_off[s];
+      p.grid.n_rot = (int)g.n_rot;
+      p.grid.mode = (int)g.mode;
+      p.n_hyp = (long long)n[s];
+      p.scores = ctx->c2f_scores.as<double>();
+      p.status = nullptr;
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
+      const int grid = (int)std::min<long long>(lp.grid, (long long)n[s]);
+      cuda_check(launch_render_score<false, true, false>(p, grid, lp.smem, ctx->stream),
+                 "render_score launch");
+      const bool sample = g.select == B3D_SELECT_SAMPLE;
+      cuda_check(launch_stage_reduce(p.scores, (long long)n[s], 1, 0, sample ? d_rng : nullptr,
+                                     d_res + s, nullptr, ctx->stream),
+                 "stage_reduce launch");
+      cuda_check(launch_select_center(p.grid, d_res + s, sample ? 1 : 0, d_centers + s + 1,
+                                      ctx->stream),
+                 "select_center launch");
+    }
+    bool sync = !dev_rng && rng_state != nullptr;
+    cuda_check(cudaMemcpyAsync(results, d_res, sizeof(KStageResult) * n_stages, cudaMemcpyDefault,
+                               ctx->stream),
+               "cudaMemcpyAsync results");
+    if (!is_device_ptr(results)) sync = true;
+    if (centers) {
+      cuda_check(cudaMemcpyAsync(centers, d_centers, sizeof(KPose) * (n_stages + 1),
+                                 cudaMemcpyDefault, ctx->stream),
+                 "cudaMemcpyAsync centres");
+      if (!is_device_ptr(centers)) sync = true;
+    }
+    if (rng_state && !dev_rng)
+      cuda_check(cudaMemcpyAsync(rng_state, d_rng, 40, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync rng");
+    if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "coarse_to_fine");
   });
 }
 

@@ -234,3 +234,62 @@ def test_device_pointers_async_path(gpu_ctx, oracle):
     torch.cuda.synchronize()
     gpu_ctx.set_stream(None)
     np.testing.assert_array_equal(ds.cpu().numpy(), s_host)
+
+
+def _oracle_stage(oracle, w, center, g):
+    poses = configs.grid_poses(center, g["extent"], g["count"], g["rotations"], g.get("mode", 0))
+    s, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, [g["noise"]],
+                              w.sigma_max, g["window"])
+    return poses, s[:, 0]
+
+
+def test_coarse_to_fine_chain_matches_oracle(gpu_ctx, oracle):
+    """Device-resident stage chain (b3d_gpu_coarse_to_fine): every stage's
+    selection equals the oracle's reduce/sample semantics applied to that
+    stage's scores, each next centre is bitwise the selected grid pose, the
+    device Rng stream advances exactly like the reference Rng, and the stage
+    scores match the oracle's within the score tolerance."""
+    from helpers import b3d_intr
+    rf = lambda k, v, t, p: oracle.render(k, [(v, t, p)])
+    w = configs.cfg2(rf, oracle.voxel_to_mesh, seed=1, counts=(4, 4, 4), n_rot=4)
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    gpu_ctx.set_likelihood([w.stages[0]["noise"]], w.sigma_max, 1)
+    st = b3d.rng_seed(2024)
+    res, centers = gpu_ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)
+    st_o = oracle.rng_seed(2024)
+    np.testing.assert_array_equal(centers[0], w.center)
+    for s, g in enumerate(w.stages):
+        # GPU scores of this stage (same centre) via score-many
+        gpu_ctx.set_likelihood([g["noise"]], w.sigma_max, g["window"])
+        grid = gpu_ctx.make_grid(centers[s], g["extent"], g["count"], g["rotations"], 0)
+        s_gpu, _ = gpu_ctx.score_grid(mid, grid)
+        poses, s_orc = _oracle_stage(oracle, w, centers[s], g)
+        assert rel_err(s_gpu[:, 0], s_orc).max() <= SCORE_RTOL
+        probs, _ = oracle.normalize(s_gpu[:, 0])
+        pick = oracle.sample_categorical(probs, st_o)
+        assert res[s].sample == pick and res[s].argmax == oracle.argmax(s_gpu[:, 0])
+        np.testing.assert_array_equal(centers[s + 1], poses[pick])
+    np.testing.assert_array_equal(st, st_o)
+
+
+def test_coarse_to_fine_argmax_selection(gpu_ctx, oracle):
+    from helpers import b3d_intr
+    rf = lambda k, v, t, p: oracle.render(k, [(v, t, p)])
+    w = configs.cfg2(rf, oracle.voxel_to_mesh, seed=2, counts=(4, 4, 2), n_rot=2, n_stages=2)
+    for g in w.stages:
+        g["select"] = b3d.SELECT_ARGMAX
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    gpu_ctx.set_likelihood([w.stages[0]["noise"]], w.sigma_max, 1)
+    res, centers = gpu_ctx.coarse_to_fine(mid, w.center, w.stages)
+    for s, g in enumerate(w.stages):
+        gpu_ctx.set_likelihood([g["noise"]], w.sigma_max, g["window"])
+        grid = gpu_ctx.make_grid(centers[s], g["extent"], g["count"], g["rotations"], 0)
+        s_gpu, _ = gpu_ctx.score_grid(mid, grid)
+        a = int(np.argmax(s_gpu[:, 0]))
+        assert res[s].argmax == a
+        poses = configs.grid_poses(centers[s], g["extent"], g["count"], g["rotations"], 0)
+        np.testing.assert_array_equal(centers[s + 1], poses[a])
