@@ -171,6 +171,70 @@ def run_reference(args, rank, world):
     print(json.dumps(line), flush=True)
 
 
+def run_tracking(ctx, b3d, configs, frames_n, render_fn):
+    """configs[3]: per frame, upload the observation (pinned host buffer) and
+    run the two-stage argmax chain (b3d_gpu_coarse_to_fine) centred on the
+    previous estimate; wall-clock per frame as in track_camera
+    (tracking.cpp:73-82), host result read back every frame."""
+    import torch
+    tr = configs.cfg4(render_fn, b3d.voxel_to_mesh, seed=0, n_frames=frames_n)
+    ctx.set_camera(b3d.Intrinsics(*tr["k"].as_tuple()))
+    mid = ctx.upload_mesh(tr["vertices"], tr["triangles"])
+    st0 = tr["stages"][0]
+    ctx.set_likelihood([st0["noise"]], 0.1, st0["window"])
+    frames = [torch.from_numpy(f).pin_memory().numpy() for f in tr["frames"]]
+    est = tr["gt"][0].copy()
+    ctx.set_observation(frames[0])  # warm-up
+    ctx.coarse_to_fine(mid, est, tr["stages"])
+    ms, errs_cm, errs_deg = [], [], []
+    for f in range(1, frames_n):
+        t0 = time.perf_counter()
+        ctx.set_observation(frames[f])
+        _, centers = ctx.coarse_to_fine(mid, est, tr["stages"])
+        est = centers[-1]
+        ms.append(1e3 * (time.perf_counter() - t0))
+        gt = tr["gt"][f]
+        errs_cm.append(100.0 * float(np.linalg.norm(est[4:] - gt[4:])))
+        d = min(1.0, abs(float(np.dot(est[:4], gt[:4]))))
+        errs_deg.append(float(np.degrees(2.0 * np.arccos(d))))
+    total = sum(ms) * 1e-3
+    return {"workload": "configs[3]: 2,000-voxel blob, 240x320, 2 stages x 8,192 hypotheses "
+                        "per frame (argmax chain on device), observation uploaded per frame",
+            "fps": (frames_n - 1) / total, "frames": frames_n - 1,
+            "ms_per_frame_mean": statistics.mean(ms), "ms_per_frame_p50": statistics.median(ms),
+            "ms_per_frame_max": max(ms), "hypotheses_per_frame": 16384,
+            "pose_error_cm_mean": statistics.mean(errs_cm),
+            "pose_error_deg_mean": statistics.mean(errs_deg),
+            "triangles": int(tr["triangles"].shape[0])}
+
+
+def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
+    """configs[1]: five 32,768-hypothesis stages chained on the device
+    (sample selection); device time per schedule with CUDA events."""
+    import torch
+    w = configs.cfg2(render_fn, b3d.voxel_to_mesh, seed=0)
+    ctx.set_camera(b3d.Intrinsics(*w.k.as_tuple()))
+    mid = ctx.upload_mesh(w.vertices, w.triangles)
+    ctx.set_likelihood([w.stages[0]["noise"]], w.sigma_max, w.stages[0]["window"])
+    d_obs = torch.from_numpy(w.observed).cuda()
+    ctx.set_observation(d_obs)
+    st = b3d.rng_seed(11)
+    ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)  # warm-up
+    times = []
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        res, centers = ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)
+        times.append(time.perf_counter() - t0)
+    n = sum(int(np.prod(g["count"])) * g["rotations"].shape[0] for g in w.stages)
+    gt = w.gt_pose
+    return {"workload": "configs[1]: 3,000-voxel blob, 200x200, 5 stages x 32,768 hypotheses, "
+                        "sampled centres, chained on device",
+            "hypotheses": n, "ms_per_schedule": 1e3 * statistics.median(times),
+            "value": n / statistics.median(times), "unit": UNIT,
+            "final_error_cm": 100.0 * float(np.linalg.norm(centers[-1][4:] - gt[4:])),
+            "triangles": int(w.triangles.shape[0])}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -179,6 +243,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--tracking-frames", type=int, default=100)
+    ap.add_argument("--no-extra", action="store_true", help="skip the cfg2/cfg4 legs")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
@@ -320,6 +386,10 @@ def main():
         cnt = None
         if not args.no_cpu_baseline:
             cpu, cnt, cpu_scores = cpu_baseline(w, seconds=args.cpu_seconds)
+        extra = {}
+        if not args.no_extra:
+            extra["coarse_to_fine"] = run_coarse_to_fine(ctx, b3d, configs, render_fn)
+            extra["tracking"] = run_tracking(ctx, b3d, configs, args.tracking_frames, render_fn)
         roof = None
         if cnt is not None and "fp64_nofma_ops" in peaks:
             ops = _ops_per_hyp(cnt, 1, 1, BATCH)
@@ -351,6 +421,7 @@ def main():
             "roofline": roof,
             "cpu_baseline": cpu,
         }
+        line.update(extra)
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
