@@ -170,6 +170,32 @@ B3D_API b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scor
                                         uint64_t* rng_state, b3d_stage_result* out,
                                         double* probs);
 
+/* Fixed scene content rendered once per context and composited under every
+ * hypothesis (render_partial / compose_render, inference.cpp:102-109,172-184):
+ * instances in draw order (table first, then base children).  Triangle draw
+ * indices run across the instances; hypotheses' triangles follow them.
+ * n = 0 removes the base scene. */
+B3D_API b3d_status b3d_gpu_set_base_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
+                                          const b3d_pose* model_to_world, uint32_t n);
+
+/* Table-contact hypotheses of one (object, face): the cell centres of an
+ * n_dx x n_dy x n_dtheta partition of the support (stage0_cells,
+ * inference.cpp:208-238), posed by contact_to_pose (scene_graph.cpp:97-121)
+ * on a table with its top at z = 0 of the world frame (ObjectModel::table).
+ * index = (ix * n_dy + iy) * n_dtheta + it. */
+typedef struct b3d_contact_grid {
+  double table_w, table_h;
+  double aabb_min[3], aabb_max[3]; /* object model-frame AABB (mesh_bounds) */
+  int32_t face;                    /* 1..6 */
+  uint32_t count[3];               /* n_dx, n_dy, n_dtheta */
+} b3d_contact_grid;
+
+B3D_API b3d_status b3d_gpu_score_contact_grid(b3d_gpu_context* ctx, int32_t mesh_id,
+                                              const b3d_contact_grid* grid, double* scores,
+                                              uint8_t* status);
+/* Host poses (model-to-world) of a contact grid, n_dx * n_dy * n_dtheta of them. */
+B3D_API b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out);
+
 /* One stage of a device-resident enumeration schedule: a pose grid around
  * the previous stage's chosen pose (the caller's centre for stage 0), its
  * likelihood settings (sigma_max and prefactor come from the context), and

@@ -56,6 +56,25 @@ class PoseGrid(C.Structure):
                 ("rotations", C.c_void_p), ("n_rot", C.c_uint32), ("mode", C.c_uint32)]
 
 
+class ContactGrid(C.Structure):
+    _fields_ = [("table_w", C.c_double), ("table_h", C.c_double), ("aabb_min", C.c_double * 3),
+                ("aabb_max", C.c_double * 3), ("face", C.c_int32), ("count", C.c_uint32 * 3)]
+
+    @classmethod
+    def make(cls, table_w, table_h, aabb_min, aabb_max, face, count):
+        g = cls()
+        g.table_w, g.table_h, g.face = float(table_w), float(table_h), int(face)
+        for a in range(3):
+            g.aabb_min[a] = float(aabb_min[a])
+            g.aabb_max[a] = float(aabb_max[a])
+            g.count[a] = int(count[a])
+        return g
+
+    @property
+    def n(self):
+        return self.count[0] * self.count[1] * self.count[2]
+
+
 class StageSpec(C.Structure):
     _fields_ = [("extent", C.c_double * 3), ("count", C.c_uint32 * 3), ("rotations", C.c_void_p),
                 ("n_rot", C.c_uint32), ("mode", C.c_uint32), ("noise", Noise),
@@ -108,6 +127,9 @@ def lib() -> C.CDLL:
         "b3d_gpu_render_poses": ([vp, i32, vp, u64, vp, vp], st),
         "b3d_gpu_stage_reduce": ([vp, vp, u64, u32, u32, vp, vp, vp], st),
         "b3d_gpu_coarse_to_fine": ([vp, i32, C.POINTER(Pose), vp, u32, vp, vp, vp], st),
+        "b3d_gpu_set_base_scene": ([vp, vp, vp, u32], st),
+        "b3d_gpu_score_contact_grid": ([vp, i32, C.POINTER(ContactGrid), vp, vp], st),
+        "b3d_contact_grid_poses": ([C.POINTER(ContactGrid), vp], st),
         "b3d_rng_seed": ([u64, vp], None),
         "b3d_rng_split": ([vp, u64, u64, u64, vp], None),
         "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
@@ -172,6 +194,13 @@ def voxel_to_mesh(voxels: np.ndarray, resolution: float, origin) -> tuple:
     _check(lib().b3d_voxel_to_mesh(v.ctypes.data, n, resolution, o.ctypes.data,
                                    verts.ctypes.data, tris.ctypes.data, C.byref(nv), C.byref(nt)))
     return verts[: nv.value].copy(), tris[: nt.value].copy()
+
+
+def contact_grid_poses(grid: "ContactGrid") -> np.ndarray:
+    """Host model-to-world poses of a table-contact grid (b3d_contact_grid_poses)."""
+    out = np.zeros((grid.n, 7), dtype=np.float64)
+    _check(lib().b3d_contact_grid_poses(C.byref(grid), out.ctypes.data))
+    return out
 
 
 def log_likelihood(observed: np.ndarray, rendered: np.ndarray, k: Intrinsics, p_outlier: float,
@@ -355,3 +384,20 @@ class GpuContext:
         outs = [StageOut(r.argmax, r.sample, r.max_score, r.logsumexp, r.total, r.sample_logp,
                          bool(r.all_zero), r.n_nonfinite, bool(r.sample_fallback)) for r in res]
         return outs, centers
+
+    def set_base_scene(self, mesh_ids: Sequence[int], poses):
+        """Fixed instances (table first, then base children) rendered once and
+        composited under every hypothesis (b3d_gpu_set_base_scene)."""
+        ids = np.ascontiguousarray(mesh_ids, dtype=np.int32)
+        P = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 7)
+        _check(self._L.b3d_gpu_set_base_scene(self.h, ids.ctypes.data if len(ids) else None,
+                                              P.ctypes.data if len(ids) else None, len(ids)))
+
+    def score_contact_grid(self, mesh: int, grid: "ContactGrid", scores=None, status=None):
+        n = grid.n
+        if scores is None:
+            scores = np.zeros((n, self.n_noise), dtype=np.float64)
+            status = np.zeros(n, dtype=np.uint8) if status is None else status
+        _check(self._L.b3d_gpu_score_contact_grid(self.h, mesh, C.byref(grid), _ptr(scores),
+                                                  _ptr(status)))
+        return scores, status

@@ -242,3 +242,62 @@ def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
     ]
     return {"k": k, "vertices": verts, "triangles": tris, "voxels": vox, "gt": np.array(gts),
             "frames": frames, "stages": stages, "name": "cfg4_tracking_240x320"}
+
+
+TABLE_THICKNESS = 0.01
+
+
+def table_mesh(mesh_box, w: float, h: float):
+    """ObjectModel::table (scene_graph.cpp:26-35): thin box, top at z = 0."""
+    lo = np.array([-w / 2, -h / 2, -TABLE_THICKNESS])
+    hi = np.array([w / 2, h / 2, 0.0])
+    v, t = mesh_box(lo, hi)
+    return v, t, lo, hi
+
+
+def cfg3(render_scene, mesh_fn, box_fn, contact_fn, seed: int = 0, counts=(16, 16, 512)):
+    """configs[2]: multi-object scene graph with occlusion, 240x320 (H x W).
+
+    A 0.5 x 0.5 m table (top plane at camera depth 0.7 m; the camera looks
+    straight down at it) carries five seeded blobs of 500-4,000 voxels: three
+    fixed ones (the base scene, rendered once), the enumerated fourth, and a
+    fifth present only in the observation (a distractor).  The fourth object
+    is enumerated over table-contact cells (face 1): a 16 x 16 (x, y) grid of
+    cell centres times 512 yaw cells = 131,072 hypotheses.  Observation:
+    ground-truth scene, N(0, 3 mm) depth noise, 5 % outliers.  Likelihood
+    r = 5 mm, 5 x 5 window, outlier_prob 0.02.  fx = fy = 400, cx = 160, cy = 120.
+
+    render_scene(k, camera, instances) -> depth; contact_fn(table_w, table_h,
+    aabb_min, aabb_max, face, dx, dy, dtheta) -> pose; box_fn(lo, hi) -> mesh.
+    """
+    rng = np.random.Generator(np.random.PCG64(5000 + seed))
+    k = Intr(400.0, 400.0, 160.0, 120.0, 320, 240, 0.01, 10.0)
+    tw = th = 0.5
+    tv, tt, tlo, thi = table_mesh(box_fn, tw, th)
+    sizes = [500, 1000, 2000, 3000, 4000]
+    objs = []
+    for i, n in enumerate(sizes):
+        vox = synth.eden_blob(n, 100 * seed + i)
+        v, t = make_mesh(vox, mesh_fn)
+        objs.append((v, t, v.min(axis=0), v.max(axis=0)))
+    # camera: 0.7 m above the table centre looking down -z (camera +z forward)
+    camera = np.array([0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.7])  # 180 deg about x
+    placements = []
+    for i in range(5):
+        v, t, lo, hi = objs[i]
+        for _ in range(100):
+            dx, dy = rng.uniform(0.05, 0.35), rng.uniform(0.05, 0.35)
+            ok = all((dx - px) ** 2 + (dy - py) ** 2 > 0.12 ** 2 for px, py, _ in placements)
+            if ok:
+                break
+        placements.append((dx, dy, rng.uniform(0.0, 2 * np.pi)))
+    poses = [contact_fn(tw, th, objs[i][2], objs[i][3], 1, *placements[i]) for i in range(5)]
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    inst = [(tv, tt, ident)] + [(objs[i][0], objs[i][1], poses[i]) for i in range(5)]
+    depth = render_scene(k, camera, inst)
+    obs = synth.noisy_observation(depth, k.far, 0.003, 0.05, 0.2, 1.5, rng, k.near)
+    return {"name": "cfg3_scene_graph_240x320", "k": k, "camera": camera, "table": (tv, tt, tlo, thi),
+            "objects": objs, "poses": poses, "placements": placements, "observed": obs,
+            "base": [0, 1, 2], "target": 3, "contact": dict(table_w=tw, table_h=th, face=1,
+                                                          count=counts),
+            "noise": [(0.02, 0.005)], "window": 2, "sigma_max": 0.1}

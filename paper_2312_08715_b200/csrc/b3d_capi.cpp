@@ -39,6 +39,8 @@ cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int co
                                 double* probs, cudaStream_t st);
 cudaError_t launch_select_center(const KGrid& g, const KStageResult* r, int use_sample,
                                  KPose* center_out, cudaStream_t st);
+cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_keys,
+                              unsigned int* padded, float* sbase, double* G, cudaStream_t st);
 cudaError_t launch_image_loglik(const float* obs, const float* rend, int W, int H,
                                 double fx, double fy, double cx, double cy, float far_f,
                                 double p_outlier, double sigma, double sigma_max,
@@ -188,6 +190,13 @@ struct b3d_gpu_context {
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
+  // fixed scene (compose_render)
+  bool has_base = false;
+  DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
+  int base_valid = 0;
+  uint32_t base_draw = 0;
+  long long obs_version = 0, base_version = 0;
+  std::string base_terms_key;
 };
 
 namespace {
@@ -350,6 +359,55 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   return p;
 }
 
+// Base-scene terms for the likelihood settings in p.lik:
+// S_base per observed pixel and sigma slot, and the Chebyshev coefficients of
+// G_e(log |y|) = sum_p log(floor_e + coef_e(|y|) * S_base(p)) on [0, log(W*H)].
+// Cached per (observation, base scene, likelihood settings).
+void attach_base(b3d_gpu_context* ctx, KParams& p) {
+  p.draw_base = ctx->base_draw;
+  if (!ctx->has_base) {
+    p.base_keys = nullptr;
+    return;
+  }
+  p.base_keys = ctx->base_keys.as<unsigned long long>();
+  p.base_valid = ctx->base_valid;
+  p.cheb_lo = 0.0;
+  p.cheb_hi = std::log((double)ctx->k.width * ctx->k.height);
+  if (p.lik.n_noise == 0) return;  // render-only use
+  std::string key(reinterpret_cast<const char*>(&p.lik), sizeof(KLik));
+  key += std::to_string(ctx->obs_version) + "/" + std::to_string(ctx->base_version);
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  if (key != ctx->base_terms_key) {
+    const int pad = p.lik.window;
+    ctx->base_pad.ensure(4ull * (ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad));
+    ctx->sbase.ensure(4ull * kMaxNoise * npx);
+    ctx->gnodes.ensure(8ull * kMaxNoise * kCheb);
+    ctx->cheb.ensure(8ull * kMaxNoise * kCheb);
+    cuda_check(launch_base_terms(p, p.base_keys, ctx->base_pad.as<unsigned int>(),
+                                 ctx->sbase.as<float>(), ctx->gnodes.as<double>(), ctx->stream),
+               "base terms launch");
+    std::vector<double> f(kMaxNoise * kCheb), coef(kMaxNoise * kCheb, 0.0);
+    cuda_check(cudaMemcpyAsync(f.data(), ctx->gnodes.p, 8ull * p.lik.n_noise * kCheb,
+                               cudaMemcpyDeviceToHost, ctx->stream),
+               "cudaMemcpyAsync G nodes");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "base terms");
+    const double pi = 3.14159265358979323846;
+    for (int e = 0; e < p.lik.n_noise; ++e)
+      for (int j = 0; j < kCheb; ++j) {
+        double s = 0.0;
+        for (int k = 0; k < kCheb; ++k)
+          s += f[e * kCheb + k] * std::cos(pi * j * (k + 0.5) / kCheb);
+        coef[e * kCheb + j] = 2.0 * s / kCheb;
+      }
+    cuda_check(cudaMemcpyAsync(ctx->cheb.p, coef.data(), 8ull * kMaxNoise * kCheb,
+                               cudaMemcpyHostToDevice, ctx->stream),
+               "cudaMemcpyAsync cheb");
+    ctx->base_terms_key = key;
+  }
+  p.sbase = ctx->sbase.as<float>();
+  p.cheb = ctx->cheb.as<double>();
+}
+
 void finish_copy_out(b3d_gpu_context* ctx, void* dst, const void* src, size_t bytes) {
   cuda_check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->stream),
              "cudaMemcpyAsync D2H");
@@ -398,8 +456,96 @@ KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
   return L;
 }
 
+// ------------------------------------------------ table contact (host side)
+constexpr double kTwoPiD = 6.283185307179586476925287;
+
+// Eigen AngleAxis -> Quaternion with a unit axis (scene_graph.cpp:60-71,116).
+void axis_angle_q(const double ax[3], double angle, double q[4]) {
+  const double ha = 0.5 * angle;
+  const double s = std::sin(ha);
+  q[0] = std::cos(ha);
+  q[1] = s * ax[0];
+  q[2] = s * ax[1];
+  q[3] = s * ax[2];
+}
+
+// scene_graph.cpp:60-71
+void face_rotation(int face, double q[4]) {
+  const double half_pi = kTwoPiD / 4.0;
+  static const double ux[3] = {1, 0, 0}, uy[3] = {0, 1, 0};
+  switch (face) {
+    case 1: q[0] = 1; q[1] = q[2] = q[3] = 0; return;
+    case 2: axis_angle_q(ux, 2 * half_pi, q); return;
+    case 3: axis_angle_q(uy, -half_pi, q); return;
+    case 4: axis_angle_q(uy, half_pi, q); return;
+    case 5: axis_angle_q(ux, half_pi, q); return;
+    default: axis_angle_q(ux, -half_pi, q); return;
+  }
+}
+
+// scene_graph.cpp:73-89 (Eigen scalar order, as the oracle)
+void rotated_bounds(const double amin[3], const double amax[3], int face, double lo[3],
+                    double hi[3]) {
+  double q[4];
+  face_rotation(face, q);
+  const double tx = 2.0 * q[1], ty = 2.0 * q[2], tz = 2.0 * q[3];
+  const double twx = tx * q[0], twy = ty * q[0], twz = tz * q[0];
+  const double txx = tx * q[1], txy = ty * q[1], txz = tz * q[1];
+  const double tyy = ty * q[2], tyz = tz * q[2], tzz = tz * q[3];
+  const double m[9] = {1.0 - (tyy + tzz), txy - twz,         txz + twy,
+                       txy + twz,         1.0 - (txx + tzz), tyz - twx,
+                       txz - twy,         tyz + twx,         1.0 - (txx + tyy)};
+  for (int i = 0; i < 8; ++i) {
+    const double c[3] = {i & 1 ? amax[0] : amin[0], i & 2 ? amax[1] : amin[1],
+                         i & 4 ? amax[2] : amin[2]};
+    for (int a = 0; a < 3; ++a) {
+      const double r = m[3 * a] * c[0] + (m[3 * a + 1] * c[1] + m[3 * a + 2] * c[2]);
+      if (i == 0) {
+        lo[a] = hi[a] = r;
+      } else {
+        lo[a] = r < lo[a] ? r : lo[a];
+        hi[a] = r > hi[a] ? r : hi[a];
+      }
+    }
+  }
+}
+
+// KGrid (mode 2) for a contact grid: face rotation, footprint and the
+// per-cell spin cos/sin computed here with libm; the rest runs on device.
+KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
+  check(g.face >= 1 && g.face <= 6, "face must be in 1..6");
+  check(g.count[0] >= 1 && g.count[1] >= 1 && g.count[2] >= 1,
+        "schedule stage: subdivision counts must be >= 1");
+  KGrid k{};
+  k.mode = 2;
+  for (int a = 0; a < 3; ++a) k.count[a] = (int)g.count[a];
+  KContact& c = k.contact;
+  face_rotation(g.face, c.face_q);
+  double lo[3], hi[3];
+  rotated_bounds(g.aabb_min, g.aabb_max, g.face, lo, hi);
+  for (int a = 0; a < 3; ++a) c.lo[a] = lo[a];
+  c.w = hi[0] - lo[0];
+  c.h = hi[1] - lo[1];
+  c.table_w = g.table_w;
+  c.table_h = g.table_h;
+  c.dx_range = g.table_w - c.w;
+  c.dy_range = g.table_h - c.h;
+  require(c.dx_range > 0 && c.dy_range > 0, ErrorCode::numeric,
+          "stage 0: empty proposal support (no object fits the table)");
+  spin.resize(2 * g.count[2]);
+  for (uint32_t it = 0; it < g.count[2]; ++it) {
+    const double dlo = kTwoPiD * it / g.count[2], dhi = kTwoPiD * (it + 1) / g.count[2];
+    const double dtheta = 0.5 * (dlo + dhi);
+    const double ha = 0.5 * dtheta;
+    spin[2 * it] = std::cos(ha);
+    spin[2 * it + 1] = std::sin(ha);
+  }
+  return k;
+}
+
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
-                  const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status) {
+                  const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
+                  const b3d_contact_grid* contact = nullptr) {
   require_ready(ctx, true, true);
   check(scores != nullptr, "bad arguments");
   check(n > 0, "score_cells: no cells");
@@ -410,6 +556,18 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   if (poses) {
     p.poses = static_cast<const KPose*>(
         stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
+  } else if (contact) {
+    std::vector<double> spin;
+    p.poses = nullptr;
+    p.grid = make_contact_grid(*contact, spin);
+    check((uint64_t)contact->count[0] * contact->count[1] * contact->count[2] == n,
+          "contact grid: n does not match the grid size");
+    ctx->spin.ensure(8 * spin.size());
+    cuda_check(cudaMemcpyAsync(ctx->spin.p, spin.data(), 8 * spin.size(), cudaMemcpyHostToDevice,
+                               ctx->stream),
+               "cudaMemcpyAsync spin");
+    p.grid.contact.spin = ctx->spin.as<double>();
+    host_in = true;
   } else {
     check(grid != nullptr && grid->rotations && grid->n_rot > 0, "bad arguments");
     const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
@@ -450,6 +608,7 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
       p.status = ctx->out_stage2.as<uint8_t>();
     }
   }
+  attach_base(ctx, p);
   LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n);
   p.zscratch = ctx->zscratch.as<unsigned long long>();
   p.vscratch = ctx->vscratch.as<double>();
@@ -662,6 +821,7 @@ b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth) {
                "obs_prepare launch");
     if (host) cuda_check(cudaStreamSynchronize(ctx->stream), "set_observation");
     ctx->has_obs = true;
+    ++ctx->obs_version;
   });
 }
 
@@ -708,6 +868,8 @@ b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d
     p.poses = static_cast<const KPose*>(
         stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
     p.n_hyp = (long long)n;
+    p.lik.n_noise = 0;  // render only
+    attach_base(ctx, p);
     const size_t npx = (size_t)ctx->k.width * ctx->k.height;
     const bool dev_d = is_device_ptr(depth);
     const bool dev_i = draw_index && is_device_ptr(draw_index);
@@ -871,6 +1033,7 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
       const b3d_stage_spec& g = stages[s];
       KParams p = base_params(ctx, m);
       p.lik = make_lik(ctx->k, &g.noise, 1, ctx->sigma_max, g.window, ctx->prefactor);
+      attach_base(ctx, p);
       p.poses = nullptr;
       p.grid.center_dev = d_centers + s;
       for (int a = 0; a < 3; ++a) {
@@ -914,6 +1077,137 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
       cuda_check(cudaMemcpyAsync(rng_state, d_rng, 40, cudaMemcpyDeviceToHost, ctx->stream),
                  "cudaMemcpyAsync rng");
     if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "coarse_to_fine");
+  });
+}
+
+b3d_status b3d_gpu_set_base_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
+                                  const b3d_pose* model_to_world, uint32_t n) {
+  return guarded([&] {
+    require_ready(ctx, false, false);
+    DeviceGuard dg(ctx->device);
+    ++ctx->base_version;
+    ctx->base_terms_key.clear();
+    if (n == 0) {
+      ctx->has_base = false;
+      ctx->base_draw = 0;
+      ctx->base_valid = 0;
+      return;
+    }
+    check(mesh_ids && model_to_world, "bad arguments");
+    const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+    ctx->base_keys.ensure(8 * npx);
+    ctx->base_tmp.ensure(8 * npx);
+    ctx->has_base = false;
+    ctx->base_draw = 0;
+    unsigned long long* cur = nullptr;  // first instance composes onto the background
+    for (uint32_t i = 0; i < n; ++i) {
+      const Mesh& m = get_mesh(ctx, mesh_ids[i]);
+      KParams p = base_params(ctx, m);
+      const KPose pose = pose_from_c(model_to_world[i]);
+      ctx->in_stage.ensure(sizeof(KPose));
+      cuda_check(cudaMemcpyAsync(ctx->in_stage.p, &pose, sizeof(KPose), cudaMemcpyHostToDevice,
+                                 ctx->stream),
+                 "cudaMemcpyAsync pose");
+      p.poses = ctx->in_stage.as<KPose>();
+      p.n_hyp = 1;
+      p.lik.n_noise = 0;
+      p.draw_base = ctx->base_draw;
+      p.base_keys = cur;
+      // ping-pong: the last instance must land in base_keys
+      unsigned long long* dst = ((n - 1 - i) % 2 == 0) ? ctx->base_keys.as<unsigned long long>()
+                                                       : ctx->base_tmp.as<unsigned long long>();
+      p.out_keys = dst;
+      p.out_depth = nullptr;
+      p.out_ids = nullptr;
+      LaunchPlan lp = plan_launch<true, false, true>(ctx, m, 1);
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
+      cuda_check(launch_render_score<true, false, true>(p, 1, lp.smem, ctx->stream),
+                 "base render launch");
+      cur = dst;
+      ctx->base_draw += (uint32_t)m.nt;
+    }
+    std::vector<unsigned long long> keys(npx);
+    cuda_check(cudaMemcpyAsync(keys.data(), ctx->base_keys.p, 8 * npx, cudaMemcpyDeviceToHost,
+                               ctx->stream),
+               "cudaMemcpyAsync base");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "set_base_scene");
+    const float far_f = static_cast<float>(ctx->k.far_m);
+    int valid = 0;
+    for (unsigned long long k : keys) {
+      const unsigned int bits = (unsigned int)(k >> 32);
+      float z;
+      std::memcpy(&z, &bits, 4);
+      valid += z < far_f;
+    }
+    ctx->base_valid = valid;
+    ctx->has_base = true;
+  });
+}
+
+b3d_status b3d_gpu_score_contact_grid(b3d_gpu_context* ctx, int32_t mesh_id,
+                                      const b3d_contact_grid* grid, double* scores,
+                                      uint8_t* status) {
+  return guarded([&] {
+    check(grid != nullptr, "bad arguments");
+    const uint64_t n = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
+    score_common(ctx, mesh_id, nullptr, nullptr, n, scores, status, grid);
+  });
+}
+
+b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out) {
+  return guarded([&] {
+    check(grid && out, "bad arguments");
+    std::vector<double> spin;
+    const KGrid g = make_contact_grid(*grid, spin);
+    const KContact& c = g.contact;
+    const uint32_t nx = grid->count[0], ny = grid->count[1], nt = grid->count[2];
+    for (uint32_t ix = 0; ix < nx; ++ix)
+      for (uint32_t iy = 0; iy < ny; ++iy)
+        for (uint32_t it = 0; it < nt; ++it) {
+          // same operations as posemath.cuh contact_pose
+          const double dx = 0.5 * (c.dx_range * ix / nx + c.dx_range * (ix + 1) / nx);
+          const double dy = 0.5 * (c.dy_range * iy / ny + c.dy_range * (iy + 1) / ny);
+          const double cs = spin[2 * it], sn = spin[2 * it + 1];
+          const double sq[4] = {cs, sn * 0.0, sn * 0.0, sn * 1.0};
+          const double cx = -c.table_w / 2, cy = -c.table_h / 2, cz = 0.0;
+          const double bt[3] = {cx + (dx - c.lo[0]), cy + (dy - c.lo[1]), cz + -c.lo[2]};
+          const double pv[3] = {cx + (dx + c.w / 2), cy + (dy + c.h / 2), cz + 0.0};
+          const double* fq = c.face_q;
+          double w = sq[0] * fq[0] - sq[1] * fq[1] - sq[2] * fq[2] - sq[3] * fq[3];
+          double x = sq[0] * fq[1] + sq[1] * fq[0] + sq[2] * fq[3] - sq[3] * fq[2];
+          double y = sq[0] * fq[2] + sq[2] * fq[0] + sq[3] * fq[1] - sq[1] * fq[3];
+          double z = sq[0] * fq[3] + sq[3] * fq[0] + sq[1] * fq[2] - sq[2] * fq[1];
+          const double n2 = (x * x + y * y) + (z * z + w * w);
+          if (n2 > 0) {
+            const double nn = std::sqrt(n2);
+            w /= nn;
+            x /= nn;
+            y /= nn;
+            z /= nn;
+          }
+          const double rel[3] = {bt[0] - pv[0], bt[1] - pv[1], bt[2] - pv[2]};
+          double uv0 = sq[2] * rel[2] - sq[3] * rel[1];
+          double uv1 = sq[3] * rel[0] - sq[1] * rel[2];
+          double uv2 = sq[1] * rel[1] - sq[2] * rel[0];
+          uv0 += uv0;
+          uv1 += uv1;
+          uv2 += uv2;
+          const double c0 = sq[2] * uv2 - sq[3] * uv1;
+          const double c1 = sq[3] * uv0 - sq[1] * uv2;
+          const double c2 = sq[1] * uv1 - sq[2] * uv0;
+          b3d_pose& o = out[((size_t)ix * ny + iy) * nt + it];
+          o.qw = w;
+          o.qx = x;
+          o.qy = y;
+          o.qz = z;
+          o.tx = (rel[0] + sq[0] * uv0 + c0) + pv[0];
+          o.ty = (rel[1] + sq[0] * uv1 + c1) + pv[1];
+          o.tz = (rel[2] + sq[0] * uv2 + c2) + pv[2];
+        }
   });
 }
 

@@ -16,17 +16,33 @@ struct KPose {
 // BASELINE 6-DoF hypothesis grid (no reference equivalent):
 // translation lattice (tracking.cpp:27-37 formula) around the centre times a
 // table of rotation perturbations, q = normalized(center.q * dq[r]).
+// Table-contact hypotheses (stage0_cells / contact_to_pose,
+// inference.cpp:208-238, scene_graph.cpp:97-121): the cell centres of an
+// n_dx x n_dy x n_dtheta partition of one (object, face) support.  Values that
+// need libm (face rotation, per-cell spin cos/sin, rotated bounds) are
+// computed once on the host with the same formulas as the oracle.
+struct KContact {
+  double face_q[4];        // face_rotation(face), (w,x,y,z)
+  double lo[3];            // rotated_bounds lo
+  double w, h;             // footprint (hi - lo) in x, y
+  double table_w, table_h;
+  double dx_range, dy_range;
+  const double* spin;      // n_dtheta x 2: cos, sin of half the cell-centre angle
+};
+
 struct KGrid {
   KPose center;             // used when center_dev == nullptr
   const KPose* center_dev;  // device-resident centre (stage chaining)
   double extent[3];
-  int count[3];
+  int count[3];             // contact mode: n_dx, n_dy, n_dtheta
   const double* rotations;  // n_rot x 4 (w,x,y,z), device
   int n_rot;
-  int mode;                 // 0 product, 1 zip
+  int mode;                 // 0 product, 1 zip, 2 table contact
+  KContact contact;
 };
 
 constexpr int kMaxNoise = 4;
+constexpr int kCheb = 64;
 
 struct KLik {
   int n_noise;
@@ -67,6 +83,13 @@ struct KParams {
   uint8_t* status;    // n_hyp (1 = empty render)
   float* out_depth;   // n_hyp x W x H  (render mode)
   int32_t* out_ids;   // n_hyp x W x H  (render mode, draw index or -1)
+  unsigned long long* out_keys;  // n_hyp x W x H raw (depth bits, draw) keys (base build)
+  // fixed scene rendered once (compose_render, inference.cpp:102-109)
+  const unsigned long long* base_keys;  // W x H keys, background depth 1e30; null = none
+  int base_valid;                       // valid pixels of the base image
+  const float* sbase;                   // n_slots x W x H window sums of the base image
+  const double* cheb;                   // n_noise x kCheb coefficients of G(log |y|)
+  double cheb_lo, cheb_hi;              // G's domain: [0, log(W*H)]
   // per-CTA global scratch (used only when the on-chip buffers overflow)
   unsigned long long* zscratch;  // gridDim x zstride keys
   long long zstride;             // (W + 4w) * (H + 4w): padded full-image region

@@ -58,7 +58,39 @@ __device__ __forceinline__ double lattice(double c, double e, int n, int i) {
   return c - e + 2.0 * e * i / (n - 1);
 }
 
+// scene_graph.cpp:97-121 for the cell centre (inference.cpp:126-137,
+// Interval::center inference.hpp:18) of contact cell (ix, iy, it).
+__device__ __forceinline__ void contact_pose(const KGrid& g, long long index, KPose& out) {
+  const KContact& c = g.contact;
+  const int nt = g.count[2], ny = g.count[1], nx = g.count[0];
+  const int it = (int)(index % nt);
+  const int iy = (int)((index / nt) % ny);
+  const int ix = (int)(index / ((long long)nt * ny));
+  const double dx = 0.5 * (c.dx_range * ix / nx + c.dx_range * (ix + 1) / nx);
+  const double dy = 0.5 * (c.dy_range * iy / ny + c.dy_range * (iy + 1) / ny);
+  const double cs = c.spin[2 * it], sn = c.spin[2 * it + 1];
+  const Q spin{cs, sn * 0.0, sn * 0.0, sn * 1.0};  // AngleAxis(dtheta, UnitZ)
+  const double cx = -c.table_w / 2, cy = -c.table_h / 2, cz = 0.0;
+  const double bt[3] = {cx + (dx - c.lo[0]), cy + (dy - c.lo[1]), cz + -c.lo[2]};
+  const double pv[3] = {cx + (dx + c.w / 2), cy + (dy + c.h / 2), cz + 0.0};
+  const Q q = q_normalized(q_mul(spin, Q{c.face_q[0], c.face_q[1], c.face_q[2], c.face_q[3]}));
+  const double rel[3] = {bt[0] - pv[0], bt[1] - pv[1], bt[2] - pv[2]};
+  double r[3];
+  q_rotate(spin, rel, r);
+  out.qw = q.w;
+  out.qx = q.x;
+  out.qy = q.y;
+  out.qz = q.z;
+  out.tx = r[0] + pv[0];
+  out.ty = r[1] + pv[1];
+  out.tz = r[2] + pv[2];
+}
+
 __device__ __forceinline__ void grid_pose(const KGrid& g, long long index, KPose& out) {
+  if (g.mode == 2) {
+    contact_pose(g, index, out);
+    return;
+  }
   long long ti, ri;
   if (g.mode == 0) {
     ti = index / g.n_rot;

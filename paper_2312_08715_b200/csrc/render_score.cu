@@ -343,6 +343,18 @@ __device__ __forceinline__ void window_sums(const KParams& p, const typename Key
   }
 }
 
+// Clenshaw evaluation of a Chebyshev series on [lo, hi].
+__device__ __forceinline__ double cheb_eval(const double* c, double x, double lo, double hi) {
+  const double t = (2.0 * x - (lo + hi)) / (hi - lo);
+  double b1 = 0.0, b2 = 0.0;
+  for (int j = kCheb - 1; j >= 1; --j) {
+    const double b0 = 2.0 * t * b1 - b2 + c[j];
+    b2 = b1;
+    b1 = b0;
+  }
+  return t * b1 - b2 + 0.5 * c[0];
+}
+
 constexpr float kBgDepth = 1e30f;
 constexpr int kThreads = 384;
 constexpr int kWarps = kThreads / 32;
@@ -379,7 +391,19 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   const Key bg = kIds ? (Key)(((unsigned long long)__float_as_uint(kBgDepth) << 32) |
                               0xffffffffull)
                       : (Key)__float_as_uint(kBgDepth);
-  for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
+  if (p.base_keys) {  // compose_render: start from the fixed scene (inference.cpp:104)
+    for (int i = tid; i < hc.rpx; i += kThreads) {
+      const int v = rg.oy + i / rg.rw, u = rg.ox + (i - (i / rg.rw) * rg.rw);
+      Key k = bg;
+      if (u >= 0 && u < p.W && v >= 0 && v < p.H) {
+        const unsigned long long b = __ldg(p.base_keys + (size_t)v * p.W + u);
+        k = kIds ? (Key)b : (Key)(unsigned int)(b >> 32);
+      }
+      zb[i] = k;
+    }
+  } else {
+    for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
+  }
   if (tid == 0) *s_ndef = 0;
   __syncthreads();
 
@@ -537,16 +561,20 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   // ---- render-many output (sentinel = (float)far, id -1 = background)
   if (kOut) {
     const size_t npx = (size_t)p.W * p.H;
-    float* od = p.out_depth + (size_t)h * npx;
+    float* od = p.out_depth ? p.out_depth + (size_t)h * npx : nullptr;
     int32_t* oi = p.out_ids ? p.out_ids + (size_t)h * npx : nullptr;
+    unsigned long long* ok = p.out_keys ? p.out_keys + (size_t)h * npx : nullptr;
     for (int i = tid; i < (int)npx; i += kThreads) {
       const int u = i % p.W, v = i / p.W;
       Key k = bg;
       if (!hc.empty_region && u >= rg.u0 && u <= rg.u1 && v >= rg.v0 && v <= rg.v1)
         k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+      else if (p.base_keys)
+        k = kIds ? (Key)__ldg(p.base_keys + i) : (Key)(unsigned int)(__ldg(p.base_keys + i) >> 32);
+      if (ok) ok[i] = kIds ? (unsigned long long)k : ((unsigned long long)k << 32) | 0xffffffffull;
       const float z = __uint_as_float(
           kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
-      od[i] = z < p.far_f ? z : p.far_f;
+      if (od) od[i] = z < p.far_f ? z : p.far_f;
       if (kIds && oi) {
         const unsigned int d = (unsigned int)((unsigned long long)k & 0xffffffffull);
         oi[i] = d == 0xffffffffu ? -1 : (int32_t)d;
@@ -556,18 +584,26 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
 
   if (kScore) {
     // ---- D1: |y| = number of valid rendered pixels (likelihood.cpp:144-158)
+    // With a base image: |y| = base count - base pixels of the region +
+    // composed pixels of the region (the halo holds base pixels too, so the
+    // interior [u0,u1]x[v0,v1] is counted).
     int cnt = 0;
-    if (!hc.empty_region)
-      for (int i = tid; i < hc.rpx; i += kThreads) {
-        const float z = __uint_as_float(
-            kIds ? (unsigned int)((unsigned long long)zb[i] >> 32) : (unsigned int)zb[i]);
-        cnt += z < p.far_f;
-      }
+    const int iw = rg.u1 - rg.u0 + 1, ipx = iw * (rg.v1 - rg.v0 + 1);
+    for (int i = tid; i < ipx; i += kThreads) {
+      const int v = rg.v0 + i / iw, u = rg.u0 + (i - (i / iw) * iw);
+      const Key k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
+      cnt += z < p.far_f;
+      if (p.base_keys)
+        cnt -= __uint_as_float((unsigned int)(__ldg(p.base_keys + (size_t)v * p.W + u) >> 32)) <
+               p.far_f;
+    }
     cnt = warp_sum_i(cnt);
     if (lane == 0 && cnt) atomicAdd(s_count, cnt);
     __syncthreads();
-    const int rend_count = *s_count;
-    if (rend_count == 0) {
+    const int rend_count = *s_count + p.base_valid;
+    if (rend_count == 0) {  // (never with a non-empty base image)
       // the reference throws (likelihood.cpp:159-160); batched callers get
       // -inf and a status flag instead
       if (tid == 0) {
@@ -611,13 +647,27 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       if (o.w == 0.f) continue;
       float S[kMaxNoise];
       window_sums<kIds>(p, zb, rg, u, v, o, S);
+      if (p.base_keys) {
+        // g(S) - g(S_base): the pixel's term relative to the base-only sum G
 #pragma unroll
-      for (int e = 0; e < kMaxNoise; ++e) {
-        if (e < p.lik.n_noise) {
-          const float Se = S[p.lik.slot_of[e]];
-          if (Se > 0.f) {
-            acc[e] += (double)__logf(floor_f[e] + coef_f[e] * Se);
-            npos[e] += 1;
+        for (int e = 0; e < kMaxNoise; ++e) {
+          if (e < p.lik.n_noise) {
+            const int sl = p.lik.slot_of[e];
+            const float Sb = __ldg(p.sbase + (size_t)sl * p.W * p.H + (size_t)v * p.W + u);
+            if (S[sl] != Sb)
+              acc[e] += (double)(__logf(floor_f[e] + coef_f[e] * S[sl]) -
+                                 __logf(floor_f[e] + coef_f[e] * Sb));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < kMaxNoise; ++e) {
+          if (e < p.lik.n_noise) {
+            const float Se = S[p.lik.slot_of[e]];
+            if (Se > 0.f) {
+              acc[e] += (double)__logf(floor_f[e] + coef_f[e] * Se);
+              npos[e] += 1;
+            }
           }
         }
       }
@@ -644,9 +694,16 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         a += s_red[k][e];
         np += s_redi[k][e];
       }
-      const int m_zero = *p.obs_count - np;
       double total = p.lik.prefactor[e] + a;
-      if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
+      if (p.base_keys) {
+        // + G(log |y|): the base-only sum over all observed pixels, a smooth
+        // function of |y| through coef; Chebyshev interpolant tabulated per
+        // observation and noise entry (base_scene.cu)
+        total += cheb_eval(p.cheb + e * kCheb, log((double)rend_count), p.cheb_lo, p.cheb_hi);
+      } else {
+        const int m_zero = *p.obs_count - np;
+        if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
+      }
       p.scores[h * p.lik.n_noise + e] = total;
     }
     if (tid == 0 && p.status) p.status[h] = 0;
@@ -796,6 +853,80 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
           def_list, &s_ndef, &s_count, s_coef, s_red, s_redi, h);
     __syncthreads();
   }
+}
+
+// ---------------------------------------------------------------- base scene
+// Padded depth-bit image of the base scene (halo of `pad` background pixels)
+// so the S_base window sums below run the exact same tap code as the
+// hypothesis kernel.
+__global__ void base_pad_kernel(const unsigned long long* keys, int W, int H, int pad,
+                                unsigned int* out) {
+  const int PW = W + 2 * pad, PH = H + 2 * pad;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < PW * PH; i += gridDim.x * blockDim.x) {
+    const int v = i / PW - pad, u = i % PW - pad;
+    out[i] = (u >= 0 && u < W && v >= 0 && v < H) ? (unsigned int)(keys[(size_t)v * W + u] >> 32)
+                                                  : __float_as_uint(kBgDepth);
+  }
+}
+
+// S_base(p, slot): the window sums of every observed pixel against the base
+// image alone (likelihood.cpp:198-214 restricted to the fixed scene).
+__global__ void sbase_kernel(const KParams p, const unsigned int* padded, int pad,
+                             float* sbase) {
+  Region rg;
+  rg.u0 = 0;
+  rg.v0 = 0;
+  rg.u1 = p.W - 1;
+  rg.v1 = p.H - 1;
+  rg.ox = -pad;
+  rg.oy = -pad;
+  rg.rw = p.W + 2 * pad;
+  rg.rh = p.H + 2 * pad;
+  const size_t npx = (size_t)p.W * p.H;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)npx; i += gridDim.x * blockDim.x) {
+    const int v = i / p.W, u = i % p.W;
+    const float4 o = p.obs[i];
+    float S[kMaxNoise];
+#pragma unroll
+    for (int sl = 0; sl < kMaxNoise; ++sl) S[sl] = 0.f;
+    if (o.w != 0.f) window_sums<false>(p, padded, rg, u, v, o, S);
+    for (int sl = 0; sl < p.lik.n_slots; ++sl) sbase[(size_t)sl * npx + i] = S[sl];
+  }
+}
+
+// G_e(l) = sum over observed pixels of log(floor_e + coef_e(|y| = e^l) * S_base)
+// at the kCheb Chebyshev nodes of [lo, hi] (fp64, fixed-order reduction).
+__global__ void gnode_kernel(const KParams p, const float* sbase, double lo, double hi,
+                             double* G) {
+  __shared__ double s_red[256];
+  const int k = blockIdx.x, e = blockIdx.y;
+  const double node = 0.5 * (lo + hi) + 0.5 * (hi - lo) * cos(3.14159265358979323846 * (k + 0.5) / kCheb);
+  const double y = exp(node);
+  const double coef = p.lik.one_minus_p[e] / y * p.lik.norm3[e];
+  const double fl = p.lik.floor_term[e];
+  const size_t npx = (size_t)p.W * p.H;
+  const float* sb = sbase + (size_t)p.lik.slot_of[e] * npx;
+  double acc = 0.0;
+  for (size_t i = threadIdx.x; i < npx; i += blockDim.x)
+    if (p.obs[i].w != 0.f) acc += log(fl + coef * (double)sb[i]);
+  s_red[threadIdx.x] = acc;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) s_red[threadIdx.x] += s_red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) G[e * kCheb + k] = s_red[0];
+}
+
+cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_keys,
+                              unsigned int* padded, float* sbase, double* G, cudaStream_t st) {
+  const int pad = p.lik.window;
+  const int n_pad = (p.W + 2 * pad) * (p.H + 2 * pad);
+  base_pad_kernel<<<(n_pad + 255) / 256, 256, 0, st>>>(base_keys, p.W, p.H, pad, padded);
+  const int npx = p.W * p.H;
+  sbase_kernel<<<(npx + 255) / 256, 256, 0, st>>>(p, padded, pad, sbase);
+  gnode_kernel<<<dim3(kCheb, p.lik.n_noise), 256, 0, st>>>(p, sbase, p.cheb_lo, p.cheb_hi, G);
+  return cudaGetLastError();
 }
 
 // Observation cache (likelihood.cpp:106-126) as per-pixel fp32 points plus

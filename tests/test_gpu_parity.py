@@ -293,3 +293,64 @@ def test_coarse_to_fine_argmax_selection(gpu_ctx, oracle):
         assert res[s].argmax == a
         poses = configs.grid_poses(centers[s], g["extent"], g["count"], g["rotations"], 0)
         np.testing.assert_array_equal(centers[s + 1], poses[a])
+
+
+def _cfg3(oracle, counts=(4, 4, 8)):
+    rs = lambda k, cam, inst: oracle.render(k, inst, camera=cam)
+    return configs.cfg3(rs, oracle.voxel_to_mesh, oracle.box_mesh, oracle.contact_to_pose,
+                        counts=counts)
+
+
+def _setup_cfg3(ctx, oracle, w):
+    from helpers import b3d_intr
+    ctx.set_camera(b3d_intr(w["k"]), w["camera"])
+    tv, tt = w["table"][0], w["table"][1]
+    mids = [ctx.upload_mesh(tv, tt)] + [ctx.upload_mesh(o[0], o[1]) for o in w["objects"]]
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    ctx.set_base_scene([mids[0]] + [mids[1 + i] for i in w["base"]],
+                       [ident] + [w["poses"][i] for i in w["base"]])
+    base_inst = [(tv, tt, ident)] + [(w["objects"][i][0], w["objects"][i][1], w["poses"][i])
+                                     for i in w["base"]]
+    return mids, base_inst
+
+
+def test_base_scene_render_parity(gpu_ctx, oracle):
+    """compose_render (inference.cpp:102-109): a fixed table + 3 objects
+    rendered once, the enumerated object composited per hypothesis; depth and
+    global draw indices bit-identical to rendering the whole scene."""
+    w = _cfg3(oracle)
+    mids, base_inst = _setup_cfg3(gpu_ctx, oracle, w)
+    o = w["objects"][w["target"]]
+    g = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, (4, 4, 8))
+    poses = b3d.contact_grid_poses(g)[::9]
+    depth, ids = gpu_ctx.render_poses(mids[1 + w["target"]], poses)
+    for i in range(poses.shape[0]):
+        od, oi = oracle.render(w["k"], base_inst + [(o[0], o[1], poses[i])], camera=w["camera"],
+                               with_ids=True)
+        np.testing.assert_array_equal(depth[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[i], oi)
+    gpu_ctx.set_base_scene([], [])
+
+
+def test_base_scene_contact_grid_score_parity(gpu_ctx, oracle):
+    """cfg3-shaped scoring: contact grid on the device, base scene composited,
+    likelihood including the base-only term G(|y|) (Chebyshev interpolant)."""
+    w = _cfg3(oracle)
+    mids, base_inst = _setup_cfg3(gpu_ctx, oracle, w)
+    gpu_ctx.set_observation(w["observed"])
+    gpu_ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    o = w["objects"][w["target"]]
+    g = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, (4, 4, 8))
+    s_gpu, st_gpu = gpu_ctx.score_contact_grid(mids[1 + w["target"]], g)
+    poses = b3d.contact_grid_poses(g)
+    base = oracle.render(w["k"], base_inst, camera=w["camera"])
+    s_orc, st_orc = oracle.score_poses(w["k"], w["observed"], o[0], o[1], poses, w["noise"],
+                                       w["sigma_max"], w["window"], base_depth=base,
+                                       camera=w["camera"])
+    assert (st_gpu == 0).all() and (st_orc == 0).all()
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+    assert np.abs(s_gpu - s_orc).max() < 0.5
+    # explicit poses through the same base scene
+    s_p, _ = gpu_ctx.score_poses(mids[1 + w["target"]], poses)
+    assert rel_err(s_p, s_orc).max() <= SCORE_RTOL
+    gpu_ctx.set_base_scene([], [])
