@@ -225,6 +225,23 @@ B3D_API b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id,
                                           uint64_t* rng_state, b3d_stage_result* results,
                                           b3d_pose* centers);
 
+/* n_samples categorical draws from the posterior softmax(scores) with
+ * consecutive uniform() values of rng_state (each draw has
+ * sample_categorical semantics, inference.cpp:345-353); also fills *out
+ * like b3d_gpu_stage_reduce (argmax, logsumexp; its `sample` = the first
+ * draw). */
+B3D_API b3d_status b3d_gpu_sample_many(b3d_gpu_context* ctx, const double* scores, uint64_t n,
+                                       uint32_t stride, uint32_t col, uint64_t* rng_state,
+                                       uint32_t n_samples, uint64_t* samples,
+                                       b3d_stage_result* out);
+
+/* Score hypotheses [first, first + n) of a device pose grid (one rank's
+ * shard of a large enumeration); scores[i] is hypothesis
+ * first + i. */
+B3D_API b3d_status b3d_gpu_score_grid_range(b3d_gpu_context* ctx, int32_t mesh_id,
+                                            const b3d_pose_grid* grid, uint64_t first,
+                                            uint64_t n, double* scores, uint8_t* status);
+
 /* Reference Rng seeding (rng.cpp:20-28), for building rng_state. */
 B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
 B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,

@@ -128,6 +128,8 @@ def lib() -> C.CDLL:
         "b3d_gpu_stage_reduce": ([vp, vp, u64, u32, u32, vp, vp, vp], st),
         "b3d_gpu_coarse_to_fine": ([vp, i32, C.POINTER(Pose), vp, u32, vp, vp, vp], st),
         "b3d_gpu_set_base_scene": ([vp, vp, vp, u32], st),
+        "b3d_gpu_sample_many": ([vp, vp, u64, u32, u32, vp, u32, vp, vp], st),
+        "b3d_gpu_score_grid_range": ([vp, i32, C.POINTER(PoseGrid), u64, u64, vp, vp], st),
         "b3d_gpu_score_contact_grid": ([vp, i32, C.POINTER(ContactGrid), vp, vp], st),
         "b3d_contact_grid_poses": ([C.POINTER(ContactGrid), vp], st),
         "b3d_rng_seed": ([u64, vp], None),
@@ -400,4 +402,29 @@ class GpuContext:
             status = np.zeros(n, dtype=np.uint8) if status is None else status
         _check(self._L.b3d_gpu_score_contact_grid(self.h, mesh, C.byref(grid), _ptr(scores),
                                                   _ptr(status)))
+        return scores, status
+
+    def sample_many(self, scores, n_samples: int, rng_state, n=None, stride=1, col=0,
+                    samples=None):
+        """n_samples posterior draws (b3d_gpu_sample_many); returns (samples, StageOut)."""
+        if n is None:
+            n = scores.shape[0]
+        if isinstance(scores, np.ndarray):
+            scores = np.ascontiguousarray(scores, dtype=np.float64)
+        if samples is None:
+            samples = np.zeros(n_samples, dtype=np.uint64)
+        res = StageResult()
+        _check(self._L.b3d_gpu_sample_many(self.h, _ptr(scores), n, stride, col, _ptr(rng_state),
+                                           n_samples, _ptr(samples), C.addressof(res)))
+        return samples, StageOut(res.argmax, res.sample, res.max_score, res.logsumexp, res.total,
+                                 res.sample_logp, bool(res.all_zero), res.n_nonfinite,
+                                 bool(res.sample_fallback))
+
+    def score_grid_range(self, mesh: int, grid: PoseGrid, first: int, n: int, scores=None,
+                         status=None):
+        if scores is None:
+            scores = np.zeros((n, self.n_noise), dtype=np.float64)
+            status = np.zeros(n, dtype=np.uint8) if status is None else status
+        _check(self._L.b3d_gpu_score_grid_range(self.h, mesh, C.byref(grid), first, n,
+                                                _ptr(scores), _ptr(status)))
         return scores, status

@@ -301,3 +301,45 @@ def cfg3(render_scene, mesh_fn, box_fn, contact_fn, seed: int = 0, counts=(16, 1
             "base": [0, 1, 2], "target": 3, "contact": dict(table_w=tw, table_h=th, face=1,
                                                           count=counts),
             "noise": [(0.02, 0.005)], "window": 2, "sigma_max": 0.1}
+
+
+def cfg5(render_scene, mesh_fn, box_fn, contact_fn, seed: int = 0, counts=(64, 64, 32),
+         n_rot: int = 8, n_library: int = 20, n_placed: int = 10):
+    """configs[4]: large-scale sharded enumeration at 480x640 (H x W),
+    fx = fy = 600, cx = 320, cy = 240.  A library of 20 seeded ~4,000-voxel
+    blobs; 10 of them placed on a 0.6 x 0.6 m table (base scene, camera 0.8 m
+    above it looking down); one more library object is enumerated over a
+    64 x 64 x 32 translation lattice (+-4 cm x/y, +-2 cm z around its true
+    position) times 8 vMF(kappa = 500) rotations = 1,048,576 6-DoF
+    hypotheses.  Observation: ground truth with N(0, 2 mm) noise and 5 %
+    outliers.  Likelihood r = 3 mm, 5 x 5 window, outlier_prob 0.02."""
+    rng = np.random.Generator(np.random.PCG64(6000 + seed))
+    k = Intr(600.0, 600.0, 320.0, 240.0, 640, 480, 0.01, 10.0)
+    tw = th = 0.6
+    tv, tt, tlo, thi = table_mesh(box_fn, tw, th)
+    lib = []
+    for i in range(n_library):
+        vox = synth.eden_blob(4000, 1000 * seed + i)
+        v, t = make_mesh(vox, mesh_fn)
+        lib.append((v, t, v.min(axis=0), v.max(axis=0)))
+    camera = np.array([0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.8])
+    placements = []
+    for i in range(n_placed + 1):
+        for _ in range(200):
+            dx, dy = rng.uniform(0.02, 0.48), rng.uniform(0.02, 0.48)
+            if all((dx - px) ** 2 + (dy - py) ** 2 > 0.11 ** 2 for px, py, _ in placements):
+                break
+        placements.append((dx, dy, rng.uniform(0.0, 2 * np.pi)))
+    poses = [contact_fn(tw, th, lib[i][2], lib[i][3], 1, *placements[i])
+             for i in range(n_placed + 1)]
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    base = [(tv, tt, ident)] + [(lib[i][0], lib[i][1], poses[i]) for i in range(n_placed)]
+    target = n_placed  # library object n_placed is the enumerated one
+    depth = render_scene(k, camera, base + [(lib[target][0], lib[target][1], poses[target])])
+    obs = synth.noisy_observation(depth, k.far, 0.002, 0.05, 0.2, 1.5, rng, k.near)
+    rots = synth.vmf_quaternions(n_rot, 500.0, rng)
+    return {"name": "cfg5_sharded_480x640", "k": k, "camera": camera, "table": (tv, tt),
+            "library": lib, "base_poses": [ident] + poses[:n_placed], "target": target,
+            "gt": poses[target], "observed": obs, "extent": (0.04, 0.04, 0.02),
+            "count": counts, "rotations": rots, "noise": [(0.02, 0.003)], "window": 2,
+            "sigma_max": 0.1, "n_hyp": counts[0] * counts[1] * counts[2] * n_rot}

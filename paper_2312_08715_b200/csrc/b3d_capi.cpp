@@ -37,6 +37,10 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
 cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
                                 unsigned long long* rng_state, KStageResult* out,
                                 double* probs, cudaStream_t st);
+cudaError_t launch_sample_many(const double* x, long long n, int stride, int col,
+                               const KStageResult* r, unsigned long long* rng_state,
+                               int n_samples, double* u_buf, unsigned long long* out,
+                               cudaStream_t st);
 cudaError_t launch_select_center(const KGrid& g, const KStageResult* r, int use_sample,
                                  KPose* center_out, cudaStream_t st);
 cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_keys,
@@ -545,7 +549,8 @@ KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
 
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
                   const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
-                  const b3d_contact_grid* contact = nullptr) {
+                  const b3d_contact_grid* contact = nullptr, uint64_t first = 0,
+                  uint64_t grid_n = 0) {
   require_ready(ctx, true, true);
   check(scores != nullptr, "bad arguments");
   check(n > 0, "score_cells: no cells");
@@ -575,7 +580,8 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
     const uint64_t gn = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
     check(grid->mode == B3D_GRID_PRODUCT || nt == grid->n_rot,
           "pose grid: zip mode needs nx*ny*nz == n_rot");
-    check(gn == n, "pose grid: n does not match the grid size");
+    check(grid_n ? (gn == grid_n && first + n <= gn) : gn == n,
+          "pose grid: n does not match the grid size");
     bool h2 = false;
     p.poses = nullptr;
     p.grid.center = pose_from_c(grid->center);
@@ -591,6 +597,7 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
     host_in = host_in || h2;
   }
   p.n_hyp = (long long)n;
+  p.index0 = (long long)first;
   const int nn = ctx->lik.n_noise;
   const bool dev_scores = is_device_ptr(scores);
   const bool dev_status = status && is_device_ptr(status);
@@ -1208,6 +1215,66 @@ b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out) {
           o.ty = (rel[1] + sq[0] * uv1 + c1) + pv[1];
           o.tz = (rel[2] + sq[0] * uv2 + c2) + pv[2];
         }
+  });
+}
+
+b3d_status b3d_gpu_score_grid_range(b3d_gpu_context* ctx, int32_t mesh_id,
+                                    const b3d_pose_grid* grid, uint64_t first, uint64_t n,
+                                    double* scores, uint8_t* status) {
+  return guarded([&] {
+    check(grid != nullptr, "bad arguments");
+    const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
+    const uint64_t gn = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
+    score_common(ctx, mesh_id, nullptr, grid, n, scores, status, nullptr, first, gn);
+  });
+}
+
+b3d_status b3d_gpu_sample_many(b3d_gpu_context* ctx, const double* scores, uint64_t n,
+                               uint32_t stride, uint32_t col, uint64_t* rng_state,
+                               uint32_t n_samples, uint64_t* samples, b3d_stage_result* out) {
+  return guarded([&] {
+    check(ctx && scores && rng_state && samples && out && n > 0 && n_samples > 0,
+          "bad arguments");
+    check(stride >= 1 && col < stride, "stage_reduce: bad stride/column");
+    DeviceGuard dg(ctx->device);
+    bool host_in = false;
+    const double* d_scores = static_cast<const double*>(
+        stage_in(ctx, ctx->in_stage, scores, sizeof(double) * n * stride, &host_in));
+    const bool dev_rng = is_device_ptr(rng_state);
+    unsigned long long* d_rng = reinterpret_cast<unsigned long long*>(rng_state);
+    if (!dev_rng) {
+      cuda_check(cudaMemcpyAsync(ctx->rng.p, rng_state, 40, cudaMemcpyHostToDevice, ctx->stream),
+                 "cudaMemcpyAsync rng");
+      d_rng = ctx->rng.as<unsigned long long>();
+    }
+    KStageResult* d_out = ctx->result.as<KStageResult>();
+    ctx->out_stage.ensure(8ull * n_samples);
+    ctx->out_stage2.ensure(8ull * n_samples);
+    const bool dev_samples = is_device_ptr(samples);
+    unsigned long long* d_samples = dev_samples ? reinterpret_cast<unsigned long long*>(samples)
+                                                : ctx->out_stage2.as<unsigned long long>();
+    // reduction without a draw, then the draws
+    cuda_check(launch_stage_reduce(d_scores, (long long)n, (int)stride, (int)col, nullptr, d_out,
+                                   nullptr, ctx->stream),
+               "stage_reduce launch");
+    cuda_check(launch_sample_many(d_scores, (long long)n, (int)stride, (int)col, d_out, d_rng,
+                                  (int)n_samples, ctx->out_stage.as<double>(), d_samples,
+                                  ctx->stream),
+               "sample_many launch");
+    cuda_check(cudaMemcpyAsync(&d_out->sample, d_samples, 8, cudaMemcpyDeviceToDevice,
+                               ctx->stream),
+               "cudaMemcpyAsync");
+    cuda_check(cudaMemcpyAsync(out, d_out, sizeof(KStageResult), cudaMemcpyDefault, ctx->stream),
+               "cudaMemcpyAsync result");
+    if (!dev_samples)
+      cuda_check(cudaMemcpyAsync(samples, d_samples, 8ull * n_samples, cudaMemcpyDeviceToHost,
+                                 ctx->stream),
+                 "cudaMemcpyAsync samples");
+    if (!dev_rng)
+      cuda_check(cudaMemcpyAsync(rng_state, d_rng, 40, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync rng");
+    if (host_in || !dev_samples || !dev_rng || !is_device_ptr(out))
+      cuda_check(cudaStreamSynchronize(ctx->stream), "sample_many");
   });
 }
 

@@ -74,6 +74,7 @@ struct KParams {
   const KPose* poses;  // nullptr => grid
   KGrid grid;
   long long n_hyp;
+  long long index0;    // grid index of hypothesis 0 (shards of a large grid)
   // observation (per pixel: x, y, z, valid) + device count of valid pixels
   const float4* obs;
   const int* obs_count;

@@ -765,7 +765,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
         if (p.poses)
           hp = p.poses[hh];
         else
-          grid_pose(p.grid, hh, hp);
+          grid_pose(p.grid, p.index0 + hh, hp);
         pose_to_rt(p.w2c, hp, s_pose[lane], s_pose[lane] + 9);
       }
     }

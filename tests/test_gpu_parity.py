@@ -354,3 +354,29 @@ def test_base_scene_contact_grid_score_parity(gpu_ctx, oracle):
     s_p, _ = gpu_ctx.score_poses(mids[1 + w["target"]], poses)
     assert rel_err(s_p, s_orc).max() <= SCORE_RTOL
     gpu_ctx.set_base_scene([], [])
+
+
+def test_sample_many_matches_sequential_draws(gpu_ctx, oracle):
+    """1,000 posterior draws (cfg5's final step): each equals
+    sample_categorical with the next uniform() of the same Rng stream."""
+    rng = np.random.Generator(np.random.PCG64(21))
+    for n in (5, 4096, 200003):
+        x = rng.normal(0.0, 3.0, size=n)
+        st_g = b3d.rng_seed(77 + n)
+        samples, r = gpu_ctx.sample_many(x, 1000, st_g)
+        st_o = oracle.rng_seed(77 + n)
+        probs, _ = oracle.normalize(x)
+        want = [oracle.sample_categorical(probs, st_o) for _ in range(1000)]
+        assert list(samples.astype(np.int64)) == want
+        np.testing.assert_array_equal(st_g, st_o)
+        assert r.argmax == oracle.argmax(x) and r.sample == want[0]
+
+
+def test_score_grid_range_is_a_shard_of_the_grid(gpu_ctx, oracle):
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    grid = gpu_ctx.make_grid(w.center, w.extent, w.count, w.rotations, w.grid_mode)
+    full, _ = gpu_ctx.score_grid(mid, grid)
+    for lo, hi in ((0, 100), (100, 611), (611, 1024)):
+        part, _ = gpu_ctx.score_grid_range(mid, grid, lo, hi - lo)
+        np.testing.assert_array_equal(part, full[lo:hi])
