@@ -235,6 +235,111 @@ def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
             "triangles": int(w.triangles.shape[0])}
 
 
+def _scene_oracle_render(k, cam, inst):
+    from oracle import pyoracle as O
+    return O.render(k, inst, camera=cam)
+
+
+def run_scene_graph(ctx, b3d, configs, reps=3):
+    """configs[2]: 131,072 table-contact hypotheses of the 4th object over a
+    fixed table + 3 objects (base scene rendered once, composited per
+    hypothesis), 240x320, device time per pass (CUDA events)."""
+    import torch
+    from oracle import pyoracle as O
+    w = configs.cfg3(_scene_oracle_render, b3d.voxel_to_mesh, O.box_mesh, O.contact_to_pose)
+    ctx.set_camera(b3d.Intrinsics(*w["k"].as_tuple()), w["camera"])
+    tv, tt = w["table"][0], w["table"][1]
+    mids = [ctx.upload_mesh(tv, tt)] + [ctx.upload_mesh(o[0], o[1]) for o in w["objects"]]
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    ctx.set_base_scene([mids[0]] + [mids[1 + i] for i in w["base"]],
+                       [ident] + [w["poses"][i] for i in w["base"]])
+    ctx.set_observation(torch.from_numpy(w["observed"]).cuda())
+    ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    o = w["objects"][w["target"]]
+    g = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, w["contact"]["count"])
+    n = g.n
+    d_scores = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
+    d_status = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    ctx.score_contact_grid(mids[1 + w["target"]], g, d_scores, d_status)  # warm-up + terms
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    times = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ctx.score_contact_grid(mids[1 + w["target"]], g, d_scores, d_status)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    best = int(torch.argmax(d_scores[:, 0]).item())
+    placements = w["placements"][w["target"]]
+    ctx.set_base_scene([], [])
+    return {"workload": "configs[2]: table + 3 fixed objects (base scene), 4th object over "
+                        "16x16 (x,y) x 512 yaw contact cells, 240x320",
+            "hypotheses": n, "ms": 1e3 * statistics.median(times),
+            "value": n / statistics.median(times), "unit": UNIT,
+            "triangles": int(o[1].shape[0]), "argmax": best,
+            "true_contact": [round(v, 4) for v in placements]}
+
+
+def run_sharded(ctx, b3d, configs, world, rank, reps=1):
+    """configs[4]: 1,048,576 6-DoF hypotheses of one object over a 10-object
+    base scene at 480x640, sharded evenly over the ranks; NCCL all-gather of
+    the scores (8 MiB), global argmax / logsumexp and 1,000 posterior samples
+    on every rank.  Device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+    from oracle import pyoracle as O
+    from paper_2312_08715_b200.shard import gather_scores, shard_range
+    w = configs.cfg5(_scene_oracle_render, b3d.voxel_to_mesh, O.box_mesh, O.contact_to_pose)
+    ctx.set_camera(b3d.Intrinsics(*w["k"].as_tuple()), w["camera"])
+    tv, tt = w["table"]
+    mids = [ctx.upload_mesh(tv, tt)] + [ctx.upload_mesh(l[0], l[1]) for l in w["library"]]
+    n_placed = len(w["base_poses"]) - 1
+    ctx.set_base_scene([mids[0]] + [mids[1 + i] for i in range(n_placed)], w["base_poses"])
+    ctx.set_observation(torch.from_numpy(w["observed"]).cuda())
+    ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    d_rot = torch.from_numpy(w["rotations"]).cuda()
+    grid = ctx.make_grid(w["gt"], w["extent"], w["count"], d_rot, b3d.GRID_PRODUCT)
+    n = w["n_hyp"]
+    lo, hi = shard_range(n, rank, world)
+    d_local = torch.zeros((hi - lo, 1), dtype=torch.float64, device="cuda")
+    d_samples = torch.zeros(1000, dtype=torch.int64, device="cuda")
+    st = torch.from_numpy(b3d.rng_seed(5).view(np.int64)).cuda()
+    stream = torch.cuda.current_stream()
+    mid = mids[1 + w["target"]]
+
+    def once():
+        ctx.score_grid_range(mid, grid, lo, hi - lo, d_local, None)
+        allv = gather_scores(d_local, n, world)
+        return ctx.sample_many(allv, 1000, st, n=n, samples=d_samples)
+
+    once()  # warm-up (builds the base-scene likelihood terms)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    times = []
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, r = once()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        times.append(e0.elapsed_time(e1) * 1e-3)
+    t = max(times)
+    if world > 1:
+        tt_ = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
+        t = float(tt_.item())
+    ctx.set_base_scene([], [])
+    return {"workload": "configs[4]: 10-object base scene, 1,048,576 6-DoF hypotheses of a "
+                        "new object, 480x640, sharded over ranks, NCCL score all-gather, global "
+                        "argmax/logsumexp + 1,000 samples",
+            "hypotheses": n, "n_gpus": world, "scaling": "strong", "s": t, "value": n / t,
+            "unit": UNIT, "triangles": int(w["library"][w["target"]][1].shape[0]),
+            "argmax": int(r.argmax), "logsumexp": r.logsumexp}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -367,6 +472,9 @@ def main():
         t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, e2e_total = t.tolist()
+    sharded = None
+    if not args.no_extra:
+        sharded = run_sharded(ctx, b3d, configs, world, rank)
 
     if rank == 0:
         value = args.steps * n_all / (total_ms * 1e-3)
@@ -390,6 +498,7 @@ def main():
         if not args.no_extra:
             extra["coarse_to_fine"] = run_coarse_to_fine(ctx, b3d, configs, render_fn)
             extra["tracking"] = run_tracking(ctx, b3d, configs, args.tracking_frames, render_fn)
+            extra["scene_graph"] = run_scene_graph(ctx, b3d, configs)
         roof = None
         if cnt is not None and "fp64_nofma_ops" in peaks:
             ops = _ops_per_hyp(cnt, 1, 1, BATCH)
@@ -422,6 +531,8 @@ def main():
             "cpu_baseline": cpu,
         }
         line.update(extra)
+        if sharded is not None:
+            line["sharded_enumeration"] = sharded
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:
