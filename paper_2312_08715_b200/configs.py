@@ -213,9 +213,10 @@ def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
     fx=fy=400 (cfg1's field of view), cx=160, cy=120.  Ground truth: seeded
     random walk, 1 cm translation and 5 degrees rotation per frame from
     (0, 0, 0.6); observations with N(0, 2 mm) noise and 5% outliers.  Per
-    frame two stages of 16x16x4 translations x 8 rotations (8,192 each)
-    centred on the previous estimate, MAP (argmax) selection; likelihood
-    r = 5 mm, 5x5 window, outlier_prob 0.05."""
+    frame two stages of 8,192 hypotheses centred on the previous estimate,
+    MAP (argmax) selection; likelihood
+    r = 5 mm, 5x5 window, outlier_prob 0.05.  Per stage 8 x 8 x 4
+    translations x 32 rotations (3x3x3 rotation-vector lattice + 5 vMF)."""
     rng = np.random.Generator(np.random.PCG64(4000 + seed))
     vox = synth.eden_blob(2000, seed)
     verts, tris = make_mesh(vox, mesh_fn)
@@ -232,12 +233,15 @@ def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
         gts.append(pose)
         depth = render_fn(k, verts, tris, pose)
         frames.append(synth.noisy_observation(depth, k.far, 0.002, 0.05, 0.2, 1.5, rng, k.near))
+    # 8 x 8 x 4 translations x 32 rotations (a 3x3x3 rotation-vector lattice
+    # plus 5 vMF draws) per stage: coarse (+-1.5 cm, 6 deg) then fine
+    # (+-3 mm, 2 deg)
     stages = [
-        {"extent": (0.02, 0.02, 0.02), "count": (16, 16, 4),
-         "rotations": np.vstack([[1.0, 0, 0, 0], synth.vmf_quaternions(7, 150.0, rng)]),
+        {"extent": (0.015, 0.015, 0.01), "count": (8, 8, 4),
+         "rotations": synth.rotation_lattice(np.deg2rad(6.0), 5, 300.0, rng),
          "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
-        {"extent": (0.004, 0.004, 0.004), "count": (16, 16, 4),
-         "rotations": np.vstack([[1.0, 0, 0, 0], synth.vmf_quaternions(7, 3000.0, rng)]),
+        {"extent": (0.003, 0.003, 0.003), "count": (8, 8, 4),
+         "rotations": synth.rotation_lattice(np.deg2rad(2.0), 5, 5000.0, rng),
          "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
     ]
     return {"k": k, "vertices": verts, "triangles": tris, "voxels": vox, "gt": np.array(gts),

@@ -116,3 +116,23 @@ def noisy_observation(depth: np.ndarray, far: float, sigma: float, outlier_frac:
     obs = np.clip(obs, max(near, 1e-6), far).astype(np.float32)
     obs[obs >= far_f] = far_f
     return obs
+
+
+def rotation_lattice(step_rad: float, extra: int = 0, kappa: float = 0.0,
+                     rng: np.random.Generator = None) -> np.ndarray:
+    """Rotation perturbations on a 3 x 3 x 3 lattice of rotation vectors
+    step * (i, j, k), i, j, k in {-1, 0, 1} (27 quaternions, identity first),
+    optionally followed by `extra` vMF(kappa) draws."""
+    qs = [np.array([1.0, 0.0, 0.0, 0.0])]
+    for i in (-1, 0, 1):
+        for j in (-1, 0, 1):
+            for k in (-1, 0, 1):
+                if i == j == k == 0:
+                    continue
+                r = step_rad * np.array([i, j, k], dtype=np.float64)
+                a = np.linalg.norm(r)
+                qs.append(np.concatenate([[np.cos(a / 2)], np.sin(a / 2) * r / a]))
+    out = np.array(qs)
+    if extra:
+        out = np.vstack([out, vmf_quaternions(extra, kappa, rng)])
+    return out

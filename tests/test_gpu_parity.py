@@ -380,3 +380,31 @@ def test_score_grid_range_is_a_shard_of_the_grid(gpu_ctx, oracle):
     for lo, hi in ((0, 100), (100, 611), (611, 1024)):
         part, _ = gpu_ctx.score_grid_range(mid, grid, lo, hi - lo)
         np.testing.assert_array_equal(part, full[lo:hi])
+
+
+def test_tracking_frames_match_oracle(gpu_ctx, oracle):
+    """cfg4 tracking: for the first frames, every stage's MAP hypothesis from
+    the device chain equals the oracle's argmax over oracle scores (or ties it
+    within the score tolerance), and the scores agree within 1e-4."""
+    from helpers import b3d_intr
+    rf = lambda k, v, t, p: oracle.render(k, [(v, t, p)])
+    tr = configs.cfg4(rf, oracle.voxel_to_mesh, seed=0, n_frames=3)
+    gpu_ctx.set_camera(b3d_intr(tr["k"]))
+    mid = gpu_ctx.upload_mesh(tr["vertices"], tr["triangles"])
+    st0 = tr["stages"][0]
+    gpu_ctx.set_likelihood([st0["noise"]], 0.1, st0["window"])
+    est = tr["gt"][0].copy()
+    for f in (1, 2):
+        gpu_ctx.set_observation(tr["frames"][f])
+        res, centers = gpu_ctx.coarse_to_fine(mid, est, tr["stages"])
+        for s, g in enumerate(tr["stages"]):
+            poses = configs.grid_poses(centers[s], g["extent"], g["count"], g["rotations"], 0)
+            s_orc, _ = oracle.score_poses(tr["k"], tr["frames"][f], tr["vertices"],
+                                          tr["triangles"], poses, [g["noise"]], 0.1, g["window"])
+            a_orc = oracle.argmax(s_orc[:, 0])
+            a_gpu = res[s].argmax
+            assert abs(res[s].max_score - s_orc[a_orc, 0]) <= SCORE_RTOL * abs(s_orc[a_orc, 0])
+            if a_gpu != a_orc:
+                assert abs(s_orc[a_gpu, 0] - s_orc[a_orc, 0]) <= SCORE_RTOL * abs(s_orc[a_orc, 0])
+            np.testing.assert_array_equal(centers[s + 1], poses[a_gpu])
+        est = centers[-1]
