@@ -195,9 +195,35 @@ struct WarpRec {
   uint32_t ia[32], ib[32], ic[32];  // vertex ids after the orientation swap
   uint32_t tri[32];                 // triangle index (draw order)
   int uv0[32];                      // u_min | v_min << 16
-  int bwf[32];                      // bbox width | edge flags << 16
-  float inv_bw[32];
+  int fl[32];                       // edge flags (canonical | top-left bits)
+  uint32_t cov[32];                 // covered pixels of the 3x3 bbox tile
 };
+
+// Coverage of one edge over a 3x3 pixel tile at (u0, v0): the reference's
+// edge value dx*(py - oy) - dy*(px - ox) (renderer.cpp:32-34, canonical
+// origin) factored into 3 row products and 3 column products -- the same
+// two fp64 products and difference per pixel, so bitwise the same values --
+// and the top-left rule (renderer.cpp:39-43).  Returns a 9-bit mask.
+__device__ __forceinline__ uint32_t tile_edge_mask(double2 a, double2 b, bool canon, bool tie,
+                                                   int u0, int v0) {
+  const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+  const double dx = b.x - a.x, dy = b.y - a.y;
+  double A[3], B[3];
+#pragma unroll
+  for (int j = 0; j < 3; ++j) A[j] = dx * ((double)(v0 + j) - oy);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) B[i] = dy * ((double)(u0 + i) - ox);
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < 3; ++j)
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      const double e = A[j] - B[i];
+      const bool c = e > 0 || (tie && e == 0);
+      m |= (uint32_t)c << (3 * j + i);
+    }
+  return m;
+}
 
 // Edge flags: bit e = canonical origin is the edge's first vertex
 // (renderer.cpp:47), bit 3+e = pixels exactly on the edge are covered
@@ -407,148 +433,119 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   if (tid == 0) *s_ndef = 0;
   __syncthreads();
 
-  // ---- C: raster.  C1: lane = triangle (mesh order): integer bbox reject,
-  // orientation, edge flags and 1/area into the warp's records.  C2: the
-  // warp's bbox pixels are dealt out one per lane (owner found by a 5-step
-  // shuffle search over the exclusive scan of pixel counts), so lanes stay
-  // busy whatever the per-triangle pixel counts are.
-  //
-  // With p.cull set, two passes: each pixel's final key is the minimum over
-  // all fragments of (fp32 depth bits[, draw index]) -- exactly the
-  // reference's strict-less test in draw order (renderer.cpp:99-100) -- so
-  // triangles may be processed in any order and one that provably cannot
-  // lower any key may be skipped.  Pass 0 rasterizes front-facing triangles
-  // and defers back-facing ones; pass 1 skips a deferred triangle when its
-  // nearest possible depth (1/max vertex 1/z, minus a 1e-9 relative margin
-  // for interpolation rounding, rounded down) is strictly behind every
-  // current depth in its bbox, and rasterizes it exactly otherwise.
+  // ---- C: raster.  Lane = triangle (mesh order): integer bbox reject,
+  // orientation swap (renderer.cpp:63-69), canonical edges; then the
+  // coverage of its bbox pixels in one straight-line pass over a 3x3 tile
+  // (voxel faces at these scales cover 1-6 bbox pixels; larger bboxes take
+  // the per-pixel loop).  Covered pixels -- ~0.6 per triangle -- are dealt
+  // one per lane (owner found by a 5-step shuffle search over the exclusive
+  // scan of coverage counts) for the perspective 1/z, the fp32 round and the
+  // strict-less z-test (renderer.cpp:94-100) with every lane busy.
   if (!hc.empty_region || hc.clip) {
     WarpRec& wr = wrec[warp];
-    const int n_pass = p.cull ? 2 : 1;
-    for (int pass = 0; pass < n_pass; ++pass) {
-      if (pass == 1) __syncthreads();
-      const int n_items = pass == 0 ? p.nt : *s_ndef;
-      for (int base = warp * 32; base < n_items; base += kThreads) {
-        __syncwarp();
-        const int ti = base + lane < n_items
-                           ? (pass == 0 ? base + lane : (int)def_list[base + lane])
-                           : p.nt;
-        int cnt = 0;
-        bool deferred = false;
-        if (ti < p.nt) {
-          const uint4 tri = __ldg(p.tris + ti);
-          uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
-          const short4 A = vs.bb[ia], B = vs.bb[ib], C = vs.bb[ic];
-          if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
-            raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
-          } else {
-            const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
-            const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
-            if (u_max != kOvf && v_max != kOvf && u_min <= u_max && v_min <= v_max) {
-              const double2 PA = vs.uv[ia];
-              double2 PB = vs.uv[ib], PC = vs.uv[ic];
-              double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
-              bool skip = area2 == 0;
-              if (!skip && p.cull && pass == 0 && area2 > 0) {  // back-facing (y down)
-                deferred = true;
-                skip = true;
+    for (int base = warp * 32; base < p.nt; base += kThreads) {
+      __syncwarp();
+      const int ti = base + lane;
+      uint32_t cov = 0;
+      if (ti < p.nt) {
+        const uint4 tri = __ldg(p.tris + ti);
+        uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
+        const short4 A = vs.bb[ia], B = vs.bb[ib], C = vs.bb[ic];
+        if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
+          raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
+        } else {
+          const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
+          const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
+          if (u_max != kOvf && v_max != kOvf && u_min <= u_max && v_min <= v_max) {
+            const double2 PA = vs.uv[ia];
+            double2 PB = vs.uv[ib], PC = vs.uv[ic];
+            double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
+            if (area2 != 0) {
+              if (area2 < 0) {
+                const double2 T = PB;
+                PB = PC;
+                PC = T;
+                const uint32_t tt = ib;
+                ib = ic;
+                ic = tt;
+                area2 = -area2;
               }
-              if (!skip && pass == 1) {  // conservative occlusion test
-                const double izm = fmax(fmax(vs.iz[ia], vs.iz[ib]), vs.iz[ic]);
-                const float zlo = __double2float_rd((1.0 / izm) * (1.0 - 1e-9));
-                float zcur = 0.f;
-                for (int pv = v_min; pv <= v_max; ++pv) {
-                  const Key* row = zb + (pv - rg.oy) * rg.rw - rg.ox;
-                  for (int pu = u_min; pu <= u_max; ++pu)
-                    zcur = fmaxf(zcur, __uint_as_float((unsigned int)(
-                                           kIds ? ((unsigned long long)row[pu] >> 32)
-                                                : (unsigned long long)row[pu])));
+              const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
+              const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+              const int bw = u_max - u_min + 1, bh = v_max - v_min + 1;
+              if (bw <= 3 && bh <= 3) {
+                const uint32_t colm = (1u << bw) - 1u;
+                uint32_t valid = colm;
+                if (bh > 1) valid |= colm << 3;
+                if (bh > 2) valid |= colm << 6;
+                cov = valid & tile_edge_mask(PA, PB, fl & 1, fl & 8, u_min, v_min) &
+                      tile_edge_mask(PB, PC, fl & 2, fl & 16, u_min, v_min) &
+                      tile_edge_mask(PC, PA, fl & 4, fl & 32, u_min, v_min);
+                if (cov) {
+                  wr.inv_area2[lane] = 1.0 / area2;
+                  wr.tri[lane] = (uint32_t)ti;
+                  wr.ia[lane] = ia;
+                  wr.ib[lane] = ib;
+                  wr.ic[lane] = ic;
+                  wr.uv0[lane] = u_min | (v_min << 16);
+                  wr.fl[lane] = fl;
+                  wr.cov[lane] = cov;
                 }
-                skip = zlo > zcur;
-              }
-              if (!skip) {
-                if (area2 < 0) {  // renderer.cpp:65-69
-                  const double2 T = PB;
-                  PB = PC;
-                  PC = T;
-                  const uint32_t tt = ib;
-                  ib = ic;
-                  ic = tt;
-                  area2 = -area2;
-                }
-                const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
-                const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
-                const int bw = u_max - u_min + 1;
-                wr.inv_area2[lane] = 1.0 / area2;
-                wr.tri[lane] = (uint32_t)ti;
-                wr.ia[lane] = ia;
-                wr.ib[lane] = ib;
-                wr.ic[lane] = ic;
-                wr.uv0[lane] = u_min | (v_min << 16);
-                wr.bwf[lane] = bw | (fl << 16);
-                wr.inv_bw[lane] = 1.0f / (float)bw;
-                cnt = bw * (v_max - v_min + 1);
+              } else {  // large bbox: the reference's per-pixel loop
+                raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz[ia]},
+                                     SV{PB.x, PB.y, vs.iz[ib]}, SV{PC.x, PC.y, vs.iz[ic]},
+                                     u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
               }
             }
           }
         }
-        if (p.cull && pass == 0) {  // append deferred triangles to the pass-1 list
-          const unsigned m = __ballot_sync(0xffffffffu, deferred);
-          int pos0 = 0;
-          if (lane == 0 && m) pos0 = atomicAdd(s_ndef, __popc(m));
-          pos0 = __shfl_sync(0xffffffffu, pos0, 0);
-          if (deferred) def_list[pos0 + __popc(m & ((1u << lane) - 1u))] = (uint32_t)ti;
-        }
-        int incl = cnt;
+      }
+      const int cnt = __popc(cov);
+      int incl = cnt;
 #pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const int y = __shfl_up_sync(0xffffffffu, incl, o);
-          if (lane >= o) incl += y;
-        }
-        const int start = incl - cnt;
-        const int total = __shfl_sync(0xffffffffu, incl, 31);
-        __syncwarp();
-        for (int c0 = 0; c0 < total; c0 += 32) {
-          const int item = c0 + lane;
-          int own = 0;  // last lane whose start <= item (never a zero-count lane)
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      const int start = incl - cnt;
+      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      __syncwarp();
+      for (int c0 = 0; c0 < total; c0 += 32) {
+        const int item = c0 + lane;
+        int own = 0;  // last lane whose start <= item (never a zero-count lane)
 #pragma unroll
-          for (int step = 16; step > 0; step >>= 1) {
-            const int sp = __shfl_sync(0xffffffffu, start, own + step);
-            if (sp <= item) own += step;
-          }
-          const int st = __shfl_sync(0xffffffffu, start, own);
-          if (item < total) {
-            const int k = item - st;
-            const int bwf = wr.bwf[own], uv0 = wr.uv0[own];
-            const int bw = bwf & 0xffff, fl = bwf >> 16;
-            const int dv = (int)(((float)k + 0.5f) * wr.inv_bw[own]);
-            const int pu = (uv0 & 0xffff) + (k - dv * bw);
-            const int pv = (uv0 >> 16) + dv;
-            const uint32_t ia = wr.ia[own], ib = wr.ib[own], ic = wr.ic[own];
-            const double2 a = vs.uv[ia], b = vs.uv[ib], c = vs.uv[ic];
-            const double px = pu, py = pv;
-            const double e_ab = edge_at(a, b, fl & 1, px, py);
-            const double e_bc = edge_at(b, c, fl & 2, px, py);
-            const double e_ca = edge_at(c, a, fl & 4, px, py);
-            if (edge_covers(e_ab, fl & 8) && edge_covers(e_bc, fl & 16) &&
-                edge_covers(e_ca, fl & 32)) {
-              // renderer.cpp:94-100
-              const double inv_z =
-                  (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * wr.inv_area2[own];
-              if (inv_z > 0) {
-                const double z = 1.0 / inv_z;
-                if (!(z < p.near_lim || z > p.far_m)) {
-                  const float zf = __double2float_rn(z);
-                  if (zf < p.far_f) {
-                    Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
-                    if (kIds)
-                      zmin((unsigned long long*)cell,
-                           ((unsigned long long)__float_as_uint(zf) << 32) |
-                               (unsigned long long)(p.draw_base + wr.tri[own]));
-                    else
-                      zmin((unsigned int*)cell, __float_as_uint(zf));
-                  }
-                }
+        for (int step = 16; step > 0; step >>= 1) {
+          const int sp = __shfl_sync(0xffffffffu, start, own + step);
+          if (sp <= item) own += step;
+        }
+        const int st = __shfl_sync(0xffffffffu, start, own);
+        if (item < total) {
+          uint32_t m = wr.cov[own];
+          for (int q = item - st; q > 0; --q) m &= m - 1;  // k-th covered pixel
+          const int bit = __ffs(m) - 1;
+          const int uv0 = wr.uv0[own], fl = wr.fl[own];
+          const int pu = (uv0 & 0xffff) + bit % 3, pv = (uv0 >> 16) + bit / 3;
+          const uint32_t ia = wr.ia[own], ib = wr.ib[own], ic = wr.ic[own];
+          const double2 A = vs.uv[ia], B = vs.uv[ib], C = vs.uv[ic];
+          const double px = pu, py = pv;
+          const double e_ab = edge_at(A, B, fl & 1, px, py);
+          const double e_bc = edge_at(B, C, fl & 2, px, py);
+          const double e_ca = edge_at(C, A, fl & 4, px, py);
+          // renderer.cpp:94-100
+          const double inv_z =
+              (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * wr.inv_area2[own];
+          if (inv_z > 0) {
+            const double z = 1.0 / inv_z;
+            if (!(z < p.near_lim || z > p.far_m)) {
+              const float zf = __double2float_rn(z);
+              if (zf < p.far_f) {
+                Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+                if (kIds)
+                  zmin((unsigned long long*)cell,
+                       ((unsigned long long)__float_as_uint(zf) << 32) |
+                           (unsigned long long)(p.draw_base + wr.tri[own]));
+                else
+                  zmin((unsigned int*)cell, __float_as_uint(zf));
               }
             }
           }
