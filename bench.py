@@ -441,17 +441,15 @@ def main():
     h_rng = b3d.rng_seed(7)
 
     def e2e_step():
-        ctx.set_observation(h_obs)
+        ctx.set_observation(h_obs)  # pinned: stream-ordered upload
+        if world == 1:  # one boundary call: upload poses, score, reduce, read back
+            return ctx.enumerate_poses(mid, h_poses, rng_state=h_rng, scores=h_scores)
         ctx.score_poses(mid, h_poses, h_scores, h_status)
-        if world > 1:
-            t = torch.from_numpy(h_scores).to(dev)
-            g = torch.empty((n_all, 1), dtype=torch.float64, device=dev)
-            dist.all_gather_into_tensor(g, t)
-            h_all[:] = g.cpu().numpy()
-            src = h_all
-        else:
-            src = h_scores
-        return ctx.stage_reduce(src, n=n_all, rng_state=h_rng)
+        t = torch.from_numpy(h_scores).to(dev)
+        g = torch.empty((n_all, 1), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(g, t)
+        h_all[:] = g.cpu().numpy()
+        return ctx.stage_reduce(h_all, n=n_all, rng_state=h_rng)
 
     for _ in range(args.warmup):
         e2e_step()
@@ -521,7 +519,7 @@ def main():
                        "vertices": int(w.vertices.shape[0]),
                        "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"dp{world} (hypothesis shards, NCCL score all-gather)"},
-            "gpu_launches": 2 * args.steps,
+            "gpu_launches": 2 * args.steps,  # render_score + stage_reduce per step
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 8 * n_all + 40),
                     "d2h_bytes_per_step": int(h_scores.nbytes + h_status.nbytes + 64 + 40),

@@ -21,7 +21,9 @@
  * device pointer (detected with cudaPointerGetAttributes).  A call whose
  * pointers are all device pointers is asynchronous on the context's stream;
  * otherwise the call copies through the stream and returns when the results
- * are in the caller's buffers.
+ * are in the caller's buffers.  Inputs in page-locked (pinned) host memory
+ * are read in stream order: such a buffer must stay unchanged until the next
+ * call that returns results to the host (or b3d_gpu_synchronize).
  */
 #ifndef B3D_B200_H
 #define B3D_B200_H
@@ -234,6 +236,15 @@ B3D_API b3d_status b3d_gpu_sample_many(b3d_gpu_context* ctx, const double* score
                                        uint32_t stride, uint32_t col, uint64_t* rng_state,
                                        uint32_t n_samples, uint64_t* samples,
                                        b3d_stage_result* out);
+
+/* One enumeration stage through the host boundary in a single call:
+ * score-many of poses (model-to-world) + the stage reduction of noise entry 0
+ * (argmax, logsumexp, one draw when rng_state != NULL); optional scores
+ * (n x n_noise).  One synchronisation per call. */
+B3D_API b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
+                                           const b3d_pose* poses, uint64_t n,
+                                           uint64_t* rng_state, b3d_stage_result* out,
+                                           double* scores);
 
 /* Score hypotheses [first, first + n) of a device pose grid (one rank's
  * shard of a large enumeration); scores[i] is hypothesis

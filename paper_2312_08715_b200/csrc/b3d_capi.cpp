@@ -156,6 +156,18 @@ struct DevBuf {
   }
 };
 
+// Page-locked host memory: copies from it are stream-ordered and need no
+// synchronisation before the call returns.
+bool is_pinned_host(const void* ptr) {
+  if (!ptr) return false;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 bool is_device_ptr(const void* ptr) {
   if (!ptr) return false;
   cudaPointerAttributes a;
@@ -826,7 +838,10 @@ b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth) {
                                   (float)(1.0 / k.fy), ctx->obs_pts.as<float4>(),
                                   ctx->obs_count.as<int>(), ctx->stream),
                "obs_prepare launch");
-    if (host) cuda_check(cudaStreamSynchronize(ctx->stream), "set_observation");
+    // pageable host memory must be consumed before returning; pinned host
+    // memory is read in stream order (see b3d_b200.h)
+    if (host && !is_pinned_host(depth))
+      cuda_check(cudaStreamSynchronize(ctx->stream), "set_observation");
     ctx->has_obs = true;
     ++ctx->obs_version;
   });
@@ -1215,6 +1230,63 @@ b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out) {
           o.ty = (rel[1] + sq[0] * uv1 + c1) + pv[1];
           o.tz = (rel[2] + sq[0] * uv2 + c2) + pv[2];
         }
+  });
+}
+
+b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
+                                   const b3d_pose* poses, uint64_t n, uint64_t* rng_state,
+                                   b3d_stage_result* out, double* scores) {
+  return guarded([&] {
+    require_ready(ctx, true, true);
+    check(poses && out && n > 0, "bad arguments");
+    DeviceGuard dg(ctx->device);
+    const Mesh& m = get_mesh(ctx, mesh_id);
+    KParams p = base_params(ctx, m);
+    bool host_in = false;
+    p.poses = static_cast<const KPose*>(
+        stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
+    p.n_hyp = (long long)n;
+    const int nn = ctx->lik.n_noise;
+    ctx->c2f_scores.ensure(sizeof(double) * n * nn);
+    p.scores = ctx->c2f_scores.as<double>();
+    p.status = nullptr;
+    attach_base(ctx, p);
+    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n);
+    p.zscratch = ctx->zscratch.as<unsigned long long>();
+    p.vscratch = ctx->vscratch.as<double>();
+    p.vcap = lp.vcap;
+    p.zcap = lp.zcap;
+    p.zstride = lp.zstride;
+    cuda_check(launch_render_score<false, true, false>(p, lp.grid, lp.smem, ctx->stream),
+               "render_score launch");
+    unsigned long long* d_rng = nullptr;
+    const bool dev_rng = rng_state && is_device_ptr(rng_state);
+    if (rng_state) {
+      if (dev_rng) {
+        d_rng = reinterpret_cast<unsigned long long*>(rng_state);
+      } else {
+        cuda_check(cudaMemcpyAsync(ctx->rng.p, rng_state, 40, cudaMemcpyHostToDevice,
+                                   ctx->stream),
+                   "cudaMemcpyAsync rng");
+        d_rng = ctx->rng.as<unsigned long long>();
+      }
+    }
+    KStageResult* d_out = ctx->result.as<KStageResult>();
+    cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
+                                   ctx->stream),
+               "stage_reduce launch");
+    cuda_check(cudaMemcpyAsync(out, d_out, sizeof(KStageResult), cudaMemcpyDefault, ctx->stream),
+               "cudaMemcpyAsync result");
+    if (scores)
+      cuda_check(cudaMemcpyAsync(scores, p.scores, sizeof(double) * n * nn, cudaMemcpyDefault,
+                                 ctx->stream),
+                 "cudaMemcpyAsync scores");
+    if (rng_state && !dev_rng)
+      cuda_check(cudaMemcpyAsync(rng_state, d_rng, 40, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync rng");
+    const bool all_dev = is_device_ptr(out) && (!scores || is_device_ptr(scores)) &&
+                         (!rng_state || dev_rng) && !host_in;
+    if (!all_dev) cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
   });
 }
 

@@ -408,3 +408,19 @@ def test_tracking_frames_match_oracle(gpu_ctx, oracle):
                 assert abs(s_orc[a_gpu, 0] - s_orc[a_orc, 0]) <= SCORE_RTOL * abs(s_orc[a_orc, 0])
             np.testing.assert_array_equal(centers[s + 1], poses[a_gpu])
         est = centers[-1]
+
+
+def test_enumerate_poses_one_call(gpu_ctx, oracle):
+    """b3d_gpu_enumerate_poses == score_poses + stage_reduce."""
+    import torch
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    poses = torch.from_numpy(w.grid_poses()).pin_memory().numpy()
+    st1, st2 = b3d.rng_seed(3), b3d.rng_seed(3)
+    scores = np.zeros((poses.shape[0], 1))
+    r1 = gpu_ctx.enumerate_poses(mid, poses, rng_state=st1, scores=scores)
+    s2, _ = gpu_ctx.score_poses(mid, poses)
+    r2 = gpu_ctx.stage_reduce(s2[:, 0], rng_state=st2)
+    np.testing.assert_array_equal(scores, s2)
+    assert (r1.argmax, r1.sample, r1.logsumexp) == (r2.argmax, r2.sample, r2.logsumexp)
+    np.testing.assert_array_equal(st1, st2)
