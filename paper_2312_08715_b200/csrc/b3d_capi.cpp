@@ -202,7 +202,6 @@ struct b3d_gpu_context {
   KLik lik{};
   double sigma_max = 0.1;
   int prefactor = B3D_PREFACTOR_PRINTED;
-  int cull = 0;  // B3D_OCCLUSION_CULL=1: exact two-pass back-face occlusion culling
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
@@ -371,7 +370,6 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.lik = ctx->lik;
   p.zscratch = ctx->zscratch.as<unsigned long long>();
   p.vscratch = ctx->vscratch.as<double>();
-  p.cull = ctx->cull;
   return p;
 }
 
@@ -747,7 +745,6 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
                "cudaDeviceGetAttribute");
     cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
-    if (const char* env = std::getenv("B3D_OCCLUSION_CULL")) c->cull = std::atoi(env) != 0;
     c->obs_count.ensure(sizeof(int));
     c->result.ensure(sizeof(KStageResult));
     c->rng.ensure(5 * sizeof(uint64_t));

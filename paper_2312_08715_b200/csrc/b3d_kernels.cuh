@@ -69,7 +69,6 @@ struct KParams {
   const uint4* tris;  // (i0, i1, i2, 0) per triangle
   int nv, nt;
   uint32_t draw_base;
-  int cull;  // two-pass conservative occlusion culling of back faces (exact)
   // hypotheses
   const KPose* poses;  // nullptr => grid
   KGrid grid;

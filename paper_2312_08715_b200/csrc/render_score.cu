@@ -403,7 +403,7 @@ struct HypCtx {
 template <bool kIds, bool kScore, bool kOut, typename VS, typename Key>
 __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
                                          const VS& vs, WarpRec* const wrec,
-                                         uint32_t* const def_list, int* s_ndef,
+
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h) {
@@ -430,7 +430,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   } else {
     for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
   }
-  if (tid == 0) *s_ndef = 0;
   __syncthreads();
 
   // ---- C: raster.  Lane = triangle (mesh order): integer bbox reject,
@@ -728,12 +727,11 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
   __shared__ int s_redi[kWarps][kMaxNoise + 1];
   __shared__ double s_coef[kMaxNoise];
   __shared__ int s_count;
-  __shared__ int s_ndef;
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
   // dynamic shared memory: [(u,v) | 1/z | packed bbox] x vcap vertices,
-  // per-warp triangle records, deferred-triangle list, region z-buffer
+  // per-warp triangle records, region z-buffer
   double* const sv_s = reinterpret_cast<double*>(smem_raw);
   VertexCache vs;
   if (kVS) {
@@ -748,8 +746,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
   }
   const int vcap = kVS ? p.vcap : 0;
   WarpRec* const wrec = reinterpret_cast<WarpRec*>(sv_s + 4 * (size_t)vcap);
-  uint32_t* const def_list = reinterpret_cast<uint32_t*>(wrec + kWarps);
-  Key* const zb_s = reinterpret_cast<Key*>(def_list + ((p.nt + 3) & ~3));
+  Key* const zb_s = reinterpret_cast<Key*>(wrec + kWarps);
 
   int kk = 0;  // hypotheses this CTA has processed
   for (long long h = blockIdx.x; h < p.n_hyp; h += gridDim.x, ++kk) {
@@ -842,12 +839,12 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wrec, def_list, &s_ndef, &s_count, s_coef,
+      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wrec, &s_count, s_coef,
                                    s_red, s_redi, h);
     else
       hyp_body<kIds, kScore, kOut>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wrec,
-          def_list, &s_ndef, &s_count, s_coef, s_red, s_redi, h);
+          &s_count, s_coef, s_red, s_redi, h);
     __syncthreads();
   }
 }
@@ -1015,8 +1012,6 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
 
 int render_score_threads() { return kThreads; }
 
-size_t render_score_staging_bytes(int nt) {
-  return sizeof(WarpRec) * kWarps + 4 * (size_t)((nt + 3) & ~3);
-}
+size_t render_score_staging_bytes(int nt) { return (void)nt, sizeof(WarpRec) * kWarps; }
 
 }  // namespace b3d200

@@ -424,3 +424,32 @@ def test_enumerate_poses_one_call(gpu_ctx, oracle):
     np.testing.assert_array_equal(scores, s2)
     assert (r1.argmax, r1.sample, r1.logsumexp) == (r2.argmax, r2.sample, r2.logsumexp)
     np.testing.assert_array_equal(st1, st2)
+
+
+def test_base_scene_with_near_clipping_and_scratch(gpu_ctx, oracle):
+    """Base scene + hypotheses crossing z = near: full-image regions that
+    spill to the global z-buffer scratch, composited over the base keys."""
+    w = _cfg3(oracle)
+    mids, base_inst = _setup_cfg3(gpu_ctx, oracle, w)
+    o = w["objects"][w["target"]]
+    rng = np.random.Generator(np.random.PCG64(8))
+    poses = []
+    for _ in range(6):  # world poses close to the camera (camera at z = 0.7 looking down)
+        q = synth.uniform_quaternion(rng)
+        poses.append([q[0], q[1], q[2], q[3], rng.uniform(-0.02, 0.02), rng.uniform(-0.02, 0.02),
+                      rng.uniform(0.66, 0.69)])
+    poses = np.array(poses)
+    depth, ids = gpu_ctx.render_poses(mids[1 + w["target"]], poses)
+    for i in range(poses.shape[0]):
+        od, oi = oracle.render(w["k"], base_inst + [(o[0], o[1], poses[i])], camera=w["camera"],
+                               with_ids=True)
+        np.testing.assert_array_equal(depth[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[i], oi)
+    gpu_ctx.set_observation(w["observed"])
+    gpu_ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    s_gpu, _ = gpu_ctx.score_poses(mids[1 + w["target"]], poses)
+    base = oracle.render(w["k"], base_inst, camera=w["camera"])
+    s_orc, _ = oracle.score_poses(w["k"], w["observed"], o[0], o[1], poses, w["noise"],
+                                  w["sigma_max"], w["window"], base_depth=base, camera=w["camera"])
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+    gpu_ctx.set_base_scene([], [])

@@ -178,3 +178,28 @@ def test_dtheta_pi_symmetric_cube(oracle):
     ia = oracle.render(k, RC.scene_instances(oracle, table, [(cube, 1, dx, dy, 0.0)]), camera=cam)
     ib = oracle.render(k, RC.scene_instances(oracle, table, [(cube, 1, dx, dy, PI)]), camera=cam)
     assert (np.abs(ia - ib) > 1e-5).sum() <= ia.size // 100
+
+
+def test_product_contact_grid_poses_match_oracle(oracle):
+    """b3d_contact_grid_poses (host side of the device contact grid) ==
+    contact_to_pose at the stage-0 cell centres (inference.cpp:208-238,
+    Interval::center), bitwise, for every face."""
+    from paper_2312_08715_b200 import b3d
+    cube = RC.make_model(oracle, RC.lblock_grid(0.015))
+    TWO_PI = 6.283185307179586476925287
+    for face in range(1, 7):
+        cnt = (3, 2, 5)
+        g = b3d.ContactGrid.make(0.5, 0.4, cube.aabb_min, cube.aabb_max, face, cnt)
+        P = b3d.contact_grid_poses(g)
+        lo, hi = oracle.rotated_bounds(cube.aabb_min, cube.aabb_max, face)
+        dxr, dyr = 0.5 - (hi[0] - lo[0]), 0.4 - (hi[1] - lo[1])
+        Q = []
+        for ix in range(cnt[0]):
+            for iy in range(cnt[1]):
+                for it in range(cnt[2]):
+                    dx = 0.5 * (dxr * ix / cnt[0] + dxr * (ix + 1) / cnt[0])
+                    dy = 0.5 * (dyr * iy / cnt[1] + dyr * (iy + 1) / cnt[1])
+                    dt = 0.5 * (TWO_PI * it / cnt[2] + TWO_PI * (it + 1) / cnt[2])
+                    Q.append(oracle.contact_to_pose(0.5, 0.4, cube.aabb_min, cube.aabb_max, face,
+                                                    dx, dy, dt))
+        assert np.array_equal(P.view(np.uint64), np.array(Q).view(np.uint64)), face
