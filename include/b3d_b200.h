@@ -142,6 +142,19 @@ B3D_API b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics
 B3D_API b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
                                        uint64_t n_vertices, const uint32_t* triangles,
                                        uint64_t n_triangles, int32_t* out_mesh_id);
+/* Back-face culling in score-many (default on).  Applies only to meshes the
+ * upload found closed (every directed edge matched by its reverse) and only
+ * to hypotheses with no vertex in front of z = near: a back face of a closed
+ * solid never holds the nearest depth of a pixel, so the
+ * scores are unchanged.  Render-many (depth/ids) never culls. */
+B3D_API b3d_status b3d_gpu_set_culling(b3d_gpu_context* ctx, int enable);
+/* +1 / -1: closed mesh, outward / inward wound; 0: not closed (no culling).
+ * The host-only form runs the same test on caller memory. */
+B3D_API b3d_status b3d_mesh_cull_sign(const double* vertices, uint64_t n_vertices,
+                                      const uint32_t* triangles, uint64_t n_triangles,
+                                      int32_t* out);
+B3D_API b3d_status b3d_gpu_mesh_cull_sign(const b3d_gpu_context* ctx, int32_t mesh_id,
+                                          int32_t* out);
 /* Observed depth image (W x H fp32, sentinel = (float)far). */
 B3D_API b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth);
 /* windowed_log_likelihood_multi settings (likelihood.hpp:65-69). */

@@ -121,6 +121,9 @@ def lib() -> C.CDLL:
         "b3d_gpu_set_camera": ([vp, C.POINTER(Intrinsics), C.POINTER(Pose)], st),
         "b3d_gpu_upload_mesh": ([vp, vp, u64, vp, u64, C.POINTER(i32)], st),
         "b3d_gpu_set_observation": ([vp, vp], st),
+        "b3d_gpu_set_culling": ([vp, st], st),
+        "b3d_mesh_cull_sign": ([vp, u64, vp, u64, C.POINTER(i32)], st),
+        "b3d_gpu_mesh_cull_sign": ([vp, i32, C.POINTER(i32)], st),
         "b3d_gpu_set_likelihood": ([vp, C.POINTER(Noise), u32, dbl, st, st], st),
         "b3d_gpu_score_poses": ([vp, i32, vp, u64, vp, vp], st),
         "b3d_gpu_score_grid": ([vp, i32, C.POINTER(PoseGrid), vp, vp], st),
@@ -138,6 +141,8 @@ def lib() -> C.CDLL:
         "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
     }
     for name, (args, res) in sig.items():
+        if os.environ.get("B3D_LIB") and not hasattr(L, name):
+            continue  # same-box A/B against an older build (scripts/gpu_ablib.sh)
         f = getattr(L, name)
         f.argtypes = args
         f.restype = res
@@ -197,6 +202,17 @@ def voxel_to_mesh(voxels: np.ndarray, resolution: float, origin) -> tuple:
     _check(lib().b3d_voxel_to_mesh(v.ctypes.data, n, resolution, o.ctypes.data,
                                    verts.ctypes.data, tris.ctypes.data, C.byref(nv), C.byref(nt)))
     return verts[: nv.value].copy(), tris[: nt.value].copy()
+
+
+def mesh_cull_sign(vertices: np.ndarray, triangles: np.ndarray) -> int:
+    """+1 / -1: closed mesh wound outward / inward (back faces may be culled in
+    score-many); 0: not closed."""
+    v = np.ascontiguousarray(vertices, dtype=np.float64)
+    t = np.ascontiguousarray(triangles, dtype=np.uint32)
+    out = C.c_int32()
+    _check(lib().b3d_mesh_cull_sign(v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0],
+                                    C.byref(out)))
+    return out.value
 
 
 def contact_grid_poses(grid: "ContactGrid") -> np.ndarray:
@@ -281,6 +297,14 @@ class GpuContext:
         _check(self._L.b3d_gpu_upload_mesh(self.h, v.ctypes.data, v.shape[0], t.ctypes.data,
                                            t.shape[0], C.byref(mid)))
         return mid.value
+
+    def set_culling(self, enable: bool):
+        _check(self._L.b3d_gpu_set_culling(self.h, 1 if enable else 0))
+
+    def mesh_cull_sign(self, mesh: int) -> int:
+        out = C.c_int32()
+        _check(self._L.b3d_gpu_mesh_cull_sign(self.h, mesh, C.byref(out)))
+        return out.value
 
     def set_observation(self, depth):
         if isinstance(depth, np.ndarray):

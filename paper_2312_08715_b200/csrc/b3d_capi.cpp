@@ -181,7 +181,46 @@ bool is_device_ptr(const void* ptr) {
 struct Mesh {
   DevBuf verts, tris;
   int nv = 0, nt = 0;
+  // +1 / -1: closed and outward / inward wound (back-face culling sign), 0:
+  // not closed (no culling)
+  int cull = 0;
 };
+
+// Back faces of a closed mesh never decide a pixel's depth: a ray through a
+// pixel centre inside a back face leaves the solid there, so it entered it
+// at a strictly nearer front face covering the same pixel.
+// Closed = every directed edge (a, b) is matched by as many (b, a); the
+// winding sign is the sign of the enclosed volume.  For a triangle with all
+// vertices at z > 0, the screen area2 of renderer.cpp:63 has the sign of
+// a . ((b - a) x (c - a)), positive for a face turned away from the camera
+// when the mesh is outward wound.
+int closed_mesh_cull_sign(const double* v, const uint32_t* t, uint64_t nt) {
+  std::unordered_map<uint64_t, int> edges;
+  edges.reserve(3 * nt);
+  for (uint64_t i = 0; i < nt; ++i)
+    for (int j = 0; j < 3; ++j) {
+      const uint64_t a = t[3 * i + j], b = t[3 * i + (j + 1) % 3];
+      if (a == b) return 0;
+      edges[(a << 32) | b] += 1;
+    }
+  for (const auto& kv : edges) {
+    const uint64_t rev = (kv.first << 32) | (kv.first >> 32);
+    auto it = edges.find(rev);
+    if (it == edges.end() || it->second != kv.second) return 0;
+  }
+  double vol = 0.0, scale = 0.0;
+  for (uint64_t i = 0; i < nt; ++i) {
+    const double* a = v + 3 * t[3 * i];
+    const double* b = v + 3 * t[3 * i + 1];
+    const double* c = v + 3 * t[3 * i + 2];
+    vol += a[0] * (b[1] * c[2] - b[2] * c[1]) - a[1] * (b[0] * c[2] - b[2] * c[0]) +
+           a[2] * (b[0] * c[1] - b[1] * c[0]);
+    scale += std::fabs(a[0]) + std::fabs(a[1]) + std::fabs(a[2]);
+  }
+  scale /= (double)nt;
+  if (!(std::fabs(vol) > 1e-9 * scale * scale * scale)) return 0;
+  return vol > 0 ? 1 : -1;
+}
 
 }  // namespace b3d200
 
@@ -210,6 +249,7 @@ struct b3d_gpu_context {
   DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
   int base_valid = 0;
   uint32_t base_draw = 0;
+  bool culling = true;  // b3d_gpu_set_culling
   long long obs_version = 0, base_version = 0;
   std::string base_terms_key;
 };
@@ -365,6 +405,7 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.nv = m.nv;
   p.nt = m.nt;
   p.draw_base = 0;
+  p.cull = ctx->culling ? m.cull : 0;
   p.obs = ctx->obs_pts.as<float4>();
   p.obs_count = ctx->obs_count.as<int>();
   p.lik = ctx->lik;
@@ -776,6 +817,30 @@ b3d_status b3d_gpu_synchronize(b3d_gpu_context* ctx) {
   });
 }
 
+b3d_status b3d_mesh_cull_sign(const double* vertices, uint64_t n_vertices,
+                              const uint32_t* triangles, uint64_t n_triangles, int32_t* out) {
+  return guarded([&] {
+    check(vertices && triangles && out, "bad arguments");
+    for (uint64_t i = 0; i < 3 * n_triangles; ++i)
+      check(triangles[i] < n_vertices, "mesh: triangle index out of range");
+    *out = closed_mesh_cull_sign(vertices, triangles, n_triangles);
+  });
+}
+
+b3d_status b3d_gpu_set_culling(b3d_gpu_context* ctx, int enable) {
+  return guarded([&] {
+    check(ctx != nullptr, "bad arguments");
+    ctx->culling = enable != 0;
+  });
+}
+
+b3d_status b3d_gpu_mesh_cull_sign(const b3d_gpu_context* ctx, int32_t mesh_id, int32_t* out) {
+  return guarded([&] {
+    check(ctx && out, "bad arguments");
+    *out = get_mesh(ctx, mesh_id).cull;
+  });
+}
+
 b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics* k,
                               const b3d_pose* camera) {
   return guarded([&] {
@@ -805,6 +870,7 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
     auto m = std::make_unique<Mesh>();
     m->nv = (int)n_vertices;
     m->nt = (int)n_triangles;
+    m->cull = closed_mesh_cull_sign(vertices, triangles, n_triangles);
     m->verts.ensure(24 * n_vertices);
     m->tris.ensure(16 * n_triangles);
     // triangles padded to 16 bytes: one 128-bit load per triangle

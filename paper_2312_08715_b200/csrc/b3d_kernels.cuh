@@ -69,6 +69,11 @@ struct KParams {
   const uint4* tris;  // (i0, i1, i2, 0) per triangle
   int nv, nt;
   uint32_t draw_base;
+  // back-face culling of a closed mesh in score mode:
+  // +1 = skip triangles with screen area2 > 0 (outward-wound mesh), -1 =
+  // area2 < 0 (inward-wound), 0 = off; ignored for hypotheses with a vertex
+  // in front of z = near
+  int cull;
   // hypotheses
   const KPose* poses;  // nullptr => grid
   KGrid grid;

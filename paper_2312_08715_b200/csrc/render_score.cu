@@ -187,37 +187,38 @@ __device__ __forceinline__ short4 vertex_bbox(const KParams& p, double u, double
   return r;
 }
 
-// Per-warp triangle records (structure of arrays: a warp reading the
-// records of different triangles hits distinct banks).  Filled by the lane
-// that sets the triangle up, read by whichever lane owns a pixel of it.
-struct WarpRec {
-  double inv_area2[32];
-  uint32_t ia[32], ib[32], ic[32];  // vertex ids after the orientation swap
-  uint32_t tri[32];                 // triangle index (draw order)
-  int uv0[32];                      // u_min | v_min << 16
-  int fl[32];                       // edge flags (canonical | top-left bits)
-  uint32_t cov[32];                 // covered pixels of the 3x3 bbox tile
+// Per-warp queues of triangles that survive the cheap tests (non-empty
+// integer bbox, non-zero area, not culled), one ring per tile class
+// (bbox <= 2x2 and <= 3x3).  Entry: vertex ids after the orientation swap
+// (renderer.cpp:63-69) + triangle index, and the packed bbox
+// u_min | (bw-1) << 14 | v_min << 16 | (bh-1) << 30.
+constexpr int kRing = 64;
+struct WarpQ {
+  uint4 tri[2][kRing];
+  uint32_t box[2][kRing];
 };
 
-// Coverage of one edge over a 3x3 pixel tile at (u0, v0): the reference's
+// Coverage of one edge over a KxK pixel tile at (u0, v0): the reference's
 // edge value dx*(py - oy) - dy*(px - ox) (renderer.cpp:32-34, canonical
-// origin) factored into 3 row products and 3 column products -- the same
+// origin) factored into K row products and K column products -- the same
 // two fp64 products and difference per pixel, so bitwise the same values --
-// and the top-left rule (renderer.cpp:39-43).  Returns a 9-bit mask.
+// and the top-left rule (renderer.cpp:39-43).  Bit 3*j + i = pixel
+// (u0 + i, v0 + j).
+template <int K>
 __device__ __forceinline__ uint32_t tile_edge_mask(double2 a, double2 b, bool canon, bool tie,
                                                    int u0, int v0) {
   const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
   const double dx = b.x - a.x, dy = b.y - a.y;
-  double A[3], B[3];
+  double A[K], B[K];
 #pragma unroll
-  for (int j = 0; j < 3; ++j) A[j] = dx * ((double)(v0 + j) - oy);
+  for (int j = 0; j < K; ++j) A[j] = dx * ((double)(v0 + j) - oy);
 #pragma unroll
-  for (int i = 0; i < 3; ++i) B[i] = dy * ((double)(u0 + i) - ox);
+  for (int i = 0; i < K; ++i) B[i] = dy * ((double)(u0 + i) - ox);
   uint32_t m = 0;
 #pragma unroll
-  for (int j = 0; j < 3; ++j)
+  for (int j = 0; j < K; ++j)
 #pragma unroll
-    for (int i = 0; i < 3; ++i) {
+    for (int i = 0; i < K; ++i) {
       const double e = A[j] - B[i];
       const bool c = e > 0 || (tie && e == 0);
       m |= (uint32_t)c << (3 * j + i);
@@ -387,6 +388,96 @@ constexpr int kWarps = kThreads / 32;
 
 }  // namespace
 
+// Pass 2 of the raster: lane l takes queue entry head + l (l < n): edge
+// flags (renderer.cpp:39-47), KxK tile coverage; the covered pixels (~0.6
+// per triangle) are then dealt one per lane -- owner found by a 5-step
+// shuffle search over the exclusive scan of coverage counts -- for the
+// perspective 1/z, the near/far tests, the fp32 round and the strict-less
+// z-test (renderer.cpp:94-100) with every lane busy.
+template <int K, bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, const Region& rg,
+                                            const VS& vs, const uint4* qt, const uint32_t* qb,
+                                            int head, int n, int lane) {
+  uint32_t cov = 0, box = 0;
+  uint4 tr = make_uint4(0u, 0u, 0u, 0u);
+  int fl = 0;
+  double inv_area2 = 0.0;
+  if (lane < n) {
+    const int s = (head + lane) & (kRing - 1);
+    tr = qt[s];
+    box = qb[s];
+    const double2 PA = vs.uv[tr.x], PB = vs.uv[tr.y], PC = vs.uv[tr.z];
+    const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
+    fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+    const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
+    const int bw = ((box >> 14) & 3) + 1, bh = (int)(box >> 30) + 1;
+    const uint32_t colm = (1u << bw) - 1u;
+    uint32_t valid = colm;
+    if (bh > 1) valid |= colm << 3;
+    if (K > 2 && bh > 2) valid |= colm << 6;
+    cov = valid & tile_edge_mask<K>(PA, PB, fl & 1, fl & 8, u0, v0) &
+          tile_edge_mask<K>(PB, PC, fl & 2, fl & 16, u0, v0) &
+          tile_edge_mask<K>(PC, PA, fl & 4, fl & 32, u0, v0);
+    // area2 of the swapped order is bitwise the negated original
+    // (renderer.cpp:66-68): the two products are the same, only swapped
+    if (cov) inv_area2 = 1.0 / ((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
+  }
+  const int cnt = __popc(cov);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int start = incl - cnt;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int c0 = 0; c0 < total; c0 += 32) {
+    const int item = c0 + lane;
+    int own = 0;  // last lane whose start <= item (never a zero-count lane)
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int sp = __shfl_sync(0xffffffffu, start, own + step);
+      if (sp <= item) own += step;
+    }
+    const int st = __shfl_sync(0xffffffffu, start, own);
+    uint32_t m = __shfl_sync(0xffffffffu, cov, own);
+    const uint32_t bx = __shfl_sync(0xffffffffu, box, own);
+    const int flo = __shfl_sync(0xffffffffu, fl, own);
+    const uint32_t ia = __shfl_sync(0xffffffffu, tr.x, own);
+    const uint32_t ib = __shfl_sync(0xffffffffu, tr.y, own);
+    const uint32_t ic = __shfl_sync(0xffffffffu, tr.z, own);
+    const uint32_t tri = __shfl_sync(0xffffffffu, tr.w, own);
+    const double ia2 = __shfl_sync(0xffffffffu, inv_area2, own);
+    if (item < total) {
+      for (int k = item - st; k > 0; --k) m &= m - 1;  // k-th covered pixel
+      const int bit = __ffs(m) - 1;
+      const int pu = (int)(bx & 0x3fff) + bit % 3, pv = (int)((bx >> 16) & 0x3fff) + bit / 3;
+      const double2 A = vs.uv[ia], B = vs.uv[ib], C = vs.uv[ic];
+      const double px = pu, py = pv;
+      const double e_ab = edge_at(A, B, flo & 1, px, py);
+      const double e_bc = edge_at(B, C, flo & 2, px, py);
+      const double e_ca = edge_at(C, A, flo & 4, px, py);
+      // renderer.cpp:94-100
+      const double inv_z = (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * ia2;
+      if (inv_z > 0) {
+        const double z = 1.0 / inv_z;
+        if (!(z < p.near_lim || z > p.far_m)) {
+          const float zf = __double2float_rn(z);
+          if (zf < p.far_f) {
+            Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+            if (kIds)
+              zmin((unsigned long long*)cell,
+                   ((unsigned long long)__float_as_uint(zf) << 32) |
+                       (unsigned long long)(p.draw_base + tri));
+            else
+              zmin((unsigned int*)cell, __float_as_uint(zf));
+          }
+        }
+      }
+    }
+  }
+}
+
 // Shared state of one CTA while it processes one hypothesis.
 struct HypCtx {
   const double* R;  // rotation (row-major) in shared memory
@@ -402,7 +493,7 @@ struct HypCtx {
 // global ones (overflow scratch), never to generic ones.
 template <bool kIds, bool kScore, bool kOut, typename VS, typename Key>
 __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
-                                         const VS& vs, WarpRec* const wrec,
+                                         const VS& vs, WarpQ* const wq,
 
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
@@ -432,20 +523,24 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   }
   __syncthreads();
 
-  // ---- C: raster.  Lane = triangle (mesh order): integer bbox reject,
-  // orientation swap (renderer.cpp:63-69), canonical edges; then the
-  // coverage of its bbox pixels in one straight-line pass over a 3x3 tile
-  // (voxel faces at these scales cover 1-6 bbox pixels; larger bboxes take
-  // the per-pixel loop).  Covered pixels -- ~0.6 per triangle -- are dealt
-  // one per lane (owner found by a 5-step shuffle search over the exclusive
-  // scan of coverage counts) for the perspective 1/z, the fp32 round and the
-  // strict-less z-test (renderer.cpp:94-100) with every lane busy.
+  // ---- C: raster, in two passes per 32-triangle chunk of each warp.
+  // Pass 1, lane = triangle (mesh order): integer bbox reject, signed area,
+  // back-face cull (closed meshes, score mode), orientation
+  // swap (renderer.cpp:63-69); survivors are appended to the warp's queue of
+  // their tile class (bbox <= 2x2 or <= 3x3; larger bboxes run the
+  // reference's per-pixel loop in place).  Pass 2 (drain_queue) runs once a
+  // queue holds 32 triangles, so the fp64 coverage work is done by full warps.
   if (!hc.empty_region || hc.clip) {
-    WarpRec& wr = wrec[warp];
+    WarpQ& q = wq[warp];
+    const int cull = (kScore && !kIds && !hc.clip) ? p.cull : 0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int head0 = 0, tail0 = 0, head1 = 0, tail1 = 0;  // warp-uniform ring cursors
     for (int base = warp * 32; base < p.nt; base += kThreads) {
       __syncwarp();
       const int ti = base + lane;
-      uint32_t cov = 0;
+      int cls = -1;
+      uint4 ent;
+      uint32_t box = 0;
       if (ti < p.nt) {
         const uint4 tri = __ldg(p.tris + ti);
         uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
@@ -459,7 +554,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
             const double2 PA = vs.uv[ia];
             double2 PB = vs.uv[ib], PC = vs.uv[ic];
             double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
-            if (area2 != 0) {
+            if (area2 != 0 && !(cull > 0 ? area2 > 0 : (cull < 0 && area2 < 0))) {
               if (area2 < 0) {
                 const double2 T = PB;
                 PB = PC;
@@ -469,27 +564,12 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                 ic = tt;
                 area2 = -area2;
               }
-              const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
-              const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
               const int bw = u_max - u_min + 1, bh = v_max - v_min + 1;
               if (bw <= 3 && bh <= 3) {
-                const uint32_t colm = (1u << bw) - 1u;
-                uint32_t valid = colm;
-                if (bh > 1) valid |= colm << 3;
-                if (bh > 2) valid |= colm << 6;
-                cov = valid & tile_edge_mask(PA, PB, fl & 1, fl & 8, u_min, v_min) &
-                      tile_edge_mask(PB, PC, fl & 2, fl & 16, u_min, v_min) &
-                      tile_edge_mask(PC, PA, fl & 4, fl & 32, u_min, v_min);
-                if (cov) {
-                  wr.inv_area2[lane] = 1.0 / area2;
-                  wr.tri[lane] = (uint32_t)ti;
-                  wr.ia[lane] = ia;
-                  wr.ib[lane] = ib;
-                  wr.ic[lane] = ic;
-                  wr.uv0[lane] = u_min | (v_min << 16);
-                  wr.fl[lane] = fl;
-                  wr.cov[lane] = cov;
-                }
+                cls = (bw <= 2 && bh <= 2) ? 0 : 1;
+                ent = make_uint4(ia, ib, ic, (uint32_t)ti);
+                box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
+                      (uint32_t)(bh - 1) << 30;
               } else {  // large bbox: the reference's per-pixel loop
                 raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz[ia]},
                                      SV{PB.x, PB.y, vs.iz[ib]}, SV{PC.x, PC.y, vs.iz[ic]},
@@ -499,58 +579,31 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
           }
         }
       }
-      const int cnt = __popc(cov);
-      int incl = cnt;
-#pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const int y = __shfl_up_sync(0xffffffffu, incl, o);
-        if (lane >= o) incl += y;
+      const uint32_t b0 = __ballot_sync(0xffffffffu, cls == 0);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, cls == 1);
+      if (cls == 0) {
+        const int s = (tail0 + __popc(b0 & lt_mask)) & (kRing - 1);
+        q.tri[0][s] = ent;
+        q.box[0][s] = box;
+      } else if (cls == 1) {
+        const int s = (tail1 + __popc(b1 & lt_mask)) & (kRing - 1);
+        q.tri[1][s] = ent;
+        q.box[1][s] = box;
       }
-      const int start = incl - cnt;
-      const int total = __shfl_sync(0xffffffffu, incl, 31);
+      tail0 += __popc(b0);
+      tail1 += __popc(b1);
       __syncwarp();
-      for (int c0 = 0; c0 < total; c0 += 32) {
-        const int item = c0 + lane;
-        int own = 0;  // last lane whose start <= item (never a zero-count lane)
-#pragma unroll
-        for (int step = 16; step > 0; step >>= 1) {
-          const int sp = __shfl_sync(0xffffffffu, start, own + step);
-          if (sp <= item) own += step;
-        }
-        const int st = __shfl_sync(0xffffffffu, start, own);
-        if (item < total) {
-          uint32_t m = wr.cov[own];
-          for (int q = item - st; q > 0; --q) m &= m - 1;  // k-th covered pixel
-          const int bit = __ffs(m) - 1;
-          const int uv0 = wr.uv0[own], fl = wr.fl[own];
-          const int pu = (uv0 & 0xffff) + bit % 3, pv = (uv0 >> 16) + bit / 3;
-          const uint32_t ia = wr.ia[own], ib = wr.ib[own], ic = wr.ic[own];
-          const double2 A = vs.uv[ia], B = vs.uv[ib], C = vs.uv[ic];
-          const double px = pu, py = pv;
-          const double e_ab = edge_at(A, B, fl & 1, px, py);
-          const double e_bc = edge_at(B, C, fl & 2, px, py);
-          const double e_ca = edge_at(C, A, fl & 4, px, py);
-          // renderer.cpp:94-100
-          const double inv_z =
-              (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * wr.inv_area2[own];
-          if (inv_z > 0) {
-            const double z = 1.0 / inv_z;
-            if (!(z < p.near_lim || z > p.far_m)) {
-              const float zf = __double2float_rn(z);
-              if (zf < p.far_f) {
-                Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
-                if (kIds)
-                  zmin((unsigned long long*)cell,
-                       ((unsigned long long)__float_as_uint(zf) << 32) |
-                           (unsigned long long)(p.draw_base + wr.tri[own]));
-                else
-                  zmin((unsigned int*)cell, __float_as_uint(zf));
-              }
-            }
-          }
-        }
+      if (tail0 - head0 >= 32) {
+        drain_queue<2, kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, 32, lane);
+        head0 += 32;
+      }
+      if (tail1 - head1 >= 32) {
+        drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, 32, lane);
+        head1 += 32;
       }
     }
+    if (tail0 > head0) drain_queue<2, kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, tail0 - head0, lane);
+    if (tail1 > head1) drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, tail1 - head1, lane);
   }
   __syncthreads();
 
@@ -745,8 +798,8 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     vs.bb = reinterpret_cast<short4*>(g + 3 * (size_t)p.nv);
   }
   const int vcap = kVS ? p.vcap : 0;
-  WarpRec* const wrec = reinterpret_cast<WarpRec*>(sv_s + 4 * (size_t)vcap);
-  Key* const zb_s = reinterpret_cast<Key*>(wrec + kWarps);
+  WarpQ* const wq = reinterpret_cast<WarpQ*>(sv_s + 4 * (size_t)vcap);
+  Key* const zb_s = reinterpret_cast<Key*>(wq + kWarps);
 
   int kk = 0;  // hypotheses this CTA has processed
   for (long long h = blockIdx.x; h < p.n_hyp; h += gridDim.x, ++kk) {
@@ -839,11 +892,11 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wrec, &s_count, s_coef,
+      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wq, &s_count, s_coef,
                                    s_red, s_redi, h);
     else
       hyp_body<kIds, kScore, kOut>(
-          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wrec,
+          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
           &s_count, s_coef, s_red, s_redi, h);
     __syncthreads();
   }
@@ -1012,6 +1065,6 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
 
 int render_score_threads() { return kThreads; }
 
-size_t render_score_staging_bytes(int nt) { return (void)nt, sizeof(WarpRec) * kWarps; }
+size_t render_score_staging_bytes(int nt) { return (void)nt, sizeof(WarpQ) * kWarps; }
 
 }  // namespace b3d200

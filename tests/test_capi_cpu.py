@@ -52,3 +52,23 @@ def test_voxel_to_mesh_errors():
     st = L.b3d_voxel_to_mesh(vox.ctypes.data, 0, 0.1, o.ctypes.data, buf.ctypes.data,
                              tb.ctypes.data, C.byref(nv), C.byref(nt))
     assert st == 1 and b"empty grid" in L.b3d_last_error()
+
+
+def test_mesh_cull_sign_closed_open_and_flipped():
+    """Back-face culling is enabled only for closed meshes (every directed edge
+    matched by its reverse); the sign follows the winding (enclosed volume)."""
+    from paper_2312_08715_b200 import synth
+    for vox in (synth.eden_blob(300, 4), synth.random_walk_blob(300, 5)):
+        v, t = b3d.voxel_to_mesh(vox, 0.005, np.zeros(3))
+        s = b3d.mesh_cull_sign(v, t)
+        assert s == 1  # voxel_to_mesh winds faces outward (geometry.cpp:142-177)
+        assert b3d.mesh_cull_sign(v, t[:, ::-1]) == -1
+        assert b3d.mesh_cull_sign(v, t[1:]) == 0      # a hole
+        t2 = t.copy()
+        t2[0] = t2[0, [0, 0, 1]]                       # degenerate index
+        assert b3d.mesh_cull_sign(v, t2) == 0
+    # the reference box mesh is closed too; a lone triangle is not
+    from oracle import pyoracle as O
+    bv, bt = O.box_mesh([-0.05, -0.04, 0.0], [0.05, 0.04, 0.09])
+    assert b3d.mesh_cull_sign(bv, bt) in (1, -1)
+    assert b3d.mesh_cull_sign(bv, bt[:1]) == 0

@@ -453,3 +453,62 @@ def test_base_scene_with_near_clipping_and_scratch(gpu_ctx, oracle):
                                   w["sigma_max"], w["window"], base_depth=base, camera=w["camera"])
     assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
     gpu_ctx.set_base_scene([], [])
+
+
+def _scores_with_and_without_culling(ctx, fn):
+    ctx.set_culling(True)
+    a = fn()
+    ctx.set_culling(False)
+    b = fn()
+    ctx.set_culling(True)
+    return a, b
+
+
+def test_back_face_culling_leaves_scores_bitwise_unchanged(gpu_ctx, oracle):
+    """Score-many culls back faces of closed meshes: the
+    region z-buffer and hence every score are bit-identical to the unculled
+    render, for the cfg1 grid, another blob, a wide window and multi-noise."""
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    assert gpu_ctx.mesh_cull_sign(mid) == 1
+    grid = gpu_ctx.make_grid(w.center, w.extent, w.count, w.rotations, w.grid_mode)
+    a, b = _scores_with_and_without_culling(gpu_ctx, lambda: gpu_ctx.score_grid(mid, grid)[0])
+    np.testing.assert_array_equal(a, b)
+    w2 = cfg1_oracle(seed=3, blob="random_walk")
+    mid2 = gpu_ctx.upload_mesh(w2.vertices, w2.triangles)
+    gpu_ctx.set_observation(w2.observed)
+    gpu_ctx.set_likelihood([(0.01, 0.005), (0.2, 0.02)], 0.1, 3)
+    rng = np.random.Generator(np.random.PCG64(9))
+    poses = []
+    for _ in range(256):
+        q = synth.uniform_quaternion(rng)
+        poses.append([*q, rng.uniform(-0.05, 0.05), rng.uniform(-0.05, 0.05),
+                      rng.uniform(0.2, 1.2)])
+    poses = np.array(poses)
+    a, b = _scores_with_and_without_culling(gpu_ctx, lambda: gpu_ctx.score_poses(mid2, poses)[0])
+    np.testing.assert_array_equal(a, b)
+    # an inward-wound copy culls the other sign and still agrees
+    mid3 = gpu_ctx.upload_mesh(w2.vertices, w2.triangles[:, ::-1])
+    assert gpu_ctx.mesh_cull_sign(mid3) == -1
+    c, _ = gpu_ctx.score_poses(mid3, poses)
+    np.testing.assert_array_equal(c, a)
+
+
+def test_back_face_culling_with_base_scene_and_near_clip(gpu_ctx, oracle):
+    """Culling composes with the base scene; hypotheses with a vertex in
+    front of z = near are never culled."""
+    w = _cfg3(oracle)
+    mids, base_inst = _setup_cfg3(gpu_ctx, oracle, w)
+    gpu_ctx.set_observation(w["observed"])
+    gpu_ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    o = w["objects"][w["target"]]
+    g = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, (4, 4, 8))
+    m = mids[1 + w["target"]]
+    a, b = _scores_with_and_without_culling(gpu_ctx, lambda: gpu_ctx.score_contact_grid(m, g)[0])
+    np.testing.assert_array_equal(a, b)
+    rng = np.random.Generator(np.random.PCG64(8))
+    poses = np.array([[*synth.uniform_quaternion(rng), rng.uniform(-0.02, 0.02),
+                       rng.uniform(-0.02, 0.02), rng.uniform(0.66, 0.69)] for _ in range(6)])
+    a, b = _scores_with_and_without_culling(gpu_ctx, lambda: gpu_ctx.score_poses(m, poses)[0])
+    np.testing.assert_array_equal(a, b)
+    gpu_ctx.set_base_scene([], [])
