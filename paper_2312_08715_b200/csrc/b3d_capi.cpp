@@ -184,7 +184,82 @@ struct Mesh {
   // +1 / -1: closed and outward / inward wound (back-face culling sign), 0:
   // not closed (no culling)
   int cull = 0;
+  // score-mode order (KParams::tris_s): axis classes sorted by plane offset
+  DevBuf tris_s, plane_off, plane_end;
+  int cls_start[8] = {0};
+  int plane_begin[8] = {0};
 };
+
+// Score-mode triangle order (b3d_kernels.cuh KParams::tris_s).  A triangle
+// whose three vertices share one coordinate k exactly (voxel faces) has the
+// winding normal +-e_k; with the mesh's winding sign w (closed_mesh_cull_sign)
+// its outward normal is s e_k, s = w * sign(n_k), class 2k + (s < 0), plane
+// offset o = s * a_k.  Everything else is class 6.
+void build_score_order(const double* v, const uint32_t* t, uint64_t nt, int wsign, Mesh& m) {
+  struct Item {
+    int cls;
+    double off;
+    uint32_t idx;
+  };
+  std::vector<Item> items(nt);
+  for (uint64_t i = 0; i < nt; ++i) {
+    const double* a = v + 3 * t[3 * i];
+    const double* b = v + 3 * t[3 * i + 1];
+    const double* cc = v + 3 * t[3 * i + 2];
+    Item it{6, 0.0, (uint32_t)i};
+    if (wsign != 0)
+      for (int k = 0; k < 3; ++k) {
+        if (a[k] != b[k] || a[k] != cc[k]) continue;
+        const int k1 = (k + 1) % 3, k2 = (k + 2) % 3;
+        const double nk = (b[k1] - a[k1]) * (cc[k2] - a[k2]) - (b[k2] - a[k2]) * (cc[k1] - a[k1]);
+        if (nk == 0) break;
+        const int s = (nk > 0 ? 1 : -1) * wsign;
+        it.cls = 2 * k + (s < 0);
+        it.off = s * a[k];
+        break;
+      }
+    items[i] = it;
+  }
+  std::stable_sort(items.begin(), items.end(), [](const Item& x, const Item& y) {
+    return x.cls != y.cls ? x.cls < y.cls : x.off < y.off;
+  });
+  std::vector<uint32_t> tri4(4 * nt);
+  std::vector<double> poff;
+  std::vector<int> pend;
+  int cls = -1;
+  for (uint64_t i = 0; i < nt; ++i) {
+    const Item& it = items[i];
+    for (int j = 0; j < 3; ++j) tri4[4 * i + j] = t[3 * it.idx + j];
+    tri4[4 * i + 3] = it.idx;
+    while (cls < it.cls) {
+      ++cls;
+      m.cls_start[cls] = (int)i;
+      m.plane_begin[cls] = (int)poff.size();
+    }
+    if (it.cls < 6) {
+      if ((int)poff.size() == m.plane_begin[cls] || poff.back() != it.off) {
+        poff.push_back(it.off);
+        pend.push_back(0);
+      }
+      pend.back() = (int)i + 1;
+    }
+  }
+  while (cls < 7) {
+    ++cls;
+    m.cls_start[cls] = (int)nt;
+    m.plane_begin[cls] = (int)poff.size();
+  }
+  m.tris_s.ensure(16 * nt);
+  cuda_check(cudaMemcpy(m.tris_s.p, tri4.data(), 16 * nt, cudaMemcpyHostToDevice), "cudaMemcpy");
+  m.plane_off.ensure(8 * (poff.size() + 1));
+  m.plane_end.ensure(4 * (pend.size() + 1));
+  if (!poff.empty()) {
+    cuda_check(cudaMemcpy(m.plane_off.p, poff.data(), 8 * poff.size(), cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    cuda_check(cudaMemcpy(m.plane_end.p, pend.data(), 4 * pend.size(), cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+  }
+}
 
 // Back faces of a closed mesh never decide a pixel's depth: a ray through a
 // pixel centre inside a back face leaves the solid there, so it entered it
@@ -406,6 +481,13 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.nt = m.nt;
   p.draw_base = 0;
   p.cull = ctx->culling ? m.cull : 0;
+  p.tris_s = m.tris_s.as<uint4>();
+  p.plane_off = m.plane_off.as<double>();
+  p.plane_end = m.plane_end.as<int>();
+  for (int i = 0; i < 8; ++i) {
+    p.cls_start[i] = m.cls_start[i];
+    p.plane_begin[i] = m.plane_begin[i];
+  }
   p.obs = ctx->obs_pts.as<float4>();
   p.obs_count = ctx->obs_count.as<int>();
   p.lik = ctx->lik;
@@ -871,6 +953,7 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
     m->nv = (int)n_vertices;
     m->nt = (int)n_triangles;
     m->cull = closed_mesh_cull_sign(vertices, triangles, n_triangles);
+    build_score_order(vertices, triangles, n_triangles, m->cull, *m);
     m->verts.ensure(24 * n_vertices);
     m->tris.ensure(16 * n_triangles);
     // triangles padded to 16 bytes: one 128-bit load per triangle

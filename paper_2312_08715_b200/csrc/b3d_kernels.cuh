@@ -74,6 +74,17 @@ struct KParams {
   // area2 < 0 (inward-wound), 0 = off; ignored for hypotheses with a vertex
   // in front of z = near
   int cull;
+  // score-mode triangle order (depth = min over fragments does not depend
+  // on draw order): 6 axis-aligned classes (+x,-x,+y,-y,+z,-z outward
+  // normal), each sorted by plane offset o = n . a, then the rest (class 6).
+  // A face of class c is turned away from the camera centre C (model frame)
+  // iff o > n . C, so the back faces of a class are a suffix found per
+  // hypothesis from the class's distinct plane offsets.
+  const uint4* tris_s;
+  int cls_start[8];         // class c = tris_s[cls_start[c], cls_start[c+1])
+  const double* plane_off;  // distinct offsets per class, ascending
+  const int* plane_end;     // tris_s index one past each plane's triangles
+  int plane_begin[8];       // class c's planes = [plane_begin[c], plane_begin[c+1])
   // hypotheses
   const KPose* poses;  // nullptr => grid
   KGrid grid;

@@ -26,6 +26,10 @@
 #include "b3d_kernels.cuh"
 #include "posemath.cuh"
 
+#ifndef B3D_PREFETCH
+#define B3D_PREFETCH 0
+#endif
+
 namespace b3d200 {
 
 namespace {
@@ -106,7 +110,7 @@ __device__ __forceinline__ void raster_tri_box(const KParams& p, typename KeyT<k
   const Edge ab = make_edge(a, b);
   const Edge bc = make_edge(b, c);
   const Edge ca = make_edge(c, a);
-  const double inv_area2 = 1.0 / area2;
+  const double inv_area2 = __drcp_rn(area2);
   for (int pv = v_min; pv <= v_max; ++pv) {
     const double py = pv;
     const double r_ab = ab.dx * (py - ab.oy);
@@ -121,7 +125,7 @@ __device__ __forceinline__ void raster_tri_box(const KParams& p, typename KeyT<k
       if (!covers(ab, e_ab) || !covers(bc, e_bc) || !covers(ca, e_ca)) continue;
       const double inv_z = (e_bc * a.iz + e_ca * b.iz + e_ab * c.iz) * inv_area2;
       if (inv_z <= 0) continue;
-      const double z = 1.0 / inv_z;
+      const double z = __drcp_rn(inv_z);
       if (z < p.near_lim || z > p.far_m) continue;
       const float zf = __double2float_rn(z);
       if (!(zf < p.far_f)) continue;
@@ -153,7 +157,7 @@ __device__ __forceinline__ void raster_tri(const KParams& p, typename KeyT<kIds>
 }
 
 __device__ __forceinline__ SV project(const KParams& p, double x, double y, double z) {
-  const double iz = 1.0 / z;
+  const double iz = __drcp_rn(z);
   SV s;
   s.u = p.fx * x * iz + p.cx;
   s.v = p.fy * y * iz + p.cy;
@@ -420,7 +424,7 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
           tile_edge_mask<K>(PC, PA, fl & 4, fl & 32, u0, v0);
     // area2 of the swapped order is bitwise the negated original
     // (renderer.cpp:66-68): the two products are the same, only swapped
-    if (cov) inv_area2 = 1.0 / ((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
+    if (cov) inv_area2 = __drcp_rn((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
   }
   const int cnt = __popc(cov);
   int incl = cnt;
@@ -460,7 +464,7 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
       // renderer.cpp:94-100
       const double inv_z = (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * ia2;
       if (inv_z > 0) {
-        const double z = 1.0 / inv_z;
+        const double z = __drcp_rn(inv_z);
         if (!(z < p.near_lim || z > p.far_m)) {
           const float zf = __double2float_rn(z);
           if (zf < p.far_f) {
@@ -493,8 +497,7 @@ struct HypCtx {
 // global ones (overflow scratch), never to generic ones.
 template <bool kIds, bool kScore, bool kOut, typename VS, typename Key>
 __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
-                                         const VS& vs, WarpQ* const wq,
-
+                                         const VS& vs, WarpQ* const wq, int* const s_seg,
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h) {
@@ -521,6 +524,22 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   } else {
     for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
   }
+  // score mode: the work list is the front part of each axis class (the cut
+  // of phase B) plus all of class 6; s_seg[0..7] = running work counts,
+  // s_seg[8..14] = first tris_s index of each segment
+  constexpr bool kSorted = kScore && !kIds;
+  if (kSorted && tid == 0) {
+    const bool cut = p.cull != 0 && !hc.clip;
+    int cum = 0;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      const int b = p.cls_start[c], e = (cut && c < 6) ? s_seg[16 + c] : p.cls_start[c + 1];
+      s_seg[c] = cum;
+      s_seg[8 + c] = b;
+      cum += e - b;
+    }
+    s_seg[7] = cum;
+  }
   __syncthreads();
 
   // ---- C: raster, in two passes per 32-triangle chunk of each warp.
@@ -535,14 +554,38 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     const int cull = (kScore && !kIds && !hc.clip) ? p.cull : 0;
     const uint32_t lt_mask = (1u << lane) - 1u;
     int head0 = 0, tail0 = 0, head1 = 0, tail1 = 0;  // warp-uniform ring cursors
-    for (int base = warp * 32; base < p.nt; base += kThreads) {
+    const int n_work = kSorted ? s_seg[7] : p.nt;
+    const uint4* const tl = kSorted ? p.tris_s : p.tris;
+    auto work_tri = [&](int w) -> uint4 {
+      int phys = w;
+      if (kSorted) {
+        int c = 0;
+#pragma unroll
+        for (int j = 1; j < 7; ++j) c += w >= s_seg[j];
+        phys = s_seg[8 + c] + (w - s_seg[c]);
+      }
+      return __ldg(tl + phys);
+    };
+#if B3D_PREFETCH
+    uint4 tri_next = make_uint4(0u, 0u, 0u, 0u);
+    if (warp * 32 + lane < n_work) tri_next = work_tri(warp * 32 + lane);
+#endif
+    for (int base = warp * 32; base < n_work; base += kThreads) {
       __syncwarp();
       const int ti = base + lane;
       int cls = -1;
       uint4 ent;
       uint32_t box = 0;
-      if (ti < p.nt) {
-        const uint4 tri = __ldg(p.tris + ti);
+#if B3D_PREFETCH
+      const uint4 tri_cur = tri_next;
+      if (ti + kThreads < n_work) tri_next = work_tri(ti + kThreads);
+#endif
+      if (ti < n_work) {
+#if B3D_PREFETCH
+        const uint4 tri = tri_cur;
+#else
+        const uint4 tri = work_tri(ti);
+#endif
         uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
         const short4 A = vs.bb[ia], B = vs.bb[ib], C = vs.bb[ic];
         if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
@@ -780,6 +823,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
   __shared__ int s_redi[kWarps][kMaxNoise + 1];
   __shared__ double s_coef[kMaxNoise];
   __shared__ int s_count;
+  __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -851,6 +895,23 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
         clip = 1;
       }
     }
+    // score mode: per axis class c (warp c), the faces turned towards the
+    // camera centre C = -R^T t (model frame) are those with plane offset
+    // o <= n . C: a prefix of the class (b3d_kernels.cuh).  The small margin
+    // keeps near-edge-on planes; they go through the exact tests.
+    if (kScore && !kIds && warp < 6) {
+      const int k = warp >> 1;
+      const double Ck = -(R[k] * t[0] + R[3 + k] * t[1] + R[6 + k] * t[2]);
+      const double thr = (warp & 1) ? -Ck : Ck;
+      const double lim = thr + 1e-9 * (1.0 + fabs(thr));
+      const int pb = p.plane_begin[warp], pe = p.plane_begin[warp + 1];
+      int n_le = 0;
+      for (int j0 = pb; j0 < pe; j0 += 32) {
+        const int j = j0 + lane;
+        n_le += __popc(__ballot_sync(0xffffffffu, j < pe && __ldg(p.plane_off + j) <= lim));
+      }
+      if (lane == 0) s_seg[16 + warp] = n_le ? __ldg(p.plane_end + pb + n_le - 1) : p.cls_start[warp];
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       lo_u = min(lo_u, __shfl_xor_sync(0xffffffffu, lo_u, o));
@@ -892,11 +953,11 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wq, &s_count, s_coef,
+      hyp_body<kIds, kScore, kOut>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
                                    s_red, s_redi, h);
     else
       hyp_body<kIds, kScore, kOut>(
-          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
+          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq, s_seg,
           &s_count, s_coef, s_red, s_redi, h);
     __syncthreads();
   }
