@@ -948,6 +948,8 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
     check(n_vertices < (1u << 30) && n_triangles < (1u << 30), "mesh: too large");
     for (uint64_t i = 0; i < 3 * n_triangles; ++i)
       check(triangles[i] < n_vertices, "mesh: triangle index out of range");
+    for (uint64_t i = 0; i < 3 * n_vertices; ++i)
+      check(std::isfinite(vertices[i]), "mesh: non-finite vertex coordinate");
     DeviceGuard dg(ctx->device);
     auto m = std::make_unique<Mesh>();
     m->nv = (int)n_vertices;

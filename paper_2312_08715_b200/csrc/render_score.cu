@@ -183,11 +183,14 @@ constexpr short kOvf = 32767;
 constexpr short kClipV = -32768;
 
 __device__ __forceinline__ short4 vertex_bbox(const KParams& p, double u, double v) {
+  // fp64 -> int conversions with directed rounding saturate (PTX cvt), so
+  // ceil/floor + clamp need no fp64 min/max; |u|, |v| >= 2^31 behave like the
+  // clamped fp64 forms (upload rejects non-finite vertices)
   short4 r;
-  r.x = (short)fmin(fmax(ceil(u), 0.0), (double)p.W);
-  r.y = u >= 2147483648.0 ? kOvf : (short)fmin(fmax(floor(u), -1.0), (double)(p.W - 1));
-  r.z = (short)fmin(fmax(ceil(v), 0.0), (double)p.H);
-  r.w = v >= 2147483648.0 ? kOvf : (short)fmin(fmax(floor(v), -1.0), (double)(p.H - 1));
+  r.x = (short)min(max(__double2int_ru(u), 0), p.W);
+  r.y = u >= 2147483648.0 ? kOvf : (short)min(max(__double2int_rd(u), -1), p.W - 1);
+  r.z = (short)min(max(__double2int_ru(v), 0), p.H);
+  r.w = v >= 2147483648.0 ? kOvf : (short)min(max(__double2int_rd(v), -1), p.H - 1);
   return r;
 }
 
@@ -218,15 +221,15 @@ __device__ __forceinline__ uint32_t tile_edge_mask(double2 a, double2 b, bool ca
   for (int j = 0; j < K; ++j) A[j] = dx * ((double)(v0 + j) - oy);
 #pragma unroll
   for (int i = 0; i < K; ++i) B[i] = dy * ((double)(u0 + i) - ox);
+  // e > 0 || (tie && e == 0)  ==  e > thr: no double lies strictly between
+  // -denorm_min and 0, and fp64 compares do not flush denormals
+  const double thr = tie ? -4.9406564584124654e-324 : 0.0;
   uint32_t m = 0;
 #pragma unroll
   for (int j = 0; j < K; ++j)
 #pragma unroll
-    for (int i = 0; i < K; ++i) {
-      const double e = A[j] - B[i];
-      const bool c = e > 0 || (tie && e == 0);
-      m |= (uint32_t)c << (3 * j + i);
-    }
+    for (int i = 0; i < K; ++i)
+      if (A[j] - B[i] > thr) m |= 1u << (3 * j + i);
   return m;
 }
 
@@ -387,10 +390,82 @@ __device__ __forceinline__ double cheb_eval(const double* c, double x, double lo
 }
 
 constexpr float kBgDepth = 1e30f;
-constexpr int kThreads = 384;
+#ifndef B3D_THREADS
+#define B3D_THREADS 384
+#endif
+constexpr int kThreads = B3D_THREADS;
 constexpr int kWarps = kThreads / 32;
 
 }  // namespace
+
+// Pass 2 for the <= 2x2 class: lane l takes queue entry head + l (l < n)
+// and finishes it alone -- the 4 tile pixels' edge values (renderer.cpp:32-34
+// factored into 2 row and 2 column products per edge, bitwise the reference's
+// values), the top-left coverage rule (renderer.cpp:39-43), then for each
+// covered pixel the perspective 1/z, near/far tests, fp32 round and
+// strict-less z-test (renderer.cpp:94-100) from the same edge values.
+template <bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void drain_small(const KParams& p, Key* const zb, const Region& rg,
+                                            const VS& vs, const uint4* qt, const uint32_t* qb,
+                                            int head, int n, int lane) {
+  if (lane >= n) return;
+  const int s = (head + lane) & (kRing - 1);
+  const uint4 tr = qt[s];
+  const uint32_t box = qb[s];
+  const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
+  const double2 PA = vs.uv[tr.x], PB = vs.uv[tr.y], PC = vs.uv[tr.z];
+  const double px0 = (double)u0, py0 = (double)v0;
+  const double px1 = px0 + 1.0, py1 = py0 + 1.0;
+  // bit 2*j + i = pixel (u0 + i, v0 + j)
+  uint32_t cov = 1u | ((box >> 14) & 1u) << 1;
+  if (box >> 30) cov |= cov << 2;
+  double e[3][4];
+  const double2 P[3] = {PA, PB, PC};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double2 a = P[k], b = P[(k + 1) % 3];
+    const bool canon = a.x < b.x || (a.x == b.x && a.y < b.y);
+    const double dx = b.x - a.x, dy = b.y - a.y;
+    const bool tie = dy < 0 || (dy == 0 && dx > 0);
+    const double thr = tie ? -4.9406564584124654e-324 : 0.0;
+    const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+    const double A0 = dx * (py0 - oy), A1 = dx * (py1 - oy);
+    const double B0 = dy * (px0 - ox), B1 = dy * (px1 - ox);
+    e[k][0] = A0 - B0;
+    e[k][1] = A0 - B1;
+    e[k][2] = A1 - B0;
+    e[k][3] = A1 - B1;
+    uint32_t m = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (e[k][q] > thr) m |= 1u << q;
+    cov &= m;
+  }
+  if (!cov) return;
+  // area2 of the swapped order is bitwise the negated original
+  // (renderer.cpp:66-68): the two products are the same, only swapped
+  const double ia2 =
+      __drcp_rn((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
+  const double iza = vs.iz[tr.x], izb = vs.iz[tr.y], izc = vs.iz[tr.z];
+  Key* const cell0 = zb + (v0 - rg.oy) * rg.rw + (u0 - rg.ox);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (!((cov >> q) & 1u)) continue;
+    // e[0] = ab, e[1] = bc, e[2] = ca (renderer.cpp:94-95)
+    const double inv_z = (e[1][q] * iza + e[2][q] * izb + e[0][q] * izc) * ia2;
+    if (!(inv_z > 0)) continue;
+    const double z = __drcp_rn(inv_z);
+    if (z < p.near_lim || z > p.far_m) continue;
+    const float zf = __double2float_rn(z);
+    if (!(zf < p.far_f)) continue;
+    Key* cell = cell0 + (q >> 1) * rg.rw + (q & 1);
+    if (kIds)
+      zmin((unsigned long long*)cell, ((unsigned long long)__float_as_uint(zf) << 32) |
+                                          (unsigned long long)(p.draw_base + tr.w));
+    else
+      zmin((unsigned int*)cell, __float_as_uint(zf));
+  }
+}
 
 // Pass 2 of the raster: lane l takes queue entry head + l (l < n): edge
 // flags (renderer.cpp:39-47), KxK tile coverage; the covered pixels (~0.6
@@ -637,7 +712,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       tail1 += __popc(b1);
       __syncwarp();
       if (tail0 - head0 >= 32) {
-        drain_queue<2, kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, 32, lane);
+        drain_small<kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, 32, lane);
         head0 += 32;
       }
       if (tail1 - head1 >= 32) {
@@ -645,7 +720,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         head1 += 32;
       }
     }
-    if (tail0 > head0) drain_queue<2, kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, tail0 - head0, lane);
+    if (tail0 > head0) drain_small<kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, tail0 - head0, lane);
     if (tail1 > head1) drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, tail1 - head1, lane);
   }
   __syncthreads();

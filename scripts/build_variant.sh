@@ -1,0 +1,17 @@
+#!/bin/bash
+# Build a variant of libb3d_b200.so with extra nvcc defines for same-box A/B:
+#   scripts/build_variant.sh NAME -DFOO=1 ...   -> _ab/lib_NAME.so
+NAME=$1; shift
+cd "$(dirname "$0")/.."
+make -s -j4 -C paper_2312_08715_b200/csrc >/dev/null 2>&1 || exit 1
+T=$(mktemp -d)
+C=paper_2312_08715_b200/csrc
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 \
+  -Xptxas -v -Xcompiler -fPIC,-fvisibility=hidden,-O2 -Iinclude -I$C "$@" -c $C/render_score.cu \
+  -o $T/rs.o 2> $T/log || { cat $T/log; exit 1; }
+grep -E "spill" $T/log | head -1
+O=build/obj
+mkdir -p _ab
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o _ab/lib_$NAME.so \
+  $T/rs.o $O/stage.cu.o $O/image_score.cu.o $O/b3d_capi.cpp.o -Xlinker --no-undefined -lpthread -ldl -lrt
+rm -rf $T
