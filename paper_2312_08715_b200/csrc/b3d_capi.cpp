@@ -440,6 +440,7 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   size_t zcap = (budget - 32ull * lp.vcap - stage) / key;
   if (zcap > npx + 8 * (ctx->k.width + ctx->k.height) + 64)
     zcap = npx + 8 * (ctx->k.width + ctx->k.height) + 64;
+  zcap &= ~size_t(7);  // the vertex records after the z-buffer stay 32-byte aligned
   lp.zcap = (int)zcap;
   lp.smem = 32ull * lp.vcap + stage + key * zcap;
   int per_sm = 0;
@@ -468,6 +469,7 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.far_m = k.far_m;
   p.near_lim = k.near_m * (1.0 - 1e-12);
   p.far_f = static_cast<float>(k.far_m);
+
   p.W = (int)k.width;
   p.H = (int)k.height;
   p.fcx = (float)k.cx;

@@ -79,6 +79,7 @@ struct KeyT<true> {
   using T = unsigned long long;
 };
 
+// Strict-less z-test (renderer.cpp:99) as an atomic min on the key.
 __device__ __forceinline__ void zmin(unsigned int* p, unsigned int v) {
   if (v < *p) atomicMin(p, v);
 }
@@ -413,7 +414,7 @@ __device__ __forceinline__ void drain_small(const KParams& p, Key* const zb, con
   const uint4 tr = qt[s];
   const uint32_t box = qb[s];
   const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
-  const double2 PA = vs.uv[tr.x], PB = vs.uv[tr.y], PC = vs.uv[tr.z];
+  const double2 PA = vs.uv(tr.x), PB = vs.uv(tr.y), PC = vs.uv(tr.z);
   const double px0 = (double)u0, py0 = (double)v0;
   const double px1 = px0 + 1.0, py1 = py0 + 1.0;
   // bit 2*j + i = pixel (u0 + i, v0 + j)
@@ -446,7 +447,7 @@ __device__ __forceinline__ void drain_small(const KParams& p, Key* const zb, con
   // (renderer.cpp:66-68): the two products are the same, only swapped
   const double ia2 =
       __drcp_rn((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
-  const double iza = vs.iz[tr.x], izb = vs.iz[tr.y], izc = vs.iz[tr.z];
+  const double iza = vs.iz(tr.x), izb = vs.iz(tr.y), izc = vs.iz(tr.z);
   Key* const cell0 = zb + (v0 - rg.oy) * rg.rw + (u0 - rg.ox);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
@@ -461,7 +462,7 @@ __device__ __forceinline__ void drain_small(const KParams& p, Key* const zb, con
     Key* cell = cell0 + (q >> 1) * rg.rw + (q & 1);
     if (kIds)
       zmin((unsigned long long*)cell, ((unsigned long long)__float_as_uint(zf) << 32) |
-                                          (unsigned long long)(p.draw_base + tr.w));
+                                                  (unsigned long long)(p.draw_base + tr.w));
     else
       zmin((unsigned int*)cell, __float_as_uint(zf));
   }
@@ -485,7 +486,7 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
     const int s = (head + lane) & (kRing - 1);
     tr = qt[s];
     box = qb[s];
-    const double2 PA = vs.uv[tr.x], PB = vs.uv[tr.y], PC = vs.uv[tr.z];
+    const double2 PA = vs.uv(tr.x), PB = vs.uv(tr.y), PC = vs.uv(tr.z);
     const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
     fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
     const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
@@ -531,13 +532,13 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
       for (int k = item - st; k > 0; --k) m &= m - 1;  // k-th covered pixel
       const int bit = __ffs(m) - 1;
       const int pu = (int)(bx & 0x3fff) + bit % 3, pv = (int)((bx >> 16) & 0x3fff) + bit / 3;
-      const double2 A = vs.uv[ia], B = vs.uv[ib], C = vs.uv[ic];
+      const double2 A = vs.uv(ia), B = vs.uv(ib), C = vs.uv(ic);
       const double px = pu, py = pv;
       const double e_ab = edge_at(A, B, flo & 1, px, py);
       const double e_bc = edge_at(B, C, flo & 2, px, py);
       const double e_ca = edge_at(C, A, flo & 4, px, py);
       // renderer.cpp:94-100
-      const double inv_z = (e_bc * vs.iz[ia] + e_ca * vs.iz[ib] + e_ab * vs.iz[ic]) * ia2;
+      const double inv_z = (e_bc * vs.iz(ia) + e_ca * vs.iz(ib) + e_ab * vs.iz(ic)) * ia2;
       if (inv_z > 0) {
         const double z = __drcp_rn(inv_z);
         if (!(z < p.near_lim || z > p.far_m)) {
@@ -546,8 +547,8 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
             Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
             if (kIds)
               zmin((unsigned long long*)cell,
-                   ((unsigned long long)__float_as_uint(zf) << 32) |
-                       (unsigned long long)(p.draw_base + tri));
+                           ((unsigned long long)__float_as_uint(zf) << 32) |
+                               (unsigned long long)(p.draw_base + tri));
             else
               zmin((unsigned int*)cell, __float_as_uint(zf));
           }
@@ -662,15 +663,15 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         const uint4 tri = work_tri(ti);
 #endif
         uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
-        const short4 A = vs.bb[ia], B = vs.bb[ib], C = vs.bb[ic];
+        const short4 A = vs.bb(ia), B = vs.bb(ib), C = vs.bb(ic);
         if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
           raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
         } else {
           const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
           const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
           if (u_max != kOvf && v_max != kOvf && u_min <= u_max && v_min <= v_max) {
-            const double2 PA = vs.uv[ia];
-            double2 PB = vs.uv[ib], PC = vs.uv[ic];
+            const double2 PA = vs.uv(ia);
+            double2 PB = vs.uv(ib), PC = vs.uv(ic);
             double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
             if (area2 != 0 && !(cull > 0 ? area2 > 0 : (cull < 0 && area2 < 0))) {
               if (area2 < 0) {
@@ -689,8 +690,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                 box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
                       (uint32_t)(bh - 1) << 30;
               } else {  // large bbox: the reference's per-pixel loop
-                raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz[ia]},
-                                     SV{PB.x, PB.y, vs.iz[ib]}, SV{PC.x, PC.y, vs.iz[ic]},
+                raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz(ia)},
+                                     SV{PB.x, PB.y, vs.iz(ib)}, SV{PC.x, PC.y, vs.iz(ic)},
                                      u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
               }
             }
@@ -754,21 +755,23 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     // With a base image: |y| = base count - base pixels of the region +
     // composed pixels of the region (the halo holds base pixels too, so the
     // interior [u0,u1]x[v0,v1] is counted).
-    int cnt = 0;
-    const int iw = rg.u1 - rg.u0 + 1, ipx = iw * (rg.v1 - rg.v0 + 1);
-    for (int i = tid; i < ipx; i += kThreads) {
-      const int v = rg.v0 + i / iw, u = rg.u0 + (i - (i / iw) * iw);
-      const Key k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
-      const float z = __uint_as_float(
-          kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
-      cnt += z < p.far_f;
-      if (p.base_keys)
-        cnt -= __uint_as_float((unsigned int)(__ldg(p.base_keys + (size_t)v * p.W + u) >> 32)) <
-               p.far_f;
+    {
+      int cnt = 0;
+      const int iw = rg.u1 - rg.u0 + 1, ipx = iw * (rg.v1 - rg.v0 + 1);
+      for (int i = tid; i < ipx; i += kThreads) {
+        const int v = rg.v0 + i / iw, u = rg.u0 + (i - (i / iw) * iw);
+        const Key k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+        const float z = __uint_as_float(
+            kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
+        cnt += z < p.far_f;
+        if (p.base_keys)
+          cnt -= __uint_as_float((unsigned int)(__ldg(p.base_keys + (size_t)v * p.W + u) >> 32)) <
+                 p.far_f;
+      }
+      cnt = warp_sum_i(cnt);
+      if (lane == 0 && cnt) atomicAdd(s_count, cnt);
+      __syncthreads();
     }
-    cnt = warp_sum_i(cnt);
-    if (lane == 0 && cnt) atomicAdd(s_count, cnt);
-    __syncthreads();
     const int rend_count = *s_count + p.base_valid;
     if (rend_count == 0) {  // (never with a non-empty base image)
       // the reference throws (likelihood.cpp:159-160); batched callers get
@@ -808,19 +811,19 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       npos[e] = 0;
     }
     for (int i = tid; i < dpx; i += kThreads) {
-      const int v = dv0 + i / dw;
-      const int u = du0 + (i - (v - dv0) * dw);
-      const float4 o = __ldg(p.obs + (size_t)v * p.W + u);
+      const int pv = dv0 + i / dw;
+      const int pu = du0 + (i - (pv - dv0) * dw);
+      const float4 o = __ldg(p.obs + (size_t)pv * p.W + pu);
       if (o.w == 0.f) continue;
       float S[kMaxNoise];
-      window_sums<kIds>(p, zb, rg, u, v, o, S);
+      window_sums<kIds>(p, zb, rg, pu, pv, o, S);
       if (p.base_keys) {
         // g(S) - g(S_base): the pixel's term relative to the base-only sum G
 #pragma unroll
         for (int e = 0; e < kMaxNoise; ++e) {
           if (e < p.lik.n_noise) {
             const int sl = p.lik.slot_of[e];
-            const float Sb = __ldg(p.sbase + (size_t)sl * p.W * p.H + (size_t)v * p.W + u);
+            const float Sb = __ldg(p.sbase + (size_t)sl * p.W * p.H + (size_t)pv * p.W + pu);
             if (S[sl] != Sb)
               acc[e] += (double)(__logf(floor_f[e] + coef_f[e] * S[sl]) -
                                  __logf(floor_f[e] + coef_f[e] * Sb));
@@ -879,10 +882,23 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
 
 // Projected-vertex cache: (u, v) and 1/z in fp64 plus the packed integer
 // bbox, in shared memory (kVS) or in the CTA's global scratch.
+// Projected-vertex cache, structure of arrays (random gathers of 16-byte
+// (u, v) pairs hit all bank groups): uv[n] | iz[n] | bb[n].
 struct VertexCache {
-  double2* uv;
-  double* iz;
-  short4* bb;
+  double2* uvp;
+  double* izp;
+  short4* bbp;
+  __device__ __forceinline__ double2 uv(uint32_t i) const { return uvp[i]; }
+  __device__ __forceinline__ double iz(uint32_t i) const { return izp[i]; }
+  __device__ __forceinline__ short4 bb(uint32_t i) const { return bbp[i]; }
+  __device__ __forceinline__ void put(uint32_t i, double u, double v, double iz, short4 bb) const {
+    uvp[i] = make_double2(u, v);
+    izp[i] = iz;
+    bbp[i] = bb;
+  }
+  __device__ __forceinline__ void put_clipped(uint32_t i) const {
+    bbp[i] = make_short4(kClipV, 0, 0, 0);
+  }
 };
 
 // kIds: 64-bit (depth, draw) keys; kScore: run the likelihood epilogue;
@@ -902,23 +918,22 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
-  // dynamic shared memory: [(u,v) | 1/z | packed bbox] x vcap vertices,
-  // per-warp triangle records, region z-buffer
-  double* const sv_s = reinterpret_cast<double*>(smem_raw);
+  // dynamic shared memory: per-warp triangle queues, region z-buffer (zcap
+  // keys, a multiple of 8), projected-vertex cache (vcap x 32 B; in the CTA's
+  // global scratch when the mesh does not fit).  The first two start at
+  // compile-time offsets.
+  WarpQ* const wq = reinterpret_cast<WarpQ*>(smem_raw);
+  Key* const zb_s = reinterpret_cast<Key*>(smem_raw + sizeof(WarpQ) * kWarps);
   VertexCache vs;
-  if (kVS) {
-    vs.uv = reinterpret_cast<double2*>(sv_s);
-    vs.iz = sv_s + 2 * (size_t)p.vcap;
-    vs.bb = reinterpret_cast<short4*>(sv_s + 3 * (size_t)p.vcap);
-  } else {
-    double* const g = p.vscratch + (size_t)blockIdx.x * 4 * p.nv;
-    vs.uv = reinterpret_cast<double2*>(g);
-    vs.iz = g + 2 * (size_t)p.nv;
-    vs.bb = reinterpret_cast<short4*>(g + 3 * (size_t)p.nv);
+  {
+    const int n = kVS ? p.vcap : p.nv;
+    double* const b = kVS ? reinterpret_cast<double*>(smem_raw + sizeof(WarpQ) * kWarps +
+                                                      (size_t)p.zcap * sizeof(Key))
+                          : p.vscratch + (size_t)blockIdx.x * 4 * p.nv;
+    vs.uvp = reinterpret_cast<double2*>(b);
+    vs.izp = b + 2 * (size_t)n;
+    vs.bbp = reinterpret_cast<short4*>(b + 3 * (size_t)n);
   }
-  const int vcap = kVS ? p.vcap : 0;
-  WarpQ* const wq = reinterpret_cast<WarpQ*>(sv_s + 4 * (size_t)vcap);
-  Key* const zb_s = reinterpret_cast<Key*>(wq + kWarps);
 
   int kk = 0;  // hypotheses this CTA has processed
   for (long long h = blockIdx.x; h < p.n_hyp; h += gridDim.x, ++kk) {
@@ -957,16 +972,14 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
       cam_vertex(R, t, p.verts + 3 * (size_t)i, c);
       if (c[2] >= p.near_m) {
         const SV s = project(p, c[0], c[1], c[2]);
-        vs.uv[i] = make_double2(s.u, s.v);
-        vs.iz[i] = s.iz;
         const short4 bb = vertex_bbox(p, s.u, s.v);
-        vs.bb[i] = bb;
+        vs.put(i, s.u, s.v, s.iz, bb);
         lo_u = min(lo_u, (int)bb.x);
         hi_u = max(hi_u, bb.y == kOvf ? p.W - 1 : (int)bb.y);
         lo_v = min(lo_v, (int)bb.z);
         hi_v = max(hi_v, bb.w == kOvf ? p.H - 1 : (int)bb.w);
       } else {
-        vs.bb[i] = make_short4(kClipV, 0, 0, 0);
+        vs.put_clipped(i);
         clip = 1;
       }
     }
