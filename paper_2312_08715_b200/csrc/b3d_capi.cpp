@@ -404,6 +404,7 @@ const void* stage_in(b3d_gpu_context* ctx, DevBuf& buf, const void* src, size_t 
 struct LaunchPlan {
   long long zstride = 0;
   int grid = 0;
+  int cap = 0;
   size_t smem = 0;
   int vcap = 0;
   int zcap = 0;
@@ -447,14 +448,16 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   cuda_check(occupancy_render_score<kIds, kScore, kOut>(&per_sm, lp.smem, lp.vcap >= m.nv), "occupancy");
   if (per_sm < 1) per_sm = 1;
   long long grid = (long long)per_sm * ctx->sm_count;
+  lp.cap = (int)grid;  // resident capacity: score launches may pair CTAs on the batch tail
   if (grid > n) grid = n;
   if (grid < 1) grid = 1;
   lp.grid = (int)grid;
   // overflow scratch for hypotheses whose region / mesh exceeds shared memory
   const int pad = kScore ? 2 * (window >= 0 ? window : ctx->lik.window) : 0;
   lp.zstride = (long long)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
-  ctx->zscratch.ensure((size_t)lp.grid * lp.zstride * 8);
-  if (lp.vcap < m.nv) ctx->vscratch.ensure((size_t)lp.grid * 32 * m.nv);
+  const size_t ctas = kScore ? (size_t)lp.cap : (size_t)lp.grid;
+  ctx->zscratch.ensure(ctas * lp.zstride * 8);
+  if (lp.vcap < m.nv) ctx->vscratch.ensure(ctas * 32 * m.nv);
   return lp;
 }
 
@@ -757,7 +760,7 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   p.vcap = lp.vcap;
   p.zcap = lp.zcap;
   p.zstride = lp.zstride;
-  cuda_check(launch_render_score<false, true, false>(p, lp.grid, lp.smem, ctx->stream),
+  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
              "render_score launch");
   bool sync = host_in;
   if (!dev_scores) {
@@ -1223,8 +1226,7 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
       p.vcap = lp.vcap;
       p.zcap = lp.zcap;
       p.zstride = lp.zstride;
-      const int grid = (int)std::min<long long>(lp.grid, (long long)n[s]);
-      cuda_check(launch_render_score<false, true, false>(p, grid, lp.smem, ctx->stream),
+      cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
                  "render_score launch");
       const bool sample = g.select == B3D_SELECT_SAMPLE;
       cuda_check(launch_stage_reduce(p.scores, (long long)n[s], 1, 0, sample ? d_rng : nullptr,
@@ -1407,7 +1409,7 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     p.vcap = lp.vcap;
     p.zcap = lp.zcap;
     p.zstride = lp.zstride;
-    cuda_check(launch_render_score<false, true, false>(p, lp.grid, lp.smem, ctx->stream),
+    cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
                "render_score launch");
     unsigned long long* d_rng = nullptr;
     const bool dev_rng = rng_state && is_device_ptr(rng_state);

@@ -1,0 +1,1080 @@
+// render_score.cuh -- fused per-hypothesis rasterizer + windowed likelihood
+// for sm_100a.  One CTA owns one hypothesis at a time (persistent over a
+// strided hypothesis range):
+//
+//   A  pose     : hypothesis pose (array or on-device grid), compose with
+//                 inverse(camera), rotation matrix              (fp64, no FMA)
+//   B  vertices : R*v + t, project to (u, v, 1/z) into shared memory, and
+//                 the screen-space region the object can touch  (fp64)
+//   C  raster   : thread per triangle, reference edge functions + top-left
+//                 rule, perspective 1/z, strict-less z-test via a shared
+//                 memory atomicMin on fp32 depth bits (or on the 64-bit key
+//                 (depth bits, draw index) when ids are requested)
+//   D  score    : |y| count, then thread per pixel of the window-dilated
+//                 region: sum_window exp(-d^2 / 2 sigma^2) over valid
+//                 rendered pixels, log(floor + coef*S), fp64 block reduction
+//
+// The rendered image never leaves the SM in score mode.  The arithmetic of
+// A-C follows renderer.cpp:61-151 / geometry.cpp:19-31 operation by
+// operation (this TU is compiled with --fmad=false), so depth and ids are
+// bit-identical to the CPU oracle.  D follows likelihood.cpp:128-220 with
+// fp32 distances/exp/log and fp64 accumulation (north_star: 1e-4 relative).
+#pragma once
+
+#include <algorithm>
+#include <cfloat>
+#include <climits>
+#include <cstdint>
+#include <type_traits>
+
+
+#include "b3d_kernels.cuh"
+#include "posemath.cuh"
+
+#ifndef B3D_PREFETCH
+#define B3D_PREFETCH 0
+#endif
+
+namespace b3d200 {
+
+namespace {
+
+using namespace pm;
+
+
+struct SV {
+  double u, v, iz;
+};
+
+// renderer.cpp:26-59.  EdgeFn::eval is sign*(cdx*(py-oy) - cdy*(px-ox))
+// with (cdx, cdy) = hi - lo of the canonically ordered endpoints.  Since
+// sign*cdx == b.u - a.u bitwise (round-to-nearest is antisymmetric) and
+// sign*(X - Y) == (sign*X') - (sign*Y') with X' = cdx*A, the edge value is
+// (b.u-a.u)*(py-oy) - (b.v-a.v)*(px-ox) with the canonical origin o: the same
+// bits except possibly the sign of an exact zero, which neither the fill
+// rule (e > 0 / e < 0 / tie) nor the 1/z test (inv_z <= 0) can observe.
+struct Edge {
+  double ox, oy, dx, dy;
+};
+
+__device__ __forceinline__ Edge make_edge(const SV& a, const SV& b) {
+  const bool canonical = a.u < b.u || (a.u == b.u && a.v < b.v);
+  Edge e;
+  e.ox = canonical ? a.u : b.u;
+  e.oy = canonical ? a.v : b.v;
+  e.dx = b.u - a.u;
+  e.dy = b.v - a.v;
+  return e;
+}
+
+__device__ __forceinline__ bool covers(const Edge& e, double v) {
+  if (v > 0) return true;
+  if (v < 0) return false;
+  return e.dy < 0 || (e.dy == 0 && e.dx > 0);
+}
+
+template <bool kIds>
+struct KeyT;
+template <>
+struct KeyT<false> {
+  using T = unsigned int;
+};
+template <>
+struct KeyT<true> {
+  using T = unsigned long long;
+};
+
+// Strict-less z-test (renderer.cpp:99) as an atomic min on the key.
+__device__ __forceinline__ void zmin(unsigned int* p, unsigned int v) {
+  if (v < *p) atomicMin(p, v);
+}
+__device__ __forceinline__ void zmin(unsigned long long* p, unsigned long long v) {
+  if (v < *p) atomicMin(p, v);
+}
+
+// Screen region of one hypothesis: interior [u0,u1]x[v0,v1] (clipped to the
+// image) that the object can touch, stored with a background halo of `pad`
+// pixels so the likelihood's window taps never need bounds checks.
+// Buffer index of pixel (u, v): (v - oy) * rw + (u - ox).
+struct Region {
+  int u0, v0, u1, v1, ox, oy, rw, rh;
+};
+
+// renderer.cpp:63-102 for a triangle whose integer pixel bbox is known.
+template <bool kIds>
+__device__ __forceinline__ void raster_tri_box(const KParams& p, typename KeyT<kIds>::T* zb,
+                                               const Region& rg, SV a, SV b, SV c, int u_min,
+                                               int u_max, int v_min, int v_max, uint32_t draw) {
+  double area2 = (b.u - a.u) * (c.v - a.v) - (b.v - a.v) * (c.u - a.u);
+  if (area2 == 0) return;
+  if (area2 < 0) {
+    const SV t = b;
+    b = c;
+    c = t;
+    area2 = -area2;
+  }
+  const Edge ab = make_edge(a, b);
+  const Edge bc = make_edge(b, c);
+  const Edge ca = make_edge(c, a);
+  const double inv_area2 = __drcp_rn(area2);
+  for (int pv = v_min; pv <= v_max; ++pv) {
+    const double py = pv;
+    const double r_ab = ab.dx * (py - ab.oy);
+    const double r_bc = bc.dx * (py - bc.oy);
+    const double r_ca = ca.dx * (py - ca.oy);
+    typename KeyT<kIds>::T* row = zb + (pv - rg.oy) * rg.rw - rg.ox;
+    for (int pu = u_min; pu <= u_max; ++pu) {
+      const double px = pu;
+      const double e_ab = r_ab - ab.dy * (px - ab.ox);
+      const double e_bc = r_bc - bc.dy * (px - bc.ox);
+      const double e_ca = r_ca - ca.dy * (px - ca.ox);
+      if (!covers(ab, e_ab) || !covers(bc, e_bc) || !covers(ca, e_ca)) continue;
+      const double inv_z = (e_bc * a.iz + e_ca * b.iz + e_ab * c.iz) * inv_area2;
+      if (inv_z <= 0) continue;
+      const double z = __drcp_rn(inv_z);
+      if (z < p.near_lim || z > p.far_m) continue;
+      const float zf = __double2float_rn(z);
+      if (!(zf < p.far_f)) continue;
+      if (kIds) {
+        const unsigned long long key =
+            ((unsigned long long)__float_as_uint(zf) << 32) | (unsigned long long)draw;
+        zmin((unsigned long long*)(row + pu), key);
+      } else {
+        zmin((unsigned int*)(row + pu), __float_as_uint(zf));
+      }
+    }
+  }
+}
+
+// renderer.cpp:61-103 -- one screen triangle into the region z-buffer
+// (clipped path: the bbox comes from the fp64 vertex coordinates).  The
+// bounds reproduce static_cast<int> on x86-64 exactly: a max u or v beyond
+// the int range converts to INT_MIN there and empties the bbox.
+template <bool kIds>
+__device__ __forceinline__ void raster_tri(const KParams& p, typename KeyT<kIds>::T* zb,
+                                           const Region& rg, SV a, SV b, SV c, uint32_t draw) {
+  const double mnu = fmin(fmin(a.u, b.u), c.u), mxu = fmax(fmax(a.u, b.u), c.u);
+  const double mnv = fmin(fmin(a.v, b.v), c.v), mxv = fmax(fmax(a.v, b.v), c.v);
+  if (!(mxu < 2147483648.0) || !(mxv < 2147483648.0)) return;
+  const double cu0 = fmax(ceil(mnu), 0.0), fu1 = fmin(floor(mxu), (double)(p.W - 1));
+  const double cv0 = fmax(ceil(mnv), 0.0), fv1 = fmin(floor(mxv), (double)(p.H - 1));
+  if (cu0 > fu1 || cv0 > fv1) return;
+  raster_tri_box<kIds>(p, zb, rg, a, b, c, (int)cu0, (int)fu1, (int)cv0, (int)fv1, draw);
+}
+
+__device__ __forceinline__ SV project(const KParams& p, double x, double y, double z) {
+  const double iz = __drcp_rn(z);
+  SV s;
+  s.u = p.fx * x * iz + p.cx;
+  s.v = p.fy * y * iz + p.cy;
+  s.iz = iz;
+  return s;
+}
+
+__device__ __forceinline__ void cam_vertex(const double* R, const double* t, const double* v,
+                                           double o[3]) {
+  // Eigen 3x3 * 3x1 lazy product, scalar redux a0 + (a1 + a2), then + t
+  o[0] = (R[0] * v[0] + (R[1] * v[1] + R[2] * v[2])) + t[0];
+  o[1] = (R[3] * v[0] + (R[4] * v[1] + R[5] * v[2])) + t[1];
+  o[2] = (R[6] * v[0] + (R[7] * v[1] + R[8] * v[2])) + t[2];
+}
+
+// Packed per-vertex integer bbox data (screen bounds of one vertex), used to
+// reject triangles and size their pixel bbox with integer min/max:
+//   x = ceil(u) clamped to [0, W], y = floor(u) clamped to [-1, W-1] or
+//   kOvf when u >= 2^31 (the reference's static_cast<int> then yields INT_MIN
+//   and an empty bbox, renderer.cpp:70-76), z/w the same for v;
+//   x = kClipV marks a vertex in front of z = near (clipped path).
+constexpr short kOvf = 32767;
+constexpr short kClipV = -32768;
+
+__device__ __forceinline__ short4 vertex_bbox(const KParams& p, double u, double v) {
+  // fp64 -> int conversions with directed rounding saturate (PTX cvt), so
+  // ceil/floor + clamp need no fp64 min/max; |u|, |v| >= 2^31 behave like the
+  // clamped fp64 forms (upload rejects non-finite vertices)
+  short4 r;
+  r.x = (short)min(max(__double2int_ru(u), 0), p.W);
+  r.y = u >= 2147483648.0 ? kOvf : (short)min(max(__double2int_rd(u), -1), p.W - 1);
+  r.z = (short)min(max(__double2int_ru(v), 0), p.H);
+  r.w = v >= 2147483648.0 ? kOvf : (short)min(max(__double2int_rd(v), -1), p.H - 1);
+  return r;
+}
+
+// Per-warp queues of triangles that survive the cheap tests (non-empty
+// integer bbox, non-zero area, not culled), one ring per tile class
+// (bbox <= 2x2 and <= 3x3).  Entry: vertex ids after the orientation swap
+// (renderer.cpp:63-69) + triangle index, and the packed bbox
+// u_min | (bw-1) << 14 | v_min << 16 | (bh-1) << 30.
+constexpr int kRing = 64;
+struct WarpQ {
+  uint4 tri[2][kRing];
+  uint32_t box[2][kRing];
+};
+
+// Coverage of one edge over a KxK pixel tile at (u0, v0): the reference's
+// edge value dx*(py - oy) - dy*(px - ox) (renderer.cpp:32-34, canonical
+// origin) factored into K row products and K column products -- the same
+// two fp64 products and difference per pixel, so bitwise the same values --
+// and the top-left rule (renderer.cpp:39-43).  Bit 3*j + i = pixel
+// (u0 + i, v0 + j).
+template <int K>
+__device__ __forceinline__ uint32_t tile_edge_mask(double2 a, double2 b, bool canon, bool tie,
+                                                   int u0, int v0) {
+  const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+  const double dx = b.x - a.x, dy = b.y - a.y;
+  double A[K], B[K];
+#pragma unroll
+  for (int j = 0; j < K; ++j) A[j] = dx * ((double)(v0 + j) - oy);
+#pragma unroll
+  for (int i = 0; i < K; ++i) B[i] = dy * ((double)(u0 + i) - ox);
+  // e > 0 || (tie && e == 0)  ==  e > thr: no double lies strictly between
+  // -denorm_min and 0, and fp64 compares do not flush denormals
+  const double thr = tie ? -4.9406564584124654e-324 : 0.0;
+  uint32_t m = 0;
+#pragma unroll
+  for (int j = 0; j < K; ++j)
+#pragma unroll
+    for (int i = 0; i < K; ++i)
+      if (A[j] - B[i] > thr) m |= 1u << (3 * j + i);
+  return m;
+}
+
+// Edge flags: bit e = canonical origin is the edge's first vertex
+// (renderer.cpp:47), bit 3+e = pixels exactly on the edge are covered
+// (top-left rule, renderer.cpp:39-43).
+__device__ __forceinline__ int edge_flags(const SV& a, const SV& b, int e) {
+  const bool canonical = a.u < b.u || (a.u == b.u && a.v < b.v);
+  const double dx = b.u - a.u, dy = b.v - a.v;
+  const bool tie = dy < 0 || (dy == 0 && dx > 0);
+  return ((int)canonical << e) | ((int)tie << (3 + e));
+}
+
+// Edge value of the directed edge (a -> b) at (px, py) with the canonical
+// origin selected by `canon` -- bitwise the reference's EdgeFn::eval.
+__device__ __forceinline__ double edge_at(double2 a, double2 b, bool canon, double px,
+                                          double py) {
+  const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+  return (b.x - a.x) * (py - oy) - (b.y - a.y) * (px - ox);
+}
+
+__device__ __forceinline__ bool edge_covers(double e, bool tie) {
+  return e > 0 || (e == 0 && tie);
+}
+
+// renderer.cpp:124-150 for a triangle with a vertex in front of z = near.
+template <bool kIds>
+__device__ void raster_clipped(const KParams& p, typename KeyT<kIds>::T* zb,
+                               const Region& rg, const double* R, const double* t,
+                               uint32_t i0, uint32_t i1, uint32_t i2, uint32_t draw) {
+  double v[3][3];
+  cam_vertex(R, t, p.verts + 3 * (size_t)i0, v[0]);
+  cam_vertex(R, t, p.verts + 3 * (size_t)i1, v[1]);
+  cam_vertex(R, t, p.verts + 3 * (size_t)i2, v[2]);
+  double poly[4][3];
+  int n = 0;
+  for (int i = 0; i < 3; ++i) {
+    const double* cur = v[i];
+    const double* nxt = v[(i + 1) % 3];
+    const bool cin = cur[2] >= p.near_m;
+    const bool nin = nxt[2] >= p.near_m;
+    if (cin) {
+      poly[n][0] = cur[0];
+      poly[n][1] = cur[1];
+      poly[n][2] = cur[2];
+      ++n;
+    }
+    if (cin != nin) {
+      const double s = (p.near_m - cur[2]) / (nxt[2] - cur[2]);
+      for (int k = 0; k < 3; ++k) poly[n][k] = cur[k] + s * (nxt[k] - cur[k]);
+      ++n;
+    }
+  }
+  if (n < 3) return;
+  const SV s0 = project(p, poly[0][0], poly[0][1], poly[0][2]);
+  SV prev = project(p, poly[1][0], poly[1][1], poly[1][2]);
+  for (int i = 2; i < n; ++i) {
+    const SV cur = project(p, poly[i][0], poly[i][1], poly[i][2]);
+    raster_tri<kIds>(p, zb, rg, s0, prev, cur, draw);
+    prev = cur;
+  }
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ int warp_sum_i(int v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// sum over the (2w+1)^2 window of exp(-|o - r|^2 / (2 sigma^2)) per distinct
+// sigma (likelihood.cpp:198-214) in fp32: rendered points back-projected on
+// the fly from the region buffer, exp as ex2 with the scale pre-multiplied
+// by log2(e).  Background taps give d^2 >= (far - z_obs)^2 and an exact 0.
+template <bool kIds, int kW, bool kS1>
+__device__ __forceinline__ void window_sums_w(const KParams& p,
+                                              const typename KeyT<kIds>::T* zb,
+                                              const Region& rg, int u, int v, float4 o,
+                                              float S[kMaxNoise]) {
+#pragma unroll
+  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  const float cu0 = ((float)(u - kW) - p.fcx) * p.inv_fx;
+  const float cv0 = ((float)(v - kW) - p.fcy) * p.inv_fy;
+  const typename KeyT<kIds>::T* row0 = zb + (v - kW - rg.oy) * rg.rw + (u - kW - rg.ox);
+#pragma unroll
+  for (int j = 0; j < 2 * kW + 1; ++j) {
+    const float cv = cv0 + (float)j * p.inv_fy;
+#pragma unroll
+    for (int k = 0; k < 2 * kW + 1; ++k) {
+      const typename KeyT<kIds>::T key = row0[j * rg.rw + k];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+      const float cu = cu0 + (float)k * p.inv_fx;
+      const float dx = __fmaf_rn(-cu, z, o.x);
+      const float dy = __fmaf_rn(-cv, z, o.y);
+      const float dz = o.z - z;
+      const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
+#pragma unroll
+      for (int s = 0; s < (kS1 ? 1 : kMaxNoise); ++s)
+        if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+    }
+  }
+}
+
+template <bool kIds, bool kS1>
+__device__ __forceinline__ void window_sums_any(const KParams& p,
+                                                const typename KeyT<kIds>::T* zb,
+                                                const Region& rg, int u, int v, float4 o,
+                                                float S[kMaxNoise]) {
+#pragma unroll
+  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  const int w = p.lik.window;
+  for (int rv = v - w; rv <= v + w; ++rv) {
+    const float cv = ((float)rv - p.fcy) * p.inv_fy;
+    for (int ru = u - w; ru <= u + w; ++ru) {
+      const typename KeyT<kIds>::T key = zb[(rv - rg.oy) * rg.rw + (ru - rg.ox)];
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+      const float cu = ((float)ru - p.fcx) * p.inv_fx;
+      const float dx = __fmaf_rn(-cu, z, o.x);
+      const float dy = __fmaf_rn(-cv, z, o.y);
+      const float dz = o.z - z;
+      const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
+#pragma unroll
+      for (int s = 0; s < (kS1 ? 1 : kMaxNoise); ++s)
+        if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+    }
+  }
+}
+
+// kWin >= 0: the launch's window radius as a compile-time constant (one
+// unrolled tap loop per kernel instantiation); kWin < 0: any radius.  kS1:
+// a single distinct sigma.
+template <bool kIds, int kWin, bool kS1>
+__device__ __forceinline__ void window_sums(const KParams& p, const typename KeyT<kIds>::T* zb,
+                                            const Region& rg, int u, int v, float4 o,
+                                            float S[kMaxNoise]) {
+  if constexpr (kWin >= 0)
+    window_sums_w<kIds, kWin, kS1>(p, zb, rg, u, v, o, S);
+  else
+    window_sums_any<kIds, kS1>(p, zb, rg, u, v, o, S);
+}
+
+template <bool kIds>
+__device__ __forceinline__ void window_sums_rt(const KParams& p, const typename KeyT<kIds>::T* zb,
+                                               const Region& rg, int u, int v, float4 o,
+                                               float S[kMaxNoise]) {
+  switch (p.lik.window) {
+    case 0: window_sums_w<kIds, 0, false>(p, zb, rg, u, v, o, S); break;
+    case 1: window_sums_w<kIds, 1, false>(p, zb, rg, u, v, o, S); break;
+    case 2: window_sums_w<kIds, 2, false>(p, zb, rg, u, v, o, S); break;
+    case 3: window_sums_w<kIds, 3, false>(p, zb, rg, u, v, o, S); break;
+    default: window_sums_any<kIds, false>(p, zb, rg, u, v, o, S); break;
+  }
+}
+
+// Clenshaw evaluation of a Chebyshev series on [lo, hi].
+__device__ __forceinline__ double cheb_eval(const double* c, double x, double lo, double hi) {
+  const double t = (2.0 * x - (lo + hi)) / (hi - lo);
+  double b1 = 0.0, b2 = 0.0;
+  for (int j = kCheb - 1; j >= 1; --j) {
+    const double b0 = 2.0 * t * b1 - b2 + c[j];
+    b2 = b1;
+    b1 = b0;
+  }
+  return t * b1 - b2 + 0.5 * c[0];
+}
+
+constexpr float kBgDepth = 1e30f;
+#ifndef B3D_THREADS
+#define B3D_THREADS 384
+#endif
+constexpr int kThreads = B3D_THREADS;
+constexpr int kWarps = kThreads / 32;
+
+}  // namespace
+
+// Pass 2 for the <= 2x2 class: lane l takes queue entry head + l (l < n)
+// and finishes it alone -- the 4 tile pixels' edge values (renderer.cpp:32-34
+// factored into 2 row and 2 column products per edge, bitwise the reference's
+// values), the top-left coverage rule (renderer.cpp:39-43), then for each
+// covered pixel the perspective 1/z, near/far tests, fp32 round and
+// strict-less z-test (renderer.cpp:94-100) from the same edge values.
+template <bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void drain_small(const KParams& p, Key* const zb, const Region& rg,
+                                            const VS& vs, const uint4* qt, const uint32_t* qb,
+                                            int head, int n, int lane) {
+  if (lane >= n) return;
+  const int s = (head + lane) & (kRing - 1);
+  const uint4 tr = qt[s];
+  const uint32_t box = qb[s];
+  const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
+  const double2 PA = vs.uv(tr.x), PB = vs.uv(tr.y), PC = vs.uv(tr.z);
+  const double px0 = (double)u0, py0 = (double)v0;
+  const double px1 = px0 + 1.0, py1 = py0 + 1.0;
+  // bit 2*j + i = pixel (u0 + i, v0 + j)
+  uint32_t cov = 1u | ((box >> 14) & 1u) << 1;
+  if (box >> 30) cov |= cov << 2;
+  double e[3][4];
+  const double2 P[3] = {PA, PB, PC};
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const double2 a = P[k], b = P[(k + 1) % 3];
+    const bool canon = a.x < b.x || (a.x == b.x && a.y < b.y);
+    const double dx = b.x - a.x, dy = b.y - a.y;
+    const bool tie = dy < 0 || (dy == 0 && dx > 0);
+    const double thr = tie ? -4.9406564584124654e-324 : 0.0;
+    const double ox = canon ? a.x : b.x, oy = canon ? a.y : b.y;
+    const double A0 = dx * (py0 - oy), A1 = dx * (py1 - oy);
+    const double B0 = dy * (px0 - ox), B1 = dy * (px1 - ox);
+    e[k][0] = A0 - B0;
+    e[k][1] = A0 - B1;
+    e[k][2] = A1 - B0;
+    e[k][3] = A1 - B1;
+    uint32_t m = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (e[k][q] > thr) m |= 1u << q;
+    cov &= m;
+  }
+  if (!cov) return;
+  // area2 of the swapped order is bitwise the negated original
+  // (renderer.cpp:66-68): the two products are the same, only swapped
+  const double ia2 =
+      __drcp_rn((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
+  const double iza = vs.iz(tr.x), izb = vs.iz(tr.y), izc = vs.iz(tr.z);
+  Key* const cell0 = zb + (v0 - rg.oy) * rg.rw + (u0 - rg.ox);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    if (!((cov >> q) & 1u)) continue;
+    // e[0] = ab, e[1] = bc, e[2] = ca (renderer.cpp:94-95)
+    const double inv_z = (e[1][q] * iza + e[2][q] * izb + e[0][q] * izc) * ia2;
+    if (!(inv_z > 0)) continue;
+    const double z = __drcp_rn(inv_z);
+    if (z < p.near_lim || z > p.far_m) continue;
+    const float zf = __double2float_rn(z);
+    if (!(zf < p.far_f)) continue;
+    Key* cell = cell0 + (q >> 1) * rg.rw + (q & 1);
+    if (kIds)
+      zmin((unsigned long long*)cell, ((unsigned long long)__float_as_uint(zf) << 32) |
+                                                  (unsigned long long)(p.draw_base + tr.w));
+    else
+      zmin((unsigned int*)cell, __float_as_uint(zf));
+  }
+}
+
+// Pass 2 of the raster: lane l takes queue entry head + l (l < n): edge
+// flags (renderer.cpp:39-47), KxK tile coverage; the covered pixels (~0.6
+// per triangle) are then dealt one per lane -- owner found by a 5-step
+// shuffle search over the exclusive scan of coverage counts -- for the
+// perspective 1/z, the near/far tests, the fp32 round and the strict-less
+// z-test (renderer.cpp:94-100) with every lane busy.
+template <int K, bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, const Region& rg,
+                                            const VS& vs, const uint4* qt, const uint32_t* qb,
+                                            int head, int n, int lane) {
+  uint32_t cov = 0, box = 0;
+  uint4 tr = make_uint4(0u, 0u, 0u, 0u);
+  int fl = 0;
+  double inv_area2 = 0.0;
+  if (lane < n) {
+    const int s = (head + lane) & (kRing - 1);
+    tr = qt[s];
+    box = qb[s];
+    const double2 PA = vs.uv(tr.x), PB = vs.uv(tr.y), PC = vs.uv(tr.z);
+    const SV a{PA.x, PA.y, 0.0}, b{PB.x, PB.y, 0.0}, c{PC.x, PC.y, 0.0};
+    fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+    const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
+    const int bw = ((box >> 14) & 3) + 1, bh = (int)(box >> 30) + 1;
+    const uint32_t colm = (1u << bw) - 1u;
+    uint32_t valid = colm;
+    if (bh > 1) valid |= colm << 3;
+    if (K > 2 && bh > 2) valid |= colm << 6;
+    cov = valid & tile_edge_mask<K>(PA, PB, fl & 1, fl & 8, u0, v0) &
+          tile_edge_mask<K>(PB, PC, fl & 2, fl & 16, u0, v0) &
+          tile_edge_mask<K>(PC, PA, fl & 4, fl & 32, u0, v0);
+    // area2 of the swapped order is bitwise the negated original
+    // (renderer.cpp:66-68): the two products are the same, only swapped
+    if (cov) inv_area2 = __drcp_rn((PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x));
+  }
+  const int cnt = __popc(cov);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int start = incl - cnt;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int c0 = 0; c0 < total; c0 += 32) {
+    const int item = c0 + lane;
+    int own = 0;  // last lane whose start <= item (never a zero-count lane)
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1) {
+      const int sp = __shfl_sync(0xffffffffu, start, own + step);
+      if (sp <= item) own += step;
+    }
+    const int st = __shfl_sync(0xffffffffu, start, own);
+    uint32_t m = __shfl_sync(0xffffffffu, cov, own);
+    const uint32_t bx = __shfl_sync(0xffffffffu, box, own);
+    const int flo = __shfl_sync(0xffffffffu, fl, own);
+    const uint32_t ia = __shfl_sync(0xffffffffu, tr.x, own);
+    const uint32_t ib = __shfl_sync(0xffffffffu, tr.y, own);
+    const uint32_t ic = __shfl_sync(0xffffffffu, tr.z, own);
+    const uint32_t tri = __shfl_sync(0xffffffffu, tr.w, own);
+    const double ia2 = __shfl_sync(0xffffffffu, inv_area2, own);
+    if (item < total) {
+      for (int k = item - st; k > 0; --k) m &= m - 1;  // k-th covered pixel
+      const int bit = __ffs(m) - 1;
+      const int pu = (int)(bx & 0x3fff) + bit % 3, pv = (int)((bx >> 16) & 0x3fff) + bit / 3;
+      const double2 A = vs.uv(ia), B = vs.uv(ib), C = vs.uv(ic);
+      const double px = pu, py = pv;
+      const double e_ab = edge_at(A, B, flo & 1, px, py);
+      const double e_bc = edge_at(B, C, flo & 2, px, py);
+      const double e_ca = edge_at(C, A, flo & 4, px, py);
+      // renderer.cpp:94-100
+      const double inv_z = (e_bc * vs.iz(ia) + e_ca * vs.iz(ib) + e_ab * vs.iz(ic)) * ia2;
+      if (inv_z > 0) {
+        const double z = __drcp_rn(inv_z);
+        if (!(z < p.near_lim || z > p.far_m)) {
+          const float zf = __double2float_rn(z);
+          if (zf < p.far_f) {
+            Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+            if (kIds)
+              zmin((unsigned long long*)cell,
+                           ((unsigned long long)__float_as_uint(zf) << 32) |
+                               (unsigned long long)(p.draw_base + tri));
+            else
+              zmin((unsigned int*)cell, __float_as_uint(zf));
+          }
+        }
+      }
+    }
+  }
+}
+
+// Shared state of one CTA while it processes one hypothesis.
+struct HypCtx {
+  const double* R;  // rotation (row-major) in shared memory
+  const double* t;
+  Region rg;
+  bool empty_region, clip;
+  int rpx;
+};
+
+// Work of one hypothesis after the vertex phase: z-buffer init, raster,
+// render-many output and/or likelihood.  Instantiated twice per kernel so
+// that the z-buffer accesses compile to shared-memory instructions (kZS) or
+// global ones (overflow scratch), never to generic ones.
+template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, typename VS, typename Key>
+__device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
+                                         const VS& vs, WarpQ* const wq, int* const s_seg,
+                                         int* s_count, double* s_coef,
+                                         double (*s_red)[kMaxNoise],
+                                         int (*s_redi)[kMaxNoise + 1], long long h) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const Region& rg = hc.rg;
+  const double* const R = hc.R;
+  const double* const t = hc.t;
+  // background depth 1e30 (not the far sentinel) so window taps on empty
+  // pixels give d^2 = inf and an exact 0 term for any sigma; the z-test is
+  // unchanged because every fragment is also tested zf < (float)far.
+  const Key bg = kIds ? (Key)(((unsigned long long)__float_as_uint(kBgDepth) << 32) |
+                              0xffffffffull)
+                      : (Key)__float_as_uint(kBgDepth);
+  if (p.base_keys) {  // compose_render: start from the fixed scene (inference.cpp:104)
+    for (int i = tid; i < hc.rpx; i += kThreads) {
+      const int v = rg.oy + i / rg.rw, u = rg.ox + (i - (i / rg.rw) * rg.rw);
+      Key k = bg;
+      if (u >= 0 && u < p.W && v >= 0 && v < p.H) {
+        const unsigned long long b = __ldg(p.base_keys + (size_t)v * p.W + u);
+        k = kIds ? (Key)b : (Key)(unsigned int)(b >> 32);
+      }
+      zb[i] = k;
+    }
+  } else {
+    for (int i = tid; i < hc.rpx; i += kThreads) zb[i] = bg;
+  }
+  // score mode: the work list is the front part of each axis class (the cut
+  // of phase B) plus all of class 6; s_seg[0..7] = running work counts,
+  // s_seg[8..14] = first tris_s index of each segment
+  constexpr bool kSorted = kScore && !kIds;
+  if (kSorted && tid == 0) {
+    const bool cut = p.cull != 0 && !hc.clip;
+    int cum = 0;
+#pragma unroll
+    for (int c = 0; c < 7; ++c) {
+      const int b = p.cls_start[c], e = (cut && c < 6) ? s_seg[16 + c] : p.cls_start[c + 1];
+      s_seg[c] = cum;
+      s_seg[8 + c] = b;
+      cum += e - b;
+    }
+    s_seg[7] = cum;
+  }
+  __syncthreads();
+
+  // ---- C: raster, in two passes per 32-triangle chunk of each warp.
+  // Pass 1, lane = triangle (mesh order): integer bbox reject, signed area,
+  // back-face cull (closed meshes, score mode), orientation
+  // swap (renderer.cpp:63-69); survivors are appended to the warp's queue of
+  // their tile class (bbox <= 2x2 or <= 3x3; larger bboxes run the
+  // reference's per-pixel loop in place).  Pass 2 (drain_queue) runs once a
+  // queue holds 32 triangles, so the fp64 coverage work is done by full warps.
+  if (!hc.empty_region || hc.clip) {
+    WarpQ& q = wq[warp];
+    const int cull = (kScore && !kIds && !hc.clip) ? p.cull : 0;
+    const uint32_t lt_mask = (1u << lane) - 1u;
+    int head0 = 0, tail0 = 0, head1 = 0, tail1 = 0;  // warp-uniform ring cursors
+    const int n_work = kSorted ? s_seg[7] : p.nt;
+    const uint4* const tl = kSorted ? p.tris_s : p.tris;
+    auto work_tri = [&](int w) -> uint4 {
+      int phys = w;
+      if (kSorted) {
+        int c = 0;
+#pragma unroll
+        for (int j = 1; j < 7; ++j) c += w >= s_seg[j];
+        phys = s_seg[8 + c] + (w - s_seg[c]);
+      }
+      return __ldg(tl + phys);
+    };
+#if B3D_PREFETCH
+    uint4 tri_next = make_uint4(0u, 0u, 0u, 0u);
+    if (c_first + lane < n_work) tri_next = work_tri(c_first + lane);
+#endif
+    const int c_first = warp * 32, c_stride = kThreads;
+    for (int base = c_first; base < n_work; base += c_stride) {
+      __syncwarp();
+      const int ti = base + lane;
+      int cls = -1;
+      uint4 ent;
+      uint32_t box = 0;
+#if B3D_PREFETCH
+      const uint4 tri_cur = tri_next;
+      if (ti + c_stride < n_work) tri_next = work_tri(ti + c_stride);
+#endif
+      if (ti < n_work) {
+#if B3D_PREFETCH
+        const uint4 tri = tri_cur;
+#else
+        const uint4 tri = work_tri(ti);
+#endif
+        uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
+        const short4 A = vs.bb(ia), B = vs.bb(ib), C = vs.bb(ic);
+        if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
+          raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
+        } else {
+          const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
+          const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
+          if (u_max != kOvf && v_max != kOvf && u_min <= u_max && v_min <= v_max) {
+            const double2 PA = vs.uv(ia);
+            double2 PB = vs.uv(ib), PC = vs.uv(ic);
+            double area2 = (PB.x - PA.x) * (PC.y - PA.y) - (PB.y - PA.y) * (PC.x - PA.x);
+            if (area2 != 0 && !(cull > 0 ? area2 > 0 : (cull < 0 && area2 < 0))) {
+              if (area2 < 0) {
+                const double2 T = PB;
+                PB = PC;
+                PC = T;
+                const uint32_t tt = ib;
+                ib = ic;
+                ic = tt;
+                area2 = -area2;
+              }
+              const int bw = u_max - u_min + 1, bh = v_max - v_min + 1;
+              if (bw <= 3 && bh <= 3) {
+                cls = (bw <= 2 && bh <= 2) ? 0 : 1;
+                ent = make_uint4(ia, ib, ic, (uint32_t)ti);
+                box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
+                      (uint32_t)(bh - 1) << 30;
+              } else {  // large bbox: the reference's per-pixel loop
+                raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz(ia)},
+                                     SV{PB.x, PB.y, vs.iz(ib)}, SV{PC.x, PC.y, vs.iz(ic)},
+                                     u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
+              }
+            }
+          }
+        }
+      }
+      const uint32_t b0 = __ballot_sync(0xffffffffu, cls == 0);
+      const uint32_t b1 = __ballot_sync(0xffffffffu, cls == 1);
+      if (cls == 0) {
+        const int s = (tail0 + __popc(b0 & lt_mask)) & (kRing - 1);
+        q.tri[0][s] = ent;
+        q.box[0][s] = box;
+      } else if (cls == 1) {
+        const int s = (tail1 + __popc(b1 & lt_mask)) & (kRing - 1);
+        q.tri[1][s] = ent;
+        q.box[1][s] = box;
+      }
+      tail0 += __popc(b0);
+      tail1 += __popc(b1);
+      __syncwarp();
+      if (tail0 - head0 >= 32) {
+        drain_small<kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, 32, lane);
+        head0 += 32;
+      }
+      if (tail1 - head1 >= 32) {
+        drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, 32, lane);
+        head1 += 32;
+      }
+    }
+    if (tail0 > head0) drain_small<kIds>(p, zb, rg, vs, q.tri[0], q.box[0], head0, tail0 - head0, lane);
+    if (tail1 > head1) drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, tail1 - head1, lane);
+  }
+  __syncthreads();
+
+  // ---- render-many output (sentinel = (float)far, id -1 = background)
+  if (kOut) {
+    const size_t npx = (size_t)p.W * p.H;
+    float* od = p.out_depth ? p.out_depth + (size_t)h * npx : nullptr;
+    int32_t* oi = p.out_ids ? p.out_ids + (size_t)h * npx : nullptr;
+    unsigned long long* ok = p.out_keys ? p.out_keys + (size_t)h * npx : nullptr;
+    for (int i = tid; i < (int)npx; i += kThreads) {
+      const int u = i % p.W, v = i / p.W;
+      Key k = bg;
+      if (!hc.empty_region && u >= rg.u0 && u <= rg.u1 && v >= rg.v0 && v <= rg.v1)
+        k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+      else if (p.base_keys)
+        k = kIds ? (Key)__ldg(p.base_keys + i) : (Key)(unsigned int)(__ldg(p.base_keys + i) >> 32);
+      if (ok) ok[i] = kIds ? (unsigned long long)k : ((unsigned long long)k << 32) | 0xffffffffull;
+      const float z = __uint_as_float(
+          kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
+      if (od) od[i] = z < p.far_f ? z : p.far_f;
+      if (kIds && oi) {
+        const unsigned int d = (unsigned int)((unsigned long long)k & 0xffffffffull);
+        oi[i] = d == 0xffffffffu ? -1 : (int32_t)d;
+      }
+    }
+  }
+
+  if (kScore) {
+    // ---- D1: |y| = number of valid rendered pixels (likelihood.cpp:144-158)
+    // With a base image: |y| = base count - base pixels of the region +
+    // composed pixels of the region (the halo holds base pixels too, so the
+    // interior [u0,u1]x[v0,v1] is counted).
+    {
+      int cnt = 0;
+      const int iw = rg.u1 - rg.u0 + 1, ipx = iw * (rg.v1 - rg.v0 + 1);
+      for (int i = tid; i < ipx; i += kThreads) {
+        const int v = rg.v0 + i / iw, u = rg.u0 + (i - (i / iw) * iw);
+        const Key k = zb[(v - rg.oy) * rg.rw + (u - rg.ox)];
+        const float z = __uint_as_float(
+            kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
+        cnt += z < p.far_f;
+        if (p.base_keys)
+          cnt -= __uint_as_float((unsigned int)(__ldg(p.base_keys + (size_t)v * p.W + u) >> 32)) <
+                 p.far_f;
+      }
+      cnt = warp_sum_i(cnt);
+      if (lane == 0 && cnt) atomicAdd(s_count, cnt);
+      __syncthreads();
+    }
+    const int rend_count = *s_count + p.base_valid;
+    // |y| = 0 (never with a non-empty base image): the reference throws
+    // (likelihood.cpp:159-160); batched callers get -inf and a status flag
+    // (DESIGN.md §5).
+    const bool empty_render = rend_count == 0;
+    if (tid < p.lik.n_noise)  // likelihood.cpp:167 coefficient order
+      s_coef[tid] = empty_render ? 0.0 : p.lik.one_minus_p[tid] / (double)rend_count * p.lik.norm3[tid];
+    __syncthreads();
+    float coef_f[kMaxNoise], floor_f[kMaxNoise];
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      coef_f[e] = e < p.lik.n_noise ? (float)s_coef[e] : 0.f;
+      floor_f[e] = e < p.lik.n_noise ? (float)p.lik.floor_term[e] : 0.f;
+    }
+
+    // ---- D2: window sums over the dilated region.  Observed pixels whose
+    // window holds no valid rendered pixel contribute exactly log(floor)
+    // (likelihood.cpp:209-216 with an empty dist2 list); they are counted.
+    // Taps are unconditional: the halo and every non-rendered pixel hold the
+    // background depth, whose Gaussian term underflows to exactly 0.
+    const int w = p.lik.window;
+    const int du0 = max(rg.u0 - w, 0), du1 = min(rg.u1 + w, p.W - 1);
+    const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
+    const int dw = du1 - du0 + 1;
+    const int dpx = (hc.empty_region || empty_render) ? 0 : dw * (dv1 - dv0 + 1);
+    double acc[kMaxNoise];
+    int npos[kMaxNoise];
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      acc[e] = 0.0;
+      npos[e] = 0;
+    }
+    for (int i = tid; i < dpx; i += kThreads) {
+      const int pv = dv0 + i / dw;
+      const int pu = du0 + (i - (pv - dv0) * dw);
+      const float4 o = __ldg(p.obs + (size_t)pv * p.W + pu);
+      if (o.w == 0.f) continue;
+      float S[kMaxNoise];
+      window_sums<kIds, kWin, kS1>(p, zb, rg, pu, pv, o, S);
+      if (p.base_keys) {
+        // g(S) - g(S_base): the pixel's term relative to the base-only sum G
+#pragma unroll
+        for (int e = 0; e < kMaxNoise; ++e) {
+          if (e < p.lik.n_noise) {
+            const int sl = p.lik.slot_of[e];
+            const float Sb = __ldg(p.sbase + (size_t)sl * p.W * p.H + (size_t)pv * p.W + pu);
+            if (S[sl] != Sb)
+              acc[e] += (double)(__logf(floor_f[e] + coef_f[e] * S[sl]) -
+                                 __logf(floor_f[e] + coef_f[e] * Sb));
+          }
+        }
+      } else {
+#pragma unroll
+        for (int e = 0; e < kMaxNoise; ++e) {
+          if (e < p.lik.n_noise) {
+            const float Se = S[p.lik.slot_of[e]];
+            if (Se > 0.f) {
+              acc[e] += (double)__logf(floor_f[e] + coef_f[e] * Se);
+              npos[e] += 1;
+            }
+          }
+        }
+      }
+    }
+    // ---- D3: fp64 block reduction -> one score per noise entry
+#pragma unroll
+    for (int e = 0; e < kMaxNoise; ++e) {
+      acc[e] = warp_sum(acc[e]);
+      npos[e] = warp_sum_i(npos[e]);
+    }
+    if (lane == 0) {
+#pragma unroll
+      for (int e = 0; e < kMaxNoise; ++e) {
+        s_red[warp][e] = acc[e];
+        s_redi[warp][e] = npos[e];
+      }
+    }
+    __syncthreads();
+    double a = 0.0;
+    int np = 0;
+    if (tid < p.lik.n_noise) {
+      for (int k = 0; k < kWarps; ++k) {
+        a += s_red[k][tid];
+        np += s_redi[k][tid];
+      }
+    }
+    if (tid < p.lik.n_noise) {
+      const int e = tid;
+      double total = p.lik.prefactor[e] + a;
+      if (empty_render) {
+        total = -__longlong_as_double(0x7ff0000000000000ll);
+      } else if (p.base_keys) {
+        // + G(log |y|): the base-only sum over all observed pixels, a smooth
+        // function of |y| through coef; Chebyshev interpolant tabulated per
+        // observation and noise entry (base_scene.cu)
+        total += cheb_eval(p.cheb + e * kCheb, log((double)rend_count), p.cheb_lo, p.cheb_hi);
+      } else {
+        const int m_zero = *p.obs_count - np;
+        if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
+      }
+      p.scores[h * p.lik.n_noise + e] = total;
+    }
+    if (tid == 0 && p.status) p.status[h] = empty_render ? 1 : 0;
+  }
+}
+
+// Projected-vertex cache: (u, v) and 1/z in fp64 plus the packed integer
+// bbox, in shared memory (kVS) or in the CTA's global scratch.
+// Projected-vertex cache, structure of arrays (random gathers of 16-byte
+// (u, v) pairs hit all bank groups): uv[n] | iz[n] | bb[n].
+struct VertexCache {
+  double2* uvp;
+  double* izp;
+  short4* bbp;
+  __device__ __forceinline__ double2 uv(uint32_t i) const { return uvp[i]; }
+  __device__ __forceinline__ double iz(uint32_t i) const { return izp[i]; }
+  __device__ __forceinline__ short4 bb(uint32_t i) const { return bbp[i]; }
+  __device__ __forceinline__ void put(uint32_t i, double u, double v, double iz, short4 bb) const {
+    uvp[i] = make_double2(u, v);
+    izp[i] = iz;
+    bbp[i] = bb;
+  }
+  __device__ __forceinline__ void put_clipped(uint32_t i) const {
+    bbp[i] = make_short4(kClipV, 0, 0, 0);
+  }
+};
+
+// kIds: 64-bit (depth, draw) keys; kScore: run the likelihood epilogue;
+// kOut: write the full depth / id images to HBM (render-many); kVS: the
+// projected vertices fit in shared memory.
+template <bool kIds, bool kScore, bool kOut, bool kVS, int kWin, bool kS1>
+__global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams p) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  __shared__ double s_pose[32][12];  // R (row-major) | t per upcoming hypothesis
+  __shared__ int s_lo_u, s_hi_u, s_lo_v, s_hi_v, s_clip;
+  __shared__ double s_red[kWarps][kMaxNoise];
+  __shared__ int s_redi[kWarps][kMaxNoise + 1];
+  __shared__ double s_coef[kMaxNoise];
+  __shared__ int s_count;
+  __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
+  using Key = typename KeyT<kIds>::T;
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+  // dynamic shared memory: per-warp triangle queues, region z-buffer (zcap
+  // keys, a multiple of 8), projected-vertex cache (vcap x 32 B; in the CTA's
+  // global scratch when the mesh does not fit).  The first two start at
+  // compile-time offsets.
+  WarpQ* const wq = reinterpret_cast<WarpQ*>(smem_raw);
+  Key* const zb_s = reinterpret_cast<Key*>(smem_raw + sizeof(WarpQ) * kWarps);
+  VertexCache vs;
+  {
+    const int n = kVS ? p.vcap : p.nv;
+    double* const b = kVS ? reinterpret_cast<double*>(smem_raw + sizeof(WarpQ) * kWarps +
+                                                      (size_t)p.zcap * sizeof(Key))
+                          : p.vscratch + (size_t)blockIdx.x * 4 * p.nv;
+    vs.uvp = reinterpret_cast<double2*>(b);
+    vs.izp = b + 2 * (size_t)n;
+    vs.bbp = reinterpret_cast<short4*>(b + 3 * (size_t)n);
+  }
+
+  // Hypotheses one per CTA, strided by the grid (persistent CTAs).
+  const long long G = gridDim.x;
+  int kk = 0;  // hypotheses this CTA has processed
+  for (long long h = blockIdx.x; h < p.n_hyp; h += G, ++kk) {
+    // ---- A: poses of this CTA's next 32 hypotheses, one per lane of warp 0
+    // (compose with inverse(camera) -> rotation matrix + translation)
+    if ((kk & 31) == 0 && warp == 0) {
+      const long long hh = h + (long long)lane * G;
+      if (hh < p.n_hyp) {
+        KPose hp;
+        if (p.poses)
+          hp = p.poses[hh];
+        else
+          grid_pose(p.grid, p.index0 + hh, hp);
+        pose_to_rt(p.w2c, hp, s_pose[lane], s_pose[lane] + 9);
+      }
+    }
+    if (tid == 0) {
+      s_lo_u = INT_MAX;
+      s_lo_v = INT_MAX;
+      s_hi_u = INT_MIN;
+      s_hi_v = INT_MIN;
+      s_clip = 0;
+      s_count = 0;
+    }
+    __syncthreads();
+    HypCtx hc;
+    hc.R = s_pose[kk & 31];  // broadcast reads from shared memory
+    hc.t = hc.R + 9;
+    const double* const R = hc.R;
+    const double* const t = hc.t;
+
+    // ---- B: vertices -> (u, v, 1/z), packed bbox, region bounds
+    int lo_u = INT_MAX, lo_v = INT_MAX, hi_u = INT_MIN, hi_v = INT_MIN, clip = 0;
+    for (int i = tid; i < p.nv; i += kThreads) {
+      double c[3];
+      cam_vertex(R, t, p.verts + 3 * (size_t)i, c);
+      if (c[2] >= p.near_m) {
+        const SV s = project(p, c[0], c[1], c[2]);
+        const short4 bb = vertex_bbox(p, s.u, s.v);
+        vs.put(i, s.u, s.v, s.iz, bb);
+        lo_u = min(lo_u, (int)bb.x);
+        hi_u = max(hi_u, bb.y == kOvf ? p.W - 1 : (int)bb.y);
+        lo_v = min(lo_v, (int)bb.z);
+        hi_v = max(hi_v, bb.w == kOvf ? p.H - 1 : (int)bb.w);
+      } else {
+        vs.put_clipped(i);
+        clip = 1;
+      }
+    }
+    // score mode: per axis class c (warp c), the faces turned towards the
+    // camera centre C = -R^T t (model frame) are those with plane offset
+    // o <= n . C: a prefix of the class (b3d_kernels.cuh).  The small margin
+    // keeps near-edge-on planes; they go through the exact tests.
+    if (kScore && !kIds && warp < 6) {
+      const int k = warp >> 1;
+      const double Ck = -(R[k] * t[0] + R[3 + k] * t[1] + R[6 + k] * t[2]);
+      const double thr = (warp & 1) ? -Ck : Ck;
+      const double lim = thr + 1e-9 * (1.0 + fabs(thr));
+      const int pb = p.plane_begin[warp], pe = p.plane_begin[warp + 1];
+      int n_le = 0;
+      for (int j0 = pb; j0 < pe; j0 += 32) {
+        const int j = j0 + lane;
+        n_le += __popc(__ballot_sync(0xffffffffu, j < pe && __ldg(p.plane_off + j) <= lim));
+      }
+      if (lane == 0) s_seg[16 + warp] = n_le ? __ldg(p.plane_end + pb + n_le - 1) : p.cls_start[warp];
+    }
+  #pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      lo_u = min(lo_u, __shfl_xor_sync(0xffffffffu, lo_u, o));
+      lo_v = min(lo_v, __shfl_xor_sync(0xffffffffu, lo_v, o));
+      hi_u = max(hi_u, __shfl_xor_sync(0xffffffffu, hi_u, o));
+      hi_v = max(hi_v, __shfl_xor_sync(0xffffffffu, hi_v, o));
+      clip |= __shfl_xor_sync(0xffffffffu, clip, o);
+    }
+    if (lane == 0) {
+      atomicMin(&s_lo_u, lo_u);
+      atomicMin(&s_lo_v, lo_v);
+      atomicMax(&s_hi_u, hi_u);
+      atomicMax(&s_hi_v, hi_v);
+      if (clip) s_clip = 1;
+    }
+    __syncthreads();
+    Region& rg = hc.rg;
+    hc.clip = s_clip != 0;
+    if (hc.clip) {
+      rg.u0 = 0;
+      rg.v0 = 0;
+      rg.u1 = p.W - 1;
+      rg.v1 = p.H - 1;
+    } else {
+      rg.u0 = max(s_lo_u, 0);
+      rg.v0 = max(s_lo_v, 0);
+      rg.u1 = min(s_hi_u, p.W - 1);
+      rg.v1 = min(s_hi_v, p.H - 1);
+    }
+    hc.empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
+    if (hc.empty_region) {  // keep one valid (unused) pixel so indexing stays sane
+      rg.u1 = rg.u0 = min(max(rg.u0, 0), p.W - 1);
+      rg.v1 = rg.v0 = min(max(rg.v0, 0), p.H - 1);
+    }
+    const int pad = kScore ? 2 * p.lik.window : 0;
+    rg.ox = rg.u0 - pad;
+    rg.oy = rg.v0 - pad;
+    rg.rw = rg.u1 - rg.u0 + 1 + 2 * pad;
+    rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
+    hc.rpx = rg.rw * rg.rh;
+    if (hc.rpx <= p.zcap)
+      hyp_body<kIds, kScore, kOut, kWin, kS1>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
+                                              s_red, s_redi, h);
+    else
+      hyp_body<kIds, kScore, kOut, kWin, kS1>(
+          p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
+          s_seg, &s_count, s_coef, s_red, s_redi, h);
+    __syncthreads();
+  }
+}
+
+}  // namespace b3d200
+
+// Explicit instantiations of the score kernels, one translation unit per
+// window radius (rs_score_w*.cu) so they compile in parallel.
+#define B3D_RS_SCORE_KERNELS(X, W)                                                         \
+  X template __global__ void render_score_kernel<false, true, false, true, W, true>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, false, W, true>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, true, W, false>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, false, W, false>(const KParams);

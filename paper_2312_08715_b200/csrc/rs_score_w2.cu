@@ -1,0 +1,6 @@
+// Score-kernel instantiations for window radius 2 (render_score.cuh).
+#include "render_score.cuh"
+
+namespace b3d200 {
+B3D_RS_SCORE_KERNELS(, 2)
+}  // namespace b3d200
