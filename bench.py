@@ -209,6 +209,46 @@ def run_tracking(ctx, b3d, configs, frames_n, render_fn):
             "triangles": int(tr["triangles"].shape[0])}
 
 
+def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_frames=120):
+    """bench-tracking (harness.cpp:704-770, the paper's Table 1 analog): per
+    resolution, an orbit sequence (table + one 1,000-voxel blob, camera at
+    0.9 m / 40 deg sweeping 360 deg) tracked by b3d_gpu_track_camera with the
+    reference's default search (5^3 spherical lattice, 3 stages, argmax);
+    frames uploaded per frame from pinned host memory; FPS = frames / sum of
+    the per-frame wall times (the reference's close_frame)."""
+    import torch
+
+    def rc(k, inst, cams):
+        ctx.set_camera(b3d.Intrinsics(*k.as_tuple()))
+        mids = [ctx.upload_mesh(v, t) for v, t, _ in inst]
+        ctx.set_camera_scene(mids, [p for _, _, p in inst])
+        return ctx.render_cameras(np.asarray(cams), with_ids=False)[0]
+
+    out = []
+    for res in resolutions:
+        seq = configs.orbit_sequence(rc, b3d.voxel_to_mesh, b3d.box_mesh, b3d.contact_to_pose,
+                                     res=res, n_frames=n_frames)
+        cams = np.array([b3d.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+                         for a in seq["azimuths"]])
+        frames = torch.from_numpy(configs.orbit_frames(seq, cams)).pin_memory().numpy()
+        ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+        ctx.track_camera(frames[:3], cams[0])  # warm-up
+        est, ms = ctx.track_camera(frames, cams[0])
+        pos = [100.0 * float(np.linalg.norm(est[i][4:] - cams[i][4:])) for i in range(n_frames)]
+        rot = [float(np.degrees(2.0 * np.arccos(min(1.0, abs(float(np.dot(est[i][:4],
+                                                                          cams[i][:4])))))))
+               for i in range(n_frames)]
+        out.append({"resolution": res, "fps": n_frames / (float(ms.sum()) * 1e-3),
+                    "ms_per_frame_mean": float(ms[1:].mean()),
+                    "mean_position_error_cm": statistics.mean(pos),
+                    "mean_orientation_error_deg": statistics.mean(rot),
+                    "window": seq["window"]})
+    return {"workload": "bench-tracking orbit (Table 1 analog): table + 1,000-voxel blob, "
+                        f"{n_frames} frames, 125-point spherical lattice x 3 stages per frame, "
+                        "camera-mode multi-instance render+score on device",
+            "frames": n_frames, "per_resolution": out}
+
+
 def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
     """configs[1]: five 32,768-hypothesis stages chained on the device
     (sample selection); device time per schedule with CUDA events."""
@@ -236,9 +276,15 @@ def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
             "triangles": int(w.triangles.shape[0])}
 
 
-def _scene_oracle_render(k, cam, inst):
-    from oracle import pyoracle as O
-    return O.render(k, inst, camera=cam)
+def _scene_renderer(ctx, b3d):
+    """render_instances of a whole scene through the product (camera mode,
+    one camera hypothesis): builds the configs' observations on the GPU."""
+    def render(k, cam, inst):
+        ctx.set_camera(b3d.Intrinsics(*k.as_tuple()))
+        mids = [ctx.upload_mesh(v, t) for v, t, _ in inst]
+        ctx.set_camera_scene(mids, [p for _, _, p in inst])
+        return ctx.render_cameras(np.asarray(cam, dtype=np.float64)[None], with_ids=False)[0][0]
+    return render
 
 
 def run_scene_graph(ctx, b3d, configs, reps=3):
@@ -246,8 +292,8 @@ def run_scene_graph(ctx, b3d, configs, reps=3):
     fixed table + 3 objects (base scene rendered once, composited per
     hypothesis), 240x320, device time per pass (CUDA events)."""
     import torch
-    from oracle import pyoracle as O
-    w = configs.cfg3(_scene_oracle_render, b3d.voxel_to_mesh, O.box_mesh, O.contact_to_pose)
+    w = configs.cfg3(_scene_renderer(ctx, b3d), b3d.voxel_to_mesh, b3d.box_mesh,
+                     b3d.contact_to_pose)
     ctx.set_camera(b3d.Intrinsics(*w["k"].as_tuple()), w["camera"])
     tv, tt = w["table"][0], w["table"][1]
     mids = [ctx.upload_mesh(tv, tt)] + [ctx.upload_mesh(o[0], o[1]) for o in w["objects"]]
@@ -290,9 +336,9 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
     on every rank.  Device time, max over ranks."""
     import torch
     import torch.distributed as dist
-    from oracle import pyoracle as O
     from paper_2312_08715_b200.shard import gather_scores, shard_range
-    w = configs.cfg5(_scene_oracle_render, b3d.voxel_to_mesh, O.box_mesh, O.contact_to_pose)
+    w = configs.cfg5(_scene_renderer(ctx, b3d), b3d.voxel_to_mesh, b3d.box_mesh,
+                     b3d.contact_to_pose)
     ctx.set_camera(b3d.Intrinsics(*w["k"].as_tuple()), w["camera"])
     tv, tt = w["table"]
     mids = [ctx.upload_mesh(tv, tt)] + [ctx.upload_mesh(l[0], l[1]) for l in w["library"]]
@@ -498,6 +544,7 @@ def main():
             extra["coarse_to_fine"] = run_coarse_to_fine(ctx, b3d, configs, render_fn)
             extra["tracking"] = run_tracking(ctx, b3d, configs, args.tracking_frames, render_fn)
             extra["scene_graph"] = run_scene_graph(ctx, b3d, configs)
+            extra["bench_tracking"] = run_bench_tracking(ctx, b3d, configs)
         roof = None
         if cnt is not None and "fp64_nofma_ops" in peaks:
             ops = _ops_per_hyp(cnt, 1, 1, BATCH)

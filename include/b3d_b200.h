@@ -266,6 +266,56 @@ B3D_API b3d_status b3d_gpu_score_grid_range(b3d_gpu_context* ctx, int32_t mesh_i
                                             const b3d_pose_grid* grid, uint64_t first,
                                             uint64_t n, double* scores, uint8_t* status);
 
+/* ---- camera mode: a scene of mesh instances under camera hypotheses ----
+ * render_instances (renderer.cpp:153-189) of up to 16 instances in draw
+ * order (draw indices continue across instances); model_to_world[i] is used
+ * verbatim, as scene_instances (inference.cpp:172-184) produces it. */
+enum { B3D_MAX_INSTANCES = 16 };
+B3D_API b3d_status b3d_gpu_set_camera_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
+                                            const b3d_pose* model_to_world, uint32_t n);
+/* render-many / score-many over camera-to-world poses cameras[0..n) (host or
+ * device memory, used verbatim like track_camera's Pose values). */
+B3D_API b3d_status b3d_gpu_render_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras,
+                                          uint64_t n, float* depth, int32_t* draw_index);
+B3D_API b3d_status b3d_gpu_score_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras,
+                                         uint64_t n, double* scores, uint8_t* status);
+
+/* TrackSearch (tracking.hpp:25-34). */
+typedef struct b3d_track_search {
+  double pos_extent;   /* +- m on distance */
+  double angle_extent; /* +- rad on azimuth / altitude */
+  int32_t points_per_dim;
+  int32_t refine_stages;
+  double refine_factor;
+  int32_t beam_width;
+  int32_t reserved;
+} b3d_track_search;
+
+/* track_camera (tracking.cpp:59-172) over the camera scene: frames are
+ * n_frames depth images (W x H fp32 each, host or device); every lattice
+ * stage is scored on the device.  Likelihood: the context's settings (one
+ * noise entry).  out_poses[n_frames] (frame 0 = initial), optional
+ * out_frame_ms[n_frames] (per-frame wall time, the reference's close_frame).
+ * camera_pose_from_spherical / camera_pose_to_spherical run on the host
+ * with the reference's libm calls (generative.cpp:35-85). */
+B3D_API b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames,
+                                        uint32_t n_frames, const b3d_pose* initial,
+                                        const b3d_track_search* search, b3d_pose* out_poses,
+                                        double* out_frame_ms);
+/* make_box_mesh (scene_graph.cpp:37-58): 8 vertices, 12 triangles. */
+B3D_API b3d_status b3d_box_mesh(const double lo[3], const double hi[3], double vertices[24],
+                                uint32_t triangles[36]);
+/* contact_to_pose (scene_graph.cpp:97-121) with the table's extents given
+ * directly; B3D_ERROR for out-of-range contact parameters. */
+B3D_API b3d_status b3d_contact_to_pose(double table_w, double table_h, const double aabb_min[3],
+                                       const double aabb_max[3], int32_t face, double dx,
+                                       double dy, double dtheta, b3d_pose* out);
+/* generative.cpp:35-59 / 61-85 on the host (exposed for tests and callers). */
+B3D_API b3d_status b3d_camera_pose_from_spherical(double distance, double azimuth,
+                                                  double altitude, b3d_pose* out);
+B3D_API int b3d_camera_pose_to_spherical(const b3d_pose* pose, double tol, double* distance,
+                                         double* azimuth, double* altitude);
+
 /* Reference Rng seeding (rng.cpp:20-28), for building rng_state. */
 B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
 B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,

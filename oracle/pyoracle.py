@@ -359,3 +359,100 @@ def ref_rng_draw(seed, split, k0, k1, k2, kind, m, n):
                                C.c_uint64, C.c_void_p, C.c_size_t]
     L.ref_rng_draw(seed, split, k0, k1, k2, kind, m, out.ctypes.data, n)
     return out
+
+
+# ---------------------------------------------------------------- tracking
+_HALF_PI = 1.5707963267948966
+_TWO_PI = 6.283185307179586476925287
+
+
+def camera_pose_to_spherical(p, tol=1e-6):
+    """generative.cpp:61-85 (libm asin/atan2/fmod as the reference; 3-term
+    norms split x2 + (y2 + z2) like Eigen's redux)."""
+    import math
+    t = [float(p[4]), float(p[5]), float(p[6])]
+    d = math.sqrt(t[0] * t[0] + (t[1] * t[1] + t[2] * t[2]))
+    if d <= 0:
+        return None
+    sin_alt = min(max(t[2] / d, -1.0), 1.0)
+    alt = math.asin(sin_alt)
+    if alt <= 0 or alt >= _HALF_PI:
+        return None
+    az = math.fmod(math.atan2(t[1], t[0]), _TWO_PI)
+    if az < 0:
+        az += _TWO_PI
+    e = camera_pose_from_spherical(d, az, alt)
+    dt = [e[4] - t[0], e[5] - t[1], e[6] - t[2]]
+    if math.sqrt(dt[0] * dt[0] + (dt[1] * dt[1] + dt[2] * dt[2])) > tol * max(1.0, d):
+        return None
+    a = [e[1] - p[1], e[2] - p[2], e[3] - p[3], e[0] - p[0]]
+    b = [e[1] + p[1], e[2] + p[2], e[3] + p[3], e[0] + p[0]]
+    qa = math.sqrt((a[0] * a[0] + a[1] * a[1]) + (a[2] * a[2] + a[3] * a[3]))
+    qb = math.sqrt((b[0] * b[0] + b[1] * b[1]) + (b[2] * b[2] + b[3] * b[3]))
+    if min(qa, qb) > tol:
+        return None
+    return d, az, alt
+
+
+def _lattice(c, e, n):
+    """tracking.cpp:27-37"""
+    if n == 1:
+        return [c]
+    return [c - e + 2.0 * e * i / (n - 1) for i in range(n)]
+
+
+def track_camera(frames, k, instances, initial, noise, sigma_max, window,
+                 pos_extent=0.03, angle_extent=0.17453292519943295, points_per_dim=5,
+                 refine_stages=2, refine_factor=3.0, beam_width=1, prefactor=0,
+                 stage_log=None):
+    """track_camera (tracking.cpp:59-172) over render_instances + the
+    windowed likelihood of this oracle; returns the camera pose per frame.
+    stage_log, if a list, receives (frame, stage, grid, scores) per stage."""
+    start = camera_pose_to_spherical(initial)
+    if start is None:
+        raise ValueError("track_camera: initial pose must look at the origin with up = +z")
+    poses = [np.asarray(initial, dtype=np.float64)]
+    beam = [(start, 0.0)]
+    n = points_per_dim
+    for f in range(1, len(frames)):
+        nxt = []
+        for seed, _ in beam:
+            center = seed
+            pe, ae = pos_extent, angle_extent
+            stage_best = (center, -np.inf)
+            for st in range(refine_stages + 1):
+                grid = [(d, az, alt) for d in _lattice(center[0], pe, n)
+                        for az in _lattice(center[1], ae, n)
+                        for alt in _lattice(center[2], ae, n)]
+                scores = []
+                for d, az, alt in grid:
+                    if d <= 0 or alt <= 0 or alt >= _HALF_PI:
+                        scores.append(-np.inf)
+                        continue
+                    cam = camera_pose_from_spherical(d, az, alt)
+                    rend = render(k, instances, camera=cam)
+                    scores.append(windowed_loglik_multi(frames[f], rend, k, [noise], sigma_max,
+                                                        window, prefactor)[0])
+                best = 0
+                for i in range(1, len(scores)):
+                    if scores[i] > scores[best]:
+                        best = i
+                if not np.isfinite(scores[best]):
+                    raise ValueError("track_camera: every candidate pose scored -inf")
+                if stage_log is not None:
+                    stage_log.append((f, st, grid, scores))
+                center = grid[best]
+                stage_best = (center, scores[best])
+                if beam_width > 1 and st == refine_stages:
+                    order = sorted(range(len(grid)), key=lambda i: -scores[i])
+                    for i in order[:beam_width]:
+                        nxt.append((grid[i], scores[i]))
+                pe /= refine_factor
+                ae /= refine_factor
+            if beam_width == 1:
+                nxt.append(stage_best)
+        nxt = sorted(nxt, key=lambda c: -c[1])[:beam_width]
+        beam = nxt
+        top = beam[0][0]
+        poses.append(camera_pose_from_spherical(*top))
+    return np.array(poses)

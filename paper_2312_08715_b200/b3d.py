@@ -85,6 +85,21 @@ SELECT_SAMPLE = 0
 SELECT_ARGMAX = 1
 
 
+class TrackSearch(C.Structure):
+    """TrackSearch (tracking.hpp:25-34); defaults as the reference's."""
+    _fields_ = [("pos_extent", C.c_double), ("angle_extent", C.c_double),
+                ("points_per_dim", C.c_int32), ("refine_stages", C.c_int32),
+                ("refine_factor", C.c_double), ("beam_width", C.c_int32),
+                ("reserved", C.c_int32)]
+
+    @classmethod
+    def default(cls, **kw):
+        d = dict(pos_extent=0.03, angle_extent=0.17453292519943295, points_per_dim=5,
+                 refine_stages=2, refine_factor=3.0, beam_width=1, reserved=0)
+        d.update(kw)
+        return cls(**d)
+
+
 class StageResult(C.Structure):
     _fields_ = [("argmax", C.c_uint64), ("sample", C.c_uint64), ("max_score", C.c_double),
                 ("logsumexp", C.c_double), ("total", C.c_double), ("sample_logp", C.c_double),
@@ -122,6 +137,16 @@ def lib() -> C.CDLL:
         "b3d_gpu_upload_mesh": ([vp, vp, u64, vp, u64, C.POINTER(i32)], st),
         "b3d_gpu_set_observation": ([vp, vp], st),
         "b3d_gpu_set_culling": ([vp, st], st),
+        "b3d_gpu_set_camera_scene": ([vp, vp, vp, u32], st),
+        "b3d_gpu_render_cameras": ([vp, vp, u64, vp, vp], st),
+        "b3d_gpu_score_cameras": ([vp, vp, u64, vp, vp], st),
+        "b3d_gpu_track_camera": ([vp, vp, u32, C.POINTER(Pose), C.POINTER(TrackSearch), vp, vp],
+                                 st),
+        "b3d_camera_pose_from_spherical": ([dbl, dbl, dbl, C.POINTER(Pose)], st),
+        "b3d_box_mesh": ([vp, vp, vp, vp], st),
+        "b3d_contact_to_pose": ([dbl, dbl, vp, vp, i32, dbl, dbl, dbl, C.POINTER(Pose)], st),
+        "b3d_camera_pose_to_spherical": ([C.POINTER(Pose), dbl, C.POINTER(dbl), C.POINTER(dbl),
+                                          C.POINTER(dbl)], C.c_int),
         "b3d_mesh_cull_sign": ([vp, u64, vp, u64, C.POINTER(i32)], st),
         "b3d_gpu_mesh_cull_sign": ([vp, i32, C.POINTER(i32)], st),
         "b3d_gpu_set_likelihood": ([vp, C.POINTER(Noise), u32, dbl, st, st], st),
@@ -213,6 +238,41 @@ def mesh_cull_sign(vertices: np.ndarray, triangles: np.ndarray) -> int:
     _check(lib().b3d_mesh_cull_sign(v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0],
                                     C.byref(out)))
     return out.value
+
+
+def box_mesh(lo, hi):
+    """make_box_mesh (scene_graph.cpp:37-58)."""
+    lo_a = np.ascontiguousarray(lo, dtype=np.float64)
+    hi_a = np.ascontiguousarray(hi, dtype=np.float64)
+    v = np.zeros((8, 3), dtype=np.float64)
+    t = np.zeros((12, 3), dtype=np.uint32)
+    _check(lib().b3d_box_mesh(lo_a.ctypes.data, hi_a.ctypes.data, v.ctypes.data, t.ctypes.data))
+    return v, t
+
+
+def contact_to_pose(table_w, table_h, aabb_min, aabb_max, face, dx, dy, dtheta) -> np.ndarray:
+    """contact_to_pose (scene_graph.cpp:97-121) on the host."""
+    lo_a = np.ascontiguousarray(aabb_min, dtype=np.float64)
+    hi_a = np.ascontiguousarray(aabb_max, dtype=np.float64)
+    out = Pose()
+    _check(lib().b3d_contact_to_pose(table_w, table_h, lo_a.ctypes.data, hi_a.ctypes.data, face,
+                                     dx, dy, dtheta, C.byref(out)))
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def camera_pose_from_spherical(distance: float, azimuth: float, altitude: float) -> np.ndarray:
+    """generative.cpp:35-59 on the host (the product's libm path)."""
+    out = Pose()
+    _check(lib().b3d_camera_pose_from_spherical(distance, azimuth, altitude, C.byref(out)))
+    return np.array([getattr(out, n) for n, _ in Pose._fields_])
+
+
+def camera_pose_to_spherical(pose, tol: float = 1e-6):
+    """generative.cpp:61-85: (distance, azimuth, altitude) or None."""
+    d, a, h = C.c_double(), C.c_double(), C.c_double()
+    ok = lib().b3d_camera_pose_to_spherical(C.byref(_pose(pose)), tol, C.byref(d), C.byref(a),
+                                            C.byref(h))
+    return (d.value, a.value, h.value) if ok else None
 
 
 def contact_grid_poses(grid: "ContactGrid") -> np.ndarray:
@@ -411,6 +471,45 @@ class GpuContext:
         outs = [StageOut(r.argmax, r.sample, r.max_score, r.logsumexp, r.total, r.sample_logp,
                          bool(r.all_zero), r.n_nonfinite, bool(r.sample_fallback)) for r in res]
         return outs, centers
+
+    def set_camera_scene(self, mesh_ids: Sequence[int], poses):
+        """Instances (draw order) rendered under camera hypotheses
+        (b3d_gpu_set_camera_scene); poses are model-to-world."""
+        ids = np.ascontiguousarray(mesh_ids, dtype=np.int32)
+        P = np.ascontiguousarray(poses, dtype=np.float64).reshape(-1, 7)
+        _check(self._L.b3d_gpu_set_camera_scene(self.h, ids.ctypes.data, P.ctypes.data, len(ids)))
+
+    def render_cameras(self, cameras, with_ids: bool = True):
+        cams = np.ascontiguousarray(cameras, dtype=np.float64).reshape(-1, 7)
+        n = cams.shape[0]
+        H, W = self.k.height, self.k.width
+        depth = np.zeros((n, H, W), dtype=np.float32)
+        ids = np.zeros((n, H, W), dtype=np.int32) if with_ids else None
+        _check(self._L.b3d_gpu_render_cameras(self.h, cams.ctypes.data, n, depth.ctypes.data,
+                                              _ptr(ids)))
+        return depth, ids
+
+    def score_cameras(self, cameras):
+        cams = np.ascontiguousarray(cameras, dtype=np.float64).reshape(-1, 7)
+        n = cams.shape[0]
+        scores = np.zeros((n, self.n_noise), dtype=np.float64)
+        status = np.zeros(n, dtype=np.uint8)
+        _check(self._L.b3d_gpu_score_cameras(self.h, cams.ctypes.data, n, scores.ctypes.data,
+                                             status.ctypes.data))
+        return scores, status
+
+    def track_camera(self, frames, initial, search: "TrackSearch" = None):
+        """track_camera (tracking.cpp:59-172): camera poses per frame and the
+        per-frame wall time in ms."""
+        fr = frames if not isinstance(frames, np.ndarray) else \
+            np.ascontiguousarray(frames, dtype=np.float32)
+        n = fr.shape[0]
+        poses = np.zeros((n, 7), dtype=np.float64)
+        ms = np.zeros(n, dtype=np.float64)
+        search = search or TrackSearch.default()
+        _check(self._L.b3d_gpu_track_camera(self.h, _ptr(fr), n, C.byref(_pose(initial)),
+                                            C.byref(search), poses.ctypes.data, ms.ctypes.data))
+        return poses, ms
 
     def set_base_scene(self, mesh_ids: Sequence[int], poses):
         """Fixed instances (table first, then base children) rendered once and

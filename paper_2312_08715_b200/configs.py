@@ -347,3 +347,56 @@ def cfg5(render_scene, mesh_fn, box_fn, contact_fn, seed: int = 0, counts=(64, 6
             "gt": poses[target], "observed": obs, "extent": (0.04, 0.04, 0.02),
             "count": counts, "rotations": rots, "noise": [(0.02, 0.003)], "window": 2,
             "sigma_max": 0.1, "n_hyp": counts[0] * counts[1] * counts[2] * n_rot}
+
+
+def square_intrinsics(res: int, fov_deg: float = 60.0, near: float = 0.1, far: float = 5.0):
+    """harness.cpp:731-740 square_intrinsics (bench-tracking)."""
+    f = res / (2.0 * np.tan(fov_deg * np.pi / 360.0))
+    return Intr(f, f, (res - 1) / 2.0, (res - 1) / 2.0, res, res, near, far)
+
+
+def default_window(width: int) -> int:
+    """likelihood.cpp:231-233"""
+    return max(1, int(np.floor(2.0 * width / 100.0 + 0.5)))
+
+
+def orbit_sequence(render_cameras, mesh_fn, box_fn, contact_fn, res: int, n_frames: int = 120,
+                   seed: int = 0, n_voxels: int = 1000, distance: float = 0.9,
+                   altitude_deg: float = 40.0, sweep_deg: float = 360.0):
+    """bench-tracking's orbit sequence (generate_orbit_sequence,
+    tracking.cpp:174-215; harness.cpp:743-770 defaults): a 0.5 x 0.5 m table
+    with one seeded voxel blob (stands in for the library object) standing on
+    face 1 at the table centre, a camera orbiting at 0.9 m / 40 deg altitude
+    sweeping 360 deg over the frames, square intrinsics (60 deg FOV, near 0.1,
+    far 5).  Frames: render + N(0, 2 mm) depth noise, 2 % outliers (noise
+    p_outlier 0.02, sigma 2 mm, the bench default).  render_cameras(k,
+    instances, cameras) -> depth images."""
+    rng = np.random.Generator(np.random.PCG64(7000 + 13 * seed + res))
+    k = square_intrinsics(res)
+    tw = th = 0.5
+    tv, tt, tlo, thi = table_mesh(box_fn, tw, th)
+    vox = synth.eden_blob(n_voxels, 500 + seed)
+    v, t = make_mesh(vox, mesh_fn)
+    lo, hi = v.min(axis=0), v.max(axis=0)
+    fp = hi[:2] - lo[:2]  # face 1 footprint (x, y extents)
+    pose = contact_fn(tw, th, lo, hi, 1, (tw - fp[0]) / 2, (th - fp[1]) / 2, 0.0)
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    inst = [(tv, tt, ident), (v, t, pose)]
+    alt = altitude_deg * np.pi / 180.0
+    sweep = sweep_deg * np.pi / 180.0
+    az = [sweep * i / n_frames for i in range(n_frames)]
+    return {"k": k, "instances": inst, "azimuths": az, "distance": distance, "altitude": alt,
+            "noise": (0.02, 0.002), "window": default_window(res), "sigma_max": 0.1,
+            "rng": rng, "render_cameras": render_cameras}
+
+
+def orbit_frames(seq, cameras):
+    """Rendered frames of an orbit sequence at the given camera poses, with
+    the sequence's seeded depth noise and outliers."""
+    k = seq["k"]
+    depth = seq["render_cameras"](k, seq["instances"], cameras)
+    out = np.empty_like(depth)
+    for i in range(depth.shape[0]):
+        out[i] = synth.noisy_observation(depth[i], k.far, 0.002, 0.02, k.near, k.far, seq["rng"],
+                                         k.near)
+    return out

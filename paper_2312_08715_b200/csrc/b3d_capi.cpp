@@ -11,6 +11,8 @@
 
 #include <cmath>
 #include <algorithm>
+#include <chrono>
+#include <limits>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -325,6 +327,11 @@ struct b3d_gpu_context {
   int base_valid = 0;
   uint32_t base_draw = 0;
   bool culling = true;  // b3d_gpu_set_culling
+  // camera mode scene (b3d_gpu_set_camera_scene): concatenated instances
+  std::unique_ptr<Mesh> cam_mesh;
+  int cam_n = 0;
+  int cam_v0[kMaxInst + 1] = {0};
+  KPose cam_pose[kMaxInst];
   long long obs_version = 0, base_version = 0;
   std::string base_terms_key;
 };
@@ -411,13 +418,19 @@ struct LaunchPlan {
 };
 
 template <bool kIds, bool kScore, bool kOut>
-LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int window = -1) {
+LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int window = -1,
+                       bool full_frame = false) {
   LaunchPlan lp;
   const size_t key = kIds ? 8 : 4;
   const size_t npx = (size_t)ctx->k.width * ctx->k.height;
-  // largest CTAs/SM (3, 2, 1) whose shared memory holds the projected
-  // vertices plus a region z-buffer of at least 4,096 pixels; otherwise the
-  // vertices spill to the per-CTA global scratch
+  const int pad = kScore ? 2 * (window >= 0 ? window : ctx->lik.window) : 0;
+  const size_t padded = (size_t)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
+  // largest CTAs/SM (2, 1) whose shared memory holds the projected vertices
+  // plus a region z-buffer of at least 2,048 pixels; otherwise the vertices
+  // spill to the per-CTA global scratch.  full_frame (camera mode: the table
+  // fills the image): prefer the first of (2 CTAs, vertices on chip), (1 CTA,
+  // vertices on chip), (1 CTA, vertices in scratch) whose z-buffer holds the
+  // whole padded image.
   const size_t vbytes = 32ull * m.nv;  // u, v, 1/z (fp64) + packed int bbox
   const size_t stage = render_score_staging_bytes(m.nt);
   const size_t zmin = std::min<size_t>(2048, npx) * key;
@@ -438,10 +451,18 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
     }
   }
   if (lp.vcap == 0) budget = budget_for(2);
+  if (full_frame && (budget - 32ull * lp.vcap - stage) / key < padded) {
+    if (vbytes + stage + padded * key <= budget_for(1)) {
+      budget = budget_for(1);
+      lp.vcap = m.nv;
+    } else if (stage + padded * key <= budget_for(1)) {
+      budget = budget_for(1);
+      lp.vcap = 0;
+    }
+  }
   size_t zcap = (budget - 32ull * lp.vcap - stage) / key;
-  if (zcap > npx + 8 * (ctx->k.width + ctx->k.height) + 64)
-    zcap = npx + 8 * (ctx->k.width + ctx->k.height) + 64;
-  zcap &= ~size_t(7);  // the vertex records after the z-buffer stay 32-byte aligned
+  if (zcap > padded + 64) zcap = padded + 64;
+  zcap &= ~size_t(7);  // the vertex cache after the z-buffer stays 32-byte aligned
   lp.zcap = (int)zcap;
   lp.smem = 32ull * lp.vcap + stage + key * zcap;
   int per_sm = 0;
@@ -453,7 +474,6 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   if (grid < 1) grid = 1;
   lp.grid = (int)grid;
   // overflow scratch for hypotheses whose region / mesh exceeds shared memory
-  const int pad = kScore ? 2 * (window >= 0 ? window : ctx->lik.window) : 0;
   lp.zstride = (long long)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
   const size_t ctas = kScore ? (size_t)lp.cap : (size_t)lp.grid;
   ctx->zscratch.ensure(ctas * lp.zstride * 8);
@@ -652,6 +672,69 @@ void rotated_bounds(const double amin[3], const double amax[3], int face, double
   }
 }
 
+// Host quaternion helpers in Eigen's evaluation order (posemath.cuh restates
+// the same on the device).
+struct HQ {
+  double w, x, y, z;
+};
+HQ hq_mul(const HQ& a, const HQ& b) {
+  return HQ{a.w * b.w - a.x * b.x - a.y * b.y - a.z * b.z,
+            a.w * b.x + a.x * b.w + a.y * b.z - a.z * b.y,
+            a.w * b.y + a.y * b.w + a.z * b.x - a.x * b.z,
+            a.w * b.z + a.z * b.w + a.x * b.y - a.y * b.x};
+}
+HQ hq_normalized(HQ q) {
+  const double n2 = (q.x * q.x + q.y * q.y) + (q.z * q.z + q.w * q.w);
+  if (n2 > 0) {
+    const double n = std::sqrt(n2);
+    q.w /= n;
+    q.x /= n;
+    q.y /= n;
+    q.z /= n;
+  }
+  return q;
+}
+void hq_rotate(const HQ& q, const double v[3], double o[3]) {
+  double uv0 = q.y * v[2] - q.z * v[1];
+  double uv1 = q.z * v[0] - q.x * v[2];
+  double uv2 = q.x * v[1] - q.y * v[0];
+  uv0 += uv0;
+  uv1 += uv1;
+  uv2 += uv2;
+  const double c0 = q.y * uv2 - q.z * uv1;
+  const double c1 = q.z * uv0 - q.x * uv2;
+  const double c2 = q.x * uv1 - q.y * uv0;
+  o[0] = v[0] + q.w * uv0 + c0;
+  o[1] = v[1] + q.w * uv1 + c1;
+  o[2] = v[2] + q.w * uv2 + c2;
+}
+
+// scene_graph.cpp:97-121 contact_to_pose (table extents given directly)
+KPose contact_to_pose_host(double table_w, double table_h, const double amin[3],
+                           const double amax[3], int face, double dx, double dy, double dtheta) {
+  require(face >= 1 && face <= 6, ErrorCode::invalid, "face must be in 1..6");
+  double lo[3], hi[3];
+  rotated_bounds(amin, amax, face, lo, hi);
+  const double w = hi[0] - lo[0];
+  const double h = hi[1] - lo[1];
+  require(dx >= 0 && dx <= table_w - w && dy >= 0 && dy <= table_h - h && dtheta >= 0 &&
+              dtheta < kTwoPiD,
+          ErrorCode::invalid, "contact params out of valid range");
+  const double corner[3] = {-table_w / 2, -table_h / 2, 0.0};
+  const double bt[3] = {corner[0] + (dx - lo[0]), corner[1] + (dy - lo[1]), corner[2] + -lo[2]};
+  const double pivot[3] = {corner[0] + (dx + w / 2), corner[1] + (dy + h / 2), corner[2] + 0.0};
+  static const double uz[3] = {0, 0, 1};
+  double s[4], f[4];
+  axis_angle_q(uz, dtheta, s);
+  face_rotation(face, f);
+  const HQ spin{s[0], s[1], s[2], s[3]};
+  const HQ q = hq_normalized(hq_mul(spin, HQ{f[0], f[1], f[2], f[3]}));
+  const double rel[3] = {bt[0] - pivot[0], bt[1] - pivot[1], bt[2] - pivot[2]};
+  double r[3];
+  hq_rotate(spin, rel, r);
+  return KPose{q.w, q.x, q.y, q.z, r[0] + pivot[0], r[1] + pivot[1], r[2] + pivot[2]};
+}
+
 // KGrid (mode 2) for a contact grid: face rotation, footprint and the
 // per-cell spin cos/sin computed here with libm; the rest runs on device.
 KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
@@ -774,6 +857,146 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "score_poses");
 }
 
+
+// ---------------------------------------------------------------- camera mode
+constexpr double kHalfPi = 1.5707963267948966;
+
+// Eigen 3-vector reductions split as a0 + (a1 + a2) (redux unroller halves)
+double sq3(const double v[3]) { return v[0] * v[0] + (v[1] * v[1] + v[2] * v[2]); }
+
+void normalize3(double v[3]) {
+  const double n2 = sq3(v);
+  if (n2 > 0) {
+    const double n = std::sqrt(n2);
+    v[0] /= n;
+    v[1] /= n;
+    v[2] /= n;
+  }
+}
+
+// Eigen Quaternion(const Matrix3&) (trace / largest-diagonal branches),
+// m row-major
+void quat_from_rot(const double m[9], double q[4]) {
+  auto M = [&](int i, int j) { return m[3 * i + j]; };
+  double t = M(0, 0) + (M(1, 1) + M(2, 2));
+  if (t > 0) {
+    t = std::sqrt(t + 1.0);
+    q[0] = 0.5 * t;
+    t = 0.5 / t;
+    q[1] = (M(2, 1) - M(1, 2)) * t;
+    q[2] = (M(0, 2) - M(2, 0)) * t;
+    q[3] = (M(1, 0) - M(0, 1)) * t;
+  } else {
+    int i = 0;
+    if (M(1, 1) > M(0, 0)) i = 1;
+    if (M(2, 2) > M(i, i)) i = 2;
+    const int j = (i + 1) % 3, k = (j + 1) % 3;
+    double c[3];
+    t = std::sqrt(M(i, i) - M(j, j) - M(k, k) + 1.0);
+    c[i] = 0.5 * t;
+    t = 0.5 / t;
+    q[0] = (M(k, j) - M(j, k)) * t;
+    c[j] = (M(j, i) + M(i, j)) * t;
+    c[k] = (M(k, i) + M(i, k)) * t;
+    q[1] = c[0];
+    q[2] = c[1];
+    q[3] = c[2];
+  }
+}
+
+// generative.cpp:35-59: camera on a sphere around the origin, optical axis
+// through it, image "down" = -(world +z projected off the axis)
+KPose camera_from_spherical(double distance, double azimuth, double altitude) {
+  require(distance > 0, ErrorCode::invalid, "camera distance must be positive");
+  require(altitude > 0 && altitude < kHalfPi, ErrorCode::invalid,
+          "camera altitude must lie within (0, pi/2)");
+  const double pos[3] = {distance * std::cos(altitude) * std::cos(azimuth),
+                         distance * std::cos(altitude) * std::sin(azimuth),
+                         distance * std::sin(altitude)};
+  double fwd[3] = {-pos[0], -pos[1], -pos[2]};
+  normalize3(fwd);
+  const double d = 0.0 * fwd[0] + (0.0 * fwd[1] + 1.0 * fwd[2]);
+  double up[3] = {0.0 - d * fwd[0], 0.0 - d * fwd[1], 1.0 - d * fwd[2]};
+  require(std::sqrt(sq3(up)) > 1e-12, ErrorCode::invalid,
+          "camera pose degenerate: looking along world z");
+  normalize3(up);
+  const double down[3] = {-up[0], -up[1], -up[2]};
+  const double right[3] = {down[1] * fwd[2] - down[2] * fwd[1],
+                           down[2] * fwd[0] - down[0] * fwd[2],
+                           down[0] * fwd[1] - down[1] * fwd[0]};
+  const double m[9] = {right[0], down[0], fwd[0], right[1], down[1],
+                       fwd[1],   right[2], down[2], fwd[2]};
+  double q[4];
+  quat_from_rot(m, q);
+  const double n2 = (q[1] * q[1] + q[2] * q[2]) + (q[3] * q[3] + q[0] * q[0]);
+  if (n2 > 0) {
+    const double n = std::sqrt(n2);
+    for (double& x : q) x /= n;
+  }
+  return KPose{q[0], q[1], q[2], q[3], pos[0], pos[1], pos[2]};
+}
+
+// generative.cpp:61-85
+bool camera_to_spherical(const KPose& pose, double tol, double& distance, double& azimuth,
+                         double& altitude) {
+  const double t[3] = {pose.tx, pose.ty, pose.tz};
+  const double d = std::sqrt(sq3(t));
+  if (d <= 0) return false;
+  const double sin_alt = std::clamp(t[2] / d, -1.0, 1.0);
+  const double alt = std::asin(sin_alt);
+  if (alt <= 0 || alt >= kHalfPi) return false;
+  double az = std::fmod(std::atan2(t[1], t[0]), kTwoPiD);
+  if (az < 0) az += kTwoPiD;
+  const KPose e = camera_from_spherical(d, az, alt);
+  const double dt[3] = {e.tx - t[0], e.ty - t[1], e.tz - t[2]};
+  if (std::sqrt(sq3(dt)) > tol * std::max(1.0, d)) return false;
+  // coeffs() order (x, y, z, w), 4-term redux (x2 + y2) + (z2 + w2)
+  const double a[4] = {e.qx - pose.qx, e.qy - pose.qy, e.qz - pose.qz, e.qw - pose.qw};
+  const double b[4] = {e.qx + pose.qx, e.qy + pose.qy, e.qz + pose.qz, e.qw + pose.qw};
+  const double qa = std::sqrt((a[0] * a[0] + a[1] * a[1]) + (a[2] * a[2] + a[3] * a[3]));
+  const double qb = std::sqrt((b[0] * b[0] + b[1] * b[1]) + (b[2] * b[2] + b[3] * b[3]));
+  if (std::min(qa, qb) > tol) return false;
+  distance = d;
+  azimuth = az;
+  altitude = alt;
+  return true;
+}
+
+// tracking.cpp:27-37
+double lattice_at(double center, double extent, int n, int i) {
+  if (n == 1) return center;
+  return center - extent + 2.0 * extent * i / (n - 1);
+}
+
+void cam_params(b3d_gpu_context* ctx, KParams& p) {
+  p.cams = nullptr;
+  p.n_inst = ctx->cam_n;
+  for (int i = 0; i <= kMaxInst; ++i) p.inst_v0[i] = ctx->cam_v0[i];
+  for (int i = 0; i < kMaxInst; ++i) p.inst_pose[i] = ctx->cam_pose[i];
+  p.draw_base = 0;
+  p.base_keys = nullptr;
+}
+
+// score-many over camera poses (device-resident `cams` of n entries) into
+// device buffers scores/status
+void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, double* scores,
+                          uint8_t* status) {
+  const Mesh& m = *ctx->cam_mesh;
+  KParams p = base_params(ctx, m);
+  cam_params(ctx, p);
+  p.cams = cams;
+  p.n_hyp = n;
+  p.scores = scores;
+  p.status = status;
+  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, n, -1, true);
+  p.zscratch = ctx->zscratch.as<unsigned long long>();
+  p.vscratch = ctx->vscratch.as<double>();
+  p.vcap = lp.vcap;
+  p.zcap = lp.zcap;
+  p.zstride = lp.zstride;
+  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
+             "render_score launch (cameras)");
+}
 }  // namespace
 
 // =================================================================== C ABI
@@ -1091,6 +1314,344 @@ b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d
       sync = true;
     }
     if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "render_poses");
+  });
+}
+
+b3d_status b3d_box_mesh(const double lo[3], const double hi[3], double vertices[24],
+                        uint32_t triangles[36]) {
+  return guarded([&] {
+    check(lo && hi && vertices && triangles, "bad arguments");
+    // scene_graph.cpp:37-58: corners by bit layout (x=1, y=2, z=4), outward
+    // quads split (0,1,2), (0,2,3)
+    for (int i = 0; i < 8; ++i) {
+      vertices[3 * i + 0] = (i & 1) ? hi[0] : lo[0];
+      vertices[3 * i + 1] = (i & 2) ? hi[1] : lo[1];
+      vertices[3 * i + 2] = (i & 4) ? hi[2] : lo[2];
+    }
+    static const uint32_t quads[6][4] = {{0, 4, 6, 2}, {1, 3, 7, 5}, {0, 1, 5, 4},
+                                         {2, 6, 7, 3}, {0, 2, 3, 1}, {4, 5, 7, 6}};
+    for (int f = 0; f < 6; ++f) {
+      const uint32_t* q = quads[f];
+      const uint32_t t[6] = {q[0], q[1], q[2], q[0], q[2], q[3]};
+      for (int j = 0; j < 6; ++j) triangles[6 * f + j] = t[j];
+    }
+  });
+}
+
+b3d_status b3d_contact_to_pose(double table_w, double table_h, const double aabb_min[3],
+                               const double aabb_max[3], int32_t face, double dx, double dy,
+                               double dtheta, b3d_pose* out) {
+  return guarded([&] {
+    check(aabb_min && aabb_max && out, "bad arguments");
+    const KPose k =
+        contact_to_pose_host(table_w, table_h, aabb_min, aabb_max, face, dx, dy, dtheta);
+    *out = b3d_pose{k.qw, k.qx, k.qy, k.qz, k.tx, k.ty, k.tz};
+  });
+}
+
+b3d_status b3d_camera_pose_from_spherical(double distance, double azimuth, double altitude,
+                                          b3d_pose* out) {
+  return guarded([&] {
+    check(out != nullptr, "bad arguments");
+    const KPose k = camera_from_spherical(distance, azimuth, altitude);
+    *out = b3d_pose{k.qw, k.qx, k.qy, k.qz, k.tx, k.ty, k.tz};
+  });
+}
+
+int b3d_camera_pose_to_spherical(const b3d_pose* pose, double tol, double* distance,
+                                 double* azimuth, double* altitude) {
+  if (!pose || !distance || !azimuth || !altitude) return 0;
+  try {
+    const KPose k{pose->qw, pose->qx, pose->qy, pose->qz, pose->tx, pose->ty, pose->tz};
+    return camera_to_spherical(k, tol, *distance, *azimuth, *altitude) ? 1 : 0;
+  } catch (...) {
+    return 0;
+  }
+}
+
+b3d_status b3d_gpu_set_camera_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
+                                    const b3d_pose* model_to_world, uint32_t n) {
+  return guarded([&] {
+    check(ctx && mesh_ids && model_to_world, "bad arguments");
+    require(n >= 1 && n <= (uint32_t)kMaxInst, ErrorCode::invalid,
+            "camera scene: 1 to 16 instances");
+    DeviceGuard dg(ctx->device);
+    auto sm = std::make_unique<Mesh>();
+    long long nv = 0, nt = 0;
+    int sign = 2;
+    for (uint32_t i = 0; i < n; ++i) {
+      const Mesh& m = get_mesh(ctx, mesh_ids[i]);
+      ctx->cam_v0[i] = (int)nv;
+      nv += m.nv;
+      nt += m.nt;
+      sign = (sign == 2 || sign == m.cull) ? m.cull : 0;
+    }
+    require(nv < (1ll << 30) && nt < (1ll << 30), ErrorCode::invalid, "camera scene: too large");
+    for (uint32_t i = n; i <= (uint32_t)kMaxInst; ++i) ctx->cam_v0[i] = (int)nv;
+    sm->nv = (int)nv;
+    sm->nt = (int)nt;
+    sm->cull = sign == 2 ? 0 : sign;  // per-triangle culling only if every mesh shares a sign
+    sm->verts.ensure(24 * nv);
+    sm->tris.ensure(16 * nt);
+    std::vector<uint32_t> tri(4 * nt);
+    long long vo = 0, to = 0;
+    for (uint32_t i = 0; i < n; ++i) {
+      const Mesh& m = get_mesh(ctx, mesh_ids[i]);
+      cuda_check(cudaMemcpy(sm->verts.as<char>() + 24 * vo, m.verts.p, 24ull * m.nv,
+                            cudaMemcpyDeviceToDevice),
+                 "cudaMemcpy");
+      cuda_check(cudaMemcpy(tri.data() + 4 * to, m.tris.p, 16ull * m.nt, cudaMemcpyDeviceToHost),
+                 "cudaMemcpy");
+      for (long long k = 0; k < m.nt; ++k)
+        for (int j = 0; j < 3; ++j) tri[4 * (to + k) + j] += (uint32_t)vo;
+      vo += m.nv;
+      to += m.nt;
+      const b3d_pose& q = model_to_world[i];
+      ctx->cam_pose[i] = KPose{q.qw, q.qx, q.qy, q.qz, q.tx, q.ty, q.tz};
+    }
+    cuda_check(cudaMemcpy(sm->tris.p, tri.data(), 16ull * nt, cudaMemcpyHostToDevice),
+               "cudaMemcpy");
+    ctx->cam_mesh = std::move(sm);
+    ctx->cam_n = (int)n;
+  });
+}
+
+b3d_status b3d_gpu_render_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras, uint64_t n,
+                                  float* depth, int32_t* draw_index) {
+  return guarded([&] {
+    require_ready(ctx, false, false);
+    check(cameras && depth && n > 0, "bad arguments");
+    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    DeviceGuard dg(ctx->device);
+    const Mesh& m = *ctx->cam_mesh;
+    KParams p = base_params(ctx, m);
+    cam_params(ctx, p);
+    bool host_in = false;
+    p.cams = static_cast<const KPose*>(
+        stage_in(ctx, ctx->in_stage, cameras, sizeof(b3d_pose) * n, &host_in));
+    p.n_hyp = (long long)n;
+    p.lik.n_noise = 0;  // render only
+    const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+    const bool dev_d = is_device_ptr(depth);
+    const bool dev_i = draw_index && is_device_ptr(draw_index);
+    if (dev_d) {
+      p.out_depth = depth;
+    } else {
+      ctx->out_stage.ensure(4 * npx * n);
+      p.out_depth = ctx->out_stage.as<float>();
+    }
+    if (draw_index) {
+      if (dev_i) {
+        p.out_ids = draw_index;
+      } else {
+        ctx->out_stage2.ensure(4 * npx * n);
+        p.out_ids = ctx->out_stage2.as<int32_t>();
+      }
+    }
+    if (draw_index) {
+      LaunchPlan lp = plan_launch<true, false, true>(ctx, m, (long long)n);
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
+      cuda_check(launch_render_score<true, false, true>(p, lp.grid, lp.smem, ctx->stream),
+                 "render launch (cameras)");
+    } else {
+      LaunchPlan lp = plan_launch<false, false, true>(ctx, m, (long long)n);
+      p.zscratch = ctx->zscratch.as<unsigned long long>();
+      p.vscratch = ctx->vscratch.as<double>();
+      p.vcap = lp.vcap;
+      p.zcap = lp.zcap;
+      p.zstride = lp.zstride;
+      cuda_check(launch_render_score<false, false, true>(p, lp.grid, lp.smem, ctx->stream),
+                 "render launch (cameras)");
+    }
+    bool sync = host_in;
+    if (!dev_d) {
+      finish_copy_out(ctx, depth, p.out_depth, 4 * npx * n);
+      sync = true;
+    }
+    if (draw_index && !dev_i) {
+      finish_copy_out(ctx, draw_index, p.out_ids, 4 * npx * n);
+      sync = true;
+    }
+    if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "render_cameras");
+  });
+}
+
+b3d_status b3d_gpu_score_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras, uint64_t n,
+                                 double* scores, uint8_t* status) {
+  return guarded([&] {
+    require_ready(ctx, true, true);
+    check(cameras && scores && n > 0, "bad arguments");
+    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    DeviceGuard dg(ctx->device);
+    bool host_in = false;
+    const KPose* cams = static_cast<const KPose*>(
+        stage_in(ctx, ctx->in_stage, cameras, sizeof(b3d_pose) * n, &host_in));
+    const int nn = ctx->lik.n_noise;
+    const bool dev_scores = is_device_ptr(scores);
+    const bool dev_status = status && is_device_ptr(status);
+    double* d_scores = scores;
+    uint8_t* d_status = status;
+    if (!dev_scores) {
+      ctx->out_stage.ensure(sizeof(double) * n * nn);
+      d_scores = ctx->out_stage.as<double>();
+    }
+    if (status && !dev_status) {
+      ctx->out_stage2.ensure(n);
+      d_status = ctx->out_stage2.as<uint8_t>();
+    }
+    launch_score_cameras(ctx, cams, (long long)n, d_scores, d_status);
+    bool sync = host_in;
+    if (!dev_scores) {
+      finish_copy_out(ctx, scores, d_scores, sizeof(double) * n * nn);
+      sync = true;
+    }
+    if (status && !dev_status) {
+      finish_copy_out(ctx, status, d_status, n);
+      sync = true;
+    }
+    if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "score_cameras");
+  });
+}
+
+b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint32_t n_frames,
+                                const b3d_pose* initial, const b3d_track_search* search,
+                                b3d_pose* out_poses, double* out_frame_ms) {
+  return guarded([&] {
+    check(ctx && frames && initial && search && out_poses, "bad arguments");
+    require(n_frames >= 1, ErrorCode::invalid, "track_camera: empty frame list");
+    require_ready(ctx, false, true);
+    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    require(ctx->lik.n_noise == 1, ErrorCode::invalid, "track_camera: one noise setting");
+    const b3d_track_search& s = *search;
+    // TrackSearch::validate (tracking.cpp:49-57)
+    require(s.pos_extent > 0 && s.angle_extent > 0, ErrorCode::invalid,
+            "track search: extents must be positive");
+    require(s.points_per_dim >= 2, ErrorCode::invalid,
+            "track search: need at least 2 points per dimension");
+    require(s.refine_stages >= 0 && s.refine_factor > 1, ErrorCode::invalid,
+            "track search: bad refinement settings");
+    require(s.beam_width >= 1, ErrorCode::invalid, "track search: beam width must be >= 1");
+    DeviceGuard dg(ctx->device);
+    using Clock = std::chrono::steady_clock;
+    auto frame_start = Clock::now();
+    auto close_frame = [&](uint32_t f) {
+      const double ms =
+          std::chrono::duration<double, std::milli>(Clock::now() - frame_start).count();
+      if (out_frame_ms) out_frame_ms[f] = std::max(ms, 1e-6);
+      frame_start = Clock::now();
+    };
+    struct Sph {
+      double d, az, alt;
+    };
+    struct Cand {
+      Sph c;
+      double score;
+    };
+    const KPose init{initial->qw, initial->qx, initial->qy, initial->qz,
+                     initial->tx, initial->ty, initial->tz};
+    Sph start{};
+    require(camera_to_spherical(init, 1e-6, start.d, start.az, start.alt), ErrorCode::invalid,
+            "track_camera: initial pose must look at the origin with up = +z");
+    out_poses[0] = *initial;
+    close_frame(0);
+    std::vector<Cand> beam{{start, 0.0}};
+    const int ppd = s.points_per_dim;
+    const size_t n_grid = (size_t)ppd * ppd * ppd;
+    const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+    const bool dev_frames = is_device_ptr(frames);
+    std::vector<KPose> cams;
+    std::vector<int> slot;
+    std::vector<double> dscore;
+    ctx->c2f_scores.ensure(8 * n_grid);
+    ctx->c2f_centers.ensure(sizeof(KPose) * n_grid);
+    constexpr double kNegInf = -std::numeric_limits<double>::infinity();
+    for (uint32_t f = 1; f < n_frames; ++f) {
+      const float* fr = frames + (size_t)f * npx;
+      {  // ObservationCache::build for this frame (tracking.cpp:112)
+        bool host = false;
+        const float* d = dev_frames ? fr
+                                    : static_cast<const float*>(stage_in(
+                                          ctx, ctx->obs_depth, fr, npx * 4, &host));
+        ctx->obs_pts.ensure(npx * sizeof(float4));
+        cuda_check(launch_obs_prepare(d, (int)ctx->k.width, (int)ctx->k.height,
+                                      static_cast<float>(ctx->k.far_m), (float)ctx->k.cx,
+                                      (float)ctx->k.cy, (float)(1.0 / ctx->k.fx),
+                                      (float)(1.0 / ctx->k.fy), ctx->obs_pts.as<float4>(),
+                                      ctx->obs_count.as<int>(), ctx->stream),
+                   "obs_prepare launch");
+        ctx->has_obs = true;
+        ++ctx->obs_version;
+      }
+      std::vector<Cand> next;
+      for (const Cand& seed : beam) {
+        Sph center = seed.c;
+        double pe = s.pos_extent, ae = s.angle_extent;
+        Cand stage_best{center, kNegInf};
+        for (int st = 0; st <= s.refine_stages; ++st) {
+          std::vector<Sph> grid;
+          grid.reserve(n_grid);
+          for (int i = 0; i < ppd; ++i)
+            for (int j = 0; j < ppd; ++j)
+              for (int k = 0; k < ppd; ++k)
+                grid.push_back({lattice_at(center.d, pe, ppd, i), lattice_at(center.az, ae, ppd, j),
+                                lattice_at(center.alt, ae, ppd, k)});
+          // score_pose (tracking.cpp:100-108): out-of-range coordinates score -inf
+          cams.clear();
+          slot.assign(grid.size(), -1);
+          for (size_t i = 0; i < grid.size(); ++i) {
+            const Sph& g = grid[i];
+            if (g.d <= 0 || g.alt <= 0 || g.alt >= kHalfPi) continue;
+            slot[i] = (int)cams.size();
+            cams.push_back(camera_from_spherical(g.d, g.az, g.alt));
+          }
+          std::vector<double> scores(grid.size(), kNegInf);
+          if (!cams.empty()) {
+            cuda_check(cudaMemcpyAsync(ctx->c2f_centers.p, cams.data(), sizeof(KPose) * cams.size(),
+                                       cudaMemcpyHostToDevice, ctx->stream),
+                       "cudaMemcpyAsync cameras");
+            launch_score_cameras(ctx, ctx->c2f_centers.as<KPose>(), (long long)cams.size(),
+                                 ctx->c2f_scores.as<double>(), nullptr);
+            dscore.resize(cams.size());
+            cuda_check(cudaMemcpyAsync(dscore.data(), ctx->c2f_scores.p, 8 * cams.size(),
+                                       cudaMemcpyDeviceToHost, ctx->stream),
+                       "cudaMemcpyAsync scores");
+            cuda_check(cudaStreamSynchronize(ctx->stream), "track_camera stage");
+            for (size_t i = 0; i < grid.size(); ++i)
+              if (slot[i] >= 0) scores[i] = dscore[slot[i]];
+          }
+          size_t best = 0;  // tracking.cpp:132-134 (strict >, first index)
+          for (size_t i = 1; i < scores.size(); ++i)
+            if (scores[i] > scores[best]) best = i;
+          require(std::isfinite(scores[best]), ErrorCode::numeric,
+                  "track_camera: every candidate pose scored -inf");
+          center = grid[best];
+          stage_best = {center, scores[best]};
+          if (s.beam_width > 1 && st == s.refine_stages) {
+            std::vector<size_t> order(grid.size());
+            for (size_t i = 0; i < order.size(); ++i) order[i] = i;
+            std::stable_sort(order.begin(), order.end(),
+                             [&](size_t a, size_t b) { return scores[a] > scores[b]; });
+            const size_t keep = std::min<size_t>((size_t)s.beam_width, order.size());
+            for (size_t i = 0; i < keep; ++i) next.push_back({grid[order[i]], scores[order[i]]});
+          }
+          pe /= s.refine_factor;
+          ae /= s.refine_factor;
+        }
+        if (s.beam_width == 1) next.push_back(stage_best);
+      }
+      std::stable_sort(next.begin(), next.end(),
+                       [](const Cand& a, const Cand& b) { return a.score > b.score; });
+      if (next.size() > (size_t)s.beam_width) next.resize(s.beam_width);
+      beam = std::move(next);
+      const Sph& top = beam.front().c;
+      const KPose cp = camera_from_spherical(top.d, top.az, top.alt);
+      out_poses[f] = b3d_pose{cp.qw, cp.qx, cp.qy, cp.qz, cp.tx, cp.ty, cp.tz};
+      close_frame(f);
+    }
   });
 }
 

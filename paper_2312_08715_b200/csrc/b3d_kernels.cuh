@@ -42,6 +42,7 @@ struct KGrid {
 };
 
 constexpr int kMaxNoise = 4;
+constexpr int kMaxInst = 16;
 constexpr int kCheb = 64;
 
 struct KLik {
@@ -85,6 +86,15 @@ struct KParams {
   const double* plane_off;  // distinct offsets per class, ascending
   const int* plane_end;     // tris_s index one past each plane's triangles
   int plane_begin[8];       // class c's planes = [plane_begin[c], plane_begin[c+1])
+  // camera mode (render_instances under per-hypothesis cameras,
+  // renderer.cpp:153-189 / tracking.cpp:100-108): hypothesis h is the
+  // camera-to-world pose cams[h]; the mesh is the concatenation of n_inst
+  // instances in draw order, instance i = vertices [inst_v0[i], inst_v0[i+1])
+  // with model-to-world pose inst_pose[i]
+  const KPose* cams;
+  int n_inst;
+  int inst_v0[kMaxInst + 1];
+  KPose inst_pose[kMaxInst];
   // hypotheses
   const KPose* poses;  // nullptr => grid
   KGrid grid;

@@ -114,6 +114,16 @@ __device__ __forceinline__ void grid_pose(const KGrid& g, long long index, KPose
   out.tz = lattice(c.tz, g.extent[2], g.count[2], iz);
 }
 
+// geometry.cpp:26-31 inverse(p): q' = normalized(conj q), t' = -(q' t)
+// (same operation order as the host's pose_inverse in b3d_capi.cpp).
+__device__ __forceinline__ KPose pose_inverse(const KPose& p) {
+  const Q q = q_normalized(Q{p.qw, -p.qx, -p.qy, -p.qz});
+  const double v[3] = {p.tx, p.ty, p.tz};
+  double r[3];
+  q_rotate(q, v, r);
+  return KPose{q.w, q.x, q.y, q.z, -r[0], -r[1], -r[2]};
+}
+
 // geometry.cpp:19-24 compose(a, b) -> rotation matrix (Eigen
 // toRotationMatrix) + translation.  R row-major.
 __device__ __forceinline__ void pose_to_rt(const KPose& a, const KPose& b, double R[9], double t[3]) {

@@ -9,6 +9,7 @@ B3D_RS_SCORE_KERNELS(extern, 1)
 B3D_RS_SCORE_KERNELS(extern, 2)
 B3D_RS_SCORE_KERNELS(extern, 3)
 B3D_RS_SCORE_KERNELS(extern, -1)
+B3D_RS_CAM_KERNELS(extern)
 
 // ---------------------------------------------------------------- base scene
 // Padded depth-bit image of the base scene (halo of `pad` background pixels)
@@ -111,19 +112,22 @@ __global__ void obs_prepare_kernel(const float* depth, int W, int H, float far_f
 }
 
 // Host-side launch helpers (declared in b3d_capi.cpp).
-template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1>
+template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, bool kCam = false>
 static auto pick_vs(bool vs) {
-  return vs ? render_score_kernel<kIds, kScore, kOut, true, kWin, kS1>
-            : render_score_kernel<kIds, kScore, kOut, false, kWin, kS1>;
+  return vs ? render_score_kernel<kIds, kScore, kOut, true, kWin, kS1, kCam>
+            : render_score_kernel<kIds, kScore, kOut, false, kWin, kS1, kCam>;
 }
 
 // Score kernels are instantiated per window radius 0..3 (else generic) and
 // for one / several distinct sigmas -- one small kernel per launch keeps the
 // hot instruction footprint down; render kernels once.
 template <bool kIds, bool kScore, bool kOut>
-static auto pick_kernel(bool vs, int window, int n_slots) {
+static auto pick_kernel(bool vs, int window, int n_slots, bool cam = false) {
   if constexpr (kScore && !kIds) {
     const bool s1 = n_slots == 1;
+    if (cam)  // camera mode: generic window loop
+      return s1 ? pick_vs<kIds, kScore, kOut, -1, true, true>(vs)
+                : pick_vs<kIds, kScore, kOut, -1, false, true>(vs);
     switch (window) {
       case 0: return s1 ? pick_vs<kIds, kScore, kOut, 0, true>(vs) : pick_vs<kIds, kScore, kOut, 0, false>(vs);
       case 1: return s1 ? pick_vs<kIds, kScore, kOut, 1, true>(vs) : pick_vs<kIds, kScore, kOut, 1, false>(vs);
@@ -134,13 +138,15 @@ static auto pick_kernel(bool vs, int window, int n_slots) {
   } else {
     (void)window;
     (void)n_slots;
-    return pick_vs<kIds, kScore, kOut, -1, false>(vs);
+    return cam ? pick_vs<kIds, kScore, kOut, -1, false, true>(vs)
+               : pick_vs<kIds, kScore, kOut, -1, false>(vs);
   }
 }
 
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_slots);
+  auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_slots,
+                                              p.cams != nullptr);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);
   if (e != cudaSuccess) return e;
@@ -161,12 +167,14 @@ cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs) {
 template <bool kIds, bool kScore, bool kOut>
 size_t static_smem_render_score() {
   size_t mx = 0;
-  for (int vs = 0; vs < 2; ++vs) {
-    cudaFuncAttributes a{};
-    if (cudaFuncGetAttributes(&a, pick_kernel<kIds, kScore, kOut>(vs, 1, 1)) != cudaSuccess)
-      return 8192;
-    if (a.sharedSizeBytes > mx) mx = a.sharedSizeBytes;
-  }
+  for (int vs = 0; vs < 2; ++vs)
+    for (int cam = 0; cam < 2; ++cam) {
+      cudaFuncAttributes a{};
+      if (cudaFuncGetAttributes(&a, pick_kernel<kIds, kScore, kOut>(vs, 1, 1, cam)) !=
+          cudaSuccess)
+        return 8192;
+      if (a.sharedSizeBytes > mx) mx = a.sharedSizeBytes;
+    }
   return mx;
 }
 

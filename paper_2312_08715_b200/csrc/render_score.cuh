@@ -417,6 +417,56 @@ constexpr int kWarps = kThreads / 32;
 
 }  // namespace
 
+// Triangles whose bbox exceeds kHugeBox pixels (a table face filling the
+// image): the whole warp sweeps the bbox of lane `src`'s triangle (vertex
+// ids already in positive-area order), one pixel per lane per step, with the
+// reference's per-pixel arithmetic (renderer.cpp:78-102).
+constexpr int kHugeBox = 64;
+
+template <bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void sweep_huge(const KParams& p, Key* const zb, const Region& rg,
+                                           const VS& vs, int src, uint4 tr, uint32_t box,
+                                           uint32_t box2, int lane) {
+  const uint32_t ia = __shfl_sync(0xffffffffu, tr.x, src);
+  const uint32_t ib = __shfl_sync(0xffffffffu, tr.y, src);
+  const uint32_t ic = __shfl_sync(0xffffffffu, tr.z, src);
+  const uint32_t draw = p.draw_base + __shfl_sync(0xffffffffu, tr.w, src);
+  const uint32_t b1 = __shfl_sync(0xffffffffu, box, src);
+  const uint32_t b2 = __shfl_sync(0xffffffffu, box2, src);
+  const int u0 = b1 & 0xffff, v0 = b1 >> 16;
+  const int bw = (int)(b2 & 0xffff) - u0 + 1, bh = (int)(b2 >> 16) - v0 + 1;
+  const double2 A = vs.uv(ia), B = vs.uv(ib), C = vs.uv(ic);
+  const double iza = vs.iz(ia), izb = vs.iz(ib), izc = vs.iz(ic);
+  const SV a{A.x, A.y, 0.0}, b{B.x, B.y, 0.0}, c{C.x, C.y, 0.0};
+  const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+  const double ia2 = __drcp_rn((B.x - A.x) * (C.y - A.y) - (B.y - A.y) * (C.x - A.x));
+  for (int row = 0; row < bh; ++row) {
+    const int pv = v0 + row;
+    const double py = pv;
+    for (int col = lane; col < bw; col += 32) {
+      const int pu = u0 + col;
+      const double px = pu;
+      const double e_ab = edge_at(A, B, fl & 1, px, py);
+      const double e_bc = edge_at(B, C, fl & 2, px, py);
+      const double e_ca = edge_at(C, A, fl & 4, px, py);
+      if (!edge_covers(e_ab, fl & 8) || !edge_covers(e_bc, fl & 16) || !edge_covers(e_ca, fl & 32))
+        continue;
+      const double inv_z = (e_bc * iza + e_ca * izb + e_ab * izc) * ia2;
+      if (!(inv_z > 0)) continue;
+      const double z = __drcp_rn(inv_z);
+      if (z < p.near_lim || z > p.far_m) continue;
+      const float zf = __double2float_rn(z);
+      if (!(zf < p.far_f)) continue;
+      Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+      if (kIds)
+        zmin((unsigned long long*)cell,
+             ((unsigned long long)__float_as_uint(zf) << 32) | (unsigned long long)draw);
+      else
+        zmin((unsigned int*)cell, __float_as_uint(zf));
+    }
+  }
+}
+
 // Pass 2 for the <= 2x2 class: lane l takes queue entry head + l (l < n)
 // and finishes it alone -- the 4 tile pixels' edge values (renderer.cpp:32-34
 // factored into 2 row and 2 column products per edge, bitwise the reference's
@@ -589,12 +639,14 @@ struct HypCtx {
 // render-many output and/or likelihood.  Instantiated twice per kernel so
 // that the z-buffer accesses compile to shared-memory instructions (kZS) or
 // global ones (overflow scratch), never to generic ones.
-template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, typename VS, typename Key>
+template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, bool kCam, typename VS,
+          typename Key>
 __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
                                          const VS& vs, WarpQ* const wq, int* const s_seg,
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
-                                         int (*s_redi)[kMaxNoise + 1], long long h) {
+                                         int (*s_redi)[kMaxNoise + 1], long long h,
+                                         const double* inst_rt) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Region& rg = hc.rg;
   const double* const R = hc.R;
@@ -621,7 +673,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   // score mode: the work list is the front part of each axis class (the cut
   // of phase B) plus all of class 6; s_seg[0..7] = running work counts,
   // s_seg[8..14] = first tris_s index of each segment
-  constexpr bool kSorted = kScore && !kIds;
+  constexpr bool kSorted = kScore && !kIds && !kCam;
   if (kSorted && tid == 0) {
     const bool cut = p.cull != 0 && !hc.clip;
     int cum = 0;
@@ -669,8 +721,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       __syncwarp();
       const int ti = base + lane;
       int cls = -1;
-      uint4 ent;
-      uint32_t box = 0;
+      uint4 ent = make_uint4(0u, 0u, 0u, 0u);
+      uint32_t box = 0, box2 = 0;
 #if B3D_PREFETCH
       const uint4 tri_cur = tri_next;
       if (ti + c_stride < n_work) tri_next = work_tri(ti + c_stride);
@@ -684,7 +736,14 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
         const short4 A = vs.bb(ia), B = vs.bb(ib), C = vs.bb(ic);
         if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
-          raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
+          if (kCam) {  // the triangle's instance transform (camera mode)
+            int ins = 0;
+            while (ins + 1 < p.n_inst && (int)ia >= p.inst_v0[ins + 1]) ++ins;
+            raster_clipped<kIds>(p, zb, rg, inst_rt + 12 * ins, inst_rt + 12 * ins + 9, ia, ib,
+                                 ic, p.draw_base + (uint32_t)ti);
+          } else {
+            raster_clipped<kIds>(p, zb, rg, R, t, ia, ib, ic, p.draw_base + (uint32_t)ti);
+          }
         } else {
           const int u_min = min(min(A.x, B.x), C.x), v_min = min(min(A.z, B.z), C.z);
           const int u_max = max(max(A.y, B.y), C.y), v_max = max(max(A.w, B.w), C.w);
@@ -708,15 +767,22 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                 ent = make_uint4(ia, ib, ic, (uint32_t)ti);
                 box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
                       (uint32_t)(bh - 1) << 30;
-              } else {  // large bbox: the reference's per-pixel loop
+              } else if (bw * bh <= kHugeBox) {  // the reference's per-pixel loop
                 raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz(ia)},
                                      SV{PB.x, PB.y, vs.iz(ib)}, SV{PC.x, PC.y, vs.iz(ic)},
                                      u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
+              } else {  // huge bbox: swept by the whole warp below
+                cls = 3;
+                ent = make_uint4(ia, ib, ic, (uint32_t)ti);
+                box = (uint32_t)u_min | (uint32_t)v_min << 16;
+                box2 = (uint32_t)u_max | (uint32_t)v_max << 16;
               }
             }
           }
         }
       }
+      for (uint32_t hb = __ballot_sync(0xffffffffu, cls == 3); hb; hb &= hb - 1)
+        sweep_huge<kIds>(p, zb, rg, vs, __ffs(hb) - 1, ent, box, box2, lane);
       const uint32_t b0 = __ballot_sync(0xffffffffu, cls == 0);
       const uint32_t b1 = __ballot_sync(0xffffffffu, cls == 1);
       if (cls == 0) {
@@ -921,7 +987,7 @@ struct VertexCache {
 // kIds: 64-bit (depth, draw) keys; kScore: run the likelihood epilogue;
 // kOut: write the full depth / id images to HBM (render-many); kVS: the
 // projected vertices fit in shared memory.
-template <bool kIds, bool kScore, bool kOut, bool kVS, int kWin, bool kS1>
+template <bool kIds, bool kScore, bool kOut, bool kVS, int kWin, bool kS1, bool kCam>
 __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_pose[32][12];  // R (row-major) | t per upcoming hypothesis
@@ -931,6 +997,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
   __shared__ double s_coef[kMaxNoise];
   __shared__ int s_count;
   __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
+  __shared__ double s_inst[kCam ? kMaxInst : 1][12];  // camera mode: R | t per instance
   using Key = typename KeyT<kIds>::T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -957,7 +1024,14 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
   for (long long h = blockIdx.x; h < p.n_hyp; h += G, ++kk) {
     // ---- A: poses of this CTA's next 32 hypotheses, one per lane of warp 0
     // (compose with inverse(camera) -> rotation matrix + translation)
-    if ((kk & 31) == 0 && warp == 0) {
+    if (kCam) {
+      // camera mode: M2C_i = compose(inverse(camera_h), model_to_world_i)
+      // (renderer.cpp:164-170) for every instance
+      if (tid < p.n_inst) {
+        const KPose w2c = pm::pose_inverse(p.cams[h]);
+        pose_to_rt(w2c, p.inst_pose[tid], s_inst[tid], s_inst[tid] + 9);
+      }
+    } else if ((kk & 31) == 0 && warp == 0) {
       const long long hh = h + (long long)lane * G;
       if (hh < p.n_hyp) {
         KPose hp;
@@ -987,7 +1061,13 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     int lo_u = INT_MAX, lo_v = INT_MAX, hi_u = INT_MIN, hi_v = INT_MIN, clip = 0;
     for (int i = tid; i < p.nv; i += kThreads) {
       double c[3];
-      cam_vertex(R, t, p.verts + 3 * (size_t)i, c);
+      if (kCam) {
+        int ins = 0;
+        while (ins + 1 < p.n_inst && i >= p.inst_v0[ins + 1]) ++ins;
+        cam_vertex(s_inst[ins], s_inst[ins] + 9, p.verts + 3 * (size_t)i, c);
+      } else {
+        cam_vertex(R, t, p.verts + 3 * (size_t)i, c);
+      }
       if (c[2] >= p.near_m) {
         const SV s = project(p, c[0], c[1], c[2]);
         const short4 bb = vertex_bbox(p, s.u, s.v);
@@ -1005,7 +1085,7 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     // camera centre C = -R^T t (model frame) are those with plane offset
     // o <= n . C: a prefix of the class (b3d_kernels.cuh).  The small margin
     // keeps near-edge-on planes; they go through the exact tests.
-    if (kScore && !kIds && warp < 6) {
+    if (kScore && !kIds && !kCam && warp < 6) {
       const int k = warp >> 1;
       const double Ck = -(R[k] * t[0] + R[3 + k] * t[1] + R[6 + k] * t[2]);
       const double thr = (warp & 1) ? -Ck : Ck;
@@ -1059,12 +1139,12 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut, kWin, kS1>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
-                                              s_red, s_redi, h);
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
+                                                    s_red, s_redi, h, &s_inst[0][0]);
     else
-      hyp_body<kIds, kScore, kOut, kWin, kS1>(
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
-          s_seg, &s_count, s_coef, s_red, s_redi, h);
+          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0]);
     __syncthreads();
   }
 }
@@ -1073,8 +1153,17 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
 
 // Explicit instantiations of the score kernels, one translation unit per
 // window radius (rs_score_w*.cu) so they compile in parallel.
-#define B3D_RS_SCORE_KERNELS(X, W)                                                         \
-  X template __global__ void render_score_kernel<false, true, false, true, W, true>(const KParams); \
-  X template __global__ void render_score_kernel<false, true, false, false, W, true>(const KParams); \
-  X template __global__ void render_score_kernel<false, true, false, true, W, false>(const KParams); \
-  X template __global__ void render_score_kernel<false, true, false, false, W, false>(const KParams);
+#define B3D_RS_SCORE_KERNELS2(X, W, C)                                                           \
+  X template __global__ void render_score_kernel<false, true, false, true, W, true, C>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, false, W, true, C>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, true, W, false, C>(const KParams); \
+  X template __global__ void render_score_kernel<false, true, false, false, W, false, C>(const KParams);
+#define B3D_RS_SCORE_KERNELS(X, W) B3D_RS_SCORE_KERNELS2(X, W, false)
+// camera mode (multi-instance scene under per-hypothesis cameras): score
+// kernels with the generic window loop, and the render kernels
+#define B3D_RS_CAM_KERNELS(X)                                                                    \
+  B3D_RS_SCORE_KERNELS2(X, -1, true)                                                             \
+  X template __global__ void render_score_kernel<true, false, true, true, -1, false, true>(const KParams);  \
+  X template __global__ void render_score_kernel<true, false, true, false, -1, false, true>(const KParams); \
+  X template __global__ void render_score_kernel<false, false, true, true, -1, false, true>(const KParams); \
+  X template __global__ void render_score_kernel<false, false, true, false, -1, false, true>(const KParams);

@@ -72,3 +72,26 @@ def test_mesh_cull_sign_closed_open_and_flipped():
     bv, bt = O.box_mesh([-0.05, -0.04, 0.0], [0.05, 0.04, 0.09])
     assert b3d.mesh_cull_sign(bv, bt) in (1, -1)
     assert b3d.mesh_cull_sign(bv, bt[:1]) == 0
+
+
+def test_box_mesh_and_contact_to_pose_match_oracle_bitwise():
+    """Host scene-graph helpers of the product (make_box_mesh,
+    contact_to_pose) against the oracle restatement."""
+    from oracle import pyoracle as O
+    from paper_2312_08715_b200 import synth
+    lo, hi = np.array([-0.25, -0.2, -0.01]), np.array([0.25, 0.2, 0.0])
+    v1, t1 = b3d.box_mesh(lo, hi)
+    v2, t2 = O.box_mesh(lo, hi)
+    np.testing.assert_array_equal(v1, v2)
+    np.testing.assert_array_equal(t1, t2)
+    assert b3d.mesh_cull_sign(v1, t1) == 1
+    v, t = b3d.voxel_to_mesh(synth.eden_blob(400, 2), 0.005, np.zeros(3))
+    amin, amax = v.min(axis=0), v.max(axis=0)
+    rng = np.random.Generator(np.random.PCG64(6))
+    for face in range(1, 7):
+        for _ in range(30):
+            dx, dy, th = rng.uniform(0, 0.3), rng.uniform(0, 0.3), rng.uniform(0, 6.28)
+            np.testing.assert_array_equal(b3d.contact_to_pose(0.5, 0.5, amin, amax, face, dx, dy, th),
+                                          O.contact_to_pose(0.5, 0.5, amin, amax, face, dx, dy, th))
+    with pytest.raises(b3d.B3DError):
+        b3d.contact_to_pose(0.5, 0.5, amin, amax, 1, 0.49, 0.1, 0.0)

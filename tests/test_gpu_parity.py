@@ -512,3 +512,80 @@ def test_back_face_culling_with_base_scene_and_near_clip(gpu_ctx, oracle):
     a, b = _scores_with_and_without_culling(gpu_ctx, lambda: gpu_ctx.score_poses(m, poses)[0])
     np.testing.assert_array_equal(a, b)
     gpu_ctx.set_base_scene([], [])
+
+
+def _orbit(oracle, res, n_frames=40, n_voxels=600):
+    rc = lambda k, inst, cams: np.stack([oracle.render(k, inst, camera=c) for c in cams])
+    return configs.orbit_sequence(rc, oracle.voxel_to_mesh, oracle.box_mesh,
+                                  oracle.contact_to_pose, res=res, n_frames=n_frames,
+                                  n_voxels=n_voxels)
+
+
+def _camera_scene(ctx, seq):
+    from helpers import b3d_intr
+    ctx.set_camera(b3d_intr(seq["k"]))
+    mids = [ctx.upload_mesh(v, t) for v, t, _ in seq["instances"]]
+    ctx.set_camera_scene(mids, [p for _, _, p in seq["instances"]])
+
+
+def test_render_cameras_multi_instance_parity(gpu_ctx, oracle):
+    """render_instances (renderer.cpp:153-189) of table + object under camera
+    hypotheses: depth and global draw indices bit-identical to the oracle,
+    including cameras close enough to clip the table at z = near."""
+    for res in (50, 100):
+        seq = _orbit(oracle, res)
+        _camera_scene(gpu_ctx, seq)
+        rng = np.random.Generator(np.random.PCG64(res))
+        cams = [oracle.camera_pose_from_spherical(rng.uniform(0.3, 1.5), rng.uniform(0, 6.28),
+                                                  rng.uniform(0.2, 1.4)) for _ in range(8)]
+        cams.append(oracle.camera_pose_from_spherical(0.12, 0.5, 0.3))  # near-plane clipping
+        d, ids = gpu_ctx.render_cameras(np.array(cams))
+        for i, c in enumerate(cams):
+            od, oi = oracle.render(seq["k"], seq["instances"], camera=c, with_ids=True)
+            np.testing.assert_array_equal(d[i].view(np.uint32), od.view(np.uint32))
+            np.testing.assert_array_equal(ids[i], oi)
+        assert (ids[:-1] >= seq["instances"][0][1].shape[0]).any()  # object pixels present
+
+
+def test_score_cameras_parity(gpu_ctx, oracle):
+    seq = _orbit(oracle, 100)
+    _camera_scene(gpu_ctx, seq)
+    cam0 = oracle.camera_pose_from_spherical(seq["distance"], 0.4, seq["altitude"])
+    obs = configs.orbit_frames(seq, [cam0])[0]
+    gpu_ctx.set_observation(obs)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    rng = np.random.Generator(np.random.PCG64(12))
+    cams = np.array([oracle.camera_pose_from_spherical(0.9 + rng.uniform(-0.05, 0.05),
+                                                       0.4 + rng.uniform(-0.2, 0.2),
+                                                       seq["altitude"] + rng.uniform(-0.2, 0.2))
+                     for _ in range(64)])
+    s_gpu, st = gpu_ctx.score_cameras(cams)
+    s_orc = np.array([oracle.windowed_loglik_multi(
+        obs, oracle.render(seq["k"], seq["instances"], camera=c), seq["k"], [seq["noise"]],
+        seq["sigma_max"], seq["window"])[0] for c in cams])
+    assert (st == 0).all()
+    assert rel_err(s_gpu[:, 0], s_orc).max() <= SCORE_RTOL
+
+
+def test_track_camera_matches_oracle(gpu_ctx, oracle):
+    """bench-tracking's orbit (harness.cpp:743-770) at 50 x 50: the device
+    track_camera picks the oracle's lattice point at every frame (poses
+    bitwise equal; a differing pick must tie within the score tolerance)."""
+    seq = _orbit(oracle, 50)
+    _camera_scene(gpu_ctx, seq)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    cams = [oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+            for a in seq["azimuths"][:4]]
+    frames = configs.orbit_frames(seq, cams)
+    est, ms = gpu_ctx.track_camera(frames, cams[0])
+    log = []
+    ref = oracle.track_camera(frames, seq["k"], seq["instances"], cams[0], seq["noise"],
+                              seq["sigma_max"], seq["window"], stage_log=log)
+    assert (ms > 0).all()
+    for f in range(4):
+        if not np.array_equal(est[f], ref[f]):
+            # only a score tie inside the tolerance may flip the pick
+            _, _, grid, scores = [e for e in log if e[0] == f][-1]
+            s = np.array(scores)
+            assert np.sort(s)[-1] - np.sort(s)[-2] <= SCORE_RTOL * abs(np.max(s))
+        assert np.linalg.norm(est[f][4:] - cams[f][4:]) < 0.03
