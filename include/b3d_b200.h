@@ -259,6 +259,13 @@ B3D_API b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id
                                            uint64_t* rng_state, b3d_stage_result* out,
                                            double* scores);
 
+/* score-many over a device pose grid followed by the stage reduction of
+ * scores[:, 0] (argmax, logsumexp, one draw with rng_state if non-NULL) in
+ * one call.  All buffers device memory; asynchronous on the context stream. */
+B3D_API b3d_status b3d_gpu_enumerate_grid(b3d_gpu_context* ctx, int32_t mesh_id,
+                                          const b3d_pose_grid* grid, uint64_t* rng_state,
+                                          b3d_stage_result* out, double* scores);
+
 /* Score hypotheses [first, first + n) of a device pose grid (one rank's
  * shard of a large enumeration); scores[i] is hypothesis
  * first + i. */

@@ -158,6 +158,7 @@ def lib() -> C.CDLL:
         "b3d_gpu_set_base_scene": ([vp, vp, vp, u32], st),
         "b3d_gpu_sample_many": ([vp, vp, u64, u32, u32, vp, u32, vp, vp], st),
         "b3d_gpu_enumerate_poses": ([vp, i32, vp, u64, vp, vp, vp], st),
+        "b3d_gpu_enumerate_grid": ([vp, i32, C.POINTER(PoseGrid), vp, vp, vp], st),
         "b3d_gpu_score_grid_range": ([vp, i32, C.POINTER(PoseGrid), u64, u64, vp, vp], st),
         "b3d_gpu_score_contact_grid": ([vp, i32, C.POINTER(ContactGrid), vp, vp], st),
         "b3d_contact_grid_poses": ([C.POINTER(ContactGrid), vp], st),
@@ -416,6 +417,12 @@ class GpuContext:
         _check(self._L.b3d_gpu_score_grid(self.h, mesh, C.byref(grid), _ptr(scores),
                                           _ptr(status)))
         return scores, status
+
+    def enumerate_grid(self, mesh: int, grid: PoseGrid, rng_state, out, scores):
+        """score_grid + stage reduction fused into one launch
+        (b3d_gpu_enumerate_grid); device tensors only, asynchronous."""
+        _check(self._L.b3d_gpu_enumerate_grid(self.h, mesh, C.byref(grid), _ptr(rng_state),
+                                              _ptr(out), _ptr(scores)))
 
     def render_poses(self, mesh: int, poses, with_ids: bool = True):
         n = poses.shape[0]

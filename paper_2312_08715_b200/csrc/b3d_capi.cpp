@@ -771,7 +771,8 @@ KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
                   const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
                   const b3d_contact_grid* contact = nullptr, uint64_t first = 0,
-                  uint64_t grid_n = 0) {
+                  uint64_t grid_n = 0, unsigned long long* stage_rng = nullptr,
+                  KStageResult* stage_out = nullptr) {
   require_ready(ctx, true, true);
   check(scores != nullptr, "bad arguments");
   check(n > 0, "score_cells: no cells");
@@ -845,6 +846,10 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   p.zstride = lp.zstride;
   cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
              "render_score launch");
+  if (stage_out)
+    cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, stage_rng, stage_out, nullptr,
+                                   ctx->stream),
+               "stage_reduce launch");
   bool sync = host_in;
   if (!dev_scores) {
     finish_copy_out(ctx, scores, p.scores, sizeof(double) * n * nn);
@@ -1970,8 +1975,6 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     p.vcap = lp.vcap;
     p.zcap = lp.zcap;
     p.zstride = lp.zstride;
-    cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
-               "render_score launch");
     unsigned long long* d_rng = nullptr;
     const bool dev_rng = rng_state && is_device_ptr(rng_state);
     if (rng_state) {
@@ -1985,6 +1988,8 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
       }
     }
     KStageResult* d_out = ctx->result.as<KStageResult>();
+    cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
+               "render_score launch");
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
                                    ctx->stream),
                "stage_reduce launch");
@@ -2000,6 +2005,23 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     const bool all_dev = is_device_ptr(out) && (!scores || is_device_ptr(scores)) &&
                          (!rng_state || dev_rng) && !host_in;
     if (!all_dev) cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
+  });
+}
+
+b3d_status b3d_gpu_enumerate_grid(b3d_gpu_context* ctx, int32_t mesh_id,
+                                  const b3d_pose_grid* grid, uint64_t* rng_state,
+                                  b3d_stage_result* out, double* scores) {
+  return guarded([&] {
+    require_ready(ctx, true, true);
+    check(grid && out && scores, "bad arguments");
+    check(is_device_ptr(scores) && is_device_ptr(out) && (!rng_state || is_device_ptr(rng_state)),
+          "enumerate_grid: scores, out and rng_state must be device memory");
+    DeviceGuard dg(ctx->device);
+    const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
+    const uint64_t n = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
+    score_common(ctx, mesh_id, nullptr, grid, n, scores, nullptr, nullptr, 0, 0,
+                 reinterpret_cast<unsigned long long*>(rng_state),
+                 reinterpret_cast<KStageResult*>(out));
   });
 }
 

@@ -13,195 +13,23 @@
 
 #include "b3d_kernels.cuh"
 #include "posemath.cuh"
+#include "stage_common.cuh"
 
 namespace b3d200 {
 
 namespace {
 
 constexpr int kT = 1024;
-constexpr int kW = kT / 32;
-
-__device__ __forceinline__ unsigned long long rotl64(unsigned long long x, int k) {
-  return (x << k) | (x >> (64 - k));
-}
-
-// rng.cpp:30-44 (state[0] = seed, state[1..4] = s)
-__device__ double rng_uniform(unsigned long long* st) {
-  unsigned long long* s = st + 1;
-  const unsigned long long result = rotl64(s[1] * 5, 7) * 9;
-  const unsigned long long t = s[1] << 17;
-  s[2] ^= s[0];
-  s[3] ^= s[1];
-  s[1] ^= s[2];
-  s[0] ^= s[3];
-  s[2] ^= t;
-  s[3] = rotl64(s[3], 45);
-  return (double)(result >> 11) * 0x1.0p-53;
-}
-
-__device__ __forceinline__ bool better(double x, long long i, double bx, long long bi) {
-  // strict max, lowest index among equals; NaN never wins
-  return x > bx || (x == bx && i < bi);
-}
+using stage::better;
+using stage::rng_uniform;
 
 }  // namespace
 
 __global__ void __launch_bounds__(kT)
 stage_reduce_kernel(const double* __restrict__ x, long long n, int stride, int col,
                     unsigned long long* rng_state, KStageResult* out, double* probs) {
-  __shared__ double s_v[kW];
-  __shared__ long long s_i[kW];
-  __shared__ double s_sum[kW];
-  __shared__ double s_max;
-  __shared__ int s_allzero;
-  __shared__ double s_total;
-  __shared__ double s_u;
-  __shared__ int s_chunk;
-  __shared__ double s_excl[kT];
-  __shared__ unsigned int s_nonfinite;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  if (tid == 0) {
-    s_chunk = INT_MAX;
-    s_nonfinite = 0;
-  }
-
-  // max / argmax
-  double bv = -DBL_MAX * 2;  // -inf
-  long long bi = LLONG_MAX;
-  unsigned int nf = 0;
-  for (long long i = tid; i < n; i += kT) {
-    const double v = x[i * stride + col];
-    nf += !isfinite(v);
-    if (better(v, i, bv, bi)) {
-      bv = v;
-      bi = i;
-    }
-  }
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-    const long long oi = __shfl_xor_sync(0xffffffffu, bi, o);
-    if (better(ov, oi, bv, bi)) {
-      bv = ov;
-      bi = oi;
-    }
-    nf += __shfl_xor_sync(0xffffffffu, nf, o);
-  }
-  if (lane == 0) {
-    s_v[warp] = bv;
-    s_i[warp] = bi;
-    atomicAdd(&s_nonfinite, nf);
-  }
-  __syncthreads();
-  if (tid == 0) {
-    double v = s_v[0];
-    long long i = s_i[0];
-    for (int k = 1; k < kW; ++k)
-      if (better(s_v[k], s_i[k], v, i)) {
-        v = s_v[k];
-        i = s_i[k];
-      }
-    if (i == LLONG_MAX) i = 0;  // every entry NaN or -inf: index 0 (tracking.cpp:132-134)
-    s_max = v;
-    s_allzero = !isfinite(v);
-    out->argmax = (unsigned long long)i;
-    out->max_score = v;
-    out->n_nonfinite = s_nonfinite;
-  }
-  __syncthreads();
-  const double m = s_max;
-  const int all_zero = s_allzero;
-
-  // sum exp(x - max) over contiguous chunks (chunk order = index order)
-  const long long chunk = (n + kT - 1) / kT;
-  const long long c0 = (long long)tid * chunk, c1 = min(n, c0 + chunk);
-  double local = 0.0;
-  if (!all_zero) {
-    for (long long i = c0; i < c1; ++i) local += exp(x[i * stride + col] - m);
-  } else {
-    for (long long i = c0; i < c1; ++i) local += 1.0;
-  }
-  // inclusive block scan of chunk sums (warp shuffle + warp totals)
-  double incl = local;
-  for (int o = 1; o < 32; o <<= 1) {
-    const double y = __shfl_up_sync(0xffffffffu, incl, o);
-    if (lane >= o) incl += y;
-  }
-  if (lane == 31) s_sum[warp] = incl;
-  __syncthreads();
-  if (warp == 0) {
-    double wv = s_sum[lane];
-    for (int o = 1; o < 32; o <<= 1) {
-      const double y = __shfl_up_sync(0xffffffffu, wv, o);
-      if (lane >= o) wv += y;
-    }
-    s_sum[lane] = wv;  // inclusive over warps
-  }
-  __syncthreads();
-  const double warp_excl = warp ? s_sum[warp - 1] : 0.0;
-  incl += warp_excl;
-  s_excl[tid] = incl - local;
-  if (tid == kT - 1) s_total = incl;
-  __syncthreads();
-  const double total = s_total;
-  if (tid == 0) {
-    out->all_zero = all_zero;
-    out->total = total;
-    out->logsumexp = all_zero ? m : m + log(total);
-  }
-
-  // optional normalised probabilities (CellScores)
-  if (probs) {
-    for (long long i = c0; i < c1; ++i)
-      probs[i] = all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
-  }
-
-  if (!rng_state) return;
-  if (tid == 0) s_u = rng_uniform(rng_state);
-  __syncthreads();
-  const double u = s_u;
-  // first chunk whose inclusive prefix exceeds u (in probability units)
-  const double incl_p = incl / total;
-  if (u < incl_p && c0 < c1) atomicMin(&s_chunk, tid);
-  __syncthreads();
-  if (tid == 0) {
-    const double eps = 8.0 * (double)n * DBL_EPSILON;
-    long long pick = -1;
-    double margin = 0.0;
-    if (s_chunk != INT_MAX) {
-      const int t = s_chunk;
-      const long long a0 = (long long)t * chunk, a1 = min(n, a0 + chunk);
-      double acc = s_excl[t] / total;
-      double prev = acc;
-      for (long long i = a0; i < a1; ++i) {
-        const double pi = all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
-        prev = acc;
-        acc += pi;
-        if (u < acc) {
-          pick = i;
-          margin = fmin(acc - u, u - prev);
-          break;
-        }
-      }
-    }
-    unsigned int fallback = 0;
-    if (pick < 0 || !(margin > eps)) {
-      // sequential CDF exactly as inference.cpp:345-353
-      fallback = 1;
-      double acc = 0.0;
-      pick = n - 1;
-      for (long long i = 0; i < n; ++i) {
-        acc += all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
-        if (u < acc) {
-          pick = i;
-          break;
-        }
-      }
-    }
-    out->sample = (unsigned long long)pick;
-    out->sample_fallback = fallback;
-    out->sample_logp =
-        all_zero ? -log((double)n) : log(exp(x[pick * stride + col] - m) / total);
-  }
+  __shared__ stage::StageSmem<kT> sm;
+  stage::block_stage_reduce<kT>(x, n, stride, col, rng_state, out, probs, sm);
 }
 
 // n_samples categorical draws from one stage's posterior (scores already

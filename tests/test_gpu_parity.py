@@ -589,3 +589,34 @@ def test_track_camera_matches_oracle(gpu_ctx, oracle):
             s = np.array(scores)
             assert np.sort(s)[-1] - np.sort(s)[-2] <= SCORE_RTOL * abs(np.max(s))
         assert np.linalg.norm(est[f][4:] - cams[f][4:]) < 0.03
+
+
+def test_enumerate_grid_matches_score_then_reduce(gpu_ctx, oracle):
+    """b3d_gpu_enumerate_grid (one call, device buffers): same scores,
+    argmax, logsumexp, draw and Rng state as score_grid followed by
+    stage_reduce, over repeated calls."""
+    import torch
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    rot = torch.from_numpy(w.rotations).cuda()
+    grid = gpu_ctx.make_grid(w.center, w.extent, w.count, rot, w.grid_mode)
+    n = w.n_hyp
+    for rep in range(3):
+        st_f = torch.from_numpy(b3d.rng_seed(11 + rep).view(np.int64)).cuda()
+        out = torch.zeros(64, dtype=torch.uint8, device="cuda")
+        sc = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
+        gpu_ctx.enumerate_grid(mid, grid, st_f, out, sc)
+        torch.cuda.synchronize()
+        s2, _ = gpu_ctx.score_grid(mid, grid)
+        np.testing.assert_array_equal(sc.cpu().numpy(), s2)
+        st_s = b3d.rng_seed(11 + rep)
+        r2 = gpu_ctx.stage_reduce(s2[:, 0], rng_state=st_s)
+        r1 = b3d.StageResult.from_buffer_copy(out.cpu().numpy().tobytes()[:C_SIZEOF_RESULT()])
+        assert (r1.argmax, r1.sample, r1.logsumexp, r1.total) == (r2.argmax, r2.sample,
+                                                                   r2.logsumexp, r2.total)
+        np.testing.assert_array_equal(st_f.cpu().numpy().view(np.uint64), st_s)
+
+
+def C_SIZEOF_RESULT():
+    import ctypes
+    return ctypes.sizeof(b3d.StageResult)
