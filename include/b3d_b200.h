@@ -95,7 +95,7 @@ typedef struct b3d_noise {
 
 enum { B3D_PREFACTOR_PRINTED = 0, B3D_PREFACTOR_UNIFORM = 1 };
 enum { B3D_GRID_PRODUCT = 0, B3D_GRID_ZIP = 1 };
-enum { B3D_MAX_NOISE = 4 };
+enum { B3D_MAX_NOISE = 12, B3D_MAX_SIGMAS = 4 };
 
 /* 6-DoF hypothesis grid generated on the device.  Translation lattice per
  * axis: center.t - extent + 2*extent*i/(n-1) (tracking.cpp:34-35); rotation

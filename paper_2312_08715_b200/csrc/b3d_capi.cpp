@@ -542,7 +542,7 @@ void attach_base(b3d_gpu_context* ctx, KParams& p) {
   if (key != ctx->base_terms_key) {
     const int pad = p.lik.window;
     ctx->base_pad.ensure(4ull * (ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad));
-    ctx->sbase.ensure(4ull * kMaxNoise * npx);
+    ctx->sbase.ensure(4ull * kMaxSlots * npx);
     ctx->gnodes.ensure(8ull * kMaxNoise * kCheb);
     ctx->cheb.ensure(8ull * kMaxNoise * kCheb);
     cuda_check(launch_base_terms(p, p.base_keys, ctx->base_pad.as<unsigned int>(),
@@ -582,7 +582,7 @@ KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
               double sigma_max, int window, int prefactor) {
   require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
   require(n_noise <= (uint32_t)kMaxNoise, ErrorCode::invalid,
-          "gpu context: at most 4 noise settings per call");
+          "gpu context: at most 12 noise settings per call");
   require(window >= 0, ErrorCode::invalid, "window radius must be >= 0");
   require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
           ErrorCode::invalid, "unknown prefactor");
@@ -612,6 +612,8 @@ KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
     if (s == slots.size()) slots.push_back(np.sigma_noise);
     L.slot_of[e] = (int)s;
   }
+  require(slots.size() <= (size_t)kMaxSlots, ErrorCode::invalid,
+          "gpu context: at most 4 distinct sigma values per call");
   L.n_slots = (int)slots.size();
   for (size_t s = 0; s < slots.size(); ++s)
     L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));

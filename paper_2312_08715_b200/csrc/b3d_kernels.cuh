@@ -41,7 +41,8 @@ struct KGrid {
   KContact contact;
 };
 
-constexpr int kMaxNoise = 4;
+constexpr int kMaxNoise = 12;  // noise entries per call (the default noise grid has 9)
+constexpr int kMaxSlots = 4;   // distinct sigmas per call
 constexpr int kMaxInst = 16;
 constexpr int kCheb = 64;
 
@@ -50,7 +51,7 @@ struct KLik {
   int n_slots;
   int window;
   int slot_of[kMaxNoise];
-  float slot_scale[kMaxNoise];   // log2(e)/(2 sigma^2) per distinct sigma (exp2 form)
+  float slot_scale[kMaxSlots];   // log2(e)/(2 sigma^2) per distinct sigma (exp2 form)
   double one_minus_p[kMaxNoise]; // 1 - p_outlier
   double norm3[kMaxNoise];       // pow(2 pi sigma^2, -1.5)
   double floor_term[kMaxNoise];  // p_outlier / V

@@ -42,9 +42,9 @@ __global__ void sbase_kernel(const KParams p, const unsigned int* padded, int pa
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < (int)npx; i += gridDim.x * blockDim.x) {
     const int v = i / p.W, u = i % p.W;
     const float4 o = p.obs[i];
-    float S[kMaxNoise];
+    float S[kMaxSlots];
 #pragma unroll
-    for (int sl = 0; sl < kMaxNoise; ++sl) S[sl] = 0.f;
+    for (int sl = 0; sl < kMaxSlots; ++sl) S[sl] = 0.f;
     if (o.w != 0.f) window_sums_rt<false>(p, padded, rg, u, v, o, S);
     for (int sl = 0; sl < p.lik.n_slots; ++sl) sbase[(size_t)sl * npx + i] = S[sl];
   }
@@ -122,9 +122,9 @@ static auto pick_vs(bool vs) {
 // for one / several distinct sigmas -- one small kernel per launch keeps the
 // hot instruction footprint down; render kernels once.
 template <bool kIds, bool kScore, bool kOut>
-static auto pick_kernel(bool vs, int window, int n_slots, bool cam = false) {
+static auto pick_kernel(bool vs, int window, int n_noise, bool cam = false) {
   if constexpr (kScore && !kIds) {
-    const bool s1 = n_slots == 1;
+    const bool s1 = n_noise == 1;
     if (cam)  // camera mode: generic window loop
       return s1 ? pick_vs<kIds, kScore, kOut, -1, true, true>(vs)
                 : pick_vs<kIds, kScore, kOut, -1, false, true>(vs);
@@ -137,7 +137,7 @@ static auto pick_kernel(bool vs, int window, int n_slots, bool cam = false) {
     }
   } else {
     (void)window;
-    (void)n_slots;
+    (void)n_noise;
     return cam ? pick_vs<kIds, kScore, kOut, -1, false, true>(vs)
                : pick_vs<kIds, kScore, kOut, -1, false>(vs);
   }
@@ -145,7 +145,7 @@ static auto pick_kernel(bool vs, int window, int n_slots, bool cam = false) {
 
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st) {
-  auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_slots,
+  auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_noise,
                                               p.cams != nullptr);
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem);

@@ -318,9 +318,9 @@ template <bool kIds, int kW, bool kS1>
 __device__ __forceinline__ void window_sums_w(const KParams& p,
                                               const typename KeyT<kIds>::T* zb,
                                               const Region& rg, int u, int v, float4 o,
-                                              float S[kMaxNoise]) {
+                                              float S[kMaxSlots]) {
 #pragma unroll
-  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  for (int s = 0; s < kMaxSlots; ++s) S[s] = 0.f;
   const float cu0 = ((float)(u - kW) - p.fcx) * p.inv_fx;
   const float cv0 = ((float)(v - kW) - p.fcy) * p.inv_fy;
   const typename KeyT<kIds>::T* row0 = zb + (v - kW - rg.oy) * rg.rw + (u - kW - rg.ox);
@@ -338,7 +338,7 @@ __device__ __forceinline__ void window_sums_w(const KParams& p,
       const float dz = o.z - z;
       const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
 #pragma unroll
-      for (int s = 0; s < (kS1 ? 1 : kMaxNoise); ++s)
+      for (int s = 0; s < (kS1 ? 1 : kMaxSlots); ++s)
         if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
     }
   }
@@ -348,9 +348,9 @@ template <bool kIds, bool kS1>
 __device__ __forceinline__ void window_sums_any(const KParams& p,
                                                 const typename KeyT<kIds>::T* zb,
                                                 const Region& rg, int u, int v, float4 o,
-                                                float S[kMaxNoise]) {
+                                                float S[kMaxSlots]) {
 #pragma unroll
-  for (int s = 0; s < kMaxNoise; ++s) S[s] = 0.f;
+  for (int s = 0; s < kMaxSlots; ++s) S[s] = 0.f;
   const int w = p.lik.window;
   for (int rv = v - w; rv <= v + w; ++rv) {
     const float cv = ((float)rv - p.fcy) * p.inv_fy;
@@ -364,7 +364,7 @@ __device__ __forceinline__ void window_sums_any(const KParams& p,
       const float dz = o.z - z;
       const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
 #pragma unroll
-      for (int s = 0; s < (kS1 ? 1 : kMaxNoise); ++s)
+      for (int s = 0; s < (kS1 ? 1 : kMaxSlots); ++s)
         if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
     }
   }
@@ -376,7 +376,7 @@ __device__ __forceinline__ void window_sums_any(const KParams& p,
 template <bool kIds, int kWin, bool kS1>
 __device__ __forceinline__ void window_sums(const KParams& p, const typename KeyT<kIds>::T* zb,
                                             const Region& rg, int u, int v, float4 o,
-                                            float S[kMaxNoise]) {
+                                            float S[kMaxSlots]) {
   if constexpr (kWin >= 0)
     window_sums_w<kIds, kWin, kS1>(p, zb, rg, u, v, o, S);
   else
@@ -386,7 +386,7 @@ __device__ __forceinline__ void window_sums(const KParams& p, const typename Key
 template <bool kIds>
 __device__ __forceinline__ void window_sums_rt(const KParams& p, const typename KeyT<kIds>::T* zb,
                                                const Region& rg, int u, int v, float4 o,
-                                               float S[kMaxNoise]) {
+                                               float S[kMaxSlots]) {
   switch (p.lik.window) {
     case 0: window_sums_w<kIds, 0, false>(p, zb, rg, u, v, o, S); break;
     case 1: window_sums_w<kIds, 1, false>(p, zb, rg, u, v, o, S); break;
@@ -865,9 +865,11 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     if (tid < p.lik.n_noise)  // likelihood.cpp:167 coefficient order
       s_coef[tid] = empty_render ? 0.0 : p.lik.one_minus_p[tid] / (double)rend_count * p.lik.norm3[tid];
     __syncthreads();
-    float coef_f[kMaxNoise], floor_f[kMaxNoise];
+    // kS1 kernels: exactly one noise entry (and sigma); else up to kMaxNoise
+    constexpr int kNN = kS1 ? 1 : kMaxNoise;
+    float coef_f[kNN], floor_f[kNN];
 #pragma unroll
-    for (int e = 0; e < kMaxNoise; ++e) {
+    for (int e = 0; e < kNN; ++e) {
       coef_f[e] = e < p.lik.n_noise ? (float)s_coef[e] : 0.f;
       floor_f[e] = e < p.lik.n_noise ? (float)p.lik.floor_term[e] : 0.f;
     }
@@ -882,10 +884,10 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
     const int dw = du1 - du0 + 1;
     const int dpx = (hc.empty_region || empty_render) ? 0 : dw * (dv1 - dv0 + 1);
-    double acc[kMaxNoise];
-    int npos[kMaxNoise];
+    double acc[kNN];
+    int npos[kNN];
 #pragma unroll
-    for (int e = 0; e < kMaxNoise; ++e) {
+    for (int e = 0; e < kNN; ++e) {
       acc[e] = 0.0;
       npos[e] = 0;
     }
@@ -894,12 +896,12 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       const int pu = du0 + (i - (pv - dv0) * dw);
       const float4 o = __ldg(p.obs + (size_t)pv * p.W + pu);
       if (o.w == 0.f) continue;
-      float S[kMaxNoise];
+      float S[kMaxSlots];
       window_sums<kIds, kWin, kS1>(p, zb, rg, pu, pv, o, S);
       if (p.base_keys) {
         // g(S) - g(S_base): the pixel's term relative to the base-only sum G
 #pragma unroll
-        for (int e = 0; e < kMaxNoise; ++e) {
+        for (int e = 0; e < kNN; ++e) {
           if (e < p.lik.n_noise) {
             const int sl = p.lik.slot_of[e];
             const float Sb = __ldg(p.sbase + (size_t)sl * p.W * p.H + (size_t)pv * p.W + pu);
@@ -910,7 +912,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         }
       } else {
 #pragma unroll
-        for (int e = 0; e < kMaxNoise; ++e) {
+        for (int e = 0; e < kNN; ++e) {
           if (e < p.lik.n_noise) {
             const float Se = S[p.lik.slot_of[e]];
             if (Se > 0.f) {
@@ -923,13 +925,13 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     }
     // ---- D3: fp64 block reduction -> one score per noise entry
 #pragma unroll
-    for (int e = 0; e < kMaxNoise; ++e) {
+    for (int e = 0; e < kNN; ++e) {
       acc[e] = warp_sum(acc[e]);
       npos[e] = warp_sum_i(npos[e]);
     }
     if (lane == 0) {
 #pragma unroll
-      for (int e = 0; e < kMaxNoise; ++e) {
+      for (int e = 0; e < kNN; ++e) {
         s_red[warp][e] = acc[e];
         s_redi[warp][e] = npos[e];
       }

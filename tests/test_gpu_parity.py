@@ -620,3 +620,20 @@ def test_enumerate_grid_matches_score_then_reduce(gpu_ctx, oracle):
 def C_SIZEOF_RESULT():
     import ctypes
     return ctypes.sizeof(b3d.StageResult)
+
+
+def test_score_parity_default_noise_grid(gpu_ctx, oracle):
+    """default_noise_grid (inference.cpp:127-133): 9 noise entries over 3
+    distinct sigmas in one call, against the oracle."""
+    w = cfg1_oracle(seed=4)
+    smax = 0.1
+    noise = [(p, f * smax) for p in (0.05, 0.3, 0.8) for f in (0.25, 0.5, 1.0)]
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    gpu_ctx.set_likelihood(noise, smax, 1)
+    poses = w.grid_poses()[::16]
+    s_gpu, _ = gpu_ctx.score_poses(mid, poses)
+    s_orc, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, noise, smax, 1)
+    assert s_gpu.shape == (poses.shape[0], 9)
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
