@@ -211,6 +211,20 @@ B3D_API b3d_status b3d_gpu_score_contact_grid(b3d_gpu_context* ctx, int32_t mesh
 /* Host poses (model-to-world) of a contact grid, n_dx * n_dy * n_dtheta of them. */
 B3D_API b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out);
 
+/* subdivide_cell (inference.cpp:240-259): the n_dx x n_dy x n_dtheta children
+ * of a parent contact cell, child (ix, iy, it) spanning
+ * [lo + (hi - lo) ix / n, lo + (hi - lo) (ix + 1) / n) per dimension; each is
+ * scored at its centre (cell_center_child, inference.cpp:126-137).  The
+ * contact grid above is the stage-0 parent [0, table - footprint] x [0, 2 pi). */
+typedef struct b3d_contact_cells {
+  b3d_contact_grid grid; /* table, object bounds, face, child counts */
+  double dx_lo, dx_hi, dy_lo, dy_hi, dtheta_lo, dtheta_hi;
+} b3d_contact_cells;
+B3D_API b3d_status b3d_gpu_score_contact_cells(b3d_gpu_context* ctx, int32_t mesh_id,
+                                               const b3d_contact_cells* cells, double* scores,
+                                               uint8_t* status);
+B3D_API b3d_status b3d_contact_cells_poses(const b3d_contact_cells* cells, b3d_pose* out);
+
 /* One stage of a device-resident enumeration schedule: a pose grid around
  * the previous stage's chosen pose (the caller's centre for stage 0), its
  * likelihood settings (sigma_max and prefactor come from the context), and
@@ -317,11 +331,62 @@ B3D_API b3d_status b3d_box_mesh(const double lo[3], const double hi[3], double v
 B3D_API b3d_status b3d_contact_to_pose(double table_w, double table_h, const double aabb_min[3],
                                        const double aabb_max[3], int32_t face, double dx,
                                        double dy, double dtheta, b3d_pose* out);
+/* rotated_bounds (scene_graph.cpp:73-89): AABB of the object with `face` down. */
+B3D_API b3d_status b3d_rotated_bounds(const double aabb_min[3], const double aabb_max[3],
+                                      int32_t face, double lo[3], double hi[3]);
 /* generative.cpp:35-59 / 61-85 on the host (exposed for tests and callers). */
 B3D_API b3d_status b3d_camera_pose_from_spherical(double distance, double azimuth,
                                                   double altitude, b3d_pose* out);
 B3D_API int b3d_camera_pose_to_spherical(const b3d_pose* pose, double tol, double* distance,
                                          double* azimuth, double* altitude);
+
+/* ---- sequential Monte Carlo over scene graphs (run_smc, inference.cpp:398-520) ----
+ * Library object: an uploaded mesh and its model-frame AABB (mesh_bounds). */
+typedef struct b3d_smc_object {
+  int32_t mesh_id;
+  int32_t reserved;
+  double aabb_min[3], aabb_max[3];
+} b3d_smc_object;
+/* ScheduleStage (inference.hpp:22-28) */
+typedef struct b3d_schedule_stage {
+  uint32_t n_dx, n_dy, n_dtheta;
+} b3d_schedule_stage;
+/* InferenceContext pieces (inference.hpp:58-72): table (top plane at z = 0,
+ * rendered first, identity pose), schedule, noise grid, model settings. */
+typedef struct b3d_smc_config {
+  double table_w, table_h;
+  int32_t table_mesh;
+  uint32_t n_refine; /* <= 4 */
+  b3d_schedule_stage stage0;
+  b3d_schedule_stage refine[4];
+  const b3d_noise* noise_grid;
+  uint32_t n_noise_grid; /* <= B3D_MAX_NOISE, <= B3D_MAX_SIGMAS distinct sigmas */
+  uint32_t n_objects;    /* objects placed, 1..B3D_SMC_MAX_CHILDREN */
+  uint32_t n_particles;
+  double resample_threshold;
+  double sigma_max;
+  int32_t window;
+  int32_t prefactor;
+} b3d_smc_config;
+enum { B3D_SMC_MAX_CHILDREN = 8 };
+typedef struct b3d_smc_child {
+  int32_t object_id, face;
+  double dx, dy, dtheta; /* ContactParams */
+} b3d_smc_child;
+typedef struct b3d_smc_particle {
+  b3d_smc_child children[8];
+  int32_t n_children, noise_index;
+  double log_target, log_weight;
+} b3d_smc_particle;
+/* run_smc: smc_init, smc_extend per further object, ESS-triggered systematic
+ * resampling, log-evidence; the reference's Rng streams (rng.split(1, i),
+ * rng.split(arity + 1, i), rng.split(0x5e5a, 0).split(stage)).  Every
+ * render+score runs on the device (stage 0 per (object, face) with the whole
+ * noise grid, refinement batched across particles).  Uses the context's
+ * camera and observation; replaces its likelihood settings and base scene. */
+B3D_API b3d_status b3d_gpu_run_smc(b3d_gpu_context* ctx, const b3d_smc_object* library,
+                                   uint32_t n_library, const b3d_smc_config* cfg, uint64_t seed,
+                                   b3d_smc_particle* particles, double* log_evidence);
 
 /* Reference Rng seeding (rng.cpp:20-28), for building rng_state. */
 B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);

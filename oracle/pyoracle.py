@@ -456,3 +456,243 @@ def track_camera(frames, k, instances, initial, noise, sigma_max, window,
         top = beam[0][0]
         poses.append(camera_pose_from_spherical(*top))
     return np.array(poses)
+
+
+# ---------------------------------------------------------------- SMC
+_TWO_PI_C = 6.283185307179586476925287
+
+
+class _Rng:
+    """rng.cpp through the pinned golden-vector restatement (rng_seed/split/uniform)."""
+
+    def __init__(self, st):
+        self.st = st
+
+    @classmethod
+    def seed(cls, s):
+        return cls(rng_seed(s))
+
+    def split(self, k0, k1=0, k2=0):
+        return _Rng(rng_split(self.st, k0, k1, k2))
+
+    def uniform(self, lo=None, hi=None):
+        u = rng_uniform(self.st)
+        return u if lo is None else lo + (hi - lo) * u
+
+
+def run_smc(k, camera, observed, library, table, schedule, noise_grid, sigma_max, window,
+            n_objects, n_particles, resample_threshold, seed, prefactor=0):
+    """run_smc (inference.cpp:398-520) restated over this oracle's render and
+    windowed likelihood.  library: [(verts, tris, aabb_min, aabb_max)];
+    table: (verts, tris, width, height); schedule: (stage0 (nx, ny, nt),
+    [refine (nx, ny, nt), ...]).  Returns (particles, log_evidence) with
+    particles = [(children [(obj, face, dx, dy, dtheta)], noise_index,
+    log_target, log_weight)]."""
+    import math
+    tv, tt, tw, th = table
+    L = len(library)
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+
+    def footprint(obj, face):
+        lo, hi = rotated_bounds(library[obj][2], library[obj][3], face)
+        return hi[0] - lo[0], hi[1] - lo[1]
+
+    def child_prior(c):  # inference.cpp:26-38
+        obj, face, dx, dy, dt = c
+        fx, fy = footprint(obj, face)
+        dxr, dyr = tw - fx, th - fy
+        if dxr <= 0 or dyr <= 0:
+            return -np.inf
+        if dx < 0 or dx > dxr or dy < 0 or dy > dyr or dt < 0 or dt >= _TWO_PI_C:
+            return -np.inf
+        return (-math.log(float(L)) - math.log(6.0) - math.log(dxr) - math.log(dyr)
+                - math.log(_TWO_PI_C))
+
+    def prior_sum(cs):
+        total = 0.0
+        for c in cs:
+            lp = child_prior(c)
+            if not np.isfinite(lp):
+                return -np.inf
+            total += lp
+        return total
+
+    def pose_of(c):
+        obj, face, dx, dy, dt = c
+        return contact_to_pose(tw, th, library[obj][2], library[obj][3], face, dx, dy, dt)
+
+    def base_depth(partial):  # render_partial
+        inst = [(tv, tt, ident)] + [(library[c[0]][0], library[c[0]][1], pose_of(c))
+                                    for c in partial]
+        return render(k, inst, camera=camera)
+
+    def score(obj, poses, noise, base):
+        s, st = score_poses(k, observed, library[obj][0], library[obj][1], np.asarray(poses),
+                            noise, sigma_max, window, prefactor, base_depth=base, camera=camera)
+        s = s.copy()
+        s[st != 0] = -np.inf
+        return s
+
+    def normalise(lt):  # inference.cpp:315-330
+        m = max(lt)
+        if not np.isfinite(m):
+            return [1.0 / len(lt)] * len(lt), True
+        sc = [math.exp(x - m) for x in lt]
+        tot = 0.0
+        for x in sc:
+            tot += x
+        return [x / tot for x in sc], False
+
+    def sample(probs, rng):  # inference.cpp:345-353
+        u = rng.uniform()
+        acc = 0.0
+        for i, p in enumerate(probs):
+            acc += p
+            if u < acc:
+                return i
+        return len(probs) - 1
+
+    def center(iv):
+        return 0.5 * (iv[0] + iv[1])
+
+    def build_stage0(partial):
+        nx, ny, nt = schedule[0]
+        bp = prior_sum(partial)
+        base = base_depth(partial)
+        cells, lt = [], []
+        for obj in range(L):
+            for face in range(1, 7):
+                fx, fy = footprint(obj, face)
+                dxr, dyr = tw - fx, th - fy
+                if dxr <= 0 or dyr <= 0:
+                    continue
+                grp = []
+                for ix in range(nx):
+                    for iy in range(ny):
+                        for it in range(nt):
+                            grp.append((obj, face, (dxr * ix / nx, dxr * (ix + 1) / nx),
+                                        (dyr * iy / ny, dyr * (iy + 1) / ny),
+                                        (_TWO_PI_C * it / nt, _TWO_PI_C * (it + 1) / nt)))
+                poses = [pose_of((c[0], c[1], center(c[2]), center(c[3]), center(c[4])))
+                         for c in grp]
+                s = score(obj, poses, noise_grid, base)
+                for ci, c in enumerate(grp):
+                    cp = child_prior((c[0], c[1], center(c[2]), center(c[3]), center(c[4])))
+                    for e in range(len(noise_grid)):
+                        cells.append(c + (e,))
+                        l = s[ci, e]
+                        lt.append(bp + cp + l if np.isfinite(bp) and np.isfinite(cp)
+                                  and np.isfinite(l) else -np.inf)
+        probs, az = normalise(lt)
+        return cells, probs, az
+
+    def subdivide(c, st):
+        nx, ny, nt = st
+        obj, face, dx, dy, dt, e = c
+        out = []
+        for ix in range(nx):
+            for iy in range(ny):
+                for it in range(nt):
+                    w0, w1, w2 = dx[1] - dx[0], dy[1] - dy[0], dt[1] - dt[0]
+                    out.append((obj, face, (dx[0] + w0 * ix / nx, dx[0] + w0 * (ix + 1) / nx),
+                                (dy[0] + w1 * iy / ny, dy[0] + w1 * (iy + 1) / ny),
+                                (dt[0] + w2 * it / nt, dt[0] + w2 * (it + 1) / nt), e))
+        return out
+
+    def propose(partial, rng, stage0=None):  # inference.cpp:357-396
+        cells, probs, _ = stage0 if stage0 is not None else build_stage0(partial)
+        pick0 = sample(probs, rng)
+        log_q = math.log(probs[pick0])
+        cur = cells[pick0]
+        for st in schedule[1]:
+            ch = subdivide(cur, st)
+            if len(ch) == 1:
+                cur = ch[0]
+                continue
+            bp = prior_sum(partial)
+            base = base_depth(partial)
+            poses = [pose_of((c[0], c[1], center(c[2]), center(c[3]), center(c[4]))) for c in ch]
+            s = score(cur[0], poses, [noise_grid[cur[5]]], base)
+            lt = []
+            for ci, c in enumerate(ch):
+                cp = child_prior((c[0], c[1], center(c[2]), center(c[3]), center(c[4])))
+                l = s[ci, 0]
+                lt.append(bp + cp + l if np.isfinite(bp) and np.isfinite(cp) and np.isfinite(l)
+                          else -np.inf)
+            sc, _ = normalise(lt)
+            pick = sample(sc, rng)
+            log_q += math.log(sc[pick])
+            cur = ch[pick]
+        obj, face, dx, dy, dt, e = cur
+        child = (obj, face, rng.uniform(dx[0], dx[1]), rng.uniform(dy[0], dy[1]),
+                 rng.uniform(dt[0], dt[1]))
+        vol = (dx[1] - dx[0]) * (dy[1] - dy[0]) * (dt[1] - dt[0])
+        log_q += -math.log(vol)
+        return child, e, log_q
+
+    def target(children, e):  # scene_target_logpdf
+        prior = prior_sum(children)
+        if not np.isfinite(prior):
+            return -np.inf
+        s = score(children[-1][0], [pose_of(children[-1])], [noise_grid[e]],
+                  base_depth(children[:-1]))
+        return prior + s[0, 0] if np.isfinite(s[0, 0]) else -np.inf
+
+    def lse(xs):
+        m = max(xs)
+        if not np.isfinite(m):
+            return -np.inf
+        acc = 0.0
+        for x in xs:
+            acc += math.exp(x - m)
+        return m + math.log(acc)
+
+    def weights(ps):
+        lw = [p[3] for p in ps]
+        l = lse(lw)
+        return [math.exp(x - l) for x in lw]
+
+    def resample(ps, rng):
+        w = weights(ps)
+        log_total = lse([p[3] for p in ps])
+        n = len(ps)
+        u = rng.uniform()
+        out, cum, src = [], 0.0, 0
+        for i in range(n):
+            pos = (float(i) + u) / float(n)
+            while src + 1 < n and cum + w[src] <= pos:
+                cum += w[src]
+                src += 1
+            out.append(ps[src])
+        reset = log_total - math.log(float(n))
+        return [(p[0], p[1], p[2], reset) for p in out]
+
+    rng = _Rng.seed(seed)
+    s0 = build_stage0([])
+    if s0[2]:
+        raise ValueError("smc_init: all-zero scores at stage 0")
+    ps = []
+    for i in range(n_particles):
+        child, e, log_q = propose([], rng.split(1, i), s0)
+        lt = target([child], e)
+        ps.append(([child], e, lt, lt - log_q))
+    rs = rng.split(0x5e5a, 0)
+
+    def maybe_resample(ps, stage):
+        w = weights(ps)
+        ess = 1.0 / sum(x * x for x in w)
+        if ess < resample_threshold * n_particles:
+            return resample(ps, rs.split(stage))
+        return ps
+
+    ps = maybe_resample(ps, 1)
+    for kk in range(2, n_objects + 1):
+        key = len(ps[0][0]) + 1
+        nps = []
+        for i, (ch, e0, lt0, lw) in enumerate(ps):
+            child, e, log_q = propose(ch, rng.split(key, i))
+            lt = target(ch + [child], e)
+            nps.append((ch + [child], e, lt, lw + lt - lt0 - log_q))
+        ps = maybe_resample(nps, kk)
+    log_ev = lse([p[3] for p in ps]) - math.log(float(n_particles))
+    return ps, log_ev

@@ -100,6 +100,35 @@ class TrackSearch(C.Structure):
         return cls(**d)
 
 
+class SmcObject(C.Structure):
+    _fields_ = [("mesh_id", C.c_int32), ("reserved", C.c_int32),
+                ("aabb_min", C.c_double * 3), ("aabb_max", C.c_double * 3)]
+
+
+class ScheduleStage(C.Structure):
+    _fields_ = [("n_dx", C.c_uint32), ("n_dy", C.c_uint32), ("n_dtheta", C.c_uint32)]
+
+
+class SmcConfig(C.Structure):
+    _fields_ = [("table_w", C.c_double), ("table_h", C.c_double), ("table_mesh", C.c_int32),
+                ("n_refine", C.c_uint32), ("stage0", ScheduleStage),
+                ("refine", ScheduleStage * 4), ("noise_grid", C.c_void_p),
+                ("n_noise_grid", C.c_uint32), ("n_objects", C.c_uint32),
+                ("n_particles", C.c_uint32), ("resample_threshold", C.c_double),
+                ("sigma_max", C.c_double), ("window", C.c_int32), ("prefactor", C.c_int32)]
+
+
+class SmcChild(C.Structure):
+    _fields_ = [("object_id", C.c_int32), ("face", C.c_int32), ("dx", C.c_double),
+                ("dy", C.c_double), ("dtheta", C.c_double)]
+
+
+class SmcParticle(C.Structure):
+    _fields_ = [("children", SmcChild * 8), ("n_children", C.c_int32),
+                ("noise_index", C.c_int32), ("log_target", C.c_double),
+                ("log_weight", C.c_double)]
+
+
 class StageResult(C.Structure):
     _fields_ = [("argmax", C.c_uint64), ("sample", C.c_uint64), ("max_score", C.c_double),
                 ("logsumexp", C.c_double), ("total", C.c_double), ("sample_logp", C.c_double),
@@ -144,6 +173,10 @@ def lib() -> C.CDLL:
                                  st),
         "b3d_camera_pose_from_spherical": ([dbl, dbl, dbl, C.POINTER(Pose)], st),
         "b3d_box_mesh": ([vp, vp, vp, vp], st),
+        "b3d_rotated_bounds": ([vp, vp, i32, vp, vp], st),
+        "b3d_gpu_score_contact_cells": ([vp, i32, vp, vp, vp], st),
+        "b3d_contact_cells_poses": ([vp, vp], st),
+        "b3d_gpu_run_smc": ([vp, vp, u32, C.POINTER(SmcConfig), u64, vp, C.POINTER(dbl)], st),
         "b3d_contact_to_pose": ([dbl, dbl, vp, vp, i32, dbl, dbl, dbl, C.POINTER(Pose)], st),
         "b3d_camera_pose_to_spherical": ([C.POINTER(Pose), dbl, C.POINTER(dbl), C.POINTER(dbl),
                                           C.POINTER(dbl)], C.c_int),
@@ -517,6 +550,42 @@ class GpuContext:
         _check(self._L.b3d_gpu_track_camera(self.h, _ptr(fr), n, C.byref(_pose(initial)),
                                             C.byref(search), poses.ctypes.data, ms.ctypes.data))
         return poses, ms
+
+    def run_smc(self, library, table_mesh: int, table_w: float, table_h: float, schedule,
+                noise_grid, sigma_max: float, window: int, n_objects: int, n_particles: int,
+                resample_threshold: float, seed: int, prefactor: int = PREFACTOR_PRINTED):
+        """run_smc (inference.cpp:398-520) with device scoring (b3d_gpu_run_smc).
+        library: [(mesh_id, aabb_min, aabb_max)]; schedule: (stage0 (nx, ny, nt),
+        [refine ...]).  Returns ([(children [(obj, face, dx, dy, dtheta)],
+        noise_index, log_target, log_weight)], log_evidence)."""
+        libs = (SmcObject * len(library))()
+        for i, (mid, lo, hi) in enumerate(library):
+            libs[i].mesh_id = mid
+            for a in range(3):
+                libs[i].aabb_min[a] = float(lo[a])
+                libs[i].aabb_max[a] = float(hi[a])
+        nz = (Noise * len(noise_grid))(*[Noise(p, s) for p, s in noise_grid])
+        cfg = SmcConfig()
+        cfg.table_w, cfg.table_h, cfg.table_mesh = table_w, table_h, table_mesh
+        cfg.stage0 = ScheduleStage(*schedule[0])
+        cfg.n_refine = len(schedule[1])
+        for r, st in enumerate(schedule[1]):
+            cfg.refine[r] = ScheduleStage(*st)
+        cfg.noise_grid = C.cast(nz, C.c_void_p)
+        cfg.n_noise_grid = len(noise_grid)
+        cfg.n_objects, cfg.n_particles = n_objects, n_particles
+        cfg.resample_threshold, cfg.sigma_max = resample_threshold, sigma_max
+        cfg.window, cfg.prefactor = window, prefactor
+        out = (SmcParticle * n_particles)()
+        le = C.c_double()
+        _check(self._L.b3d_gpu_run_smc(self.h, libs, len(library), C.byref(cfg), seed, out,
+                                       C.byref(le)))
+        ps = []
+        for p in out:
+            ch = [(c.object_id, c.face, c.dx, c.dy, c.dtheta)
+                  for c in list(p.children)[:p.n_children]]
+            ps.append((ch, p.noise_index, p.log_target, p.log_weight))
+        return ps, le.value
 
     def set_base_scene(self, mesh_ids: Sequence[int], poses):
         """Fixed instances (table first, then base children) rendered once and

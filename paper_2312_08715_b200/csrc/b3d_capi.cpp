@@ -737,9 +737,12 @@ KPose contact_to_pose_host(double table_w, double table_h, const double amin[3],
   return KPose{q.w, q.x, q.y, q.z, r[0] + pivot[0], r[1] + pivot[1], r[2] + pivot[2]};
 }
 
-// KGrid (mode 2) for a contact grid: face rotation, footprint and the
-// per-cell spin cos/sin computed here with libm; the rest runs on device.
-KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
+// KGrid (mode 2) for the children of a contact cell (subdivide_cell): face
+// rotation, footprint and the per-cell spin cos/sin computed here with
+// libm; the rest runs on device.  cells.grid alone (stage 0) is the parent
+// [0, table - footprint] x [0, 2 pi).
+KGrid make_contact_cells(const b3d_contact_cells& cells, std::vector<double>& spin) {
+  const b3d_contact_grid& g = cells.grid;
   check(g.face >= 1 && g.face <= 6, "face must be in 1..6");
   check(g.count[0] >= 1 && g.count[1] >= 1 && g.count[2] >= 1,
         "schedule stage: subdivision counts must be >= 1");
@@ -755,13 +758,15 @@ KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
   c.h = hi[1] - lo[1];
   c.table_w = g.table_w;
   c.table_h = g.table_h;
-  c.dx_range = g.table_w - c.w;
-  c.dy_range = g.table_h - c.h;
-  require(c.dx_range > 0 && c.dy_range > 0, ErrorCode::numeric,
-          "stage 0: empty proposal support (no object fits the table)");
+  c.dx_lo = cells.dx_lo;
+  c.dx_w = cells.dx_hi - cells.dx_lo;
+  c.dy_lo = cells.dy_lo;
+  c.dy_w = cells.dy_hi - cells.dy_lo;
   spin.resize(2 * g.count[2]);
+  const double tw = cells.dtheta_hi - cells.dtheta_lo;
   for (uint32_t it = 0; it < g.count[2]; ++it) {
-    const double dlo = kTwoPiD * it / g.count[2], dhi = kTwoPiD * (it + 1) / g.count[2];
+    const double dlo = cells.dtheta_lo + tw * it / g.count[2];
+    const double dhi = cells.dtheta_lo + tw * (it + 1) / g.count[2];
     const double dtheta = 0.5 * (dlo + dhi);
     const double ha = 0.5 * dtheta;
     spin[2 * it] = std::cos(ha);
@@ -770,9 +775,47 @@ KGrid make_contact_grid(const b3d_contact_grid& g, std::vector<double>& spin) {
   return k;
 }
 
+// stage 0 of one (object, face): the full contact support as parent cell
+b3d_contact_cells stage0_parent(const b3d_contact_grid& g) {
+  check(g.face >= 1 && g.face <= 6, "face must be in 1..6");
+  double lo[3], hi[3];
+  rotated_bounds(g.aabb_min, g.aabb_max, g.face, lo, hi);
+  b3d_contact_cells cells{};
+  cells.grid = g;
+  cells.dx_lo = 0.0;
+  cells.dx_hi = g.table_w - (hi[0] - lo[0]);
+  cells.dy_lo = 0.0;
+  cells.dy_hi = g.table_h - (hi[1] - lo[1]);
+  cells.dtheta_lo = 0.0;
+  cells.dtheta_hi = kTwoPiD;
+  require(cells.dx_hi > 0 && cells.dy_hi > 0, ErrorCode::numeric,
+          "stage 0: empty proposal support (no object fits the table)");
+  return cells;
+}
+
+// Host pose of child (ix, iy, it): the operations of posemath.cuh contact_pose.
+b3d_pose contact_cell_pose(const KGrid& g, const std::vector<double>& spin, uint32_t ix,
+                           uint32_t iy, uint32_t it) {
+  const KContact& c = g.contact;
+  const uint32_t nx = g.count[0], ny = g.count[1];
+  const double dx = 0.5 * ((c.dx_lo + c.dx_w * ix / nx) + (c.dx_lo + c.dx_w * (ix + 1) / nx));
+  const double dy = 0.5 * ((c.dy_lo + c.dy_w * iy / ny) + (c.dy_lo + c.dy_w * (iy + 1) / ny));
+  const HQ spin_q{spin[2 * it], spin[2 * it + 1] * 0.0, spin[2 * it + 1] * 0.0,
+                  spin[2 * it + 1] * 1.0};
+  const double cx = -c.table_w / 2, cy = -c.table_h / 2, cz = 0.0;
+  const double bt[3] = {cx + (dx - c.lo[0]), cy + (dy - c.lo[1]), cz + -c.lo[2]};
+  const double pv[3] = {cx + (dx + c.w / 2), cy + (dy + c.h / 2), cz + 0.0};
+  const HQ q = hq_normalized(
+      hq_mul(spin_q, HQ{c.face_q[0], c.face_q[1], c.face_q[2], c.face_q[3]}));
+  const double rel[3] = {bt[0] - pv[0], bt[1] - pv[1], bt[2] - pv[2]};
+  double r[3];
+  hq_rotate(spin_q, rel, r);
+  return b3d_pose{q.w, q.x, q.y, q.z, r[0] + pv[0], r[1] + pv[1], r[2] + pv[2]};
+}
+
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
                   const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
-                  const b3d_contact_grid* contact = nullptr, uint64_t first = 0,
+                  const b3d_contact_cells* contact = nullptr, uint64_t first = 0,
                   uint64_t grid_n = 0, unsigned long long* stage_rng = nullptr,
                   KStageResult* stage_out = nullptr) {
   require_ready(ctx, true, true);
@@ -788,9 +831,9 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   } else if (contact) {
     std::vector<double> spin;
     p.poses = nullptr;
-    p.grid = make_contact_grid(*contact, spin);
-    check((uint64_t)contact->count[0] * contact->count[1] * contact->count[2] == n,
-          "contact grid: n does not match the grid size");
+    p.grid = make_contact_cells(*contact, spin);
+    const uint32_t* cnt = contact->grid.count;
+    check((uint64_t)cnt[0] * cnt[1] * cnt[2] == n, "contact grid: n does not match the grid size");
     ctx->spin.ensure(8 * spin.size());
     cuda_check(cudaMemcpyAsync(ctx->spin.p, spin.data(), 8 * spin.size(), cudaMemcpyHostToDevice,
                                ctx->stream),
@@ -1005,6 +1048,9 @@ void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, 
              "render_score launch (cameras)");
 }
 }  // namespace
+
+// the thread-local error channel, shared with smc.cpp (not exported)
+void b3d200_set_last_error(const char* msg) { g_last_error = msg; }
 
 // =================================================================== C ABI
 extern "C" {
@@ -1321,6 +1367,15 @@ b3d_status b3d_gpu_render_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d
       sync = true;
     }
     if (sync) cuda_check(cudaStreamSynchronize(ctx->stream), "render_poses");
+  });
+}
+
+b3d_status b3d_rotated_bounds(const double aabb_min[3], const double aabb_max[3], int32_t face,
+                              double lo[3], double hi[3]) {
+  return guarded([&] {
+    check(aabb_min && aabb_max && lo && hi, "bad arguments");
+    check(face >= 1 && face <= 6, "face must be in 1..6");
+    rotated_bounds(aabb_min, aabb_max, face, lo, hi);
   });
 }
 
@@ -1895,61 +1950,46 @@ b3d_status b3d_gpu_score_contact_grid(b3d_gpu_context* ctx, int32_t mesh_id,
                                       uint8_t* status) {
   return guarded([&] {
     check(grid != nullptr, "bad arguments");
+    const b3d_contact_cells cells = stage0_parent(*grid);
     const uint64_t n = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
-    score_common(ctx, mesh_id, nullptr, nullptr, n, scores, status, grid);
+    score_common(ctx, mesh_id, nullptr, nullptr, n, scores, status, &cells);
   });
 }
+
+b3d_status b3d_gpu_score_contact_cells(b3d_gpu_context* ctx, int32_t mesh_id,
+                                       const b3d_contact_cells* cells, double* scores,
+                                       uint8_t* status) {
+  return guarded([&] {
+    check(cells != nullptr, "bad arguments");
+    const uint64_t n =
+        (uint64_t)cells->grid.count[0] * cells->grid.count[1] * cells->grid.count[2];
+    score_common(ctx, mesh_id, nullptr, nullptr, n, scores, status, cells);
+  });
+}
+
+namespace {
+void cells_poses(const b3d_contact_cells& cells, b3d_pose* out) {
+  std::vector<double> spin;
+  const KGrid g = make_contact_cells(cells, spin);
+  const uint32_t nx = g.count[0], ny = g.count[1], nt = g.count[2];
+  for (uint32_t ix = 0; ix < nx; ++ix)
+    for (uint32_t iy = 0; iy < ny; ++iy)
+      for (uint32_t it = 0; it < nt; ++it)
+        out[((size_t)ix * ny + iy) * nt + it] = contact_cell_pose(g, spin, ix, iy, it);
+}
+}  // namespace
 
 b3d_status b3d_contact_grid_poses(const b3d_contact_grid* grid, b3d_pose* out) {
   return guarded([&] {
     check(grid && out, "bad arguments");
-    std::vector<double> spin;
-    const KGrid g = make_contact_grid(*grid, spin);
-    const KContact& c = g.contact;
-    const uint32_t nx = grid->count[0], ny = grid->count[1], nt = grid->count[2];
-    for (uint32_t ix = 0; ix < nx; ++ix)
-      for (uint32_t iy = 0; iy < ny; ++iy)
-        for (uint32_t it = 0; it < nt; ++it) {
-          // same operations as posemath.cuh contact_pose
-          const double dx = 0.5 * (c.dx_range * ix / nx + c.dx_range * (ix + 1) / nx);
-          const double dy = 0.5 * (c.dy_range * iy / ny + c.dy_range * (iy + 1) / ny);
-          const double cs = spin[2 * it], sn = spin[2 * it + 1];
-          const double sq[4] = {cs, sn * 0.0, sn * 0.0, sn * 1.0};
-          const double cx = -c.table_w / 2, cy = -c.table_h / 2, cz = 0.0;
-          const double bt[3] = {cx + (dx - c.lo[0]), cy + (dy - c.lo[1]), cz + -c.lo[2]};
-          const double pv[3] = {cx + (dx + c.w / 2), cy + (dy + c.h / 2), cz + 0.0};
-          const double* fq = c.face_q;
-          double w = sq[0] * fq[0] - sq[1] * fq[1] - sq[2] * fq[2] - sq[3] * fq[3];
-          double x = sq[0] * fq[1] + sq[1] * fq[0] + sq[2] * fq[3] - sq[3] * fq[2];
-          double y = sq[0] * fq[2] + sq[2] * fq[0] + sq[3] * fq[1] - sq[1] * fq[3];
-          double z = sq[0] * fq[3] + sq[3] * fq[0] + sq[1] * fq[2] - sq[2] * fq[1];
-          const double n2 = (x * x + y * y) + (z * z + w * w);
-          if (n2 > 0) {
-            const double nn = std::sqrt(n2);
-            w /= nn;
-            x /= nn;
-            y /= nn;
-            z /= nn;
-          }
-          const double rel[3] = {bt[0] - pv[0], bt[1] - pv[1], bt[2] - pv[2]};
-          double uv0 = sq[2] * rel[2] - sq[3] * rel[1];
-          double uv1 = sq[3] * rel[0] - sq[1] * rel[2];
-          double uv2 = sq[1] * rel[1] - sq[2] * rel[0];
-          uv0 += uv0;
-          uv1 += uv1;
-          uv2 += uv2;
-          const double c0 = sq[2] * uv2 - sq[3] * uv1;
-          const double c1 = sq[3] * uv0 - sq[1] * uv2;
-          const double c2 = sq[1] * uv1 - sq[2] * uv0;
-          b3d_pose& o = out[((size_t)ix * ny + iy) * nt + it];
-          o.qw = w;
-          o.qx = x;
-          o.qy = y;
-          o.qz = z;
-          o.tx = (rel[0] + sq[0] * uv0 + c0) + pv[0];
-          o.ty = (rel[1] + sq[0] * uv1 + c1) + pv[1];
-          o.tz = (rel[2] + sq[0] * uv2 + c2) + pv[2];
-        }
+    cells_poses(stage0_parent(*grid), out);
+  });
+}
+
+b3d_status b3d_contact_cells_poses(const b3d_contact_cells* cells, b3d_pose* out) {
+  return guarded([&] {
+    check(cells && out, "bad arguments");
+    cells_poses(*cells, out);
   });
 }
 

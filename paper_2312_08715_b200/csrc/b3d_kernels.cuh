@@ -26,7 +26,10 @@ struct KContact {
   double lo[3];            // rotated_bounds lo
   double w, h;             // footprint (hi - lo) in x, y
   double table_w, table_h;
-  double dx_range, dy_range;
+  // parent cell (subdivide_cell, inference.cpp:240-259): child ix spans
+  // [dx_lo + dx_w*ix/n, dx_lo + dx_w*(ix+1)/n); stage 0 is the parent
+  // [0, table_w - w] (stage0_cells, inference.cpp:208-238)
+  double dx_lo, dx_w, dy_lo, dy_w;
   const double* spin;      // n_dtheta x 2: cos, sin of half the cell-centre angle
 };
 

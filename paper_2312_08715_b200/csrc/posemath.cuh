@@ -66,8 +66,8 @@ __device__ __forceinline__ void contact_pose(const KGrid& g, long long index, KP
   const int it = (int)(index % nt);
   const int iy = (int)((index / nt) % ny);
   const int ix = (int)(index / ((long long)nt * ny));
-  const double dx = 0.5 * (c.dx_range * ix / nx + c.dx_range * (ix + 1) / nx);
-  const double dy = 0.5 * (c.dy_range * iy / ny + c.dy_range * (iy + 1) / ny);
+  const double dx = 0.5 * ((c.dx_lo + c.dx_w * ix / nx) + (c.dx_lo + c.dx_w * (ix + 1) / nx));
+  const double dy = 0.5 * ((c.dy_lo + c.dy_w * iy / ny) + (c.dy_lo + c.dy_w * (iy + 1) / ny));
   const double cs = c.spin[2 * it], sn = c.spin[2 * it + 1];
   const Q spin{cs, sn * 0.0, sn * 0.0, sn * 1.0};  // AngleAxis(dtheta, UnitZ)
   const double cx = -c.table_w / 2, cy = -c.table_h / 2, cz = 0.0;

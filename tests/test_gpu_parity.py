@@ -637,3 +637,60 @@ def test_score_parity_default_noise_grid(gpu_ctx, oracle):
     s_orc, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, noise, smax, 1)
     assert s_gpu.shape == (poses.shape[0], 9)
     assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+
+
+def _smc_setup(gpu_ctx, oracle, n_placed):
+    import smc_case as S
+    from helpers import b3d_intr
+
+    def render_scene(k, cam, inst):
+        return oracle.render(k, inst, camera=cam)
+    lib, (tv, tt), obs, placed = S.build(oracle.voxel_to_mesh, oracle.box_mesh,
+                                         oracle.contact_to_pose, render_scene, n_placed)
+    gpu_ctx.set_camera(b3d_intr(S.K), S.CAMERA)
+    table = gpu_ctx.upload_mesh(tv, tt)
+    mids = [gpu_ctx.upload_mesh(v, t) for v, t, _, _ in lib]
+    gpu_ctx.set_observation(obs)
+    return S, lib, (tv, tt), obs, table, mids
+
+
+def _compare_smc(ps_g, le_g, ps_o, le_o):
+    assert len(ps_g) == len(ps_o)
+    for (cg, eg, ltg, lwg), (co, eo, lto, lwo) in zip(ps_g, ps_o):
+        assert eg == eo and len(cg) == len(co)
+        for a, b in zip(cg, co):
+            assert a[:2] == b[:2]                      # object, face
+            assert np.allclose(a[2:], b[2:], rtol=0, atol=1e-12)  # same leaf draws
+        assert abs(ltg - lto) <= SCORE_RTOL * abs(lto)
+        assert abs(lwg - lwo) <= SCORE_RTOL * max(1.0, abs(lwo))
+    assert abs(le_g - le_o) <= SCORE_RTOL * max(1.0, abs(le_o))
+
+
+def test_run_smc_matches_oracle(gpu_ctx, oracle):
+    """run_smc (inference.cpp:398-520) with every render+score on the device:
+    stage-0 cells (2 objects x 6 faces x 36 cells x 9 noise entries), one
+    refine stage, 4 particles; the same cells, leaf draws and noise choices
+    as the oracle's restatement, weights within the score tolerance."""
+    S, lib, (tv, tt), obs, table, mids = _smc_setup(gpu_ctx, oracle, 1)
+    ps_g, le_g = gpu_ctx.run_smc([(mids[i], lib[i][2], lib[i][3]) for i in range(2)], table,
+                                 S.TABLE_W, S.TABLE_H, S.SCHEDULE, S.NOISE_GRID, 0.1, 1,
+                                 n_objects=1, n_particles=4, resample_threshold=0.5, seed=9)
+    ps_o, le_o = oracle.run_smc(S.K, S.CAMERA, obs, lib, (tv, tt, S.TABLE_W, S.TABLE_H),
+                                S.SCHEDULE, S.NOISE_GRID, 0.1, 1, n_objects=1, n_particles=4,
+                                resample_threshold=0.5, seed=9)
+    _compare_smc(ps_g, le_g, ps_o, le_o)
+    gpu_ctx.set_base_scene([], [])
+
+
+def test_run_smc_two_objects_with_extend_and_resampling(gpu_ctx, oracle):
+    """smc_extend (per-particle partial scenes as the base image) and the
+    ESS-triggered systematic resampling, against the oracle."""
+    S, lib, (tv, tt), obs, table, mids = _smc_setup(gpu_ctx, oracle, 2)
+    ps_g, le_g = gpu_ctx.run_smc([(mids[i], lib[i][2], lib[i][3]) for i in range(2)], table,
+                                 S.TABLE_W, S.TABLE_H, S.SCHEDULE, S.NOISE_GRID, 0.1, 1,
+                                 n_objects=2, n_particles=3, resample_threshold=0.9, seed=4)
+    ps_o, le_o = oracle.run_smc(S.K, S.CAMERA, obs, lib, (tv, tt, S.TABLE_W, S.TABLE_H),
+                                S.SCHEDULE, S.NOISE_GRID, 0.1, 1, n_objects=2, n_particles=3,
+                                resample_threshold=0.9, seed=4)
+    _compare_smc(ps_g, le_g, ps_o, le_o)
+    gpu_ctx.set_base_scene([], [])
