@@ -249,6 +249,62 @@ def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_fram
             "frames": n_frames, "per_resolution": out}
 
 
+def run_smc_leg(ctx, b3d, configs, n_particles=1000, seed=0):
+    """Scene-graph SMC (cmd_infer / cmd_pose_benchmark: run_smc with the
+    harness defaults, harness.cpp:463-475): 0.5 x 0.5 m table seen from 0.7 m,
+    a 5-blob library (500-4,000 voxels), one object placed in the observation
+    (240x320, N(0, 3 mm), 5 % outliers), stage 0 10x10x8 x 6 faces x 9 noise
+    entries, two 5x5x5 refine stages, 1,000 particles.  Every render+score runs
+    on the device (b3d_gpu_run_smc); wall time of the whole inference."""
+    import torch
+    rng = np.random.Generator(np.random.PCG64(8000 + seed))
+    k = configs.Intr(400.0, 400.0, 160.0, 120.0, 320, 240, 0.01, 10.0)
+    camera = np.array([0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.7])
+    tw = th = 0.5
+    tv, tt, _, _ = configs.table_mesh(b3d.box_mesh, tw, th)
+    lib = []
+    for i, n in enumerate((500, 1000, 2000, 3000, 4000)):
+        v, t = configs.make_mesh(configs.synth.eden_blob(n, 300 + i), b3d.voxel_to_mesh)
+        lib.append((v, t, v.min(axis=0), v.max(axis=0)))
+    truth = (2, 1, 0.21, 0.17, 2.2)
+    pose = b3d.contact_to_pose(tw, th, lib[2][2], lib[2][3], 1, *truth[2:])
+    render = _scene_renderer(ctx, b3d)
+    depth = render(k, camera, [(tv, tt, np.array([1.0, 0, 0, 0, 0, 0, 0])),
+                               (lib[2][0], lib[2][1], pose)])
+    obs = configs.synth.noisy_observation(depth, k.far, 0.003, 0.05, 0.2, 1.5, rng, k.near)
+    ctx.set_camera(b3d.Intrinsics(*k.as_tuple()), camera)
+    table = ctx.upload_mesh(tv, tt)
+    mids = [ctx.upload_mesh(v, t) for v, t, _, _ in lib]
+    ctx.set_observation(obs)
+    noise = [(p, f * 0.1) for p in (0.05, 0.3, 0.8) for f in (0.25, 0.5, 1.0)]
+    sched = ((10, 10, 8), [(5, 5, 5), (5, 5, 5)])
+    libs = [(mids[i], lib[i][2], lib[i][3]) for i in range(len(lib))]
+    ctx.run_smc(libs, table, tw, th, ((2, 2, 2), [(2, 2, 2)]), noise, 0.1, 2, 1, 8, 0.5, 1)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ps, le = ctx.run_smc(libs, table, tw, th, sched, noise, 0.1, 2, n_objects=1,
+                         n_particles=n_particles, resample_threshold=0.5, seed=seed)
+    dt = time.perf_counter() - t0
+    ctx.set_base_scene([], [])
+    n_stage0 = 0
+    for o in lib:
+        for face in range(1, 7):
+            lo, hi = b3d.rotated_bounds(o[2], o[3], face)
+            if tw - (hi[0] - lo[0]) > 0 and th - (hi[1] - lo[1]) > 0:
+                n_stage0 += 800
+    renders = n_stage0 + n_particles * (2 * 125 + 1)
+    best = max(ps, key=lambda p: p[3])
+    c = best[0][0]
+    return {"workload": "run_smc harness defaults: 5-object library, 240x320, stage 0 "
+                        "10x10x8 x faces x 9 noise, 2 x 5x5x5 refine, 1,000 particles, "
+                        "1 object; all render+score on device",
+            "particles": n_particles, "seconds": dt, "renders": renders,
+            "renders_per_s": renders / dt, "log_evidence": le,
+            "map_child": list(c), "truth": list(truth),
+            "map_position_error_cm": 100.0 * float(np.hypot(c[2] - truth[2], c[3] - truth[3])),
+            "map_object_correct": bool(c[0] == truth[0])}
+
+
 def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
     """configs[1]: five 32,768-hypothesis stages chained on the device
     (sample selection); device time per schedule with CUDA events."""
@@ -549,6 +605,7 @@ def main():
             extra["tracking"] = run_tracking(ctx, b3d, configs, args.tracking_frames, render_fn)
             extra["scene_graph"] = run_scene_graph(ctx, b3d, configs)
             extra["bench_tracking"] = run_bench_tracking(ctx, b3d, configs)
+            extra["smc"] = run_smc_leg(ctx, b3d, configs)
         roof = None
         if cnt is not None and "fp64_nofma_ops" in peaks:
             ops = _ops_per_hyp(cnt, 1, 1, BATCH)

@@ -274,6 +274,16 @@ def mesh_cull_sign(vertices: np.ndarray, triangles: np.ndarray) -> int:
     return out.value
 
 
+def rotated_bounds(aabb_min, aabb_max, face):
+    """rotated_bounds (scene_graph.cpp:73-89): AABB with `face` down."""
+    lo_a = np.ascontiguousarray(aabb_min, dtype=np.float64)
+    hi_a = np.ascontiguousarray(aabb_max, dtype=np.float64)
+    lo, hi = np.zeros(3), np.zeros(3)
+    _check(lib().b3d_rotated_bounds(lo_a.ctypes.data, hi_a.ctypes.data, face, lo.ctypes.data,
+                                    hi.ctypes.data))
+    return lo, hi
+
+
 def box_mesh(lo, hi):
     """make_box_mesh (scene_graph.cpp:37-58)."""
     lo_a = np.ascontiguousarray(lo, dtype=np.float64)

@@ -29,6 +29,8 @@ elif leg == "scene_graph":
     out = bench.run_scene_graph(ctx, b3d, configs)
 elif leg == "coarse_to_fine":
     out = bench.run_coarse_to_fine(ctx, b3d, configs, render_fn)
+elif leg == "smc":
+    out = bench.run_smc_leg(ctx, b3d, configs)
 elif leg == "tracking":
     out = bench.run_tracking(ctx, b3d, configs, 40, render_fn)
 else:
