@@ -31,6 +31,12 @@
 #include "b3d_kernels.cuh"
 #include "posemath.cuh"
 
+#ifndef B3D_MINB
+#define B3D_MINB 2
+#endif
+#ifndef B3D_L2_PREFETCH
+#define B3D_L2_PREFETCH 1
+#endif
 #ifndef B3D_PREFETCH
 #define B3D_PREFETCH 0
 #endif
@@ -990,7 +996,7 @@ struct VertexCache {
 // kOut: write the full depth / id images to HBM (render-many); kVS: the
 // projected vertices fit in shared memory.
 template <bool kIds, bool kScore, bool kOut, bool kVS, int kWin, bool kS1, bool kCam>
-__global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams p) {
+__global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const KParams p) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   __shared__ double s_pose[32][12];  // R (row-major) | t per upcoming hypothesis
   __shared__ int s_lo_u, s_hi_u, s_lo_v, s_hi_v, s_clip;
@@ -1020,6 +1026,23 @@ __global__ void __launch_bounds__(kThreads, 2) render_score_kernel(const KParams
     vs.bbp = reinterpret_cast<short4*>(b + 3 * (size_t)n);
   }
 
+#if B3D_L2_PREFETCH
+  // Shared read-only inputs (mesh, sorted triangles, observation) into L2 in
+  // one parallel burst spread over all CTAs, instead of every CTA's first
+  // hypothesis meeting them at DRAM latency one dependent load at a time.
+  {
+    auto pf = [&](const void* base, size_t bytes) {
+      const char* b = static_cast<const char*>(base);
+      if (!b) return;
+      for (size_t off = ((size_t)blockIdx.x * kThreads + threadIdx.x) * 128; off < bytes;
+           off += (size_t)gridDim.x * kThreads * 128)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(b + off));
+    };
+    pf(p.verts, 24ull * p.nv);
+    pf(kScore && !kIds && !kCam ? (const void*)p.tris_s : (const void*)p.tris, 16ull * p.nt);
+    if (kScore) pf(p.obs, 16ull * p.W * p.H);
+  }
+#endif
   // Hypotheses one per CTA, strided by the grid (persistent CTAs).
   const long long G = gridDim.x;
   int kk = 0;  // hypotheses this CTA has processed
