@@ -3,6 +3,10 @@
 // (render_score.cuh; score variants instantiated in rs_score_w*.cu).
 #include "render_score.cuh"
 
+#include <map>
+#include <mutex>
+#include <tuple>
+
 namespace b3d200 {
 B3D_RS_SCORE_KERNELS(extern, 0)
 B3D_RS_SCORE_KERNELS(extern, 1)
@@ -143,12 +147,33 @@ static auto pick_kernel(bool vs, int window, int n_noise, bool cam = false) {
   }
 }
 
+// Host-side launch bookkeeping is cached: the dynamic shared-memory limit is
+// set once per (kernel, size) and occupancy / static shared memory are
+// queried once -- per call these CUDA runtime queries cost tens of us, as
+// much as a small batch's kernel (device ordinal is part of the key).
+namespace {
+std::mutex g_launch_mu;
+std::map<std::tuple<const void*, int, size_t>, int> g_occupancy;  // -> blocks/SM
+std::map<std::pair<const void*, int>, size_t> g_smem_limit;        // -> current limit
+
+cudaError_t ensure_smem_limit(const void* kern, size_t smem) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_launch_mu);
+  size_t& cur = g_smem_limit[{kern, dev}];
+  if (cur >= smem) return cudaSuccess;
+  const cudaError_t e =
+      cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess) cur = smem;
+  return e;
+}
+}  // namespace
+
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st) {
   auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_noise,
                                               p.cams != nullptr);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  cudaError_t e = ensure_smem_limit(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   if (p.n_hyp <= 0) return cudaSuccess;
   kern<<<(int)std::min<long long>(grid, p.n_hyp), kThreads, smem, st>>>(p);
@@ -158,24 +183,42 @@ cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStr
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs) {
   auto kern = pick_kernel<kIds, kScore, kOut>(vs, 1, 1);  // same resources for every variant
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                       (int)smem);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const auto key = std::make_tuple(reinterpret_cast<const void*>(kern), dev, smem);
+  {
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    auto it = g_occupancy.find(key);
+    if (it != g_occupancy.end()) {
+      *blocks = it->second;
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = ensure_smem_limit(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
-  return cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, kThreads, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks, kern, kThreads, smem);
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(g_launch_mu);
+    g_occupancy[key] = *blocks;
+  }
+  return e;
 }
 
 template <bool kIds, bool kScore, bool kOut>
 size_t static_smem_render_score() {
-  size_t mx = 0;
-  for (int vs = 0; vs < 2; ++vs)
-    for (int cam = 0; cam < 2; ++cam) {
-      cudaFuncAttributes a{};
-      if (cudaFuncGetAttributes(&a, pick_kernel<kIds, kScore, kOut>(vs, 1, 1, cam)) !=
-          cudaSuccess)
-        return 8192;
-      if (a.sharedSizeBytes > mx) mx = a.sharedSizeBytes;
-    }
-  return mx;
+  static const size_t cached = [] {
+    size_t mx = 0;
+    for (int vs = 0; vs < 2; ++vs)
+      for (int cam = 0; cam < 2; ++cam) {
+        cudaFuncAttributes a{};
+        if (cudaFuncGetAttributes(&a, pick_kernel<kIds, kScore, kOut>(vs, 1, 1, cam)) !=
+            cudaSuccess)
+          return (size_t)8192;
+        if (a.sharedSizeBytes > mx) mx = a.sharedSizeBytes;
+      }
+    return mx;
+  }();
+  return cached;
 }
 
 #define B3D_INST(I, S, O)                                                                 \
