@@ -65,10 +65,12 @@ typedef struct b3d_pose {
 B3D_API const char* b3d_version(void);
 B3D_API const char* b3d_last_error(void);
 
-/* b3d.h:39,59-68 (in-memory subset; SDPT file I/O is out of scope) */
+/* b3d.h:39,59-68 (SDPT on disk: "SDPT" | u32 w | u32 h | f32[w*h]) */
 typedef struct b3d_depth_image b3d_depth_image;
 B3D_API b3d_status b3d_depth_image_create(uint32_t width, uint32_t height,
                                           const float* depth, b3d_depth_image** out);
+B3D_API b3d_status b3d_depth_image_load(const char* path, b3d_depth_image** out);
+B3D_API b3d_status b3d_depth_image_save(const b3d_depth_image* img, const char* path);
 B3D_API uint32_t b3d_depth_image_width(const b3d_depth_image* img);
 B3D_API uint32_t b3d_depth_image_height(const b3d_depth_image* img);
 B3D_API const float* b3d_depth_image_data(const b3d_depth_image* img);
@@ -82,6 +84,67 @@ B3D_API b3d_status b3d_log_likelihood(const b3d_depth_image* observed,
                                       const b3d_intrinsics* k, double p_outlier,
                                       double sigma_noise, double sigma_max,
                                       int window, double* out);
+
+/* ---- object models, libraries, scenes (b3d.h:40-43,72-101) ---- */
+typedef struct b3d_object_model b3d_object_model;
+typedef struct b3d_library b3d_library;
+typedef struct b3d_scene b3d_scene;
+typedef struct b3d_particles b3d_particles;
+
+/* SVOX on disk ("SVOX" | f32 res | f32 origin[3] | u32 n | i32[3n]);
+ * ObjectModel::from_grid: voxel_to_mesh in stored voxel order + mesh_bounds. */
+B3D_API b3d_status b3d_model_load(const char* path, int id, b3d_object_model** out);
+B3D_API b3d_status b3d_model_save(const b3d_object_model* model, const char* path);
+B3D_API b3d_status b3d_model_bbox(const b3d_object_model* model, double extents[3]);
+B3D_API b3d_status b3d_model_resolution(const b3d_object_model* model, double* out);
+B3D_API b3d_status b3d_model_voxel_count(const b3d_object_model* model, size_t* out);
+B3D_API void b3d_model_destroy(b3d_object_model* model);
+/* In-memory model (extension): n voxels (i,j,k) in stored order. */
+B3D_API b3d_status b3d_model_from_voxels(const int32_t* voxels, size_t n, double resolution,
+                                         const double origin[3], int id,
+                                         b3d_object_model** out);
+/* The model's mesh (extension; views owned by the model). */
+B3D_API b3d_status b3d_model_mesh(const b3d_object_model* model, const double** vertices,
+                                  uint64_t* n_vertices, const uint32_t** triangles,
+                                  uint64_t* n_triangles);
+
+/* Manifest JSON {"models": [{"id", "path"}]} with paths relative to it. */
+B3D_API b3d_status b3d_library_open(const char* manifest_path, b3d_library** out);
+/* In-memory library (extension): copies of models[0..n), object id = index. */
+B3D_API b3d_status b3d_library_create(const b3d_object_model* const* models, size_t n,
+                                      b3d_library** out);
+B3D_API size_t b3d_library_size(const b3d_library* lib);
+B3D_API void b3d_library_destroy(b3d_library* lib);
+
+/* Scene JSON: {"table": {"width", "height"[, "thickness"]}, "children":
+ * [{"object_id", "face", "dx", "dy", "dtheta"}]} (b3d.h:92-98). */
+B3D_API b3d_status b3d_scene_from_json(const char* json, const b3d_library* lib,
+                                       b3d_scene** out);
+B3D_API b3d_status b3d_scene_to_json(const b3d_scene* scene, char** out_json);
+B3D_API void b3d_scene_destroy(b3d_scene* scene);
+B3D_API void b3d_string_free(char* s);
+
+/* b3d.h:107-108 -- render_depth of the scene at `camera` (camera-to-world),
+ * on the device: table, then children in order (draw order = ids). */
+B3D_API b3d_status b3d_render(const b3d_scene* scene, const b3d_pose* camera,
+                              const b3d_intrinsics* k, b3d_depth_image** out);
+
+/* b3d.h:121-141 -- run_smc over the library with the `infer` config schema
+ * (intrinsics required; table, sigma_max, window >= 0, schedule
+ * (<= 4 refine stages), noise_grid, particles, resample_threshold,
+ * n_objects, threads accepted), every render+score on the device. */
+B3D_API b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
+                             const b3d_library* lib, const char* config_json, uint64_t seed,
+                             b3d_particles** out);
+B3D_API size_t b3d_particles_count(const b3d_particles* p);
+B3D_API b3d_status b3d_particles_log_evidence(const b3d_particles* p, double* out);
+/* One JSON object per line: children, noise, log_weight. */
+B3D_API b3d_status b3d_particles_to_jsonl(const b3d_particles* p, char** out);
+B3D_API b3d_status b3d_particles_type_marginal(const b3d_particles* p, double* probs,
+                                               size_t capacity);
+B3D_API b3d_status b3d_particles_map_pose(const b3d_particles* p, size_t index,
+                                          b3d_pose* out);
+B3D_API void b3d_particles_destroy(b3d_particles* p);
 
 /* ===================== part 2: batched GPU entry points ================= */
 

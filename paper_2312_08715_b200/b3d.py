@@ -18,6 +18,10 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("B3D_LIB") or os.path.join(_HERE, "_lib", "libb3d_b200.so")
 
 B3D_OK = 0
+B3D_ERROR = 1
+B3D_ERROR_CONFIG = 2
+B3D_ERROR_IO = 3
+B3D_ERROR_NUMERIC = 4
 PREFACTOR_PRINTED = 0
 PREFACTOR_UNIFORM = 1
 GRID_PRODUCT = 0
@@ -173,6 +177,33 @@ def lib() -> C.CDLL:
                                  st),
         "b3d_camera_pose_from_spherical": ([dbl, dbl, dbl, C.POINTER(Pose)], st),
         "b3d_box_mesh": ([vp, vp, vp, vp], st),
+        "b3d_depth_image_load": ([C.c_char_p, C.POINTER(vp)], st),
+        "b3d_depth_image_save": ([vp, C.c_char_p], st),
+        "b3d_model_from_voxels": ([vp, C.c_size_t, dbl, vp, st, C.POINTER(vp)], st),
+        "b3d_model_load": ([C.c_char_p, st, C.POINTER(vp)], st),
+        "b3d_model_save": ([vp, C.c_char_p], st),
+        "b3d_model_bbox": ([vp, vp], st),
+        "b3d_model_resolution": ([vp, C.POINTER(dbl)], st),
+        "b3d_model_voxel_count": ([vp, C.POINTER(C.c_size_t)], st),
+        "b3d_model_mesh": ([vp, C.POINTER(vp), C.POINTER(u64), C.POINTER(vp), C.POINTER(u64)],
+                           st),
+        "b3d_model_destroy": ([vp], None),
+        "b3d_library_open": ([C.c_char_p, C.POINTER(vp)], st),
+        "b3d_library_create": ([vp, C.c_size_t, C.POINTER(vp)], st),
+        "b3d_library_size": ([vp], C.c_size_t),
+        "b3d_library_destroy": ([vp], None),
+        "b3d_scene_from_json": ([C.c_char_p, vp, C.POINTER(vp)], st),
+        "b3d_scene_to_json": ([vp, C.POINTER(C.c_void_p)], st),
+        "b3d_scene_destroy": ([vp], None),
+        "b3d_string_free": ([C.c_void_p], None),
+        "b3d_render": ([vp, C.POINTER(Pose), C.POINTER(Intrinsics), C.POINTER(vp)], st),
+        "b3d_infer": ([vp, C.POINTER(Pose), vp, C.c_char_p, u64, C.POINTER(vp)], st),
+        "b3d_particles_count": ([vp], C.c_size_t),
+        "b3d_particles_log_evidence": ([vp, C.POINTER(dbl)], st),
+        "b3d_particles_to_jsonl": ([vp, C.POINTER(C.c_void_p)], st),
+        "b3d_particles_type_marginal": ([vp, vp, C.c_size_t], st),
+        "b3d_particles_map_pose": ([vp, C.c_size_t, C.POINTER(Pose)], st),
+        "b3d_particles_destroy": ([vp], None),
         "b3d_rotated_bounds": ([vp, vp, i32, vp, vp], st),
         "b3d_gpu_score_contact_cells": ([vp, i32, vp, vp, vp], st),
         "b3d_contact_cells_poses": ([vp, vp], st),
@@ -272,6 +303,178 @@ def mesh_cull_sign(vertices: np.ndarray, triangles: np.ndarray) -> int:
     _check(lib().b3d_mesh_cull_sign(v.ctypes.data, v.shape[0], t.ctypes.data, t.shape[0],
                                     C.byref(out)))
     return out.value
+
+
+# ---- the reference's handle API (b3d.h), thin Python wrappers --------------
+def _owned_string(fn, *args) -> str:
+    out = C.c_void_p()
+    _check(fn(*args, C.byref(out)))
+    try:
+        return C.cast(out, C.c_char_p).value.decode()
+    finally:
+        lib().b3d_string_free(out)
+
+
+class Model:
+    """b3d_object_model handle."""
+
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def from_voxels(cls, voxels, resolution, origin, id_=0):
+        v = np.ascontiguousarray(voxels, dtype=np.int32)
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        h = C.c_void_p()
+        _check(lib().b3d_model_from_voxels(v.ctypes.data, v.shape[0], resolution, o.ctypes.data,
+                                           id_, C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def load(cls, path, id_=0):
+        h = C.c_void_p()
+        _check(lib().b3d_model_load(str(path).encode(), id_, C.byref(h)))
+        return cls(h)
+
+    def save(self, path):
+        _check(lib().b3d_model_save(self.h, str(path).encode()))
+
+    def bbox(self):
+        e = np.zeros(3)
+        _check(lib().b3d_model_bbox(self.h, e.ctypes.data))
+        return e
+
+    def resolution(self):
+        r = C.c_double()
+        _check(lib().b3d_model_resolution(self.h, C.byref(r)))
+        return r.value
+
+    def voxel_count(self):
+        n = C.c_size_t()
+        _check(lib().b3d_model_voxel_count(self.h, C.byref(n)))
+        return n.value
+
+    def mesh(self):
+        vp_, tp_, nv, nt = C.c_void_p(), C.c_void_p(), C.c_uint64(), C.c_uint64()
+        _check(lib().b3d_model_mesh(self.h, C.byref(vp_), C.byref(nv), C.byref(tp_), C.byref(nt)))
+        v = np.ctypeslib.as_array(C.cast(vp_, C.POINTER(C.c_double)), (nv.value, 3)).copy()
+        t = np.ctypeslib.as_array(C.cast(tp_, C.POINTER(C.c_uint32)), (nt.value, 3)).copy()
+        return v, t
+
+    def __del__(self):
+        try:
+            lib().b3d_model_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Library:
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def create(cls, models):
+        arr = (C.c_void_p * len(models))(*[m.h.value for m in models])
+        h = C.c_void_p()
+        _check(lib().b3d_library_create(arr, len(models), C.byref(h)))
+        return cls(h)
+
+    @classmethod
+    def open(cls, manifest):
+        h = C.c_void_p()
+        _check(lib().b3d_library_open(str(manifest).encode(), C.byref(h)))
+        return cls(h)
+
+    def __len__(self):
+        return lib().b3d_library_size(self.h)
+
+    def __del__(self):
+        try:
+            lib().b3d_library_destroy(self.h)
+        except Exception:
+            pass
+
+
+class Scene:
+    def __init__(self, handle):
+        self.h = handle
+
+    @classmethod
+    def from_json(cls, text, library):
+        h = C.c_void_p()
+        _check(lib().b3d_scene_from_json(text.encode(), library.h, C.byref(h)))
+        return cls(h)
+
+    def to_json(self) -> str:
+        return _owned_string(lib().b3d_scene_to_json, self.h)
+
+    def __del__(self):
+        try:
+            lib().b3d_scene_destroy(self.h)
+        except Exception:
+            pass
+
+
+def _image_from_handle(h) -> np.ndarray:
+    L = lib()
+    w, hh = L.b3d_depth_image_width(h), L.b3d_depth_image_height(h)
+    d = np.ctypeslib.as_array(C.cast(L.b3d_depth_image_data(h), C.POINTER(C.c_float)),
+                              (hh, w)).copy()
+    L.b3d_depth_image_destroy(h)
+    return d
+
+
+def _image_handle(depth: np.ndarray):
+    d = np.ascontiguousarray(depth, dtype=np.float32)
+    h = C.c_void_p()
+    _check(lib().b3d_depth_image_create(d.shape[1], d.shape[0], d.ctypes.data, C.byref(h)))
+    return h
+
+
+def depth_image_save(depth: np.ndarray, path):
+    h = _image_handle(depth)
+    try:
+        _check(lib().b3d_depth_image_save(h, str(path).encode()))
+    finally:
+        lib().b3d_depth_image_destroy(h)
+
+
+def depth_image_load(path) -> np.ndarray:
+    h = C.c_void_p()
+    _check(lib().b3d_depth_image_load(str(path).encode(), C.byref(h)))
+    return _image_from_handle(h)
+
+
+def render(scene: Scene, camera, k: Intrinsics) -> np.ndarray:
+    """b3d_render (reference b3d.h:107-108), device-backed."""
+    h = C.c_void_p()
+    _check(lib().b3d_render(scene.h, C.byref(_pose(camera)), C.byref(k), C.byref(h)))
+    return _image_from_handle(h)
+
+
+def infer(observed: np.ndarray, camera, library: Library, config_json: str, seed: int):
+    """b3d_infer (reference b3d.h:121-124): returns (jsonl lines, log_evidence,
+    type marginal or None, map pose of child 0)."""
+    L = lib()
+    img = _image_handle(observed)
+    p = C.c_void_p()
+    try:
+        _check(L.b3d_infer(img, C.byref(_pose(camera)), library.h, config_json.encode(), seed,
+                           C.byref(p)))
+    finally:
+        L.b3d_depth_image_destroy(img)
+    try:
+        lines = _owned_string(L.b3d_particles_to_jsonl, p).strip().splitlines()
+        le = C.c_double()
+        _check(L.b3d_particles_log_evidence(p, C.byref(le)))
+        marg = np.zeros(len(library))
+        st = L.b3d_particles_type_marginal(p, marg.ctypes.data, len(marg))
+        pose = Pose()
+        _check(L.b3d_particles_map_pose(p, 0, C.byref(pose)))
+        return (lines, le.value, marg if st == B3D_OK else None,
+                np.array([getattr(pose, n) for n, _ in Pose._fields_]))
+    finally:
+        L.b3d_particles_destroy(p)
 
 
 def rotated_bounds(aabb_min, aabb_max, face):

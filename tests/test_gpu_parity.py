@@ -694,3 +694,71 @@ def test_run_smc_two_objects_with_extend_and_resampling(gpu_ctx, oracle):
                                 resample_threshold=0.9, seed=4)
     _compare_smc(ps_g, le_g, ps_o, le_o)
     gpu_ctx.set_base_scene([], [])
+
+
+def test_b3d_render_scene_handle_matches_oracle(oracle):
+    """b3d_render (b3d.h:107-108): render_depth of a scene JSON over an
+    in-memory library (table + 2 children), bitwise equal to the oracle."""
+    import json
+    vox0, vox1 = synth.eden_blob(300, 1), synth.eden_blob(500, 2)
+    m0 = b3d.Model.from_voxels(vox0, 0.005, np.zeros(3), 0)
+    m1 = b3d.Model.from_voxels(vox1, 0.005, np.zeros(3), 1)
+    lib = b3d.Library.create([m0, m1])
+    children = [(1, 3, 0.1, 0.2, 0.7), (0, 1, 0.25, 0.05, 5.5)]
+    sc = b3d.Scene.from_json(json.dumps({"table": {"width": 0.5, "height": 0.4},
+                                         "children": [dict(object_id=o, face=f, dx=x, dy=y,
+                                                           dtheta=t)
+                                                      for o, f, x, y, t in children]}), lib)
+    k = configs.Intr(200.0, 200.0, 79.5, 59.5, 160, 120, 0.05, 5.0)
+    intr = b3d_intr(k)
+    inst = [(*configs.table_mesh(oracle.box_mesh, 0.5, 0.4)[:2], np.array([1.0, 0, 0, 0, 0, 0, 0]))]
+    for o, f, x, y, t in children:
+        v, tt = (m0 if o == 0 else m1).mesh()
+        pose = oracle.contact_to_pose(0.5, 0.4, v.min(axis=0), v.max(axis=0), f, x, y, t)
+        inst.append((v, tt, pose))
+    for d, az, alt in ((0.9, 0.3, 0.7), (0.6, 2.0, 1.1), (1.2, 4.0, 0.4)):
+        cam = oracle.camera_pose_from_spherical(d, az, alt)
+        got = b3d.render(sc, cam, intr)
+        want = oracle.render(k, inst, camera=cam)
+        np.testing.assert_array_equal(got.view(np.uint32), want.view(np.uint32))
+
+
+def test_b3d_infer_matches_oracle_run_smc(oracle):
+    """b3d_infer (b3d.h:121-124) with the `infer` JSON schema: particles,
+    log-evidence and MAP pose agree with the oracle's run_smc on the same
+    seed (same draws, weights within the score tolerance)."""
+    import json
+    import smc_case as S
+    lib_o, (tv, tt), obs, placed = S.build(oracle.voxel_to_mesh, oracle.box_mesh,
+                                           oracle.contact_to_pose,
+                                           lambda k, c, i: oracle.render(k, i, camera=c))
+    models = [b3d.Model.from_voxels(synth.eden_blob(n, 40 + i), configs.RESOLUTION,
+                                    configs.synth.centered_origin(synth.eden_blob(n, 40 + i),
+                                                                  configs.RESOLUTION), i)
+              for i, n in enumerate((150, 260))]
+    for m, lo in zip(models, lib_o):
+        np.testing.assert_array_equal(m.mesh()[0], lo[0])
+    lib = b3d.Library.create(models)
+    cfg = {"intrinsics": {"fx": S.K.fx, "fy": S.K.fy, "cx": S.K.cx, "cy": S.K.cy,
+                          "width": S.K.width, "height": S.K.height, "near": S.K.near,
+                          "far": S.K.far},
+           "table": {"width": S.TABLE_W, "height": S.TABLE_H}, "sigma_max": 0.1, "window": 1,
+           "schedule": {"stage0": list(S.SCHEDULE[0]), "refine": [list(s) for s in S.SCHEDULE[1]]},
+           "particles": 4, "resample_threshold": 0.5, "n_objects": 1}
+    lines, le, marg, map_pose = b3d.infer(obs, S.CAMERA, lib, json.dumps(cfg), 9)
+    ps_o, le_o = oracle.run_smc(S.K, S.CAMERA, obs, lib_o, (tv, tt, S.TABLE_W, S.TABLE_H),
+                                S.SCHEDULE, S.NOISE_GRID, 0.1, 1, n_objects=1, n_particles=4,
+                                resample_threshold=0.5, seed=9)
+    assert len(lines) == 4 and abs(le - le_o) <= SCORE_RTOL * abs(le_o)
+    for line, (co, eo, lto, lwo) in zip(lines, ps_o):
+        j = json.loads(line)
+        c = j["children"][0]
+        assert (c["object_id"], c["face"]) == co[0][:2]
+        assert np.allclose([c["dx"], c["dy"], c["dtheta"]], co[0][2:], rtol=0, atol=1e-12)
+        assert (j["noise"]["p_outlier"], j["noise"]["sigma_noise"]) == S.NOISE_GRID[eo]
+        assert abs(j["log_weight"] - lwo) <= SCORE_RTOL * max(1.0, abs(lwo))
+    assert marg is not None and abs(marg.sum() - 1.0) < 1e-12
+    best = max(ps_o, key=lambda p: p[2])
+    o, f, x, y, t = best[0][0]
+    want = oracle.contact_to_pose(S.TABLE_W, S.TABLE_H, lib_o[o][2], lib_o[o][3], f, x, y, t)
+    np.testing.assert_allclose(map_pose, want, rtol=0, atol=1e-15)
