@@ -162,7 +162,6 @@ def run_reference(args, rank, world):
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "kernel_ms": kern_avg * 1e3,
             "data": "synthetic (seeded voxel blob, BASELINE cfg1)", "impl": "reference",
             "config": {"workload": "configs[0]: single-object scoring 160x120 (WxH), 1,024 "
                                    "hypotheses/step", "hypotheses_per_step": BATCH},
