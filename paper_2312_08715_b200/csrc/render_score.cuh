@@ -1026,6 +1026,10 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     vs.bbp = reinterpret_cast<short4*>(b + 3 * (size_t)n);
   }
 
+  // let a dependent launch (the stage reduction, launched with programmatic
+  // stream serialization) be scheduled into SMs this grid leaves idle; it
+  // waits for this grid's completion itself (griddepcontrol.wait)
+  asm volatile("griddepcontrol.launch_dependents;");
 #if B3D_L2_PREFETCH
   // Shared read-only inputs (mesh, sorted triangles, observation) into L2 in
   // one parallel burst spread over all CTAs, instead of every CTA's first

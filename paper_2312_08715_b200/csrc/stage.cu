@@ -28,6 +28,10 @@ using stage::rng_uniform;
 __global__ void __launch_bounds__(kT)
 stage_reduce_kernel(const double* __restrict__ x, long long n, int stride, int col,
                     unsigned long long* rng_state, KStageResult* out, double* probs) {
+  // programmatic dependent launch: this CTA may be resident before the
+  // score kernel that produced x has finished (it is launched into the last
+  // wave's idle SMs); wait for that grid's completion and memory here
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   __shared__ stage::StageSmem<kT> sm;
   stage::block_stage_reduce<kT>(x, n, stride, col, rng_state, out, probs, sm);
 }
@@ -127,8 +131,18 @@ __global__ void select_center_kernel(KGrid g, const KStageResult* r, int use_sam
 cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
                                 unsigned long long* rng_state, KStageResult* out,
                                 double* probs, cudaStream_t st) {
-  stage_reduce_kernel<<<1, kT, 0, st>>>(x, n, stride, col, rng_state, out, probs);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(kT);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e =
+      cudaLaunchKernelEx(&cfg, stage_reduce_kernel, x, n, stride, col, rng_state, out, probs);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_select_center(const KGrid& g, const KStageResult* r, int use_sample,
