@@ -37,6 +37,26 @@ UNIT = "hypotheses/s"
 BATCH = 1024
 
 
+def _ncu_traffic():
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the score
+    kernel from the newest committed `ncu --set full` summary
+    (profiles/r*_render_score_details.txt), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_render_score_details.txt")))
+    if not files:
+        return None
+    text = open(files[-1]).read()
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    total = 0.0
+    for key in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+        m = re.search(key + r"\s+([0-9.]+)\s+(\w+)", text)
+        if not m:
+            return None
+        total += float(m.group(1)) * scale.get(m.group(2), 1.0)
+    return {"bytes_per_launch": total, "source": os.path.relpath(files[-1], ROOT)}
+
+
 def _ops_per_hyp(c: dict, n_sigma: int, n_noise: int, n: int) -> float:
     """Algorithmic op count per hypothesis (BASELINE.md §3 / SURVEY.md 8d),
     from the oracle's exact counters."""
@@ -534,7 +554,17 @@ def main():
     if world > 1:
         dist.barrier()
     step_ms = [e0.elapsed_time(e1) for e0, _, e1 in evs]
-    kern_ms = [e0.elapsed_time(ek) for e0, ek, _ in evs]
+    # the score kernel alone (roofline): same batch, L2 flushed before each
+    # launch, CUDA events on the launching stream, outside the timed steps
+    kern_ms = []
+    for i in range(10):
+        flush.fill_(float(i))
+        ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ka.record(stream)
+        ctx.score_grid(mid, grid, d_scores, d_status)
+        kb.record(stream)
+        torch.cuda.synchronize()
+        kern_ms.append(ka.elapsed_time(kb))
     total_ms = sum(step_ms)
 
     # ---- end-to-end arm: public C ABI with pinned host buffers
@@ -611,7 +641,10 @@ def main():
             achieved = ops * BATCH / kern_avg
             roof = {"bound": "sm_fp64", "achieved": achieved / 1e12,
                     "peak": peaks["fp64_nofma_ops"] / 1e12, "unit": "Tops/s",
-                    "frac": achieved / peaks["fp64_nofma_ops"], "traffic": None,
+                    "frac": achieved / peaks["fp64_nofma_ops"],
+                    "traffic": (_ncu_traffic() or {}).get("bytes_per_launch"),
+                    "traffic_unit": "DRAM bytes per launch (ncu --set full)",
+                    "traffic_source": (_ncu_traffic() or {}).get("source"),
                     "ops_per_hypothesis": ops,
                     "kernel_ms": kern_avg * 1e3,
                     "peak_source": "measured in-run (non-FMA DMUL/DADD microbenchmark)"}
