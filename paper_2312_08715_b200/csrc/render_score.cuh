@@ -868,15 +868,16 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     // (likelihood.cpp:159-160); batched callers get -inf and a status flag
     // (DESIGN.md §5).
     const bool empty_render = rend_count == 0;
-    if (tid < p.lik.n_noise)  // likelihood.cpp:167 coefficient order
-      s_coef[tid] = empty_render ? 0.0 : p.lik.one_minus_p[tid] / (double)rend_count * p.lik.norm3[tid];
-    __syncthreads();
-    // kS1 kernels: exactly one noise entry (and sigma); else up to kMaxNoise
+    // kS1 kernels: exactly one noise entry (and sigma); else up to kMaxNoise.
+    // coef in fp64 in likelihood.cpp:167's order, by every thread (no
+    // shared copy, no barrier)
     constexpr int kNN = kS1 ? 1 : kMaxNoise;
     float coef_f[kNN], floor_f[kNN];
 #pragma unroll
     for (int e = 0; e < kNN; ++e) {
-      coef_f[e] = e < p.lik.n_noise ? (float)s_coef[e] : 0.f;
+      coef_f[e] = (e < p.lik.n_noise && !empty_render)
+                      ? (float)(p.lik.one_minus_p[e] / (double)rend_count * p.lik.norm3[e])
+                      : 0.f;
       floor_f[e] = e < p.lik.n_noise ? (float)p.lik.floor_term[e] : 0.f;
     }
 
@@ -1174,7 +1175,10 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
           s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0]);
-    __syncthreads();
+    // No barrier here: before the next hypothesis's first barrier only
+    // s_pose (warp 0), the region / count words (thread 0) and s_inst are
+    // written, and none of them is read after hyp_body's last barrier; the
+    // z-buffer and the vertex cache are rewritten only after that barrier.
   }
 }
 
