@@ -762,3 +762,61 @@ def test_b3d_infer_matches_oracle_run_smc(oracle):
     o, f, x, y, t = best[0][0]
     want = oracle.contact_to_pose(S.TABLE_W, S.TABLE_H, lib_o[o][2], lib_o[o][3], f, x, y, t)
     np.testing.assert_allclose(map_pose, want, rtol=0, atol=1e-15)
+
+
+def test_ragged_batches_and_image_borders(gpu_ctx, oracle):
+    """Batch sizes that are not multiples of the persistent grid (1, 295,
+    297), objects straddling the image borders (regions clipped to the
+    image), and an empty batch (the reference's "score_cells: no cells")."""
+    w = cfg1_oracle(seed=5)
+    mid = _setup(gpu_ctx, w)
+    rng = np.random.Generator(np.random.PCG64(31))
+    base = w.grid_poses()
+    for n in (1, 295, 297):
+        poses = base[rng.choice(base.shape[0], n)].copy()
+        # push about a third across the left / right / top / bottom borders
+        shift = rng.integers(0, 6, n)
+        poses[shift == 1, 4] -= 0.45
+        poses[shift == 2, 4] += 0.45
+        poses[shift == 3, 5] -= 0.34
+        poses[shift == 4, 5] += 0.34
+        s_gpu, st_gpu = gpu_ctx.score_poses(mid, poses)
+        s_orc, st_orc = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses,
+                                           w.noise, w.sigma_max, w.window)
+        np.testing.assert_array_equal(st_gpu, st_orc)
+        ok = st_orc == 0
+        assert rel_err(s_gpu[ok], s_orc[ok]).max() <= SCORE_RTOL
+    d, ids = gpu_ctx.render_poses(mid, base[:3] + np.array([0, 0, 0, 0, 0.42, 0.3, 0]))
+    for i in range(3):
+        od, oi = oracle.render(w.k, [(w.vertices, w.triangles, base[i] +
+                                      np.array([0, 0, 0, 0, 0.42, 0.3, 0]))], with_ids=True)
+        np.testing.assert_array_equal(d[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[i], oi)
+    with pytest.raises(b3d.B3DError) as e:
+        gpu_ctx.score_poses(mid, base[:0])
+    assert "score_cells: no cells" in str(e.value)
+
+
+def test_large_image_regions_in_global_scratch(gpu_ctx, oracle):
+    """A 1,024 x 768 image with the object close enough that its region
+    exceeds shared memory: the global-scratch instantiation, against the
+    oracle (depth/ids bitwise, scores within the tolerance)."""
+    w = cfg1_oracle(seed=6)
+    k = configs.Intr(700.0, 700.0, 511.5, 383.5, 1024, 768, 0.01, 10.0)
+    rf = lambda kk, v, t, p: oracle.render(kk, [(v, t, p)])
+    obs = rf(k, w.vertices, w.triangles, np.array([*w.gt_pose[:4], 0.0, 0.0, 0.25]))
+    gpu_ctx.set_camera(b3d_intr(k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(obs)
+    gpu_ctx.set_likelihood([(0.05, 0.004)], 0.1, 2)
+    rng = np.random.Generator(np.random.PCG64(3))
+    poses = np.array([[*w.gt_pose[:4], rng.uniform(-0.01, 0.01), rng.uniform(-0.01, 0.01),
+                       rng.uniform(0.2, 0.3)] for _ in range(6)])
+    s_gpu, _ = gpu_ctx.score_poses(mid, poses)
+    s_orc, _ = oracle.score_poses(k, obs, w.vertices, w.triangles, poses, [(0.05, 0.004)], 0.1, 2)
+    assert rel_err(s_gpu, s_orc).max() <= SCORE_RTOL
+    d, ids = gpu_ctx.render_poses(mid, poses[:2])
+    for i in range(2):
+        od, oi = oracle.render(k, [(w.vertices, w.triangles, poses[i])], with_ids=True)
+        np.testing.assert_array_equal(d[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[i], oi)
