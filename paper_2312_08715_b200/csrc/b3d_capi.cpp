@@ -425,9 +425,11 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   const size_t npx = (size_t)ctx->k.width * ctx->k.height;
   const int pad = kScore ? 2 * (window >= 0 ? window : ctx->lik.window) : 0;
   const size_t padded = (size_t)(ctx->k.width + 2 * pad) * (ctx->k.height + 2 * pad);
-  // largest CTAs/SM (2, 1) whose shared memory holds the projected vertices
-  // plus a region z-buffer of at least 2,048 pixels; otherwise the vertices
-  // spill to the per-CTA global scratch.  full_frame (camera mode: the table
+  // 2 CTAs/SM; the projected vertices go to shared memory when they fit
+  // next to a region z-buffer of at least 2,048 pixels, otherwise to the
+  // per-CTA global scratch (L1/L2).  Occupancy wins over the on-chip vertex
+  // cache: 1 CTA/SM with the cache on chip measured 29 % slower on cfg4
+  // (2,000 voxels) and 12 % on cfg2 (3,000 voxels).  full_frame (camera mode: the table
   // fills the image): prefer the first of (2 CTAs, vertices on chip), (1 CTA,
   // vertices on chip), (1 CTA, vertices in scratch) whose z-buffer holds the
   // whole padded image.
@@ -443,7 +445,11 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   };
   size_t budget = 0;
   lp.vcap = 0;
-  for (int b = 2; b >= 1; --b) {
+  static const int min_b = [] {
+    const char* e = std::getenv("B3D_PLAN_MINB");  // 1: allow 1 CTA/SM (A/B only)
+    return e ? std::atoi(e) : 2;
+  }();
+  for (int b = 2; b >= min_b; --b) {
     budget = budget_for(b);
     if (vbytes + stage + zmin <= budget) {
       lp.vcap = m.nv;
