@@ -449,9 +449,10 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
     const char* e = std::getenv("B3D_PLAN_MINB");  // 1: allow 1 CTA/SM (A/B only)
     return e ? std::atoi(e) : 2;
   }();
+  static const bool no_vcache = std::getenv("B3D_PLAN_VCAP0") != nullptr;  // A/B only
   for (int b = 2; b >= min_b; --b) {
     budget = budget_for(b);
-    if (vbytes + stage + zmin <= budget) {
+    if (!no_vcache && vbytes + stage + zmin <= budget) {
       lp.vcap = m.nv;
       break;
     }
