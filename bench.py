@@ -197,6 +197,8 @@ def run_tracking(ctx, b3d, configs, frames_n, render_fn):
     previous estimate; wall-clock per frame as in track_camera
     (tracking.cpp:73-82), host result read back every frame."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     tr = configs.cfg4(render_fn, b3d.voxel_to_mesh, seed=0, n_frames=frames_n)
     ctx.set_camera(b3d.Intrinsics(*tr["k"].as_tuple()))
     mid = ctx.upload_mesh(tr["vertices"], tr["triangles"])
@@ -236,6 +238,8 @@ def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_fram
     frames uploaded per frame from pinned host memory; FPS = frames / sum of
     the per-frame wall times (the reference's close_frame)."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
 
     def rc(k, inst, cams):
         ctx.set_camera(b3d.Intrinsics(*k.as_tuple()))
@@ -276,6 +280,8 @@ def run_smc_leg(ctx, b3d, configs, n_particles=1000, seed=0):
     entries, two 5x5x5 refine stages, 1,000 particles.  Every render+score runs
     on the device (b3d_gpu_run_smc); wall time of the whole inference."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     rng = np.random.Generator(np.random.PCG64(8000 + seed))
     k = configs.Intr(400.0, 400.0, 160.0, 120.0, 320, 240, 0.01, 10.0)
     camera = np.array([0.0, 1.0, 0.0, 0.0, 0.0, 0.0, 0.7])
@@ -328,6 +334,8 @@ def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
     """configs[1]: five 32,768-hypothesis stages chained on the device
     (sample selection); device time per schedule with CUDA events."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     w = configs.cfg2(render_fn, b3d.voxel_to_mesh, seed=0)
     ctx.set_camera(b3d.Intrinsics(*w.k.as_tuple()))
     mid = ctx.upload_mesh(w.vertices, w.triangles)
@@ -367,6 +375,8 @@ def run_scene_graph(ctx, b3d, configs, reps=3):
     fixed table + 3 objects (base scene rendered once, composited per
     hypothesis), 240x320, device time per pass (CUDA events)."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     w = configs.cfg3(_scene_renderer(ctx, b3d), b3d.voxel_to_mesh, b3d.box_mesh,
                      b3d.contact_to_pose)
     ctx.set_camera(b3d.Intrinsics(*w["k"].as_tuple()), w["camera"])
@@ -410,6 +420,8 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
     the scores (8 MiB), global argmax / logsumexp and 1,000 posterior samples
     on every rank.  Device time, max over ranks."""
     import torch
+    # the context's work and the CUDA events / NCCL calls below on one stream
+    ctx.set_stream(torch.cuda.current_stream().cuda_stream)
     import torch.distributed as dist
     from paper_2312_08715_b200.shard import gather_scores, shard_range
     w = configs.cfg5(_scene_renderer(ctx, b3d), b3d.voxel_to_mesh, b3d.box_mesh,

@@ -34,7 +34,7 @@ for r in rows:
     tot_s += st
     ln = int(r[0])
     name = "other:" + fname
-    if fname == "render_score.cu":
+    if fname.startswith("render_score.cu"):
         for n, lo, hi in ranges:
             if lo <= ln <= hi:
                 name = n
