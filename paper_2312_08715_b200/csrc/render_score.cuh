@@ -37,9 +37,6 @@
 #ifndef B3D_L2_PREFETCH
 #define B3D_L2_PREFETCH 1
 #endif
-#ifndef B3D_PREFETCH
-#define B3D_PREFETCH 0
-#endif
 
 namespace b3d200 {
 
@@ -718,10 +715,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       }
       return __ldg(tl + phys);
     };
-#if B3D_PREFETCH
-    uint4 tri_next = make_uint4(0u, 0u, 0u, 0u);
-    if (c_first + lane < n_work) tri_next = work_tri(c_first + lane);
-#endif
     const int c_first = warp * 32, c_stride = kThreads;
     for (int base = c_first; base < n_work; base += c_stride) {
       __syncwarp();
@@ -729,16 +722,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       int cls = -1;
       uint4 ent = make_uint4(0u, 0u, 0u, 0u);
       uint32_t box = 0, box2 = 0;
-#if B3D_PREFETCH
-      const uint4 tri_cur = tri_next;
-      if (ti + c_stride < n_work) tri_next = work_tri(ti + c_stride);
-#endif
       if (ti < n_work) {
-#if B3D_PREFETCH
-        const uint4 tri = tri_cur;
-#else
         const uint4 tri = work_tri(ti);
-#endif
         uint32_t ia = tri.x, ib = tri.y, ic = tri.z;
         const short4 A = vs.bb(ia), B = vs.bb(ib), C = vs.bb(ic);
         if (A.x == kClipV || B.x == kClipV || C.x == kClipV) {
