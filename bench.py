@@ -533,11 +533,36 @@ def main():
     d_res = torch.zeros(64, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    def step(ev_k=None):
+    # N > 1: the score all-gather fused into the score kernel -- every rank
+    # stores its scores straight into all ranks' symmetric-memory copies of
+    # the global array over NVLink (b3d_gpu_set_score_peers), then one
+    # symmetric-memory barrier; NCCL all_gather_into_tensor is the fallback
+    # (and the check: both must give the same array, else NCCL is used).
+    p2p = None
+    gather = "single rank"
+    if world > 1:
+        gather = "nccl all_gather_into_tensor"
+        try:
+            import torch.distributed._symmetric_memory as symm_mem
+            sym = symm_mem.empty(n_all, 1, dtype=torch.float64, device=dev)
+            hdl = symm_mem.rendezvous(sym, dist.group.WORLD)
+            p2p = (sym, hdl, [int(x) for x in hdl.buffer_ptrs])
+        except Exception as e:  # pragma: no cover - depends on the box
+            gather = f"nccl all_gather_into_tensor (symmetric memory unavailable: {e})"
+
+    def step(ev_k=None, use_p2p=True):
         if world == 1:  # score-many + stage reduction through one API call
             ctx.enumerate_grid(mid, grid, d_rng, d_res, d_scores)
             if ev_k is not None:
                 ev_k.record(stream)
+            return
+        if p2p is not None and use_p2p:
+            sym, hdl, _ = p2p
+            ctx.score_grid(mid, grid, d_scores, d_status)  # + remote stores to every rank
+            if ev_k is not None:
+                ev_k.record(stream)
+            hdl.barrier(channel=0)
+            ctx.stage_reduce(sym, n=n_all, rng_state=d_rng, out=d_res)
             return
         ctx.score_grid(mid, grid, d_scores, d_status)
         if ev_k is not None:
@@ -545,6 +570,19 @@ def main():
         dist.all_gather_into_tensor(d_all, d_scores)
         ctx.stage_reduce(d_all, n=n_all, rng_state=d_rng, out=d_res)
 
+    if p2p is not None:
+        step(use_p2p=False)  # reference gather
+        ctx.set_score_peers(p2p[2], rank * BATCH)
+        step()
+        torch.cuda.synchronize()
+        same = torch.tensor([1 if torch.equal(p2p[0], d_all) else 0], device=dev)
+        dist.all_reduce(same, op=dist.ReduceOp.MIN)
+        if int(same.item()) == 1:
+            gather = "fused into the score kernel (NVLink remote stores to symmetric memory)"
+        else:
+            ctx.set_score_peers([], 0)
+            p2p = None
+            gather = "nccl all_gather_into_tensor (fused path disagreed; fell back)"
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
@@ -565,6 +603,8 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    if p2p is not None:
+        ctx.set_score_peers([], 0)  # only the timed batch writes into the symmetric array
     step_ms = [e0.elapsed_time(e1) for e0, _, e1 in evs]
     # the score kernel alone (roofline): same batch, L2 flushed before each
     # launch, CUDA events on the launching stream, outside the timed steps
@@ -672,7 +712,8 @@ def main():
                        "triangles": int(w.triangles.shape[0]),
                        "vertices": int(w.vertices.shape[0]),
                        "l2": "flushed between timed steps (256 MB write)",
-                       "parallelism": f"dp{world} (hypothesis shards, NCCL score all-gather)"},
+                       "parallelism": f"dp{world} (hypothesis shards, score all-gather)",
+                       "score_gather": gather},
             "gpu_launches": 2 * args.steps,  # render_score + stage_reduce per step
             "e2e": {"value": e2e_value, "unit": UNIT,
                     "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 8 * n_all + 40),

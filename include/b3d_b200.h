@@ -205,6 +205,15 @@ B3D_API b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics
 B3D_API b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
                                        uint64_t n_vertices, const uint32_t* triangles,
                                        uint64_t n_triangles, int32_t* out_mesh_id);
+/* Fused score all-gather for one-process-per-GPU runs:
+ * every score-many launch of this context also stores score (h, e) into
+ * peer_ptrs[r][(offset + h) * n_noise + e] for r < n_peers -- device
+ * addresses of each rank's copy of the global score array, mapped on this
+ * device (e.g. symmetric memory over NVLink); the caller makes the ranks
+ * meet (a symmetric-memory barrier) before reading.  n_peers = 0 turns it
+ * off. */
+B3D_API b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t* peer_ptrs,
+                                           uint32_t n_peers, uint64_t offset);
 /* Back-face culling in score-many (default on).  Applies only to meshes the
  * upload found closed (every directed edge matched by its reverse) and only
  * to hypotheses with no vertex in front of z = near: a back face of a closed

@@ -170,6 +170,7 @@ def lib() -> C.CDLL:
         "b3d_gpu_upload_mesh": ([vp, vp, u64, vp, u64, C.POINTER(i32)], st),
         "b3d_gpu_set_observation": ([vp, vp], st),
         "b3d_gpu_set_culling": ([vp, st], st),
+        "b3d_gpu_set_score_peers": ([vp, vp, u32, u64], st),
         "b3d_gpu_set_camera_scene": ([vp, vp, vp, u32], st),
         "b3d_gpu_render_cameras": ([vp, vp, u64, vp, vp], st),
         "b3d_gpu_score_cameras": ([vp, vp, u64, vp, vp], st),
@@ -604,6 +605,11 @@ class GpuContext:
         _check(self._L.b3d_gpu_upload_mesh(self.h, v.ctypes.data, v.shape[0], t.ctypes.data,
                                            t.shape[0], C.byref(mid)))
         return mid.value
+
+    def set_score_peers(self, peer_ptrs, offset: int):
+        """Fused all-gather targets (b3d_gpu_set_score_peers); [] turns it off."""
+        arr = (C.c_uint64 * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
+        _check(self._L.b3d_gpu_set_score_peers(self.h, arr, len(peer_ptrs), offset))
 
     def set_culling(self, enable: bool):
         _check(self._L.b3d_gpu_set_culling(self.h, 1 if enable else 0))

@@ -327,6 +327,10 @@ struct b3d_gpu_context {
   int base_valid = 0;
   uint32_t base_draw = 0;
   bool culling = true;  // b3d_gpu_set_culling
+  // b3d_gpu_set_score_peers: fused score all-gather targets
+  double* score_peers[8] = {nullptr};
+  int n_score_peers = 0;
+  long long score_peer_offset = 0;
   // camera mode scene (b3d_gpu_set_camera_scene): concatenated instances
   std::unique_ptr<Mesh> cam_mesh;
   int cam_n = 0;
@@ -513,6 +517,9 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.nt = m.nt;
   p.draw_base = 0;
   p.cull = ctx->culling ? m.cull : 0;
+  for (int r = 0; r < 8; ++r) p.score_peers[r] = ctx->score_peers[r];
+  p.n_score_peers = ctx->n_score_peers;
+  p.score_peer_offset = ctx->score_peer_offset;
   p.tris_s = m.tris_s.as<uint4>();
   p.plane_off = m.plane_off.as<double>();
   p.plane_end = m.plane_end.as<int>();
@@ -1194,6 +1201,18 @@ b3d_status b3d_mesh_cull_sign(const double* vertices, uint64_t n_vertices,
     for (uint64_t i = 0; i < 3 * n_triangles; ++i)
       check(triangles[i] < n_vertices, "mesh: triangle index out of range");
     *out = closed_mesh_cull_sign(vertices, triangles, n_triangles);
+  });
+}
+
+b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t* peer_ptrs,
+                                   uint32_t n_peers, uint64_t offset) {
+  return guarded([&] {
+    check(ctx != nullptr && (n_peers == 0 || peer_ptrs != nullptr), "bad arguments");
+    require(n_peers <= 8, ErrorCode::invalid, "score peers: at most 8 ranks");
+    for (uint32_t r = 0; r < 8; ++r)
+      ctx->score_peers[r] = r < n_peers ? reinterpret_cast<double*>(peer_ptrs[r]) : nullptr;
+    ctx->n_score_peers = (int)n_peers;
+    ctx->score_peer_offset = (long long)offset;
   });
 }
 

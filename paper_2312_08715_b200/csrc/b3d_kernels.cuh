@@ -110,6 +110,12 @@ struct KParams {
   KLik lik;
   // outputs
   double* scores;     // n_hyp x n_noise
+  // fused score all-gather over NVLink: every score is also stored into
+  // score_peers[r][(score_peer_offset + h) * n_noise + e] for each rank r
+  // (peer-mapped symmetric buffers), so no separate collective is needed
+  double* score_peers[8];
+  int n_score_peers;
+  long long score_peer_offset;
   uint8_t* status;    // n_hyp (1 = empty render)
   float* out_depth;   // n_hyp x W x H  (render mode)
   int32_t* out_ids;   // n_hyp x W x H  (render mode, draw index or -1)

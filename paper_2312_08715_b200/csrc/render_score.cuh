@@ -952,6 +952,11 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
       }
       p.scores[h * p.lik.n_noise + e] = total;
+      if (p.n_score_peers) {  // the all-gather, fused: remote stores over NVLink
+        const long long g = (p.score_peer_offset + h) * p.lik.n_noise + e;
+        for (int r = 0; r < p.n_score_peers; ++r) p.score_peers[r][g] = total;
+        __threadfence_system();
+      }
     }
     if (tid == 0 && p.status) p.status[h] = empty_render ? 1 : 0;
   }

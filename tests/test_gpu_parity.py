@@ -820,3 +820,70 @@ def test_large_image_regions_in_global_scratch(gpu_ctx, oracle):
         od, oi = oracle.render(k, [(w.vertices, w.triangles, poses[i])], with_ids=True)
         np.testing.assert_array_equal(d[i].view(np.uint32), od.view(np.uint32))
         np.testing.assert_array_equal(ids[i], oi)
+
+
+def test_fused_score_gather_to_peer_buffers(gpu_ctx, oracle):
+    """b3d_gpu_set_score_peers: the score kernel stores every score into each
+    peer copy of the global array at its rank offset (the all-gather fused
+    into the kernel); here two local buffers stand in for two ranks' copies."""
+    import torch
+    w = cfg1_oracle()
+    mid = _setup(gpu_ctx, w)
+    grid = gpu_ctx.make_grid(w.center, w.extent, w.count, torch.from_numpy(w.rotations).cuda(),
+                             w.grid_mode)
+    n = w.n_hyp
+    a = torch.full((3 * n, 1), -1.0, dtype=torch.float64, device="cuda")
+    b = torch.full((3 * n, 1), -1.0, dtype=torch.float64, device="cuda")
+    sc = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
+    gpu_ctx.set_score_peers([a.data_ptr(), b.data_ptr()], n)  # this "rank" owns [n, 2n)
+    try:
+        gpu_ctx.score_grid(mid, grid, sc, None)
+        torch.cuda.synchronize()
+    finally:
+        gpu_ctx.set_score_peers([], 0)
+    for buf in (a, b):
+        assert torch.equal(buf[n:2 * n], sc)
+        assert (buf[:n] == -1).all() and (buf[2 * n:] == -1).all()
+    s2, _ = gpu_ctx.score_grid(mid, grid)  # peers off again: plain scores
+    np.testing.assert_array_equal(s2, sc.cpu().numpy())
+
+
+def test_fused_score_gather_symmetric_memory_single_rank(gpu_ctx, oracle):
+    """The bench's N > 1 plumbing on one rank: a 1-rank NCCL group,
+    symmetric-memory rendezvous, the peer pointer from the handle, the
+    symmetric-memory barrier."""
+    import os
+    import socket
+    import torch
+    import torch.distributed as dist
+    try:
+        import torch.distributed._symmetric_memory as symm_mem
+    except Exception:
+        pytest.skip("symmetric memory unavailable")
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                            device_id=torch.device("cuda", 0))
+    try:
+        w = cfg1_oracle()
+        mid = _setup(gpu_ctx, w)
+        poses = torch.from_numpy(w.grid_poses()[:300]).cuda()
+        try:
+            sym = symm_mem.empty(300, 1, dtype=torch.float64, device="cuda")
+            hdl = symm_mem.rendezvous(sym, dist.group.WORLD)
+        except Exception as e:
+            pytest.skip(f"symmetric memory rendezvous unavailable: {e}")
+        sym.fill_(0.0)
+        sc = torch.zeros((300, 1), dtype=torch.float64, device="cuda")
+        gpu_ctx.set_score_peers([int(x) for x in hdl.buffer_ptrs], 0)
+        try:
+            gpu_ctx.score_poses(mid, poses, sc, None)
+            hdl.barrier(channel=0)
+            torch.cuda.synchronize()
+        finally:
+            gpu_ctx.set_score_peers([], 0)
+        assert torch.equal(sym, sc)
+    finally:
+        dist.destroy_process_group()
