@@ -138,6 +138,27 @@ double visible_volume(const b3d_intrinsics& k) {
 }
 
 // ---------------------------------------------------------- device buffers
+// Page-locked host staging (track_camera's per-stage camera / score copies).
+struct PinnedBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  void ensure(size_t n) {
+    if (n <= bytes) return;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    cuda_check(cudaMallocHost(&p, n), "cudaMallocHost");
+    bytes = n;
+  }
+  ~PinnedBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  template <class T>
+  T* as() const {
+    return static_cast<T*>(p);
+  }
+};
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
@@ -321,6 +342,7 @@ struct b3d_gpu_context {
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
+  PinnedBuf pin_cams, pin_scores;  // track_camera staging
   // fixed scene (compose_render)
   bool has_base = false;
   DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
@@ -1653,7 +1675,6 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
     const bool dev_frames = is_device_ptr(frames);
     std::vector<KPose> cams;
     std::vector<int> slot;
-    std::vector<double> dscore;
     ctx->c2f_scores.ensure(8 * n_grid);
     ctx->c2f_centers.ensure(sizeof(KPose) * n_grid);
     constexpr double kNegInf = -std::numeric_limits<double>::infinity();
@@ -1697,19 +1718,23 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
             cams.push_back(camera_from_spherical(g.d, g.az, g.alt));
           }
           std::vector<double> scores(grid.size(), kNegInf);
-          if (!cams.empty()) {
-            cuda_check(cudaMemcpyAsync(ctx->c2f_centers.p, cams.data(), sizeof(KPose) * cams.size(),
-                                       cudaMemcpyHostToDevice, ctx->stream),
+          if (!cams.empty()) {  // pinned staging: asynchronous copies, one sync per stage
+            ctx->pin_cams.ensure(sizeof(KPose) * n_grid);
+            ctx->pin_scores.ensure(8 * n_grid);
+            std::copy(cams.begin(), cams.end(), ctx->pin_cams.as<KPose>());
+            cuda_check(cudaMemcpyAsync(ctx->c2f_centers.p, ctx->pin_cams.p,
+                                       sizeof(KPose) * cams.size(), cudaMemcpyHostToDevice,
+                                       ctx->stream),
                        "cudaMemcpyAsync cameras");
             launch_score_cameras(ctx, ctx->c2f_centers.as<KPose>(), (long long)cams.size(),
                                  ctx->c2f_scores.as<double>(), nullptr);
-            dscore.resize(cams.size());
-            cuda_check(cudaMemcpyAsync(dscore.data(), ctx->c2f_scores.p, 8 * cams.size(),
+            cuda_check(cudaMemcpyAsync(ctx->pin_scores.p, ctx->c2f_scores.p, 8 * cams.size(),
                                        cudaMemcpyDeviceToHost, ctx->stream),
                        "cudaMemcpyAsync scores");
             cuda_check(cudaStreamSynchronize(ctx->stream), "track_camera stage");
+            const double* ds = ctx->pin_scores.as<double>();
             for (size_t i = 0; i < grid.size(); ++i)
-              if (slot[i] >= 0) scores[i] = dscore[slot[i]];
+              if (slot[i] >= 0) scores[i] = ds[slot[i]];
           }
           size_t best = 0;  // tracking.cpp:132-134 (strict >, first index)
           for (size_t i = 1; i < scores.size(); ++i)
