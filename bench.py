@@ -249,8 +249,12 @@ def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_fram
 
     out = []
     for res in resolutions:
-        seq = configs.orbit_sequence(rc, b3d.voxel_to_mesh, b3d.box_mesh, b3d.contact_to_pose,
-                                     res=res, n_frames=n_frames)
+        # the reference's frames: sample_observation with Rng(0).split(obj, res).split(0x0f, i)
+        seq = configs.orbit_sequence(
+            rc, b3d.voxel_to_mesh, b3d.box_mesh, b3d.contact_to_pose, res=res, n_frames=n_frames,
+            sample_fn=lambda k, d, p, s, st: b3d.sample_observations(
+                b3d.Intrinsics(*k.as_tuple()), d, p, s, st),
+            rng_state=b3d.rng_split(b3d.rng_seed(0), 0, res))
         cams = np.array([b3d.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
                          for a in seq["azimuths"]])
         frames = torch.from_numpy(configs.orbit_frames(seq, cams)).pin_memory().numpy()
@@ -267,7 +271,9 @@ def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_fram
                     "mean_orientation_error_deg": statistics.mean(rot),
                     "window": seq["window"]})
     return {"workload": "bench-tracking orbit (Table 1 analog): table + 1,000-voxel blob, "
-                        f"{n_frames} frames, 125-point spherical lattice x 3 stages per frame, "
+                        f"{n_frames} frames (the reference's sample_observation noise model, "
+                        "p_outlier 0.02, sigma 2 mm), 125-point spherical lattice x 3 stages "
+                        "per frame, "
                         "camera-mode multi-instance render+score on device",
             "frames": n_frames, "per_resolution": out}
 

@@ -465,6 +465,27 @@ B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
 B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,
                            uint64_t out[5]);
 
+/* sample_observation (likelihood.cpp:44-80; replaces the reference's
+ * b3d::sample_observation, likelihood.hpp:34-35): a synthetic observed depth
+ * image from a rendered one -- |cloud| draws, each an outlier uniform in the
+ * viewing frustum with probability p_outlier, else a rendered point drawn with
+ * replacement plus N(0, sigma) per axis, reprojected (lround) and kept as the
+ * nearest fp32 depth.  Bitwise the reference's on the same Rng state, which
+ * is advanced in place.  Host code: one sequential Rng stream.
+ * Errors: invalid noise (sigma <= 0, p outside [0,1]) or an all-sentinel
+ * render -> B3D_ERROR (the reference throws ErrorCode::invalid). */
+B3D_API b3d_status b3d_sample_observation(const b3d_intrinsics* k, const float* rendered,
+                                          const b3d_noise* noise, uint64_t rng_state[5],
+                                          float* out);
+/* n frames at once as generate_orbit_sequence draws them
+ * (tracking.cpp:199-202): frame i uses rng_state.split(split_key, i)
+ * (0x0f in the reference); frames run on all host threads.  rendered / out:
+ * n x H x W fp32.  rng_state is not advanced. */
+B3D_API b3d_status b3d_sample_observations(const b3d_intrinsics* k, const float* rendered,
+                                           uint64_t n, const b3d_noise* noise,
+                                           const uint64_t rng_state[5], uint64_t split_key,
+                                           float* out);
+
 /* voxel_to_mesh (geometry.cpp:142-177) on the host: exterior faces of the
  * occupied voxels in stored order.  Capacities: vertices >= 24*n doubles,
  * triangles >= 36*n u32. */

@@ -874,6 +874,56 @@ void orc_depth_to_cloud(const float* depth, const orc_intrinsics* k, double* out
   *n = m;
 }
 
+/* sample_observation (likelihood.cpp:44-80): |cloud| draws from one Rng
+ * stream -- with probability p_outlier a point uniform in the viewing
+ * frustum (depth density ~ z^2), else a rendered point drawn with
+ * replacement plus N(0, sigma) per axis -- reprojected with lround and kept
+ * as the nearest fp32 depth per pixel.  Returns 1 for invalid noise or an
+ * all-sentinel render (the reference throws). */
+int orc_sample_observation(const float* rendered, const orc_intrinsics* k, double p_outlier,
+                           double sigma, uint64_t st[5], float* out) {
+  if (!(k->far_m > 0) || !(sigma > 0) || !(p_outlier >= 0 && p_outlier <= 1)) return 1;
+  const size_t npx = (size_t)k->width * k->height;
+  double* cloud = (double*)malloc(sizeof(double) * 3 * (npx ? npx : 1));
+  size_t n = 0;
+  orc_depth_to_cloud(rendered, k, cloud, &n);
+  if (n == 0) {
+    free(cloud);
+    return 1;
+  }
+  const double near3 = k->near_m * k->near_m * k->near_m;
+  const double far3 = k->far_m * k->far_m * k->far_m;
+  const float sentinel = (float)k->far_m;
+  for (size_t i = 0; i < npx; ++i) out[i] = sentinel;
+  for (size_t i = 0; i < n; ++i) {
+    double x, y, z;
+    if (orc_rng_uniform(st) < p_outlier) {
+      z = cbrt(near3 + orc_rng_uniform(st) * (far3 - near3));
+      const double xl = (0.0 - k->cx) * z / k->fx, xh = (k->width - k->cx) * z / k->fx;
+      x = xl + (xh - xl) * orc_rng_uniform(st);
+      const double yl = (0.0 - k->cy) * z / k->fy, yh = (k->height - k->cy) * z / k->fy;
+      y = yl + (yh - yl) * orc_rng_uniform(st);
+    } else {
+      const size_t j = (size_t)orc_rng_uniform_int(st, n);
+      x = cloud[3 * j];
+      y = cloud[3 * j + 1];
+      z = cloud[3 * j + 2];
+      x += 0.0 + sigma * orc_rng_normal(st);
+      y += 0.0 + sigma * orc_rng_normal(st);
+      z += 0.0 + sigma * orc_rng_normal(st);
+    }
+    if (z < k->near_m || z >= k->far_m) continue;
+    const long u = lround(k->fx * x / z + k->cx);
+    const long v = lround(k->fy * y / z + k->cy);
+    if (u < 0 || u >= (long)k->width || v < 0 || v >= (long)k->height) continue;
+    float* cell = out + (size_t)v * k->width + (size_t)u;
+    const float zf = (float)z;
+    if (zf < *cell) *cell = zf;
+  }
+  free(cloud);
+  return 0;
+}
+
 /* likelihood.cpp:82-104 */
 int orc_full_loglik_points(const double* op, size_t no, const double* rp, size_t nr,
                            const orc_noise* np, double volume, double sigma_max, int prefactor,

@@ -137,6 +137,10 @@ int orc_windowed_loglik_multi(const float* observed, const float* rendered,
 /* depth_to_cloud (geometry.cpp:54-70): non-sentinel pixels row-major,
  * ((u-cx)z/fx, (v-cy)z/fy, z).  out: capacity W*H*3 doubles. */
 void orc_depth_to_cloud(const float* depth, const orc_intrinsics* k, double* out, size_t* n);
+/* sample_observation (likelihood.cpp:44-80) with the reference's Rng stream;
+ * out: W*H fp32 depths.  Returns 1 on invalid noise / all-sentinel render. */
+int orc_sample_observation(const float* rendered, const orc_intrinsics* k, double p_outlier,
+                           double sigma, uint64_t st[5], float* out);
 /* full_log_likelihood over explicit point clouds (likelihood.cpp:82-104).
  * Returns 1 for an empty rendered cloud / invalid noise. */
 int orc_full_loglik_points(const double* obs, size_t n_obs, const double* rend,

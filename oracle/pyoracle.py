@@ -89,6 +89,7 @@ def lib():
         L.orc_full_loglik_points.argtypes = [vp, C.c_size_t, vp, C.c_size_t, vp, d, d, C.c_int,
                                              vp]
         L.orc_depth_to_cloud.argtypes = [vp, vp, vp, vp]
+        L.orc_sample_observation.argtypes = [vp, vp, d, d, vp, vp]
         L.orc_raster_mesh.argtypes = [vp, vp, vp, vp, C.c_uint64, vp, C.c_uint64, vp,
                                       C.c_uint32, vp]
         L.orc_render_instances.argtypes = [vp, vp, vp, C.c_size_t, vp, vp, vp]
@@ -297,6 +298,17 @@ def depth_to_cloud(depth, k):
     n = C.c_size_t()
     lib().orc_depth_to_cloud(_p(d), C.byref(ki), _p(out), C.byref(n))
     return out[: n.value].copy()
+
+
+def sample_observation(rendered, k, p_outlier, sigma, st):
+    """likelihood.cpp:44-80; st (5 x uint64) advanced in place.  None when the
+    reference would throw."""
+    r = np.ascontiguousarray(rendered, dtype=np.float32)
+    out = np.empty_like(r)
+    ki = intr(k)
+    if lib().orc_sample_observation(_p(r), C.byref(ki), p_outlier, sigma, _p(st), _p(out)):
+        return None
+    return out
 
 
 def visible_volume(k):

@@ -230,6 +230,9 @@ def lib() -> C.CDLL:
         "b3d_rng_seed": ([u64, vp], None),
         "b3d_rng_split": ([vp, u64, u64, u64, vp], None),
         "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
+        "b3d_sample_observation": ([C.POINTER(Intrinsics), vp, C.POINTER(Noise), vp, vp], st),
+        "b3d_sample_observations": ([C.POINTER(Intrinsics), vp, u64, C.POINTER(Noise), vp, u64,
+                                     vp], st),
     }
     for name, (args, res) in sig.items():
         if os.environ.get("B3D_LIB") and not hasattr(L, name):
@@ -280,6 +283,36 @@ def rng_seed(seed: int) -> np.ndarray:
 def rng_split(state: np.ndarray, k0: int, k1: int = 0, k2: int = 0) -> np.ndarray:
     out = np.zeros(5, dtype=np.uint64)
     lib().b3d_rng_split(state.ctypes.data, k0, k1, k2, out.ctypes.data)
+    return out
+
+
+def sample_observation(k: Intrinsics, rendered: np.ndarray, p_outlier: float, sigma: float,
+                       rng_state: np.ndarray) -> np.ndarray:
+    """The reference's sample_observation (likelihood.cpp:44-80): a synthetic
+    observed depth image from a rendered one; rng_state (5 x uint64) is
+    advanced in place, as the reference's Rng& is."""
+    r = np.ascontiguousarray(rendered, dtype=np.float32)
+    assert r.shape == (k.height, k.width)
+    assert rng_state.dtype == np.uint64 and rng_state.flags.c_contiguous
+    out = np.empty_like(r)
+    nz = Noise(p_outlier, sigma)
+    _check(lib().b3d_sample_observation(C.byref(k), r.ctypes.data, C.byref(nz),
+                                        rng_state.ctypes.data, out.ctypes.data))
+    return out
+
+
+def sample_observations(k: Intrinsics, rendered: np.ndarray, p_outlier: float, sigma: float,
+                        rng_state: np.ndarray, split_key: int = 0x0F) -> np.ndarray:
+    """Frames of generate_orbit_sequence (tracking.cpp:199-202): frame i is
+    sample_observation(rendered[i]) with rng_state.split(split_key, i); all host
+    threads."""
+    r = np.ascontiguousarray(rendered, dtype=np.float32)
+    assert r.ndim == 3 and r.shape[1:] == (k.height, k.width)
+    st = np.ascontiguousarray(rng_state, dtype=np.uint64)
+    out = np.empty_like(r)
+    nz = Noise(p_outlier, sigma)
+    _check(lib().b3d_sample_observations(C.byref(k), r.ctypes.data, r.shape[0], C.byref(nz),
+                                         st.ctypes.data, split_key, out.ctypes.data))
     return out
 
 

@@ -362,7 +362,8 @@ def default_window(width: int) -> int:
 
 def orbit_sequence(render_cameras, mesh_fn, box_fn, contact_fn, res: int, n_frames: int = 120,
                    seed: int = 0, n_voxels: int = 1000, distance: float = 0.9,
-                   altitude_deg: float = 40.0, sweep_deg: float = 360.0):
+                   altitude_deg: float = 40.0, sweep_deg: float = 360.0, sample_fn=None,
+                   rng_state=None):
     """bench-tracking's orbit sequence (generate_orbit_sequence,
     tracking.cpp:174-215; harness.cpp:743-770 defaults): a 0.5 x 0.5 m table
     with one seeded voxel blob (stands in for the library object) standing on
@@ -370,7 +371,13 @@ def orbit_sequence(render_cameras, mesh_fn, box_fn, contact_fn, res: int, n_fram
     sweeping 360 deg over the frames, square intrinsics (60 deg FOV, near 0.1,
     far 5).  Frames: render + N(0, 2 mm) depth noise, 2 % outliers (noise
     p_outlier 0.02, sigma 2 mm, the bench default).  render_cameras(k,
-    instances, cameras) -> depth images."""
+    instances, cameras) -> depth images.
+
+    With sample_fn(k, depth_stack, p_outlier, sigma, rng_state) -> frames
+    (b3d.sample_observations) and rng_state = Rng(seed).split(obj, res), the
+    frames are the reference's own: sample_observation with
+    rng.split(0x0f, i) per frame (tracking.cpp:196-203, harness.cpp:744-746);
+    without, a numpy depth-noise model stands in."""
     rng = np.random.Generator(np.random.PCG64(7000 + 13 * seed + res))
     k = square_intrinsics(res)
     tw = th = 0.5
@@ -387,7 +394,8 @@ def orbit_sequence(render_cameras, mesh_fn, box_fn, contact_fn, res: int, n_fram
     az = [sweep * i / n_frames for i in range(n_frames)]
     return {"k": k, "instances": inst, "azimuths": az, "distance": distance, "altitude": alt,
             "noise": (0.02, 0.002), "window": default_window(res), "sigma_max": 0.1,
-            "rng": rng, "render_cameras": render_cameras}
+            "rng": rng, "render_cameras": render_cameras, "sample_fn": sample_fn,
+            "rng_state": rng_state}
 
 
 def orbit_frames(seq, cameras):
@@ -395,6 +403,9 @@ def orbit_frames(seq, cameras):
     the sequence's seeded depth noise and outliers."""
     k = seq["k"]
     depth = seq["render_cameras"](k, seq["instances"], cameras)
+    if seq.get("sample_fn") is not None:  # frames 0..n-1 of the sequence
+        p_out, sigma = seq["noise"]
+        return seq["sample_fn"](k, depth, p_out, sigma, seq["rng_state"])
     out = np.empty_like(depth)
     for i in range(depth.shape[0]):
         out[i] = synth.noisy_observation(depth[i], k.far, 0.002, 0.02, k.near, k.far, seq["rng"],

@@ -20,6 +20,8 @@
 #include <string>
 #include <unordered_map>
 #include <vector>
+#include <atomic>
+#include <thread>
 
 #include "b3d_kernels.cuh"
 
@@ -2269,6 +2271,150 @@ b3d_status b3d_voxel_to_mesh(const int32_t* voxels, uint64_t n, double resolutio
     }
     *n_vertices = nv;
     *n_triangles = nt;
+  });
+}
+
+// ---- synthetic observations (likelihood.cpp:44-80, tracking.cpp:174-206)
+//
+// sample_observation consumes ONE Rng stream with a data-dependent number of
+// draws per point (outlier test, rejection-sampled index, Box-Muller loops),
+// so it cannot be split across threads without changing the stream; it runs
+// on the host with the reference's libm calls (cbrt, log, cos, sqrt, lround),
+// which makes it bitwise the reference's.  Frames of a sequence use
+// independent split streams and run one thread per frame.
+namespace {
+
+struct HostRng {
+  uint64_t s[5];
+  uint64_t next() {  // rng.cpp:30-40 (xoshiro256**)
+    uint64_t* q = s + 1;
+    auto rotl = [](uint64_t x, int k) { return (x << k) | (x >> (64 - k)); };
+    const uint64_t r = rotl(q[1] * 5, 7) * 9;
+    const uint64_t t = q[1] << 17;
+    q[2] ^= q[0];
+    q[3] ^= q[1];
+    q[1] ^= q[2];
+    q[0] ^= q[3];
+    q[2] ^= t;
+    q[3] = rotl(q[3], 45);
+    return r;
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+  double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }
+  uint64_t uniform_int(uint64_t n) {  // rng.cpp:48-57
+    const uint64_t limit = n * (UINT64_MAX / n);
+    uint64_t x;
+    do {
+      x = next();
+    } while (x >= limit);
+    return x % n;
+  }
+  double normal() {  // rng.cpp:59-64
+    double u1 = uniform();
+    double u2 = uniform();
+    while (u1 <= 0.0) u1 = uniform();
+    return std::sqrt(-2.0 * std::log(u1)) * std::cos(6.283185307179586476925287 * u2);
+  }
+};
+
+void check_noise(const b3d_intrinsics& k, const b3d_noise& np) {
+  // validate_noise(np, k.far) (likelihood.cpp:21-27)
+  check(k.far_m > 0, "sigma_max must be positive");
+  check(np.sigma_noise > 0, "sigma_noise must be positive");
+  check(np.p_outlier >= 0 && np.p_outlier <= 1, "p_outlier must be in [0,1]");
+}
+
+void sample_one(const b3d_intrinsics& k, const float* rendered, const b3d_noise& np,
+                HostRng& rng, float* out) {
+  // depth_to_cloud (geometry.cpp:54-70)
+  const float sentinel = static_cast<float>(k.far_m);
+  std::vector<double> cloud;
+  cloud.reserve(3 * (size_t)k.width * k.height);
+  for (uint32_t v = 0; v < k.height; ++v)
+    for (uint32_t u = 0; u < k.width; ++u) {
+      const float z = rendered[(size_t)v * k.width + u];
+      if (z >= sentinel) continue;
+      const double zd = z;
+      cloud.push_back((u - k.cx) * zd / k.fx);
+      cloud.push_back((v - k.cy) * zd / k.fy);
+      cloud.push_back(zd);
+    }
+  const size_t n = cloud.size() / 3;
+  check(n > 0, "sample_observation: all-sentinel render");
+  const double near3 = k.near_m * k.near_m * k.near_m;
+  const double far3 = k.far_m * k.far_m * k.far_m;
+  std::fill(out, out + (size_t)k.width * k.height, sentinel);
+  for (size_t i = 0; i < n; ++i) {
+    double x, y, z;
+    if (rng.uniform() < np.p_outlier) {
+      // uniform in the viewing frustum: depth density ~ z^2
+      z = std::cbrt(near3 + rng.uniform() * (far3 - near3));
+      x = rng.uniform((0.0 - k.cx) * z / k.fx, (k.width - k.cx) * z / k.fx);
+      y = rng.uniform((0.0 - k.cy) * z / k.fy, (k.height - k.cy) * z / k.fy);
+    } else {
+      const size_t j = (size_t)rng.uniform_int(n);
+      x = cloud[3 * j];
+      y = cloud[3 * j + 1];
+      z = cloud[3 * j + 2];
+      x += 0.0 + np.sigma_noise * rng.normal();
+      y += 0.0 + np.sigma_noise * rng.normal();
+      z += 0.0 + np.sigma_noise * rng.normal();
+    }
+    if (z < k.near_m || z >= k.far_m) continue;
+    const long u = std::lround(k.fx * x / z + k.cx);
+    const long v = std::lround(k.fy * y / z + k.cy);
+    if (u < 0 || u >= static_cast<long>(k.width) || v < 0 || v >= static_cast<long>(k.height))
+      continue;
+    float& cell = out[(size_t)v * k.width + (size_t)u];
+    cell = std::min(cell, static_cast<float>(z));
+  }
+}
+
+}  // namespace
+
+b3d_status b3d_sample_observation(const b3d_intrinsics* k, const float* rendered,
+                                  const b3d_noise* noise, uint64_t rng_state[5], float* out) {
+  return guarded([&] {
+    check(k && rendered && noise && rng_state && out, "bad arguments");
+    check(k->width > 0 && k->height > 0, "bad intrinsics");
+    check_noise(*k, *noise);
+    HostRng rng;
+    std::memcpy(rng.s, rng_state, sizeof(rng.s));
+    sample_one(*k, rendered, *noise, rng, out);
+    std::memcpy(rng_state, rng.s, sizeof(rng.s));
+  });
+}
+
+b3d_status b3d_sample_observations(const b3d_intrinsics* k, const float* rendered, uint64_t n,
+                                   const b3d_noise* noise, const uint64_t rng_state[5],
+                                   uint64_t split_key, float* out) {
+  return guarded([&] {
+    check(k && rendered && noise && rng_state && out, "bad arguments");
+    check(k->width > 0 && k->height > 0, "bad intrinsics");
+    check_noise(*k, *noise);
+    const size_t npx = (size_t)k->width * k->height;
+    std::vector<uint8_t> empty(n, 0);
+    const float sentinel = static_cast<float>(k->far_m);
+    for (uint64_t i = 0; i < n; ++i) {
+      const float* r = rendered + i * npx;
+      empty[i] = std::none_of(r, r + npx, [&](float z) { return z < sentinel; });
+    }
+    check(std::find(empty.begin(), empty.end(), 1) == empty.end(),
+          "sample_observation: all-sentinel render");
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const unsigned nth = (unsigned)std::min<uint64_t>(n, hw);
+    std::vector<std::thread> pool;
+    std::atomic<uint64_t> next{0};
+    for (unsigned t = 0; t < nth; ++t)
+      pool.emplace_back([&] {
+        for (uint64_t i; (i = next.fetch_add(1)) < n;) {
+          // Rng frame_rng = rng.split(split_key, i) (tracking.cpp:200)
+          HostRng rng;
+          b3d_rng_split(rng_state, split_key, i, 0, rng.s);
+          sample_one(*k, rendered + i * npx, *noise, rng, out + i * npx);
+        }
+      });
+    for (auto& th : pool) th.join();
   });
 }
 

@@ -514,11 +514,19 @@ def test_back_face_culling_with_base_scene_and_near_clip(gpu_ctx, oracle):
     gpu_ctx.set_base_scene([], [])
 
 
-def _orbit(oracle, res, n_frames=40, n_voxels=600):
+def _orbit(oracle, res, n_frames=40, n_voxels=600, ref_frames=False):
+    """ref_frames: the reference's sample_observation frames (oracle restatement,
+    Rng(0).split(0, res).split(0x0f, i))."""
     rc = lambda k, inst, cams: np.stack([oracle.render(k, inst, camera=c) for c in cams])
+    kw = {}
+    if ref_frames:
+        kw = dict(sample_fn=lambda k, d, p, s, st: np.stack([
+            oracle.sample_observation(d[i], k, p, s, oracle.rng_split(st, 0x0F, i))
+            for i in range(d.shape[0])]),
+                  rng_state=oracle.rng_split(oracle.rng_seed(0), 0, res))
     return configs.orbit_sequence(rc, oracle.voxel_to_mesh, oracle.box_mesh,
                                   oracle.contact_to_pose, res=res, n_frames=n_frames,
-                                  n_voxels=n_voxels)
+                                  n_voxels=n_voxels, **kw)
 
 
 def _camera_scene(ctx, seq):
@@ -571,7 +579,7 @@ def test_track_camera_matches_oracle(gpu_ctx, oracle):
     """bench-tracking's orbit (harness.cpp:743-770) at 50 x 50: the device
     track_camera picks the oracle's lattice point at every frame (poses
     bitwise equal; a differing pick must tie within the score tolerance)."""
-    seq = _orbit(oracle, 50)
+    seq = _orbit(oracle, 50, ref_frames=True)
     _camera_scene(gpu_ctx, seq)
     gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
     cams = [oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
@@ -589,6 +597,22 @@ def test_track_camera_matches_oracle(gpu_ctx, oracle):
             s = np.array(scores)
             assert np.sort(s)[-1] - np.sort(s)[-2] <= SCORE_RTOL * abs(np.max(s))
         assert np.linalg.norm(est[f][4:] - cams[f][4:]) < 0.03
+
+
+def test_orbit_frames_equal_the_reference(gpu_ctx, oracle):
+    """generate_orbit_sequence (tracking.cpp:174-206) as the bench builds it:
+    device camera renders + the product's sample_observation on split streams
+    give frames bitwise equal to the oracle's render + sample_observation."""
+    for res in (25, 100):
+        seq = _orbit(oracle, res, ref_frames=True)
+        _camera_scene(gpu_ctx, seq)
+        cams = np.array([oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+                         for a in seq["azimuths"][:6]])
+        want = configs.orbit_frames(seq, cams)
+        d = gpu_ctx.render_cameras(cams, with_ids=False)[0]
+        got = b3d.sample_observations(b3d_intr(seq["k"]), d, *seq["noise"],
+                                      b3d.rng_split(b3d.rng_seed(0), 0, res))
+        assert got.tobytes() == want.tobytes()
 
 
 def test_enumerate_grid_matches_score_then_reduce(gpu_ctx, oracle):
