@@ -344,7 +344,8 @@ struct b3d_gpu_context {
   DevBuf zscratch, vscratch;
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
-  PinnedBuf pin_cams, pin_scores;  // track_camera staging
+  PinnedBuf pin_cams, pin_scores;  // track_camera / enumerate_poses staging
+  PinnedBuf io_pin;                 // stage result + Rng state (enumerate_poses)
   // fixed scene (compose_render)
   bool has_base = false;
   DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
@@ -1188,7 +1189,9 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
     cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
     c->stream = c->own;
     c->obs_count.ensure(sizeof(int));
-    c->result.ensure(sizeof(KStageResult));
+    static_assert(sizeof(KStageResult) <= 64, "rng slot at +64");
+    c->result.ensure(128);  // KStageResult, then an Rng state at +64
+    c->io_pin.ensure(128);
     c->rng.ensure(5 * sizeof(uint64_t));
     *out = c.release();
   });
@@ -2075,11 +2078,12 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     if (rng_state) {
       if (dev_rng) {
         d_rng = reinterpret_cast<unsigned long long*>(rng_state);
-      } else {
-        cuda_check(cudaMemcpyAsync(ctx->rng.p, rng_state, 40, cudaMemcpyHostToDevice,
-                                   ctx->stream),
+      } else {  // through pinned staging: an asynchronous copy
+        std::memcpy(static_cast<char*>(ctx->io_pin.p) + 64, rng_state, 40);
+        d_rng = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->result.p) + 64);
+        cuda_check(cudaMemcpyAsync(d_rng, static_cast<char*>(ctx->io_pin.p) + 64, 40,
+                                   cudaMemcpyHostToDevice, ctx->stream),
                    "cudaMemcpyAsync rng");
-        d_rng = ctx->rng.as<unsigned long long>();
       }
     }
     KStageResult* d_out = ctx->result.as<KStageResult>();
@@ -2088,18 +2092,34 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
                                    ctx->stream),
                "stage_reduce launch");
-    cuda_check(cudaMemcpyAsync(out, d_out, sizeof(KStageResult), cudaMemcpyDefault, ctx->stream),
-               "cudaMemcpyAsync result");
-    if (scores)
-      cuda_check(cudaMemcpyAsync(scores, p.scores, sizeof(double) * n * nn, cudaMemcpyDefault,
+    // host results: the stage result and the advanced Rng state sit next to
+    // each other on the device (result buffer, rng slot at +64) and come back
+    // in ONE copy into pinned staging; pageable score buffers are staged too,
+    // so nothing blocks before the single synchronize
+    const bool host_out = !is_device_ptr(out);
+    const bool host_scores = scores && !is_device_ptr(scores);
+    const bool pin_scores = host_scores && !is_pinned_host(scores);
+    if (host_out || (rng_state && !dev_rng))
+      cuda_check(cudaMemcpyAsync(ctx->io_pin.p, ctx->result.p, 128, cudaMemcpyDeviceToHost,
                                  ctx->stream),
+                 "cudaMemcpyAsync result");
+    if (!host_out)
+      cuda_check(cudaMemcpyAsync(out, d_out, sizeof(KStageResult), cudaMemcpyDeviceToDevice,
+                                 ctx->stream),
+                 "cudaMemcpyAsync result");
+    const size_t sbytes = sizeof(double) * n * nn;
+    if (pin_scores) ctx->pin_scores.ensure(sbytes);
+    if (scores)
+      cuda_check(cudaMemcpyAsync(pin_scores ? ctx->pin_scores.p : scores, p.scores, sbytes,
+                                 cudaMemcpyDefault, ctx->stream),
                  "cudaMemcpyAsync scores");
-    if (rng_state && !dev_rng)
-      cuda_check(cudaMemcpyAsync(rng_state, d_rng, 40, cudaMemcpyDeviceToHost, ctx->stream),
-                 "cudaMemcpyAsync rng");
-    const bool all_dev = is_device_ptr(out) && (!scores || is_device_ptr(scores)) &&
-                         (!rng_state || dev_rng) && !host_in;
-    if (!all_dev) cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
+    if (host_out || host_scores || (rng_state && !dev_rng) || host_in) {
+      cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
+      if (host_out) std::memcpy(out, ctx->io_pin.p, sizeof(KStageResult));
+      if (rng_state && !dev_rng)
+        std::memcpy(rng_state, static_cast<char*>(ctx->io_pin.p) + 64, 40);
+      if (pin_scores) std::memcpy(scores, ctx->pin_scores.p, sbytes);
+    }
   });
 }
 
