@@ -465,6 +465,17 @@ B3D_API void b3d_rng_seed(uint64_t seed, uint64_t state[5]);
 B3D_API void b3d_rng_split(const uint64_t state[5], uint64_t k0, uint64_t k1, uint64_t k2,
                            uint64_t out[5]);
 
+/* voxel_to_mesh on the device (8f.4, for large grids): the same vertices,
+ * vertex numbering and triangle order as b3d_voxel_to_mesh / the reference's
+ * voxel_to_mesh (geometry.cpp:142-177), built with hash sets and prefix scans
+ * instead of the sequential first-seen walk.  voxels: host or device int32
+ * n x 3 with coordinates in [-2^20+1, 2^20-2]; vertices / triangles: host or
+ * device, capacity 8n x 3 doubles / 12n x 3 uint32.  Synchronous. */
+B3D_API b3d_status b3d_gpu_voxel_to_mesh(b3d_gpu_context* ctx, const int32_t* voxels, uint64_t n,
+                                         double resolution, const double origin[3],
+                                         double* vertices, uint32_t* triangles,
+                                         uint64_t* n_vertices, uint64_t* n_triangles);
+
 /* sample_observation (likelihood.cpp:44-80; replaces the reference's
  * b3d::sample_observation, likelihood.hpp:34-35): a synthetic observed depth
  * image from a rendered one -- |cloud| draws, each an outlier uniform in the

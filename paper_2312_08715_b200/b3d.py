@@ -230,6 +230,8 @@ def lib() -> C.CDLL:
         "b3d_rng_seed": ([u64, vp], None),
         "b3d_rng_split": ([vp, u64, u64, u64, vp], None),
         "b3d_voxel_to_mesh": ([vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)], st),
+        "b3d_gpu_voxel_to_mesh": ([vp, vp, u64, dbl, vp, vp, vp, C.POINTER(u64), C.POINTER(u64)],
+                                  st),
         "b3d_sample_observation": ([C.POINTER(Intrinsics), vp, C.POINTER(Noise), vp, vp], st),
         "b3d_sample_observations": ([C.POINTER(Intrinsics), vp, u64, C.POINTER(Noise), vp, u64,
                                      vp], st),
@@ -638,6 +640,27 @@ class GpuContext:
         _check(self._L.b3d_gpu_upload_mesh(self.h, v.ctypes.data, v.shape[0], t.ctypes.data,
                                            t.shape[0], C.byref(mid)))
         return mid.value
+
+    def voxel_to_mesh(self, voxels, resolution: float, origin) -> tuple:
+        """b3d_gpu_voxel_to_mesh: voxels (n,3) int32 numpy or torch (host/device);
+        returns host numpy (vertices, triangles) for numpy input, device torch
+        tensors for a device tensor."""
+        o = np.ascontiguousarray(origin, dtype=np.float64)
+        nv, nt = C.c_uint64(), C.c_uint64()
+        if isinstance(voxels, np.ndarray):
+            v = np.ascontiguousarray(voxels, dtype=np.int32)
+            n = v.shape[0]
+            verts = np.zeros((8 * n, 3), dtype=np.float64)
+            tris = np.zeros((12 * n, 3), dtype=np.uint32)
+        else:
+            import torch
+            v = voxels.contiguous()
+            n = v.shape[0]
+            verts = torch.empty((8 * n, 3), dtype=torch.float64, device=v.device)
+            tris = torch.empty((12 * n, 3), dtype=torch.int32, device=v.device)
+        _check(self._L.b3d_gpu_voxel_to_mesh(self.h, _ptr(v), n, resolution, o.ctypes.data,
+                                             _ptr(verts), _ptr(tris), C.byref(nv), C.byref(nt)))
+        return verts[: nv.value], tris[: nt.value]
 
     def set_score_peers(self, peer_ptrs, offset: int):
         """Fused all-gather targets (b3d_gpu_set_score_peers); [] turns it off."""

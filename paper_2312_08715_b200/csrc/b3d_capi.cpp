@@ -35,6 +35,12 @@ cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs);
 template <bool kIds, bool kScore, bool kOut>
 size_t static_smem_render_score();
 size_t render_score_staging_bytes(int nt);
+// mesh_build.cu
+cudaError_t voxel_to_mesh_device(const int* d_vox, unsigned long long n, double res,
+                                 const double origin[3], double* d_verts, unsigned* d_tris,
+                                 unsigned long long* n_vertices, unsigned long long* n_triangles,
+                                 cudaStream_t stream);
+
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
@@ -2289,6 +2295,41 @@ b3d_status b3d_voxel_to_mesh(const int32_t* voxels, uint64_t n, double resolutio
         nt += 2;
       }
     }
+    *n_vertices = nv;
+    *n_triangles = nt;
+  });
+}
+
+b3d_status b3d_gpu_voxel_to_mesh(b3d_gpu_context* ctx, const int32_t* voxels, uint64_t n,
+                                 double resolution, const double origin[3], double* vertices,
+                                 uint32_t* triangles, uint64_t* n_vertices,
+                                 uint64_t* n_triangles) {
+  return guarded([&] {
+    check(ctx && voxels && origin && vertices && triangles && n_vertices && n_triangles,
+          "bad arguments");
+    require(n > 0, ErrorCode::invalid, "voxel_to_mesh: empty grid");
+    check(n < (1ull << 26), "voxel_to_mesh: too many voxels");
+    DeviceGuard dg(ctx->device);
+    bool host_in = false;
+    DevBuf vin, vout, tout;
+    const int* d_vox = static_cast<const int*>(stage_in(ctx, vin, voxels, 12 * n, &host_in));
+    const bool host_v = !is_device_ptr(vertices), host_t = !is_device_ptr(triangles);
+    if (host_v) vout.ensure(24 * 8 * n);
+    if (host_t) tout.ensure(12 * 12 * n);
+    double* dv = host_v ? vout.as<double>() : vertices;
+    unsigned* dt = host_t ? tout.as<unsigned>() : reinterpret_cast<unsigned*>(triangles);
+    unsigned long long nv = 0, nt = 0;
+    const cudaError_t e =
+        voxel_to_mesh_device(d_vox, n, resolution, origin, dv, dt, &nv, &nt, ctx->stream);
+    check(e != cudaErrorInvalidValue, "voxel_to_mesh: coordinates outside [-2^20+1, 2^20-2]");
+    cuda_check(e, "voxel_to_mesh_device");
+    if (host_v)
+      cuda_check(cudaMemcpyAsync(vertices, dv, 24 * nv, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync vertices");
+    if (host_t)
+      cuda_check(cudaMemcpyAsync(triangles, dt, 12 * nt, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync triangles");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "voxel_to_mesh");
     *n_vertices = nv;
     *n_triangles = nt;
   });

@@ -911,3 +911,30 @@ def test_fused_score_gather_symmetric_memory_single_rank(gpu_ctx, oracle):
         assert torch.equal(sym, sc)
     finally:
         dist.destroy_process_group()
+
+
+def test_device_voxel_to_mesh_matches_host_walk(gpu_ctx, oracle):
+    """voxel_to_mesh on the device (hash sets + prefix scans) gives the
+    reference walk's vertices, numbering and triangle order (geometry.cpp:142-177):
+    blobs, a sparse random grid, duplicate voxels, negative coordinates, and
+    device-resident input/output."""
+    import torch
+    rng = np.random.Generator(np.random.PCG64(5))
+    grids = [synth.eden_blob(1000, 1), synth.random_walk_blob(3000, 2), synth.eden_blob(20000, 3),
+             rng.integers(-40, 40, size=(5000, 3)).astype(np.int32),
+             np.array([[0, 0, 0], [1, 0, 0], [0, 0, 0], [-7, 3, 1 << 19]], dtype=np.int32)]
+    for g in grids:
+        origin = (-0.0123, 0.5, 0.25)
+        hv, ht = b3d.voxel_to_mesh(g, 0.005, origin)
+        dv, dt = gpu_ctx.voxel_to_mesh(g, 0.005, origin)
+        np.testing.assert_array_equal(dt, ht)
+        np.testing.assert_array_equal(dv.view(np.uint64), hv.view(np.uint64))
+        if g.shape[0] <= 1000:
+            ov, ot = oracle.voxel_to_mesh(g, 0.005, origin)
+            np.testing.assert_array_equal(ot, ht)
+    tv, tt = gpu_ctx.voxel_to_mesh(torch.from_numpy(grids[1]).cuda(), 0.005, (0, 0, 0))
+    hv, ht = b3d.voxel_to_mesh(grids[1], 0.005, (0, 0, 0))
+    np.testing.assert_array_equal(tt.cpu().numpy().astype(np.uint32), ht)
+    np.testing.assert_array_equal(tv.cpu().numpy(), hv)
+    with pytest.raises(b3d.B3DError):
+        gpu_ctx.voxel_to_mesh(np.array([[1 << 21, 0, 0]], dtype=np.int32), 0.005, (0, 0, 0))
