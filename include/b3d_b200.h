@@ -193,7 +193,10 @@ typedef struct b3d_stage_result {
 /* Context: device, stream, uploaded meshes, observation, likelihood config. */
 B3D_API b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out);
 B3D_API void b3d_gpu_context_destroy(b3d_gpu_context* ctx);
-/* Use an external cudaStream_t (NULL = the context's own stream). */
+/* Use an external cudaStream_t (NULL = the context's own stream).  The own
+ * stream is a blocking stream: it is ordered with work on the legacy default
+ * stream (e.g. torch's default stream), so device inputs produced there are
+ * complete before a call reads them, and events recorded there bracket it. */
 B3D_API b3d_status b3d_gpu_set_stream(b3d_gpu_context* ctx, void* cuda_stream);
 B3D_API b3d_status b3d_gpu_synchronize(b3d_gpu_context* ctx);
 

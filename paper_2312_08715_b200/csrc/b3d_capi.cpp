@@ -1192,7 +1192,8 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
     c->device = device;
     cuda_check(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device),
                "cudaDeviceGetAttribute");
-    cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    // blocking: ordered with the legacy default stream (b3d_b200.h)
+    cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamDefault), "cudaStreamCreate");
     c->stream = c->own;
     c->obs_count.ensure(sizeof(int));
     static_assert(sizeof(KStageResult) <= 64, "rng slot at +64");
