@@ -470,6 +470,61 @@ __device__ __forceinline__ void sweep_huge(const KParams& p, Key* const zb, cons
   }
 }
 
+// Triangles with bboxes above kHugeBox pixels are collected per CTA (a table
+// face under a camera hypothesis covers most of the image) and swept after
+// the warps' raster passes by all kThreads threads, one pixel each per step,
+// instead of by the one warp that met them; per-pixel arithmetic as in
+// sweep_huge.  Overflow beyond kMaxHuge stays with the owning warp.
+// Camera-mode kernels only (object hypotheses rarely have huge triangles:
+// the table is in the pre-rendered base scene there).
+constexpr int kMaxHuge = 32;
+template <int kCap>
+struct HugeListT {
+  uint4 tri[kCap];
+  uint2 box[kCap];  // (u_min | v_min << 16, u_max | v_max << 16)
+  // entry count, double-buffered by hypothesis parity: thread 0 resets the
+  // next hypothesis's count while slow warps may still read this one's
+  // (render mode has no barrier after the read)
+  int n[2];
+};
+using HugeList = HugeListT<kMaxHuge>;
+
+template <bool kIds, typename VS, typename Key>
+__device__ __forceinline__ void sweep_huge_cta(const KParams& p, Key* const zb, const Region& rg,
+                                               const VS& vs, uint4 tr, uint2 bx, int tid) {
+  const int u0 = bx.x & 0xffff, v0 = bx.x >> 16;
+  const int bw = (int)(bx.y & 0xffff) - u0 + 1, bh = (int)(bx.y >> 16) - v0 + 1;
+  const double2 A = vs.uv(tr.x), B = vs.uv(tr.y), C = vs.uv(tr.z);
+  const double iza = vs.iz(tr.x), izb = vs.iz(tr.y), izc = vs.iz(tr.z);
+  const SV a{A.x, A.y, 0.0}, b{B.x, B.y, 0.0}, c{C.x, C.y, 0.0};
+  const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+  const double ia2 = __drcp_rn((B.x - A.x) * (C.y - A.y) - (B.y - A.y) * (C.x - A.x));
+  const uint32_t draw = p.draw_base + tr.w;
+  const int n = bw * bh;
+  for (int i = tid; i < n; i += kThreads) {
+    const int row = i / bw;
+    const int pu = u0 + (i - row * bw), pv = v0 + row;
+    const double px = pu, py = pv;
+    const double e_ab = edge_at(A, B, fl & 1, px, py);
+    const double e_bc = edge_at(B, C, fl & 2, px, py);
+    const double e_ca = edge_at(C, A, fl & 4, px, py);
+    if (!edge_covers(e_ab, fl & 8) || !edge_covers(e_bc, fl & 16) || !edge_covers(e_ca, fl & 32))
+      continue;
+    const double inv_z = (e_bc * iza + e_ca * izb + e_ab * izc) * ia2;
+    if (!(inv_z > 0)) continue;
+    const double z = __drcp_rn(inv_z);
+    if (z < p.near_lim || z > p.far_m) continue;
+    const float zf = __double2float_rn(z);
+    if (!(zf < p.far_f)) continue;
+    Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+    if (kIds)
+      zmin((unsigned long long*)cell,
+           ((unsigned long long)__float_as_uint(zf) << 32) | (unsigned long long)draw);
+    else
+      zmin((unsigned int*)cell, __float_as_uint(zf));
+  }
+}
+
 // Pass 2 for the <= 2x2 class: lane l takes queue entry head + l (l < n)
 // and finishes it alone -- the 4 tile pixels' edge values (renderer.cpp:32-34
 // factored into 2 row and 2 column products per edge, bitwise the reference's
@@ -649,7 +704,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h,
-                                         const double* inst_rt) {
+                                         const double* inst_rt, HugeListT<kCam ? kMaxHuge : 1>* hl,
+                                         int par) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Region& rg = hc.rg;
   const double* const R = hc.R;
@@ -772,6 +828,14 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
           }
         }
       }
+      if (kCam && cls == 3) {  // to the CTA's list, swept by all threads after the raster passes
+        const int j = atomicAdd(&hl->n[par], 1);
+        if (j < kMaxHuge) {
+          hl->tri[j] = ent;
+          hl->box[j] = make_uint2(box, box2);
+          cls = -1;
+        }
+      }
       for (uint32_t hb = __ballot_sync(0xffffffffu, cls == 3); hb; hb &= hb - 1)
         sweep_huge<kIds>(p, zb, rg, vs, __ffs(hb) - 1, ent, box, box2, lane);
       const uint32_t b0 = __ballot_sync(0xffffffffu, cls == 0);
@@ -801,6 +865,10 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     if (tail1 > head1) drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, tail1 - head1, lane);
   }
   __syncthreads();
+  if (const int nh = kCam ? min(hl->n[par], kMaxHuge) : 0) {  // uniform after the barrier
+    for (int j = 0; j < nh; ++j) sweep_huge_cta<kIds>(p, zb, rg, vs, hl->tri[j], hl->box[j], tid);
+    __syncthreads();
+  }
 
   // ---- render-many output (sentinel = (float)far, id -1 = background)
   if (kOut) {
@@ -997,6 +1065,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   __shared__ int s_count;
   __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
   __shared__ double s_inst[kCam ? kMaxInst : 1][12];  // camera mode: R | t per instance
+  __shared__ HugeListT<kCam ? kMaxHuge : 1> s_huge;
   using Key = typename KeyT<kIds>::T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1069,6 +1138,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       s_hi_v = INT_MIN;
       s_clip = 0;
       s_count = 0;
+      if (kCam) s_huge.n[kk & 1] = 0;
     }
     __syncthreads();
     HypCtx hc;
@@ -1160,11 +1230,11 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
-                                                    s_red, s_redi, h, &s_inst[0][0]);
+                                                    s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     else
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
-          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0]);
+          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     // No barrier here: before the next hypothesis's first barrier only
     // s_pose (warp 0), the region / count words (thread 0) and s_inst are
     // written, and none of them is read after hyp_body's last barrier; the
