@@ -208,6 +208,24 @@ __device__ __forceinline__ short4 vertex_bbox(const KParams& p, double u, double
 // (bbox <= 2x2 and <= 3x3).  Entry: vertex ids after the orientation swap
 // (renderer.cpp:63-69) + triangle index, and the packed bbox
 // u_min | (bw-1) << 14 | v_min << 16 | (bh-1) << 30.
+// B3D_PHASE_CLOCK=1 (diagnostic builds only, scripts/phase_probe.py): thread 0
+// of CTAs < 256 stamps %globaltimer at the phase boundaries of its latest
+// hypothesis into g_phase (read back by b3d_debug_phase_clock, rs_cam.cu).
+#if B3D_PHASE_CLOCK
+__device__ long long g_phase[256][8];
+#define B3D_PCLK(i)                                                       \
+  do {                                                                    \
+    if (threadIdx.x == 0 && blockIdx.x < 256) {                           \
+      long long t_;                                                       \
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_));              \
+      g_phase[blockIdx.x][i] = t_;                                        \
+    }                                                                     \
+  } while (0)
+#else
+#define B3D_PCLK(i) \
+  do {              \
+  } while (0)
+#endif
 constexpr int kRing = 64;
 struct WarpQ {
   uint4 tri[2][kRing];
@@ -470,37 +488,70 @@ __device__ __forceinline__ void sweep_huge(const KParams& p, Key* const zb, cons
   }
 }
 
-// Triangles with bboxes above kHugeBox pixels are collected per CTA (a table
-// face under a camera hypothesis covers most of the image) and swept after
-// the warps' raster passes by all kThreads threads, one pixel each per step,
-// instead of by the one warp that met them; per-pixel arithmetic as in
-// sweep_huge.  Overflow beyond kMaxHuge stays with the owning warp.
-// Camera-mode kernels only (object hypotheses rarely have huge triangles:
-// the table is in the pre-rendered base scene there).
+// Camera mode: triangles whose bbox exceeds the 3x3 tile classes (table faces
+// under a camera hypothesis cover much of the image) are collected per CTA
+// and rasterized after the warps' passes by all kThreads threads over the
+// concatenation of their bbox pixels -- not by the one lane (per-pixel loop)
+// or warp (sweep) that met them, which serialises a single hypothesis when a
+// small batch leaves one CTA per SM.  Per-pixel arithmetic as sweep_huge
+// (renderer.cpp:78-102).  Overflow beyond kMaxHuge keeps the per-lane / per-
+// warp paths.  Object-mode kernels do not use it (the table is in the
+// pre-rendered base scene there).
 constexpr int kMaxHuge = 32;
 template <int kCap>
 struct HugeListT {
-  uint4 tri[kCap];
-  uint2 box[kCap];  // (u_min | v_min << 16, u_max | v_max << 16)
+  uint4 tri[kCap];      // vertex ids (positive-area order), triangle index
+  uint2 box[kCap];      // (u_min | v_min << 16, u_max | v_max << 16)
+  double ia2[kCap];     // 1 / area2
+  int fl[kCap];         // edge_flags
+  int pre[kCap + 1];    // exclusive prefix of bbox pixel counts
   // entry count, double-buffered by hypothesis parity: thread 0 resets the
   // next hypothesis's count while slow warps may still read this one's
   // (render mode has no barrier after the read)
   int n[2];
 };
-using HugeList = HugeListT<kMaxHuge>;
 
-template <bool kIds, typename VS, typename Key>
+// Warp 0: per-entry edge flags, 1/area2 and the pixel prefix (nh <= 32).
+template <typename VS, int kCap>
+__device__ __forceinline__ void huge_prepare(HugeListT<kCap>* hl, const VS& vs, int nh, int lane) {
+  int area = 0;
+  if (lane < nh) {
+    const uint4 tr = hl->tri[lane];
+    const uint2 bx = hl->box[lane];
+    const double2 A = vs.uv(tr.x), B = vs.uv(tr.y), C = vs.uv(tr.z);
+    const SV a{A.x, A.y, 0.0}, b{B.x, B.y, 0.0}, c{C.x, C.y, 0.0};
+    hl->fl[lane] = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
+    hl->ia2[lane] = __drcp_rn((B.x - A.x) * (C.y - A.y) - (B.y - A.y) * (C.x - A.x));
+    area = ((int)(bx.y & 0xffff) - (int)(bx.x & 0xffff) + 1) *
+           ((int)(bx.y >> 16) - (int)(bx.x >> 16) + 1);
+    if (area > kHugeBox) area = 0;  // swept one triangle at a time (sweep_huge_cta)
+  }
+  int incl = area;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  if (lane < nh) hl->pre[lane + 1] = incl;
+  if (lane == 0) hl->pre[0] = 0;
+}
+
+// One huge list entry, all threads: bbox pixels strided by kThreads.
+template <bool kIds, typename VS, typename Key, int kCap>
 __device__ __forceinline__ void sweep_huge_cta(const KParams& p, Key* const zb, const Region& rg,
-                                               const VS& vs, uint4 tr, uint2 bx, int tid) {
+                                               const VS& vs, const HugeListT<kCap>* hl, int j,
+                                               int tid) {
+  const uint4 tr = hl->tri[j];
+  const uint2 bx = hl->box[j];
   const int u0 = bx.x & 0xffff, v0 = bx.x >> 16;
   const int bw = (int)(bx.y & 0xffff) - u0 + 1, bh = (int)(bx.y >> 16) - v0 + 1;
+  const int n = bw * bh;
+  if (n <= kHugeBox) return;  // in the flattened sweep
   const double2 A = vs.uv(tr.x), B = vs.uv(tr.y), C = vs.uv(tr.z);
   const double iza = vs.iz(tr.x), izb = vs.iz(tr.y), izc = vs.iz(tr.z);
-  const SV a{A.x, A.y, 0.0}, b{B.x, B.y, 0.0}, c{C.x, C.y, 0.0};
-  const int fl = edge_flags(a, b, 0) | edge_flags(b, c, 1) | edge_flags(c, a, 2);
-  const double ia2 = __drcp_rn((B.x - A.x) * (C.y - A.y) - (B.y - A.y) * (C.x - A.x));
+  const int fl = hl->fl[j];
+  const double ia2 = hl->ia2[j];
   const uint32_t draw = p.draw_base + tr.w;
-  const int n = bw * bh;
   for (int i = tid; i < n; i += kThreads) {
     const int row = i / bw;
     const int pu = u0 + (i - row * bw), pv = v0 + row;
@@ -520,6 +571,48 @@ __device__ __forceinline__ void sweep_huge_cta(const KParams& p, Key* const zb, 
     if (kIds)
       zmin((unsigned long long*)cell,
            ((unsigned long long)__float_as_uint(zf) << 32) | (unsigned long long)draw);
+    else
+      zmin((unsigned int*)cell, __float_as_uint(zf));
+  }
+}
+
+// All entries with bboxes <= kHugeBox pixels at once: thread i takes pixel
+// i of the concatenated bboxes (entry found by binary search of the prefix).
+template <bool kIds, typename VS, typename Key, int kCap>
+__device__ __forceinline__ void sweep_list_cta(const KParams& p, Key* const zb, const Region& rg,
+                                               const VS& vs, const HugeListT<kCap>* hl, int nh,
+                                               int tid) {
+  const int total = hl->pre[nh];
+  for (int i = tid; i < total; i += kThreads) {
+    int j = 0;  // last entry whose prefix <= i
+#pragma unroll
+    for (int step = 16; step > 0; step >>= 1)
+      if (j + step < nh && hl->pre[j + step] <= i) j += step;
+    const uint4 tr = hl->tri[j];
+    const uint2 bx = hl->box[j];
+    const int u0 = bx.x & 0xffff, v0 = bx.x >> 16;
+    const int bw = (int)(bx.y & 0xffff) - u0 + 1;
+    const int k = i - hl->pre[j];
+    const int row = k / bw;
+    const int pu = u0 + (k - row * bw), pv = v0 + row;
+    const double px = pu, py = pv;
+    const int fl = hl->fl[j];
+    const double2 A = vs.uv(tr.x), B = vs.uv(tr.y), C = vs.uv(tr.z);
+    const double e_ab = edge_at(A, B, fl & 1, px, py);
+    const double e_bc = edge_at(B, C, fl & 2, px, py);
+    const double e_ca = edge_at(C, A, fl & 4, px, py);
+    if (!edge_covers(e_ab, fl & 8) || !edge_covers(e_bc, fl & 16) || !edge_covers(e_ca, fl & 32))
+      continue;
+    const double inv_z = (e_bc * vs.iz(tr.x) + e_ca * vs.iz(tr.y) + e_ab * vs.iz(tr.z)) * hl->ia2[j];
+    if (!(inv_z > 0)) continue;
+    const double z = __drcp_rn(inv_z);
+    if (z < p.near_lim || z > p.far_m) continue;
+    const float zf = __double2float_rn(z);
+    if (!(zf < p.far_f)) continue;
+    Key* cell = zb + (pv - rg.oy) * rg.rw + (pu - rg.ox);
+    if (kIds)
+      zmin((unsigned long long*)cell,
+           ((unsigned long long)__float_as_uint(zf) << 32) | (unsigned long long)(p.draw_base + tr.w));
     else
       zmin((unsigned int*)cell, __float_as_uint(zf));
   }
@@ -746,6 +839,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     s_seg[7] = cum;
   }
   __syncthreads();
+  B3D_PCLK(3);
 
   // ---- C: raster, in two passes per 32-triangle chunk of each warp.
   // Pass 1, lane = triangle (mesh order): integer bbox reject, signed area,
@@ -814,26 +908,30 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                 ent = make_uint4(ia, ib, ic, (uint32_t)ti);
                 box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
                       (uint32_t)(bh - 1) << 30;
-              } else if (bw * bh <= kHugeBox) {  // the reference's per-pixel loop
-                raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz(ia)},
-                                     SV{PB.x, PB.y, vs.iz(ib)}, SV{PC.x, PC.y, vs.iz(ic)},
-                                     u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
-              } else {  // huge bbox: swept by the whole warp below
-                cls = 3;
-                ent = make_uint4(ia, ib, ic, (uint32_t)ti);
-                box = (uint32_t)u_min | (uint32_t)v_min << 16;
-                box2 = (uint32_t)u_max | (uint32_t)v_max << 16;
+              } else {
+                int j = kMaxHuge;
+                if (kCam) {  // to the CTA's list (camera mode)
+                  j = atomicAdd(&hl->n[par], 1);
+                  if (j < kMaxHuge) {
+                    hl->tri[j] = make_uint4(ia, ib, ic, (uint32_t)ti);
+                    hl->box[j] = make_uint2((uint32_t)u_min | (uint32_t)v_min << 16,
+                                            (uint32_t)u_max | (uint32_t)v_max << 16);
+                  }
+                }
+                if (j < kMaxHuge) {
+                } else if (bw * bh <= kHugeBox) {  // the reference's per-pixel loop
+                  raster_tri_box<kIds>(p, zb, rg, SV{PA.x, PA.y, vs.iz(ia)},
+                                       SV{PB.x, PB.y, vs.iz(ib)}, SV{PC.x, PC.y, vs.iz(ic)},
+                                       u_min, u_max, v_min, v_max, p.draw_base + (uint32_t)ti);
+                } else {  // huge bbox: swept by the whole warp below
+                  cls = 3;
+                  ent = make_uint4(ia, ib, ic, (uint32_t)ti);
+                  box = (uint32_t)u_min | (uint32_t)v_min << 16;
+                  box2 = (uint32_t)u_max | (uint32_t)v_max << 16;
+                }
               }
             }
           }
-        }
-      }
-      if (kCam && cls == 3) {  // to the CTA's list, swept by all threads after the raster passes
-        const int j = atomicAdd(&hl->n[par], 1);
-        if (j < kMaxHuge) {
-          hl->tri[j] = ent;
-          hl->box[j] = make_uint2(box, box2);
-          cls = -1;
         }
       }
       for (uint32_t hb = __ballot_sync(0xffffffffu, cls == 3); hb; hb &= hb - 1)
@@ -865,10 +963,15 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     if (tail1 > head1) drain_queue<3, kIds>(p, zb, rg, vs, q.tri[1], q.box[1], head1, tail1 - head1, lane);
   }
   __syncthreads();
+  B3D_PCLK(4);
   if (const int nh = kCam ? min(hl->n[par], kMaxHuge) : 0) {  // uniform after the barrier
-    for (int j = 0; j < nh; ++j) sweep_huge_cta<kIds>(p, zb, rg, vs, hl->tri[j], hl->box[j], tid);
+    if (warp == 0) huge_prepare(hl, vs, nh, lane);
+    __syncthreads();
+    sweep_list_cta<kIds>(p, zb, rg, vs, hl, nh, tid);
+    for (int j = 0; j < nh; ++j) sweep_huge_cta<kIds>(p, zb, rg, vs, hl, j, tid);
     __syncthreads();
   }
+  B3D_PCLK(5);
 
   // ---- render-many output (sentinel = (float)far, id -1 = background)
   if (kOut) {
@@ -915,6 +1018,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       cnt = warp_sum_i(cnt);
       if (lane == 0 && cnt) atomicAdd(s_count, cnt);
       __syncthreads();
+      B3D_PCLK(6);
     }
     const int rend_count = *s_count + p.base_valid;
     // |y| = 0 (never with a non-empty base image): the reference throws
@@ -1090,6 +1194,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   // stream serialization) be scheduled into SMs this grid leaves idle; it
   // waits for this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
+  B3D_PCLK(0);
 #if B3D_L2_PREFETCH
   // Shared read-only inputs (mesh, sorted triangles, observation) into L2 in
   // one parallel burst spread over all CTAs, instead of every CTA's first
@@ -1141,6 +1246,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       if (kCam) s_huge.n[kk & 1] = 0;
     }
     __syncthreads();
+    B3D_PCLK(1);
     HypCtx hc;
     hc.R = s_pose[kk & 31];  // broadcast reads from shared memory
     hc.t = hc.R + 9;
@@ -1204,6 +1310,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       if (clip) s_clip = 1;
     }
     __syncthreads();
+    B3D_PCLK(2);
     Region& rg = hc.rg;
     hc.clip = s_clip != 0;
     if (hc.clip) {
@@ -1235,6 +1342,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
           s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
+    B3D_PCLK(7);
     // No barrier here: before the next hypothesis's first barrier only
     // s_pose (warp 0), the region / count words (thread 0) and s_inst are
     // written, and none of them is read after hyp_body's last barrier; the

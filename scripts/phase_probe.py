@@ -12,7 +12,8 @@ from paper_2312_08715_b200 import b3d, configs  # noqa: E402
 
 ctx = b3d.GpuContext(0)
 L = ctx._L
-names = ["prologue+A", "B vertices", "zinit", "raster", "D1 count", "D2 window", "D3 reduce"]
+names = ["prologue+A", "B vertices", "zinit", "raster (warps)", "huge (CTA)", "D1 count",
+         "D2+D3 score"]
 
 
 def rc(k, inst, cams):
