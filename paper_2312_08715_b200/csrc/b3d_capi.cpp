@@ -35,6 +35,12 @@ cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs);
 template <bool kIds, bool kScore, bool kOut>
 size_t static_smem_render_score();
 size_t render_score_staging_bytes(int nt);
+// track.cu
+cudaError_t launch_cam_lattice(const double* tab, int n_tab, int off, int ppd, const int* state,
+                               KPose* cams, unsigned char* valid, const KPose& fallback,
+                               cudaStream_t st);
+cudaError_t launch_cam_argmax(const double* scores, const unsigned char* valid, int ppd,
+                              int* state, cudaStream_t st);
 // mesh_build.cu
 cudaError_t voxel_to_mesh_device(const int* d_vox, unsigned long long n, double res,
                                  const double origin[3], double* d_verts, unsigned* d_tris,
@@ -352,6 +358,8 @@ struct b3d_gpu_context {
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
   PinnedBuf pin_cams, pin_scores;  // track_camera / enumerate_poses staging
   PinnedBuf io_pin;                 // stage result + Rng state (enumerate_poses)
+  PinnedBuf trk_tab_pin, trk_state_pin;  // track_camera device chain: tables, picks
+  DevBuf trk_tab, trk_state, trk_valid;
   // fixed scene (compose_render)
   bool has_base = false;
   DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
@@ -1706,6 +1714,80 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
                    "obs_prepare launch");
         ctx->has_obs = true;
         ++ctx->obs_version;
+      }
+      if (s.beam_width == 1) {
+        // the frame's stages chained on the device (track.cu): every lattice
+        // value the frame can visit and its sin / cos from this libm, one
+        // upload, ppd^3 poses / score / argmax per stage, one read-back
+        const Sph c0 = beam.front().c;
+        const int S = s.refine_stages;
+        std::vector<int> off(S + 2, 0);
+        for (int st = 0, w = ppd; st <= S; ++st, w *= ppd) off[st + 1] = off[st] + w;
+        const int n_tab = off[S + 1];
+        ctx->trk_tab_pin.ensure(sizeof(double) * 7 * n_tab);
+        double* tab = ctx->trk_tab_pin.as<double>();
+        double* td = tab;
+        double* taz = tab + n_tab;
+        double* talt = tab + 2 * n_tab;
+        double pe = s.pos_extent, ae = s.angle_extent;
+        for (int st = 0; st <= S; ++st) {
+          const int parents = st == 0 ? 1 : off[st] - off[st - 1];
+          for (int q = 0; q < parents; ++q) {
+            const double cd = st == 0 ? c0.d : td[off[st - 1] + q];
+            const double caz = st == 0 ? c0.az : taz[off[st - 1] + q];
+            const double calt = st == 0 ? c0.alt : talt[off[st - 1] + q];
+            for (int i = 0; i < ppd; ++i) {
+              const int o = off[st] + q * ppd + i;
+              td[o] = lattice_at(cd, pe, ppd, i);
+              taz[o] = lattice_at(caz, ae, ppd, i);
+              talt[o] = lattice_at(calt, ae, ppd, i);
+            }
+          }
+          pe /= s.refine_factor;
+          ae /= s.refine_factor;
+        }
+        for (int o = 0; o < n_tab; ++o) {  // generative.cpp:40-43's trig, host libm
+          tab[3 * n_tab + o] = std::cos(talt[o]);
+          tab[4 * n_tab + o] = std::sin(talt[o]);
+          tab[5 * n_tab + o] = std::cos(taz[o]);
+          tab[6 * n_tab + o] = std::sin(taz[o]);
+        }
+        ctx->trk_tab.ensure(sizeof(double) * 7 * n_tab);
+        ctx->trk_state.ensure(8 * sizeof(int));
+        ctx->trk_valid.ensure(n_grid);
+        ctx->trk_state_pin.ensure(8 * sizeof(int));
+        cuda_check(cudaMemcpyAsync(ctx->trk_tab.p, tab, sizeof(double) * 7 * n_tab,
+                                   cudaMemcpyHostToDevice, ctx->stream),
+                   "cudaMemcpyAsync track tables");
+        cuda_check(cudaMemsetAsync(ctx->trk_state.p, 0, 8 * sizeof(int), ctx->stream),
+                   "cudaMemsetAsync track state");
+        const KPose fallback = camera_from_spherical(c0.d, c0.az, c0.alt);
+        int* dstate = ctx->trk_state.as<int>();
+        for (int st = 0; st <= S; ++st) {
+          cuda_check(launch_cam_lattice(ctx->trk_tab.as<double>(), n_tab, off[st], ppd, dstate,
+                                        ctx->c2f_centers.as<KPose>(),
+                                        ctx->trk_valid.as<unsigned char>(), fallback,
+                                        ctx->stream),
+                     "cam_lattice launch");
+          launch_score_cameras(ctx, ctx->c2f_centers.as<KPose>(), (long long)n_grid,
+                               ctx->c2f_scores.as<double>(), nullptr);
+          cuda_check(launch_cam_argmax(ctx->c2f_scores.as<double>(),
+                                       ctx->trk_valid.as<unsigned char>(), ppd, dstate,
+                                       ctx->stream),
+                     "cam_argmax launch");
+        }
+        int* hs = ctx->trk_state_pin.as<int>();
+        cuda_check(cudaMemcpyAsync(hs, dstate, 8 * sizeof(int), cudaMemcpyDeviceToHost,
+                                   ctx->stream),
+                   "cudaMemcpyAsync track state");
+        cuda_check(cudaStreamSynchronize(ctx->stream), "track_camera frame");
+        require(hs[4] == 0, ErrorCode::numeric, "track_camera: every candidate pose scored -inf");
+        const Sph top{td[off[S] + hs[0]], taz[off[S] + hs[1]], talt[off[S] + hs[2]]};
+        beam = {{top, 0.0}};
+        const KPose cp = camera_from_spherical(top.d, top.az, top.alt);
+        out_poses[f] = b3d_pose{cp.qw, cp.qx, cp.qy, cp.qz, cp.tx, cp.ty, cp.tz};
+        close_frame(f);
+        continue;
       }
       std::vector<Cand> next;
       for (const Cand& seed : beam) {
