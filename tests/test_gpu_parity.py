@@ -599,6 +599,30 @@ def test_track_camera_matches_oracle(gpu_ctx, oracle):
         assert np.linalg.norm(est[f][4:] - cams[f][4:]) < 0.03
 
 
+@pytest.mark.parametrize("ppd,stages,beam", [(4, 1, 1), (3, 3, 1), (5, 2, 2)])
+def test_track_camera_search_variants_match_oracle(gpu_ctx, oracle, ppd, stages, beam):
+    """Other TrackSearch settings: the device stage chain (beam 1; even
+    lattices, deeper refinement) and the host beam path (beam 2) pick the
+    oracle's lattice points (a differing pick must tie within the tolerance)."""
+    seq = _orbit(oracle, 25, ref_frames=True)
+    _camera_scene(gpu_ctx, seq)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    cams = [oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+            for a in seq["azimuths"][:4]]
+    frames = configs.orbit_frames(seq, cams)
+    search = b3d.TrackSearch.default(points_per_dim=ppd, refine_stages=stages, beam_width=beam)
+    est, _ = gpu_ctx.track_camera(frames, cams[0], search)
+    log = []
+    ref = oracle.track_camera(frames, seq["k"], seq["instances"], cams[0], seq["noise"],
+                              seq["sigma_max"], seq["window"], points_per_dim=ppd,
+                              refine_stages=stages, beam_width=beam, stage_log=log)
+    for f in range(4):
+        if not np.array_equal(est[f], ref[f]):
+            _, _, grid, scores = [e for e in log if e[0] == f][-1]
+            s = np.sort(np.array(scores))
+            assert s[-1] - s[-2] <= SCORE_RTOL * abs(s[-1])
+
+
 def test_orbit_frames_equal_the_reference(gpu_ctx, oracle):
     """generate_orbit_sequence (tracking.cpp:174-206) as the bench builds it:
     device camera renders + the product's sample_observation on split streams
