@@ -221,10 +221,16 @@ __device__ long long g_phase[256][8];
       g_phase[blockIdx.x][i] = t_;                                        \
     }                                                                     \
   } while (0)
+// one reader per translation unit (each holds its own g_phase)
+#define B3D_PHASE_READER(NAME)                                                       \
+  extern "C" __attribute__((visibility("default"))) int NAME(long long* out) {       \
+    return (int)cudaMemcpyFromSymbol(out, b3d200::g_phase, sizeof(b3d200::g_phase)); \
+  }
 #else
 #define B3D_PCLK(i) \
   do {              \
   } while (0)
+#define B3D_PHASE_READER(NAME)
 #endif
 constexpr int kRing = 64;
 struct WarpQ {
