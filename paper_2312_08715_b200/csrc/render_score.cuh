@@ -501,8 +501,9 @@ __device__ __forceinline__ void sweep_huge(const KParams& p, Key* const zb, cons
 // or warp (sweep) that met them, which serialises a single hypothesis when a
 // small batch leaves one CTA per SM.  Per-pixel arithmetic as sweep_huge
 // (renderer.cpp:78-102).  Overflow beyond kMaxHuge keeps the per-lane / per-
-// warp paths.  Object-mode kernels do not use it (the table is in the
-// pre-rendered base scene there).
+// warp paths.  Render-mode kernels use it too (a base scene or b3d_render is
+// one hypothesis in one CTA); object-mode score kernels do not (the table is
+// in the pre-rendered base scene there).
 constexpr int kMaxHuge = 32;
 template <int kCap>
 struct HugeListT {
@@ -803,7 +804,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                                          int* s_count, double* s_coef,
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h,
-                                         const double* inst_rt, HugeListT<kCam ? kMaxHuge : 1>* hl,
+                                         const double* inst_rt, HugeListT<(kCam || !kScore) ? kMaxHuge : 1>* hl,
                                          int par) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Region& rg = hc.rg;
@@ -916,7 +917,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                       (uint32_t)(bh - 1) << 30;
               } else {
                 int j = kMaxHuge;
-                if (kCam) {  // to the CTA's list (camera mode)
+                if (kCam || !kScore) {  // to the CTA's list (camera / render mode)
                   j = atomicAdd(&hl->n[par], 1);
                   if (j < kMaxHuge) {
                     hl->tri[j] = make_uint4(ia, ib, ic, (uint32_t)ti);
@@ -970,7 +971,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   }
   __syncthreads();
   B3D_PCLK(4);
-  if (const int nh = kCam ? min(hl->n[par], kMaxHuge) : 0) {  // uniform after the barrier
+  if (const int nh = (kCam || !kScore) ? min(hl->n[par], kMaxHuge) : 0) {  // uniform after the barrier
     if (warp == 0) huge_prepare(hl, vs, nh, lane);
     __syncthreads();
     sweep_list_cta<kIds>(p, zb, rg, vs, hl, nh, tid);
@@ -1175,7 +1176,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   __shared__ int s_count;
   __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
   __shared__ double s_inst[kCam ? kMaxInst : 1][12];  // camera mode: R | t per instance
-  __shared__ HugeListT<kCam ? kMaxHuge : 1> s_huge;
+  __shared__ HugeListT<(kCam || !kScore) ? kMaxHuge : 1> s_huge;
   using Key = typename KeyT<kIds>::T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1249,7 +1250,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       s_hi_v = INT_MIN;
       s_clip = 0;
       s_count = 0;
-      if (kCam) s_huge.n[kk & 1] = 0;
+      if (kCam || !kScore) s_huge.n[kk & 1] = 0;
     }
     __syncthreads();
     B3D_PCLK(1);
