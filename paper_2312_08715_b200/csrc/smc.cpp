@@ -16,8 +16,13 @@
 //   * the final scene_target_logpdf of each particle, batched the same way.
 // Scores carry the fp32-term likelihood (<= 1e-4 relative of the reference,
 // DESIGN.md 5.1); everything else is the reference's arithmetic.
+#include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <limits>
 #include <map>
 #include <stdexcept>
@@ -45,6 +50,37 @@ void ok(b3d_status s) {
 }
 void need(bool c, b3d_status s, const char* m) {
   if (!c) throw Fail(s, m);
+}
+
+// The per-particle host work (cell subdivision, child poses, priors,
+// normalisation, draws from each particle's own stream) runs on all host
+// threads, as the reference's parallel_for does (parallel.hpp:19-54); the
+// result does not depend on the thread count.
+template <class F>
+void parallel_for(size_t n, F&& f) {
+  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+  const size_t nth = std::min<size_t>(hw, (n + 31) / 32);
+  if (nth <= 1) {
+    for (size_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::exception_ptr err;
+  std::mutex mu;
+  auto work = [&] {
+    try {
+      for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
+    } catch (...) {
+      std::lock_guard<std::mutex> lk(mu);
+      if (!err) err = std::current_exception();
+      next = n;
+    }
+  };
+  std::vector<std::thread> pool;
+  for (size_t t = 1; t < nth; ++t) pool.emplace_back(work);
+  work();
+  for (auto& th : pool) th.join();
+  if (err) std::rethrow_exception(err);
 }
 
 // rng.cpp: xoshiro256** seeded by splitmix64, split via mix()
@@ -304,21 +340,23 @@ struct Smc {
                             const Stage0* shared) {
     const size_t P = stream.size();
     std::vector<Prop> props(P);
-    for (size_t i = 0; i < P; ++i) {
-      Stage0 local;
-      const Stage0* s0 = shared;
-      if (!s0) {
-        local = build_stage0(partial[i]);
-        s0 = &local;
+    auto pick0 = [&](size_t i, const Stage0* s0) {
+      const size_t k = sample(s0->scores, stream[i]);
+      props[i].log_q = std::log(s0->scores[k]);
+      props[i].current = s0->cells[k];
+    };
+    if (shared) {
+      parallel_for(P, [&](size_t i) { pick0(i, shared); });
+    } else {
+      for (size_t i = 0; i < P; ++i) {  // a device stage 0 per particle
+        const Stage0 local = build_stage0(partial[i]);
+        pick0(i, &local);
       }
-      const size_t pick0 = sample(s0->scores, stream[i]);
-      props[i].log_q = std::log(s0->scores[pick0]);
-      props[i].current = s0->cells[pick0];
     }
     for (uint32_t r = 0; r < cfg.n_refine; ++r) {
       const b3d_schedule_stage& st = cfg.refine[r];
       std::vector<std::vector<Cell>> cells(P);
-      for (size_t i = 0; i < P; ++i) cells[i] = subdivide(props[i].current, st);
+      parallel_for(P, [&](size_t i) { cells[i] = subdivide(props[i].current, st); });
       if (cells[0].size() == 1) {
         for (size_t i = 0; i < P; ++i) props[i].current = cells[i][0];
         continue;
@@ -327,8 +365,12 @@ struct Smc {
       // particle's noise: the cells inherit noise_index)
       std::vector<std::vector<double>> lt(P);
       auto fill = [&](const std::vector<size_t>& members) {
-        std::vector<b3d_pose> poses;
-        for (size_t i : members) {
+        std::vector<size_t> offs(members.size() + 1, 0);
+        for (size_t m = 0; m < members.size(); ++m)
+          offs[m + 1] = offs[m] + cells[members[m]].size();
+        std::vector<b3d_pose> poses(offs.back());
+        parallel_for(members.size(), [&](size_t m) {
+          const size_t i = members[m];
           b3d_contact_cells cc{};
           cc.grid = contact(props[i].current.object_id, props[i].current.face);
           cc.grid.count[0] = st.n_dx;
@@ -341,15 +383,15 @@ struct Smc {
           cc.dy_hi = cur.dy.hi;
           cc.dtheta_lo = cur.dtheta.lo;
           cc.dtheta_hi = cur.dtheta.hi;
-          const size_t off = poses.size();
-          poses.resize(off + cells[i].size());
-          ok(b3d_contact_cells_poses(&cc, poses.data() + off));
-        }
+          ok(b3d_contact_cells_poses(&cc, poses.data() + offs[m]));
+        });
         const Cell& lead = props[members[0]].current;
         const std::vector<double> lik = score_poses(lead.object_id, lead.noise_index, poses);
-        size_t k = 0;
-        for (size_t i : members) {
+        parallel_for(members.size(), [&](size_t m) {
+          const size_t i = members[m];
           const double base_prior = prior_sum(partial[i]);
+          size_t k = offs[m];
+          lt[i].reserve(cells[i].size());
           for (const Cell& c : cells[i]) {
             const Child cc{c.object_id, c.face, c.dx.center(), c.dy.center(), c.dtheta.center()};
             const double cp = child_prior(cc);
@@ -358,7 +400,7 @@ struct Smc {
                                 ? base_prior + cp + l
                                 : kNegInf);
           }
-        }
+        });
       };
       if (shared) {  // one base scene: batch by (object, noise entry)
         set_base(partial[0]);
@@ -372,13 +414,13 @@ struct Smc {
           fill({i});
         }
       }
-      for (size_t i = 0; i < P; ++i) {
+      parallel_for(P, [&](size_t i) {
         bool az;
         const std::vector<double> sc = normalise(lt[i], az);
         const size_t pick = sample(sc, stream[i]);
         props[i].log_q += std::log(sc[pick]);
         props[i].current = cells[i][pick];
-      }
+      });
     }
     for (size_t i = 0; i < P; ++i) {
       Prop& pr = props[i];
@@ -400,8 +442,8 @@ struct Smc {
     const size_t P = props.size();
     std::vector<double> out(P, kNegInf);
     auto fill = [&](const std::vector<size_t>& members) {
-      std::vector<b3d_pose> poses;
-      for (size_t i : members) poses.push_back(child_pose(props[i].child));
+      std::vector<b3d_pose> poses(members.size());
+      parallel_for(members.size(), [&](size_t m) { poses[m] = child_pose(props[members[m]].child); });
       const std::vector<double> lik =
           score_poses(props[members[0]].child.object_id, props[members[0]].current.noise_index,
                       poses);
