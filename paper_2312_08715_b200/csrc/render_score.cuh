@@ -262,7 +262,7 @@ __device__ __forceinline__ uint32_t tile_edge_mask(double2 a, double2 b, bool ca
   for (int j = 0; j < K; ++j)
 #pragma unroll
     for (int i = 0; i < K; ++i)
-      if (A[j] - B[i] > thr) m |= 1u << (3 * j + i);
+      if (A[j] - B[i] > thr) m |= 1u << (K * j + i);
   return m;
 }
 
@@ -449,6 +449,7 @@ constexpr int kWarps = kThreads / 32;
 // ids already in positive-area order), one pixel per lane per step, with the
 // reference's per-pixel arithmetic (renderer.cpp:78-102).
 constexpr int kHugeBox = 64;
+
 
 template <bool kIds, typename VS, typename Key>
 __device__ __forceinline__ void sweep_huge(const KParams& p, Key* const zb, const Region& rg,
@@ -718,9 +719,10 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
     const int u0 = box & 0x3fff, v0 = (box >> 16) & 0x3fff;
     const int bw = ((box >> 14) & 3) + 1, bh = (int)(box >> 30) + 1;
     const uint32_t colm = (1u << bw) - 1u;
-    uint32_t valid = colm;
-    if (bh > 1) valid |= colm << 3;
-    if (K > 2 && bh > 2) valid |= colm << 6;
+    uint32_t valid = colm;  // bit K*j + i = pixel (u0 + i, v0 + j)
+#pragma unroll
+    for (int j = 1; j < K; ++j)
+      if (bh > j) valid |= colm << (K * j);
     cov = valid & tile_edge_mask<K>(PA, PB, fl & 1, fl & 8, u0, v0) &
           tile_edge_mask<K>(PB, PC, fl & 2, fl & 16, u0, v0) &
           tile_edge_mask<K>(PC, PA, fl & 4, fl & 32, u0, v0);
@@ -757,7 +759,7 @@ __device__ __forceinline__ void drain_queue(const KParams& p, Key* const zb, con
     if (item < total) {
       for (int k = item - st; k > 0; --k) m &= m - 1;  // k-th covered pixel
       const int bit = __ffs(m) - 1;
-      const int pu = (int)(bx & 0x3fff) + bit % 3, pv = (int)((bx >> 16) & 0x3fff) + bit / 3;
+      const int pu = (int)(bx & 0x3fff) + bit % K, pv = (int)((bx >> 16) & 0x3fff) + bit / K;
       const double2 A = vs.uv(ia), B = vs.uv(ib), C = vs.uv(ic);
       const double px = pu, py = pv;
       const double e_ab = edge_at(A, B, flo & 1, px, py);
@@ -791,14 +793,15 @@ struct HypCtx {
   Region rg;
   bool empty_region, clip;
   int rpx;
+  int q1;  // largest bbox side of the tile classes (2 or 3)
 };
 
 // Work of one hypothesis after the vertex phase: z-buffer init, raster,
 // render-many output and/or likelihood.  Instantiated twice per kernel so
 // that the z-buffer accesses compile to shared-memory instructions (kZS) or
 // global ones (overflow scratch), never to generic ones.
-template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, bool kCam, typename VS,
-          typename Key>
+template <bool kIds, bool kScore, bool kOut, int kWin, bool kS1, bool kCam, bool kQA,
+          typename VS, typename Key>
 __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key* const zb,
                                          const VS& vs, WarpQ* const wq, int* const s_seg,
                                          int* s_count, double* s_coef,
@@ -910,7 +913,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                 area2 = -area2;
               }
               const int bw = u_max - u_min + 1, bh = v_max - v_min + 1;
-              if (bw <= 3 && bh <= 3) {
+              if (bw <= (kQA ? hc.q1 : 3) && bh <= (kQA ? hc.q1 : 3)) {
                 cls = (bw <= 2 && bh <= 2) ? 0 : 1;
                 ent = make_uint4(ia, ib, ic, (uint32_t)ti);
                 box = (uint32_t)u_min | (uint32_t)(bw - 1) << 14 | (uint32_t)v_min << 16 |
@@ -1332,6 +1335,16 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       rg.v1 = min(s_hi_v, p.H - 1);
     }
     hc.empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
+    // 3x3 bboxes: the tile class with a dealt fragment pass pays off for
+    // small projected triangles; when the mesh's faces span ~2.7+ px (region
+    // area > 0.4 nt; a voxel blob's ratio grows with the squared projected
+    // voxel size: cfg2 0.24 at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane
+    // loop is faster (cfg3/cfg4 +12 %; forcing it on cfg2 costs 12 %).
+    // Meshes whose vertex cache fits on chip are small and keep the class.
+    hc.q1 = (!kVS && !hc.empty_region &&
+             5ll * (rg.u1 - rg.u0 + 1) * (rg.v1 - rg.v0 + 1) > 2ll * p.nt)
+                ? 2
+                : 3;
     if (hc.empty_region) {  // keep one valid (unused) pixel so indexing stays sane
       rg.u1 = rg.u0 = min(max(rg.u0, 0), p.W - 1);
       rg.v1 = rg.v0 = min(max(rg.v0, 0), p.H - 1);
@@ -1343,10 +1356,10 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
                                                     s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     else
-      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam>(
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
           s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     B3D_PCLK(7);
