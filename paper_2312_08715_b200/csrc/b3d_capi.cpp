@@ -225,6 +225,7 @@ struct Mesh {
   DevBuf tris_s, plane_off, plane_end;
   int cls_start[8] = {0};
   int plane_begin[8] = {0};
+  double radius = 0;  // max |vertex| (model frame): bounds the projected region
 };
 
 // Score-mode triangle order (b3d_kernels.cuh KParams::tris_s).  A triangle
@@ -460,9 +461,43 @@ struct LaunchPlan {
   int zcap = 0;
 };
 
+// Bound on a hypothesis's region (pixels incl. the likelihood halo) when its
+// model-to-world pose lies within `spread` (m) of `center`: the mesh fits in
+// a sphere of radius R, whose projection at depth z has half-width
+// <= f R / (z - R).  0 = no useful bound (object may reach the near plane).
+double sq3(const double v[3]) { return v[0] * v[0] + (v[1] * v[1] + v[2] * v[2]); }
+double cam_z(const b3d_gpu_context* ctx, double tx, double ty, double tz) {
+  const KPose& c = ctx->w2c;  // camera-frame depth of a model-to-world translation
+  return 2 * (c.qx * c.qz - c.qw * c.qy) * tx + 2 * (c.qy * c.qz + c.qw * c.qx) * ty +
+         (1 - 2 * (c.qx * c.qx + c.qy * c.qy)) * tz + c.tz;
+}
+size_t region_hint_z(const b3d_gpu_context* ctx, const Mesh& m, double zc, int window) {
+  const double zmin = zc - m.radius;
+  if (!(zmin > std::max(ctx->k.near_m, 1e-6)) || !(m.radius > 0)) return 0;
+  const int pad = 2 * std::max(window, 0);
+  const double su = 2.0 * ctx->k.fx * m.radius / zmin + 3 + 2 * pad;
+  const double sv = 2.0 * ctx->k.fy * m.radius / zmin + 3 + 2 * pad;
+  const double px = 1.15 * su * sv;
+  return px < 1e9 ? (size_t)px : 0;
+}
+size_t region_hint(const b3d_gpu_context* ctx, const Mesh& m, const KPose& center, double spread,
+                   int window) {
+  return region_hint_z(ctx, m, cam_z(ctx, center.tx, center.ty, center.tz) - spread, window);
+}
+// explicit host poses: the nearest of up to 4,096 evenly spaced samples
+// (hypotheses nearer still just take the scratch z-buffer)
+size_t region_hint_poses(const b3d_gpu_context* ctx, const Mesh& m, const b3d_pose* poses,
+                         uint64_t n, int window) {
+  double zc = std::numeric_limits<double>::infinity();
+  const uint64_t step = std::max<uint64_t>(1, n / 4096);
+  for (uint64_t i = 0; i < n; i += step)
+    zc = std::min(zc, cam_z(ctx, poses[i].tx, poses[i].ty, poses[i].tz));
+  return std::isfinite(zc) ? region_hint_z(ctx, m, zc, window) : 0;
+}
+
 template <bool kIds, bool kScore, bool kOut>
 LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int window = -1,
-                       bool full_frame = false) {
+                       bool full_frame = false, size_t zhint = 0) {
   LaunchPlan lp;
   const size_t key = kIds ? 8 : 4;
   const size_t npx = (size_t)ctx->k.width * ctx->k.height;
@@ -512,6 +547,16 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
   }
   size_t zcap = (budget - 32ull * lp.vcap - stage) / key;
   if (zcap > padded + 64) zcap = padded + 64;
+  static const long long zcap_env = [] {
+    const char* e = std::getenv("B3D_PLAN_ZCAP");  // A/B only: cap the z-buffer keys
+    return e ? std::atoll(e) : 0ll;
+  }();
+  if (zcap_env > 0 && lp.vcap == 0 && !full_frame && zcap > (size_t)zcap_env) zcap = zcap_env;
+  // a z-buffer sized to the batch's projected regions rather than to the
+  // whole budget: with the vertex cache in scratch, the shared memory not
+  // requested is L1 for it (cfg2 +8 %); regions beyond it take the scratch
+  // z-buffer, so the hint only moves speed, never results
+  if (zhint > 0 && lp.vcap == 0 && !full_frame) zcap = std::min(zcap, std::max<size_t>(zhint, 2048));
   zcap &= ~size_t(7);  // the vertex cache after the z-buffer stays 32-byte aligned
   lp.zcap = (int)zcap;
   lp.smem = 32ull * lp.vcap + stage + key * zcap;
@@ -936,7 +981,14 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
     }
   }
   attach_base(ctx, p);
-  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n);
+  size_t zhint = 0;
+  if (poses && host_in) {
+    zhint = region_hint_poses(ctx, m, poses, n, ctx->lik.window);
+  } else if (!poses && !contact) {
+    zhint = region_hint(ctx, m, p.grid.center,
+                        std::sqrt(sq3(grid->extent)), ctx->lik.window);
+  }
+  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n, -1, false, zhint);
   p.zscratch = ctx->zscratch.as<unsigned long long>();
   p.vscratch = ctx->vscratch.as<double>();
   p.vcap = lp.vcap;
@@ -965,7 +1017,6 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
 constexpr double kHalfPi = 1.5707963267948966;
 
 // Eigen 3-vector reductions split as a0 + (a1 + a2) (redux unroller halves)
-double sq3(const double v[3]) { return v[0] * v[0] + (v[1] * v[1] + v[2] * v[2]); }
 
 void normalize3(double v[3]) {
   const double n2 = sq3(v);
@@ -1304,6 +1355,8 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
     m->nv = (int)n_vertices;
     m->nt = (int)n_triangles;
     m->cull = closed_mesh_cull_sign(vertices, triangles, n_triangles);
+    for (uint64_t i = 0; i < n_vertices; ++i)
+      m->radius = std::max(m->radius, std::sqrt(sq3(vertices + 3 * i)));
     build_score_order(vertices, triangles, n_triangles, m->cull, *m);
     m->verts.ensure(24 * n_vertices);
     m->tris.ensure(16 * n_triangles);
@@ -1971,7 +2024,10 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
       }
     }
     KStageResult* d_res = ctx->c2f_results.as<KStageResult>();
-    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n_max, w_max);
+    double spread = 0;  // the chained centres stay within the summed extents
+    for (uint32_t s = 0; s < n_stages; ++s) spread += std::sqrt(sq3(stages[s].extent));
+    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n_max, w_max, false,
+                                                    region_hint(ctx, m, c0, spread, w_max));
     for (uint32_t s = 0; s < n_stages; ++s) {
       const b3d_stage_spec& g = stages[s];
       KParams p = base_params(ctx, m);

@@ -57,3 +57,16 @@ P[:, 4:] += rng.uniform(-0.015, 0.015, size=(8192, 3))
 for _ in range(3):
     ctx.score_poses(mid, P)
 report("cfg4", "b3d_debug_phase_clock_w2", 296)
+
+# cfg2: 3,000-voxel blob at 200x200, stage windows 3 and 1
+w2 = configs.cfg2(render_fn, b3d.voxel_to_mesh, seed=0)
+ctx.set_camera(b3d.Intrinsics(*w2.k.as_tuple()))
+mid = ctx.upload_mesh(w2.vertices, w2.triangles)
+ctx.set_observation(w2.observed)
+P = np.repeat(w2.gt_pose[None], 32768, axis=0)
+P[:, 4:] += rng.uniform(-0.02, 0.02, size=(32768, 3))
+for win, reader in ((3, "b3d_debug_phase_clock_w3"), (1, "b3d_debug_phase_clock_w1")):
+    ctx.set_likelihood([(0.01, 0.01)], 0.1, win)
+    for _ in range(2):
+        ctx.score_poses(mid, P)
+    report(f"cfg2 window {win}", reader, 296)
