@@ -962,3 +962,75 @@ def test_device_voxel_to_mesh_matches_host_walk(gpu_ctx, oracle):
     np.testing.assert_array_equal(tv.cpu().numpy(), hv)
     with pytest.raises(b3d.B3DError):
         gpu_ctx.voxel_to_mesh(np.array([[1 << 21, 0, 0]], dtype=np.int32), 0.005, (0, 0, 0))
+
+
+def test_cfg5_full_size_shards_and_spot_parity(gpu_ctx, oracle):
+    """BASELINE configs[4] at full size (1,048,576 hypotheses, 480x640, a
+    10-object base scene): scoring the grid in four shards gives the single
+    call's scores bitwise (the multi-GPU partition), and the global argmax plus
+    15 random hypotheses score within 1e-4 of the oracle's composed render."""
+    import torch
+    from helpers import b3d_intr
+    rs = lambda k, cam, inst: oracle.render(k, inst, camera=cam)
+    w = configs.cfg5(rs, oracle.voxel_to_mesh, oracle.box_mesh, oracle.contact_to_pose)
+    gpu_ctx.set_camera(b3d_intr(w["k"]), w["camera"])
+    tv, tt = w["table"]
+    mids = [gpu_ctx.upload_mesh(tv, tt)] + [gpu_ctx.upload_mesh(l[0], l[1]) for l in w["library"]]
+    n_placed = len(w["base_poses"]) - 1
+    gpu_ctx.set_base_scene([mids[0]] + [mids[1 + i] for i in range(n_placed)], w["base_poses"])
+    gpu_ctx.set_observation(w["observed"])
+    gpu_ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    d_rot = torch.from_numpy(w["rotations"]).cuda()
+    grid = gpu_ctx.make_grid(w["gt"], w["extent"], w["count"], d_rot, b3d.GRID_PRODUCT)
+    n = w["n_hyp"]
+    mid = mids[1 + w["target"]]
+    full = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
+    gpu_ctx.score_grid_range(mid, grid, 0, n, full, None)
+    parts = torch.zeros_like(full)
+    bounds = [0, n // 4, n // 2, 3 * n // 4 + 17, n]
+    for lo, hi in zip(bounds[:-1], bounds[1:]):
+        gpu_ctx.score_grid_range(mid, grid, lo, hi - lo, parts[lo:hi], None)
+    torch.cuda.synchronize()
+    assert torch.equal(full, parts)
+    s = full[:, 0].cpu().numpy()
+    rng = np.random.Generator(np.random.PCG64(55))
+    pick = np.concatenate([[int(np.argmax(s))], rng.integers(0, n, size=15)])
+    poses = configs.grid_poses(w["gt"], w["extent"], w["count"], w["rotations"], 0)[pick]
+    base = [(tv, tt, w["base_poses"][0])] + [
+        (w["library"][i][0], w["library"][i][1], w["base_poses"][1 + i]) for i in range(n_placed)]
+    base_depth = oracle.render(w["k"], base, camera=w["camera"])
+    lib_t = w["library"][w["target"]]
+    s_orc, st = oracle.score_poses(w["k"], w["observed"], lib_t[0], lib_t[1], poses, w["noise"],
+                                   w["sigma_max"], w["window"], base_depth=base_depth,
+                                   camera=w["camera"])
+    assert (st == 0).all()
+    assert rel_err(s[pick], s_orc[:, 0]).max() <= SCORE_RTOL
+    gpu_ctx.set_base_scene([], [])
+
+
+def test_cfg3_full_size_contact_grid_spot_parity(gpu_ctx, oracle):
+    """BASELINE configs[2] at full size (16 x 16 x 512 = 131,072 contact
+    hypotheses over the base scene): the argmax and 31 random cells score
+    within 1e-4 of the oracle, and the argmax lies at the true contact."""
+    w = _cfg3(oracle, counts=(16, 16, 512))
+    mids, base_inst = _setup_cfg3(gpu_ctx, oracle, w)
+    gpu_ctx.set_observation(w["observed"])
+    gpu_ctx.set_likelihood(w["noise"], w["sigma_max"], w["window"])
+    o = w["objects"][w["target"]]
+    g = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, (16, 16, 512))
+    s_gpu, st_gpu = gpu_ctx.score_contact_grid(mids[1 + w["target"]], g)
+    assert s_gpu.shape[0] == 131072
+    rng = np.random.Generator(np.random.PCG64(33))
+    best = int(np.argmax(s_gpu[:, 0]))
+    pick = np.concatenate([[best], rng.integers(0, s_gpu.shape[0], size=31)])
+    poses = b3d.contact_grid_poses(g)[pick]
+    base = oracle.render(w["k"], base_inst, camera=w["camera"])
+    s_orc, st_orc = oracle.score_poses(w["k"], w["observed"], o[0], o[1], poses, w["noise"],
+                                       w["sigma_max"], w["window"], base_depth=base,
+                                       camera=w["camera"])
+    assert (st_orc == st_gpu[pick]).all()
+    ok = st_orc == 0
+    assert rel_err(s_gpu[pick][ok, 0], s_orc[ok, 0]).max() <= SCORE_RTOL
+    truth = w["poses"][w["target"]]
+    assert np.linalg.norm(poses[0][4:6] - truth[4:6]) < 0.03  # within about one grid cell
+    gpu_ctx.set_base_scene([], [])
