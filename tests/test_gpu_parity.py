@@ -1034,3 +1034,41 @@ def test_cfg3_full_size_contact_grid_spot_parity(gpu_ctx, oracle):
     truth = w["poses"][w["target"]]
     assert np.linalg.norm(poses[0][4:6] - truth[4:6]) < 0.03  # within about one grid cell
     gpu_ctx.set_base_scene([], [])
+
+
+def test_cfg2_full_size_chain_spot_parity_and_determinism(gpu_ctx, oracle):
+    """BASELINE configs[1] at full size (5 stages x 32,768 hypotheses, 200x200,
+    3,000 voxels): the device chain is deterministic (two runs bitwise
+    equal), each stage's sample / argmax are the reference semantics over that
+    stage's device scores, each next centre is the drawn grid pose, and the
+    drawn pose plus 7 random ones per stage score within 1e-4 of the oracle."""
+    from helpers import b3d_intr
+    rf = lambda k, v, t, p: oracle.render(k, [(v, t, p)])
+    w = configs.cfg2(rf, oracle.voxel_to_mesh, seed=0)
+    assert w.stages[0]["count"] == (16, 16, 16) and len(w.stages) == 5
+    gpu_ctx.set_camera(b3d_intr(w.k))
+    mid = gpu_ctx.upload_mesh(w.vertices, w.triangles)
+    gpu_ctx.set_observation(w.observed)
+    gpu_ctx.set_likelihood([w.stages[0]["noise"]], w.sigma_max, 1)
+    st = b3d.rng_seed(99)
+    res, centers = gpu_ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)
+    st2 = b3d.rng_seed(99)
+    res2, centers2 = gpu_ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st2)
+    np.testing.assert_array_equal(np.array(centers), np.array(centers2))
+    assert [r.sample for r in res] == [r.sample for r in res2]
+    st_o = oracle.rng_seed(99)
+    rng = np.random.Generator(np.random.PCG64(8))
+    for s, g in enumerate(w.stages):
+        gpu_ctx.set_likelihood([g["noise"]], w.sigma_max, g["window"])
+        grid = gpu_ctx.make_grid(centers[s], g["extent"], g["count"], g["rotations"], 0)
+        s_gpu, _ = gpu_ctx.score_grid(mid, grid)
+        probs, _ = oracle.normalize(s_gpu[:, 0])
+        pick = oracle.sample_categorical(probs, st_o)
+        assert res[s].sample == pick and res[s].argmax == oracle.argmax(s_gpu[:, 0])
+        poses = configs.grid_poses(centers[s], g["extent"], g["count"], g["rotations"], 0)
+        np.testing.assert_array_equal(centers[s + 1], poses[pick])
+        idx = np.concatenate([[pick], rng.integers(0, poses.shape[0], size=7)])
+        s_orc, _ = oracle.score_poses(w.k, w.observed, w.vertices, w.triangles, poses[idx],
+                                      [g["noise"]], w.sigma_max, g["window"])
+        assert rel_err(s_gpu[idx, 0], s_orc[:, 0]).max() <= SCORE_RTOL
+    np.testing.assert_array_equal(st, st_o)
