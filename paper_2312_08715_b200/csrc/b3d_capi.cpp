@@ -1768,7 +1768,14 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
         ctx->has_obs = true;
         ++ctx->obs_version;
       }
-      if (s.beam_width == 1) {
+      // tables of ppd + ppd^2 + ... + ppd^(S+1) values per axis: the device
+      // chain is used while that stays small (always at the defaults: 155)
+      double tab_n = 0;
+      for (int st = 0, w = 1; st <= s.refine_stages && tab_n <= (1 << 20); ++st) {
+        w = (int)std::min<double>((double)w * ppd, 1 << 21);
+        tab_n += w;
+      }
+      if (s.beam_width == 1 && tab_n <= (1 << 20)) {
         // the frame's stages chained on the device (track.cu): every lattice
         // value the frame can visit and its sin / cos from this libm, one
         // upload, ppd^3 poses / score / argmax per stage, one read-back
