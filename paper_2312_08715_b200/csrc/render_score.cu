@@ -14,6 +14,9 @@ B3D_RS_SCORE_KERNELS(extern, 2)
 B3D_RS_SCORE_KERNELS(extern, 3)
 B3D_RS_SCORE_KERNELS(extern, -1)
 B3D_RS_CAM_KERNELS(extern)
+B3D_RS_SCORE_KERNELS2(extern, 1, true)
+B3D_RS_SCORE_KERNELS2(extern, 2, true)
+B3D_RS_SCORE_KERNELS2(extern, 4, true)
 
 // ---------------------------------------------------------------- base scene
 // Padded depth-bit image of the base scene (halo of `pad` background pixels)
@@ -129,9 +132,14 @@ template <bool kIds, bool kScore, bool kOut>
 static auto pick_kernel(bool vs, int window, int n_noise, bool cam = false) {
   if constexpr (kScore && !kIds) {
     const bool s1 = n_noise == 1;
-    if (cam)  // camera mode: generic window loop
-      return s1 ? pick_vs<kIds, kScore, kOut, -1, true, true>(vs)
-                : pick_vs<kIds, kScore, kOut, -1, false, true>(vs);
+    if (cam) {  // camera mode: the bench-tracking windows (1, 2, 4), else generic
+      switch (window) {
+        case 1: return s1 ? pick_vs<kIds, kScore, kOut, 1, true, true>(vs) : pick_vs<kIds, kScore, kOut, 1, false, true>(vs);
+        case 2: return s1 ? pick_vs<kIds, kScore, kOut, 2, true, true>(vs) : pick_vs<kIds, kScore, kOut, 2, false, true>(vs);
+        case 4: return s1 ? pick_vs<kIds, kScore, kOut, 4, true, true>(vs) : pick_vs<kIds, kScore, kOut, 4, false, true>(vs);
+        default: return s1 ? pick_vs<kIds, kScore, kOut, -1, true, true>(vs) : pick_vs<kIds, kScore, kOut, -1, false, true>(vs);
+      }
+    }
     switch (window) {
       case 0: return s1 ? pick_vs<kIds, kScore, kOut, 0, true>(vs) : pick_vs<kIds, kScore, kOut, 0, false>(vs);
       case 1: return s1 ? pick_vs<kIds, kScore, kOut, 1, true>(vs) : pick_vs<kIds, kScore, kOut, 1, false>(vs);

@@ -7,7 +7,7 @@ make -s -j8 -C paper_2312_08715_b200/csrc >/dev/null 2>&1 || exit 1
 T=$(mktemp -d)
 C=paper_2312_08715_b200/csrc
 FL="-gencode arch=compute_100a,code=sm_100a -O3 -lineinfo --fmad=false -std=c++17 -Xptxas -v -Xcompiler -fPIC,-fvisibility=hidden,-O2 -Iinclude -I$C"
-for f in render_score rs_score_w0 rs_score_w1 rs_score_w2 rs_score_w3 rs_score_wx rs_cam; do
+for f in render_score rs_score_w0 rs_score_w1 rs_score_w2 rs_score_w3 rs_score_wx rs_cam rs_cam_w1 rs_cam_w2 rs_cam_w4; do
   /usr/local/cuda/bin/nvcc $FL "$@" -c $C/$f.cu -o $T/$f.o 2> $T/$f.log &
 done
 wait
