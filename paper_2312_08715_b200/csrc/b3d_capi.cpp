@@ -50,13 +50,14 @@ cudaError_t voxel_to_mesh_device(const int* d_vox, unsigned long long n, double 
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
+size_t stage_scratch_bytes(long long n);  // stage.cu: grid-wide reduction partials
 cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
                                 unsigned long long* rng_state, KStageResult* out,
-                                double* probs, cudaStream_t st);
+                                double* probs, cudaStream_t st, void* scratch);
 cudaError_t launch_sample_many(const double* x, long long n, int stride, int col,
                                const KStageResult* r, unsigned long long* rng_state,
                                int n_samples, double* u_buf, unsigned long long* out,
-                               cudaStream_t st);
+                               cudaStream_t st, void* scratch);
 cudaError_t launch_select_center(const KGrid& g, const KStageResult* r, int use_sample,
                                  KPose* center_out, cudaStream_t st);
 cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_keys,
@@ -360,6 +361,7 @@ struct b3d_gpu_context {
   PinnedBuf pin_cams, pin_scores;  // track_camera / enumerate_poses staging
   PinnedBuf io_pin;                 // stage result + Rng state (enumerate_poses)
   PinnedBuf trk_tab_pin, trk_state_pin;  // track_camera device chain: tables, picks
+  DevBuf stage_part;                     // grid-wide stage reduction partials
   DevBuf trk_tab, trk_state, trk_valid;
   // fixed scene (compose_render)
   bool has_base = false;
@@ -422,6 +424,13 @@ struct DeviceGuard {
     if (prev >= 0 && cur != prev) cudaSetDevice(prev);
   }
 };
+
+void* stage_scratch(b3d_gpu_context* ctx, long long n) {
+  const size_t b = stage_scratch_bytes(n);
+  if (!b) return nullptr;
+  ctx->stage_part.ensure(b);
+  return ctx->stage_part.p;
+}
 
 void require_ready(const b3d_gpu_context* ctx, bool need_obs, bool need_lik) {
   check(ctx != nullptr, "bad arguments");
@@ -998,7 +1007,7 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
              "render_score launch");
   if (stage_out)
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, stage_rng, stage_out, nullptr,
-                                   ctx->stream),
+                                   ctx->stream, stage_scratch(ctx, (long long)n)),
                "stage_reduce launch");
   bool sync = host_in;
   if (!dev_scores) {
@@ -1959,7 +1968,7 @@ b3d_status b3d_gpu_stage_reduce(b3d_gpu_context* ctx, const double* scores, uint
       }
     }
     cuda_check(launch_stage_reduce(d_scores, (long long)n, (int)stride, (int)col, d_rng, d_out,
-                                   d_probs, ctx->stream),
+                                   d_probs, ctx->stream, stage_scratch(ctx, (long long)n)),
                "stage_reduce launch");
     bool sync = host_in;
     if (!dev_out) {
@@ -2061,7 +2070,8 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
                  "render_score launch");
       const bool sample = g.select == B3D_SELECT_SAMPLE;
       cuda_check(launch_stage_reduce(p.scores, (long long)n[s], 1, 0, sample ? d_rng : nullptr,
-                                     d_res + s, nullptr, ctx->stream),
+                                     d_res + s, nullptr, ctx->stream,
+                                     stage_scratch(ctx, (long long)n[s])),
                  "stage_reduce launch");
       cuda_check(launch_select_center(p.grid, d_res + s, sample ? 1 : 0, d_centers + s + 1,
                                       ctx->stream),
@@ -2242,7 +2252,7 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
                "render_score launch");
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
-                                   ctx->stream),
+                                   ctx->stream, stage_scratch(ctx, (long long)n)),
                "stage_reduce launch");
     // host results: the stage result and the advanced Rng state sit next to
     // each other on the device (result buffer, rng slot at +64) and come back
@@ -2328,12 +2338,13 @@ b3d_status b3d_gpu_sample_many(b3d_gpu_context* ctx, const double* scores, uint6
     unsigned long long* d_samples = dev_samples ? reinterpret_cast<unsigned long long*>(samples)
                                                 : ctx->out_stage2.as<unsigned long long>();
     // reduction without a draw, then the draws
+    void* scr = stage_scratch(ctx, (long long)n);
     cuda_check(launch_stage_reduce(d_scores, (long long)n, (int)stride, (int)col, nullptr, d_out,
-                                   nullptr, ctx->stream),
+                                   nullptr, ctx->stream, scr),
                "stage_reduce launch");
     cuda_check(launch_sample_many(d_scores, (long long)n, (int)stride, (int)col, d_out, d_rng,
                                   (int)n_samples, ctx->out_stage.as<double>(), d_samples,
-                                  ctx->stream),
+                                  ctx->stream, scr),
                "sample_many launch");
     cuda_check(cudaMemcpyAsync(&d_out->sample, d_samples, 8, cudaMemcpyDeviceToDevice,
                                ctx->stream),

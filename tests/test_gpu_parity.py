@@ -162,7 +162,8 @@ def test_empty_render_status(gpu_ctx, oracle):
 
 def test_stage_reduce_matches_oracle(gpu_ctx, oracle):
     rng = np.random.Generator(np.random.PCG64(9))
-    for n in (1, 7, 1024, 32768, 100003):
+    # sizes above 16,384 take the grid-wide reduction (stage.cu)
+    for n in (1, 7, 1024, 16384, 16385, 32768, 100003, 1 << 20):
         x = rng.normal(-2.0e4, 30.0, size=n)
         if n > 10:
             x[n // 3] = x.max() + 5.0
@@ -182,12 +183,26 @@ def test_stage_reduce_matches_oracle(gpu_ctx, oracle):
 
 
 def test_stage_reduce_all_neg_inf(gpu_ctx, oracle):
-    x = np.full(1000, -np.inf)
-    st_g, st_o = b3d.rng_seed(5), oracle.rng_seed(5)
-    r = gpu_ctx.stage_reduce(x, rng_state=st_g)
-    probs_o, all_zero = oracle.normalize(x)
-    assert r.all_zero and all_zero and r.argmax == 0
-    assert r.sample == oracle.sample_categorical(probs_o, st_o)
+    for n in (1000, 50000):  # single-CTA and grid-wide paths
+        x = np.full(n, -np.inf)
+        st_g, st_o = b3d.rng_seed(5), oracle.rng_seed(5)
+        r = gpu_ctx.stage_reduce(x, rng_state=st_g)
+        probs_o, all_zero = oracle.normalize(x)
+        assert r.all_zero and all_zero and r.argmax == 0
+        assert r.sample == oracle.sample_categorical(probs_o, st_o)
+
+
+def test_stage_reduce_nonfinite_entries(gpu_ctx, oracle):
+    """NaN never wins the argmax and is counted (with +-inf) as non-finite,
+    on both reduction paths."""
+    rng = np.random.Generator(np.random.PCG64(4))
+    for n in (3000, 70000):
+        x = rng.normal(0.0, 1.0, size=n)
+        x[[3, n // 2, n - 1]] = np.nan
+        x[[7, n // 3]] = -np.inf
+        r = gpu_ctx.stage_reduce(x)
+        finite = np.where(np.isfinite(x), x, -np.inf)
+        assert r.argmax == int(np.argmax(finite)) and r.n_nonfinite == 5
 
 
 def test_log_likelihood_c_abi(oracle):
@@ -360,7 +375,7 @@ def test_sample_many_matches_sequential_draws(gpu_ctx, oracle):
     """1,000 posterior draws (cfg5's final step): each equals
     sample_categorical with the next uniform() of the same Rng stream."""
     rng = np.random.Generator(np.random.PCG64(21))
-    for n in (5, 4096, 200003):
+    for n in (5, 4096, 200003, 1 << 20):
         x = rng.normal(0.0, 3.0, size=n)
         st_g = b3d.rng_seed(77 + n)
         samples, r = gpu_ctx.sample_many(x, 1000, st_g)
