@@ -265,14 +265,24 @@ def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_fram
         rot = [float(np.degrees(2.0 * np.arccos(min(1.0, abs(float(np.dot(est[i][:4],
                                                                           cams[i][:4])))))))
                for i in range(n_frames)]
+        # the paper's Table 1 budget: 2,048 hypotheses per frame
+        # as an 8^3 lattice x 4 stages of the same search
+        wide = b3d.TrackSearch.default(points_per_dim=8, refine_stages=3)
+        ctx.track_camera(frames[:3], cams[0], wide)
+        est2, ms2 = ctx.track_camera(frames, cams[0], wide)
+        pos2 = [100.0 * float(np.linalg.norm(est2[i][4:] - cams[i][4:])) for i in range(n_frames)]
         out.append({"resolution": res, "fps": n_frames / (float(ms.sum()) * 1e-3),
                     "ms_per_frame_mean": float(ms[1:].mean()),
                     "mean_position_error_cm": statistics.mean(pos),
                     "mean_orientation_error_deg": statistics.mean(rot),
-                    "window": seq["window"]})
+                    "window": seq["window"],
+                    "fps_2048_hypotheses_per_frame": n_frames / (float(ms2.sum()) * 1e-3),
+                    "mean_position_error_cm_2048": statistics.mean(pos2)})
     return {"workload": "bench-tracking orbit (Table 1 analog): table + 1,000-voxel blob, "
                         f"{n_frames} frames (the reference's sample_observation noise model, "
                         "p_outlier 0.02, sigma 2 mm), 125-point spherical lattice x 3 stages "
+                        "(the reference harness's search; fps_2048_hypotheses_per_frame: 512 x 4, "
+                        "the paper's Table 1 budget) "
                         "per frame, "
                         "camera-mode multi-instance render+score on device",
             "frames": n_frames, "per_resolution": out}
