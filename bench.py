@@ -765,8 +765,13 @@ def main():
                        "score_gather": gather},
             "gpu_launches": 2 * args.steps,  # render_score + stage_reduce per step
             "e2e": {"value": e2e_value, "unit": UNIT,
-                    "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 8 * n_all + 40),
-                    "d2h_bytes_per_step": int(h_scores.nbytes + h_status.nbytes + 64 + 40),
+                    # N = 1: observation + poses + Rng state in; scores + stage result +
+                    # Rng state out (b3d_gpu_enumerate_poses).  N > 1 adds the status
+                    # bytes out and the gathered scores back in for the host reduction.
+                    "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 40
+                                              + (8 * n_all if world > 1 else 0)),
+                    "d2h_bytes_per_step": int(h_scores.nbytes + 64 + 40
+                                              + (h_status.nbytes if world > 1 else 0)),
                     "ms_per_step": e2e_total / args.steps},
             "clocks": clk,
             "roofline": roof,
