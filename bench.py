@@ -678,9 +678,9 @@ def main():
     h_rng = b3d.rng_seed(7)
 
     def e2e_step():
+        if world == 1:  # one boundary call: upload observation + poses, score, reduce, read back
+            return ctx.enumerate_observed(mid, h_obs, h_poses, rng_state=h_rng, scores=h_scores)
         ctx.set_observation(h_obs)  # pinned: stream-ordered upload
-        if world == 1:  # one boundary call: upload poses, score, reduce, read back
-            return ctx.enumerate_poses(mid, h_poses, rng_state=h_rng, scores=h_scores)
         ctx.score_poses(mid, h_poses, h_scores, h_status)
         t = torch.from_numpy(h_scores).to(dev)
         g = torch.empty((n_all, 1), dtype=torch.float64, device=dev)

@@ -347,6 +347,13 @@ B3D_API b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id
                                            const b3d_pose* poses, uint64_t n,
                                            uint64_t* rng_state, b3d_stage_result* out,
                                            double* scores);
+/* One frame of the hot loop (score_cells after ObservationCache::build,
+ * inference.cpp:261-353): b3d_gpu_set_observation(depth) followed by
+ * b3d_gpu_enumerate_poses in one call (one boundary crossing). */
+B3D_API b3d_status b3d_gpu_enumerate_observed(b3d_gpu_context* ctx, int32_t mesh_id,
+                                              const float* depth, const b3d_pose* poses,
+                                              uint64_t n, uint64_t* rng_state,
+                                              b3d_stage_result* out, double* scores);
 
 /* score-many over a device pose grid followed by the stage reduction of
  * scores[:, 0] (argmax, logsumexp, one draw with rng_state if non-NULL) in

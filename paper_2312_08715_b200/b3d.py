@@ -223,6 +223,7 @@ def lib() -> C.CDLL:
         "b3d_gpu_set_base_scene": ([vp, vp, vp, u32], st),
         "b3d_gpu_sample_many": ([vp, vp, u64, u32, u32, vp, u32, vp, vp], st),
         "b3d_gpu_enumerate_poses": ([vp, i32, vp, u64, vp, vp, vp], st),
+        "b3d_gpu_enumerate_observed": ([vp, i32, vp, vp, u64, vp, vp, vp], st),
         "b3d_gpu_enumerate_grid": ([vp, i32, C.POINTER(PoseGrid), vp, vp, vp], st),
         "b3d_gpu_score_grid_range": ([vp, i32, C.POINTER(PoseGrid), u64, u64, vp, vp], st),
         "b3d_gpu_score_contact_grid": ([vp, i32, C.POINTER(ContactGrid), vp, vp], st),
@@ -903,6 +904,21 @@ class GpuContext:
         _check(self._L.b3d_gpu_score_grid_range(self.h, mesh, C.byref(grid), first, n,
                                                 _ptr(scores), _ptr(status)))
         return scores, status
+
+    def enumerate_observed(self, mesh: int, depth, poses, rng_state=None,
+                           scores=None) -> "StageOut":
+        """b3d_gpu_enumerate_observed: set_observation + enumerate_poses in one call."""
+        if isinstance(depth, np.ndarray):
+            depth = np.ascontiguousarray(depth, dtype=np.float32)
+        if isinstance(poses, np.ndarray):
+            poses = np.ascontiguousarray(poses, dtype=np.float64)
+        res = StageResult()
+        _check(self._L.b3d_gpu_enumerate_observed(self.h, mesh, _ptr(depth), _ptr(poses),
+                                                  poses.shape[0], _ptr(rng_state),
+                                                  C.addressof(res), _ptr(scores)))
+        return StageOut(res.argmax, res.sample, res.max_score, res.logsumexp, res.total,
+                        res.sample_logp, bool(res.all_zero), res.n_nonfinite,
+                        bool(res.sample_fallback))
 
     def enumerate_poses(self, mesh: int, poses, rng_state=None, scores=None) -> "StageOut":
         """b3d_gpu_enumerate_poses: score-many + stage reduce in one call."""

@@ -2285,6 +2285,14 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
   });
 }
 
+b3d_status b3d_gpu_enumerate_observed(b3d_gpu_context* ctx, int32_t mesh_id, const float* depth,
+                                      const b3d_pose* poses, uint64_t n, uint64_t* rng_state,
+                                      b3d_stage_result* out, double* scores) {
+  const b3d_status st = b3d_gpu_set_observation(ctx, depth);
+  if (st != B3D_OK) return st;
+  return b3d_gpu_enumerate_poses(ctx, mesh_id, poses, n, rng_state, out, scores);
+}
+
 b3d_status b3d_gpu_enumerate_grid(b3d_gpu_context* ctx, int32_t mesh_id,
                                   const b3d_pose_grid* grid, uint64_t* rng_state,
                                   b3d_stage_result* out, double* scores) {

@@ -439,6 +439,13 @@ def test_enumerate_poses_one_call(gpu_ctx, oracle):
     np.testing.assert_array_equal(scores, s2)
     assert (r1.argmax, r1.sample, r1.logsumexp) == (r2.argmax, r2.sample, r2.logsumexp)
     np.testing.assert_array_equal(st1, st2)
+    # observation + enumeration in one boundary call (the bench's e2e step)
+    st3 = b3d.rng_seed(3)
+    obs = torch.from_numpy(np.ascontiguousarray(w.observed)).pin_memory().numpy()
+    scores3 = np.zeros_like(scores)
+    r3 = gpu_ctx.enumerate_observed(mid, obs, poses, rng_state=st3, scores=scores3)
+    np.testing.assert_array_equal(scores3, s2)
+    assert (r3.argmax, r3.sample) == (r2.argmax, r2.sample)
 
 
 def test_base_scene_with_near_clipping_and_scratch(gpu_ctx, oracle):
