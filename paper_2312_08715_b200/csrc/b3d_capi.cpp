@@ -51,6 +51,7 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
 size_t stage_scratch_bytes(long long n);  // stage.cu: grid-wide reduction partials
+size_t obs_count_ints();                 // render_score.cu: obs_prepare count buffer
 cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
                                 unsigned long long* rng_state, KStageResult* out,
                                 double* probs, cudaStream_t st, void* scratch);
@@ -1263,7 +1264,8 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
     // blocking: ordered with the legacy default stream (b3d_b200.h)
     cuda_check(cudaStreamCreateWithFlags(&c->own, cudaStreamDefault), "cudaStreamCreate");
     c->stream = c->own;
-    c->obs_count.ensure(sizeof(int));
+    c->obs_count.ensure(sizeof(int) * obs_count_ints());
+    cuda_check(cudaMemset(c->obs_count.p, 0, sizeof(int) * obs_count_ints()), "cudaMemset");
     static_assert(sizeof(KStageResult) <= 64, "rng slot at +64");
     c->result.ensure(128);  // KStageResult, then an Rng state at +64
     c->io_pin.ensure(128);
@@ -2225,7 +2227,10 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
         stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
     p.n_hyp = (long long)n;
     const int nn = ctx->lik.n_noise;
-    ctx->c2f_scores.ensure(sizeof(double) * n * nn);
+    // device layout: scores (n x n_noise), then the stage result (64 B) and
+    // the Rng state (40 B), so one read-back returns everything
+    const size_t sbytes = sizeof(double) * n * nn;
+    ctx->c2f_scores.ensure(sbytes + 128);
     p.scores = ctx->c2f_scores.as<double>();
     p.status = nullptr;
     attach_base(ctx, p);
@@ -2235,52 +2240,48 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     p.vcap = lp.vcap;
     p.zcap = lp.zcap;
     p.zstride = lp.zstride;
+    char* const tail = static_cast<char*>(ctx->c2f_scores.p) + sbytes;
+    KStageResult* d_out = reinterpret_cast<KStageResult*>(tail);
     unsigned long long* d_rng = nullptr;
     const bool dev_rng = rng_state && is_device_ptr(rng_state);
     if (rng_state) {
       if (dev_rng) {
         d_rng = reinterpret_cast<unsigned long long*>(rng_state);
-      } else {  // through pinned staging: an asynchronous copy
-        std::memcpy(static_cast<char*>(ctx->io_pin.p) + 64, rng_state, 40);
-        d_rng = reinterpret_cast<unsigned long long*>(static_cast<char*>(ctx->result.p) + 64);
-        cuda_check(cudaMemcpyAsync(d_rng, static_cast<char*>(ctx->io_pin.p) + 64, 40,
-                                   cudaMemcpyHostToDevice, ctx->stream),
-                   "cudaMemcpyAsync rng");
+      } else {  // the render kernel stores the state as it starts (KParams::rng_dst)
+        d_rng = reinterpret_cast<unsigned long long*>(tail + 64);
+        p.rng_dst = d_rng;
+        std::memcpy(p.rng_init, rng_state, 40);
       }
     }
-    KStageResult* d_out = ctx->result.as<KStageResult>();
     cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
                "render_score launch");
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
                                    ctx->stream, stage_scratch(ctx, (long long)n)),
                "stage_reduce launch");
-    // host results: the stage result and the advanced Rng state sit next to
-    // each other on the device (result buffer, rng slot at +64) and come back
-    // in ONE copy into pinned staging; pageable score buffers are staged too,
-    // so nothing blocks before the single synchronize
     const bool host_out = !is_device_ptr(out);
+    const bool host_rng = rng_state && !dev_rng;
     const bool host_scores = scores && !is_device_ptr(scores);
-    const bool pin_scores = host_scores && !is_pinned_host(scores);
-    if (host_out || (rng_state && !dev_rng))
-      cuda_check(cudaMemcpyAsync(ctx->io_pin.p, ctx->result.p, 128, cudaMemcpyDeviceToHost,
-                                 ctx->stream),
-                 "cudaMemcpyAsync result");
     if (!host_out)
       cuda_check(cudaMemcpyAsync(out, d_out, sizeof(KStageResult), cudaMemcpyDeviceToDevice,
                                  ctx->stream),
                  "cudaMemcpyAsync result");
-    const size_t sbytes = sizeof(double) * n * nn;
-    if (pin_scores) ctx->pin_scores.ensure(sbytes);
-    if (scores)
-      cuda_check(cudaMemcpyAsync(pin_scores ? ctx->pin_scores.p : scores, p.scores, sbytes,
-                                 cudaMemcpyDefault, ctx->stream),
+    if (scores && !host_scores)
+      cuda_check(cudaMemcpyAsync(scores, p.scores, sbytes, cudaMemcpyDeviceToDevice, ctx->stream),
                  "cudaMemcpyAsync scores");
-    if (host_out || host_scores || (rng_state && !dev_rng) || host_in) {
+    if (host_out || host_rng || host_scores) {
+      // one read-back into pinned staging: [scores if wanted] + result + Rng
+      const size_t from = host_scores ? 0 : sbytes;
+      ctx->pin_scores.ensure(sbytes + 128);
+      char* const pin = static_cast<char*>(ctx->pin_scores.p);
+      cuda_check(cudaMemcpyAsync(pin + from, static_cast<char*>(ctx->c2f_scores.p) + from,
+                                 sbytes + 128 - from, cudaMemcpyDeviceToHost, ctx->stream),
+                 "cudaMemcpyAsync results");
       cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
-      if (host_out) std::memcpy(out, ctx->io_pin.p, sizeof(KStageResult));
-      if (rng_state && !dev_rng)
-        std::memcpy(rng_state, static_cast<char*>(ctx->io_pin.p) + 64, 40);
-      if (pin_scores) std::memcpy(scores, ctx->pin_scores.p, sbytes);
+      if (host_out) std::memcpy(out, pin + sbytes, sizeof(KStageResult));
+      if (host_rng) std::memcpy(rng_state, pin + sbytes + 64, 40);
+      if (host_scores) std::memcpy(scores, pin, sbytes);
+    } else if (host_in) {
+      cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_poses");
     }
   });
 }

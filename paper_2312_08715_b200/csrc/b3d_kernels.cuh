@@ -132,6 +132,11 @@ struct KParams {
   double* vscratch;              // gridDim x 3*nv
   int vcap;                      // vertices cached in shared memory
   int zcap;                      // z-buffer pixels in shared memory
+  // optional: CTA 0 stores rng_init at rng_dst when the kernel starts (the
+  // stage reduction launched after it then draws from that state, without
+  // a separate host-to-device copy of 40 bytes)
+  unsigned long long* rng_dst;
+  unsigned long long rng_init[5];
 };
 
 struct KStageResult {

@@ -93,7 +93,9 @@ cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_k
 }
 
 // Observation cache (likelihood.cpp:106-126) as per-pixel fp32 points plus
-// the valid count M.
+// the valid count M.  count[0] = M; count[1] = a block counter that wraps
+// back to 0 (atomicInc); count[2 + b] = block b's partial: the last block to
+// finish sums the partials, so no memset precedes the launch.
 __global__ void obs_prepare_kernel(const float* depth, int W, int H, float far_f, float fcx,
                                    float fcy, float inv_fx, float inv_fy, float4* out,
                                    int* count) {
@@ -115,7 +117,16 @@ __global__ void obs_prepare_kernel(const float* depth, int W, int H, float far_f
   c = warp_sum_i(c);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_cnt, c);
   __syncthreads();
-  if (threadIdx.x == 0 && s_cnt) atomicAdd(count, s_cnt);
+  if (threadIdx.x == 0) {
+    count[2 + blockIdx.x] = s_cnt;
+    __threadfence();
+    if (atomicInc(reinterpret_cast<unsigned int*>(count + 1), gridDim.x - 1) == gridDim.x - 1) {
+      __threadfence();
+      int m = 0;
+      for (unsigned int b = 0; b < gridDim.x; ++b) m += __ldcg(count + 2 + b);
+      count[0] = m;
+    }
+  }
 }
 
 // Host-side launch helpers (declared in b3d_capi.cpp).
@@ -239,14 +250,15 @@ B3D_INST(true, false, true)
 B3D_INST(false, false, true)
 #undef B3D_INST
 
+constexpr int kObsBlocks = 1184;
+size_t obs_count_ints() { return 2 + kObsBlocks; }  // count buffer (zeroed once)
+
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out, int* count,
                                cudaStream_t st) {
-  cudaError_t e = cudaMemsetAsync(count, 0, sizeof(int), st);
-  if (e != cudaSuccess) return e;
   const int n = W * H;
   int grid = (n + 255) / 256;
-  if (grid > 1184) grid = 1184;
+  if (grid > kObsBlocks) grid = kObsBlocks;
   obs_prepare_kernel<<<grid, 256, 0, st>>>(depth, W, H, far_f, fcx, fcy, inv_fx, inv_fy, out,
                                            count);
   return cudaGetLastError();

@@ -1204,6 +1204,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   // stream serialization) be scheduled into SMs this grid leaves idle; it
   // waits for this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
+  if (p.rng_dst && blockIdx.x == 0 && threadIdx.x < 5) p.rng_dst[threadIdx.x] = p.rng_init[threadIdx.x];
   B3D_PCLK(0);
 #if B3D_L2_PREFETCH
   // Shared read-only inputs (mesh, sorted triangles, observation) into L2 in
