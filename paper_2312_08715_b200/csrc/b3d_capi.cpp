@@ -36,11 +36,12 @@ template <bool kIds, bool kScore, bool kOut>
 size_t static_smem_render_score();
 size_t render_score_staging_bytes(int nt);
 // track.cu
-cudaError_t launch_cam_lattice(const double* tab, int n_tab, int off, int ppd, const int* state,
-                               KPose* cams, unsigned char* valid, const KPose& fallback,
-                               cudaStream_t st);
 cudaError_t launch_cam_argmax(const double* scores, const unsigned char* valid, int ppd,
                               int* state, cudaStream_t st);
+cudaError_t launch_cam_stage(const double* tab, int n_tab, int off, int ppd, int first,
+                             const double* prev_scores, const unsigned char* valid_prev,
+                             int* state, KPose* cams, unsigned char* valid,
+                             const KPose& fallback, cudaStream_t st);
 // mesh_build.cu
 cudaError_t voxel_to_mesh_device(const int* d_vox, unsigned long long n, double res,
                                  const double origin[3], double* d_verts, unsigned* d_tris,
@@ -1830,23 +1831,22 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
         cuda_check(cudaMemcpyAsync(ctx->trk_tab.p, tab, sizeof(double) * 7 * n_tab,
                                    cudaMemcpyHostToDevice, ctx->stream),
                    "cudaMemcpyAsync track tables");
-        cuda_check(cudaMemsetAsync(ctx->trk_state.p, 0, 8 * sizeof(int), ctx->stream),
-                   "cudaMemsetAsync track state");
         const KPose fallback = camera_from_spherical(c0.d, c0.az, c0.alt);
         int* dstate = ctx->trk_state.as<int>();
-        for (int st = 0; st <= S; ++st) {
-          cuda_check(launch_cam_lattice(ctx->trk_tab.as<double>(), n_tab, off[st], ppd, dstate,
-                                        ctx->c2f_centers.as<KPose>(),
-                                        ctx->trk_valid.as<unsigned char>(), fallback,
-                                        ctx->stream),
-                     "cam_lattice launch");
+        for (int st = 0; st <= S; ++st) {  // stage 0's kernel also zeroes the state
+          cuda_check(launch_cam_stage(ctx->trk_tab.as<double>(), n_tab, off[st], ppd, st == 0,
+                                      ctx->c2f_scores.as<double>(),
+                                      ctx->trk_valid.as<unsigned char>(), dstate,
+                                      ctx->c2f_centers.as<KPose>(),
+                                      ctx->trk_valid.as<unsigned char>(), fallback, ctx->stream),
+                     "cam_stage launch");
           launch_score_cameras(ctx, ctx->c2f_centers.as<KPose>(), (long long)n_grid,
                                ctx->c2f_scores.as<double>(), nullptr);
-          cuda_check(launch_cam_argmax(ctx->c2f_scores.as<double>(),
-                                       ctx->trk_valid.as<unsigned char>(), ppd, dstate,
-                                       ctx->stream),
-                     "cam_argmax launch");
         }
+        cuda_check(launch_cam_argmax(ctx->c2f_scores.as<double>(),
+                                     ctx->trk_valid.as<unsigned char>(), ppd, dstate,
+                                     ctx->stream),
+                   "cam_argmax launch");
         int* hs = ctx->trk_state_pin.as<int>();
         cuda_check(cudaMemcpyAsync(hs, dstate, 8 * sizeof(int), cudaMemcpyDeviceToHost,
                                    ctx->stream),

@@ -8,12 +8,16 @@
 // every azimuth and altitude with its own libm, exactly the values the
 // reference's camera_pose_from_spherical would use -- once per frame.  The
 // device then chains the stages without a host round trip:
-//   cam_lattice_kernel: the stage's ppd^3 camera poses from the tables
-//     (generative.cpp:35-59 arithmetic after the trig calls: products, sqrt,
-//     divisions -- IEEE-exact, no FMA contraction, so bitwise the host's);
+//   cam_stage_kernel: the previous stage's argmax -- first index of the
+//     strict maximum over the valid lattice points (tracking.cpp:132-134),
+//     appended to the per-axis path -- then this stage's ppd^3 camera poses
+//     from the tables (generative.cpp:35-59 arithmetic after the trig calls:
+//     products, sqrt, divisions -- IEEE-exact, no FMA contraction, so
+//     bitwise the host's);
 //   the camera-mode score kernel;
-//   cam_argmax_kernel: first index of the strict maximum over the valid
-//     lattice points (tracking.cpp:132-134), appended to the per-axis path.
+//   cam_argmax_kernel: the last stage's argmax.
+// The argmax kernels are launched with programmatic stream serialization, so
+// they are resident when the score grid ends.
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -94,24 +98,6 @@ __device__ KPose camera_from_trig(double distance, double ca, double sa, double 
 
 // tab: 7 rows of n_tab doubles -- d, az, alt, cos(alt), sin(alt), cos(az),
 // sin(az) -- per axis value; level s values start at off (the caller's).
-__global__ void cam_lattice_kernel(const double* __restrict__ tab, int n_tab, int off, int ppd,
-                                   const int* __restrict__ path, KPose* __restrict__ cams,
-                                   unsigned char* __restrict__ valid, KPose fallback) {
-  const int n = ppd * ppd * ppd;
-  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n; idx += gridDim.x * blockDim.x) {
-    const int i = idx / (ppd * ppd), j = (idx / ppd) % ppd, k = idx % ppd;
-    const int id = off + path[0] * ppd + i;   // distance value
-    const int iz = off + path[1] * ppd + j;   // azimuth value
-    const int ia = off + path[2] * ppd + k;   // altitude value
-    const double dist = tab[id], alt = tab[2 * n_tab + ia];
-    // score_pose (tracking.cpp:100-108): out-of-range points score -inf
-    const bool ok = dist > 0 && alt > 0 && alt < kHalfPiD;
-    valid[idx] = ok;
-    cams[idx] = ok ? camera_from_trig(dist, tab[3 * n_tab + ia], tab[4 * n_tab + ia],
-                                      tab[5 * n_tab + iz], tab[6 * n_tab + iz])
-                   : fallback;
-  }
-}
 
 // First index of the strict maximum over the valid points (invalid = -inf,
 // start at index 0 as the reference's loop); appends the pick to the per-axis
@@ -119,6 +105,7 @@ __global__ void cam_lattice_kernel(const double* __restrict__ tab, int n_tab, in
 __global__ void cam_argmax_kernel(const double* __restrict__ scores,
                                   const unsigned char* __restrict__ valid, int ppd,
                                   int* __restrict__ state /* path[3], best, err */) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the score kernel's results
   const int n = ppd * ppd * ppd;
   constexpr double kNegInf = -__builtin_huge_val();
   double bv = kNegInf;
@@ -167,21 +154,121 @@ __global__ void cam_argmax_kernel(const double* __restrict__ scores,
   }
 }
 
+// One stage of the chain in one CTA: the previous stage's argmax (appended
+// to the path; skipped for stage 0, which starts the path at the root), then
+// this stage's ppd^3 camera poses.  Launched with programmatic stream
+// serialization after the score kernel, so it is resident when that grid
+// finishes and waits for its scores here.
+__global__ void __launch_bounds__(1024)
+cam_stage_kernel(const double* __restrict__ tab, int n_tab, int off, int ppd, int first,
+                 const double* __restrict__ prev_scores, const unsigned char* __restrict__ valid_prev,
+                 int* __restrict__ state, KPose* __restrict__ cams,
+                 unsigned char* __restrict__ valid, KPose fallback) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int n = ppd * ppd * ppd;
+  constexpr double kNegInf = -__builtin_huge_val();
+  __shared__ int s_path[3];
+  if (first) {
+    if (threadIdx.x == 0) {
+      for (int i = 0; i < 8; ++i) state[i] = 0;
+      s_path[0] = s_path[1] = s_path[2] = 0;
+    }
+  } else {
+    double bv = kNegInf;
+    int bi = 0x7fffffff;
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      const double v = valid_prev[i] ? prev_scores[i] : kNegInf;
+      if (bi == 0x7fffffff || v > bv) {
+        bv = v;
+        bi = i;
+      }
+    }
+    __shared__ double sv[32];
+    __shared__ int si[32];
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sv[threadIdx.x >> 5] = bv;
+      si[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      bv = sv[0];
+      bi = si[0];
+      for (int w = 1; w < (int)((blockDim.x + 31) / 32); ++w)
+        if (si[w] != 0x7fffffff && (bi == 0x7fffffff || sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
+          bv = sv[w];
+          bi = si[w];
+        }
+      if (!(bv > kNegInf)) {
+        bi = 0;
+        state[4] = 1;
+      }
+      state[3] = bi;
+      state[0] = state[0] * ppd + bi / (ppd * ppd);
+      state[1] = state[1] * ppd + (bi / ppd) % ppd;
+      state[2] = state[2] * ppd + bi % ppd;
+      s_path[0] = state[0];
+      s_path[1] = state[1];
+      s_path[2] = state[2];
+    }
+  }
+  __syncthreads();
+  asm volatile("griddepcontrol.launch_dependents;");
+  for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+    const int i = idx / (ppd * ppd), j = (idx / ppd) % ppd, k = idx % ppd;
+    const int id = off + s_path[0] * ppd + i;
+    const int iz = off + s_path[1] * ppd + j;
+    const int ia = off + s_path[2] * ppd + k;
+    const double dist = tab[id], alt = tab[2 * n_tab + ia];
+    // score_pose (tracking.cpp:100-108): out-of-range points score -inf
+    const bool ok = dist > 0 && alt > 0 && alt < kHalfPiD;
+    valid[idx] = ok;
+    cams[idx] = ok ? camera_from_trig(dist, tab[3 * n_tab + ia], tab[4 * n_tab + ia],
+                                      tab[5 * n_tab + iz], tab[6 * n_tab + iz])
+                   : fallback;
+  }
+}
+
 }  // namespace
 
-cudaError_t launch_cam_lattice(const double* tab, int n_tab, int off, int ppd, const int* state,
-                               KPose* cams, unsigned char* valid, const KPose& fallback,
-                               cudaStream_t st) {
-  const int n = ppd * ppd * ppd;
-  const int block = 128, grid = (n + block - 1) / block;
-  cam_lattice_kernel<<<grid, block, 0, st>>>(tab, n_tab, off, ppd, state, cams, valid, fallback);
-  return cudaGetLastError();
+cudaError_t launch_cam_stage(const double* tab, int n_tab, int off, int ppd, int first,
+                             const double* prev_scores, const unsigned char* valid_prev,
+                             int* state, KPose* cams, unsigned char* valid,
+                             const KPose& fallback, cudaStream_t st) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(ppd * ppd * ppd >= 1024 ? 1024 : ((ppd * ppd * ppd + 31) / 32) * 32);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = first ? 0 : 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cam_stage_kernel, tab, n_tab, off, ppd, first,
+                                           prev_scores, valid_prev, state, cams, valid, fallback);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_cam_argmax(const double* scores, const unsigned char* valid, int ppd,
                               int* state, cudaStream_t st) {
-  cam_argmax_kernel<<<1, 1024, 0, st>>>(scores, valid, ppd, state);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(1);
+  cfg.blockDim = dim3(1024);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, cam_argmax_kernel, scores, valid, ppd, state);
+  return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace b3d200
