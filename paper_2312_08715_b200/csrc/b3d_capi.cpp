@@ -29,7 +29,8 @@ namespace b3d200 {
 
 // kernels (render_score.cu, stage.cu, image_score.cu)
 template <bool kIds, bool kScore, bool kOut>
-cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st,
+                                bool pdl = false);
 template <bool kIds, bool kScore, bool kOut>
 cudaError_t occupancy_render_score(int* blocks, size_t smem, bool vs);
 template <bool kIds, bool kScore, bool kOut>
@@ -1145,7 +1146,7 @@ void cam_params(b3d_gpu_context* ctx, KParams& p) {
 // score-many over camera poses (device-resident `cams` of n entries) into
 // device buffers scores/status
 void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, double* scores,
-                          uint8_t* status) {
+                          uint8_t* status, bool pdl = false) {
   const Mesh& m = *ctx->cam_mesh;
   KParams p = base_params(ctx, m);
   cam_params(ctx, p);
@@ -1159,7 +1160,7 @@ void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, 
   p.vcap = lp.vcap;
   p.zcap = lp.zcap;
   p.zstride = lp.zstride;
-  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
+  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream, pdl),
              "render_score launch (cameras)");
 }
 }  // namespace
@@ -1841,7 +1842,7 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
                                       ctx->trk_valid.as<unsigned char>(), fallback, ctx->stream),
                      "cam_stage launch");
           launch_score_cameras(ctx, ctx->c2f_centers.as<KPose>(), (long long)n_grid,
-                               ctx->c2f_scores.as<double>(), nullptr);
+                               ctx->c2f_scores.as<double>(), nullptr, /*pdl=*/true);
         }
         cuda_check(launch_cam_argmax(ctx->c2f_scores.as<double>(),
                                      ctx->trk_valid.as<unsigned char>(), ppd, dstate,

@@ -189,12 +189,27 @@ cudaError_t ensure_smem_limit(const void* kern, size_t smem) {
 }  // namespace
 
 template <bool kIds, bool kScore, bool kOut>
-cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st) {
+cudaError_t launch_render_score(const KParams& p, int grid, size_t smem, cudaStream_t st,
+                                bool pdl) {
   auto kern = pick_kernel<kIds, kScore, kOut>(p.nv <= p.vcap, p.lik.window, p.lik.n_noise,
                                               p.cams != nullptr);
   cudaError_t e = ensure_smem_limit(reinterpret_cast<const void*>(kern), smem);
   if (e != cudaSuccess) return e;
   if (p.n_hyp <= 0) return cudaSuccess;
+  if (pdl) {  // camera mode: the kernel waits (griddepcontrol.wait) before reading inputs
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)std::min<long long>(grid, p.n_hyp));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    e = cudaLaunchKernelEx(&cfg, kern, p);
+    return e != cudaSuccess ? e : cudaGetLastError();
+  }
   kern<<<(int)std::min<long long>(grid, p.n_hyp), kThreads, smem, st>>>(p);
   return cudaGetLastError();
 }
@@ -242,7 +257,7 @@ size_t static_smem_render_score() {
 
 #define B3D_INST(I, S, O)                                                                 \
   template cudaError_t launch_render_score<I, S, O>(const KParams&, int, size_t,         \
-                                                    cudaStream_t);                       \
+                                                    cudaStream_t, bool);                 \
   template cudaError_t occupancy_render_score<I, S, O>(int*, size_t, bool);              \
   template size_t static_smem_render_score<I, S, O>();
 B3D_INST(false, true, false)

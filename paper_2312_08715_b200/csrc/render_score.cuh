@@ -1223,6 +1223,10 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     if (kScore) pf(p.obs, 16ull * p.W * p.H);
   }
 #endif
+  // camera mode may be launched with programmatic serialization behind the
+  // kernel that wrote the camera poses (track.cu): wait for it here, after
+  // the prefetch of the inputs it does not write (a no-op otherwise)
+  if (kCam) asm volatile("griddepcontrol.wait;" ::: "memory");
   // Hypotheses one per CTA, strided by the grid (persistent CTAs).
   const long long G = gridDim.x;
   int kk = 0;  // hypotheses this CTA has processed
