@@ -362,7 +362,6 @@ struct b3d_gpu_context {
   DevBuf in_stage, out_stage, out_stage2, rot_stage, result, rng;
   DevBuf c2f_scores, c2f_rot, c2f_centers, c2f_results;
   PinnedBuf pin_cams, pin_scores;  // track_camera / enumerate_poses staging
-  PinnedBuf io_pin;                 // stage result + Rng state (enumerate_poses)
   PinnedBuf trk_tab_pin, trk_state_pin;  // track_camera device chain: tables, picks
   DevBuf stage_part;                     // grid-wide stage reduction partials
   DevBuf trk_tab, trk_state, trk_valid;
@@ -1270,7 +1269,6 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
     cuda_check(cudaMemset(c->obs_count.p, 0, sizeof(int) * obs_count_ints()), "cudaMemset");
     static_assert(sizeof(KStageResult) <= 64, "rng slot at +64");
     c->result.ensure(128);  // KStageResult, then an Rng state at +64
-    c->io_pin.ensure(128);
     c->rng.ensure(5 * sizeof(uint64_t));
     *out = c.release();
   });
