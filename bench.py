@@ -43,7 +43,9 @@ def _ncu_traffic():
     (profiles/r*_render_score_details.txt), or None."""
     import glob
     import re
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_render_score_details.txt")))
+    # the most recent capture: round tags sort by length then name (r1z < r1z4)
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_render_score_details.txt")),
+                   key=lambda f: (len(os.path.basename(f)), os.path.basename(f)))
     if not files:
         return None
     text = open(files[-1]).read()
