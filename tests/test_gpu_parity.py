@@ -645,6 +645,20 @@ def test_track_camera_search_variants_match_oracle(gpu_ctx, oracle, ppd, stages,
             assert s[-1] - s[-2] <= SCORE_RTOL * abs(s[-1])
 
 
+def test_track_camera_device_frames_equal_host_frames(gpu_ctx, oracle):
+    """Frames already on the device (no per-frame upload) track identically."""
+    import torch
+    seq = _orbit(oracle, 50, ref_frames=True)
+    _camera_scene(gpu_ctx, seq)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    cams = [oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+            for a in seq["azimuths"][:6]]
+    frames = configs.orbit_frames(seq, cams)
+    est_h, _ = gpu_ctx.track_camera(frames, cams[0])
+    est_d, _ = gpu_ctx.track_camera(torch.from_numpy(frames).cuda(), cams[0])
+    np.testing.assert_array_equal(est_h, est_d)
+
+
 def test_orbit_frames_equal_the_reference(gpu_ctx, oracle):
     """generate_orbit_sequence (tracking.cpp:174-206) as the bench builds it:
     device camera renders + the product's sample_observation on split streams
