@@ -589,6 +589,14 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
 
 KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   KParams p{};
+  // big projected faces: only 1x1 bboxes stay in the tile queue; 2x2 and
+  // 3x3 take the per-lane loop too (cfg4 173 -> 180 FPS, cfg3 +3 % vs
+  // queueing 2x2; B3D_Q1_SMALL overrides for A/B)
+  static const int q1_small = [] {
+    const char* e = std::getenv("B3D_Q1_SMALL");
+    return e ? std::atoi(e) : 1;
+  }();
+  p.q1_small = q1_small;
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;
   p.fy = k.fy;

@@ -137,6 +137,7 @@ struct KParams {
   // a separate host-to-device copy of 40 bytes)
   unsigned long long* rng_dst;
   unsigned long long rng_init[5];
+  int q1_small;  // tile-class bound for big projected faces (render_score.cuh hc.q1)
 };
 
 struct KStageResult {

@@ -1340,15 +1340,16 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       rg.v1 = min(s_hi_v, p.H - 1);
     }
     hc.empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
-    // 3x3 bboxes: the tile class with a dealt fragment pass pays off for
-    // small projected triangles; when the mesh's faces span ~2.7+ px (region
-    // area > 0.4 nt; a voxel blob's ratio grows with the squared projected
-    // voxel size: cfg2 0.24 at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane
-    // loop is faster (cfg3/cfg4 +12 %; forcing it on cfg2 costs 12 %).
+    // The tile classes (queues + dealt fragments) pay off for small projected
+    // triangles; when the mesh's faces span ~2.7+ px (region area > 0.4 nt; a
+    // voxel blob's ratio grows with the squared projected voxel size: cfg2
+    // 0.24 at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane loop is faster for
+    // everything above p.q1_small px a side (cfg3/cfg4 +15 %; forcing it on
+    // cfg2 costs 12 %).
     // Meshes whose vertex cache fits on chip are small and keep the class.
     hc.q1 = (!kVS && !hc.empty_region &&
              5ll * (rg.u1 - rg.u0 + 1) * (rg.v1 - rg.v0 + 1) > 2ll * p.nt)
-                ? 2
+                ? p.q1_small
                 : 3;
     if (hc.empty_region) {  // keep one valid (unused) pixel so indexing stays sane
       rg.u1 = rg.u0 = min(max(rg.u0, 0), p.W - 1);
