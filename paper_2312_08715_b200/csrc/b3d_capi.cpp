@@ -597,6 +597,11 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
     return e ? std::atoi(e) : 1;
   }();
   p.q1_small = q1_small;
+  static const int q1_ratio = [] {  // region px per 100 triangles (B3D_Q1_RATIO: A/B)
+    const char* e = std::getenv("B3D_Q1_RATIO");
+    return e ? std::atoi(e) : 20;
+  }();
+  p.q1_ratio = q1_ratio;
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;
   p.fy = k.fy;

@@ -1341,14 +1341,14 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     }
     hc.empty_region = rg.u0 > rg.u1 || rg.v0 > rg.v1;
     // The tile classes (queues + dealt fragments) pay off for small projected
-    // triangles; when the mesh's faces span ~2.7+ px (region area > 0.4 nt; a
-    // voxel blob's ratio grows with the squared projected voxel size: cfg2
-    // 0.24 at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane loop is faster for
-    // everything above p.q1_small px a side (cfg3/cfg4 +15 %; forcing it on
-    // cfg2 costs 12 %).
+    // triangles; when the mesh's faces span ~2 px or more (region area >
+    // p.q1_ratio / 100 x triangles, default 0.2; a voxel blob's ratio grows
+    // with the squared projected voxel size: cfg1 0.19 at 1.7 px, cfg2 0.24
+    // at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane loop is faster for every
+    // bbox above p.q1_small px a side (cfg3/cfg4 +15 %, cfg2 +1.5 %).
     // Meshes whose vertex cache fits on chip are small and keep the class.
     hc.q1 = (!kVS && !hc.empty_region &&
-             5ll * (rg.u1 - rg.u0 + 1) * (rg.v1 - rg.v0 + 1) > 2ll * p.nt)
+             100ll * (rg.u1 - rg.u0 + 1) * (rg.v1 - rg.v0 + 1) > (long long)p.q1_ratio * p.nt)
                 ? p.q1_small
                 : 3;
     if (hc.empty_region) {  // keep one valid (unused) pixel so indexing stays sane
