@@ -1346,7 +1346,9 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     // with the squared projected voxel size: cfg1 0.19 at 1.7 px, cfg2 0.24
     // at 2.1 px, cfg4 0.68 at 3.3 px) the per-lane loop is faster for every
     // bbox above p.q1_small px a side (cfg3/cfg4 +15 %, cfg2 +1.5 %).
-    // Meshes whose vertex cache fits on chip are small and keep the class.
+    // Meshes whose vertex cache fits on chip are small and keep the class;
+    // so does camera mode, whose full-frame region says nothing about the
+    // triangles' size (bench-tracking 200 px 1.7k -> 2.3k FPS with it).
     hc.q1 = (!kVS && !hc.empty_region &&
              100ll * (rg.u1 - rg.u0 + 1) * (rg.v1 - rg.v0 + 1) > (long long)p.q1_ratio * p.nt)
                 ? p.q1_small
@@ -1362,10 +1364,10 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     rg.rh = rg.v1 - rg.v0 + 1 + 2 * pad;
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
-      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
                                                     s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     else
-      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS>(
+      hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
           s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
     B3D_PCLK(7);
