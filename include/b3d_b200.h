@@ -158,6 +158,8 @@ typedef struct b3d_noise {
 
 enum { B3D_PREFACTOR_PRINTED = 0, B3D_PREFACTOR_UNIFORM = 1 };
 enum { B3D_GRID_PRODUCT = 0, B3D_GRID_ZIP = 1 };
+/* noise entries / distinct sigmas per fused launch; calls with more are split
+ * into several launches (no limit on the call) */
 enum { B3D_MAX_NOISE = 12, B3D_MAX_SIGMAS = 4 };
 
 /* 6-DoF hypothesis grid generated on the device.  Translation lattice per
@@ -232,7 +234,15 @@ B3D_API b3d_status b3d_gpu_mesh_cull_sign(const b3d_gpu_context* ctx, int32_t me
                                           int32_t* out);
 /* Observed depth image (W x H fp32, sentinel = (float)far). */
 B3D_API b3d_status b3d_gpu_set_observation(b3d_gpu_context* ctx, const float* depth);
-/* windowed_log_likelihood_multi settings (likelihood.hpp:65-69). */
+/* Likelihood settings (likelihood.hpp:65-69), any number of noise entries.
+ * Score-many (object mode) is the score_cells seam, observation_loglik_cached_multi
+ * (inference.cpp:40-83): an entry outside the noise support (p_outlier not in
+ * [0,1], sigma_noise <= 0 or > sigma_max) scores -inf, window < 0 is the
+ * untruncated likelihood.  The camera paths are windowed_log_likelihood_multi
+ * itself (tracking.cpp:98-101): such entries and window < 0 are errors there,
+ * sigma_noise > sigma_max is scored.  window < 0 or p_outlier < 1e-6 run on the
+ * fp64 image path (render, then exact_score.cu) so -inf and tiny-floor terms
+ * are the reference's. */
 B3D_API b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
                                           uint32_t n_noise, double sigma_max, int window,
                                           int prefactor);
@@ -438,16 +448,16 @@ typedef struct b3d_schedule_stage {
 typedef struct b3d_smc_config {
   double table_w, table_h;
   int32_t table_mesh;
-  uint32_t n_refine; /* <= 4 */
+  uint32_t n_refine; /* any number of refine stages (Schedule::refine) */
   b3d_schedule_stage stage0;
-  b3d_schedule_stage refine[4];
+  const b3d_schedule_stage* refine; /* n_refine entries */
   const b3d_noise* noise_grid;
-  uint32_t n_noise_grid; /* <= B3D_MAX_NOISE, <= B3D_MAX_SIGMAS distinct sigmas */
+  uint32_t n_noise_grid; /* any size; entries must lie in the noise support */
   uint32_t n_objects;    /* objects placed, 1..B3D_SMC_MAX_CHILDREN */
   uint32_t n_particles;
   double resample_threshold;
   double sigma_max;
-  int32_t window;
+  int32_t window; /* < 0: untruncated likelihood (ModelConfig::windowed = false) */
   int32_t prefactor;
 } b3d_smc_config;
 enum { B3D_SMC_MAX_CHILDREN = 8 };

@@ -76,7 +76,7 @@ def lib():
                      "refb_contact_to_pose", "refb_voxel_to_mesh", "refb_render_instances",
                      "refb_windowed_multi", "refb_full_loglik", "refb_score_poses",
                      "refb_sample_observation", "refb_stage0", "refb_propose", "refb_run_smc",
-                     "refb_track_camera", "refb_orbit_sequence"):
+                     "refb_track_camera", "refb_orbit_sequence", "refb_stage0_cell_poses"):
             getattr(L, name).restype = C.c_int
         _lib = L
     return _lib
@@ -276,6 +276,17 @@ def stage0(k, observed, camera, world: World, cap=1 << 22):
                              C.byref(n), _p(ints), _p(iv), _p(sc), C.byref(az)))
     m = n.value
     return ints[:m].copy(), iv[:m].copy(), sc[:m].copy(), bool(az.value)
+
+
+def stage0_cell_poses(k, world: World, obj, face, cap=1 << 21):
+    """World poses of the stage-0 cell centres of one (object, face) branch."""
+    ki = intr(k)
+    obs = np.full((ki.height, ki.width), ki.far_m, dtype=np.float32)
+    n = C.c_uint64()
+    out = np.zeros((cap, 7))
+    _check(lib().refb_stage0_cell_poses(C.byref(ki), _p(obs), C.byref(world.spec), obj, face,
+                                        C.c_uint64(cap), C.byref(n), _p(out)))
+    return out[: n.value].copy()
 
 
 def propose(k, observed, camera, world: World, seed, n_props):

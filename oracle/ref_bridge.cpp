@@ -356,6 +356,29 @@ std::unique_ptr<SmcWorld> make_world(const RefIntr* k, const float* obs, const d
 
 }  // namespace
 
+// Model-to-world poses of the stage-0 cell centres of one (object, face):
+// stage0_cells (inference.cpp:208-238) filtered to that branch and noise
+// entry 0, then cell_center_child + contact_to_pose (inference.cpp:126-137,
+// scene_graph.cpp:97-121).  The cfg3 contact grid is exactly this set.
+REFB_API int refb_stage0_cell_poses(const RefIntr* k, const float* obs, const RefSmcSpec* s,
+                                    int object, int face, uint64_t cap, uint64_t* n_out,
+                                    double* poses) {
+  return guarded([&] {
+    const double ident[7] = {1, 0, 0, 0, 0, 0, 0};
+    auto w = make_world(k, obs, ident, s);
+    const std::vector<b3d::Cell> cells = b3d::stage0_cells(w->ctx);
+    uint64_t n = 0;
+    for (const b3d::Cell& c : cells) {
+      if (c.object_id != object || c.face != face || c.noise_index != 0) continue;
+      b3d::require(n < cap, b3d::ErrorCode::invalid, "refb_stage0_cell_poses: capacity");
+      const b3d::SceneChild ch = b3d::cell_center_child(c, w->library);
+      pose_out(b3d::contact_to_pose(*w->table, *ch.object, ch.face, ch.contact), poses + 7 * n);
+      ++n;
+    }
+    *n_out = n;
+  });
+}
+
 // cells_out: per cell (object, face, noise_index) ints and (dx.lo, dx.hi, dy.lo,
 // dy.hi, dth.lo, dth.hi) doubles; scores_out: normalised probabilities.
 REFB_API int refb_stage0(const RefIntr* k, const float* obs, const double* camera,

@@ -116,7 +116,7 @@ class ScheduleStage(C.Structure):
 class SmcConfig(C.Structure):
     _fields_ = [("table_w", C.c_double), ("table_h", C.c_double), ("table_mesh", C.c_int32),
                 ("n_refine", C.c_uint32), ("stage0", ScheduleStage),
-                ("refine", ScheduleStage * 4), ("noise_grid", C.c_void_p),
+                ("refine", C.c_void_p), ("noise_grid", C.c_void_p),
                 ("n_noise_grid", C.c_uint32), ("n_objects", C.c_uint32),
                 ("n_particles", C.c_uint32), ("resample_threshold", C.c_double),
                 ("sigma_max", C.c_double), ("window", C.c_int32), ("prefactor", C.c_int32)]
@@ -845,8 +845,9 @@ class GpuContext:
         cfg.table_w, cfg.table_h, cfg.table_mesh = table_w, table_h, table_mesh
         cfg.stage0 = ScheduleStage(*schedule[0])
         cfg.n_refine = len(schedule[1])
-        for r, st in enumerate(schedule[1]):
-            cfg.refine[r] = ScheduleStage(*st)
+        refine = (ScheduleStage * max(1, len(schedule[1])))(*[ScheduleStage(*st)
+                                                               for st in schedule[1]])
+        cfg.refine = C.cast(refine, C.c_void_p)
         cfg.noise_grid = C.cast(nz, C.c_void_p)
         cfg.n_noise_grid = len(noise_grid)
         cfg.n_objects, cfg.n_particles = n_objects, n_particles

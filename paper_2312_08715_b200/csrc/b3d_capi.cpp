@@ -52,6 +52,9 @@ cudaError_t voxel_to_mesh_device(const int* d_vox, unsigned long long n, double 
 cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, float fcx,
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
+cudaError_t launch_exact_score(const KExactArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_fill_column(double* s, long long n, int ld, int col, double v, cudaStream_t st);
+size_t exact_score_pts_bytes(int W, int H, int ctas);
 size_t stage_scratch_bytes(long long n);  // stage.cu: grid-wide reduction partials
 size_t obs_count_ints();                 // render_score.cu: obs_prepare count buffer
 cudaError_t launch_stage_reduce(const double* x, long long n, int stride, int col,
@@ -343,6 +346,26 @@ int closed_mesh_cull_sign(const double* v, const uint32_t* t, uint64_t nt) {
 
 using namespace b3d200;
 
+// one fused launch's noise entries: output columns [col0, col0 + lik.n_noise)
+struct LikChunk {
+  int col0 = 0;
+  KLik lik{};
+  KExactLik ex{};
+};
+
+// likelihood settings of a score call (make_spec)
+struct LikSpec {
+  int n_cols = 0;             // output columns = noise entries
+  int window = 0;             // < 0: untruncated likelihood
+  bool exact = false;         // fp64 image path (exact_score.cu)
+  std::vector<int> gated;     // columns outside the noise support: -inf
+  std::vector<LikChunk> chunks;
+  // one fused launch writes every column in place
+  bool single() const {
+    return !exact && gated.empty() && chunks.size() == 1 && chunks[0].lik.n_noise == n_cols;
+  }
+};
+
 struct b3d_gpu_context {
   int device = 0;
   int sm_count = 0;
@@ -355,7 +378,11 @@ struct b3d_gpu_context {
   bool has_obs = false;
   DevBuf obs_depth, obs_pts, obs_count;
   bool has_lik = false;
-  KLik lik{};
+  KLik lik{};                 // first fused chunk (window for launch plans)
+  LikSpec spec;               // score-cells seam (gated)
+  LikSpec cam_spec;           // windowed_log_likelihood_multi seam (camera paths)
+  std::string cam_spec_err;   // why cam_spec is unusable ("" = usable)
+  DevBuf chunk_scores, ex_depth, ex_pts;
   double sigma_max = 0.1;
   int prefactor = B3D_PREFACTOR_PRINTED;
   DevBuf zscratch, vscratch;
@@ -697,31 +724,17 @@ void finish_copy_out(b3d_gpu_context* ctx, void* dst, const void* src, size_t by
              "cudaMemcpyAsync D2H");
 }
 
-// windowed_log_likelihood_multi settings (likelihood.cpp:14-26,162-186):
-// per-noise coefficients and the distinct-sigma slots, validated like the
-// reference (validate_noise).
+// windowed_log_likelihood_multi settings (likelihood.cpp:14-26,162-186) for
+// one fused launch: per-noise coefficients and the distinct-sigma slots.
 KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
               double sigma_max, int window, int prefactor) {
-  require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
-  require(n_noise <= (uint32_t)kMaxNoise, ErrorCode::invalid,
-          "gpu context: at most 12 noise settings per call");
-  require(window >= 0, ErrorCode::invalid, "window radius must be >= 0");
-  require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
-          ErrorCode::invalid, "unknown prefactor");
   const double vol = visible_volume(k);
-  require(vol > 0, ErrorCode::invalid, "scene volume must be positive");
   KLik L{};
   L.n_noise = (int)n_noise;
   L.window = window;
   std::vector<double> slots;
   for (uint32_t e = 0; e < n_noise; ++e) {
     const b3d_noise& np = noise[e];
-    require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
-    require(np.sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
-    require(np.p_outlier >= 0 && np.p_outlier <= 1, ErrorCode::invalid,
-            "p_outlier must be in [0,1]");
-    require(np.p_outlier > 0, ErrorCode::invalid,
-            "gpu context: p_outlier must be > 0 on the fp32 likelihood path");
     const double sigma2 = np.sigma_noise * np.sigma_noise;
     L.one_minus_p[e] = 1.0 - np.p_outlier;
     L.norm3[e] = std::pow(6.283185307179586476925287 * sigma2, -1.5);
@@ -734,12 +747,102 @@ KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
     if (s == slots.size()) slots.push_back(np.sigma_noise);
     L.slot_of[e] = (int)s;
   }
-  require(slots.size() <= (size_t)kMaxSlots, ErrorCode::invalid,
-          "gpu context: at most 4 distinct sigma values per call");
   L.n_slots = (int)slots.size();
   for (size_t s = 0; s < slots.size(); ++s)
     L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
   return L;
+}
+
+// The same entries for the fp64 image path (exact_score.cu), with each
+// form's own rounding of 1/(2 sigma^2): windowed 1/((2 s) s)
+// (likelihood.cpp:186-187), full 1/(2 (s s)) (likelihood.cpp:91-92).
+KExactLik make_exact_lik(const KLik& L, const b3d_noise* noise, int window) {
+  KExactLik X{};
+  X.n_noise = L.n_noise;
+  X.n_slots = L.n_slots;
+  X.window = window;
+  for (int e = 0; e < L.n_noise; ++e) {
+    X.slot_of[e] = L.slot_of[e];
+    X.one_minus_p[e] = L.one_minus_p[e];
+    X.norm3[e] = L.norm3[e];
+    X.floor_term[e] = L.floor_term[e];
+    X.prefactor[e] = L.prefactor[e];
+    const double sg = noise[e].sigma_noise;
+    X.inv2s2[L.slot_of[e]] = window >= 0 ? 1.0 / (2.0 * sg * sg) : 1.0 / (2.0 * (sg * sg));
+  }
+  return X;
+}
+
+// Outlier probabilities below this take the fp64 image path: with the floor
+// p/V that small, an fp32 window sum that underflows to 0 (exp of < -103)
+// changes the pixel's term from log(coef * S) (finite in fp64 down to exp of
+// -745) to log(floor); above it coef * S at fp32 underflow is < 1e-25 of
+// the floor and the fused kernel's terms are exact to its tolerance.
+constexpr double kExactOutlierP = 1e-6;
+
+// Likelihood settings of one score call (b3d_gpu_set_likelihood, a
+// coarse-to-fine stage): the noise entries split into launches the fused
+// kernel supports -- contiguous runs of <= kMaxNoise entries with <=
+// kMaxSlots distinct sigmas -- plus the columns that score -inf.
+//
+// gate = true is the inference seam (score_cells -> observation_loglik_cached_multi,
+// inference.cpp:40-45,59-83): an entry outside the noise support (p_outlier
+// outside [0,1], sigma_noise <= 0 or > sigma_max) scores -inf and the others
+// are scored; window < 0 selects the untruncated likelihood (inference.cpp:51-56).
+// gate = false is windowed_log_likelihood_multi itself (likelihood.cpp:137-141):
+// validate_noise errors, sigma_noise > sigma_max is scored, window >= 0.
+LikSpec make_spec(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
+                  double sigma_max, int window, int prefactor, bool gate) {
+  require(n_noise >= 1, ErrorCode::invalid, "no noise settings given");
+  require(gate || window >= 0, ErrorCode::invalid, "window radius must be >= 0");
+  require(prefactor == B3D_PREFACTOR_PRINTED || prefactor == B3D_PREFACTOR_UNIFORM,
+          ErrorCode::invalid, "unknown prefactor");
+  const double vol = visible_volume(k);
+  require(vol > 0, ErrorCode::invalid, "scene volume must be positive");
+  require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
+  LikSpec spec;
+  spec.n_cols = (int)n_noise;
+  spec.window = window;
+  spec.exact = window < 0;
+  std::vector<uint32_t> live;
+  for (uint32_t e = 0; e < n_noise; ++e) {
+    const b3d_noise& np = noise[e];
+    if (gate) {
+      if (!(np.p_outlier >= 0 && np.p_outlier <= 1 && np.sigma_noise > 0 &&
+            np.sigma_noise <= sigma_max)) {
+        spec.gated.push_back((int)e);
+        continue;
+      }
+    } else {
+      require(np.sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
+      require(np.p_outlier >= 0 && np.p_outlier <= 1, ErrorCode::invalid,
+              "p_outlier must be in [0,1]");
+    }
+    if (np.p_outlier < kExactOutlierP) spec.exact = true;
+    live.push_back(e);
+  }
+  // contiguous runs of live entries, cut at kMaxNoise entries / kMaxSlots sigmas
+  size_t i = 0;
+  while (i < live.size()) {
+    size_t j = i;
+    std::vector<double> slots;
+    while (j < live.size() && (j == i || live[j] == live[j - 1] + 1) && j - i < (size_t)kMaxNoise) {
+      const double sg = noise[live[j]].sigma_noise;
+      if (std::find(slots.begin(), slots.end(), sg) == slots.end()) {
+        if (slots.size() == (size_t)kMaxSlots) break;
+        slots.push_back(sg);
+      }
+      ++j;
+    }
+    LikChunk c;
+    c.col0 = (int)live[i];
+    c.lik = make_lik(k, noise + live[i], (uint32_t)(j - i), sigma_max, window < 0 ? 0 : window,
+                     prefactor);
+    c.ex = make_exact_lik(c.lik, noise + live[i], window);
+    spec.chunks.push_back(c);
+    i = j;
+  }
+  return spec;
 }
 
 // ------------------------------------------------ table contact (host side)
@@ -935,6 +1038,116 @@ b3d_pose contact_cell_pose(const KGrid& g, const std::vector<double>& spin, uint
   return b3d_pose{q.w, q.x, q.y, q.z, r[0] + pv[0], r[1] + pv[1], r[2] + pv[2]};
 }
 
+// The fp64 image path (exact_score.cu): render the hypotheses of p in chunks
+// (render-mode kernel, depth to HBM), then score every image per chunk of
+// noise entries.  p is a score-mode parameter block (object or camera mode,
+// base attached); d_scores n x spec.n_cols and d_status are device memory.
+void exact_scores(b3d_gpu_context* ctx, const Mesh& m, const KParams& p, const LikSpec& spec,
+                  long long n, double* d_scores, uint8_t* d_status, bool camera) {
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  const long long chunk = std::max<long long>(1, std::min<long long>(n, (256ll << 20) / (4 * npx)));
+  ctx->ex_depth.ensure(4 * npx * (size_t)chunk);
+  const int ctas = (int)std::min<long long>(chunk, 4ll * ctx->sm_count);
+  if (spec.window < 0) ctx->ex_pts.ensure(exact_score_pts_bytes((int)ctx->k.width, (int)ctx->k.height, ctas));
+  for (long long h0 = 0; h0 < n; h0 += chunk) {
+    const long long c = std::min(chunk, n - h0);
+    KParams q = p;
+    q.lik.n_noise = 0;  // render only
+    if (!camera) attach_base(ctx, q);
+    q.scores = nullptr;
+    q.status = nullptr;
+    q.n_score_peers = 0;
+    q.rng_dst = nullptr;
+    q.n_hyp = c;
+    if (camera)
+      q.cams = p.cams + h0;
+    else if (p.poses)
+      q.poses = p.poses + h0;
+    else
+      q.index0 = p.index0 + h0;
+    q.out_depth = ctx->ex_depth.as<float>();
+    q.out_ids = nullptr;
+    q.out_keys = nullptr;
+    LaunchPlan lp = plan_launch<false, false, true>(ctx, m, c);
+    q.zscratch = ctx->zscratch.as<unsigned long long>();
+    q.vscratch = ctx->vscratch.as<double>();
+    q.vcap = lp.vcap;
+    q.zcap = lp.zcap;
+    q.zstride = lp.zstride;
+    cuda_check(launch_render_score<false, false, true>(q, lp.grid, lp.smem, ctx->stream),
+               "render launch (fp64 path)");
+    for (const LikChunk& ch : spec.chunks) {
+      KExactArgs a{};
+      a.obs = ctx->obs_pts.as<float4>();
+      a.rend = ctx->ex_depth.as<float>();
+      a.W = (int)ctx->k.width;
+      a.H = (int)ctx->k.height;
+      a.fx = ctx->k.fx;
+      a.fy = ctx->k.fy;
+      a.cx = ctx->k.cx;
+      a.cy = ctx->k.cy;
+      a.far_f = static_cast<float>(ctx->k.far_m);
+      a.n = c;
+      a.scores = d_scores + (size_t)h0 * spec.n_cols;
+      a.ld = spec.n_cols;
+      a.col0 = ch.col0;
+      a.status = d_status ? d_status + h0 : nullptr;
+      a.pts = spec.window < 0 ? ctx->ex_pts.as<double>() : nullptr;
+      a.lik = ch.ex;
+      cuda_check(launch_exact_score(a, (int)std::min<long long>(c, ctas), ctx->stream),
+                 "exact_score launch");
+    }
+  }
+}
+
+// Scores the n hypotheses of p (score mode, everything set but lik / scores /
+// status / plan) under `spec` into device arrays: one fused launch when the
+// spec fits it, else one launch per chunk of entries (columns copied into
+// place), -inf for gated columns, or the fp64 image path.
+void run_scores(b3d_gpu_context* ctx, const Mesh& m, KParams p, const LikSpec& spec, long long n,
+                double* d_scores, uint8_t* d_status, bool camera, size_t zhint,
+                bool pdl = false) {
+  const int nc = spec.n_cols;
+  for (int col : spec.gated)
+    cuda_check(launch_fill_column(d_scores, n, nc, col, -std::numeric_limits<double>::infinity(),
+                                  ctx->stream),
+               "fill launch");
+  if (spec.chunks.empty()) {  // every entry outside the support: nothing rendered
+    if (d_status) cuda_check(cudaMemsetAsync(d_status, 0, (size_t)n, ctx->stream), "memset");
+    return;
+  }
+  if (spec.exact) {
+    exact_scores(ctx, m, p, spec, n, d_scores, d_status, camera);
+    return;
+  }
+  const bool in_place = spec.single();
+  if (!in_place) {
+    p.n_score_peers = 0;
+    size_t widest = 0;
+    for (const LikChunk& ch : spec.chunks) widest = std::max(widest, (size_t)ch.lik.n_noise);
+    ctx->chunk_scores.ensure(8 * widest * (size_t)n);
+  }
+  for (const LikChunk& ch : spec.chunks) {
+    p.lik = ch.lik;
+    if (!camera) attach_base(ctx, p);
+    p.scores = in_place ? d_scores : ctx->chunk_scores.as<double>();
+    p.status = d_status;
+    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, n, ch.lik.window, camera, zhint);
+    p.zscratch = ctx->zscratch.as<unsigned long long>();
+    p.vscratch = ctx->vscratch.as<double>();
+    p.vcap = lp.vcap;
+    p.zcap = lp.zcap;
+    p.zstride = lp.zstride;
+    cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream, pdl),
+               camera ? "render_score launch (cameras)" : "render_score launch");
+    if (!in_place)
+      cuda_check(cudaMemcpy2DAsync(d_scores + ch.col0, 8ull * nc, p.scores,
+                                   8ull * ch.lik.n_noise, 8ull * ch.lik.n_noise, (size_t)n,
+                                   cudaMemcpyDeviceToDevice, ctx->stream),
+                 "cudaMemcpy2DAsync scores");
+  }
+}
+
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
                   const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
                   const b3d_contact_cells* contact = nullptr, uint64_t first = 0,
@@ -987,7 +1200,8 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   }
   p.n_hyp = (long long)n;
   p.index0 = (long long)first;
-  const int nn = ctx->lik.n_noise;
+  const LikSpec& spec = ctx->spec;
+  const int nn = spec.n_cols;
   const bool dev_scores = is_device_ptr(scores);
   const bool dev_status = status && is_device_ptr(status);
   if (dev_scores) {
@@ -1004,22 +1218,14 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
       p.status = ctx->out_stage2.as<uint8_t>();
     }
   }
-  attach_base(ctx, p);
   size_t zhint = 0;
   if (poses && host_in) {
-    zhint = region_hint_poses(ctx, m, poses, n, ctx->lik.window);
+    zhint = region_hint_poses(ctx, m, poses, n, std::max(spec.window, 0));
   } else if (!poses && !contact) {
     zhint = region_hint(ctx, m, p.grid.center,
-                        std::sqrt(sq3(grid->extent)), ctx->lik.window);
+                        std::sqrt(sq3(grid->extent)), std::max(spec.window, 0));
   }
-  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n, -1, false, zhint);
-  p.zscratch = ctx->zscratch.as<unsigned long long>();
-  p.vscratch = ctx->vscratch.as<double>();
-  p.vcap = lp.vcap;
-  p.zcap = lp.zcap;
-  p.zstride = lp.zstride;
-  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
-             "render_score launch");
+  run_scores(ctx, m, p, spec, (long long)n, p.scores, p.status, false, zhint);
   if (stage_out)
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, stage_rng, stage_out, nullptr,
                                    ctx->stream, stage_scratch(ctx, (long long)n)),
@@ -1159,21 +1365,13 @@ void cam_params(b3d_gpu_context* ctx, KParams& p) {
 // device buffers scores/status
 void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, double* scores,
                           uint8_t* status, bool pdl = false) {
+  require(ctx->cam_spec_err.empty(), ErrorCode::invalid, ctx->cam_spec_err);
   const Mesh& m = *ctx->cam_mesh;
   KParams p = base_params(ctx, m);
   cam_params(ctx, p);
   p.cams = cams;
   p.n_hyp = n;
-  p.scores = scores;
-  p.status = status;
-  LaunchPlan lp = plan_launch<false, true, false>(ctx, m, n, -1, true);
-  p.zscratch = ctx->zscratch.as<unsigned long long>();
-  p.vscratch = ctx->vscratch.as<double>();
-  p.vcap = lp.vcap;
-  p.zcap = lp.zcap;
-  p.zstride = lp.zstride;
-  cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream, pdl),
-             "render_score launch (cameras)");
+  run_scores(ctx, m, p, ctx->cam_spec, n, scores, status, true, 0, pdl);
 }
 }  // namespace
 
@@ -1427,7 +1625,16 @@ b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
   return guarded([&] {
     check(ctx && noise, "bad arguments");
     require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
-    ctx->lik = make_lik(ctx->k, noise, n_noise, sigma_max, window, prefactor);
+    ctx->spec = make_spec(ctx->k, noise, n_noise, sigma_max, window, prefactor, true);
+    try {
+      ctx->cam_spec = make_spec(ctx->k, noise, n_noise, sigma_max, window, prefactor, false);
+      ctx->cam_spec_err.clear();
+    } catch (const Error& e) {
+      ctx->cam_spec = LikSpec{};
+      ctx->cam_spec_err = e.what();
+    }
+    ctx->lik = ctx->spec.chunks.empty() ? KLik{} : ctx->spec.chunks[0].lik;
+    ctx->lik.window = std::max(window, 0);
     ctx->sigma_max = sigma_max;
     ctx->prefactor = prefactor;
     ctx->has_lik = true;
@@ -1697,7 +1904,8 @@ b3d_status b3d_gpu_score_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras, 
     bool host_in = false;
     const KPose* cams = static_cast<const KPose*>(
         stage_in(ctx, ctx->in_stage, cameras, sizeof(b3d_pose) * n, &host_in));
-    const int nn = ctx->lik.n_noise;
+    require(ctx->cam_spec_err.empty(), ErrorCode::invalid, ctx->cam_spec_err);
+    const int nn = ctx->cam_spec.n_cols;
     const bool dev_scores = is_device_ptr(scores);
     const bool dev_status = status && is_device_ptr(status);
     double* d_scores = scores;
@@ -1732,7 +1940,8 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
     require(n_frames >= 1, ErrorCode::invalid, "track_camera: empty frame list");
     require_ready(ctx, false, true);
     require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
-    require(ctx->lik.n_noise == 1, ErrorCode::invalid, "track_camera: one noise setting");
+    require(ctx->cam_spec_err.empty(), ErrorCode::invalid, ctx->cam_spec_err);
+    require(ctx->cam_spec.n_cols == 1, ErrorCode::invalid, "track_camera: one noise setting");
     const b3d_track_search& s = *search;
     // TrackSearch::validate (tracking.cpp:49-57)
     require(s.pos_extent > 0 && s.angle_extent > 0, ErrorCode::invalid,
@@ -1799,7 +2008,7 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
         w = (int)std::min<double>((double)w * ppd, 1 << 21);
         tab_n += w;
       }
-      if (s.beam_width == 1 && tab_n <= (1 << 20)) {
+      if (s.beam_width == 1 && tab_n <= (1 << 20) && ctx->cam_spec.single()) {
         // the frame's stages chained on the device (track.cu): every lattice
         // value the frame can visit and its sin / cos from this libm, one
         // upload, ppd^3 poses / score / argmax per stage, one read-back
@@ -2060,9 +2269,11 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
                                                     region_hint(ctx, m, c0, spread, w_max));
     for (uint32_t s = 0; s < n_stages; ++s) {
       const b3d_stage_spec& g = stages[s];
+      // coarse_to_fine_propose scores through score_cells (inference.cpp:381):
+      // the gated inference seam
+      const LikSpec spec =
+          make_spec(ctx->k, &g.noise, 1, ctx->sigma_max, g.window, ctx->prefactor, true);
       KParams p = base_params(ctx, m);
-      p.lik = make_lik(ctx->k, &g.noise, 1, ctx->sigma_max, g.window, ctx->prefactor);
-      attach_base(ctx, p);
       p.poses = nullptr;
       p.grid.center_dev = d_centers + s;
       for (int a = 0; a < 3; ++a) {
@@ -2075,13 +2286,19 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
       p.n_hyp = (long long)n[s];
       p.scores = ctx->c2f_scores.as<double>();
       p.status = nullptr;
-      p.zscratch = ctx->zscratch.as<unsigned long long>();
-      p.vscratch = ctx->vscratch.as<double>();
-      p.vcap = lp.vcap;
-      p.zcap = lp.zcap;
-      p.zstride = lp.zstride;
-      cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
-                 "render_score launch");
+      if (spec.single()) {
+        p.lik = spec.chunks[0].lik;
+        attach_base(ctx, p);
+        p.zscratch = ctx->zscratch.as<unsigned long long>();
+        p.vscratch = ctx->vscratch.as<double>();
+        p.vcap = lp.vcap;
+        p.zcap = lp.zcap;
+        p.zstride = lp.zstride;
+        cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
+                   "render_score launch");
+      } else {
+        run_scores(ctx, m, p, spec, (long long)n[s], p.scores, nullptr, false, 0);
+      }
       const bool sample = g.select == B3D_SELECT_SAMPLE;
       cuda_check(launch_stage_reduce(p.scores, (long long)n[s], 1, 0, sample ? d_rng : nullptr,
                                      d_res + s, nullptr, ctx->stream,
@@ -2238,7 +2455,8 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
     p.poses = static_cast<const KPose*>(
         stage_in(ctx, ctx->in_stage, poses, sizeof(b3d_pose) * n, &host_in));
     p.n_hyp = (long long)n;
-    const int nn = ctx->lik.n_noise;
+    const LikSpec& spec = ctx->spec;
+    const int nn = spec.n_cols;
     // device layout: scores (n x n_noise), then the stage result (64 B) and
     // the Rng state (40 B), so one read-back returns everything
     const size_t sbytes = sizeof(double) * n * nn;
@@ -2265,8 +2483,16 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
         std::memcpy(p.rng_init, rng_state, 40);
       }
     }
-    cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
-               "render_score launch");
+    if (spec.single()) {
+      cuda_check(launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream),
+                 "render_score launch");
+    } else {
+      if (p.rng_dst)
+        cuda_check(cudaMemcpyAsync(p.rng_dst, rng_state, 40, cudaMemcpyHostToDevice, ctx->stream),
+                   "cudaMemcpyAsync rng");
+      p.rng_dst = nullptr;
+      run_scores(ctx, m, p, spec, (long long)n, p.scores, nullptr, false, 0);
+    }
     cuda_check(launch_stage_reduce(p.scores, (long long)n, nn, 0, d_rng, d_out, nullptr,
                                    ctx->stream, stage_scratch(ctx, (long long)n)),
                "stage_reduce launch");

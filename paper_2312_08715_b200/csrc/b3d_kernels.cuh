@@ -154,4 +154,27 @@ struct KStageResult {
   unsigned int pad;
 };
 
+// fp64 image likelihood (exact_score.cu): one chunk of <= kMaxNoise noise
+// entries with <= kMaxSlots distinct sigmas, window < 0 = full likelihood
+struct KExactLik {
+  int n_noise, n_slots, window;
+  int slot_of[kMaxNoise];
+  double inv2s2[kMaxSlots];  // 1 / (2 sigma^2) in the form's own rounding order
+  double one_minus_p[kMaxNoise], norm3[kMaxNoise], floor_term[kMaxNoise], prefactor[kMaxNoise];
+};
+
+struct KExactArgs {
+  const float4* obs;  // W x H observation cache (x, y, z, valid); z is the raw depth
+  const float* rend;  // n x W x H rendered depth (sentinel = (float)far)
+  int W, H;
+  double fx, fy, cx, cy;
+  float far_f;
+  long long n;
+  double* scores;  // scores[h * ld + col0 + e]
+  int ld, col0;
+  uint8_t* status;  // 1 = empty render (may be null)
+  double* pts;      // full form: per-CTA rendered cloud, 3 x W x H doubles per CTA
+  KExactLik lik;
+};
+
 }  // namespace b3d200

@@ -544,8 +544,8 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     }
     const double sigma_max = r.num_or("sigma_max", 0.1);
     const long long window = r.int_or("window", 2);
-    require(window >= 0, B3D_ERROR_CONFIG,
-            "b3d_infer: the untruncated likelihood (window < 0) is not on the B200 path");
+    // window < 0: ModelConfig::windowed = false, the untruncated likelihood
+    // (b3d_capi.cpp:328-330) -- scored on the device's fp64 image path
     double tw, th, thick;
     {
       Reader tr = r.object("table");
@@ -557,8 +557,7 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     }
     b3d_smc_config cfg{};
     cfg.stage0 = {10, 10, 8};  // Schedule defaults (inference.hpp:30-31)
-    cfg.n_refine = 2;
-    cfg.refine[0] = cfg.refine[1] = {5, 5, 5};
+    std::vector<b3d_schedule_stage> refine{{5, 5, 5}, {5, 5, 5}};
     if (r.has("schedule")) {
       Reader sr = r.object("schedule");
       auto stage = [](const J::Value& v) {
@@ -572,10 +571,9 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
       };
       cfg.stage0 = stage(sr.raw("stage0"));
       const J::Value& rf = sr.raw("refine");
-      require(rf.is_array() && rf.arr.size() <= 4, B3D_ERROR_CONFIG,
-              "schedule: at most 4 refine stages on the B200 path");
-      cfg.n_refine = (uint32_t)rf.arr.size();
-      for (size_t i = 0; i < rf.arr.size(); ++i) cfg.refine[i] = stage(rf.arr[i]);
+      require(rf.is_array(), B3D_ERROR_CONFIG, "schedule stages must be [n_dx, n_dy, n_dtheta]");
+      refine.clear();
+      for (const J::Value& v : rf.arr) refine.push_back(stage(v));
       sr.finish();
     }
     std::vector<b3d_noise> grid;  // default_noise_grid (inference.cpp:127-133)
@@ -615,6 +613,8 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     cfg.table_w = tw / 2 - (-tw / 2);  // ObjectModel::table extents
     cfg.table_h = th / 2 - (-th / 2);
     cfg.table_mesh = g_gpu.table(tw, th, thick);
+    cfg.n_refine = (uint32_t)refine.size();
+    cfg.refine = refine.data();
     cfg.noise_grid = grid.data();
     cfg.n_noise_grid = (uint32_t)grid.size();
     cfg.sigma_max = sigma_max;

@@ -582,7 +582,7 @@ extern "C" b3d_status b3d_gpu_run_smc(b3d_gpu_context* ctx, const b3d_smc_object
     need(cfg->n_objects >= 1 && cfg->n_objects <= B3D_SMC_MAX_CHILDREN, B3D_ERROR,
          "run_smc: n_objects must be in 1..8");
     need(cfg->n_particles >= 1, B3D_ERROR, "smc_init: need at least one particle");
-    need(cfg->n_refine <= 4, B3D_ERROR, "run_smc: at most 4 refine stages");
+    need(cfg->n_refine == 0 || cfg->refine, B3D_ERROR, "bad arguments");
     auto valid = [](const b3d_schedule_stage& s) {
       return s.n_dx >= 1 && s.n_dy >= 1 && s.n_dtheta >= 1;
     };
