@@ -462,41 +462,47 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
     mid = mids[1 + w["target"]]
 
     # N > 1: scores stored straight into every rank's symmetric-memory copy
-    # of the 1M-entry array by the score kernel (fused all-gather over
-    # NVLink), checked once against the NCCL gather; NCCL otherwise
-    p2p = None
+    # of the 1M-entry array by the score kernel (the all-gather fused into the
+    # scoring over NVLink), the ranks meet on a device signal-pad barrier,
+    # every rank reduces / samples its complete copy; the two halves of each
+    # copy alternate per exchange so no rank overwrites a half a peer may
+    # still be reading.  Checked once against the NCCL gather; NCCL otherwise.
+    xch = None
     gather = "single rank" if world == 1 else "nccl all_gather_into_tensor"
     if world > 1:
         try:
-            import torch.distributed._symmetric_memory as symm_mem
-            sym = symm_mem.empty(n, 1, dtype=torch.float64, device="cuda")
-            hdl = symm_mem.rendezvous(sym, dist.group.WORLD)
-            p2p = (sym, hdl, [int(x) for x in hdl.buffer_ptrs])
+            from paper_2312_08715_b200.shard import SymmetricExchange
+            xch = SymmetricExchange(n, 1, torch.device("cuda", torch.cuda.current_device()))
         except Exception as e:  # pragma: no cover - depends on the box
             gather = f"nccl all_gather_into_tensor (symmetric memory unavailable: {e})"
 
-    def once(use_p2p=True):
-        ctx.score_grid_range(mid, grid, lo, hi - lo, d_local, None)
-        if p2p is not None and use_p2p:
-            p2p[1].barrier(channel=0)
-            allv = p2p[0]
+    def once(use_x=True):
+        if xch is not None and use_x:
+            e = xch.epoch + 1
+            own = xch.half(e)
+            ctx.set_score_peers(xch.peer_ptrs(e), lo, n)
+            ctx.score_grid_range(mid, grid, lo, hi - lo, own[lo:hi], None)
+            ctx.set_score_peers([], 0)
+            xch.epoch = e
+            ctx.shard_barrier(xch.signal_ptrs, rank, e)
+            allv = own
         else:
+            ctx.score_grid_range(mid, grid, lo, hi - lo, d_local, None)
             allv = gather_scores(d_local, n, world)
-        return ctx.sample_many(allv, 1000, st, n=n, samples=d_samples)
+        return allv, ctx.sample_many(allv, 1000, st, n=n, samples=d_samples)
 
-    once(use_p2p=False)  # warm-up (builds the base-scene likelihood terms)
-    if p2p is not None:
+    once(use_x=False)  # warm-up (builds the base-scene likelihood terms)
+    if xch is not None:
         ref_all = gather_scores(d_local, n, world).clone()
-        ctx.set_score_peers(p2p[2], lo)
-        once()
+        allv, _ = once()
         torch.cuda.synchronize()
-        same = torch.tensor([1 if torch.equal(p2p[0], ref_all) else 0], device="cuda")
+        same = torch.tensor([1 if torch.equal(allv, ref_all) else 0], device="cuda")
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
         if int(same.item()) == 1:
-            gather = "fused into the score kernel (NVLink remote stores to symmetric memory)"
+            gather = ("fused into the score kernel (NVLink remote stores to symmetric memory, "
+                      "signal-pad barrier, double-buffered)")
         else:
-            ctx.set_score_peers([], 0)
-            p2p = None
+            xch = None
             gather = "nccl all_gather_into_tensor (fused path disagreed; fell back)"
     torch.cuda.synchronize()
     if world > 1:
@@ -505,13 +511,11 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _, r = once()
+        _, (_, r) = once()
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
     t = max(times)
-    if p2p is not None:
-        ctx.set_score_peers([], 0)
     if world > 1:
         tt_ = torch.tensor([t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
@@ -525,6 +529,39 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
             "argmax": int(r.argmax), "logsumexp": r.logsumexp, "score_gather": gather}
 
 
+def spawn_ranks(args):
+    """`bench.py --gpus N` run directly: re-launch as N ranks under
+    torch.distributed.run on 127.0.0.1 (the driver's own launch), so the
+    line reports the N-rank measurement, never a silent single rank."""
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1", "--master-port",
+           str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    os.execv(sys.executable, cmd)
+
+
+def dry_run(args, rank, world):
+    """--dry-run: the ranks rendezvous (gloo, no GPU work) and all-reduce their
+    ranks; rank 0 prints one line.  Checks the N-rank launch on CPU."""
+    import torch
+    import torch.distributed as dist
+    total = rank
+    if world > 1:
+        dist.init_process_group("gloo")
+        t = torch.tensor([rank], dtype=torch.int64)
+        dist.all_reduce(t)
+        total = int(t.item())
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps({"dry_run": True, "n_gpus": world, "rank_sum": total,
+                          "impl": args.impl}), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -535,12 +572,20 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--tracking-frames", type=int, default=100)
     ap.add_argument("--no-extra", action="store_true", help="skip the cfg2/cfg4 legs")
+    ap.add_argument("--dry-run", action="store_true",
+                    help="launch / rendezvous check only: ranks meet over gloo, rank 0 prints")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        return spawn_ranks(args)  # one process per GPU, as the driver's torchrun would
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "ours" and world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if args.dry_run:
+        return dry_run(args, rank, world)
     if args.impl == "reference":
         return run_reference(args, rank, world)
 
@@ -584,36 +629,34 @@ def main():
     d_res = torch.zeros(64, dtype=torch.uint8, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)  # > 126 MB L2
 
-    # N > 1: the score all-gather fused into the score kernel -- every rank
-    # stores its scores straight into all ranks' symmetric-memory copies of
-    # the global array over NVLink (b3d_gpu_set_score_peers), then one
-    # symmetric-memory barrier; NCCL all_gather_into_tensor is the fallback
-    # (and the check: both must give the same array, else NCCL is used).
-    p2p = None
+    # N > 1: one b3d_gpu_enumerate_shard call per step -- the score kernel
+    # stores every score straight into all ranks' symmetric-memory copies of
+    # the global array over NVLink (the all-gather fused into the scoring), a
+    # device signal-pad barrier, then every rank reduces its complete copy
+    # (the copies' two halves alternate per step: no write-after-read race).
+    # NCCL all_gather_into_tensor is the fallback and the check: both must
+    # give the same global array, else NCCL is used.
+    xch = None
     gather = "single rank"
     if world > 1:
         gather = "nccl all_gather_into_tensor"
         try:
-            import torch.distributed._symmetric_memory as symm_mem
-            sym = symm_mem.empty(n_all, 1, dtype=torch.float64, device=dev)
-            hdl = symm_mem.rendezvous(sym, dist.group.WORLD)
-            p2p = (sym, hdl, [int(x) for x in hdl.buffer_ptrs])
+            from paper_2312_08715_b200.shard import SymmetricExchange
+            xch = SymmetricExchange(n_all, 1, dev)
         except Exception as e:  # pragma: no cover - depends on the box
             gather = f"nccl all_gather_into_tensor (symmetric memory unavailable: {e})"
 
-    def step(ev_k=None, use_p2p=True):
+    def step(ev_k=None, use_x=True):
         if world == 1:  # score-many + stage reduction through one API call
             ctx.enumerate_grid(mid, grid, d_rng, d_res, d_scores)
             if ev_k is not None:
                 ev_k.record(stream)
             return
-        if p2p is not None and use_p2p:
-            sym, hdl, _ = p2p
-            ctx.score_grid(mid, grid, d_scores, d_status)  # + remote stores to every rank
+        if xch is not None and use_x:
+            ctx.enumerate_shard(mid, xch.exchange(rank * BATCH), grid=grid, n_local=BATCH,
+                                rng_state=d_rng, out=d_res)
             if ev_k is not None:
                 ev_k.record(stream)
-            hdl.barrier(channel=0)
-            ctx.stage_reduce(sym, n=n_all, rng_state=d_rng, out=d_res)
             return
         ctx.score_grid(mid, grid, d_scores, d_status)
         if ev_k is not None:
@@ -621,18 +664,17 @@ def main():
         dist.all_gather_into_tensor(d_all, d_scores)
         ctx.stage_reduce(d_all, n=n_all, rng_state=d_rng, out=d_res)
 
-    if p2p is not None:
-        step(use_p2p=False)  # reference gather
-        ctx.set_score_peers(p2p[2], rank * BATCH)
+    if xch is not None:
+        step(use_x=False)  # reference gather into d_all
         step()
         torch.cuda.synchronize()
-        same = torch.tensor([1 if torch.equal(p2p[0], d_all) else 0], device=dev)
+        same = torch.tensor([1 if torch.equal(xch.half(), d_all) else 0], device=dev)
         dist.all_reduce(same, op=dist.ReduceOp.MIN)
         if int(same.item()) == 1:
-            gather = "fused into the score kernel (NVLink remote stores to symmetric memory)"
+            gather = ("fused into the score kernel (b3d_gpu_enumerate_shard: NVLink remote "
+                      "stores to symmetric memory, signal-pad barrier, double-buffered)")
         else:
-            ctx.set_score_peers([], 0)
-            p2p = None
+            xch = None
             gather = "nccl all_gather_into_tensor (fused path disagreed; fell back)"
     for _ in range(args.warmup):
         step()
@@ -654,8 +696,6 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    if p2p is not None:
-        ctx.set_score_peers([], 0)  # only the timed batch writes into the symmetric array
     step_ms = [e0.elapsed_time(e1) for e0, _, e1 in evs]
     # the score kernel alone (roofline): same batch, L2 flushed before each
     # launch, CUDA events on the launching stream, outside the timed steps
@@ -682,6 +722,9 @@ def main():
     def e2e_step():
         if world == 1:  # one boundary call: upload observation + poses, score, reduce, read back
             return ctx.enumerate_observed(mid, h_obs, h_poses, rng_state=h_rng, scores=h_scores)
+        if xch is not None:  # one boundary call: observation + shard in, fused gather, result out
+            return ctx.enumerate_shard(mid, xch.exchange(rank * BATCH), poses=h_poses,
+                                       depth=h_obs, rng_state=h_rng)
         ctx.set_observation(h_obs)  # pinned: stream-ordered upload
         ctx.score_poses(mid, h_poses, h_scores, h_status)
         t = torch.from_numpy(h_scores).to(dev)
@@ -768,12 +811,16 @@ def main():
             "gpu_launches": 2 * args.steps,  # render_score + stage_reduce per step
             "e2e": {"value": e2e_value, "unit": UNIT,
                     # N = 1: observation + poses + Rng state in; scores + stage result +
-                    # Rng state out (b3d_gpu_enumerate_poses).  N > 1 adds the status
-                    # bytes out and the gathered scores back in for the host reduction.
+                    # Rng state out (b3d_gpu_enumerate_observed).  N > 1
+                    # (b3d_gpu_enumerate_shard): observation + shard poses + Rng in,
+                    # stage result + Rng out; the gather stays on the devices.
                     "h2d_bytes_per_step": int(h_obs.nbytes + h_poses.nbytes + 40
-                                              + (8 * n_all if world > 1 else 0)),
-                    "d2h_bytes_per_step": int(h_scores.nbytes + 64 + 40
-                                              + (h_status.nbytes if world > 1 else 0)),
+                                              + (0 if world == 1 or xch is not None
+                                                 else h_scores.nbytes + h_all.nbytes)),
+                    "d2h_bytes_per_step": int(h_scores.nbytes + 64 + 40 if world == 1
+                                              else 64 + 40 if xch is not None
+                                              else h_scores.nbytes + h_status.nbytes
+                                              + h_all.nbytes + 64 + 40),
                     "ms_per_step": e2e_total / args.steps},
             "clocks": clk,
             "roofline": roof,

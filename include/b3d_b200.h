@@ -211,14 +211,28 @@ B3D_API b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* verti
                                        uint64_t n_vertices, const uint32_t* triangles,
                                        uint64_t n_triangles, int32_t* out_mesh_id);
 /* Fused score all-gather for one-process-per-GPU runs:
- * every score-many launch of this context also stores score (h, e) into
- * peer_ptrs[r][(offset + h) * n_noise + e] for r < n_peers -- device
- * addresses of each rank's copy of the global score array, mapped on this
- * device (e.g. symmetric memory over NVLink); the caller makes the ranks
- * meet (a symmetric-memory barrier) before reading.  n_peers = 0 turns it
- * off. */
+ * score_poses / score_grid / score_grid_range / enumerate_grid launches of
+ * this context also store score (h, e) into peer_ptrs[r][(offset + h) *
+ * n_noise + e] for r < n_peers -- device addresses of each rank's copy of the
+ * global score array, mapped on this device (e.g. symmetric memory over
+ * NVLink) -- when that element index is below `capacity` (elements per
+ * array).  The caller makes the ranks meet (b3d_gpu_shard_barrier) before
+ * reading, and must not let a rank write an array a peer may still be
+ * reading (alternate two arrays: see b3d_gpu_enumerate_shard).  n_peers = 0
+ * turns it off.  Other score paths (contact cells, camera mode, chains) never
+ * store to peers. */
 B3D_API b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t* peer_ptrs,
-                                           uint32_t n_peers, uint64_t offset);
+                                           uint32_t n_peers, uint64_t offset,
+                                           uint64_t capacity);
+/* Device barrier of the ranks of a sharded stage: rank `rank` stores `epoch`
+ * into slot `rank` of every rank's signal pad (signal_ptrs[r]: n_ranks u64,
+ * mapped on this device, zero-initialised once) with a system-scope release
+ * after a system fence, then waits until every slot of its own pad holds at
+ * least `epoch` (acquire).  Epochs must grow from call to call.  Stream
+ * ordered on the context stream; a rank that never arrives makes the call
+ * fail after 20 s instead of hanging the device. */
+B3D_API b3d_status b3d_gpu_shard_barrier(b3d_gpu_context* ctx, const uint64_t* signal_ptrs,
+                                         uint32_t n_ranks, uint32_t rank, uint64_t epoch);
 /* Back-face culling in score-many (default on).  Applies only to meshes the
  * upload found closed (every directed edge matched by its reverse) and only
  * to hypotheses with no vertex in front of z = near: a back face of a closed
@@ -364,6 +378,35 @@ B3D_API b3d_status b3d_gpu_enumerate_observed(b3d_gpu_context* ctx, int32_t mesh
                                               const float* depth, const b3d_pose* poses,
                                               uint64_t n, uint64_t* rng_state,
                                               b3d_stage_result* out, double* scores);
+
+/* One stage of a hypothesis-sharded enumeration in one call.
+ * Each rank's global score array (scores[r], peer-mapped) holds 2 x n_total
+ * x n_noise doubles: exchange `epoch` uses half (epoch & 1), so a rank never
+ * writes the half a slower peer may still be reducing (the barrier of
+ * exchange e+1 orders every rank's reduction of e before anyone's writes of
+ * e+2).  The call: b3d_gpu_set_observation(depth) when depth != NULL; score
+ * the n_local hypotheses (poses; or grid rows [offset, offset + n_local) of a
+ * global grid of n_total rows, rows [0, n_local) of a per-rank grid of any
+ * other size) with every score also stored into every rank's array at row
+ * offset + i (the all-gather fused into the score kernel); the signal-pad
+ * barrier; the stage reduction (argmax, logsumexp, one draw with rng_state)
+ * of this rank's complete array.  Every rank computes the same result,
+ * bitwise, for any rank count.  out / rng_state may be host (one read-back)
+ * or device memory. */
+typedef struct b3d_shard_exchange {
+  uint32_t n_ranks; /* <= 8 */
+  uint32_t rank;
+  uint64_t offset;  /* this rank's first global hypothesis */
+  uint64_t n_total; /* global hypotheses */
+  uint64_t scores[8];  /* rank r's global score array (2 x n_total x n_noise) */
+  uint64_t signals[8]; /* rank r's signal pad (n_ranks u64) */
+  uint64_t epoch;      /* > the previous exchange's */
+} b3d_shard_exchange;
+B3D_API b3d_status b3d_gpu_enumerate_shard(b3d_gpu_context* ctx, int32_t mesh_id,
+                                           const float* depth, const b3d_pose* poses,
+                                           const b3d_pose_grid* grid, uint64_t n_local,
+                                           const b3d_shard_exchange* ex, uint64_t* rng_state,
+                                           b3d_stage_result* out);
 
 /* score-many over a device pose grid followed by the stage reduction of
  * scores[:, 0] (argmax, logsumexp, one draw with rng_state if non-NULL) in

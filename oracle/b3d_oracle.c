@@ -786,13 +786,12 @@ static int windowed_loglik_cached(const obs_cache* oc, const float* rend,
     return 1; /* "windowed likelihood: empty rendered cloud" */
   }
 
-  /* 162-186 */
-  double coef[16], floor_term[16], slot_scale[16], slot_sigma[16], slot_sum[16];
-  size_t slot_of[16], n_slots = 0;
-  if (n_noise > 16) {
-    free(rp); free(rvalid);
-    return 1;
-  }
+  /* 162-186 (any number of noise entries) */
+  double* const nbuf = (double*)malloc(sizeof(double) * 5 * n_noise);
+  size_t* const slot_of = (size_t*)malloc(sizeof(size_t) * n_noise);
+  double *coef = nbuf, *floor_term = nbuf + n_noise, *slot_scale = nbuf + 2 * n_noise,
+         *slot_sigma = nbuf + 3 * n_noise, *slot_sum = nbuf + 4 * n_noise;
+  size_t n_slots = 0;
   for (size_t e = 0; e < n_noise; ++e) {
     const double sigma2 = noise[e].sigma_noise * noise[e].sigma_noise;
     coef[e] = (1.0 - noise[e].p_outlier) / rend_count * pow(kTwoPi * sigma2, -1.5);
@@ -840,6 +839,7 @@ static int windowed_loglik_cached(const obs_cache* oc, const float* rend,
     }
   }
   if (d2 != dist2) free(d2);
+  free(nbuf); free(slot_of);
   free(rp); free(rvalid);
   return 0;
 }

@@ -133,6 +133,24 @@ class SmcParticle(C.Structure):
                 ("log_weight", C.c_double)]
 
 
+class ShardExchange(C.Structure):
+    """b3d_shard_exchange: peer-mapped score arrays (2 x n_total x n_noise
+    doubles each) and signal pads (n_ranks u64 each) of every rank."""
+    _fields_ = [("n_ranks", C.c_uint32), ("rank", C.c_uint32), ("offset", C.c_uint64),
+                ("n_total", C.c_uint64), ("scores", C.c_uint64 * 8), ("signals", C.c_uint64 * 8),
+                ("epoch", C.c_uint64)]
+
+    @classmethod
+    def make(cls, rank, offset, n_total, score_ptrs, signal_ptrs, epoch):
+        ex = cls()
+        ex.n_ranks, ex.rank, ex.offset, ex.n_total = len(score_ptrs), rank, offset, n_total
+        for r, (a, b) in enumerate(zip(score_ptrs, signal_ptrs)):
+            ex.scores[r] = int(a)
+            ex.signals[r] = int(b)
+        ex.epoch = epoch
+        return ex
+
+
 class StageResult(C.Structure):
     _fields_ = [("argmax", C.c_uint64), ("sample", C.c_uint64), ("max_score", C.c_double),
                 ("logsumexp", C.c_double), ("total", C.c_double), ("sample_logp", C.c_double),
@@ -170,7 +188,10 @@ def lib() -> C.CDLL:
         "b3d_gpu_upload_mesh": ([vp, vp, u64, vp, u64, C.POINTER(i32)], st),
         "b3d_gpu_set_observation": ([vp, vp], st),
         "b3d_gpu_set_culling": ([vp, st], st),
-        "b3d_gpu_set_score_peers": ([vp, vp, u32, u64], st),
+        "b3d_gpu_set_score_peers": ([vp, vp, u32, u64, u64], st),
+        "b3d_gpu_shard_barrier": ([vp, vp, u32, u32, u64], st),
+        "b3d_gpu_enumerate_shard": ([vp, i32, vp, vp, vp, u64, C.POINTER(ShardExchange), vp, vp],
+                                    st),
         "b3d_gpu_set_camera_scene": ([vp, vp, vp, u32], st),
         "b3d_gpu_render_cameras": ([vp, vp, u64, vp, vp], st),
         "b3d_gpu_score_cameras": ([vp, vp, u64, vp, vp], st),
@@ -663,10 +684,39 @@ class GpuContext:
                                              _ptr(verts), _ptr(tris), C.byref(nv), C.byref(nt)))
         return verts[: nv.value], tris[: nt.value]
 
-    def set_score_peers(self, peer_ptrs, offset: int):
-        """Fused all-gather targets (b3d_gpu_set_score_peers); [] turns it off."""
+    def set_score_peers(self, peer_ptrs, offset: int, capacity: int = 0):
+        """Fused all-gather targets (b3d_gpu_set_score_peers): score (h, e) also
+        goes to peer[(offset + h) * n_noise + e] below `capacity` elements;
+        [] turns it off."""
         arr = (C.c_uint64 * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
-        _check(self._L.b3d_gpu_set_score_peers(self.h, arr, len(peer_ptrs), offset))
+        _check(self._L.b3d_gpu_set_score_peers(self.h, arr, len(peer_ptrs), offset, capacity))
+
+    def shard_barrier(self, signal_ptrs, rank: int, epoch: int):
+        """b3d_gpu_shard_barrier over the ranks' signal pads."""
+        arr = (C.c_uint64 * max(1, len(signal_ptrs)))(*[int(x) for x in signal_ptrs])
+        _check(self._L.b3d_gpu_shard_barrier(self.h, arr, len(signal_ptrs), rank, epoch))
+
+    def enumerate_shard(self, mesh: int, ex: "ShardExchange", poses=None, grid=None, depth=None,
+                        n_local: int = None, rng_state=None, out=None):
+        """b3d_gpu_enumerate_shard: [observation], this rank's shard scored into
+        every rank's array, barrier, stage reduction of the whole array.
+        Returns a StageOut (host out) or None (device out)."""
+        if isinstance(depth, np.ndarray):
+            depth = np.ascontiguousarray(depth, dtype=np.float32)
+        if isinstance(poses, np.ndarray):
+            poses = np.ascontiguousarray(poses, dtype=np.float64)
+        if n_local is None:
+            n_local = poses.shape[0]
+        res = StageResult() if out is None else None
+        _check(self._L.b3d_gpu_enumerate_shard(
+            self.h, mesh, _ptr(depth), _ptr(poses), C.byref(grid) if grid is not None else None,
+            n_local, C.byref(ex), _ptr(rng_state),
+            _ptr(out) if out is not None else C.addressof(res)))
+        if res is None:
+            return None
+        return StageOut(res.argmax, res.sample, res.max_score, res.logsumexp, res.total,
+                        res.sample_logp, bool(res.all_zero), res.n_nonfinite,
+                        bool(res.sample_fallback))
 
     def set_culling(self, enable: bool):
         _check(self._L.b3d_gpu_set_culling(self.h, 1 if enable else 0))

@@ -53,6 +53,9 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
 cudaError_t launch_exact_score(const KExactArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_shard_barrier(const KBarrier& b, cudaStream_t st);
+cudaError_t launch_copy_to_peers(const double* src, long long n_elems, double* const* peers,
+                                 int n_peers, long long offset, long long cap, cudaStream_t st);
 cudaError_t launch_fill_column(double* s, long long n, int ld, int col, double v, cudaStream_t st);
 size_t exact_score_pts_bytes(int W, int H, int ctas);
 size_t stage_scratch_bytes(long long n);  // stage.cu: grid-wide reduction partials
@@ -402,6 +405,7 @@ struct b3d_gpu_context {
   double* score_peers[8] = {nullptr};
   int n_score_peers = 0;
   long long score_peer_offset = 0;
+  long long score_peer_cap = 0;
   // camera mode scene (b3d_gpu_set_camera_scene): concatenated instances
   std::unique_ptr<Mesh> cam_mesh;
   int cam_n = 0;
@@ -652,9 +656,7 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.nt = m.nt;
   p.draw_base = 0;
   p.cull = ctx->culling ? m.cull : 0;
-  for (int r = 0; r < 8; ++r) p.score_peers[r] = ctx->score_peers[r];
-  p.n_score_peers = ctx->n_score_peers;
-  p.score_peer_offset = ctx->score_peer_offset;
+  p.n_score_peers = 0;  // set per call by the peer-enabled score paths only
   p.tris_s = m.tris_s.as<uint4>();
   p.plane_off = m.plane_off.as<double>();
   p.plane_end = m.plane_end.as<int>();
@@ -1114,19 +1116,33 @@ void run_scores(b3d_gpu_context* ctx, const Mesh& m, KParams p, const LikSpec& s
                "fill launch");
   if (spec.chunks.empty()) {  // every entry outside the support: nothing rendered
     if (d_status) cuda_check(cudaMemsetAsync(d_status, 0, (size_t)n, ctx->stream), "memset");
+    if (p.n_score_peers)
+      cuda_check(launch_copy_to_peers(d_scores, n * nc, p.score_peers, p.n_score_peers,
+                                      p.score_peer_offset * nc, p.score_peer_cap, ctx->stream),
+                 "copy_to_peers launch");
     return;
   }
+  // peers requested but the scores do not come out of one fused launch:
+  // store them to the peers after the fact (same elements, same capacity)
+  auto copy_to_peers = [&] {
+    if (!p.n_score_peers) return;
+    cuda_check(launch_copy_to_peers(d_scores, n * nc, p.score_peers, p.n_score_peers,
+                                    p.score_peer_offset * nc, p.score_peer_cap, ctx->stream),
+               "copy_to_peers launch");
+  };
   if (spec.exact) {
     exact_scores(ctx, m, p, spec, n, d_scores, d_status, camera);
+    copy_to_peers();
     return;
   }
   const bool in_place = spec.single();
   if (!in_place) {
-    p.n_score_peers = 0;
     size_t widest = 0;
     for (const LikChunk& ch : spec.chunks) widest = std::max(widest, (size_t)ch.lik.n_noise);
     ctx->chunk_scores.ensure(8 * widest * (size_t)n);
   }
+  const int peers = p.n_score_peers;
+  if (!in_place) p.n_score_peers = 0;
   for (const LikChunk& ch : spec.chunks) {
     p.lik = ch.lik;
     if (!camera) attach_base(ctx, p);
@@ -1146,13 +1162,17 @@ void run_scores(b3d_gpu_context* ctx, const Mesh& m, KParams p, const LikSpec& s
                                    cudaMemcpyDeviceToDevice, ctx->stream),
                  "cudaMemcpy2DAsync scores");
   }
+  if (!in_place) {
+    p.n_score_peers = peers;
+    copy_to_peers();
+  }
 }
 
 void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
                   const b3d_pose_grid* grid, uint64_t n, double* scores, uint8_t* status,
                   const b3d_contact_cells* contact = nullptr, uint64_t first = 0,
                   uint64_t grid_n = 0, unsigned long long* stage_rng = nullptr,
-                  KStageResult* stage_out = nullptr) {
+                  KStageResult* stage_out = nullptr, bool peers = false) {
   require_ready(ctx, true, true);
   check(scores != nullptr, "bad arguments");
   check(n > 0, "score_cells: no cells");
@@ -1224,6 +1244,12 @@ void score_common(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_pose* poses,
   } else if (!poses && !contact) {
     zhint = region_hint(ctx, m, p.grid.center,
                         std::sqrt(sq3(grid->extent)), std::max(spec.window, 0));
+  }
+  if (peers && ctx->n_score_peers) {  // b3d_gpu_set_score_peers: the fused all-gather
+    for (int r = 0; r < 8; ++r) p.score_peers[r] = ctx->score_peers[r];
+    p.n_score_peers = ctx->n_score_peers;
+    p.score_peer_offset = ctx->score_peer_offset;
+    p.score_peer_cap = ctx->score_peer_cap;
   }
   run_scores(ctx, m, p, spec, (long long)n, p.scores, p.status, false, zhint);
   if (stage_out)
@@ -1520,14 +1546,133 @@ b3d_status b3d_mesh_cull_sign(const double* vertices, uint64_t n_vertices,
 }
 
 b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t* peer_ptrs,
-                                   uint32_t n_peers, uint64_t offset) {
+                                   uint32_t n_peers, uint64_t offset, uint64_t capacity) {
   return guarded([&] {
     check(ctx != nullptr && (n_peers == 0 || peer_ptrs != nullptr), "bad arguments");
     require(n_peers <= 8, ErrorCode::invalid, "score peers: at most 8 ranks");
+    for (uint32_t r = 0; r < n_peers; ++r)
+      check(peer_ptrs[r] != 0, "score peers: null peer array");
     for (uint32_t r = 0; r < 8; ++r)
       ctx->score_peers[r] = r < n_peers ? reinterpret_cast<double*>(peer_ptrs[r]) : nullptr;
     ctx->n_score_peers = (int)n_peers;
     ctx->score_peer_offset = (long long)offset;
+    ctx->score_peer_cap = (long long)capacity;
+  });
+}
+
+b3d_status b3d_gpu_shard_barrier(b3d_gpu_context* ctx, const uint64_t* signal_ptrs,
+                                 uint32_t n_ranks, uint32_t rank, uint64_t epoch) {
+  return guarded([&] {
+    check(ctx && signal_ptrs && n_ranks >= 1 && n_ranks <= 8 && rank < n_ranks && epoch > 0,
+          "bad arguments");
+    DeviceGuard dg(ctx->device);
+    KBarrier b{};
+    for (uint32_t r = 0; r < n_ranks; ++r) {
+      check(signal_ptrs[r] != 0, "shard barrier: null signal pad");
+      b.sig[r] = reinterpret_cast<unsigned long long*>(signal_ptrs[r]);
+    }
+    b.n_ranks = (int)n_ranks;
+    b.rank = (int)rank;
+    b.epoch = epoch;
+    cuda_check(launch_shard_barrier(b, ctx->stream), "shard barrier launch");
+  });
+}
+
+b3d_status b3d_gpu_enumerate_shard(b3d_gpu_context* ctx, int32_t mesh_id, const float* depth,
+                                   const b3d_pose* poses, const b3d_pose_grid* grid,
+                                   uint64_t n_local, const b3d_shard_exchange* ex,
+                                   uint64_t* rng_state, b3d_stage_result* out) {
+  return guarded([&] {
+    check(ctx && ex && out && n_local > 0 && ((poses != nullptr) != (grid != nullptr)),
+          "bad arguments");
+    check(ex->n_ranks >= 1 && ex->n_ranks <= 8 && ex->rank < ex->n_ranks && ex->epoch > 0,
+          "shard exchange: bad ranks / epoch");
+    check(ex->offset + n_local <= ex->n_total, "shard exchange: shard outside the global array");
+    for (uint32_t r = 0; r < ex->n_ranks; ++r)
+      check(ex->scores[r] != 0 && ex->signals[r] != 0, "shard exchange: null peer buffer");
+    if (depth) {
+      const b3d_status st = b3d_gpu_set_observation(ctx, depth);
+      if (st != B3D_OK) throw Error(ErrorCode::invalid, b3d_last_error());
+    }
+    require_ready(ctx, true, true);
+    DeviceGuard dg(ctx->device);
+    const long long nn = ctx->spec.n_cols;
+    const long long half = (long long)(ex->epoch & 1) * (long long)ex->n_total * nn;
+    double* own = reinterpret_cast<double*>(ex->scores[ex->rank]) + half;
+    // this rank's scores land in its own array directly; the kernel stores
+    // them into the other ranks' arrays (the fused all-gather)
+    double* const saved[8] = {ctx->score_peers[0], ctx->score_peers[1], ctx->score_peers[2],
+                              ctx->score_peers[3], ctx->score_peers[4], ctx->score_peers[5],
+                              ctx->score_peers[6], ctx->score_peers[7]};
+    const int saved_n = ctx->n_score_peers;
+    const long long saved_off = ctx->score_peer_offset, saved_cap = ctx->score_peer_cap;
+    int np = 0;
+    for (uint32_t r = 0; r < ex->n_ranks; ++r)
+      if (r != ex->rank) ctx->score_peers[np++] = reinterpret_cast<double*>(ex->scores[r]) + half;
+    ctx->n_score_peers = np;
+    ctx->score_peer_offset = (long long)ex->offset;
+    ctx->score_peer_cap = (long long)ex->n_total * nn;
+    try {
+      if (poses)
+        score_common(ctx, mesh_id, poses, nullptr, n_local, own + (long long)ex->offset * nn,
+                     nullptr, nullptr, 0, 0, nullptr, nullptr, true);
+      else {
+        // a grid of n_total rows is the global one (this shard = rows offset +
+        // i); any other size is this rank's own grid (rows i)
+        const uint64_t gn = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2] *
+                            (grid->mode == B3D_GRID_PRODUCT ? grid->n_rot : 1);
+        score_common(ctx, mesh_id, nullptr, grid, n_local, own + (long long)ex->offset * nn,
+                     nullptr, nullptr, gn == ex->n_total ? ex->offset : 0, gn, nullptr, nullptr,
+                     true);
+      }
+    } catch (...) {
+      for (int r = 0; r < 8; ++r) ctx->score_peers[r] = saved[r];
+      ctx->n_score_peers = saved_n;
+      ctx->score_peer_offset = saved_off;
+      ctx->score_peer_cap = saved_cap;
+      throw;
+    }
+    for (int r = 0; r < 8; ++r) ctx->score_peers[r] = saved[r];
+    ctx->n_score_peers = saved_n;
+    ctx->score_peer_offset = saved_off;
+    ctx->score_peer_cap = saved_cap;
+    KBarrier b{};
+    for (uint32_t r = 0; r < ex->n_ranks; ++r)
+      b.sig[r] = reinterpret_cast<unsigned long long*>(ex->signals[r]);
+    b.n_ranks = (int)ex->n_ranks;
+    b.rank = (int)ex->rank;
+    b.epoch = ex->epoch;
+    cuda_check(launch_shard_barrier(b, ctx->stream), "shard barrier launch");
+    // stage reduction of the complete array; result + Rng come back in one copy
+    ctx->result.ensure(128);
+    char* tail = static_cast<char*>(ctx->result.p);
+    const bool dev_out = is_device_ptr(out);
+    const bool dev_rng = rng_state && is_device_ptr(rng_state);
+    KStageResult* d_out = dev_out ? reinterpret_cast<KStageResult*>(out)
+                                  : reinterpret_cast<KStageResult*>(tail);
+    unsigned long long* d_rng = nullptr;
+    if (rng_state) {
+      if (dev_rng) {
+        d_rng = reinterpret_cast<unsigned long long*>(rng_state);
+      } else {
+        d_rng = reinterpret_cast<unsigned long long*>(tail + 64);
+        cuda_check(cudaMemcpyAsync(d_rng, rng_state, 40, cudaMemcpyHostToDevice, ctx->stream),
+                   "cudaMemcpyAsync rng");
+      }
+    }
+    cuda_check(launch_stage_reduce(own, (long long)ex->n_total, (int)nn, 0, d_rng, d_out, nullptr,
+                                   ctx->stream, stage_scratch(ctx, (long long)ex->n_total)),
+               "stage_reduce launch");
+    if (!dev_out || (rng_state && !dev_rng)) {
+      ctx->pin_scores.ensure(128);
+      cuda_check(cudaMemcpyAsync(ctx->pin_scores.p, tail, 104, cudaMemcpyDeviceToHost,
+                                 ctx->stream),
+                 "cudaMemcpyAsync result");
+      cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_shard");
+      const char* pin = static_cast<const char*>(ctx->pin_scores.p);
+      if (!dev_out) std::memcpy(out, pin, sizeof(KStageResult));
+      if (rng_state && !dev_rng) std::memcpy(rng_state, pin + 64, 40);
+    }
   });
 }
 
@@ -1645,7 +1790,8 @@ b3d_status b3d_gpu_score_poses(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_
                                uint64_t n, double* scores, uint8_t* status) {
   return guarded([&] {
     check(poses != nullptr, "bad arguments");
-    score_common(ctx, mesh_id, poses, nullptr, n, scores, status);
+    score_common(ctx, mesh_id, poses, nullptr, n, scores, status, nullptr, 0, 0, nullptr,
+                 nullptr, true);
   });
 }
 
@@ -1655,7 +1801,8 @@ b3d_status b3d_gpu_score_grid(b3d_gpu_context* ctx, int32_t mesh_id, const b3d_p
     check(grid != nullptr, "bad arguments");
     const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
     const uint64_t n = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
-    score_common(ctx, mesh_id, nullptr, grid, n, scores, status);
+    score_common(ctx, mesh_id, nullptr, grid, n, scores, status, nullptr, 0, 0, nullptr,
+                 nullptr, true);
   });
 }
 
@@ -2545,7 +2692,7 @@ b3d_status b3d_gpu_enumerate_grid(b3d_gpu_context* ctx, int32_t mesh_id,
     const uint64_t n = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
     score_common(ctx, mesh_id, nullptr, grid, n, scores, nullptr, nullptr, 0, 0,
                  reinterpret_cast<unsigned long long*>(rng_state),
-                 reinterpret_cast<KStageResult*>(out));
+                 reinterpret_cast<KStageResult*>(out), true);
   });
 }
 
@@ -2556,7 +2703,8 @@ b3d_status b3d_gpu_score_grid_range(b3d_gpu_context* ctx, int32_t mesh_id,
     check(grid != nullptr, "bad arguments");
     const uint64_t nt = (uint64_t)grid->count[0] * grid->count[1] * grid->count[2];
     const uint64_t gn = grid->mode == B3D_GRID_PRODUCT ? nt * grid->n_rot : nt;
-    score_common(ctx, mesh_id, nullptr, grid, n, scores, status, nullptr, first, gn);
+    score_common(ctx, mesh_id, nullptr, grid, n, scores, status, nullptr, first, gn, nullptr,
+                 nullptr, true);
   });
 }
 

@@ -116,6 +116,7 @@ struct KParams {
   double* score_peers[8];
   int n_score_peers;
   long long score_peer_offset;
+  long long score_peer_cap;  // elements per peer array; stores at or beyond are skipped
   uint8_t* status;    // n_hyp (1 = empty render)
   float* out_depth;   // n_hyp x W x H  (render mode)
   int32_t* out_ids;   // n_hyp x W x H  (render mode, draw index or -1)
@@ -152,6 +153,13 @@ struct KStageResult {
   unsigned int n_nonfinite;
   unsigned int sample_fallback;  // sequential CDF rescan was needed
   unsigned int pad;
+};
+
+// signal-pad barrier of a sharded stage (exchange.cu)
+struct KBarrier {
+  unsigned long long* sig[8];  // rank r's signal pad, mapped on this device
+  int n_ranks, rank;
+  unsigned long long epoch;
 };
 
 // fp64 image likelihood (exact_score.cu): one chunk of <= kMaxNoise noise

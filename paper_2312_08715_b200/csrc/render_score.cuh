@@ -1136,7 +1136,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       p.scores[h * p.lik.n_noise + e] = total;
       if (p.n_score_peers) {  // the all-gather, fused: remote stores over NVLink
         const long long g = (p.score_peer_offset + h) * p.lik.n_noise + e;
-        for (int r = 0; r < p.n_score_peers; ++r) p.score_peers[r][g] = total;
+        if (g < p.score_peer_cap)
+          for (int r = 0; r < p.n_score_peers; ++r) p.score_peers[r][g] = total;
         __threadfence_system();
       }
     }

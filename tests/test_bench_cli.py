@@ -18,3 +18,22 @@ def test_reference_arm_prints_one_json_line():
                 "cpu_baseline", "e2e", "config"):
         assert key in line
     assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+
+
+def test_gpus_flag_launches_that_many_ranks():
+    """`bench.py --gpus 2` run directly re-launches itself as 2 ranks
+    (torch.distributed.run on 127.0.0.1); --dry-run makes the ranks meet over
+    gloo and rank 0 report, so no GPU is needed."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--dry-run"], capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    assert line == {"dry_run": True, "n_gpus": 2, "rank_sum": 1, "impl": "ours"}
+
+
+def test_gpus_flag_must_match_world_size():
+    env = dict(os.environ, WORLD_SIZE="1", RANK="0", LOCAL_RANK="0")
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--gpus", "2",
+                          "--dry-run"], capture_output=True, text=True, timeout=300, cwd=ROOT,
+                         env=env)
+    assert out.returncode != 0 and "--gpus 2 but WORLD_SIZE=1" in out.stderr

@@ -919,7 +919,7 @@ def test_fused_score_gather_to_peer_buffers(gpu_ctx, oracle):
     a = torch.full((3 * n, 1), -1.0, dtype=torch.float64, device="cuda")
     b = torch.full((3 * n, 1), -1.0, dtype=torch.float64, device="cuda")
     sc = torch.zeros((n, 1), dtype=torch.float64, device="cuda")
-    gpu_ctx.set_score_peers([a.data_ptr(), b.data_ptr()], n)  # this "rank" owns [n, 2n)
+    gpu_ctx.set_score_peers([a.data_ptr(), b.data_ptr()], n, 3 * n)  # this "rank" owns [n, 2n)
     try:
         gpu_ctx.score_grid(mid, grid, sc, None)
         torch.cuda.synchronize()
@@ -961,7 +961,7 @@ def test_fused_score_gather_symmetric_memory_single_rank(gpu_ctx, oracle):
             pytest.skip(f"symmetric memory rendezvous unavailable: {e}")
         sym.fill_(0.0)
         sc = torch.zeros((300, 1), dtype=torch.float64, device="cuda")
-        gpu_ctx.set_score_peers([int(x) for x in hdl.buffer_ptrs], 0)
+        gpu_ctx.set_score_peers([int(x) for x in hdl.buffer_ptrs], 0, 300)
         try:
             gpu_ctx.score_poses(mid, poses, sc, None)
             hdl.barrier(channel=0)
