@@ -59,6 +59,68 @@ def _ncu_traffic():
     return {"bytes_per_launch": total, "source": os.path.relpath(files[-1], ROOT)}
 
 
+def _golden(name):
+    """A committed reference fixture (tests/golden/ref_<name>.npz, produced by
+    the reference's own C++: tests/golden/make_ref_golden.py), or None."""
+    path = os.path.join(ROOT, "tests", "golden", f"ref_{name}.npz")
+    return np.load(path, allow_pickle=False) if os.path.exists(path) else None
+
+
+def _max_rel(got, want) -> float:
+    got = np.asarray(got, dtype=np.float64).ravel()
+    want = np.asarray(want, dtype=np.float64).ravel()
+    fin = np.isfinite(want)
+    if not np.array_equal(np.isfinite(got), fin):
+        return float("inf")
+    if not fin.any():
+        return 0.0
+    return float((np.abs(got[fin] - want[fin]) / np.abs(want[fin])).max())
+
+
+LEG_CPU = {"enabled": True, "seconds": 4.0, "fp64_peak": None}
+
+
+def leg_cpu_and_roofline(k, observed, verts, tris, poses, noise, sigma_max, window, gpu_value,
+                         base=None, camera=None, what=""):
+    """A leg's CPU baseline -- the oracle port of the reference algorithm on
+    all host threads, timed on a bounded sample of the leg's own hypotheses
+    (about LEG_CPU seconds) -- and its roofline: the oracle's exact
+    algorithmic op count per hypothesis times the leg's
+    measured device rate, against the in-run non-FMA FP64 peak."""
+    if not LEG_CPU["enabled"]:
+        return None, None
+    from oracle import pyoracle as O
+    threads = cpu_threads()
+    base_depth = None
+    if base:
+        base_depth = O.render(k, base, camera=camera)
+    kw = dict(base_depth=base_depth, camera=camera, threads=threads)
+    m = min(64, poses.shape[0])
+    _, _, cnt = O.score_poses(k, observed, verts, tris, poses[:m], noise, sigma_max, window,
+                              counters=True, **kw)
+    n_sigma = len({s for _, s in noise})
+    ops = _ops_per_hyp(cnt, n_sigma, len(noise), m)
+    done, t0, chunk = 0, time.perf_counter(), 16 * threads
+    while True:
+        i0 = done % poses.shape[0]
+        sel = poses[i0:i0 + chunk]
+        O.score_poses(k, observed, verts, tris, sel, noise, sigma_max, window, **kw)
+        done += sel.shape[0]
+        el = time.perf_counter() - t0
+        if el >= LEG_CPU["seconds"]:
+            break
+        chunk = min(4 * chunk, max(threads, int(done / el * (LEG_CPU["seconds"] - el)) + 1))
+    cpu = {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"{done} of the leg's hypotheses{what}, {el:.1f} s"}
+    roof = None
+    if LEG_CPU["fp64_peak"]:
+        ach = ops * gpu_value
+        roof = {"bound": "sm_fp64", "achieved": ach / 1e12, "peak": LEG_CPU["fp64_peak"] / 1e12,
+                "unit": "Tops/s", "frac": ach / LEG_CPU["fp64_peak"], "ops_per_hypothesis": ops,
+                "note": "leg rate over its whole device time (all kernels of the leg)"}
+    return cpu, roof
+
+
 def _ops_per_hyp(c: dict, n_sigma: int, n_noise: int, n: int) -> float:
     """Algorithmic op count per hypothesis (BASELINE.md §3 / SURVEY.md 8d),
     from the oracle's exact counters."""
@@ -161,34 +223,55 @@ def cpu_baseline(w, seconds=12.0, threads=None, counters=True):
                       f"{el:.1f} s"}, cnt, scores
 
 
+def bench_config(world: int, w) -> dict:
+    """The workload both arms report (identical dicts: same_config)."""
+    return {"workload": "configs[0]: single-object scoring 160x120 (WxH), 1,024 "
+                        "hypotheses/step/GPU (weak scaling: rank r scores rotation batch r)",
+            "hypotheses_per_step": BATCH * world, "image": "120x160", "window": "3x3",
+            "triangles": int(w.triangles.shape[0]), "vertices": int(w.vertices.shape[0]),
+            "parallelism": f"dp{world} (hypothesis shards, score all-gather)"}
+
+
+DTYPE = "f64/f32"
+DTYPE_NOTE = ("pose math and raster in fp64 without FMA (bitwise the reference's depth); "
+              "likelihood terms in fp32, accumulated in fp64 (SURVEY.md A.4)")
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (oracle port) on host cores."""
+    """--impl reference: the reference algorithm (oracle port) on host cores,
+    all threads, over the same workload as our arm at this rank count (one
+    1,024-hypothesis batch per GPU-rank per step).  Rank 0 alone runs."""
     if rank != 0:
         return
-    w = build_workload_oracle()
     from oracle import pyoracle as O
     threads = cpu_threads()
-    poses = w.grid_poses()
-    for _ in range(args.warmup):
-        O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise, w.sigma_max,
-                      w.window, threads=threads)
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        s, _ = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
-                             w.sigma_max, w.window, threads=threads)
+    batches = [build_workload_oracle(shard=r) for r in range(world)]
+    w = batches[0]
+
+    def step():
+        for b in batches:
+            s, _ = O.score_poses(b.k, b.observed, b.vertices, b.triangles, b.grid_poses(),
+                                 b.noise, b.sigma_max, b.window, threads=threads)
         probs, _ = O.normalize(s[:, 0])
         O.argmax(s[:, 0])
         O.sample_categorical(probs, O.rng_seed(7))
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
     el = time.perf_counter() - t0
-    v = args.steps * BATCH / el
-    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+    v = args.steps * BATCH * world / el
+    line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic (seeded voxel blob, BASELINE cfg1)", "impl": "reference",
-            "config": {"workload": "configs[0]: single-object scoring 160x120 (WxH), 1,024 "
-                                   "hypotheses/step", "hypotheses_per_step": BATCH},
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+            "dtype_note": "the oracle port computes everything in fp64",
+            "data": "synthetic (seeded 1,000-voxel Eden blob, noisy rendered observation)",
+            "impl": "reference", "config": bench_config(world, w),
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": f"{args.steps} steps x {BATCH} hypotheses (full batch)"},
+                             "sample": f"{args.steps} steps x {world} x {BATCH} hypotheses "
+                                       "(the full per-step workload)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -210,26 +293,54 @@ def run_tracking(ctx, b3d, configs, frames_n, render_fn):
     est = tr["gt"][0].copy()
     ctx.set_observation(frames[0])  # warm-up
     ctx.coarse_to_fine(mid, est, tr["stages"])
-    ms, errs_cm, errs_deg = [], [], []
+    ms, errs_cm, errs_deg, picks = [], [], [], []
     for f in range(1, frames_n):
         t0 = time.perf_counter()
         ctx.set_observation(frames[f])
-        _, centers = ctx.coarse_to_fine(mid, est, tr["stages"])
+        res, centers = ctx.coarse_to_fine(mid, est, tr["stages"])
         est = centers[-1]
         ms.append(1e3 * (time.perf_counter() - t0))
+        picks += [(r.argmax, r.max_score, centers[s]) for s, r in enumerate(res)]
         gt = tr["gt"][f]
         errs_cm.append(100.0 * float(np.linalg.norm(est[4:] - gt[4:])))
         d = min(1.0, abs(float(np.dot(est[:4], gt[:4]))))
         errs_deg.append(float(np.degrees(2.0 * np.arccos(d))))
     total = sum(ms) * 1e-3
-    return {"workload": "configs[3]: 2,000-voxel blob, 240x320, 2 stages x 8,192 hypotheses "
+    # per-stage argmax agreement with the reference's chain over the same
+    # frames (tracking.cpp:132-139 semantics; a tie within 1e-4 of the
+    # reference's best counts as agreement)
+    agree = None
+    g = _golden("cfg4")
+    if g is not None and len(picks) == g["argmax"].shape[0]:
+        ok, same_idx, centres_ok, worst = 0, 0, 0, 0.0
+        for i, (a, m, c) in enumerate(picks):
+            top = float(g["top2"][i][0])
+            same_idx += int(a == g["argmax"][i])
+            ok += int(a == g["argmax"][i] or abs(m - top) <= 1e-4 * abs(top))
+            centres_ok += int(np.array_equal(c, g["centers"][i]))
+            worst = max(worst, abs(m - top) / abs(top))
+        agree = {"stages": len(picks), "argmax_agreement": ok / len(picks),
+                 "same_index": same_idx, "same_centre_bitwise": centres_ok,
+                 "max_rel_err_best_score": worst,
+                 "reference": "tests/golden/ref_cfg4.npz (the reference's own render + "
+                              "windowed likelihood over the 100-frame sequence)"}
+    g0 = tr["stages"][0]
+    cpu, roof = leg_cpu_and_roofline(
+        tr["k"], tr["frames"][1], tr["vertices"], tr["triangles"],
+        configs.grid_poses(tr["gt"][0], g0["extent"], g0["count"], g0["rotations"], 0),
+        [g0["noise"]], 0.1, g0["window"], 16384 * (frames_n - 1) / total,
+        what=" (frame 1, stage 0)")
+    if cpu is not None:
+        cpu["fps"] = cpu["value"] / 16384.0
+    return {"cpu_baseline": cpu, "roofline": roof,
+            "workload": "configs[3]: 2,000-voxel blob, 240x320, 2 stages x 8,192 hypotheses "
                         "per frame (argmax chain on device), observation uploaded per frame",
             "fps": (frames_n - 1) / total, "frames": frames_n - 1,
             "ms_per_frame_mean": statistics.mean(ms), "ms_per_frame_p50": statistics.median(ms),
             "ms_per_frame_max": max(ms), "hypotheses_per_frame": 16384,
             "pose_error_cm_mean": statistics.mean(errs_cm),
             "pose_error_deg_mean": statistics.mean(errs_deg),
-            "triangles": int(tr["triangles"].shape[0])}
+            "triangles": int(tr["triangles"].shape[0]), "reference_agreement": agree}
 
 
 def run_bench_tracking(ctx, b3d, configs, resolutions=(25, 50, 100, 200), n_frames=120):
@@ -360,8 +471,16 @@ def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
     ctx.set_likelihood([w.stages[0]["noise"]], w.sigma_max, w.stages[0]["window"])
     d_obs = torch.from_numpy(w.observed).cuda()
     ctx.set_observation(d_obs)
-    st = b3d.rng_seed(11)
-    ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)  # warm-up
+    st = b3d.rng_seed(99)
+    res0, centers0 = ctx.coarse_to_fine(mid, w.center, w.stages, rng_state=st)  # warm-up
+    parity = None
+    g = _golden("cfg2")
+    if g is not None:  # the first chain from Rng(99) against the reference-scored chain
+        parity = {"same_draws": [int(r.sample) for r in res0] == [int(x) for x in g["picks"]],
+                  "same_argmax": [int(r.argmax) for r in res0] == [int(x) for x in g["argmax"]],
+                  "same_centres_bitwise": bool(np.array_equal(centers0, g["centers"])),
+                  "max_rel_err_stage_max": _max_rel([r.max_score for r in res0],
+                                                    [s.max() for s in g["scores"]])}
     times = []
     for _ in range(reps):
         t0 = time.perf_counter()
@@ -369,12 +488,19 @@ def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
         times.append(time.perf_counter() - t0)
     n = sum(int(np.prod(g["count"])) * g["rotations"].shape[0] for g in w.stages)
     gt = w.gt_pose
+    g0 = w.stages[0]
+    cpu, roof = leg_cpu_and_roofline(
+        w.k, w.observed, w.vertices, w.triangles,
+        configs.grid_poses(w.center, g0["extent"], g0["count"], g0["rotations"], 0),
+        [g0["noise"]], w.sigma_max, g0["window"], n / statistics.median(times),
+        what=" (stage 0's 32,768)")
     return {"workload": "configs[1]: 3,000-voxel blob, 200x200, 5 stages x 32,768 hypotheses, "
                         "sampled centres, chained on device",
             "hypotheses": n, "ms_per_schedule": 1e3 * statistics.median(times),
-            "value": n / statistics.median(times), "unit": UNIT,
+            "value": n / statistics.median(times), "unit": UNIT, "cpu_baseline": cpu,
+            "roofline": roof,
             "final_error_cm": 100.0 * float(np.linalg.norm(centers[-1][4:] - gt[4:])),
-            "triangles": int(w.triangles.shape[0])}
+            "triangles": int(w.triangles.shape[0]), "reference_parity": parity}
 
 
 def _scene_renderer(ctx, b3d):
@@ -422,14 +548,28 @@ def run_scene_graph(ctx, b3d, configs, reps=3):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
     best = int(torch.argmax(d_scores[:, 0]).item())
+    g = _golden("cfg3")
+    parity = None
+    if g is not None:
+        s = d_scores[:, 0].cpu().numpy()
+        parity = {"hypotheses_compared": int(s.shape[0]),
+                  "max_rel_err": _max_rel(s, g["scores"]),
+                  "same_argmax": best == int(np.argmax(g["scores"]))}
     placements = w["placements"][w["target"]]
     ctx.set_base_scene([], [])
+    base = [(tv, tt, ident)] + [(w["objects"][i][0], w["objects"][i][1], w["poses"][i])
+                                for i in w["base"]]
+    cpu, roof = leg_cpu_and_roofline(
+        w["k"], w["observed"], o[0], o[1], b3d.contact_grid_poses(g)[best // 64 * 64:][:4096],
+        w["noise"], w["sigma_max"], w["window"], n / statistics.median(times), base=base,
+        camera=w["camera"], what=" (contact cells around the argmax)")
     return {"workload": "configs[2]: table + 3 fixed objects (base scene), 4th object over "
                         "16x16 (x,y) x 512 yaw contact cells, 240x320",
             "hypotheses": n, "ms": 1e3 * statistics.median(times),
             "value": n / statistics.median(times), "unit": UNIT,
             "triangles": int(o[1].shape[0]), "argmax": best,
-            "true_contact": [round(v, 4) for v in placements]}
+            "true_contact": [round(v, 4) for v in placements], "reference_parity": parity,
+            "cpu_baseline": cpu, "roofline": roof}
 
 
 def run_sharded(ctx, b3d, configs, world, rank, reps=1):
@@ -511,7 +651,7 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
     for _ in range(reps):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        _, (_, r) = once()
+        allv, (_, r) = once()
         e1.record(stream)
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
@@ -520,13 +660,35 @@ def run_sharded(ctx, b3d, configs, world, rank, reps=1):
         tt_ = torch.tensor([t], dtype=torch.float64, device="cuda")
         dist.all_reduce(tt_, op=dist.ReduceOp.MAX)
         t = float(tt_.item())
+    cpu = roof = None
+    if rank == 0:
+        base = [(tv, tt, w["base_poses"][0])] + [
+            (w["library"][i][0], w["library"][i][1], w["base_poses"][1 + i])
+            for i in range(n_placed)]
+        lt = w["library"][w["target"]]
+        best = int(r.argmax)
+        allp = configs.grid_poses(w["gt"], w["extent"], w["count"], w["rotations"], 0)
+        cpu, roof = leg_cpu_and_roofline(
+            w["k"], w["observed"], lt[0], lt[1], allp[best // 64 * 64:][:4096], w["noise"],
+            w["sigma_max"], w["window"], n / t, base=base, camera=w["camera"],
+            what=" (a slice at the argmax)")
+    parity = None
+    g = _golden("cfg5")
+    if g is not None:
+        lo5 = int(g["first"])
+        s5 = allv[lo5:lo5 + g["scores"].shape[0], 0].cpu().numpy()
+        parity = {"hypotheses_compared": int(s5.shape[0]), "first": lo5,
+                  "max_rel_err": _max_rel(s5, g["scores"]),
+                  "global_argmax_in_slice_and_equal": int(r.argmax) == lo5 + int(
+                      np.argmax(g["scores"]))}
     ctx.set_base_scene([], [])
     return {"workload": "configs[4]: 10-object base scene, 1,048,576 6-DoF hypotheses of a "
                         "new object, 480x640, sharded over ranks, NCCL score all-gather, global "
                         "argmax/logsumexp + 1,000 samples",
             "hypotheses": n, "n_gpus": world, "scaling": "strong", "s": t, "value": n / t,
             "unit": UNIT, "triangles": int(w["library"][w["target"]][1].shape[0]),
-            "argmax": int(r.argmax), "logsumexp": r.logsumexp, "score_gather": gather}
+            "argmax": int(r.argmax), "logsumexp": r.logsumexp, "score_gather": gather,
+            "reference_parity": parity, "cpu_baseline": cpu, "roofline": roof}
 
 
 def spawn_ranks(args):
@@ -709,6 +871,13 @@ def main():
         torch.cuda.synchronize()
         kern_ms.append(ka.elapsed_time(kb))
     total_ms = sum(step_ms)
+    parity_cfg1 = None
+    g1 = _golden("score_cfg1")
+    if g1 is not None and rank == 0:  # rank 0 scores configs[0]'s own batch (shard 0)
+        s1 = d_scores[:, 0].cpu().numpy()
+        parity_cfg1 = {"hypotheses_compared": int(s1.shape[0]),
+                       "max_rel_err": _max_rel(s1, g1["scores"]),
+                       "same_argmax": int(np.argmax(s1)) == int(np.argmax(g1["scores"]))}
 
     # ---- end-to-end arm: public C ABI with pinned host buffers
     ctx.set_stream(None)
@@ -752,6 +921,18 @@ def main():
         t = torch.tensor([total_ms, e2e_total], dtype=torch.float64, device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, e2e_total = t.tolist()
+    peaks = {}
+    try:  # the roofline denominator, measured in-run (non-FMA DMUL/DADD probe)
+        import ctypes
+        L = ctypes.CDLL(os.path.join(ROOT, "paper_2312_08715_b200", "_lib", "libb3d_peaks.so"))
+        r = ctypes.c_double()
+        L.b3d_bench_fp64_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+        if L.b3d_bench_fp64_rate(local, ctypes.byref(r)) == 0:
+            peaks["fp64_nofma_ops"] = r.value
+    except Exception as e:  # pragma: no cover
+        peaks["error"] = str(e)
+    LEG_CPU["enabled"] = not args.no_cpu_baseline
+    LEG_CPU["fp64_peak"] = peaks.get("fp64_nofma_ops")
     sharded = None
     if not args.no_extra:
         sharded = run_sharded(ctx, b3d, configs, world, rank)
@@ -760,16 +941,6 @@ def main():
         value = args.steps * n_all / (total_ms * 1e-3)
         e2e_value = args.steps * n_all / (e2e_total * 1e-3)
         kern_avg = statistics.mean(kern_ms) * 1e-3
-        peaks = {}
-        try:
-            import ctypes
-            L = ctypes.CDLL(os.path.join(ROOT, "paper_2312_08715_b200", "_lib", "libb3d_peaks.so"))
-            r = ctypes.c_double()
-            L.b3d_bench_fp64_rate.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
-            if L.b3d_bench_fp64_rate(local, ctypes.byref(r)) == 0:
-                peaks["fp64_nofma_ops"] = r.value
-        except Exception as e:  # pragma: no cover
-            peaks["error"] = str(e)
         cpu = None
         cnt = None
         if not args.no_cpu_baseline:
@@ -797,17 +968,11 @@ def main():
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "kernel_ms": kern_avg * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
+            "dtype_note": DTYPE_NOTE, "kernel_ms": kern_avg * 1e3,
             "data": "synthetic (seeded 1,000-voxel Eden blob, noisy rendered observation)",
-            "config": {"workload": "configs[0]: single-object scoring 160x120 (WxH), "
-                                   "1,024 hypotheses/step/GPU",
-                       "hypotheses_per_step": n_all, "image": "120x160", "window": "3x3",
-                       "triangles": int(w.triangles.shape[0]),
-                       "vertices": int(w.vertices.shape[0]),
-                       "l2": "flushed between timed steps (256 MB write)",
-                       "parallelism": f"dp{world} (hypothesis shards, score all-gather)",
-                       "score_gather": gather},
+            "config": bench_config(world, w),
+            "l2": "flushed between timed steps (256 MB write)", "score_gather": gather,
             "gpu_launches": 2 * args.steps,  # render_score + stage_reduce per step
             "e2e": {"value": e2e_value, "unit": UNIT,
                     # N = 1: observation + poses + Rng state in; scores + stage result +
@@ -829,6 +994,18 @@ def main():
         line.update(extra)
         if sharded is not None:
             line["sharded_enumeration"] = sharded
+        # parity against the reference's own output on the same inputs
+        # (tests/golden/ref_*.npz from the reference C++ compiled unmodified)
+        line["parity"] = {
+            "reference": "tests/golden/ref_*.npz (make_ref_golden.py: the reference's own "
+                         "renderer, likelihood, inference and tracking code)",
+            "bar": "scores <= 1e-4 relative; argmax equal or tied within 1e-4; depth/ids "
+                   "bitwise (GPU tests)",
+            "cfg1": parity_cfg1,
+            "cfg2": extra.get("coarse_to_fine", {}).get("reference_parity"),
+            "cfg3": extra.get("scene_graph", {}).get("reference_parity"),
+            "cfg4": extra.get("tracking", {}).get("reference_agreement"),
+            "cfg5": (sharded or {}).get("reference_parity")}
         print(json.dumps(line), flush=True)
     ctx.close()
     if world > 1:

@@ -336,10 +336,13 @@ def test_b3d_infer_reference_c_abi(key, overrides):
     g = _load("smc")
     k = _intr(g["k"])
     cfg = dict(json.loads(str(g["infer_cfg"])), **overrides)
+    # the reference loaded its library from SVOX files, whose resolution and
+    # origin are float32 (io.hpp:19-20): the same values here
     models = []
     for i, nv in enumerate((60, 120, 200)):
         vox = synth.eden_blob(nv, 40 + i)
-        models.append(b3d.Model.from_voxels(vox, 0.01, synth.centered_origin(vox, 0.01), i))
+        org = synth.centered_origin(vox, 0.01).astype(np.float32).astype(np.float64)
+        models.append(b3d.Model.from_voxels(vox, float(np.float32(0.01)), org, i))
     lib = b3d.Library.create(models)
     seed = 10 if key == "infer_deep" else 9
     lines, ev, _, map_pose = b3d.infer(g["observed"], g["camera"], lib, json.dumps(cfg), seed)
