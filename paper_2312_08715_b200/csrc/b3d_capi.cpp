@@ -10,6 +10,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdio>
 #include <algorithm>
 #include <chrono>
 #include <limits>
@@ -623,14 +624,22 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   // big projected faces: only 1x1 bboxes stay in the tile queue; 2x2 and
   // 3x3 take the per-lane loop too (cfg4 173 -> 180 FPS, cfg3 +3 % vs
   // queueing 2x2; B3D_Q1_SMALL overrides for A/B)
+  // (A/B overrides; out-of-range values are ignored: the 3x3 tile queue
+  // covers at most 3 columns / rows and the packed bh-1 field is 2 bits)
   static const int q1_small = [] {
     const char* e = std::getenv("B3D_Q1_SMALL");
-    return e ? std::atoi(e) : 1;
+    const int v = e ? std::atoi(e) : 1;
+    if (e) std::fprintf(stderr, "b3d: B3D_Q1_SMALL=%s %s\n", e,
+                        v >= 1 && v <= 3 ? "(A/B override)" : "ignored (must be 1..3)");
+    return v >= 1 && v <= 3 ? v : 1;
   }();
   p.q1_small = q1_small;
   static const int q1_ratio = [] {  // region px per 100 triangles (B3D_Q1_RATIO: A/B)
     const char* e = std::getenv("B3D_Q1_RATIO");
-    return e ? std::atoi(e) : 20;
+    const int v = e ? std::atoi(e) : 20;
+    if (e) std::fprintf(stderr, "b3d: B3D_Q1_RATIO=%s %s\n", e,
+                        v >= 0 ? "(A/B override)" : "ignored (must be >= 0)");
+    return v >= 0 ? v : 20;
   }();
   p.q1_ratio = q1_ratio;
   const b3d_intrinsics& k = ctx->k;

@@ -286,17 +286,9 @@ stage_finish_kernel(const double* __restrict__ x, long long n, int stride, int c
     }
   }
   unsigned int fallback = 0;
-  if (pick < 0 || !(margin > eps)) {  // sequential CDF exactly as inference.cpp:345-353
+  if (pick < 0 || !(margin > eps)) {  // near a boundary: the reference's order
     fallback = 1;
-    double acc = 0.0;
-    pick = n - 1;
-    for (long long i = 0; i < n; ++i) {
-      acc += all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
-      if (u < acc) {
-        pick = i;
-        break;
-      }
-    }
+    pick = stage::sequential_pick(x, n, stride, col, m, all_zero, u);
   }
   out->sample = (unsigned long long)pick;
   out->sample_fallback = fallback;
@@ -424,17 +416,8 @@ sample_many_kernel(const double* __restrict__ x, long long n, int stride, int co
         }
       }
     }
-    if (pick < 0 || !(margin > eps)) {
-      double acc = 0.0;
-      pick = n - 1;
-      for (long long i = 0; i < n; ++i) {
-        acc += all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / tot;
-        if (u < acc) {
-          pick = i;
-          break;
-        }
-      }
-    }
+    if (pick < 0 || !(margin > eps))  // near a boundary: the reference's order
+      pick = stage::sequential_pick(x, n, stride, col, m, all_zero, u);
     out[k] = (unsigned long long)pick;
   }
 }

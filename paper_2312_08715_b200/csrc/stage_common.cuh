@@ -34,6 +34,27 @@ __device__ __forceinline__ double rng_uniform(unsigned long long* st) {
   return (double)(result >> 11) * 0x1.0p-53;
 }
 
+// The reference's draw, sequentially (score_cells + sample_categorical,
+// inference.cpp:315-330 and 345-353): total = sum of exp(x - max) in index
+// order, then the first i whose running sum of exp(x_i - max) / total exceeds
+// u (the last index if none).  Used when u lies within 8 n eps of a boundary
+// of the parallel CDF, where summation order could move the pick; it then
+// agrees with the reference up to exp's last-ulp differences between this
+// device's libm and the host's.
+__device__ __noinline__ long long sequential_pick(const double* __restrict__ x, long long n,
+                                                  int stride, int col, double m, int all_zero,
+                                                  double u) {
+  double total = 0.0;
+  if (!all_zero)
+    for (long long i = 0; i < n; ++i) total += exp(x[i * stride + col] - m);
+  double acc = 0.0;
+  for (long long i = 0; i < n; ++i) {
+    acc += all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
+    if (u < acc) return i;
+  }
+  return n - 1;
+}
+
 __device__ __forceinline__ bool better(double x, long long i, double bx, long long bi) {
   // strict max, lowest index among equals; NaN never wins
   return x > bx || (x == bx && i < bi);
@@ -204,18 +225,9 @@ __device__ __forceinline__ void block_stage_reduce(const double* __restrict__ x,
     }
   }
   unsigned int fallback = 0;
-  if (pick < 0 || !(margin > eps)) {
-    // sequential CDF exactly as inference.cpp:345-353
+  if (pick < 0 || !(margin > eps)) {  // near a boundary: the reference's order
     fallback = 1;
-    double acc = 0.0;
-    pick = n - 1;
-    for (long long i = 0; i < n; ++i) {
-      acc += all_zero ? 1.0 / (double)n : exp(x[i * stride + col] - m) / total;
-      if (u < acc) {
-        pick = i;
-        break;
-      }
-    }
+    pick = sequential_pick(x, n, stride, col, m, all_zero, u);
   }
   out->sample = (unsigned long long)pick;
   out->sample_fallback = fallback;

@@ -99,19 +99,22 @@ __device__ KPose camera_from_trig(double distance, double ca, double sa, double 
 // tab: 7 rows of n_tab doubles -- d, az, alt, cos(alt), sin(alt), cos(az),
 // sin(az) -- per axis value; level s values start at off (the caller's).
 
-// First index of the strict maximum over the valid points (invalid = -inf,
-// start at index 0 as the reference's loop); appends the pick to the per-axis
-// path; flags a stage whose best score is -inf.
-__global__ void cam_argmax_kernel(const double* __restrict__ scores,
-                                  const unsigned char* __restrict__ valid, int ppd,
-                                  int* __restrict__ state /* path[3], best, err */) {
-  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the score kernel's results
-  const int n = ppd * ppd * ppd;
-  constexpr double kNegInf = -__builtin_huge_val();
-  double bv = kNegInf;
+// The reference's stage argmax (tracking.cpp:132-137): best = 0, then every
+// i with scores[i] > scores[best] takes over.  A NaN never wins a comparison,
+// so a NaN at index 0 keeps index 0 and a NaN elsewhere is never picked; keyed
+// here as +inf / -inf, after which "first index of the strict maximum" over
+// the keys is exactly the reference's pick.  Invalid (out-of-range) points
+// score -inf (tracking.cpp:100-101).  Every thread of the CTA calls this; the
+// result is valid in thread 0.
+__device__ void stage_argmax(const double* __restrict__ scores,
+                             const unsigned char* __restrict__ valid, int n, double& best_v,
+                             int& best_i) {
+  constexpr double kInf = __builtin_huge_val();
+  double bv = -kInf;
   int bi = 0x7fffffff;
   for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double v = valid[i] ? scores[i] : kNegInf;
+    double v = valid[i] ? scores[i] : -kInf;
+    if (v != v) v = i == 0 ? kInf : -kInf;
     if (bi == 0x7fffffff || v > bv) {
       bv = v;
       bi = i;
@@ -127,26 +130,39 @@ __global__ void cam_argmax_kernel(const double* __restrict__ scores,
       bi = oi;
     }
   }
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (lane == 0) {
-    sv[warp] = bv;
-    si[warp] = bi;
+  if ((threadIdx.x & 31) == 0) {
+    sv[threadIdx.x >> 5] = bv;
+    si[threadIdx.x >> 5] = bi;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    const int nw = (blockDim.x + 31) / 32;
     bv = sv[0];
     bi = si[0];
-    for (int w = 1; w < nw; ++w)
+    for (int w = 1; w < (int)((blockDim.x + 31) / 32); ++w)
       if (si[w] != 0x7fffffff && (bi == 0x7fffffff || sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
         bv = sv[w];
         bi = si[w];
       }
-    // all equal to -inf: the reference's loop keeps index 0, then throws
-    if (!(bv > kNegInf)) {
-      bi = 0;
-      state[4] = 1;
-    }
+    best_v = bv;
+    best_i = bi;
+  }
+}
+
+// First index of the strict maximum over the valid points (invalid = -inf,
+// start at index 0 as the reference's loop); appends the pick to the per-axis
+// path; flags a stage whose best score is -inf.
+__global__ void cam_argmax_kernel(const double* __restrict__ scores,
+                                  const unsigned char* __restrict__ valid, int ppd,
+                                  int* __restrict__ state /* path[3], best, err */) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: the score kernel's results
+  const int n = ppd * ppd * ppd;
+  double bv;
+  int bi;
+  stage_argmax(scores, valid, n, bv, bi);
+  if (threadIdx.x == 0) {
+    // best score not finite (all -inf, or a NaN / +inf pick): the reference
+    // throws (tracking.cpp:135-136)
+    if (!isfinite(bv)) state[4] = 1;
     state[3] = bi;
     state[0] = state[0] * ppd + bi / (ppd * ppd);
     state[1] = state[1] * ppd + (bi / ppd) % ppd;
@@ -166,7 +182,6 @@ cam_stage_kernel(const double* __restrict__ tab, int n_tab, int off, int ppd, in
                  unsigned char* __restrict__ valid, KPose fallback) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int n = ppd * ppd * ppd;
-  constexpr double kNegInf = -__builtin_huge_val();
   __shared__ int s_path[3];
   if (first) {
     if (threadIdx.x == 0) {
@@ -174,42 +189,11 @@ cam_stage_kernel(const double* __restrict__ tab, int n_tab, int off, int ppd, in
       s_path[0] = s_path[1] = s_path[2] = 0;
     }
   } else {
-    double bv = kNegInf;
-    int bi = 0x7fffffff;
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      const double v = valid_prev[i] ? prev_scores[i] : kNegInf;
-      if (bi == 0x7fffffff || v > bv) {
-        bv = v;
-        bi = i;
-      }
-    }
-    __shared__ double sv[32];
-    __shared__ int si[32];
-    for (int o = 16; o > 0; o >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
-      if (oi != 0x7fffffff && (bi == 0x7fffffff || ov > bv || (ov == bv && oi < bi))) {
-        bv = ov;
-        bi = oi;
-      }
-    }
-    if ((threadIdx.x & 31) == 0) {
-      sv[threadIdx.x >> 5] = bv;
-      si[threadIdx.x >> 5] = bi;
-    }
-    __syncthreads();
+    double bv;
+    int bi;
+    stage_argmax(prev_scores, valid_prev, n, bv, bi);
     if (threadIdx.x == 0) {
-      bv = sv[0];
-      bi = si[0];
-      for (int w = 1; w < (int)((blockDim.x + 31) / 32); ++w)
-        if (si[w] != 0x7fffffff && (bi == 0x7fffffff || sv[w] > bv || (sv[w] == bv && si[w] < bi))) {
-          bv = sv[w];
-          bi = si[w];
-        }
-      if (!(bv > kNegInf)) {
-        bi = 0;
-        state[4] = 1;
-      }
+      if (!isfinite(bv)) state[4] = 1;
       state[3] = bi;
       state[0] = state[0] * ppd + bi / (ppd * ppd);
       state[1] = state[1] * ppd + (bi / ppd) % ppd;

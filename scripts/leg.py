@@ -12,6 +12,7 @@ import bench  # noqa: E402
 from paper_2312_08715_b200 import b3d, configs  # noqa: E402
 
 ctx = b3d.GpuContext(0)
+bench.LEG_CPU["enabled"] = False  # device legs only (ncu captures)
 
 
 def render_fn(k, v, t, p):
