@@ -268,3 +268,57 @@ def test_oracle_equals_reference_random_cases(oracle):
         sr, str_ = R.score_poses(k, obs, v, t, poses, noise, 0.1, wi)
         np.testing.assert_array_equal(sto, str_)
         _eq(so, sr)
+
+
+def test_cfg3_cfg4_cfg5_reference_spot(oracle):
+    """The full-size fixtures (cfg3's 131,072 contact cells, cfg4's 100-frame
+    chain, cfg5's 65,536-hypothesis slice): the oracle reproduces sampled
+    entries bitwise, so the GPU tests against these files and against the
+    oracle judge the same numbers."""
+    from oracle import pyoracle as O
+    rng = np.random.Generator(np.random.PCG64(9))
+    ident = np.array([1.0, 0, 0, 0, 0, 0, 0])
+    rs = lambda k, cam, inst: O.render(k, inst, camera=cam)
+    # cfg3
+    g = _load("cfg3")
+    w = configs.cfg3(rs, O.voxel_to_mesh, O.box_mesh, O.contact_to_pose, counts=(16, 16, 512))
+    _eq(w["observed"], g["observed"])
+    tv, tt, _, _ = w["table"]
+    base = [(tv, tt, ident)] + [(w["objects"][i][0], w["objects"][i][1], w["poses"][i])
+                               for i in w["base"]]
+    o = w["objects"][w["target"]]
+    cg = b3d.ContactGrid.make(0.5, 0.5, o[2], o[3], 1, (16, 16, 512))
+    _eq(b3d.contact_grid_poses(cg), g["poses"])  # product host cells = reference stage0_cells
+    idx = np.concatenate([[int(np.argmax(g["scores"]))], rng.integers(0, 131072, 11)])
+    bd = O.render(w["k"], base, camera=w["camera"])
+    s, _ = O.score_poses(w["k"], w["observed"], o[0], o[1], g["poses"][idx], w["noise"],
+                         w["sigma_max"], w["window"], base_depth=bd, camera=w["camera"])
+    _eq(s[:, 0], g["scores"][idx])
+    # cfg4: frame 1, both stages' sampled scores
+    g = _load("cfg4")
+    # (all 100 frames: the stage rotation tables are drawn after the frames)
+    tr = configs.cfg4(lambda k, v, t, p: O.render(k, [(v, t, p)]), O.voxel_to_mesh, seed=0)
+    for st in range(2):
+        stg = tr["stages"][st]
+        poses = configs.grid_poses(g["centers"][st], stg["extent"], stg["count"],
+                                   stg["rotations"], 0)
+        ii = g["sample_idx"][st][:16]
+        s, _ = O.score_poses(tr["k"], tr["frames"][1], tr["vertices"], tr["triangles"], poses[ii],
+                             [stg["noise"]], 0.1, stg["window"])
+        _eq(s[:, 0], g["sample_scores"][st][:16])
+    # cfg5: a few slice entries incl. the slice argmax
+    g = _load("cfg5")
+    w = configs.cfg5(rs, O.voxel_to_mesh, O.box_mesh, O.contact_to_pose)
+    _eq(w["observed"], g["observed"])
+    lo = int(g["first"])
+    idx = np.concatenate([[int(np.argmax(g["scores"]))], rng.integers(0, 65536, 3)])
+    allp = configs.grid_poses(w["gt"], w["extent"], w["count"], w["rotations"], 0)
+    tv, tt = w["table"]
+    n_placed = len(w["base_poses"]) - 1
+    base = [(tv, tt, w["base_poses"][0])] + [
+        (w["library"][i][0], w["library"][i][1], w["base_poses"][1 + i]) for i in range(n_placed)]
+    bd = O.render(w["k"], base, camera=w["camera"])
+    lt = w["library"][w["target"]]
+    s, _ = O.score_poses(w["k"], w["observed"], lt[0], lt[1], allp[lo + idx], w["noise"],
+                         w["sigma_max"], w["window"], base_depth=bd, camera=w["camera"])
+    _eq(s[:, 0], g["scores"][idx])
