@@ -548,13 +548,13 @@ def run_scene_graph(ctx, b3d, configs, reps=3):
         torch.cuda.synchronize()
         times.append(e0.elapsed_time(e1) * 1e-3)
     best = int(torch.argmax(d_scores[:, 0]).item())
-    g = _golden("cfg3")
+    gold = _golden("cfg3")
     parity = None
-    if g is not None:
+    if gold is not None:
         s = d_scores[:, 0].cpu().numpy()
         parity = {"hypotheses_compared": int(s.shape[0]),
-                  "max_rel_err": _max_rel(s, g["scores"]),
-                  "same_argmax": best == int(np.argmax(g["scores"]))}
+                  "max_rel_err": _max_rel(s, gold["scores"]),
+                  "same_argmax": best == int(np.argmax(gold["scores"]))}
     placements = w["placements"][w["target"]]
     ctx.set_base_scene([], [])
     base = [(tv, tt, ident)] + [(w["objects"][i][0], w["objects"][i][1], w["poses"][i])

@@ -642,6 +642,11 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
     return v >= 0 ? v : 20;
   }();
   p.q1_ratio = q1_ratio;
+  static const int obs_stage = [] {  // B3D_OBS_STAGE=0/1 (A/B of the bulk-copy staging)
+    const char* e = std::getenv("B3D_OBS_STAGE");
+    return e ? (std::atoi(e) != 0) : 0;
+  }();
+  p.obs_stage = obs_stage;
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;
   p.fy = k.fy;

@@ -796,6 +796,39 @@ struct HypCtx {
   int q1;  // largest bbox side of the tile classes (2 or 3)
 };
 
+// Observation staging (north_star (3)): after the raster the on-chip vertex
+// cache is dead, so the window-dilated region's observation rows (float4
+// x, y, z, valid) are fetched into it by the bulk-copy engine
+// (cp.async.bulk, completion counted on an mbarrier) while the CTA counts
+// |y|; the window sums then read shared memory instead of L2.
+__device__ __forceinline__ void mbar_init(unsigned long long* bar, unsigned count) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* bar, unsigned bytes) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* bar) {
+  const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+  const unsigned b = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(d), "l"(src), "r"(bytes), "r"(b) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* bar, unsigned phase) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done) : "r"(a), "r"(phase) : "memory");
+}
+
 // Work of one hypothesis after the vertex phase: z-buffer init, raster,
 // render-many output and/or likelihood.  Instantiated twice per kernel so
 // that the z-buffer accesses compile to shared-memory instructions (kZS) or
@@ -808,7 +841,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h,
                                          const double* inst_rt, HugeListT<(kCam || !kScore) ? kMaxHuge : 1>* hl,
-                                         int par) {
+                                         int par, unsigned long long* obs_bar, unsigned& obs_phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Region& rg = hc.rg;
   const double* const R = hc.R;
@@ -983,6 +1016,27 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   }
   B3D_PCLK(5);
 
+  // ---- observation staging into the (now dead) on-chip vertex cache
+  float4* staged = nullptr;
+  if (kScore && !kIds && !kCam && !kQA && p.obs_stage && !hc.empty_region) {
+    const int w = p.lik.window;
+    const int du0 = max(rg.u0 - w, 0), du1 = min(rg.u1 + w, p.W - 1);
+    const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
+    const int dw = du1 - du0 + 1, dh = dv1 - dv0 + 1;
+    if ((long long)dw * dh * 16 <= 32ll * p.vcap) {  // uniform across the CTA
+      staged = reinterpret_cast<float4*>(vs.uvp);
+      if (tid == 0) {
+        // the raster's generic reads of this buffer (ordered by the barrier
+        // above) before the bulk engine's writes
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_expect_tx(obs_bar, (unsigned)(dw * dh * 16));
+        for (int r = 0; r < dh; ++r)
+          bulk_g2s(staged + r * dw, p.obs + (size_t)(dv0 + r) * p.W + du0, (unsigned)(dw * 16),
+                   obs_bar);
+      }
+    }
+  }
+
   // ---- render-many output (sentinel = (float)far, id -1 = background)
   if (kOut) {
     const size_t npx = (size_t)p.W * p.H;
@@ -1058,6 +1112,10 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     const int dv0 = max(rg.v0 - w, 0), dv1 = min(rg.v1 + w, p.H - 1);
     const int dw = du1 - du0 + 1;
     const int dpx = (hc.empty_region || empty_render) ? 0 : dw * (dv1 - dv0 + 1);
+    if (staged) {  // every thread waits, so the phase completes even unused
+      mbar_wait(obs_bar, obs_phase);
+      obs_phase ^= 1u;
+    }
     double acc[kNN];
     int npos[kNN];
 #pragma unroll
@@ -1068,7 +1126,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     for (int i = tid; i < dpx; i += kThreads) {
       const int pv = dv0 + i / dw;
       const int pu = du0 + (i - (pv - dv0) * dw);
-      const float4 o = __ldg(p.obs + (size_t)pv * p.W + pu);
+      const float4 o = staged ? staged[i] : __ldg(p.obs + (size_t)pv * p.W + pu);
       if (o.w == 0.f) continue;
       float S[kMaxSlots];
       window_sums<kIds, kWin, kS1>(p, zb, rg, pu, pv, o, S);
@@ -1181,6 +1239,7 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   __shared__ int s_seg[24];  // score-mode work segments (hyp_body) + per-class cuts
   __shared__ double s_inst[kCam ? kMaxInst : 1][12];  // camera mode: R | t per instance
   __shared__ HugeListT<(kCam || !kScore) ? kMaxHuge : 1> s_huge;
+  __shared__ __align__(8) unsigned long long s_obs_bar;  // observation staging
   using Key = typename KeyT<kIds>::T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1206,6 +1265,8 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   // waits for this grid's completion itself (griddepcontrol.wait)
   asm volatile("griddepcontrol.launch_dependents;");
   if (p.rng_dst && blockIdx.x == 0 && threadIdx.x < 5) p.rng_dst[threadIdx.x] = p.rng_init[threadIdx.x];
+  unsigned obs_phase = 0;
+  if (kScore && !kIds && !kCam && kVS && p.obs_stage && threadIdx.x == 0) mbar_init(&s_obs_bar, 1);
   B3D_PCLK(0);
 #if B3D_L2_PREFETCH
   // Shared read-only inputs (mesh, sorted triangles, observation) into L2 in
@@ -1366,11 +1427,11 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
-                                                    s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
+                                                    s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase);
     else
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
-          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1);
+          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase);
     B3D_PCLK(7);
     // No barrier here: before the next hypothesis's first barrier only
     // s_pose (warp 0), the region / count words (thread 0) and s_inst are

@@ -26,10 +26,12 @@ if [ "$2" == "ncu" ]; then
       -s 2 -c 1 -o gpurun_out/prof_${TAG}_cfg1 $B > gpurun_out/ncu_${TAG}_cfg1.log 2>&1
   echo "ncu cfg1 rc=$?"
   # leg captures: skip the observation renders / warm-up launches
-  for spec in "coarse_to_fine 8" "scene_graph 3" "tracking 12" "sharded 3"; do
+  # (score-mode launches only: demangled names "render_score_kernel<false, true, ...")
+  for spec in "coarse_to_fine 5" "scene_graph 1" "tracking 10" "sharded 1"; do
     set -- $spec
     timeout 600 python scripts/leg.py $1 > gpurun_out/leg_${TAG}_$1.log 2>&1 && \
-    timeout 900 ncu --set full --clock-control none --import-source on -k regex:render_score \
+    timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
+        -k "regex:render_score_kernel<false, true" \
         -s $2 -c 1 -o gpurun_out/prof_${TAG}_$1 python scripts/leg.py $1 \
         > gpurun_out/ncu_${TAG}_$1.log 2>&1
     echo "ncu $1 rc=$?"
