@@ -11,6 +11,7 @@ prefactor "printed".
 """
 from __future__ import annotations
 
+import math
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -176,7 +177,7 @@ def cfg2(render_fn: RenderFn, mesh_fn, seed: int = 0, n_stages: int = 5,
     obs = synth.noisy_observation(depth, k.far, 0.002, 0.10, 0.2, 1.5, rng, k.near)
     d = rng.standard_normal(3)
     start = gt.copy()
-    start[4:] += 0.015 * d / np.linalg.norm(d)
+    start[4:] += 0.015 * d / synth.norm(d)
     dq = synth.vmf_quaternions(1, 300.0, rng)[0]
     start[:4] = _qmul(gt[:4], dq)
     widths = [0.04, 0.02, 0.01, 0.005, 0.002]
@@ -199,13 +200,13 @@ def _qmul(a, b):
     bw, bx, by, bz = b
     q = np.array([aw * bw - ax * bx - ay * by - az * bz, aw * bx + ax * bw + ay * bz - az * by,
                   aw * by + ay * bw + az * bx - ax * bz, aw * bz + az * bw + ax * by - ay * bx])
-    return q / np.linalg.norm(q)
+    return q / synth.norm(q)
 
 
 def _axis_angle_q(axis, angle):
     axis = np.asarray(axis, dtype=np.float64)
-    axis = axis / np.linalg.norm(axis)
-    return np.concatenate([[np.cos(angle / 2)], np.sin(angle / 2) * axis])
+    axis = axis / synth.norm(axis)
+    return np.concatenate([[math.cos(angle / 2)], math.sin(angle / 2) * axis])
 
 
 def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
@@ -228,8 +229,8 @@ def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
         if f:
             d = rng.standard_normal(3)
             pose = pose.copy()
-            pose[4:] += 0.01 * d / np.linalg.norm(d)
-            pose[:4] = _qmul(_axis_angle_q(rng.standard_normal(3), np.deg2rad(5.0)), pose[:4])
+            pose[4:] += 0.01 * d / synth.norm(d)
+            pose[:4] = _qmul(_axis_angle_q(rng.standard_normal(3), math.radians(5.0)), pose[:4])
         gts.append(pose)
         depth = render_fn(k, verts, tris, pose)
         frames.append(synth.noisy_observation(depth, k.far, 0.002, 0.05, 0.2, 1.5, rng, k.near))
@@ -238,10 +239,10 @@ def cfg4(render_fn: RenderFn, mesh_fn, seed: int = 0, n_frames: int = 100):
     # (+-3 mm, 2 deg)
     stages = [
         {"extent": (0.015, 0.015, 0.01), "count": (8, 8, 4),
-         "rotations": synth.rotation_lattice(np.deg2rad(6.0), 5, 300.0, rng),
+         "rotations": synth.rotation_lattice(math.radians(6.0), 5, 300.0, rng),
          "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
         {"extent": (0.003, 0.003, 0.003), "count": (8, 8, 4),
-         "rotations": synth.rotation_lattice(np.deg2rad(2.0), 5, 5000.0, rng),
+         "rotations": synth.rotation_lattice(math.radians(2.0), 5, 5000.0, rng),
          "mode": 0, "noise": (0.05, 0.005), "window": 2, "select": 1},
     ]
     return {"k": k, "vertices": verts, "triangles": tris, "voxels": vox, "gt": np.array(gts),
@@ -351,7 +352,7 @@ def cfg5(render_scene, mesh_fn, box_fn, contact_fn, seed: int = 0, counts=(64, 6
 
 def square_intrinsics(res: int, fov_deg: float = 60.0, near: float = 0.1, far: float = 5.0):
     """harness.cpp:731-740 square_intrinsics (bench-tracking)."""
-    f = res / (2.0 * np.tan(fov_deg * np.pi / 360.0))
+    f = res / (2.0 * math.tan(fov_deg * math.pi / 360.0))
     return Intr(f, f, (res - 1) / 2.0, (res - 1) / 2.0, res, res, near, far)
 
 

@@ -8,6 +8,8 @@ are input generation only -- neither product nor oracle.
 """
 from __future__ import annotations
 
+import math
+
 import numpy as np
 
 _NBR = np.array([[-1, 0, 0], [1, 0, 0], [0, -1, 0], [0, 1, 0], [0, 0, -1], [0, 0, 1]],
@@ -68,10 +70,23 @@ def centered_origin(voxels: np.ndarray, resolution: float) -> np.ndarray:
     return -resolution * (lo + (hi - lo + 1.0) / 2.0)
 
 
+# The generators below use Python's math (the image's libm) and explicit
+# sums, never numpy's SIMD transcendental / BLAS kernels: those dispatch on
+# the CPU's vector extensions, so the build container and a GPU box would
+# otherwise draw ulp-different rotations from the same seed, and the
+# committed reference fixtures (tests/golden) would not match bit for bit.
+def norm(v) -> float:
+    """Euclidean norm, summed in index order."""
+    s = 0.0
+    for x in v:
+        s += float(x) * float(x)
+    return math.sqrt(s)
+
+
 def uniform_quaternion(rng: np.random.Generator) -> np.ndarray:
     """Uniform random rotation: normalised 4-D Gaussian, (w, x, y, z), w >= 0."""
     q = rng.standard_normal(4)
-    q /= np.linalg.norm(q)
+    q /= norm(q)
     return q if q[0] >= 0 else -q
 
 
@@ -80,22 +95,22 @@ def vmf_quaternions(n: int, kappa: float, rng: np.random.Generator) -> np.ndarra
     (1,0,0,0) and concentration kappa (Wood 1994 rejection sampler, p = 4).
     Used as rotation perturbations dq: q_hyp = q_center * dq."""
     m = 4
-    b = (-2.0 * kappa + np.sqrt(4.0 * kappa * kappa + (m - 1) ** 2)) / (m - 1)
+    b = (-2.0 * kappa + math.sqrt(4.0 * kappa * kappa + (m - 1) ** 2)) / (m - 1)
     x0 = (1.0 - b) / (1.0 + b)
-    c = kappa * x0 + (m - 1) * np.log(1.0 - x0 * x0)
+    c = kappa * x0 + (m - 1) * math.log(1.0 - x0 * x0)
     out = np.zeros((n, 4), dtype=np.float64)
     for i in range(n):
         while True:
-            z = rng.beta((m - 1) / 2.0, (m - 1) / 2.0)
+            z = float(rng.beta((m - 1) / 2.0, (m - 1) / 2.0))
             w = (1.0 - (1.0 + b) * z) / (1.0 - (1.0 - b) * z)
-            u = rng.random()
-            if kappa * w + (m - 1) * np.log(1.0 - x0 * w) - c >= np.log(u):
+            u = float(rng.random())
+            if kappa * w + (m - 1) * math.log(1.0 - x0 * w) - c >= math.log(u):
                 break
         v = rng.standard_normal(3)
-        v /= np.linalg.norm(v)
+        v /= norm(v)
         out[i, 0] = w
-        out[i, 1:] = np.sqrt(max(0.0, 1.0 - w * w)) * v
-        out[i] /= np.linalg.norm(out[i])
+        out[i, 1:] = math.sqrt(max(0.0, 1.0 - w * w)) * v
+        out[i] /= norm(out[i])
     return out
 
 
@@ -130,8 +145,8 @@ def rotation_lattice(step_rad: float, extra: int = 0, kappa: float = 0.0,
                 if i == j == k == 0:
                     continue
                 r = step_rad * np.array([i, j, k], dtype=np.float64)
-                a = np.linalg.norm(r)
-                qs.append(np.concatenate([[np.cos(a / 2)], np.sin(a / 2) * r / a]))
+                a = norm(r)
+                qs.append(np.concatenate([[math.cos(a / 2)], math.sin(a / 2) * r / a]))
     out = np.array(qs)
     if extra:
         out = np.vstack([out, vmf_quaternions(extra, kappa, rng)])
