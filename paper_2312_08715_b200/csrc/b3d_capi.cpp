@@ -400,6 +400,18 @@ struct b3d_gpu_context {
   bool has_base = false;
   DevBuf base_keys, base_tmp, base_pad, sbase, gnodes, cheb, spin;
   int base_valid = 0;
+  uint64_t gen = 0;  // bumped by every setter: cached launch graphs check it
+  // b3d_gpu_enumerate_observed with page-locked inputs: the whole step
+  // (uploads, observation cache, score kernel, stage reduction, read-back)
+  // captured once into a CUDA graph and replayed while its inputs stay
+  struct E2E {
+    bool valid = false;
+    int warm = 0;
+    cudaGraphExec_t exec = nullptr;
+    std::vector<const void*> key;
+  } e2e;
+  PinnedBuf pin_rng;
+  DevBuf e2e_rng;
   uint32_t base_draw = 0;
   bool culling = true;  // b3d_gpu_set_culling
   // b3d_gpu_set_score_peers: fused score all-gather targets
@@ -1531,6 +1543,7 @@ b3d_status b3d_gpu_context_create(int device, b3d_gpu_context** out) {
 }
 
 void b3d_gpu_context_destroy(b3d_gpu_context* ctx) {
+  if (ctx && ctx->e2e.exec) cudaGraphExecDestroy(ctx->e2e.exec);
   if (!ctx) return;
   DeviceGuard dg(ctx->device);
   cudaStreamSynchronize(ctx->stream);
@@ -1541,6 +1554,7 @@ void b3d_gpu_context_destroy(b3d_gpu_context* ctx) {
 
 b3d_status b3d_gpu_set_stream(b3d_gpu_context* ctx, void* cuda_stream) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx != nullptr, "bad arguments");
     ctx->stream = cuda_stream ? static_cast<cudaStream_t>(cuda_stream) : ctx->own;
   });
@@ -1567,6 +1581,7 @@ b3d_status b3d_mesh_cull_sign(const double* vertices, uint64_t n_vertices,
 b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t* peer_ptrs,
                                    uint32_t n_peers, uint64_t offset, uint64_t capacity) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx != nullptr && (n_peers == 0 || peer_ptrs != nullptr), "bad arguments");
     require(n_peers <= 8, ErrorCode::invalid, "score peers: at most 8 ranks");
     for (uint32_t r = 0; r < n_peers; ++r)
@@ -1697,6 +1712,7 @@ b3d_status b3d_gpu_enumerate_shard(b3d_gpu_context* ctx, int32_t mesh_id, const 
 
 b3d_status b3d_gpu_set_culling(b3d_gpu_context* ctx, int enable) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx != nullptr, "bad arguments");
     ctx->culling = enable != 0;
   });
@@ -1712,6 +1728,7 @@ b3d_status b3d_gpu_mesh_cull_sign(const b3d_gpu_context* ctx, int32_t mesh_id, i
 b3d_status b3d_gpu_set_camera(b3d_gpu_context* ctx, const b3d_intrinsics* k,
                               const b3d_pose* camera) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx && k, "bad arguments");
     validate_intrinsics(*k);
     require(k->width <= 16384 && k->height <= 16384, ErrorCode::invalid,
@@ -1729,6 +1746,7 @@ b3d_status b3d_gpu_upload_mesh(b3d_gpu_context* ctx, const double* vertices,
                                uint64_t n_vertices, const uint32_t* triangles,
                                uint64_t n_triangles, int32_t* out_mesh_id) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx && vertices && triangles && out_mesh_id, "bad arguments");
     check(n_vertices > 0 && n_triangles > 0, "mesh: empty");
     check(n_vertices < (1u << 30) && n_triangles < (1u << 30), "mesh: too large");
@@ -1787,6 +1805,7 @@ b3d_status b3d_gpu_set_likelihood(b3d_gpu_context* ctx, const b3d_noise* noise,
                                   uint32_t n_noise, double sigma_max, int window,
                                   int prefactor) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx && noise, "bad arguments");
     require(ctx->has_camera, ErrorCode::invalid, "gpu context: intrinsics not set");
     ctx->spec = make_spec(ctx->k, noise, n_noise, sigma_max, window, prefactor, true);
@@ -1952,6 +1971,7 @@ int b3d_camera_pose_to_spherical(const b3d_pose* pose, double tol, double* dista
 b3d_status b3d_gpu_set_camera_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
                                     const b3d_pose* model_to_world, uint32_t n) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     check(ctx && mesh_ids && model_to_world, "bad arguments");
     require(n >= 1 && n <= (uint32_t)kMaxInst, ErrorCode::invalid,
             "camera scene: 1 to 16 instances");
@@ -2495,6 +2515,7 @@ b3d_status b3d_gpu_coarse_to_fine(b3d_gpu_context* ctx, int32_t mesh_id, const b
 b3d_status b3d_gpu_set_base_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
                                   const b3d_pose* model_to_world, uint32_t n) {
   return guarded([&] {
+    if (ctx) ++ctx->gen;
     require_ready(ctx, false, false);
     DeviceGuard dg(ctx->device);
     ++ctx->base_version;
@@ -2690,9 +2711,151 @@ b3d_status b3d_gpu_enumerate_poses(b3d_gpu_context* ctx, int32_t mesh_id,
   });
 }
 
+namespace {
+
+// The graph-replayed form of b3d_gpu_enumerate_observed (all inputs
+// page-locked host memory, one fused launch, no base scene, no peers):
+// captured on the second call with the same buffers and context state,
+// replayed afterwards -- one host launch instead of seven stream operations,
+// and the score kernel launched with programmatic serialization right
+// behind the observation cache (it waits for it before its window sums).
+// Returns false when the form does not apply (the caller runs the plain path).
+bool enumerate_observed_graph(b3d_gpu_context* ctx, int32_t mesh_id, const float* depth,
+                              const b3d_pose* poses, uint64_t n, uint64_t* rng_state,
+                              b3d_stage_result* out, double* scores) {
+  static const bool enabled = [] {
+    const char* e = std::getenv("B3D_E2E_GRAPH");  // 0 disables (A/B)
+    return !e || std::atoi(e) != 0;
+  }();
+  if (!enabled || !ctx || !depth || !poses || !out || n == 0) return false;
+  if (!ctx->has_camera || !ctx->has_lik || ctx->has_base || ctx->n_score_peers) return false;
+  if (!ctx->spec.single()) return false;
+  if (!is_pinned_host(depth) || !is_pinned_host(poses) || is_device_ptr(out)) return false;
+  if (scores && !is_pinned_host(scores)) return false;
+  if (rng_state && is_device_ptr(rng_state)) return false;
+  if (mesh_id < 0 || mesh_id >= (int)ctx->meshes.size()) return false;
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  const int nn = ctx->spec.n_cols;
+  const size_t sbytes = sizeof(double) * n * nn;
+  ctx->obs_depth.ensure(npx * 4);
+  ctx->obs_pts.ensure(npx * sizeof(float4));
+  ctx->in_stage.ensure(sizeof(b3d_pose) * n);
+  ctx->c2f_scores.ensure(sbytes + 128);
+  ctx->pin_scores.ensure(128);
+  ctx->pin_rng.ensure(64);
+  ctx->e2e_rng.ensure(64);
+  const Mesh& m = get_mesh(ctx, mesh_id);
+  std::vector<const void*> key{reinterpret_cast<const void*>(ctx->gen),
+                               reinterpret_cast<const void*>((uintptr_t)mesh_id),
+                               reinterpret_cast<const void*>((uintptr_t)n),
+                               reinterpret_cast<const void*>((uintptr_t)(rng_state != nullptr)),
+                               depth, poses, scores, ctx->stream, ctx->obs_depth.p,
+                               ctx->obs_pts.p, ctx->obs_count.p, ctx->in_stage.p,
+                               ctx->c2f_scores.p, ctx->pin_scores.p, ctx->pin_rng.p,
+                               ctx->e2e_rng.p, ctx->zscratch.p, ctx->vscratch.p,
+                               ctx->stage_part.p, m.verts.p};
+  if (!(ctx->e2e.valid && ctx->e2e.key == key)) {
+    // first sight of this configuration: run the plain path once (it sizes
+    // every buffer and sets the kernels' attributes), capture on the next
+    if (ctx->e2e.warm == 0 || ctx->e2e.key != key) {
+      if (ctx->e2e.exec) cudaGraphExecDestroy(ctx->e2e.exec);
+      ctx->e2e = b3d_gpu_context::E2E{};
+      ctx->e2e.key = key;
+      ctx->e2e.warm = 1;
+      return false;
+    }
+    char* const tail = static_cast<char*>(ctx->c2f_scores.p) + sbytes;
+    KStageResult* d_out = reinterpret_cast<KStageResult*>(tail);
+    unsigned long long* d_rng = ctx->e2e_rng.as<unsigned long long>();
+    KParams p = base_params(ctx, m);
+    p.poses = ctx->in_stage.as<KPose>();
+    p.n_hyp = (long long)n;
+    p.scores = ctx->c2f_scores.as<double>();
+    p.status = nullptr;
+    attach_base(ctx, p);
+    LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n, -1, false,
+                                                    region_hint_poses(ctx, m, poses, n,
+                                                                      ctx->lik.window));
+    p.zscratch = ctx->zscratch.as<unsigned long long>();
+    p.vscratch = ctx->vscratch.as<double>();
+    p.vcap = lp.vcap;
+    p.zcap = lp.zcap;
+    p.zstride = lp.zstride;
+    void* const scratch = stage_scratch(ctx, (long long)n);
+    // the key as captured (plan_launch / stage_scratch may have grown buffers)
+    key[16] = ctx->zscratch.p;
+    key[17] = ctx->vscratch.p;
+    key[18] = ctx->stage_part.p;
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal),
+               "begin capture");
+    cudaError_t e = cudaMemcpyAsync(ctx->in_stage.p, poses, sizeof(b3d_pose) * n,
+                                    cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess && rng_state)
+      e = cudaMemcpyAsync(d_rng, ctx->pin_rng.p, 40, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ctx->obs_depth.p, depth, npx * 4, cudaMemcpyHostToDevice, ctx->stream);
+    if (e == cudaSuccess)
+      e = launch_obs_prepare(ctx->obs_depth.as<float>(), (int)ctx->k.width, (int)ctx->k.height,
+                             static_cast<float>(ctx->k.far_m), (float)ctx->k.cx, (float)ctx->k.cy,
+                             (float)(1.0 / ctx->k.fx), (float)(1.0 / ctx->k.fy),
+                             ctx->obs_pts.as<float4>(), ctx->obs_count.as<int>(), ctx->stream);
+    if (e == cudaSuccess)
+      e = launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream, true);
+    if (e == cudaSuccess)
+      e = launch_stage_reduce(p.scores, (long long)n, nn, 0, rng_state ? d_rng : nullptr, d_out,
+                              nullptr, ctx->stream, scratch);
+    if (e == cudaSuccess)
+      e = cudaMemcpyAsync(ctx->pin_scores.p, tail, 64, cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && rng_state)
+      e = cudaMemcpyAsync(static_cast<char*>(ctx->pin_scores.p) + 64, d_rng, 40,
+                          cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess && scores)
+      e = cudaMemcpyAsync(scores, p.scores, sbytes, cudaMemcpyDeviceToHost, ctx->stream);
+    const cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &graph);
+    cudaGetLastError();
+    if (e != cudaSuccess || e2 != cudaSuccess || !graph) {
+      if (graph) cudaGraphDestroy(graph);
+      ctx->e2e.warm = 2;  // this configuration cannot be captured: plain path
+      return false;
+    }
+    cudaGraphExec_t exec = nullptr;
+    const cudaError_t e3 = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e3 != cudaSuccess) {
+      cudaGetLastError();
+      ctx->e2e.warm = 2;
+      return false;
+    }
+    ctx->e2e.exec = exec;
+    ctx->e2e.valid = true;
+    ctx->e2e.key = key;
+  }
+  if (rng_state) std::memcpy(ctx->pin_rng.p, rng_state, 40);
+  cuda_check(cudaGraphLaunch(ctx->e2e.exec, ctx->stream), "cudaGraphLaunch");
+  cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_observed");
+  const char* pin = static_cast<const char*>(ctx->pin_scores.p);
+  std::memcpy(out, pin, sizeof(KStageResult));
+  if (rng_state) std::memcpy(rng_state, pin + 64, 40);
+  ctx->has_obs = true;
+  ++ctx->obs_version;
+  return true;
+}
+
+}  // namespace
+
 b3d_status b3d_gpu_enumerate_observed(b3d_gpu_context* ctx, int32_t mesh_id, const float* depth,
                                       const b3d_pose* poses, uint64_t n, uint64_t* rng_state,
                                       b3d_stage_result* out, double* scores) {
+  bool done = false;
+  const b3d_status g = guarded([&] {
+    if (ctx && ctx->e2e.warm != 2) {
+      DeviceGuard dg(ctx->device);
+      done = enumerate_observed_graph(ctx, mesh_id, depth, poses, n, rng_state, out, scores);
+    }
+  });
+  if (g != B3D_OK) return g;
+  if (done) return B3D_OK;
   const b3d_status st = b3d_gpu_set_observation(ctx, depth);
   if (st != B3D_OK) return st;
   return b3d_gpu_enumerate_poses(ctx, mesh_id, poses, n, rng_state, out, scores);

@@ -99,6 +99,9 @@ cudaError_t launch_base_terms(const KParams& p, const unsigned long long* base_k
 __global__ void obs_prepare_kernel(const float* depth, int W, int H, float far_f, float fcx,
                                    float fcy, float inv_fx, float inv_fy, float4* out,
                                    int* count) {
+  // a score kernel launched behind this one with programmatic serialization
+  // may start now; it waits (griddepcontrol.wait) before reading the cache
+  asm volatile("griddepcontrol.launch_dependents;");
   __shared__ int s_cnt;
   if (threadIdx.x == 0) s_cnt = 0;
   __syncthreads();

@@ -1074,6 +1074,10 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   }
 
   if (kScore) {
+    // launched with programmatic serialization behind the observation cache
+    // (b3d_gpu_enumerate_observed's graph): everything above ran before it
+    // finished; wait for it here (a no-op otherwise, and after the first time)
+    if (!kCam) asm volatile("griddepcontrol.wait;" ::: "memory");
     // ---- D1: |y| = number of valid rendered pixels (likelihood.cpp:144-158)
     // With a base image: |y| = base count - base pixels of the region +
     // composed pixels of the region (the halo holds base pixels too, so the

@@ -136,3 +136,36 @@ def test_enumerate_shard_on_symmetric_memory_single_rank(gpu_ctx):
             assert torch.equal(d_res, ref_res) and torch.equal(d_rng, ref_rng)
     finally:
         dist.destroy_process_group()
+
+
+def test_enumerate_observed_graph_replay_tracks_inputs(gpu_ctx):
+    """b3d_gpu_enumerate_observed with page-locked buffers is captured into a
+    CUDA graph on its second call and replayed afterwards: the replays read
+    the buffers' current contents (new observation / poses / Rng state every
+    call) and equal the plain path exactly; a setter invalidates the graph."""
+    w, mid = _setup(gpu_ctx)
+    n = 512
+    h_obs = torch.from_numpy(w.observed).pin_memory().numpy()
+    h_poses = torch.from_numpy(w.grid_poses()[:n]).pin_memory().numpy()
+    h_sc = torch.zeros((n, 1), dtype=torch.float64).pin_memory().numpy()
+    rng = np.random.Generator(np.random.PCG64(4))
+    for it in range(6):
+        obs = w.observed.copy()
+        y, x = rng.integers(0, 100), rng.integers(0, 140)
+        obs[y:y + 20, x:x + 20] = np.float32(0.3 + 0.05 * it)
+        h_obs[:] = obs
+        h_poses[:] = w.grid_poses()[it * 64:it * 64 + n]
+        st = b3d.rng_seed(100 + it)
+        res = gpu_ctx.enumerate_observed(mid, h_obs, h_poses, rng_state=st, scores=h_sc)
+        # plain reference: device buffers, separate calls
+        gpu_ctx.set_observation(torch.from_numpy(obs).cuda())
+        ref_sc, _ = gpu_ctx.score_poses(mid, w.grid_poses()[it * 64:it * 64 + n])
+        st_ref = b3d.rng_seed(100 + it)
+        ref = gpu_ctx.stage_reduce(ref_sc[:, 0], rng_state=st_ref)
+        np.testing.assert_array_equal(h_sc, ref_sc)
+        assert (res.argmax, res.sample, res.max_score, res.logsumexp) == \
+            (ref.argmax, ref.sample, ref.max_score, ref.logsumexp)
+        np.testing.assert_array_equal(st, st_ref)
+        if it == 3:  # a setter in between: the next call recaptures
+            gpu_ctx.set_likelihood([(0.02, 0.006)], w.sigma_max, 2)
+    gpu_ctx.set_likelihood(w.noise, w.sigma_max, w.window)
