@@ -2754,6 +2754,14 @@ bool enumerate_observed_graph(b3d_gpu_context* ctx, int32_t mesh_id, const float
                                ctx->c2f_scores.p, ctx->pin_scores.p, ctx->pin_rng.p,
                                ctx->e2e_rng.p, ctx->zscratch.p, ctx->vscratch.p,
                                ctx->stage_part.p, m.verts.p};
+  static const bool dbg = std::getenv("B3D_E2E_DEBUG") != nullptr;
+  if (dbg && !(ctx->e2e.valid && ctx->e2e.key == key)) {
+    std::fprintf(stderr, "b3d e2e graph: (re)capture needed, warm %d valid %d, differing key slots:",
+                 ctx->e2e.warm, (int)ctx->e2e.valid);
+    for (size_t i = 0; i < key.size() && i < ctx->e2e.key.size(); ++i)
+      if (key[i] != ctx->e2e.key[i]) std::fprintf(stderr, " %zu", i);
+    std::fprintf(stderr, "\n");
+  }
   if (!(ctx->e2e.valid && ctx->e2e.key == key)) {
     // first sight of this configuration: run the plain path once (it sizes
     // every buffer and sets the kernels' attributes), capture on the next
@@ -2764,13 +2772,27 @@ bool enumerate_observed_graph(b3d_gpu_context* ctx, int32_t mesh_id, const float
       ctx->e2e.warm = 1;
       return false;
     }
-    char* const tail = static_cast<char*>(ctx->c2f_scores.p) + sbytes;
-    KStageResult* d_out = reinterpret_cast<KStageResult*>(tail);
-    unsigned long long* d_rng = ctx->e2e_rng.as<unsigned long long>();
+    // zero-copy: the page-locked inputs are read by the kernels through
+    // their device mappings (no upload copies), the stage result and the Rng
+    // state live in mapped page-locked memory
+    void *d_depth = nullptr, *d_poses = nullptr, *d_pin = nullptr, *d_pin_rng = nullptr,
+         *d_scores_host = nullptr;
+    if ((scores && cudaHostGetDevicePointer(&d_scores_host, scores, 0) != cudaSuccess) ||
+        cudaHostGetDevicePointer(&d_depth, const_cast<float*>(depth), 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d_poses, const_cast<b3d_pose*>(poses), 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d_pin, ctx->pin_scores.p, 0) != cudaSuccess ||
+        cudaHostGetDevicePointer(&d_pin_rng, ctx->pin_rng.p, 0) != cudaSuccess) {
+      cudaGetLastError();
+      ctx->e2e.warm = 2;
+      return false;
+    }
+    KStageResult* d_out = static_cast<KStageResult*>(d_pin);
+    unsigned long long* d_rng = static_cast<unsigned long long*>(d_pin_rng);
     KParams p = base_params(ctx, m);
-    p.poses = ctx->in_stage.as<KPose>();
+    p.poses = static_cast<const KPose*>(d_poses);
     p.n_hyp = (long long)n;
     p.scores = ctx->c2f_scores.as<double>();
+    p.scores_mirror = static_cast<double*>(d_scores_host);  // the caller's scores, zero-copy
     p.status = nullptr;
     attach_base(ctx, p);
     LaunchPlan lp = plan_launch<false, true, false>(ctx, m, (long long)n, -1, false,
@@ -2789,31 +2811,23 @@ bool enumerate_observed_graph(b3d_gpu_context* ctx, int32_t mesh_id, const float
     cudaGraph_t graph = nullptr;
     cuda_check(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal),
                "begin capture");
-    cudaError_t e = cudaMemcpyAsync(ctx->in_stage.p, poses, sizeof(b3d_pose) * n,
-                                    cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess && rng_state)
-      e = cudaMemcpyAsync(d_rng, ctx->pin_rng.p, 40, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(ctx->obs_depth.p, depth, npx * 4, cudaMemcpyHostToDevice, ctx->stream);
-    if (e == cudaSuccess)
-      e = launch_obs_prepare(ctx->obs_depth.as<float>(), (int)ctx->k.width, (int)ctx->k.height,
-                             static_cast<float>(ctx->k.far_m), (float)ctx->k.cx, (float)ctx->k.cy,
-                             (float)(1.0 / ctx->k.fx), (float)(1.0 / ctx->k.fy),
-                             ctx->obs_pts.as<float4>(), ctx->obs_count.as<int>(), ctx->stream);
+    cudaError_t e = launch_obs_prepare(static_cast<const float*>(d_depth), (int)ctx->k.width,
+                                       (int)ctx->k.height, static_cast<float>(ctx->k.far_m),
+                                       (float)ctx->k.cx, (float)ctx->k.cy,
+                                       (float)(1.0 / ctx->k.fx), (float)(1.0 / ctx->k.fy),
+                                       ctx->obs_pts.as<float4>(), ctx->obs_count.as<int>(),
+                                       ctx->stream);
     if (e == cudaSuccess)
       e = launch_render_score<false, true, false>(p, lp.cap, lp.smem, ctx->stream, true);
     if (e == cudaSuccess)
       e = launch_stage_reduce(p.scores, (long long)n, nn, 0, rng_state ? d_rng : nullptr, d_out,
                               nullptr, ctx->stream, scratch);
-    if (e == cudaSuccess)
-      e = cudaMemcpyAsync(ctx->pin_scores.p, tail, 64, cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess && rng_state)
-      e = cudaMemcpyAsync(static_cast<char*>(ctx->pin_scores.p) + 64, d_rng, 40,
-                          cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess && scores)
-      e = cudaMemcpyAsync(scores, p.scores, sbytes, cudaMemcpyDeviceToHost, ctx->stream);
     const cudaError_t e2 = cudaStreamEndCapture(ctx->stream, &graph);
     cudaGetLastError();
+    static const bool dbg = std::getenv("B3D_E2E_DEBUG") != nullptr;
+    if (dbg)
+      std::fprintf(stderr, "b3d e2e graph capture: %s / %s\n", cudaGetErrorString(e),
+                   cudaGetErrorString(e2));
     if (e != cudaSuccess || e2 != cudaSuccess || !graph) {
       if (graph) cudaGraphDestroy(graph);
       ctx->e2e.warm = 2;  // this configuration cannot be captured: plain path
@@ -2834,9 +2848,8 @@ bool enumerate_observed_graph(b3d_gpu_context* ctx, int32_t mesh_id, const float
   if (rng_state) std::memcpy(ctx->pin_rng.p, rng_state, 40);
   cuda_check(cudaGraphLaunch(ctx->e2e.exec, ctx->stream), "cudaGraphLaunch");
   cuda_check(cudaStreamSynchronize(ctx->stream), "enumerate_observed");
-  const char* pin = static_cast<const char*>(ctx->pin_scores.p);
-  std::memcpy(out, pin, sizeof(KStageResult));
-  if (rng_state) std::memcpy(rng_state, pin + 64, 40);
+  std::memcpy(out, ctx->pin_scores.p, sizeof(KStageResult));
+  if (rng_state) std::memcpy(rng_state, ctx->pin_rng.p, 40);
   ctx->has_obs = true;
   ++ctx->obs_version;
   return true;

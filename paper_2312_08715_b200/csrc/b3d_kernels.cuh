@@ -110,6 +110,7 @@ struct KParams {
   KLik lik;
   // outputs
   double* scores;     // n_hyp x n_noise
+  double* scores_mirror;  // optional second copy (mapped page-locked host memory)
   // fused score all-gather over NVLink: every score is also stored into
   // score_peers[r][(score_peer_offset + h) * n_noise + e] for each rank r
   // (peer-mapped symmetric buffers), so no separate collective is needed

@@ -1208,6 +1208,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         if (m_zero > 0) total += (double)m_zero * p.lik.log_floor[e];
       }
       p.scores[h * p.lik.n_noise + e] = total;
+      if (p.scores_mirror) p.scores_mirror[h * p.lik.n_noise + e] = total;
       if (p.n_score_peers) {  // the all-gather, fused: remote stores over NVLink
         const long long g = (p.score_peer_offset + h) * p.lik.n_noise + e;
         if (g < p.score_peer_cap)

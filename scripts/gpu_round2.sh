@@ -31,7 +31,7 @@ if [ "$2" == "ncu" ]; then
     set -- $spec
     timeout 600 python scripts/leg.py $1 > gpurun_out/leg_${TAG}_$1.log 2>&1 && \
     timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-        -k "regex:render_score_kernel<false, true" \
+        -k "regex:render_score_kernel<\\(bool\\)0, \\(bool\\)1" \
         -s $2 -c 1 -o gpurun_out/prof_${TAG}_$1 python scripts/leg.py $1 \
         > gpurun_out/ncu_${TAG}_$1.log 2>&1
     echo "ncu $1 rc=$?"
