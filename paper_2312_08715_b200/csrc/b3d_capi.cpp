@@ -661,19 +661,10 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
   p.obs_stage = obs_stage;
   static const int l2_discard = [] {  // B3D_L2_DISCARD=0/1 (A/B)
     const char* e = std::getenv("B3D_L2_DISCARD");
-    return e ? (std::atoi(e) != 0) : 1;
-  }();
-  p.l2_discard = l2_discard;
-  static const int dyn_chunks = [] {  // B3D_DYN_CHUNKS=0/1 (A/B)
-    const char* e = std::getenv("B3D_DYN_CHUNKS");
     return e ? (std::atoi(e) != 0) : 0;
   }();
-  p.dyn_chunks = dyn_chunks;
-  static const int row_exit = [] {  // B3D_ROW_EXIT=0/1 (A/B)
-    const char* e = std::getenv("B3D_ROW_EXIT");
-    return e ? (std::atoi(e) != 0) : 1;
-  }();
-  p.row_exit = row_exit;
+  p.l2_discard = l2_discard;
+
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;
   p.fy = k.fy;

@@ -126,21 +126,12 @@ __device__ __forceinline__ void raster_tri_box(const KParams& p, typename KeyT<k
     const double r_bc = bc.dx * (py - bc.oy);
     const double r_ca = ca.dx * (py - ca.oy);
     typename KeyT<kIds>::T* row = zb + (pv - rg.oy) * rg.rw - rg.ox;
-    // along a row each computed edge value is monotone in px (px - ox is
-    // correctly rounded, hence monotone, and so are the product and the
-    // difference), so the covered pixels of a row are one run: once the
-    // row has been entered, the first uncovered pixel ends it
-    bool entered = false;
     for (int pu = u_min; pu <= u_max; ++pu) {
       const double px = pu;
       const double e_ab = r_ab - ab.dy * (px - ab.ox);
       const double e_bc = r_bc - bc.dy * (px - bc.ox);
       const double e_ca = r_ca - ca.dy * (px - ca.ox);
-      if (!covers(ab, e_ab) || !covers(bc, e_bc) || !covers(ca, e_ca)) {
-        if (entered) break;
-        continue;
-      }
-      entered = p.row_exit != 0;
+      if (!covers(ab, e_ab) || !covers(bc, e_bc) || !covers(ca, e_ca)) continue;
       const double inv_z = (e_bc * a.iz + e_ca * b.iz + e_ab * c.iz) * inv_area2;
       if (inv_z <= 0) continue;
       const double z = __drcp_rn(inv_z);
@@ -917,18 +908,8 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       }
       return __ldg(tl + phys);
     };
-    // 32-triangle chunks: warp w takes chunks w, w + 12, ... (static), or
-    // the next unclaimed chunk from a shared counter (p.dyn_chunks: warps
-    // that meet cheap chunks take more, shortening the wait at the barrier
-    // that ends the raster)
-    const bool dyn = p.dyn_chunks != 0;
-    auto claim = [&]() {
-      int b = 0;
-      if (lane == 0) b = atomicAdd(&s_seg[22], 32);
-      return __shfl_sync(0xffffffffu, b, 0);
-    };
-    for (int base = dyn ? claim() : warp * 32; base < n_work;
-         base = dyn ? claim() : base + kThreads) {
+    const int c_first = warp * 32, c_stride = kThreads;
+    for (int base = c_first; base < n_work; base += c_stride) {
       __syncwarp();
       const int ti = base + lane;
       int cls = -1;
@@ -1356,7 +1337,6 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
       s_hi_v = INT_MIN;
       s_clip = 0;
       s_count = 0;
-      s_seg[22] = 0;  // raster chunk counter (p.dyn_chunks)
       if (kCam || !kScore) s_huge.n[kk & 1] = 0;
     }
     __syncthreads();

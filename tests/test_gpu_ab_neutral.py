@@ -1,9 +1,8 @@
-"""GPU: the A/B switches of the score kernel change where data lives or how
-much work is skipped, never the scores -- the bulk-copy observation staging
-(B3D_OBS_STAGE: window sums read shared memory instead of L2), the L2 discard
-of the scratch vertex cache (B3D_L2_DISCARD, big meshes) and the per-lane
-loop's row exit (B3D_ROW_EXIT): scored in two processes, switch on and off,
-bitwise equal."""
+"""GPU: the A/B switches of the score kernel change where data lives, never
+the scores -- the bulk-copy observation staging (B3D_OBS_STAGE: window sums
+read shared memory instead of L2) and the L2 discard of the scratch vertex
+cache (B3D_L2_DISCARD, big meshes): scored in two processes, switch on and
+off, bitwise equal."""
 import os
 import subprocess
 import sys
@@ -63,10 +62,3 @@ def test_l2_discard_is_bitwise_neutral(tmp_path):
     b = _run("B3D_L2_DISCARD", "0", tmp_path / "off.npy", big=True)
     np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
 
-
-def test_row_exit_is_bitwise_neutral(tmp_path):
-    """The per-lane bbox loop leaving a row after its covered run (edge values
-    are monotone along a row) renders the same depth bits: scores equal."""
-    a = _run("B3D_ROW_EXIT", "1", tmp_path / "on.npy", big=True)
-    b = _run("B3D_ROW_EXIT", "0", tmp_path / "off.npy", big=True)
-    np.testing.assert_array_equal(a.view(np.uint64), b.view(np.uint64))
