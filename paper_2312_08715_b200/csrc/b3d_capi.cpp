@@ -659,11 +659,6 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
     return e ? (std::atoi(e) != 0) : 0;
   }();
   p.obs_stage = obs_stage;
-  static const int l2_discard = [] {  // B3D_L2_DISCARD=0/1 (A/B)
-    const char* e = std::getenv("B3D_L2_DISCARD");
-    return e ? (std::atoi(e) != 0) : 0;
-  }();
-  p.l2_discard = l2_discard;
 
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;

@@ -1016,18 +1016,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
   }
   B3D_PCLK(5);
 
-  // ---- the vertex cache in global scratch is dead from here on: drop its
-  // L2 lines without write-back (the next hypothesis rewrites every entry
-  // it reads), so the ~32 B/vertex/hypothesis scratch traffic never reaches
-  // DRAM (cfg2: 292 MB of write-back per 32,768-hypothesis stage without)
-  if (kQA && p.l2_discard) {
-    const uintptr_t b0 = reinterpret_cast<uintptr_t>(vs.uvp);
-    const uintptr_t lo = (b0 + 127) & ~uintptr_t(127);
-    const uintptr_t hi = (b0 + 32ull * (size_t)p.nv) & ~uintptr_t(127);
-    for (uintptr_t a = lo + 128ull * tid; a < hi; a += 128ull * kThreads)
-      asm volatile("discard.global.L2 [%0], 128;" ::"l"(a) : "memory");
-  }
-
   // ---- observation staging into the (now dead) on-chip vertex cache
   float4* staged = nullptr;
   if (kScore && !kIds && !kCam && !kQA && p.obs_stage && !hc.empty_region) {
