@@ -21,6 +21,7 @@ tests/test_oracle_stage.py) on reference-computed scores, and says so.
 """
 from __future__ import annotations
 
+import math
 import os
 import sys
 import time
@@ -227,6 +228,16 @@ def sec_cfg5():
     _save("cfg5", observed=w["observed"], first=np.int64(lo), scores=s[:, 0], status=st)
 
 
+def _from_c(p):
+    """The reference C ABI's from_c (b3d_capi.cpp:68-75): q / ||q|| with
+    Eigen's scalar norm, (x^2 + y^2) + (z^2 + w^2)."""
+    p = np.array(p, dtype=np.float64)
+    w, x, y, z = (float(v) for v in p[:4])
+    n = math.sqrt((x * x + y * y) + (z * z + w * w))
+    p[:4] = [w / n, x / n, y / n, z / n]
+    return p
+
+
 def sec_cfg4():
     """BASELINE configs[3]: the 100-frame tracking sequence.  Per frame two
     argmax stages (strict >, lowest index: tracking.cpp:132-134) of 8,192
@@ -254,7 +265,9 @@ def sec_cfg4():
             samp_idx.append(ii)
             samp.append(s[ii])
             c = poses[a]
-        est = c
+        # the next frame's centre crosses the C ABI as a b3d_pose, which the
+        # boundary renormalises (from_c, b3d_capi.cpp:68-75)
+        est = _from_c(c)
         if f % 10 == 0:
             print(f"  cfg4 frame {f}: {time.time() - t0:.0f} s")
     _save("cfg4", centers=np.array(centers), argmax=np.array(amax), top2=np.array(top2),
