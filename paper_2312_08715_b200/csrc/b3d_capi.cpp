@@ -659,11 +659,6 @@ KParams base_params(b3d_gpu_context* ctx, const Mesh& m) {
     return e ? (std::atoi(e) != 0) : 0;
   }();
   p.obs_stage = obs_stage;
-  static const int win_skip = [] {  // B3D_WIN_SKIP=0/1 (A/B)
-    const char* e = std::getenv("B3D_WIN_SKIP");
-    return e ? (std::atoi(e) != 0) : 1;
-  }();
-  p.win_skip = win_skip;
 
   const b3d_intrinsics& k = ctx->k;
   p.fx = k.fx;

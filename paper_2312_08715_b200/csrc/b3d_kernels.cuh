@@ -140,7 +140,6 @@ struct KParams {
   unsigned long long* rng_dst;
   unsigned long long rng_init[5];
   int obs_stage;  // stage the observation region into shared memory (bulk copy)
-  int win_skip;   // skip window sums with no rendered pixel in reach (radius >= 2)
   int q1_small;  // tile-class bound for big projected faces (render_score.cuh hc.q1)
   int q1_ratio;  // region px per 100 triangles above which faces count as big
 };

@@ -796,14 +796,6 @@ struct HypCtx {
   int q1;  // largest bbox side of the tile classes (2 or 3)
 };
 
-// Window skip (windows of radius >= 2, no base scene): per interior row of
-// the region, the leftmost / rightmost rendered column, gathered while |y| is
-// counted; an observed pixel none of whose window rows holds a rendered
-// column within reach has S = 0 exactly (every tap is background), so its
-// (2w+1)^2 taps are not evaluated -- it is counted like every other empty
-// window (likelihood.cpp:209-216 with an empty list).
-constexpr int kRowMax = 512;
-
 // Observation staging (north_star (3)): after the raster the on-chip vertex
 // cache is dead, so the window-dilated region's observation rows (float4
 // x, y, z, valid) are fetched into it by the bulk-copy engine
@@ -849,8 +841,7 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
                                          double (*s_red)[kMaxNoise],
                                          int (*s_redi)[kMaxNoise + 1], long long h,
                                          const double* inst_rt, HugeListT<(kCam || !kScore) ? kMaxHuge : 1>* hl,
-                                         int par, unsigned long long* obs_bar, unsigned& obs_phase,
-                                         int* rowx) {
+                                         int par, unsigned long long* obs_bar, unsigned& obs_phase) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const Region& rg = hc.rg;
   const double* const R = hc.R;
@@ -1079,8 +1070,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
     // With a base image: |y| = base count - base pixels of the region +
     // composed pixels of the region (the halo holds base pixels too, so the
     // interior [u0,u1]x[v0,v1] is counted).
-    const bool wskip = !kCam && !kIds && p.win_skip && p.lik.window >= 2 && !p.base_keys &&
-                       !hc.empty_region && rg.v1 - rg.v0 + 1 <= kRowMax;  // uniform
     {
       int cnt = 0;
       const int iw = rg.u1 - rg.u0 + 1, ipx = iw * (rg.v1 - rg.v0 + 1);
@@ -1090,10 +1079,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
         const float z = __uint_as_float(
             kIds ? (unsigned int)((unsigned long long)k >> 32) : (unsigned int)k);
         cnt += z < p.far_f;
-        if (wskip && z < p.far_f) {
-          atomicMin(rowx + (v - rg.v0), u);
-          atomicMax(rowx + kRowMax + (v - rg.v0), u);
-        }
         if (p.base_keys)
           cnt -= __uint_as_float((unsigned int)(__ldg(p.base_keys + (size_t)v * p.W + u) >> 32)) <
                  p.far_f;
@@ -1147,13 +1132,6 @@ __device__ __forceinline__ void hyp_body(const KParams& p, const HypCtx& hc, Key
       const int pu = du0 + (i - (pv - dv0) * dw);
       const float4 o = staged ? staged[i] : __ldg(p.obs + (size_t)pv * p.W + pu);
       if (o.w == 0.f) continue;
-      if (wskip) {  // any rendered column within reach in the window's rows?
-        const int r0 = max(pv - w, rg.v0) - rg.v0, r1 = min(pv + w, rg.v1) - rg.v0;
-        bool any = false;
-        for (int r = r0; r <= r1; ++r)
-          any |= rowx[r] <= pu + w && rowx[kRowMax + r] >= pu - w;
-        if (!any) continue;  // S = 0: counted below as log(floor)
-      }
       float S[kMaxSlots];
       window_sums<kIds, kWin, kS1>(p, zb, rg, pu, pv, o, S);
       if (p.base_keys) {
@@ -1267,7 +1245,6 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
   __shared__ double s_inst[kCam ? kMaxInst : 1][12];  // camera mode: R | t per instance
   __shared__ HugeListT<(kCam || !kScore) ? kMaxHuge : 1> s_huge;
   __shared__ __align__(8) unsigned long long s_obs_bar;  // observation staging
-  __shared__ int s_rowx[(kScore && !kCam && !kIds) ? 2 * kRowMax : 1];  // window skip
   using Key = typename KeyT<kIds>::T;
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -1341,8 +1318,6 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
         pose_to_rt(p.w2c, hp, s_pose[lane], s_pose[lane] + 9);
       }
     }
-    if (kScore && !kCam && !kIds && p.win_skip && p.lik.window >= 2 && !p.base_keys)
-      for (int i = tid; i < 2 * kRowMax; i += kThreads) s_rowx[i] = i < kRowMax ? INT_MAX : INT_MIN;
     if (tid == 0) {
       s_lo_u = INT_MAX;
       s_lo_v = INT_MAX;
@@ -1457,11 +1432,11 @@ __global__ void __launch_bounds__(kThreads, B3D_MINB) render_score_kernel(const 
     hc.rpx = rg.rw * rg.rh;
     if (hc.rpx <= p.zcap)
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(p, hc, zb_s, vs, wq, s_seg, &s_count, s_coef,
-                                                    s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase, s_rowx);
+                                                    s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase);
     else
       hyp_body<kIds, kScore, kOut, kWin, kS1, kCam, !kVS && !kCam>(
           p, hc, reinterpret_cast<Key*>(p.zscratch + (size_t)blockIdx.x * p.zstride), vs, wq,
-          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase, s_rowx);
+          s_seg, &s_count, s_coef, s_red, s_redi, h, &s_inst[0][0], &s_huge, kk & 1, &s_obs_bar, obs_phase);
     B3D_PCLK(7);
     // No barrier here: before the next hypothesis's first barrier only
     // s_pose (warp 0), the region / count words (thread 0) and s_inst are
