@@ -98,9 +98,18 @@ def leg_cpu_and_roofline(k, observed, verts, tris, poses, noise, sigma_max, wind
         base_depth = O.render(k, base, camera=camera)
     kw = dict(base_depth=base_depth, camera=camera, threads=threads)
     m = min(64, poses.shape[0])
-    _, _, cnt = O.score_poses(k, observed, verts, tris, poses[:m], noise, sigma_max, window,
-                              counters=True, **kw)
     n_sigma = len({s for _, s in noise})
+    if base:
+        # the base-scene path's own work: the object's raster
+        # and its windowed pairs; the base scene's per-pixel terms are a
+        # per-observation table, so neither the base's pairs nor the
+        # whole-image log terms are per-hypothesis work
+        _, _, cnt = O.score_poses(k, observed, verts, tris, poses[:m], noise, sigma_max, window,
+                                  counters=True, camera=camera, threads=threads)
+        cnt = dict(cnt, obs_valid=0)
+    else:
+        _, _, cnt = O.score_poses(k, observed, verts, tris, poses[:m], noise, sigma_max, window,
+                                  counters=True, **kw)
     ops = _ops_per_hyp(cnt, n_sigma, len(noise), m)
     done, t0, chunk = 0, time.perf_counter(), 16 * threads
     while True:
@@ -119,7 +128,9 @@ def leg_cpu_and_roofline(k, observed, verts, tris, poses, noise, sigma_max, wind
         ach = ops * gpu_value
         roof = {"bound": "sm_fp64", "achieved": ach / 1e12, "peak": LEG_CPU["fp64_peak"] / 1e12,
                 "unit": "Tops/s", "frac": ach / LEG_CPU["fp64_peak"], "ops_per_hypothesis": ops,
-                "note": "leg rate over its whole device time (all kernels of the leg)"}
+                "note": "leg rate over its whole device time (all kernels of the leg)"
+                        + ("; ops = the object's raster + windowed pairs (base-scene terms are "
+                           "tabulated once per observation)" if base else "")}
     return cpu, roof
 
 
