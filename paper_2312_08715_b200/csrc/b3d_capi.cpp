@@ -1431,6 +1431,40 @@ void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, 
 // the thread-local error channel, shared with smc.cpp (not exported)
 void b3d200_set_last_error(const char* msg) { g_last_error = msg; }
 
+// CameraIntrinsics::validate (geometry.cpp:38-44) for the handle layer
+void b3d200_validate_intrinsics(const b3d_intrinsics& k) { validate_intrinsics(k); }
+
+// render_instances (renderer.cpp:174-184) for scenes with more instances than
+// the camera-mode kernel holds: the instances rasterized one after another
+// into the base-scene key buffer (object mode, the same arithmetic, draw
+// order table -> children), read back as depth with the far sentinel.
+void b3d200_render_scene_keys(b3d_gpu_context* ctx, const b3d_intrinsics* k,
+                              const b3d_pose* camera, const int32_t* ids, const b3d_pose* poses,
+                              uint32_t n, float* out) {
+  auto ok = [](b3d_status s) {
+    if (s != B3D_OK) throw Error(static_cast<ErrorCode>(s), b3d_last_error());
+  };
+  ok(b3d_gpu_set_camera(ctx, k, camera));
+  ok(b3d_gpu_set_base_scene(ctx, ids, poses, n));
+  const size_t npx = (size_t)k->width * k->height;
+  std::vector<unsigned long long> keys(npx);
+  {
+    DeviceGuard dg(ctx->device);
+    cuda_check(cudaMemcpyAsync(keys.data(), ctx->base_keys.p, 8 * npx, cudaMemcpyDeviceToHost,
+                               ctx->stream),
+               "cudaMemcpyAsync keys");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "render_scene_keys");
+  }
+  const float far_f = static_cast<float>(k->far_m);
+  for (size_t i = 0; i < npx; ++i) {
+    const unsigned int bits = (unsigned int)(keys[i] >> 32);
+    float z;
+    std::memcpy(&z, &bits, 4);
+    out[i] = z < far_f ? z : far_f;
+  }
+  ok(b3d_gpu_set_base_scene(ctx, nullptr, nullptr, 0));
+}
+
 // =================================================================== C ABI
 extern "C" {
 

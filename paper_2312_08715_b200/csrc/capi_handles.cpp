@@ -24,6 +24,10 @@
 #include "json_mini.hpp"
 
 void b3d200_set_last_error(const char* msg);  // b3d_capi.cpp
+void b3d200_validate_intrinsics(const b3d_intrinsics& k);
+void b3d200_render_scene_keys(b3d_gpu_context* ctx, const b3d_intrinsics* k,
+                              const b3d_pose* camera, const int32_t* ids, const b3d_pose* poses,
+                              uint32_t n, float* out);
 
 namespace {
 
@@ -391,6 +395,44 @@ b3d_status b3d_model_mesh(const b3d_object_model* model, const double** vertices
 
 void b3d_model_destroy(b3d_object_model* model) { delete model; }
 
+// The reference parses scene / manifest JSON with nlohmann::json and reports
+// its exceptions verbatim (scene_graph.cpp:201-203, 219-221): the same text
+// for the same defect -- at() on a missing key (out_of_range.403), get<T>() of
+// the wrong type (type_error.302), at() on a non-object (type_error.304).
+const char* nl_type_name(const J::Value& v) {
+  switch (v.kind) {
+    case J::Value::Null: return "null";
+    case J::Value::Bool: return "boolean";
+    case J::Value::Number: return "number";
+    case J::Value::String: return "string";
+    case J::Value::Array: return "array";
+    default: return "object";
+  }
+}
+struct NlError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+const J::Value& nl_at(const J::Value& o, const char* key) {
+  if (!o.is_object())
+    throw NlError(std::string("[json.exception.type_error.304] cannot use at() with ") +
+                  nl_type_name(o));
+  const J::Value* x = o.find(key);
+  if (!x) throw NlError(std::string("[json.exception.out_of_range.403] key '") + key + "' not found");
+  return *x;
+}
+double nl_number(const J::Value& v) {
+  if (v.kind != J::Value::Number)
+    throw NlError(std::string("[json.exception.type_error.302] type must be number, but is ") +
+                  nl_type_name(v));
+  return v.num;
+}
+const std::string& nl_string(const J::Value& v) {
+  if (v.kind != J::Value::String)
+    throw NlError(std::string("[json.exception.type_error.302] type must be string, but is ") +
+                  nl_type_name(v));
+  return v.str;
+}
+
 b3d_status b3d_library_open(const char* manifest_path, b3d_library** out) {
   return guarded([&] {  // load_library (scene_graph.cpp:206-234)
     check(out && manifest_path, "bad arguments");
@@ -406,15 +448,18 @@ b3d_status b3d_library_open(const char* manifest_path, b3d_library** out) {
     auto lib = std::make_unique<b3d_library>();
     lib->models.resize(models->arr.size());
     for (const J::Value& m : models->arr) {
-      const J::Value* idv = m.is_object() ? m.find("id") : nullptr;
-      const J::Value* pv = m.is_object() ? m.find("path") : nullptr;
-      require(idv && idv->kind == J::Value::Number && pv && pv->kind == J::Value::String,
-              B3D_ERROR_CONFIG, mp + ": bad model entry");
-      const int id = (int)idv->num;
+      int id = 0;
+      std::string rel;
+      try {  // mj.at("id").get<int>(), mj.at("path").get<std::string>()
+        id = (int)nl_number(nl_at(m, "id"));
+        rel = nl_string(nl_at(m, "path"));
+      } catch (const NlError& e) {
+        throw Fail(B3D_ERROR_CONFIG, mp + ": bad model entry: " + e.what());
+      }
       require(id >= 0 && (size_t)id < lib->models.size(), B3D_ERROR_CONFIG,
               mp + ": model ids must be dense 0-based");
       require(!lib->models[id], B3D_ERROR_CONFIG, mp + ": duplicate model id");
-      lib->models[id] = load_svox(base + pv->str, id);
+      lib->models[id] = load_svox(base + rel, id);
     }
     *out = lib.release();
   });
@@ -443,28 +488,34 @@ b3d_status b3d_scene_from_json(const char* json, const b3d_library* lib, b3d_sce
     const J::Value j = parse_or(json, B3D_ERROR_CONFIG, "invalid scene JSON");
     const J::Value* t = j.is_object() ? j.find("table") : nullptr;
     require(t != nullptr, B3D_ERROR_CONFIG, "scene JSON: missing 'table'");
-    auto need_num = [](const J::Value* o, const char* k) {
-      const J::Value* x = o && o->is_object() ? o->find(k) : nullptr;
-      require(x && x->kind == J::Value::Number, B3D_ERROR_CONFIG,
-              std::string("bad scene JSON: key '") + k + "' missing or not a number");
-      return x->num;
-    };
     auto s = std::make_unique<b3d_scene>();
-    s->table_w = need_num(t, "width");
-    s->table_h = need_num(t, "height");
-    const J::Value* th = t->find("thickness");
-    s->thickness = th ? need_num(t, "thickness") : 0.01;
-    require(s->table_w > 0 && s->table_h > 0 && s->thickness > 0, B3D_ERROR,
-            "table: extents must be positive");
-    if (const J::Value* ch = j.find("children")) {
-      require(ch->is_array(), B3D_ERROR_CONFIG, "bad scene JSON: 'children' must be an array");
-      for (const J::Value& c : ch->arr) {
-        const int id = (int)need_num(&c, "object_id");
-        require(id >= 0 && (size_t)id < lib->models.size(), B3D_ERROR_CONFIG,
-                "scene JSON: object_id out of library range");
-        s->children.push_back({lib->models[id], (int)need_num(&c, "face"), need_num(&c, "dx"),
-                               need_num(&c, "dy"), need_num(&c, "dtheta")});
+    try {  // the reference's order: thickness (value), width, height, then children
+      const J::Value* th = t->is_object() ? t->find("thickness") : nullptr;
+      if (!t->is_object())
+        throw NlError(std::string("[json.exception.type_error.306] cannot use value() with ") +
+                      nl_type_name(*t));
+      s->thickness = th ? nl_number(*th) : 0.01;
+      s->table_w = nl_number(nl_at(*t, "width"));
+      s->table_h = nl_number(nl_at(*t, "height"));
+      require(s->table_w > 0 && s->table_h > 0 && s->thickness > 0, B3D_ERROR,
+              "table: extents must be positive");
+      if (const J::Value* ch = j.find("children")) {
+        if (!ch->is_array())
+          throw NlError(std::string("[json.exception.type_error.302] type must be array, but is ") +
+                        nl_type_name(*ch));
+        for (const J::Value& c : ch->arr) {
+          const int id = (int)nl_number(nl_at(c, "object_id"));
+          require(id >= 0 && (size_t)id < lib->models.size(), B3D_ERROR_CONFIG,
+                  "scene JSON: object_id out of library range");
+          const int face = (int)nl_number(nl_at(c, "face"));
+          const double dx = nl_number(nl_at(c, "dx"));
+          const double dy = nl_number(nl_at(c, "dy"));
+          const double dth = nl_number(nl_at(c, "dtheta"));
+          s->children.push_back({lib->models[id], face, dx, dy, dth});
+        }
       }
+    } catch (const NlError& e) {
+      throw Fail(B3D_ERROR_CONFIG, std::string("bad scene JSON: ") + e.what());
     }
     *out = s.release();
   });
@@ -499,22 +550,28 @@ b3d_status b3d_render(const b3d_scene* scene, const b3d_pose* camera, const b3d_
   return guarded([&] {  // render_depth (renderer.cpp:176-179) on the device
     check(scene && camera && k && out, "bad arguments");
     const b3d_pose cam = normalized_pose(*camera);
-    b3d_gpu_context* g = g_gpu.get();
-    ok(b3d_gpu_set_camera(g, k, nullptr));
-    std::vector<int32_t> ids{g_gpu.table(scene->table_w, scene->table_h, scene->thickness)};
+    // scene_instances (renderer.cpp:153-162) first -- contact errors come
+    // before the intrinsics check of render_instances (renderer.cpp:176)
     std::vector<b3d_pose> poses{b3d_pose{1, 0, 0, 0, 0, 0, 0}};
-    for (const auto& c : scene->children) {  // scene_instances (renderer.cpp:153-162)
-      ids.push_back(g_gpu.mesh(*c.obj));
+    for (const auto& c : scene->children) {
       b3d_pose p;
       ok(b3d_contact_to_pose(scene->table_w, scene->table_h, c.obj->aabb_min, c.obj->aabb_max,
                              c.face, c.dx, c.dy, c.dtheta, &p));
       poses.push_back(p);
     }
-    require(ids.size() <= B3D_MAX_INSTANCES, B3D_ERROR,
-            "b3d_render: at most 15 children per scene on the B200 path");
-    ok(b3d_gpu_set_camera_scene(g, ids.data(), poses.data(), (uint32_t)ids.size()));
+    b3d200_validate_intrinsics(*k);
+    b3d_gpu_context* g = g_gpu.get();
+    std::vector<int32_t> ids{g_gpu.table(scene->table_w, scene->table_h, scene->thickness)};
+    for (const auto& c : scene->children) ids.push_back(g_gpu.mesh(*c.obj));
     std::vector<float> depth((size_t)k->width * k->height);
-    ok(b3d_gpu_render_cameras(g, &cam, 1, depth.data(), nullptr));
+    if (ids.size() <= B3D_MAX_INSTANCES) {  // camera mode: one launch
+      ok(b3d_gpu_set_camera(g, k, nullptr));
+      ok(b3d_gpu_set_camera_scene(g, ids.data(), poses.data(), (uint32_t)ids.size()));
+      ok(b3d_gpu_render_cameras(g, &cam, 1, depth.data(), nullptr));
+    } else {  // any number of children: instance after instance
+      b3d200_render_scene_keys(g, k, &cam, ids.data(), poses.data(), (uint32_t)ids.size(),
+                               depth.data());
+    }
     ok(b3d_depth_image_create(k->width, k->height, depth.data(), out));
   });
 }

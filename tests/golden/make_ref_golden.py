@@ -358,9 +358,23 @@ def sec_track():
           default=default, ppd3=var3, beam2=beam2, sampled=obs1)
 
 
+def sec_capi():
+    """The reference C ABI's status codes and error texts for boundary misuse
+    (tests/capi_cases.py, the same calls the product is checked with)."""
+    import json
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import capi_cases
+    out = capi_cases.run_cases(R.lib(), gpu=True)
+    path = os.path.join(HERE, "ref_capi.json")
+    with open(path, "w") as f:
+        json.dump(out, f, indent=1, sort_keys=True)
+    print(f"  wrote {os.path.relpath(path, ROOT)} ({len(out)} cases)")
+
+
+
 SECTIONS = {"pose": sec_pose, "mesh": sec_mesh, "render": sec_render, "score_cfg1": sec_score_cfg1,
             "smc": sec_smc, "track": sec_track, "cfg2": sec_cfg2, "cfg3": sec_cfg3,
-            "cfg5": sec_cfg5, "cfg4": sec_cfg4}
+            "cfg5": sec_cfg5, "cfg4": sec_cfg4, "capi": sec_capi}
 
 
 def main(argv):
@@ -374,3 +388,4 @@ def main(argv):
 
 if __name__ == "__main__":
     main(sys.argv[1:])
+
