@@ -496,20 +496,19 @@ typedef struct b3d_smc_config {
   const b3d_schedule_stage* refine; /* n_refine entries */
   const b3d_noise* noise_grid;
   uint32_t n_noise_grid; /* any size; entries must lie in the noise support */
-  uint32_t n_objects;    /* objects placed, 1..B3D_SMC_MAX_CHILDREN */
+  uint32_t n_objects;    /* objects placed, >= 1 (inference.cpp:495) */
   uint32_t n_particles;
   double resample_threshold;
   double sigma_max;
   int32_t window; /* < 0: untruncated likelihood (ModelConfig::windowed = false) */
   int32_t prefactor;
 } b3d_smc_config;
-enum { B3D_SMC_MAX_CHILDREN = 8 };
 typedef struct b3d_smc_child {
   int32_t object_id, face;
   double dx, dy, dtheta; /* ContactParams */
 } b3d_smc_child;
 typedef struct b3d_smc_particle {
-  b3d_smc_child children[8];
+  b3d_smc_child* children; /* caller storage for cfg->n_objects entries */
   int32_t n_children, noise_index;
   double log_target, log_weight;
 } b3d_smc_particle;

@@ -128,7 +128,7 @@ class SmcChild(C.Structure):
 
 
 class SmcParticle(C.Structure):
-    _fields_ = [("children", SmcChild * 8), ("n_children", C.c_int32),
+    _fields_ = [("children", C.POINTER(SmcChild)), ("n_children", C.c_int32),
                 ("noise_index", C.c_int32), ("log_target", C.c_double),
                 ("log_weight", C.c_double)]
 
@@ -904,13 +904,17 @@ class GpuContext:
         cfg.resample_threshold, cfg.sigma_max = resample_threshold, sigma_max
         cfg.window, cfg.prefactor = window, prefactor
         out = (SmcParticle * n_particles)()
+        kids = (SmcChild * (n_particles * max(1, n_objects)))()
+        for i in range(n_particles):
+            out[i].children = C.cast(C.byref(kids, i * max(1, n_objects) * C.sizeof(SmcChild)),
+                                     C.POINTER(SmcChild))
         le = C.c_double()
         _check(self._L.b3d_gpu_run_smc(self.h, libs, len(library), C.byref(cfg), seed, out,
                                        C.byref(le)))
         ps = []
         for p in out:
             ch = [(c.object_id, c.face, c.dx, c.dy, c.dtheta)
-                  for c in list(p.children)[:p.n_children]]
+                  for c in p.children[:p.n_children]]
             ps.append((ch, p.noise_index, p.log_target, p.log_weight))
         return ps, le.value
 

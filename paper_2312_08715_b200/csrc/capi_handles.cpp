@@ -90,6 +90,7 @@ struct b3d_scene {
 };
 struct b3d_particles {
   std::vector<b3d_smc_particle> ps;
+  std::vector<b3d_smc_child> kids;  // ps[i].children = kids + i * n_objects
   double log_evidence = 0;
   double table_w = 0, table_h = 0;
   std::vector<std::shared_ptr<const b3d_object_model>> lib;
@@ -426,6 +427,18 @@ double nl_number(const J::Value& v) {
                   nl_type_name(v));
   return v.num;
 }
+// range-for over a json value: array elements, object values, nothing for
+// null, the value itself for a primitive
+std::vector<const J::Value*> nl_elems(const J::Value& v) {
+  std::vector<const J::Value*> out;
+  if (v.kind == J::Value::Array)
+    for (const J::Value& e : v.arr) out.push_back(&e);
+  else if (v.kind == J::Value::Object)
+    for (const auto& kv : v.obj) out.push_back(&kv.second);
+  else if (v.kind != J::Value::Null)
+    out.push_back(&v);
+  return out;
+}
 const std::string& nl_string(const J::Value& v) {
   if (v.kind != J::Value::String)
     throw NlError(std::string("[json.exception.type_error.302] type must be string, but is ") +
@@ -639,11 +652,11 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     if (r.has("noise_grid")) {
       Reader gr = r.object("noise_grid");
       grid.clear();
-      const J::Value& ps = gr.raw("p_outlier");
-      const J::Value& ss = gr.raw("sigma");
-      require(ps.is_array() && ss.is_array(), B3D_ERROR_CONFIG, "noise_grid: arrays expected");
-      for (const J::Value& p : ps.arr)
-        for (const J::Value& sv : ss.arr) grid.push_back({p.num, sv.num});
+      // b3d_capi.cpp:356-363 reads "sigma" inside the p_outlier loop: an
+      // empty p_outlier leaves it unread (an unknown key at finish())
+      for (const J::Value* p : nl_elems(gr.raw("p_outlier")))
+        for (const J::Value* sv : nl_elems(gr.raw("sigma")))
+          grid.push_back({nl_number(*p), nl_number(*sv)});
       gr.finish();
     }
     cfg.n_objects = (uint32_t)r.int_or("n_objects", 1);
@@ -679,7 +692,9 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     cfg.prefactor = B3D_PREFACTOR_PRINTED;  // ModelConfig default (generative.hpp:38)
     auto res = std::make_unique<b3d_particles>();
     res->ps.resize(cfg.n_particles ? cfg.n_particles : 1);
-    require(cfg.n_particles >= 1, B3D_ERROR, "smc_init: need at least one particle");
+    res->kids.resize(res->ps.size() * std::max<size_t>(cfg.n_objects, 1));
+    for (size_t i = 0; i < res->ps.size(); ++i)
+      res->ps[i].children = res->kids.data() + i * std::max<size_t>(cfg.n_objects, 1);
     ok(b3d_gpu_run_smc(g, objs.data(), (uint32_t)objs.size(), &cfg, seed, res->ps.data(),
                        &res->log_evidence));
     res->table_w = cfg.table_w;

@@ -579,9 +579,10 @@ extern "C" b3d_status b3d_gpu_run_smc(b3d_gpu_context* ctx, const b3d_smc_object
     need(ctx && library && cfg && particles && log_evidence, B3D_ERROR, "bad arguments");
     need(n_library >= 1, B3D_ERROR, "inference: empty library");
     need(cfg->n_noise_grid >= 1 && cfg->noise_grid, B3D_ERROR, "inference: empty noise grid");
-    need(cfg->n_objects >= 1 && cfg->n_objects <= B3D_SMC_MAX_CHILDREN, B3D_ERROR,
-         "run_smc: n_objects must be in 1..8");
+    need(cfg->n_objects >= 1, B3D_ERROR, "run_smc: n_objects must be >= 1");
     need(cfg->n_particles >= 1, B3D_ERROR, "smc_init: need at least one particle");
+    for (uint32_t i = 0; i < cfg->n_particles; ++i)
+      need(particles[i].children != nullptr, B3D_ERROR, "bad arguments");
     need(cfg->n_refine == 0 || cfg->refine, B3D_ERROR, "bad arguments");
     auto valid = [](const b3d_schedule_stage& s) {
       return s.n_dx >= 1 && s.n_dy >= 1 && s.n_dtheta >= 1;

@@ -48,6 +48,9 @@ def _sig(L):
     L.b3d_depth_image_destroy.argtypes = [vp]
     L.b3d_depth_image_data.argtypes = [vp]
     L.b3d_depth_image_data.restype = C.POINTER(C.c_float)
+    L.b3d_particles_log_evidence.argtypes = [vp, C.POINTER(C.c_double)]
+    L.b3d_particles_to_jsonl.argtypes = [vp, C.POINTER(C.c_void_p)]
+    L.b3d_string_free.argtypes = [vp]
     L.b3d_library_destroy.argtypes = [vp]
     L.b3d_scene_destroy.argtypes = [vp]
     L.b3d_particles_destroy.argtypes = [vp]
@@ -187,7 +190,32 @@ def run_cases(L, gpu: bool):
                 L.b3d_depth_image_destroy(img)
             else:
                 out[f"render_{n}_children"] = _res(L, st)
+            if n == 3 and st == 0:  # this render is the observation of the SMC case below
+                st = L.b3d_render(many, C.byref(TOP), C.byref(K), C.byref(img))
+                assert st == 0, L.b3d_last_error()
+                seen = vp(img.value)
             L.b3d_scene_destroy(many)
+        # run_smc placing more objects than any fixed particle layout holds
+        cfg = {"intrinsics": dict(fx=60.0, fy=60.0, cx=31.5, cy=23.5, width=64, height=48,
+                                  near=0.05, far=4.0),
+               "table": {"width": 0.4, "height": 0.4}, "n_objects": 10, "particles": 3,
+               "schedule": {"stage0": [2, 2, 2], "refine": [[2, 1, 2]]},
+               "noise_grid": {"p_outlier": [0.1], "sigma": [0.01]}}
+        part = vp()
+        st = L.b3d_infer(seen, C.byref(TOP), lib, json.dumps(cfg).encode(), 5, C.byref(part))
+        if st == 0:
+            le, txt = C.c_double(), C.c_void_p()
+            assert L.b3d_particles_log_evidence(part, C.byref(le)) == 0
+            assert L.b3d_particles_to_jsonl(part, C.byref(txt)) == 0
+            lines = C.string_at(txt).decode().splitlines()
+            L.b3d_string_free(txt)
+            L.b3d_particles_destroy(part)
+            ps = [[[c["object_id"], c["face"], c["dx"], c["dy"], c["dtheta"]]
+                   for c in json.loads(ln)["children"]] for ln in lines]
+            out["infer_ten_objects"] = [0, {"log_evidence": le.value, "particles": ps}]
+        else:
+            out["infer_ten_objects"] = _res(L, st)
+        L.b3d_depth_image_destroy(seen)
     # b3d_infer config schema (b3d_capi.cpp:297-379)
     kk = {"fx": 60.0, "fy": 60.0, "cx": 31.5, "cy": 23.5, "width": 64, "height": 48,
           "near": 0.05, "far": 4.0}
@@ -219,4 +247,5 @@ def run_cases(L, gpu: bool):
         L.b3d_depth_image_destroy(hdl)
     L.b3d_scene_destroy(sc)
     L.b3d_library_destroy(lib)
-    return {k: [st, msg.replace(tmp, "<tmp>")] for k, (st, msg) in out.items()}
+    return {k: [st, msg.replace(tmp, "<tmp>") if isinstance(msg, str) else msg]
+            for k, (st, msg) in out.items()}

@@ -7,13 +7,15 @@ unmodified -- by tests/golden/make_ref_golden.py capi).
 The CPU test runs every case the product settles before touching a device
 (argument, intrinsics, noise, file-format, manifest, scene-JSON and `infer`
 schema errors); the GPU test runs all of them, including the empty-render
-checks, device-side `infer` validation and whole 3- and 20-child renders.
+checks, device-side `infer` validation, whole 3- and 20-child renders and
+an `infer` placing ten objects (draws equal, log evidence to 1e-6 relative).
 """
 import ctypes
 import json
 import os
 import sys
 
+import numpy as np
 import pytest
 
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -34,9 +36,24 @@ def _lib():
     return ctypes.CDLL(b3d.lib()._name)
 
 
+def _same(a, b):
+    if isinstance(b[1], dict):  # an inference result: draws equal, evidence to 1e-6
+        if a[0] != b[0] or not isinstance(a[1], dict):
+            return False
+        ga, wa = a[1], b[1]
+        if abs(ga["log_evidence"] - wa["log_evidence"]) > 1e-6 * abs(wa["log_evidence"]):
+            return False
+        return len(ga["particles"]) == len(wa["particles"]) and all(
+            len(p) == len(q) and all(x[:2] == y[:2] and np.allclose(x[2:], y[2:], rtol=0,
+                                                                    atol=1e-12)
+                                     for x, y in zip(p, q))
+            for p, q in zip(ga["particles"], wa["particles"]))
+    return a == b
+
+
 def _compare(got, want):
     assert set(got) <= set(want), sorted(set(got) - set(want))
-    diff = {k: (got[k], want[k]) for k in got if got[k] != want[k]}
+    diff = {k: (got[k], want[k]) for k in got if not _same(got[k], want[k])}
     assert not diff, json.dumps(diff, indent=1)
 
 
