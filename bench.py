@@ -466,7 +466,13 @@ def run_smc_leg(ctx, b3d, configs, n_particles=1000, seed=0):
                         "10x10x8 x faces x 9 noise, 2 x 5x5x5 refine, 1,000 particles, "
                         "1 object; all render+score on device",
             "particles": n_particles, "seconds": dt, "renders": renders,
-            "renders_per_s": renders / dt, "log_evidence": le,
+            "renders_per_s": renders / dt,
+            "renders_device": ctx.last_smc_renders,
+            "renders_note": "renders = the reference's render+score evaluations for this "
+                            "workload; renders_device = distinct ones launched (particles on "
+                            "the same base scene, object, noise entry and cell share them: "
+                            "identical values)",
+            "log_evidence": le,
             "map_child": list(c), "truth": list(truth),
             "map_position_error_cm": 100.0 * float(np.hypot(c[2] - truth[2], c[3] - truth[3])),
             "map_object_correct": bool(c[0] == truth[0])}

@@ -502,6 +502,9 @@ typedef struct b3d_smc_config {
   double sigma_max;
   int32_t window; /* < 0: untruncated likelihood (ModelConfig::windowed = false) */
   int32_t prefactor;
+  uint64_t* renders; /* optional out: hypotheses rendered+scored on the device
+                        (distinct evaluations; particles sharing a base scene,
+                        object, noise entry and cell share them) */
 } b3d_smc_config;
 typedef struct b3d_smc_child {
   int32_t object_id, face;

@@ -119,7 +119,8 @@ class SmcConfig(C.Structure):
                 ("refine", C.c_void_p), ("noise_grid", C.c_void_p),
                 ("n_noise_grid", C.c_uint32), ("n_objects", C.c_uint32),
                 ("n_particles", C.c_uint32), ("resample_threshold", C.c_double),
-                ("sigma_max", C.c_double), ("window", C.c_int32), ("prefactor", C.c_int32)]
+                ("sigma_max", C.c_double), ("window", C.c_int32), ("prefactor", C.c_int32),
+                ("renders", C.c_void_p)]
 
 
 class SmcChild(C.Structure):
@@ -903,6 +904,8 @@ class GpuContext:
         cfg.n_objects, cfg.n_particles = n_objects, n_particles
         cfg.resample_threshold, cfg.sigma_max = resample_threshold, sigma_max
         cfg.window, cfg.prefactor = window, prefactor
+        renders = C.c_uint64()
+        cfg.renders = C.cast(C.byref(renders), C.c_void_p)
         out = (SmcParticle * n_particles)()
         kids = (SmcChild * (n_particles * max(1, n_objects)))()
         for i in range(n_particles):
@@ -916,6 +919,7 @@ class GpuContext:
             ch = [(c.object_id, c.face, c.dx, c.dy, c.dtheta)
                   for c in p.children[:p.n_children]]
             ps.append((ch, p.noise_index, p.log_target, p.log_weight))
+        self.last_smc_renders = renders.value  # device evaluations of that run
         return ps, le.value
 
     def set_base_scene(self, mesh_ids: Sequence[int], poses):

@@ -9,15 +9,23 @@
 //   * stage 0: one contact-cells launch per (object, face) with all noise
 //     entries, over the particle's partial scene as the base image
 //     (score_cells, inference.cpp:261-331; shared by all particles in
-//     smc_init, per particle in smc_extend as the reference does);
-//   * refine stages: the children of every particle's current cell, batched
+//     smc_init, per distinct partial scene in smc_extend);
+//   * refine stages: the children of every distinct current cell, batched
 //     across particles that share (object, noise) and base scene into one
-//     explicit-pose launch (smc_init), else one launch per particle;
+//     explicit-pose launch; particles on the same cell share its scores and
+//     normalisation (see "Memoised evaluation" below);
 //   * the final scene_target_logpdf of each particle, batched the same way.
 // Scores carry the fp32-term likelihood (<= 1e-4 relative of the reference,
 // DESIGN.md 5.1); everything else is the reference's arithmetic.
 #include <algorithm>
+#include <sched.h>
+
 #include <atomic>
+#include <condition_variable>
+#include <functional>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <cmath>
 #include <cstdint>
 #include <exception>
@@ -53,34 +61,106 @@ void need(bool c, b3d_status s, const char* m) {
 }
 
 // The per-particle host work (cell subdivision, child poses, priors,
-// normalisation, draws from each particle's own stream) runs on all host
-// threads, as the reference's parallel_for does (parallel.hpp:19-54); the
-// result does not depend on the thread count.
+// normalisation, draws from each particle's own stream) runs on the host
+// threads this process may use, as the reference's parallel_for does
+// (parallel.hpp:19-54); the result does not depend on the thread count.
+// Workers persist across calls (a call costs a wake-up, not a spawn).
+class Pool {
+ public:
+  static Pool& get() {
+    static Pool p;
+    return p;
+  }
+  size_t threads() const { return workers_.size() + 1; }
+  static bool& in_pool() {  // a parallel_for inside a job runs serially
+    thread_local bool f = false;
+    return f;
+  }
+  void run(size_t n, const std::function<void(size_t)>& f) {
+    std::unique_lock<std::mutex> lk(run_mu_);  // one job at a time
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      job_ = &f;
+      n_ = n;
+      next_ = 0;
+      err_ = nullptr;
+      busy_ = workers_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> g(mu_);
+    done_.wait(g, [&] { return busy_ == 0; });
+    job_ = nullptr;
+    if (err_) std::rethrow_exception(err_);
+  }
+  ~Pool() {
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : workers_) t.join();
+  }
+
+ private:
+  Pool() {
+    size_t hw = std::max(1u, std::thread::hardware_concurrency());
+    cpu_set_t set;
+    if (sched_getaffinity(0, sizeof set, &set) == 0) hw = std::max(1, CPU_COUNT(&set));
+    for (size_t t = 1; t < std::min<size_t>(hw, 64); ++t)
+      workers_.emplace_back([this] { loop(); });
+  }
+  void work() {
+    in_pool() = true;
+    try {
+      for (size_t i; (i = next_.fetch_add(1)) < n_;) (*job_)(i);
+    } catch (...) {
+      std::lock_guard<std::mutex> g(mu_);
+      if (!err_) err_ = std::current_exception();
+      next_ = n_;
+    }
+    in_pool() = false;
+  }
+  void loop() {
+    uint64_t seen = 0;
+    for (;;) {
+      {
+        std::unique_lock<std::mutex> g(mu_);
+        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
+        if (stop_) return;
+        seen = gen_;
+      }
+      work();
+      std::lock_guard<std::mutex> g(mu_);
+      if (--busy_ == 0) done_.notify_one();
+    }
+  }
+  std::vector<std::thread> workers_;
+  std::mutex mu_, run_mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(size_t)>* job_ = nullptr;
+  size_t n_ = 0, busy_ = 0;
+  std::atomic<size_t> next_{0};
+  std::exception_ptr err_;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
+};
+
 template <class F>
 void parallel_for(size_t n, F&& f) {
-  const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-  const size_t nth = std::min<size_t>(hw, (n + 31) / 32);
-  if (nth <= 1) {
+  if (n < 64 || Pool::get().threads() == 1 || Pool::in_pool()) {
     for (size_t i = 0; i < n; ++i) f(i);
     return;
   }
-  std::atomic<size_t> next{0};
-  std::exception_ptr err;
-  std::mutex mu;
-  auto work = [&] {
-    try {
-      for (size_t i; (i = next.fetch_add(1)) < n;) f(i);
-    } catch (...) {
-      std::lock_guard<std::mutex> lk(mu);
-      if (!err) err = std::current_exception();
-      next = n;
-    }
+  // chunks of >= 16 items per atomic claim
+  const size_t chunk = std::max<size_t>(16, n / (8 * Pool::get().threads()));
+  const size_t nc = (n + chunk - 1) / chunk;
+  const std::function<void(size_t)> body = [&](size_t c) {
+    const size_t e = std::min(n, (c + 1) * chunk);
+    for (size_t i = c * chunk; i < e; ++i) f(i);
   };
-  std::vector<std::thread> pool;
-  for (size_t t = 1; t < nth; ++t) pool.emplace_back(work);
-  work();
-  for (auto& th : pool) th.join();
-  if (err) std::rethrow_exception(err);
+  Pool::get().run(nc, body);
 }
 
 // rng.cpp: xoshiro256** seeded by splitmix64, split via mix()
@@ -139,10 +219,36 @@ struct Smc {
   uint32_t n_lib;
   const b3d_smc_config& cfg;
   std::vector<b3d_noise> grid;
+  uint64_t renders = 0;  // device render+score evaluations
 
   // footprint(obj, face) (scene_graph.cpp:91-95): x, y extents of the
-  // face-down AABB; the stage-0 parent's upper ends are table - footprint
+  // face-down AABB; the stage-0 parent's upper ends are table - footprint.
+  // Tabulated once per (object, face 1..6) by init().
+  std::vector<double> fp_tab, prior_tab;
+  void init() {
+    fp_tab.assign((size_t)n_lib * 12, 0.0);
+    prior_tab.assign((size_t)n_lib * 6, kNegInf);
+    for (uint32_t o = 0; o < n_lib; ++o)
+      for (int f = 1; f <= 6; ++f) {
+        double lo[3], hi[3];
+        rotated((int)o, f, lo, hi);
+        const size_t j = o * 6 + (f - 1);
+        fp_tab[2 * j] = hi[0] - lo[0];
+        fp_tab[2 * j + 1] = hi[1] - lo[1];
+        // child_prior's in-support value (the same expression, evaluated once)
+        const double dx_range = cfg.table_w - fp_tab[2 * j],
+                     dy_range = cfg.table_h - fp_tab[2 * j + 1];
+        if (dx_range > 0 && dy_range > 0)
+          prior_tab[j] = -std::log(static_cast<double>(n_lib)) - std::log(6.0) -
+                         std::log(dx_range) - std::log(dy_range) - std::log(kTwoPi);
+      }
+  }
   void footprint(int obj, int face, double& fx, double& fy) const {
+    if (face >= 1 && face <= 6 && (size_t)obj < n_lib) {
+      fx = fp_tab[((size_t)obj * 6 + (face - 1)) * 2];
+      fy = fp_tab[((size_t)obj * 6 + (face - 1)) * 2 + 1];
+      return;
+    }
     double lo[3], hi[3];
     rotated(obj, face, lo, hi);
     fx = hi[0] - lo[0];
@@ -172,6 +278,8 @@ struct Smc {
     if (c.dx < 0 || c.dx > dx_range || c.dy < 0 || c.dy > dy_range || c.dtheta < 0 ||
         c.dtheta >= kTwoPi)
       return kNegInf;
+    if (c.face >= 1 && c.face <= 6 && (size_t)c.object_id < n_lib)
+      return prior_tab[(size_t)c.object_id * 6 + (c.face - 1)];
     return -std::log(static_cast<double>(n_lib)) - std::log(6.0) - std::log(dx_range) -
            std::log(dy_range) - std::log(kTwoPi);
   }
@@ -193,38 +301,61 @@ struct Smc {
   }
   // render_partial (inference.cpp:172-184) as the base image: table, then
   // the partial scene's children in order
+  bool base_valid = false;
+  std::string base_key;  // partial_key of the context's current base scene
   void set_base(const std::vector<Child>& partial) {
+    const std::string key = partial_key(partial);
+    if (base_valid && key == base_key) return;  // already the context's base image
     std::vector<int32_t> ids{cfg.table_mesh};
     std::vector<b3d_pose> poses{b3d_pose{1, 0, 0, 0, 0, 0, 0}};
     for (const Child& c : partial) {
       ids.push_back(lib[c.object_id].mesh_id);
       poses.push_back(child_pose(c));
     }
+    base_valid = false;
     ok(b3d_gpu_set_base_scene(g, ids.data(), poses.data(), (uint32_t)ids.size()));
+    base_key = key;
+    base_valid = true;
   }
   void set_noise(const b3d_noise* nz, uint32_t n) {
     ok(b3d_gpu_set_likelihood(g, nz, n, cfg.sigma_max, cfg.window, cfg.prefactor));
   }
 
   // score_cells normalisation (inference.cpp:315-330)
-  static std::vector<double> normalise(const std::vector<double>& lt, bool& all_zero) {
-    std::vector<double> s(lt.size(), 0.0);
+  static void normalise_into(const double* lt, size_t n, std::vector<double>& s,
+                             bool& all_zero) {
+    if (s.size() < n) s.resize(n);
     double max_log = kNegInf;
-    for (double x : lt) max_log = std::max(max_log, x);
+    for (size_t i = 0; i < n; ++i) max_log = std::max(max_log, lt[i]);
     all_zero = !std::isfinite(max_log);
     if (all_zero) {
-      std::fill(s.begin(), s.end(), 1.0 / lt.size());
-      return s;
+      std::fill(s.begin(), s.begin() + n, 1.0 / n);
+      return;
     }
+    // the exps in parallel, their total in index order (the same bits)
+    parallel_for((n + 255) / 256, [&](size_t b) {
+      const size_t e = std::min(n, (b + 1) * 256);
+      for (size_t i = b * 256; i < e; ++i) s[i] = std::exp(lt[i] - max_log);
+    });
     double total = 0;
-    for (size_t i = 0; i < lt.size(); ++i) {
-      s[i] = std::exp(lt[i] - max_log);
-      total += s[i];
-    }
-    for (double& x : s) x /= total;
+    for (size_t i = 0; i < n; ++i) total += s[i];
+    for (size_t i = 0; i < n; ++i) s[i] /= total;
+  }
+  static std::vector<double> normalise(const std::vector<double>& lt, bool& all_zero) {
+    std::vector<double> s;
+    normalise_into(lt.data(), lt.size(), s, all_zero);
+    s.resize(lt.size());
     return s;
   }
   // sample_categorical (inference.cpp:345-353)
+  // The same draw against a precomputed running sum: cdf[i] is the value of
+  // the loop's `acc` after probs[i] (the same additions in the same order),
+  // non-decreasing, so the loop's first i with u < acc is an upper_bound.
+  static size_t sample_cdf(const double* cdf, size_t n, Rng& rng) {
+    const double u = rng.uniform();
+    const size_t i = std::upper_bound(cdf, cdf + n, u) - cdf;
+    return i < n ? i : n - 1;
+  }
   static size_t sample(const std::vector<double>& probs, Rng& rng) {
     const double u = rng.uniform();
     double acc = 0;
@@ -237,62 +368,111 @@ struct Smc {
 
   // build_stage0 (inference.cpp:332-340) over `partial`: cells in the
   // reference's order (object, face, ix, iy, it, noise) and their scores
+  // The cells are implicit -- per (object, face) block its first index and
+  // support, cell k decoded on demand -- and the score buffers persist
+  // across calls (stage 0 of smc_extend runs once per distinct partial scene).
   struct Stage0 {
-    std::vector<Cell> cells;
-    std::vector<double> scores;
+    struct Block {
+      size_t first;
+      int obj, face;
+      double dx_range, dy_range;
+    };
+    std::vector<Block> blocks;
+    size_t n = 0, nn = 1;
+    b3d_schedule_stage s{};
+    std::vector<double> lt, scores, cdf;
     bool all_zero = false;
+    // stage0_cells (inference.cpp:208-238): order (object, face, ix, iy,
+    // it, noise), the reference's interval arithmetic
+    Cell cell(size_t k) const {
+      size_t b = blocks.size() - 1;
+      while (blocks[b].first > k) --b;
+      const Block& bl = blocks[b];
+      const size_t local = k - bl.first, ci = local / nn;
+      const uint32_t it = (uint32_t)(ci % s.n_dtheta);
+      const uint32_t iy = (uint32_t)((ci / s.n_dtheta) % s.n_dy);
+      const uint32_t ix = (uint32_t)(ci / ((size_t)s.n_dtheta * s.n_dy));
+      Cell c;
+      c.object_id = bl.obj;
+      c.face = bl.face;
+      c.dx = {bl.dx_range * ix / s.n_dx, bl.dx_range * (ix + 1) / s.n_dx};
+      c.dy = {bl.dy_range * iy / s.n_dy, bl.dy_range * (iy + 1) / s.n_dy};
+      c.dtheta = {kTwoPi * it / s.n_dtheta, kTwoPi * (it + 1) / s.n_dtheta};
+      c.noise_index = (int)(local % nn);
+      return c;
+    }
   };
-  Stage0 build_stage0(const std::vector<Child>& partial) {
-    Stage0 t;
+  Stage0 s0_buf;
+  std::vector<b3d_pose> s0_poses;
+  std::vector<double> s0_lik;
+  std::vector<uint8_t> s0_st;
+  const Stage0& build_stage0(const std::vector<Child>& partial) {
+    Stage0& t = s0_buf;
     const b3d_schedule_stage& s = cfg.stage0;
+    t.s = s;
+    t.blocks.clear();
     const double base_prior = prior_sum(partial);
     set_base(partial);
     set_noise(grid.data(), (uint32_t)grid.size());
     const size_t nn = grid.size();
-    std::vector<double> lt;
-    for (uint32_t obj = 0; obj < n_lib; ++obj)
+    t.nn = nn;
+    const size_t nc = (size_t)s.n_dx * s.n_dy * s.n_dtheta;
+    size_t total = 0;
+    for (uint32_t obj = 0; obj < n_lib; ++obj) {
+      // one device launch per object: every face's cells, all noise entries
+      const size_t first = total;
+      size_t np = 0;
       for (int face = 1; face <= 6; ++face) {
         double fx, fy;
         footprint(obj, face, fx, fy);
         const double dx_range = cfg.table_w - fx, dy_range = cfg.table_h - fy;
         if (dx_range <= 0 || dy_range <= 0) continue;  // empty support branch
-        const size_t first = t.cells.size();
-        for (uint32_t ix = 0; ix < s.n_dx; ++ix)
-          for (uint32_t iy = 0; iy < s.n_dy; ++iy)
-            for (uint32_t it = 0; it < s.n_dtheta; ++it) {
-              Cell c;
-              c.object_id = (int)obj;
-              c.face = face;
-              c.dx = {dx_range * ix / s.n_dx, dx_range * (ix + 1) / s.n_dx};
-              c.dy = {dy_range * iy / s.n_dy, dy_range * (iy + 1) / s.n_dy};
-              c.dtheta = {kTwoPi * it / s.n_dtheta, kTwoPi * (it + 1) / s.n_dtheta};
-              for (size_t e = 0; e < nn; ++e) {
-                c.noise_index = (int)e;
-                t.cells.push_back(c);
-              }
-            }
-        // one device launch for the whole (object, face) group, all noise
-        b3d_contact_grid cg = contact(obj, face);
-        cg.count[0] = s.n_dx;
-        cg.count[1] = s.n_dy;
-        cg.count[2] = s.n_dtheta;
-        const size_t nc = (size_t)s.n_dx * s.n_dy * s.n_dtheta;
-        std::vector<double> lik(nc * nn);
-        std::vector<uint8_t> st(nc);
-        ok(b3d_gpu_score_contact_grid(g, lib[obj].mesh_id, &cg, lik.data(), st.data()));
-        for (size_t k = 0; k < nc * nn; ++k) {
-          const Cell& c = t.cells[first + k];
+        t.blocks.push_back({total, (int)obj, face, dx_range, dy_range});
+        total += nc * nn;
+        // the stage-0 parent [0, table - footprint] x [0, 2 pi) subdivided:
+        // the block's cells posed at their centres (the device contact
+        // grid's poses)
+        b3d_contact_cells cc{};
+        cc.grid = contact(obj, face);
+        cc.grid.count[0] = s.n_dx;
+        cc.grid.count[1] = s.n_dy;
+        cc.grid.count[2] = s.n_dtheta;
+        cc.dx_hi = dx_range;
+        cc.dy_hi = dy_range;
+        cc.dtheta_hi = kTwoPi;
+        if (s0_poses.size() < np + nc) s0_poses.resize(np + nc);
+        ok(b3d_contact_cells_poses(&cc, s0_poses.data() + np));
+        np += nc;
+      }
+      if (np == 0) continue;
+      if (s0_lik.size() < np * nn) s0_lik.resize(np * nn);
+      if (s0_st.size() < np) s0_st.resize(np);
+      prof("s0 host");
+      ok(b3d_gpu_score_poses(g, lib[obj].mesh_id, s0_poses.data(), np, s0_lik.data(),
+                             s0_st.data()));
+      prof("s0 device");
+      renders += np;
+      if (t.lt.size() < total) t.lt.resize(total);
+      parallel_for(np, [&](size_t j) {
+        for (size_t e = 0; e < nn; ++e) {
+          const size_t k = j * nn + e;
+          const Cell c = t.cell(first + k);
           const Child cc{c.object_id, c.face, c.dx.center(), c.dy.center(), c.dtheta.center()};
           const double cp = child_prior(cc);
-          const double l = st[k / nn] ? kNegInf : lik[k];
-          lt.push_back(std::isfinite(base_prior) && std::isfinite(cp) && std::isfinite(l)
-                           ? base_prior + cp + l
-                           : kNegInf);
+          const double l = s0_st[j] ? kNegInf : s0_lik[k];
+          t.lt[first + k] = std::isfinite(base_prior) && std::isfinite(cp) && std::isfinite(l)
+                                ? base_prior + cp + l
+                                : kNegInf;
         }
-      }
-    need(!t.cells.empty(), B3D_ERROR_NUMERIC,
+      });
+    }
+    need(total > 0, B3D_ERROR_NUMERIC,
          "stage 0: empty proposal support (no object fits the table)");
-    t.scores = normalise(lt, t.all_zero);
+    t.n = total;
+    normalise_into(t.lt.data(), total, t.scores, t.all_zero);
+    if (t.cdf.size() < total) t.cdf.resize(total);
+    double acc = 0;  // sample_categorical's running sum (see sample_cdf)
+    for (size_t i = 0; i < total; ++i) t.cdf[i] = acc += t.scores[i];
     return t;
   }
 
@@ -320,6 +500,7 @@ struct Smc {
     set_noise(&grid[noise_index], 1);
     std::vector<double> s(poses.size());
     std::vector<uint8_t> st(poses.size());
+    renders += poses.size();
     ok(b3d_gpu_score_poses(g, lib[obj].mesh_id, poses.data(), poses.size(), s.data(),
                            st.data()));
     for (size_t i = 0; i < s.size(); ++i)
@@ -333,94 +514,159 @@ struct Smc {
     Child child{};
   };
 
+  // Memoised evaluation.  A stage's log targets are a pure function of the
+  // base scene (the partial children), the object, the noise entry and the
+  // cell, and so are its normalised scores: particles that share them (many
+  // draw the same stage-0 cell; resampled particles are copies) share one
+  // device launch slot and one normalisation, and only their draws -- each
+  // from the particle's own stream -- stay per particle.  Identical values
+  // to evaluating every particle separately (the kernel's score of a pose
+  // does not depend on the rest of its batch).  Keys are the fields' bytes.
+  template <class T>
+  static void put(std::string& k, const T& v) {
+    k.append(reinterpret_cast<const char*>(&v), sizeof v);
+  }
+  static std::string partial_key(const std::vector<Child>& cs) {
+    std::string k;
+    for (const Child& c : cs) {
+      put(k, c.object_id);
+      put(k, c.face);
+      put(k, c.dx);
+      put(k, c.dy);
+      put(k, c.dtheta);
+    }
+    return k;
+  }
+  static std::string cell_key(const Cell& c) {
+    std::string k;
+    put(k, c.object_id);
+    put(k, c.face);
+    put(k, c.noise_index);
+    for (const Interval* iv : {&c.dx, &c.dy, &c.dtheta}) {
+      put(k, iv->lo);
+      put(k, iv->hi);
+    }
+    return k;
+  }
+  // distinct values of key(i) for i in members, in first-member order:
+  // returns the representatives and sets of[m] = representative slot of
+  // members[m]
+  template <class K>
+  static std::vector<size_t> distinct(const std::vector<size_t>& members, K&& key,
+                                      std::vector<size_t>& of) {
+    std::map<std::string, size_t> idx;
+    std::vector<size_t> rep;
+    of.resize(members.size());
+    for (size_t m = 0; m < members.size(); ++m) {
+      const auto ins = idx.emplace(key(members[m]), rep.size());
+      if (ins.second) rep.push_back(members[m]);
+      of[m] = ins.first->second;
+    }
+    return rep;
+  }
+  // particles grouped by identical partial scene (= base image)
+  static std::vector<std::vector<size_t>> by_partial(
+      const std::vector<std::vector<Child>>& partial) {
+    std::vector<size_t> all(partial.size()), of;
+    for (size_t i = 0; i < all.size(); ++i) all[i] = i;
+    const std::vector<size_t> rep =
+        distinct(all, [&](size_t i) { return partial_key(partial[i]); }, of);
+    std::vector<std::vector<size_t>> groups(rep.size());
+    for (size_t i = 0; i < all.size(); ++i) groups[of[i]].push_back(i);
+    return groups;
+  }
+
   // coarse_to_fine_propose (inference.cpp:357-396) for a batch of particles
-  // (stream[i], partial[i]); stage0 shared (smc_init) or per particle.
+  // (stream[i], partial[i]); stage0 shared (smc_init) or per distinct partial
+  // scene (smc_extend).
   std::vector<Prop> propose(std::vector<Rng>& stream,
                             const std::vector<std::vector<Child>>& partial,
                             const Stage0* shared) {
     const size_t P = stream.size();
     std::vector<Prop> props(P);
     auto pick0 = [&](size_t i, const Stage0* s0) {
-      const size_t k = sample(s0->scores, stream[i]);
+      const size_t k = sample_cdf(s0->cdf.data(), s0->n, stream[i]);
       props[i].log_q = std::log(s0->scores[k]);
-      props[i].current = s0->cells[k];
+      props[i].current = s0->cell(k);
     };
+    const std::vector<std::vector<size_t>> bases = by_partial(partial);
     if (shared) {
       parallel_for(P, [&](size_t i) { pick0(i, shared); });
     } else {
-      for (size_t i = 0; i < P; ++i) {  // a device stage 0 per particle
-        const Stage0 local = build_stage0(partial[i]);
-        pick0(i, &local);
+      for (const std::vector<size_t>& grp : bases) {  // a device stage 0 per partial scene
+        const Stage0& local = build_stage0(partial[grp[0]]);
+        parallel_for(grp.size(), [&](size_t m) { pick0(grp[m], &local); });
       }
     }
     for (uint32_t r = 0; r < cfg.n_refine; ++r) {
       const b3d_schedule_stage& st = cfg.refine[r];
-      std::vector<std::vector<Cell>> cells(P);
-      parallel_for(P, [&](size_t i) { cells[i] = subdivide(props[i].current, st); });
-      if (cells[0].size() == 1) {
-        for (size_t i = 0; i < P; ++i) props[i].current = cells[i][0];
+      if ((size_t)st.n_dx * st.n_dy * st.n_dtheta == 1) {
+        parallel_for(P, [&](size_t i) { props[i].current = subdivide(props[i].current, st)[0]; });
         continue;
       }
-      // log targets of every particle's children (score_cells with the
-      // particle's noise: the cells inherit noise_index)
-      std::vector<std::vector<double>> lt(P);
-      auto fill = [&](const std::vector<size_t>& members) {
-        std::vector<size_t> offs(members.size() + 1, 0);
-        for (size_t m = 0; m < members.size(); ++m)
-          offs[m + 1] = offs[m] + cells[members[m]].size();
-        std::vector<b3d_pose> poses(offs.back());
-        parallel_for(members.size(), [&](size_t m) {
-          const size_t i = members[m];
-          b3d_contact_cells cc{};
-          cc.grid = contact(props[i].current.object_id, props[i].current.face);
-          cc.grid.count[0] = st.n_dx;
-          cc.grid.count[1] = st.n_dy;
-          cc.grid.count[2] = st.n_dtheta;
-          const Cell& cur = props[i].current;
-          cc.dx_lo = cur.dx.lo;
-          cc.dx_hi = cur.dx.hi;
-          cc.dy_lo = cur.dy.lo;
-          cc.dy_hi = cur.dy.hi;
-          cc.dtheta_lo = cur.dtheta.lo;
-          cc.dtheta_hi = cur.dtheta.hi;
-          ok(b3d_contact_cells_poses(&cc, poses.data() + offs[m]));
-        });
-        const Cell& lead = props[members[0]].current;
-        const std::vector<double> lik = score_poses(lead.object_id, lead.noise_index, poses);
-        parallel_for(members.size(), [&](size_t m) {
-          const size_t i = members[m];
-          const double base_prior = prior_sum(partial[i]);
-          size_t k = offs[m];
-          lt[i].reserve(cells[i].size());
-          for (const Cell& c : cells[i]) {
-            const Child cc{c.object_id, c.face, c.dx.center(), c.dy.center(), c.dtheta.center()};
-            const double cp = child_prior(cc);
-            const double l = lik[k++];
-            lt[i].push_back(std::isfinite(base_prior) && std::isfinite(cp) && std::isfinite(l)
-                                ? base_prior + cp + l
-                                : kNegInf);
-          }
-        });
-      };
-      if (shared) {  // one base scene: batch by (object, noise entry)
-        set_base(partial[0]);
-        std::map<std::pair<int, int>, std::vector<size_t>> groups;
-        for (size_t i = 0; i < P; ++i)
-          groups[{props[i].current.object_id, props[i].current.noise_index}].push_back(i);
-        for (const auto& kv : groups) fill(kv.second);
-      } else {
-        for (size_t i = 0; i < P; ++i) {
-          set_base(partial[i]);
-          fill({i});
+      for (const std::vector<size_t>& grp : bases) {
+        // the group's distinct current cells: children, log targets and
+        // normalised scores once each (score_cells with the particle's noise:
+        // the cells inherit noise_index)
+        std::vector<size_t> of;
+        const std::vector<size_t> rep =
+            distinct(grp, [&](size_t i) { return cell_key(props[i].current); }, of);
+        const size_t U = rep.size();
+        std::vector<std::vector<Cell>> cells(U);
+        std::vector<std::vector<double>> sc(U);
+        parallel_for(U, [&](size_t u) { cells[u] = subdivide(props[rep[u]].current, st); });
+        const double base_prior = prior_sum(partial[grp[0]]);
+        set_base(partial[grp[0]]);
+        std::map<std::pair<int, int>, std::vector<size_t>> batches;  // (object, noise)
+        for (size_t u = 0; u < U; ++u)
+          batches[{props[rep[u]].current.object_id, props[rep[u]].current.noise_index}]
+              .push_back(u);
+        for (const auto& kv : batches) {
+          const std::vector<size_t>& us = kv.second;
+          std::vector<size_t> offs(us.size() + 1, 0);
+          for (size_t m = 0; m < us.size(); ++m) offs[m + 1] = offs[m] + cells[us[m]].size();
+          std::vector<b3d_pose> poses(offs.back());
+          parallel_for(us.size(), [&](size_t m) {
+            const Cell& cur = props[rep[us[m]]].current;
+            b3d_contact_cells cc{};
+            cc.grid = contact(cur.object_id, cur.face);
+            cc.grid.count[0] = st.n_dx;
+            cc.grid.count[1] = st.n_dy;
+            cc.grid.count[2] = st.n_dtheta;
+            cc.dx_lo = cur.dx.lo;
+            cc.dx_hi = cur.dx.hi;
+            cc.dy_lo = cur.dy.lo;
+            cc.dy_hi = cur.dy.hi;
+            cc.dtheta_lo = cur.dtheta.lo;
+            cc.dtheta_hi = cur.dtheta.hi;
+            ok(b3d_contact_cells_poses(&cc, poses.data() + offs[m]));
+          });
+          const std::vector<double> lik = score_poses(kv.first.first, kv.first.second, poses);
+          parallel_for(us.size(), [&](size_t m) {
+            const size_t u = us[m];
+            std::vector<double> lt;
+            lt.reserve(cells[u].size());
+            size_t k = offs[m];
+            for (const Cell& c : cells[u]) {
+              const Child cc{c.object_id, c.face, c.dx.center(), c.dy.center(),
+                             c.dtheta.center()};
+              const double cp = child_prior(cc);
+              const double l = lik[k++];
+              lt.push_back(std::isfinite(base_prior) && std::isfinite(cp) && std::isfinite(l)
+                               ? base_prior + cp + l
+                               : kNegInf);
+            }
+            bool az;
+            sc[u] = normalise(lt, az);
+          });
         }
+        parallel_for(grp.size(), [&](size_t m) {
+          const size_t i = grp[m], u = of[m];
+          const size_t pick = sample(sc[u], stream[i]);
+          props[i].log_q += std::log(sc[u][pick]);
+          props[i].current = cells[u][pick];
+        });
       }
-      parallel_for(P, [&](size_t i) {
-        bool az;
-        const std::vector<double> sc = normalise(lt[i], az);
-        const size_t pick = sample(sc, stream[i]);
-        props[i].log_q += std::log(sc[pick]);
-        props[i].current = cells[i][pick];
-      });
     }
     for (size_t i = 0; i < P; ++i) {
       Prop& pr = props[i];
@@ -436,36 +682,42 @@ struct Smc {
   }
 
   // scene_target_logpdf (inference.cpp:186-196) of each particle's scene
-  // (partial + its new child) with its noise; same batching as propose
+  // (partial + its new child) with its noise: per partial scene one launch
+  // per (object, noise) over the distinct children
   std::vector<double> targets(const std::vector<std::vector<Child>>& partial,
-                              const std::vector<Prop>& props, bool shared_base) {
+                              const std::vector<Prop>& props) {
     const size_t P = props.size();
     std::vector<double> out(P, kNegInf);
-    auto fill = [&](const std::vector<size_t>& members) {
-      std::vector<b3d_pose> poses(members.size());
-      parallel_for(members.size(), [&](size_t m) { poses[m] = child_pose(props[members[m]].child); });
-      const std::vector<double> lik =
-          score_poses(props[members[0]].child.object_id, props[members[0]].current.noise_index,
-                      poses);
-      for (size_t k = 0; k < members.size(); ++k) {
-        const size_t i = members[k];
+    for (const std::vector<size_t>& grp : by_partial(partial)) {
+      std::vector<size_t> of;
+      const std::vector<size_t> rep = distinct(
+          grp,
+          [&](size_t i) {
+            std::string k = partial_key({props[i].child});
+            put(k, props[i].current.noise_index);
+            return k;
+          },
+          of);
+      set_base(partial[grp[0]]);
+      std::map<std::pair<int, int>, std::vector<size_t>> batches;  // (object, noise)
+      for (size_t u = 0; u < rep.size(); ++u)
+        batches[{props[rep[u]].child.object_id, props[rep[u]].current.noise_index}].push_back(u);
+      std::vector<double> lik(rep.size());
+      for (const auto& kv : batches) {
+        std::vector<b3d_pose> poses(kv.second.size());
+        parallel_for(poses.size(),
+                     [&](size_t m) { poses[m] = child_pose(props[rep[kv.second[m]]].child); });
+        const std::vector<double> l = score_poses(kv.first.first, kv.first.second, poses);
+        for (size_t m = 0; m < poses.size(); ++m) lik[kv.second[m]] = l[m];
+      }
+      parallel_for(grp.size(), [&](size_t m) {
+        const size_t i = grp[m];
         std::vector<Child> all = partial[i];
         all.push_back(props[i].child);
         const double prior = prior_sum(all);
-        out[i] = (std::isfinite(prior) && std::isfinite(lik[k])) ? prior + lik[k] : kNegInf;
-      }
-    };
-    if (shared_base) {
-      set_base(partial[0]);
-      std::map<std::pair<int, int>, std::vector<size_t>> groups;
-      for (size_t i = 0; i < P; ++i)
-        groups[{props[i].child.object_id, props[i].current.noise_index}].push_back(i);
-      for (const auto& kv : groups) fill(kv.second);
-    } else {
-      for (size_t i = 0; i < P; ++i) {
-        set_base(partial[i]);
-        fill({i});
-      }
+        const double l = lik[of[m]];
+        out[i] = (std::isfinite(prior) && std::isfinite(l)) ? prior + l : kNegInf;
+      });
     }
     return out;
   }
@@ -516,18 +768,33 @@ struct Smc {
   }
 
   // run_smc (inference.cpp:493-520)
+  // B3D_SMC_PROFILE=1: wall time of each phase on stderr (diagnostics)
+  std::chrono::steady_clock::time_point t_prev = std::chrono::steady_clock::now();
+  const bool profiling = std::getenv("B3D_SMC_PROFILE") != nullptr;
+  void prof(const char* what) {
+    if (!profiling) return;
+    const auto now = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "smc %-10s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(now - t_prev).count());
+    t_prev = now;
+  }
+
   std::vector<Particle> run(uint64_t seed, double& log_evidence) {
     const Rng rng(seed);
     const size_t P = cfg.n_particles;
     std::vector<Particle> ps(P);
     {  // smc_init (inference.cpp:398-420)
-      const Stage0 s0 = build_stage0({});
+      prof("start");
+      const Stage0& s0 = build_stage0({});
+      prof("stage0");
       need(!s0.all_zero, B3D_ERROR_NUMERIC, "smc_init: all-zero scores at stage 0");
       std::vector<Rng> streams;
       for (size_t i = 0; i < P; ++i) streams.push_back(rng.split(1, i));
       const std::vector<std::vector<Child>> partial(P);
       const std::vector<Prop> props = propose(streams, partial, &s0);
-      const std::vector<double> lt = targets(partial, props, true);
+      prof("propose");
+      const std::vector<double> lt = targets(partial, props);
+      prof("targets");
       for (size_t i = 0; i < P; ++i) {
         ps[i].children = {props[i].child};
         ps[i].noise_index = props[i].current.noise_index;
@@ -552,7 +819,7 @@ struct Smc {
         partial.push_back(ps[i].children);
       }
       const std::vector<Prop> props = propose(streams, partial, nullptr);
-      const std::vector<double> lt = targets(partial, props, false);
+      const std::vector<double> lt = targets(partial, props);
       for (size_t i = 0; i < P; ++i) {
         const double prev = ps[i].log_target;
         ps[i].children.push_back(props[i].child);
@@ -597,6 +864,7 @@ extern "C" b3d_status b3d_gpu_run_smc(b3d_gpu_context* ctx, const b3d_smc_object
            B3D_ERROR, "noise grid entry outside support");
     }
     Smc smc{ctx, library, n_library, *cfg, {}};
+    smc.init();
     smc.grid.assign(cfg->noise_grid, cfg->noise_grid + cfg->n_noise_grid);
     double le = 0;
     const std::vector<Particle> ps = smc.run(seed, le);
@@ -612,6 +880,7 @@ extern "C" b3d_status b3d_gpu_run_smc(b3d_gpu_context* ctx, const b3d_smc_object
       o.log_weight = ps[i].log_weight;
     }
     *log_evidence = le;
+    if (cfg->renders) *cfg->renders = smc.renders;
     return B3D_OK;
   } catch (const Fail& f) {
     b3d200_set_last_error(f.what());
