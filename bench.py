@@ -1005,7 +1005,9 @@ def main():
                                               else 64 + 40 if xch is not None
                                               else h_scores.nbytes + h_status.nbytes
                                               + h_all.nbytes + 64 + 40),
-                    "ms_per_step": e2e_total / args.steps},
+                    "ms_per_step": e2e_total / args.steps,
+                    "ms_per_step_p50": float(np.median(e2e_ms)),
+                    "ms_per_step_max": float(max(e2e_ms))},
             "clocks": clk,
             "roofline": roof,
             "cpu_baseline": cpu,
