@@ -233,6 +233,15 @@ B3D_API b3d_status b3d_gpu_set_score_peers(b3d_gpu_context* ctx, const uint64_t*
  * fail after 20 s instead of hanging the device. */
 B3D_API b3d_status b3d_gpu_shard_barrier(b3d_gpu_context* ctx, const uint64_t* signal_ptrs,
                                          uint32_t n_ranks, uint32_t rank, uint64_t epoch);
+/* Diagnostics: the exchange protocol (stores into every rank's array half,
+ * signal-pad barrier, reads of the own half) for n_ranks ranks emulated as the
+ * blocks of one cooperative launch on this device, `rounds` epochs, one rank
+ * per epoch holding its reads hold_ns apart.  *errors = reads that saw a value
+ * other than the epoch's (0 double-buffered; single-buffered shows the race
+ * the double buffer removes). */
+B3D_API b3d_status b3d_gpu_test_exchange_emulation(b3d_gpu_context* ctx, uint32_t n_ranks,
+                                                   uint32_t rounds, int32_t double_buffered,
+                                                   uint64_t hold_ns, uint32_t* errors);
 /* Back-face culling in score-many (default on).  Applies only to meshes the
  * upload found closed (every directed edge matched by its reverse) and only
  * to hypotheses with no vertex in front of z = near: a back face of a closed

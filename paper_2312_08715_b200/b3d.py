@@ -191,6 +191,7 @@ def lib() -> C.CDLL:
         "b3d_gpu_set_culling": ([vp, st], st),
         "b3d_gpu_set_score_peers": ([vp, vp, u32, u64, u64], st),
         "b3d_gpu_shard_barrier": ([vp, vp, u32, u32, u64], st),
+        "b3d_gpu_test_exchange_emulation": ([vp, u32, u32, C.c_int32, u64, vp], st),
         "b3d_gpu_enumerate_shard": ([vp, i32, vp, vp, vp, u64, C.POINTER(ShardExchange), vp, vp],
                                     st),
         "b3d_gpu_set_camera_scene": ([vp, vp, vp, u32], st),
@@ -696,6 +697,16 @@ class GpuContext:
         """b3d_gpu_shard_barrier over the ranks' signal pads."""
         arr = (C.c_uint64 * max(1, len(signal_ptrs)))(*[int(x) for x in signal_ptrs])
         _check(self._L.b3d_gpu_shard_barrier(self.h, arr, len(signal_ptrs), rank, epoch))
+
+    def exchange_emulation(self, n_ranks: int, rounds: int, double_buffered: bool = True,
+                           hold_ns: int = 50_000) -> int:
+        """b3d_gpu_test_exchange_emulation: the exchange protocol for n_ranks
+        ranks emulated in one cooperative launch; returns the stale reads."""
+        err = C.c_uint32()
+        _check(self._L.b3d_gpu_test_exchange_emulation(self.h, n_ranks, rounds,
+                                                       1 if double_buffered else 0, hold_ns,
+                                                       C.byref(err)))
+        return err.value
 
     def enumerate_shard(self, mesh: int, ex: "ShardExchange", poses=None, grid=None, depth=None,
                         n_local: int = None, rng_state=None, out=None):

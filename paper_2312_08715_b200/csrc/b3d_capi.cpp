@@ -55,6 +55,10 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
                                int* count, cudaStream_t st);
 cudaError_t launch_exact_score(const KExactArgs& a, int ctas, cudaStream_t st);
 cudaError_t launch_shard_barrier(const KBarrier& b, cudaStream_t st);
+cudaError_t launch_exchange_emulation(unsigned long long* sig, double* arr, int n_ranks,
+                                      int rounds, int double_buffered,
+                                      unsigned long long hold_ns, unsigned int* errors,
+                                      cudaStream_t st);
 cudaError_t launch_copy_to_peers(const double* src, long long n_elems, double* const* peers,
                                  int n_peers, long long offset, long long cap, cudaStream_t st);
 cudaError_t launch_fill_column(double* s, long long n, int ld, int col, double v, cudaStream_t st);
@@ -1639,6 +1643,30 @@ b3d_status b3d_gpu_shard_barrier(b3d_gpu_context* ctx, const uint64_t* signal_pt
     b.rank = (int)rank;
     b.epoch = epoch;
     cuda_check(launch_shard_barrier(b, ctx->stream), "shard barrier launch");
+  });
+}
+
+b3d_status b3d_gpu_test_exchange_emulation(b3d_gpu_context* ctx, uint32_t n_ranks,
+                                           uint32_t rounds, int32_t double_buffered,
+                                           uint64_t hold_ns, uint32_t* errors) {
+  return guarded([&] {
+    check(ctx && errors && n_ranks >= 1 && n_ranks <= 8 && rounds >= 1, "bad arguments");
+    check(hold_ns <= 100000000ull, "exchange emulation: hold at most 0.1 s");
+    DeviceGuard dg(ctx->device);
+    DevBuf sig, arr, err;
+    sig.ensure(8 * 64);
+    arr.ensure(8 * 8 * 2 * 8);
+    err.ensure(4);
+    cuda_check(cudaMemsetAsync(sig.p, 0, 8 * 64, ctx->stream), "cudaMemsetAsync");
+    cuda_check(cudaMemsetAsync(arr.p, 0xff, 8 * 8 * 2 * 8, ctx->stream), "cudaMemsetAsync");
+    cuda_check(cudaMemsetAsync(err.p, 0, 4, ctx->stream), "cudaMemsetAsync");
+    cuda_check(launch_exchange_emulation(sig.as<unsigned long long>(), arr.as<double>(),
+                                         (int)n_ranks, (int)rounds, double_buffered ? 1 : 0,
+                                         hold_ns, err.as<unsigned int>(), ctx->stream),
+               "exchange emulation launch");
+    cuda_check(cudaMemcpyAsync(errors, err.p, 4, cudaMemcpyDeviceToHost, ctx->stream),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(ctx->stream), "exchange emulation");
   });
 }
 

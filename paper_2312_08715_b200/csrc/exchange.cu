@@ -34,8 +34,10 @@ __device__ __forceinline__ unsigned long long global_ns() {
   return t;
 }
 
-__global__ void shard_barrier_kernel(KBarrier b) {
-  const int t = threadIdx.x;
+// One rank's barrier episode: announce `epoch` in slot `rank` of every pad,
+// then wait (thread t) until slot t of this rank's pad holds it.
+__device__ __forceinline__ void barrier_episode(const KBarrier& b, int t,
+                                                unsigned long long timeout_ns) {
   __threadfence_system();
   if (t < b.n_ranks) st_release_sys(b.sig[t] + b.rank, b.epoch);
   if (t < b.n_ranks) {
@@ -43,10 +45,50 @@ __global__ void shard_barrier_kernel(KBarrier b) {
     const unsigned long long t0 = global_ns();
     while (ld_acquire_sys(mine) < b.epoch) {
       __nanosleep(64);
-      if (global_ns() - t0 > 20000000000ull) __trap();
+      if (global_ns() - t0 > timeout_ns) __trap();
     }
   }
   __syncwarp();
+}
+
+__global__ void shard_barrier_kernel(KBarrier b) {
+  barrier_episode(b, threadIdx.x, 20000000000ull);
+}
+
+// The exchange protocol with every rank emulated by one block of one
+// cooperative launch (ranks that wait on one another must run concurrently;
+// separate launches on one GPU give no such guarantee).  Epoch e: rank r
+// stores e * 16 + r into slot r of every rank's array -- half e & 1 when
+// double-buffered, else half 0 -- as the score kernel's remote stores do,
+// meets the others at the barrier, then reads its own half twice; one rank
+// per epoch holds `hold_ns` between the reads (a slow reduction).  A value
+// that is not epoch e's is a peer's next-epoch store that landed early.
+__global__ void exchange_emulation_kernel(unsigned long long* sig, double* arr, int n_ranks,
+                                          int rounds, int double_buffered,
+                                          unsigned long long hold_ns, unsigned int* errors) {
+  const int r = blockIdx.x, t = threadIdx.x;
+  KBarrier b{};
+  for (int q = 0; q < n_ranks; ++q) b.sig[q] = sig + 8 * q;
+  b.n_ranks = n_ranks;
+  b.rank = r;
+  for (int e = 1; e <= rounds; ++e) {
+    const int half = double_buffered ? (e & 1) : 0;
+    if (t < n_ranks) arr[(t * 2 + half) * 8 + r] = (double)(e * 16 + r);
+    b.epoch = (unsigned long long)e;
+    barrier_episode(b, t, 2000000000ull);
+    unsigned int bad = 0;
+    if (t < n_ranks) {
+      const volatile double* mine = arr + (r * 2 + half) * 8;
+      const double want = (double)(e * 16 + t);
+      bad += mine[t] != want;
+      const unsigned long long t0 = global_ns();
+      const unsigned long long hold = r == e % n_ranks ? hold_ns : 0ull;
+      while (global_ns() - t0 < hold) __nanosleep(128);
+      bad += mine[t] != want;
+    }
+    if (bad) atomicAdd(errors, bad);
+    __syncwarp();
+  }
 }
 
 // scores computed off the fused path (chunked / fp64 launches) stored to the
@@ -79,6 +121,15 @@ cudaError_t launch_copy_to_peers(const double* src, long long n, double* const* 
 cudaError_t launch_shard_barrier(const KBarrier& b, cudaStream_t st) {
   shard_barrier_kernel<<<1, 32, 0, st>>>(b);
   return cudaGetLastError();
+}
+
+cudaError_t launch_exchange_emulation(unsigned long long* sig, double* arr, int n_ranks,
+                                      int rounds, int double_buffered,
+                                      unsigned long long hold_ns, unsigned int* errors,
+                                      cudaStream_t st) {
+  void* args[] = {&sig, &arr, &n_ranks, &rounds, &double_buffered, &hold_ns, &errors};
+  return cudaLaunchCooperativeKernel(reinterpret_cast<const void*>(exchange_emulation_kernel),
+                                     dim3(n_ranks), dim3(32), args, 0, st);
 }
 
 }  // namespace b3d200

@@ -169,3 +169,17 @@ def test_enumerate_observed_graph_replay_tracks_inputs(gpu_ctx):
         if it == 3:  # a setter in between: the next call recaptures
             gpu_ctx.set_likelihood([(0.02, 0.006)], w.sigma_max, 2)
     gpu_ctx.set_likelihood(w.noise, w.sigma_max, w.window)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_ranks", [2, 3, 4, 8])
+def test_exchange_protocol_emulated_ranks(gpu_ctx, n_ranks):
+    """The exchange protocol for 2-8 ranks, every rank one block of one
+    cooperative launch on this GPU (the recipe's stand-in for more GPUs):
+    stores into every rank's array half, signal-pad barrier with growing
+    epochs, own-half reads with one slow reader per epoch.  Double-buffered
+    (the product's layout): no reader ever sees a peer's next-epoch value.
+    Single-buffered (control): the slow reader does -- the race the halves
+    remove, so the test can see it."""
+    assert gpu_ctx.exchange_emulation(n_ranks, 200, double_buffered=True, hold_ns=20_000) == 0
+    assert gpu_ctx.exchange_emulation(n_ranks, 50, double_buffered=False, hold_ns=50_000) > 0
