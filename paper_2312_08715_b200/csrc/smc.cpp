@@ -19,6 +19,7 @@
 // DESIGN.md 5.1); everything else is the reference's arithmetic.
 #include <algorithm>
 #include <sched.h>
+#include <unistd.h>
 
 #include <atomic>
 #include <condition_variable>
@@ -71,7 +72,8 @@ class Pool {
     static Pool p;
     return p;
   }
-  size_t threads() const { return workers_.size() + 1; }
+  // a forked child has none of the workers: it runs serially
+  size_t threads() const { return getpid() == pid_ ? workers_.size() + 1 : 1; }
   static bool& in_pool() {  // a parallel_for inside a job runs serially
     thread_local bool f = false;
     return f;
@@ -104,7 +106,7 @@ class Pool {
   }
 
  private:
-  Pool() {
+  Pool() : pid_(getpid()) {
     size_t hw = std::max(1u, std::thread::hardware_concurrency());
     cpu_set_t set;
     if (sched_getaffinity(0, sizeof set, &set) == 0) hw = std::max(1, CPU_COUNT(&set));
@@ -136,6 +138,7 @@ class Pool {
       if (--busy_ == 0) done_.notify_one();
     }
   }
+  const pid_t pid_;
   std::vector<std::thread> workers_;
   std::mutex mu_, run_mu_;
   std::condition_variable cv_, done_;
