@@ -32,6 +32,20 @@ elif leg == "coarse_to_fine":
     out = bench.run_coarse_to_fine(ctx, b3d, configs, render_fn)
 elif leg == "smc":
     out = bench.run_smc_leg(ctx, b3d, configs)
+elif leg == "cfg1":  # the headline batch: five score launches of configs[0]
+    w = configs.cfg1(render_fn, b3d.voxel_to_mesh, seed=0)
+    ctx.set_camera(b3d.Intrinsics(*w.k.as_tuple()))
+    mid = ctx.upload_mesh(w.vertices, w.triangles)
+    ctx.set_likelihood(w.noise, w.sigma_max, w.window)
+    ctx.set_observation(torch.from_numpy(w.observed).cuda())
+    grid = ctx.make_grid(w.center, w.extent, w.count, torch.from_numpy(w.rotations).cuda(),
+                         w.grid_mode)
+    sc = torch.zeros((1024, 1), dtype=torch.float64, device="cuda")
+    st = torch.zeros(1024, dtype=torch.uint8, device="cuda")
+    for _ in range(5):
+        ctx.score_grid(mid, grid, sc, st)
+    torch.cuda.synchronize()
+    out = {"scores_sum": float(sc.sum())}
 elif leg == "tracking":
     out = bench.run_tracking(ctx, b3d, configs, 40, render_fn)
 else:
