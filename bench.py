@@ -82,11 +82,42 @@ def _max_rel(got, want) -> float:
 LEG_CPU = {"enabled": True, "seconds": 4.0, "fp64_peak": None}
 
 
+def cpu_scorer(threads):
+    """The CPU implementation the baselines time: the reference's own code --
+    oracle/_ref/libb3d_ref.so, the reference's sources compiled unmodified
+    (render_instances / raster_mesh / ObservationCache / windowed likelihood
+    under its own parallel_for) -- when it is present (kind "reference"),
+    else the oracle port of the same algorithm (kind "port").  Both give the
+    same scores bit for bit (tests/test_ref_golden.py)."""
+    try:
+        from oracle import pyref as R
+        have_ref = os.path.exists(R.LIB)
+    except Exception:  # pragma: no cover
+        have_ref = False
+    if have_ref:
+        def ref(k, obs, v, t, poses, noise, smax, window, base=None, camera=None):
+            return R.score_poses(k, obs, v, t, poses, noise, smax, window, threads=threads,
+                                 camera=camera, base=base or ())[0]
+        return "reference", ref
+    from oracle import pyoracle as O
+    rendered = {}
+
+    def port(k, obs, v, t, poses, noise, smax, window, base=None, camera=None):
+        bd = None
+        if base:
+            if id(base) not in rendered:
+                rendered[id(base)] = O.render(k, base, camera=camera)
+            bd = rendered[id(base)]
+        return O.score_poses(k, obs, v, t, poses, noise, smax, window, base_depth=bd,
+                             camera=camera, threads=threads)[0]
+    return "port", port
+
+
 def leg_cpu_and_roofline(k, observed, verts, tris, poses, noise, sigma_max, window, gpu_value,
                          base=None, camera=None, what=""):
-    """A leg's CPU baseline -- the oracle port of the reference algorithm on
-    all host threads, timed on a bounded sample of the leg's own hypotheses
-    (about LEG_CPU seconds) -- and its roofline: the oracle's exact
+    """A leg's CPU baseline -- the reference's own code (or the oracle port,
+    cpu_scorer) on all host threads, timed on a bounded sample of the leg's
+    own hypotheses (about LEG_CPU seconds) -- and its roofline: the oracle's exact
     algorithmic op count per hypothesis times the leg's
     measured device rate, against the in-run non-FMA FP64 peak."""
     if not LEG_CPU["enabled"]:
@@ -111,17 +142,18 @@ def leg_cpu_and_roofline(k, observed, verts, tris, poses, noise, sigma_max, wind
         _, _, cnt = O.score_poses(k, observed, verts, tris, poses[:m], noise, sigma_max, window,
                                   counters=True, **kw)
     ops = _ops_per_hyp(cnt, n_sigma, len(noise), m)
+    kind, score = cpu_scorer(threads)
     done, t0, chunk = 0, time.perf_counter(), 16 * threads
     while True:
         i0 = done % poses.shape[0]
         sel = poses[i0:i0 + chunk]
-        O.score_poses(k, observed, verts, tris, sel, noise, sigma_max, window, **kw)
+        score(k, observed, verts, tris, sel, noise, sigma_max, window, base=base, camera=camera)
         done += sel.shape[0]
         el = time.perf_counter() - t0
         if el >= LEG_CPU["seconds"]:
             break
         chunk = min(4 * chunk, max(threads, int(done / el * (LEG_CPU["seconds"] - el)) + 1))
-    cpu = {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
+    cpu = {"value": done / el, "unit": UNIT, "cores": threads, "kind": kind,
            "sample": f"{done} of the leg's hypotheses{what}, {el:.1f} s"}
     roof = None
     if LEG_CPU["fp64_peak"]:
@@ -212,26 +244,27 @@ def build_workload_oracle(seed=0, shard=0):
 
 
 def cpu_baseline(w, seconds=12.0, threads=None, counters=True):
-    """The oracle port (the reference's algorithm, scalar fp64) timed on this
-    host's cores over repeated passes of the 1,024-hypothesis batch."""
+    """The reference's own code (cpu_scorer: oracle/_ref, else the oracle
+    port) timed on this host's cores over repeated passes of the
+    1,024-hypothesis batch; the oracle's op counters from one untimed pass."""
     from oracle import pyoracle as O
     threads = threads or cpu_threads()
     poses = w.grid_poses()
-    done, t0, cnt = 0, time.perf_counter(), None
+    cnt = None
+    if counters:
+        _, _, cnt = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
+                                  w.sigma_max, w.window, threads=threads, counters=True)
+    kind, score = cpu_scorer(threads)
+    done, t0 = 0, time.perf_counter()
     scores = None
     while True:
-        if counters and cnt is None:
-            scores, _, cnt = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses,
-                                           w.noise, w.sigma_max, w.window, threads=threads,
-                                           counters=True)
-        else:
-            scores, _ = O.score_poses(w.k, w.observed, w.vertices, w.triangles, poses, w.noise,
-                                      w.sigma_max, w.window, threads=threads)
+        scores = score(w.k, w.observed, w.vertices, w.triangles, poses, w.noise, w.sigma_max,
+                       w.window)
         done += poses.shape[0]
         el = time.perf_counter() - t0
         if el >= seconds or done >= 64 * poses.shape[0]:
             break
-    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": "port",
+    return {"value": done / el, "unit": UNIT, "cores": threads, "kind": kind,
             "sample": f"{done} hypotheses ({done // poses.shape[0]} passes of the cfg1 batch), "
                       f"{el:.1f} s"}, cnt, scores
 
@@ -251,20 +284,23 @@ DTYPE_NOTE = ("pose math and raster in fp64 without FMA (bitwise the reference's
 
 
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm (oracle port) on host cores,
-    all threads, over the same workload as our arm at this rank count (one
-    1,024-hypothesis batch per GPU-rank per step).  Rank 0 alone runs."""
+    """--impl reference: the reference's own code (cpu_scorer: oracle/_ref,
+    compiled unmodified from the reference sources; the oracle port if it is
+    absent) on host cores, all threads, over the same workload as our arm at
+    this rank count (one 1,024-hypothesis batch per GPU-rank per step); the
+    stage's normalisation / argmax / draw by the oracle.  Rank 0 alone runs."""
     if rank != 0:
         return
     from oracle import pyoracle as O
     threads = cpu_threads()
+    kind, score = cpu_scorer(threads)
     batches = [build_workload_oracle(shard=r) for r in range(world)]
     w = batches[0]
 
     def step():
         for b in batches:
-            s, _ = O.score_poses(b.k, b.observed, b.vertices, b.triangles, b.grid_poses(),
-                                 b.noise, b.sigma_max, b.window, threads=threads)
+            s = score(b.k, b.observed, b.vertices, b.triangles, b.grid_poses(), b.noise,
+                      b.sigma_max, b.window)
         probs, _ = O.normalize(s[:, 0])
         O.argmax(s[:, 0])
         O.sample_categorical(probs, O.rng_seed(7))
@@ -278,11 +314,12 @@ def run_reference(args, rank, world):
     v = args.steps * BATCH * world / el
     line = {"metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * el / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": DTYPE,
-            "dtype_note": "the oracle port computes everything in fp64",
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "dtype_note": ("the reference's own code" if kind == "reference" else
+                           "the oracle port") + " computes everything in fp64",
             "data": "synthetic (seeded 1,000-voxel Eden blob, noisy rendered observation)",
             "impl": "reference", "config": bench_config(world, w),
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": "port",
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": threads, "kind": kind,
                              "sample": f"{args.steps} steps x {world} x {BATCH} hypotheses "
                                        "(the full per-step workload)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

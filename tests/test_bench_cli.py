@@ -17,7 +17,10 @@ def test_reference_arm_prints_one_json_line():
     for key in ("metric", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
                 "cpu_baseline", "e2e", "config"):
         assert key in line
-    assert line["e2e"]["h2d_bytes_per_step"] == 0 and line["cpu_baseline"]["kind"] == "port"
+    # the reference's own code when oracle/_ref was built here, else the port
+    ref_built = os.path.exists(os.path.join(ROOT, "oracle", "_ref", "libb3d_ref.so"))
+    assert line["e2e"]["h2d_bytes_per_step"] == 0
+    assert line["cpu_baseline"]["kind"] == ("reference" if ref_built else "port")
 
 
 def test_gpus_flag_launches_that_many_ranks():
