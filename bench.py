@@ -499,6 +499,32 @@ def run_smc_leg(ctx, b3d, configs, n_particles=1000, seed=0):
     renders = n_stage0 + n_particles * (2 * 125 + 1)
     best = max(ps, key=lambda p: p[3])
     c = best[0][0]
+    cpu = None
+    if LEG_CPU["enabled"]:
+        # the reference's own render+score (cpu_scorer) on a bounded sample of
+        # the inference's stage-0 hypotheses (object 2 = the true one, face 1,
+        # all 9 noise entries, over the table): its render+score rate and the
+        # run_smc time it implies for the workload's 275,000 renders
+        threads = cpu_threads()
+        kind, score = cpu_scorer(threads)
+        cg = b3d.ContactGrid.make(tw, th, lib[2][2], lib[2][3], 1, (10, 10, 8))
+        cells = b3d.contact_grid_poses(cg)
+        table_inst = [(tv, tt, np.array([1.0, 0, 0, 0, 0, 0, 0]))]
+        done, t0, chunk = 0, time.perf_counter(), threads
+        while True:
+            sel = cells[done % cells.shape[0]:done % cells.shape[0] + chunk]
+            score(k, obs, lib[2][0], lib[2][1], sel, noise, 0.1, 2, base=table_inst,
+                  camera=camera)
+            done += sel.shape[0]
+            el = time.perf_counter() - t0
+            if el >= LEG_CPU["seconds"]:
+                break
+            chunk = min(4 * chunk, max(threads, int(done / el * (LEG_CPU["seconds"] - el)) + 1))
+        rate = done / el
+        cpu = {"value": rate, "unit": "renders/s", "cores": threads, "kind": kind,
+               "sample": f"{done} stage-0 hypotheses (true object, face 1, 9 noise entries, "
+                         f"table base), {el:.1f} s",
+               "seconds_for_the_workload_est": renders / rate}
     return {"workload": "run_smc harness defaults: 5-object library, 240x320, stage 0 "
                         "10x10x8 x faces x 9 noise, 2 x 5x5x5 refine, 1,000 particles, "
                         "1 object; all render+score on device",
@@ -512,7 +538,7 @@ def run_smc_leg(ctx, b3d, configs, n_particles=1000, seed=0):
             "log_evidence": le,
             "map_child": list(c), "truth": list(truth),
             "map_position_error_cm": 100.0 * float(np.hypot(c[2] - truth[2], c[3] - truth[3])),
-            "map_object_correct": bool(c[0] == truth[0])}
+            "map_object_correct": bool(c[0] == truth[0]), "cpu_baseline": cpu}
 
 
 def run_coarse_to_fine(ctx, b3d, configs, render_fn, reps=5):
