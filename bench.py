@@ -1045,6 +1045,12 @@ def main():
                     "traffic_unit": "DRAM bytes per launch (ncu --set full)",
                     "traffic_source": (_ncu_traffic() or {}).get("source"),
                     "ops_per_hypothesis": ops,
+                    # transcendentals reported separately
+                    "transcendentals_per_hypothesis": {
+                        "exp": cnt["pairs"] * 1 / BATCH, "log": cnt["obs_valid"] * 1 / BATCH},
+                    "counts_per_hypothesis": {k: cnt[k] / BATCH for k in (
+                        "vertices", "triangles", "bbox_px", "fragments", "rend_valid", "pairs",
+                        "obs_valid") if k in cnt},
                     "kernel_ms": kern_avg * 1e3,
                     "peak_source": "measured in-run (non-FMA DMUL/DADD microbenchmark)"}
         line = {
