@@ -69,8 +69,10 @@ void need(bool c, b3d_status s, const char* m) {
 class Pool {
  public:
   static Pool& get() {
-    static Pool p;
-    return p;
+    // never destroyed: the workers block on a condition variable until the
+    // process ends (no join at exit, none attempted in a forked child)
+    static Pool* p = new Pool;
+    return *p;
   }
   // a forked child has none of the workers: it runs serially
   size_t threads() const { return getpid() == pid_ ? workers_.size() + 1 : 1; }
@@ -96,14 +98,6 @@ class Pool {
     job_ = nullptr;
     if (err_) std::rethrow_exception(err_);
   }
-  ~Pool() {
-    {
-      std::lock_guard<std::mutex> g(mu_);
-      stop_ = true;
-    }
-    cv_.notify_all();
-    for (auto& t : workers_) t.join();
-  }
 
  private:
   Pool() : pid_(getpid()) {
@@ -111,7 +105,7 @@ class Pool {
     cpu_set_t set;
     if (sched_getaffinity(0, sizeof set, &set) == 0) hw = std::max(1, CPU_COUNT(&set));
     for (size_t t = 1; t < std::min<size_t>(hw, 64); ++t)
-      workers_.emplace_back([this] { loop(); });
+      workers_.emplace_back([this] { loop(); }).detach();
   }
   void work() {
     in_pool() = true;
@@ -129,8 +123,7 @@ class Pool {
     for (;;) {
       {
         std::unique_lock<std::mutex> g(mu_);
-        cv_.wait(g, [&] { return stop_ || gen_ != seen; });
-        if (stop_) return;
+        cv_.wait(g, [&] { return gen_ != seen; });
         seen = gen_;
       }
       work();
@@ -147,7 +140,6 @@ class Pool {
   std::atomic<size_t> next_{0};
   std::exception_ptr err_;
   uint64_t gen_ = 0;
-  bool stop_ = false;
 };
 
 template <class F>
