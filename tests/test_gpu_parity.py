@@ -1108,3 +1108,46 @@ def test_cfg2_full_size_chain_spot_parity_and_determinism(gpu_ctx, oracle):
                                       [g["noise"]], w.sigma_max, g["window"])
         assert rel_err(s_gpu[idx, 0], s_orc[:, 0]).max() <= SCORE_RTOL
     np.testing.assert_array_equal(st, st_o)
+
+
+def test_c_abi_is_thread_safe_like_the_reference():
+    """The reference's C ABI is pure host code, callable from many threads at
+    once (thread-local error, no shared state).  Here every thread gets its
+    own device context: b3d_render and b3d_log_likelihood called from 8
+    threads at once (ctypes releases the GIL) give exactly the serial results."""
+    import json
+    import threading
+    vox = synth.eden_blob(400, 5)
+    m0 = b3d.Model.from_voxels(vox, 0.005, np.zeros(3), 0)
+    lib = b3d.Library.create([m0])
+    k = configs.Intr(200.0, 200.0, 79.5, 59.5, 160, 120, 0.05, 5.0)
+    intr = b3d_intr(k)
+    cams = [np.array([0.0, 1.0, 0.0, 0.0, 0.02 * i, 0.01 * i, 0.8]) for i in range(8)]
+    scenes = [b3d.Scene.from_json(json.dumps({"table": {"width": 0.5, "height": 0.4},
+                                              "children": [dict(object_id=0, face=1 + i % 6,
+                                                                dx=0.05 + 0.03 * i, dy=0.1,
+                                                                dtheta=0.4 * i)]}), lib)
+              for i in range(8)]
+    serial = [b3d.render(scenes[i], cams[i], intr) for i in range(8)]
+    serial_ll = [b3d.log_likelihood(serial[i], serial[(i + 1) % 8], intr, 0.1, 0.01, 0.1, 2)
+                 for i in range(8)]
+    got, got_ll, errs = [None] * 8, [None] * 8, []
+
+    def work(i):
+        try:
+            for _ in range(5):
+                got[i] = b3d.render(scenes[i], cams[i], intr)
+                got_ll[i] = b3d.log_likelihood(got[i], serial[(i + 1) % 8], intr, 0.1, 0.01,
+                                               0.1, 2)
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    ts = [threading.Thread(target=work, args=(i,)) for i in range(8)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errs, errs
+    for i in range(8):
+        np.testing.assert_array_equal(got[i].view(np.uint32), serial[i].view(np.uint32))
+        assert got_ll[i] == serial_ll[i]
