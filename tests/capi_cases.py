@@ -51,6 +51,8 @@ def _sig(L):
     L.b3d_particles_log_evidence.argtypes = [vp, C.POINTER(C.c_double)]
     L.b3d_particles_to_jsonl.argtypes = [vp, C.POINTER(C.c_void_p)]
     L.b3d_string_free.argtypes = [vp]
+    L.b3d_particles_type_marginal.argtypes = [vp, C.POINTER(C.c_double), C.c_size_t]
+    L.b3d_particles_map_pose.argtypes = [vp, C.c_size_t, C.POINTER(Pose)]
     L.b3d_library_destroy.argtypes = [vp]
     L.b3d_scene_destroy.argtypes = [vp]
     L.b3d_particles_destroy.argtypes = [vp]
@@ -201,20 +203,36 @@ def run_cases(L, gpu: bool):
                "table": {"width": 0.4, "height": 0.4}, "n_objects": 10, "particles": 3,
                "schedule": {"stage0": [2, 2, 2], "refine": [[2, 1, 2]]},
                "noise_grid": {"p_outlier": [0.1], "sigma": [0.01]}}
-        part = vp()
-        st = L.b3d_infer(seen, C.byref(TOP), lib, json.dumps(cfg).encode(), 5, C.byref(part))
-        if st == 0:
+        marg = (C.c_double * 2)()
+        mp = Pose()
+        for name, n_obj in (("infer_ten_objects", 10), ("infer_one_object", 1)):
+            part = vp()
+            st = L.b3d_infer(seen, C.byref(TOP), lib, json.dumps(dict(cfg, n_objects=n_obj)).encode(),
+                             5, C.byref(part))
+            if st != 0:
+                out[name] = _res(L, st)
+                continue
             le, txt = C.c_double(), C.c_void_p()
             assert L.b3d_particles_log_evidence(part, C.byref(le)) == 0
             assert L.b3d_particles_to_jsonl(part, C.byref(txt)) == 0
             lines = C.string_at(txt).decode().splitlines()
             L.b3d_string_free(txt)
-            L.b3d_particles_destroy(part)
             ps = [[[c["object_id"], c["face"], c["dx"], c["dy"], c["dtheta"]]
                    for c in json.loads(ln)["children"]] for ln in lines]
-            out["infer_ten_objects"] = [0, {"log_evidence": le.value, "particles": ps}]
-        else:
-            out["infer_ten_objects"] = _res(L, st)
+            res = {"log_evidence": le.value, "particles": ps}
+            st = L.b3d_particles_type_marginal(part, marg, 2)
+            if st == 0:
+                res["marginal"] = list(marg)
+            else:
+                out[name + "_marginal"] = _res(L, st)
+            st = L.b3d_particles_map_pose(part, 0, C.byref(mp))
+            if st == 0:
+                res["map_pose"] = [getattr(mp, f) for f, _ in Pose._fields_]
+            out[name + "_map_pose_index"] = _res(L, L.b3d_particles_map_pose(part, n_obj,
+                                                                              C.byref(mp)))
+            out[name + "_marginal_small"] = _res(L, L.b3d_particles_type_marginal(part, marg, 1))
+            L.b3d_particles_destroy(part)
+            out[name] = [0, res]
         L.b3d_depth_image_destroy(seen)
     # b3d_infer config schema (b3d_capi.cpp:297-379)
     kk = {"fx": 60.0, "fy": 60.0, "cx": 31.5, "cy": 23.5, "width": 64, "height": 48,

@@ -8,7 +8,8 @@ The CPU test runs every case the product settles before touching a device
 (argument, intrinsics, noise, file-format, manifest, scene-JSON and `infer`
 schema errors); the GPU test runs all of them, including the empty-render
 checks, device-side `infer` validation, whole 3- and 20-child renders and
-an `infer` placing ten objects (draws equal, log evidence to 1e-6 relative).
+`infer` runs placing ten objects and one (draws equal, log evidence to 1e-6
+relative, type marginal and MAP pose, the accessors' errors).
 """
 import ctypes
 import json
@@ -42,6 +43,16 @@ def _same(a, b):
             return False
         ga, wa = a[1], b[1]
         if abs(ga["log_evidence"] - wa["log_evidence"]) > 1e-6 * abs(wa["log_evidence"]):
+            return False
+        if set(ga) != set(wa):
+            return False
+        # the marginal is a sum of exp(log weight - lse): a weight's absolute
+        # error (scores ~4e3 at ~3e-8 relative) moves it by ~1e-6 relative
+        if "marginal" in wa and not np.allclose(ga["marginal"], wa["marginal"], rtol=1e-4,
+                                                atol=1e-9):
+            return False
+        if "map_pose" in wa and not np.allclose(ga["map_pose"], wa["map_pose"], rtol=0,
+                                                atol=1e-12):
             return False
         return len(ga["particles"]) == len(wa["particles"]) and all(
             len(p) == len(q) and all(x[:2] == y[:2] and np.allclose(x[2:], y[2:], rtol=0,
