@@ -6,6 +6,7 @@
 // runs on the device through a per-thread GPU context (device
 // $B3D_DEVICE, default 0).
 #include <atomic>
+#include <climits>
 #include <cmath>
 #include <cstdlib>
 #include <tuple>
@@ -190,6 +191,34 @@ std::shared_ptr<b3d_object_model> load_svox(const std::string& path, int id) {  
 }
 
 // ConfigReader (config.cpp): strict object view, unknown keys are errors
+// nlohmann's number -> int / uint32_t conversions as the reference's build
+// performs them (static_cast under gcc on x86-64): integers wrap modulo
+// 2^32; a float truncates toward zero, out of range giving INT_MIN (int,
+// cvttsd2si) or 0 (uint32_t, through the 64-bit conversion).
+int json_int(const J::Value& x) {
+  if (x.kind == J::Value::Bool) return x.b ? 1 : 0;  // nlohmann converts booleans too
+  if (x.integral) {
+    if (x.num >= 9223372036854775808.0) return (int)(uint32_t)(uint64_t)x.num;
+    return (int)(uint32_t)(uint64_t)(int64_t)x.num;
+  }
+  return (x.num > -2147483649.0 && x.num < 2147483648.0) ? (int)x.num : INT_MIN;
+}
+uint32_t json_u32(const J::Value& x) {
+  if (x.kind == J::Value::Bool) return x.b ? 1u : 0u;
+  if (x.integral) {
+    if (x.num >= 9223372036854775808.0) return (uint32_t)(uint64_t)x.num;
+    return (uint32_t)(uint64_t)(int64_t)x.num;
+  }
+  return (x.num > -9223372036854775809.0 && x.num < 9223372036854775808.0)
+             ? (uint32_t)(uint64_t)(int64_t)x.num
+             : 0u;
+}
+
+// the JSON kinds nlohmann's get<int> / get<uint32_t> accept (its generic
+// arithmetic from_json converts booleans too); get<double> goes through
+// get_arithmetic_value, numbers only
+bool is_arith(const J::Value& x) { return x.kind == J::Value::Number || x.kind == J::Value::Bool; }
+
 struct Reader {
   const J::Value& v;
   std::string ctx;
@@ -204,22 +233,26 @@ struct Reader {
     require(x != nullptr, B3D_ERROR_CONFIG, ctx + ": missing required key '" + k + "'");
     return *x;
   }
-  double num(const std::string& k) {
+  double num(const std::string& k) {  // get<double>: numbers only
     const J::Value& x = raw(k);
     require(x.kind == J::Value::Number, B3D_ERROR_CONFIG,
             ctx + ": key '" + k + "' has the wrong type");
     return x.num;
   }
   double num_or(const std::string& k, double d) { return has(k) ? num(k) : (seen.insert(k), d); }
-  long long integer(const std::string& k) {
+  // get<int> / get<uint32_t> (config.hpp:21-27, 50-56): any JSON number
+  // converts (json_int / json_u32), anything else is the wrong type
+  int integer(const std::string& k) {
     const J::Value& x = raw(k);
-    require(x.kind == J::Value::Number && x.integral, B3D_ERROR_CONFIG,
-            ctx + ": key '" + k + "' has the wrong type");
-    return (long long)x.num;
+    require(is_arith(x), B3D_ERROR_CONFIG, ctx + ": key '" + k + "' has the wrong type");
+    return json_int(x);
   }
-  long long int_or(const std::string& k, long long d) {
-    return has(k) ? integer(k) : (seen.insert(k), d);
+  uint32_t u32(const std::string& k) {
+    const J::Value& x = raw(k);
+    require(is_arith(x), B3D_ERROR_CONFIG, ctx + ": key '" + k + "' has the wrong type");
+    return json_u32(x);
   }
+  int int_or(const std::string& k, int d) { return has(k) ? integer(k) : (seen.insert(k), d); }
   Reader object(const std::string& k) { return Reader(raw(k), ctx + "." + k); }
   void finish() const {
     for (const auto& kv : v.obj)
@@ -421,11 +454,19 @@ const J::Value& nl_at(const J::Value& o, const char* key) {
   if (!x) throw NlError(std::string("[json.exception.out_of_range.403] key '") + key + "' not found");
   return *x;
 }
-double nl_number(const J::Value& v) {
+double nl_number(const J::Value& v) {  // get<double>
   if (v.kind != J::Value::Number)
     throw NlError(std::string("[json.exception.type_error.302] type must be number, but is ") +
                   nl_type_name(v));
   return v.num;
+}
+// Json::get<int>() outside a ConfigReader (the schedule lambda,
+// b3d_capi.cpp:344-349): a non-number is nlohmann's own type_error
+int nl_get_int(const J::Value& v) {
+  if (!is_arith(v))
+    throw NlError(std::string("[json.exception.type_error.302] type must be number, but is ") +
+                  nl_type_name(v));
+  return json_int(v);
 }
 // range-for over a json value: array elements, object values, nothing for
 // null, the value itself for a primitive
@@ -464,7 +505,7 @@ b3d_status b3d_library_open(const char* manifest_path, b3d_library** out) {
       int id = 0;
       std::string rel;
       try {  // mj.at("id").get<int>(), mj.at("path").get<std::string>()
-        id = (int)nl_number(nl_at(m, "id"));
+        id = nl_get_int(nl_at(m, "id"));
         rel = nl_string(nl_at(m, "path"));
       } catch (const NlError& e) {
         throw Fail(B3D_ERROR_CONFIG, mp + ": bad model entry: " + e.what());
@@ -502,25 +543,24 @@ b3d_status b3d_scene_from_json(const char* json, const b3d_library* lib, b3d_sce
     const J::Value* t = j.is_object() ? j.find("table") : nullptr;
     require(t != nullptr, B3D_ERROR_CONFIG, "scene JSON: missing 'table'");
     auto s = std::make_unique<b3d_scene>();
-    try {  // the reference's order: thickness (value), width, height, then children
+    try {  // the reference's order: thickness (value), then the table() arguments
+           // right to left as its build (gcc) evaluates them, then children
       const J::Value* th = t->is_object() ? t->find("thickness") : nullptr;
       if (!t->is_object())
         throw NlError(std::string("[json.exception.type_error.306] cannot use value() with ") +
                       nl_type_name(*t));
       s->thickness = th ? nl_number(*th) : 0.01;
-      s->table_w = nl_number(nl_at(*t, "width"));
       s->table_h = nl_number(nl_at(*t, "height"));
+      s->table_w = nl_number(nl_at(*t, "width"));
       require(s->table_w > 0 && s->table_h > 0 && s->thickness > 0, B3D_ERROR,
               "table: extents must be positive");
-      if (const J::Value* ch = j.find("children")) {
-        if (!ch->is_array())
-          throw NlError(std::string("[json.exception.type_error.302] type must be array, but is ") +
-                        nl_type_name(*ch));
-        for (const J::Value& c : ch->arr) {
-          const int id = (int)nl_number(nl_at(c, "object_id"));
+      if (const J::Value* ch = j.find("children")) {  // j.value("children", [])
+        for (const J::Value* cp : nl_elems(*ch)) {
+          const J::Value& c = *cp;
+          const int id = nl_get_int(nl_at(c, "object_id"));
           require(id >= 0 && (size_t)id < lib->models.size(), B3D_ERROR_CONFIG,
                   "scene JSON: object_id out of library range");
-          const int face = (int)nl_number(nl_at(c, "face"));
+          const int face = nl_get_int(nl_at(c, "face"));
           const double dx = nl_number(nl_at(c, "dx"));
           const double dy = nl_number(nl_at(c, "dy"));
           const double dth = nl_number(nl_at(c, "dtheta"));
@@ -606,44 +646,46 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
       ik.fy = ir.num("fy");
       ik.cx = ir.num("cx");
       ik.cy = ir.num("cy");
-      ik.width = (uint32_t)ir.integer("width");
-      ik.height = (uint32_t)ir.integer("height");
+      ik.width = ir.u32("width");
+      ik.height = ir.u32("height");
       ik.near_m = ir.num("near");
       ik.far_m = ir.num("far");
       ir.finish();
+      b3d200_validate_intrinsics(ik);  // from_c (b3d_capi.cpp:54-65)
     }
     const double sigma_max = r.num_or("sigma_max", 0.1);
-    const long long window = r.int_or("window", 2);
+    const int window = r.int_or("window", 2);
     // window < 0: ModelConfig::windowed = false, the untruncated likelihood
     // (b3d_capi.cpp:328-330) -- scored on the device's fp64 image path
     double tw, th, thick;
     {
       Reader tr = r.object("table");
-      tw = tr.num("width");
-      th = tr.num("height");
+      // ObjectModel::table(get("width"), get("height"), get_or("thickness"))
+      // (b3d_capi.cpp:335-337): the reference's build (gcc) evaluates the
+      // arguments right to left, so a bad thickness is reported first
       thick = tr.num_or("thickness", 0.01);
-      tr.finish();
+      th = tr.num("height");
+      tw = tr.num("width");
+      // ObjectModel::table (scene_graph.cpp:26-28) runs before tr.finish()
       require(tw > 0 && th > 0 && thick > 0, B3D_ERROR, "table: extents must be positive");
+      tr.finish();
     }
     b3d_smc_config cfg{};
-    cfg.stage0 = {10, 10, 8};  // Schedule defaults (inference.hpp:30-31)
-    std::vector<b3d_schedule_stage> refine{{5, 5, 5}, {5, 5, 5}};
+    struct StageI {
+      int n_dx, n_dy, n_dtheta;
+    };
+    StageI stage0{10, 10, 8};  // Schedule defaults (inference.hpp:30-31)
+    std::vector<StageI> refine_i{{5, 5, 5}, {5, 5, 5}};
     if (r.has("schedule")) {
       Reader sr = r.object("schedule");
       auto stage = [](const J::Value& v) {
         require(v.is_array() && v.arr.size() == 3, B3D_ERROR_CONFIG,
                 "schedule stages must be [n_dx, n_dy, n_dtheta]");
-        for (const J::Value& x : v.arr)
-          require(x.kind == J::Value::Number && x.integral, B3D_ERROR_CONFIG,
-                  "schedule stages must be [n_dx, n_dy, n_dtheta]");
-        return b3d_schedule_stage{(uint32_t)v.arr[0].num, (uint32_t)v.arr[1].num,
-                                  (uint32_t)v.arr[2].num};
+        return StageI{nl_get_int(v.arr[0]), nl_get_int(v.arr[1]), nl_get_int(v.arr[2])};
       };
-      cfg.stage0 = stage(sr.raw("stage0"));
-      const J::Value& rf = sr.raw("refine");
-      require(rf.is_array(), B3D_ERROR_CONFIG, "schedule stages must be [n_dx, n_dy, n_dtheta]");
-      refine.clear();
-      for (const J::Value& v : rf.arr) refine.push_back(stage(v));
+      stage0 = stage(sr.raw("stage0"));
+      refine_i.clear();
+      for (const J::Value* v : nl_elems(sr.raw("refine"))) refine_i.push_back(stage(*v));
       sr.finish();
     }
     std::vector<b3d_noise> grid;  // default_noise_grid (inference.cpp:127-133)
@@ -659,13 +701,34 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
           grid.push_back({nl_number(*p), nl_number(*sv)});
       gr.finish();
     }
-    cfg.n_objects = (uint32_t)r.int_or("n_objects", 1);
-    cfg.n_particles = (uint32_t)r.int_or("particles", 1000);
+    const int n_objects = r.int_or("n_objects", 1);
+    const int n_particles = r.int_or("particles", 1000);
     cfg.resample_threshold = r.num_or("resample_threshold", 0.5);
     r.finish();
+    // make_inference_context (inference.cpp:140-157), then run_smc / smc_init
+    // (inference.cpp:495, 400): the reference's checks in its order, all
+    // before any device work
+    require(!lib->models.empty(), B3D_ERROR, "inference: empty library");
+    require(!grid.empty(), B3D_ERROR, "inference: empty noise grid");
+    auto valid = [](const StageI& st) { return st.n_dx >= 1 && st.n_dy >= 1 && st.n_dtheta >= 1; };
+    require(valid(stage0), B3D_ERROR, "schedule stage: subdivision counts must be >= 1");
+    for (const StageI& st : refine_i)
+      require(valid(st), B3D_ERROR, "schedule stage: subdivision counts must be >= 1");
+    for (const b3d_noise& np : grid)
+      require(np.p_outlier >= 0 && np.p_outlier <= 1 && np.sigma_noise > 0 &&
+                  np.sigma_noise <= sigma_max,
+              B3D_ERROR, "noise grid entry outside support");
     require(b3d_depth_image_width(observed) == ik.width &&
                 b3d_depth_image_height(observed) == ik.height,
             B3D_ERROR, "observation dimensions do not match intrinsics");
+    require(n_objects >= 1, B3D_ERROR, "run_smc: n_objects must be >= 1");
+    require(n_particles >= 1, B3D_ERROR, "smc_init: need at least one particle");
+    cfg.stage0 = {(uint32_t)stage0.n_dx, (uint32_t)stage0.n_dy, (uint32_t)stage0.n_dtheta};
+    std::vector<b3d_schedule_stage> refine;
+    for (const StageI& st : refine_i)
+      refine.push_back({(uint32_t)st.n_dx, (uint32_t)st.n_dy, (uint32_t)st.n_dtheta});
+    cfg.n_objects = (uint32_t)n_objects;
+    cfg.n_particles = (uint32_t)n_particles;
     const b3d_pose cam = normalized_pose(*camera);
     b3d_gpu_context* g = g_gpu.get();
     ok(b3d_gpu_set_camera(g, &ik, &cam));

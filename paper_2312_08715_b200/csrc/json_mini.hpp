@@ -1,10 +1,13 @@
 // json_mini.hpp -- a small strict JSON reader for the reference's
 // configuration objects (b3d_scene_from_json, b3d_infer config, library
 // manifests) and a compact writer; the reference uses nlohmann::json, which
-// this image does not ship.  Numbers are parsed with strtod (round-trip
-// exact for the %.17g the writer emits); object keys keep their order.
+// this image does not ship.  Numbers are parsed with strtod and written as
+// nlohmann's dump writes them (shortest round-trip digits); object keys keep
+// their order.
 #pragma once
 
+#include <charconv>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <map>
@@ -160,10 +163,38 @@ class Parser {
 
 inline Value parse(const std::string& s) { return Parser(s).parse(); }
 
+// A double as nlohmann::json::dump writes it: the shortest digits that read
+// back to the same value (std::to_chars; nlohmann's Grisu2 agrees except in
+// rare cases where Grisu2 is one digit longer), fixed notation for decimal
+// exponents in (-4, 15] with ".0" on integral values, else d.ddde+XX;
+// "null" for non-finite values.
 inline std::string num(double x) {
-  char buf[32];
-  std::snprintf(buf, sizeof buf, "%.17g", x);
-  return buf;
+  if (!std::isfinite(x)) return "null";
+  std::string out = std::signbit(x) ? "-" : "";
+  if (x == 0) return out + "0.0";
+  char buf[64];
+  const auto r = std::to_chars(buf, buf + sizeof buf, std::fabs(x), std::chars_format::scientific);
+  const std::string s(buf, r.ptr);  // d[.ddd]e(+|-)XX
+  const size_t epos = s.find('e');
+  std::string digits = s.substr(0, 1) + (epos > 2 ? s.substr(2, epos - 2) : std::string());
+  const int k = (int)digits.size();
+  const int n = std::atoi(s.c_str() + epos + 1) + 1;  // digits before the decimal point
+  if (k <= n && n <= 15) {
+    out += digits + std::string(n - k, '0') + ".0";
+  } else if (0 < n && n <= 15) {
+    out += digits.substr(0, n) + "." + digits.substr(n);
+  } else if (-4 < n && n <= 0) {
+    out += "0." + std::string(-n, '0') + digits;
+  } else {
+    out += digits.substr(0, 1);
+    if (k > 1) out += "." + digits.substr(1);
+    const int e = n - 1;
+    out += e < 0 ? "e-" : "e+";
+    const int ae = e < 0 ? -e : e;
+    if (ae < 10) out += '0';
+    out += std::to_string(ae);
+  }
+  return out;
 }
 inline std::string quote(const std::string& s) {
   std::string o = "\"";

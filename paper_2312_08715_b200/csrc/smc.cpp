@@ -312,6 +312,12 @@ struct Smc {
     base_key = key;
     base_valid = true;
   }
+  // an empty render: the windowed likelihood throws (likelihood.cpp:159-160)
+  // and with it the whole inference; the untruncated one scores it -inf
+  // (observation_loglik_cached, inference.cpp:52-54)
+  void empty_render() const {
+    if (cfg.window >= 0) throw Fail(B3D_ERROR, "windowed likelihood: empty rendered cloud");
+  }
   void set_noise(const b3d_noise* nz, uint32_t n) {
     ok(b3d_gpu_set_likelihood(g, nz, n, cfg.sigma_max, cfg.window, cfg.prefactor));
   }
@@ -447,6 +453,8 @@ struct Smc {
                              s0_st.data()));
       prof("s0 device");
       renders += np;
+      for (size_t j = 0; j < np; ++j)
+        if (s0_st[j]) empty_render();
       if (t.lt.size() < total) t.lt.resize(total);
       parallel_for(np, [&](size_t j) {
         for (size_t e = 0; e < nn; ++e) {
@@ -499,7 +507,10 @@ struct Smc {
     ok(b3d_gpu_score_poses(g, lib[obj].mesh_id, poses.data(), poses.size(), s.data(),
                            st.data()));
     for (size_t i = 0; i < s.size(); ++i)
-      if (st[i]) s[i] = kNegInf;
+      if (st[i]) {
+        empty_render();
+        s[i] = kNegInf;
+      }
     return s;
   }
 

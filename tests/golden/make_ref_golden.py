@@ -372,9 +372,32 @@ def sec_capi():
 
 
 
+def sec_fuzz():
+    """The reference's b3d_infer on 240 seeded random configurations and its
+    b3d_scene_from_json / b3d_scene_to_json on 200 random scene documents
+    (tests/infer_fuzz.py): status + message, or the result."""
+    import json
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    import infer_fuzz
+    texts = infer_fuzz.configs()
+    res = infer_fuzz.run(R.lib(), texts, True)
+    path = os.path.join(HERE, "ref_infer_fuzz.json")
+    with open(path, "w") as f:
+        json.dump([{"config": t, "result": r} for t, r in zip(texts, res)], f, indent=0)
+    ok = sum(1 for r in res if r[0] == 0)
+    print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases, {ok} valid)")
+    scenes = infer_fuzz.scene_texts()
+    res = infer_fuzz.run_scenes(R.lib(), scenes)
+    path = os.path.join(HERE, "ref_scene_fuzz.json")
+    with open(path, "w") as f:
+        json.dump([{"scene": t, "result": r} for t, r in zip(scenes, res)], f, indent=0)
+    print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
+
+
 SECTIONS = {"pose": sec_pose, "mesh": sec_mesh, "render": sec_render, "score_cfg1": sec_score_cfg1,
             "smc": sec_smc, "track": sec_track, "cfg2": sec_cfg2, "cfg3": sec_cfg3,
-            "cfg5": sec_cfg5, "cfg4": sec_cfg4, "capi": sec_capi}
+            "cfg5": sec_cfg5, "cfg4": sec_cfg4, "capi": sec_capi,
+            "fuzz": sec_fuzz}
 
 
 def main(argv):

@@ -80,3 +80,53 @@ def test_capi_errors_and_renders_match_reference_gpu():
     got = capi_cases.run_cases(_lib(), gpu=True)
     assert set(got) == set(want)
     _compare(got, want)
+
+
+def _fuzz():
+    with open(os.path.join(HERE, "golden", "ref_infer_fuzz.json")) as f:
+        return json.load(f)
+
+
+def _device_error(res):
+    return res[0] != 0 and "cuda" in res[1].lower()
+
+
+def test_infer_config_fuzz_cpu():
+    """240 seeded random b3d_infer configurations (tests/infer_fuzz.py): every
+    one the product settles on the host -- JSON and schema errors, nlohmann's
+    number conversions (booleans and floats into integers, wrapping, gcc's
+    right-to-left argument order), make_inference_context / run_smc checks
+    in the reference's order -- gives the reference's status and text."""
+    import infer_fuzz
+    cases = _fuzz()
+    got = infer_fuzz.run(_lib(), [c["config"] for c in cases], False)
+    compared = 0
+    for c, g in zip(cases, got):
+        if _device_error(g):
+            continue  # needs the device: the GPU test covers it
+        compared += 1
+        assert _same(g, c["result"]), (c["config"], g, c["result"])
+    assert compared >= 200
+
+
+@pytest.mark.gpu
+def test_infer_config_fuzz_gpu():
+    """All 240, including the valid ones (particles and evidence) and the
+    errors the inference itself raises (empty renders, all-zero stage 0)."""
+    import infer_fuzz
+    cases = _fuzz()
+    got = infer_fuzz.run(_lib(), [c["config"] for c in cases], True)
+    for c, g in zip(cases, got):
+        assert _same(g, c["result"]), (c["config"], g, c["result"])
+
+
+def test_scene_json_fuzz():
+    """200 seeded random scene documents through b3d_scene_from_json and back
+    through b3d_scene_to_json: the reference's status and message, or its
+    exact output text (nlohmann's number format)."""
+    import infer_fuzz
+    with open(os.path.join(HERE, "golden", "ref_scene_fuzz.json")) as f:
+        cases = json.load(f)
+    got = infer_fuzz.run_scenes(_lib(), [c["scene"] for c in cases])
+    for c, g in zip(cases, got):
+        assert g == c["result"], (c["scene"], g, c["result"])
