@@ -1493,6 +1493,19 @@ b3d_status b3d_depth_image_create(uint32_t width, uint32_t height, const float* 
   });
 }
 
+// load_depth_image (io.cpp:104-116) builds the image without
+// b3d_depth_image_create's argument checks: a 0 x N file loads (handle layer)
+}  // extern "C"
+b3d_depth_image* b3d200_depth_image_new(uint32_t width, uint32_t height,
+                                        std::vector<float>&& depth) {
+  auto h = std::make_unique<b3d_depth_image>();
+  h->width = width;
+  h->height = height;
+  h->depth = std::move(depth);
+  return h.release();
+}
+extern "C" {
+
 uint32_t b3d_depth_image_width(const b3d_depth_image* img) { return img ? img->width : 0; }
 uint32_t b3d_depth_image_height(const b3d_depth_image* img) { return img ? img->height : 0; }
 const float* b3d_depth_image_data(const b3d_depth_image* img) {

@@ -25,6 +25,8 @@
 #include "json_mini.hpp"
 
 void b3d200_set_last_error(const char* msg);  // b3d_capi.cpp
+b3d_depth_image* b3d200_depth_image_new(uint32_t width, uint32_t height,
+                                        std::vector<float>&& depth);
 void b3d200_validate_intrinsics(const b3d_intrinsics& k);
 void b3d200_render_scene_keys(b3d_gpu_context* ctx, const b3d_intrinsics* k,
                               const b3d_pose* camera, const int32_t* ids, const b3d_pose* poses,
@@ -345,7 +347,7 @@ b3d_status b3d_depth_image_load(const char* path, b3d_depth_image** out) {
     require(data.size() == 12 + count * 4, B3D_ERROR_IO, std::string(path) + ": size mismatch");
     std::vector<float> d(count);
     for (float& z : d) z = r.read<float>();
-    ok(b3d_depth_image_create(w, h, d.data(), out));
+    *out = b3d200_depth_image_new(w, h, std::move(d));
   });
 }
 

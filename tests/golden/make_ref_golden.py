@@ -392,6 +392,20 @@ def sec_fuzz():
     with open(path, "w") as f:
         json.dump([{"scene": t, "result": r} for t, r in zip(scenes, res)], f, indent=0)
     print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
+    import base64
+    files = infer_fuzz.file_cases()
+    res = infer_fuzz.run_files(R.lib(), files)
+    path = os.path.join(HERE, "ref_file_fuzz.json")
+    with open(path, "w") as f:
+        json.dump([{"kind": k, "bytes": base64.b64encode(b).decode(), "result": r}
+                   for (k, b), r in zip(files, res)], f, indent=0)
+    print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
+    mans = infer_fuzz.manifest_texts()
+    res = infer_fuzz.run_manifests(R.lib(), mans)
+    path = os.path.join(HERE, "ref_manifest_fuzz.json")
+    with open(path, "w") as f:
+        json.dump([{"manifest": t, "result": r} for t, r in zip(mans, res)], f, indent=0)
+    print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
 
 
 SECTIONS = {"pose": sec_pose, "mesh": sec_mesh, "render": sec_render, "score_cfg1": sec_score_cfg1,

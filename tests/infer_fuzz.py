@@ -183,3 +183,156 @@ def run_scenes(L, texts):
         L.b3d_scene_destroy(sc)
     L.b3d_library_destroy(lib)
     return out
+
+
+def _sdpt(w, h, vals):
+    return b"SDPT" + struct.pack("<II", w, h) + np.asarray(vals, dtype="<f4").tobytes()
+
+
+def _svox_bytes(res, origin, voxels):
+    v = np.asarray(voxels, dtype="<i4").reshape(-1, 3)
+    return (b"SVOX" + struct.pack("<4f", res, *origin) + struct.pack("<I", v.shape[0])
+            + v.tobytes())
+
+
+def file_cases(seed: int = 5, n: int = 200) -> list:
+    """Seeded random SDPT / SVOX files (io.cpp:93-147): byte flips, cuts,
+    appended bytes, edited headers and payloads."""
+    rng = random.Random(seed)
+    base_sdpt = _sdpt(4, 3, [0.5 + 0.1 * i for i in range(12)])
+    base_svox = _svox_bytes(0.01, (0.0, 0.0, 0.0), [[0, 0, 0], [1, 0, 0], [0, 2, -1]])
+    out = []
+    for _ in range(n):
+        kind = rng.choice(["sdpt", "svox"])
+        b = bytearray(base_sdpt if kind == "sdpt" else base_svox)
+        for _ in range(rng.randint(1, 2)):
+            op = rng.random()
+            if op < 0.25 and len(b) > 1:
+                del b[rng.randint(1, len(b) - 1):]
+            elif op < 0.45 and len(b) > 0:
+                i = rng.randint(0, len(b) - 1)
+                b[i] = rng.randint(0, 255)
+            elif op < 0.55:
+                b += bytes(rng.randint(0, 255) for _ in range(rng.choice([1, 4, 12])))
+            elif op < 0.75 and len(b) >= 12:
+                # a header field: dims / resolution / origin / count
+                off = rng.choice([4, 8] if kind == "sdpt" else [4, 8, 12, 16, 20])
+                val = rng.choice([0, 1, 2, 3, 5, 0xFFFFFFFF, 0x7FFFFFFF])
+                if kind == "svox" and off < 20 and rng.random() < 0.7:
+                    b[off:off + 4] = struct.pack("<f", rng.choice(
+                        [0.0, -0.01, 1e-30, float("nan"), float("inf"), 1e30, 0.5]))
+                else:
+                    b[off:off + 4] = struct.pack("<I", val)
+            else:  # payload values
+                if len(b) >= 16:
+                    i = rng.randrange(12 if kind == "sdpt" else 24, max(len(b) - 3, 13), 4) \
+                        if len(b) > 24 else 12
+                    b[i:i + 4] = struct.pack("<f" if kind == "sdpt" else "<i", rng.choice(
+                        [0.0, -1.0, 1e30, float("nan"), 2.5]) if kind == "sdpt" else
+                        rng.choice([-2147483648, 2147483647, -5, 1000]))
+        out.append((kind, bytes(b)))
+    return out
+
+
+def run_files(L, cases):
+    """[status, message] per file, or [0, summary]: an image's width, height
+    and sha256 of its floats; a model's SVOX re-saved by b3d_model_save."""
+    import hashlib
+    _sig(L)
+    L.b3d_depth_image_width.argtypes = [C.c_void_p]
+    L.b3d_depth_image_width.restype = C.c_uint32
+    L.b3d_depth_image_height.argtypes = [C.c_void_p]
+    L.b3d_depth_image_height.restype = C.c_uint32
+    L.b3d_depth_image_data.argtypes = [C.c_void_p]
+    L.b3d_depth_image_data.restype = C.POINTER(C.c_float)
+    L.b3d_model_save.argtypes = [C.c_void_p, C.c_char_p]
+    L.b3d_model_destroy.argtypes = [C.c_void_p]
+    tmp = tempfile.mkdtemp()
+    out = []
+    for kind, data in cases:
+        path = os.path.join(tmp, "f." + kind)
+        with open(path, "wb") as f:
+            f.write(data)
+        h = C.c_void_p()
+        if kind == "sdpt":
+            st = L.b3d_depth_image_load(path.encode(), C.byref(h))
+            if st == 0:
+                w, hh = L.b3d_depth_image_width(h), L.b3d_depth_image_height(h)
+                a = np.ctypeslib.as_array(L.b3d_depth_image_data(h), shape=(w * hh,)) \
+                    if w * hh else np.zeros(0, np.float32)
+                out.append([0, [w, hh, hashlib.sha256(a.tobytes()).hexdigest()]])
+                L.b3d_depth_image_destroy(h)
+                continue
+        else:
+            st = L.b3d_model_load(path.encode(), 3, C.byref(h))
+            if st == 0:
+                p2 = os.path.join(tmp, "g.svox")
+                st2 = L.b3d_model_save(h, p2.encode())
+                L.b3d_model_destroy(h)
+                if st2 != 0:
+                    out.append([int(st2), "save: " + L.b3d_last_error().decode()])
+                    continue
+                with open(p2, "rb") as f:
+                    out.append([0, hashlib.sha256(f.read()).hexdigest()])
+                continue
+        out.append([int(st), L.b3d_last_error().decode().replace(tmp, "<tmp>")])
+    return out
+
+
+MANIFEST = {"models": [{"id": 0, "path": "a.svox"}, {"id": 1, "path": "b.svox"}]}
+
+
+def manifest_texts(seed: int = 11, n: int = 150) -> list:
+    """Seeded random library manifests (scene_graph.cpp:206-234)."""
+    rng = random.Random(seed)
+    paths = ["a.svox", "b.svox", "bad.svox", "none.svox", "", "sub/../a.svox"]
+    out = []
+    for _ in range(n):
+        cfg = copy.deepcopy(MANIFEST)
+        for _ in range(rng.randint(1, 3)):
+            ps = _paths(cfg)
+            if not ps:
+                break
+            path = rng.choice(ps)
+            parent = _get(cfg, path[:-1])
+            op = rng.random()
+            if op < 0.2 and isinstance(parent, dict):
+                del parent[path[-1]]
+            elif op < 0.3 and isinstance(parent, dict):
+                parent["bogus"] = rng.choice(VALUES)
+            elif op < 0.4 and isinstance(parent, list):
+                parent.append({"id": rng.choice([0, 1, 2, 3, -1, 2.5]), "path": rng.choice(paths)})
+            elif op < 0.6 and path[-1] == "path":
+                parent["path"] = rng.choice(paths)
+            else:
+                parent[path[-1]] = copy.deepcopy(rng.choice(VALUES))
+        text = json.dumps(cfg)
+        if rng.random() < 0.04:
+            text = text[: rng.randint(1, len(text) - 1)]
+        out.append(text)
+    return out
+
+
+def run_manifests(L, texts):
+    """[status, message] per manifest, or [0, number of models]."""
+    _sig(L)
+    L.b3d_library_size.argtypes = [C.c_void_p]
+    L.b3d_library_size.restype = C.c_size_t
+    tmp = tempfile.mkdtemp()
+    _svox(os.path.join(tmp, "a.svox"), [[0, 0, 0], [1, 0, 0]], res=0.01)
+    _svox(os.path.join(tmp, "b.svox"), [[0, 0, 0], [0, 1, 0], [0, 0, 1]], res=0.01)
+    _svox(os.path.join(tmp, "bad.svox"), [[0, 0, 0]], magic=b"SVOY")
+    os.makedirs(os.path.join(tmp, "sub"), exist_ok=True)
+    out = []
+    for text in texts:
+        man = os.path.join(tmp, "m.json")
+        with open(man, "w") as f:
+            f.write(text)
+        lib = C.c_void_p()
+        st = L.b3d_library_open(man.encode(), C.byref(lib))
+        if st == 0:
+            out.append([0, int(L.b3d_library_size(lib))])
+            L.b3d_library_destroy(lib)
+        else:
+            out.append([int(st), L.b3d_last_error().decode().replace(tmp, "<tmp>")])
+    return out

@@ -130,3 +130,28 @@ def test_scene_json_fuzz():
     got = infer_fuzz.run_scenes(_lib(), [c["scene"] for c in cases])
     for c, g in zip(cases, got):
         assert g == c["result"], (c["scene"], g, c["result"])
+
+
+def test_file_format_fuzz():
+    """200 seeded random SDPT / SVOX files (byte flips, cuts, edited headers
+    and payloads): the reference's status and message, or the same image
+    (dims + float bytes) / the same model re-saved byte for byte."""
+    import base64
+    import infer_fuzz
+    with open(os.path.join(HERE, "golden", "ref_file_fuzz.json")) as f:
+        cases = json.load(f)
+    got = infer_fuzz.run_files(_lib(), [(c["kind"], base64.b64decode(c["bytes"]))
+                                        for c in cases])
+    for c, g in zip(cases, got):
+        assert g == c["result"], (c["kind"], c["bytes"], g, c["result"])
+
+
+def test_manifest_fuzz():
+    """150 seeded random library manifests: the reference's status and
+    message (nlohmann's own exception texts included), or the same library size."""
+    import infer_fuzz
+    with open(os.path.join(HERE, "golden", "ref_manifest_fuzz.json")) as f:
+        cases = json.load(f)
+    got = infer_fuzz.run_manifests(_lib(), [c["manifest"] for c in cases])
+    for c, g in zip(cases, got):
+        assert g == c["result"], (c["manifest"], g, c["result"])
