@@ -1518,21 +1518,31 @@ b3d_status b3d_log_likelihood(const b3d_depth_image* observed, const b3d_depth_i
                               double sigma_max, int window, double* out) {
   return guarded([&] {
     check(observed && rendered && k && out, "bad arguments");
-    validate_intrinsics(*k);
-    // likelihood.cpp:21-26 validate_noise
-    require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
-    require(sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
-    require(p_outlier >= 0 && p_outlier <= 1, ErrorCode::invalid,
-            "p_outlier must be in [0,1]");
-    if (window >= 0) {
+    validate_intrinsics(*k);  // from_c + visible_volume (b3d_capi.cpp:283-285)
+    auto validate_noise = [&] {  // likelihood.cpp:21-26
+      require(sigma_max > 0, ErrorCode::invalid, "sigma_max must be positive");
+      require(sigma_noise > 0, ErrorCode::invalid, "sigma_noise must be positive");
+      require(p_outlier >= 0 && p_outlier <= 1, ErrorCode::invalid,
+              "p_outlier must be in [0,1]");
+    };
+    const float far_f = static_cast<float>(k->far_m);
+    size_t rend_valid = 0;
+    for (float z : rendered->depth) rend_valid += z < far_f;
+    if (window >= 0) {  // ObservationCache::build, then windowed_log_likelihood_multi
       require(observed->width == k->width && observed->height == k->height,
               ErrorCode::invalid, "observation dimensions do not match intrinsics");
       require(observed->width == rendered->width && observed->height == rendered->height,
               ErrorCode::invalid, "windowed likelihood: image dimension mismatch");
-    } else {
-      require(observed->width == k->width && observed->height == k->height &&
-                  rendered->width == k->width && rendered->height == k->height,
+      validate_noise();
+      require(rend_valid > 0, ErrorCode::invalid, "windowed likelihood: empty rendered cloud");
+    } else {  // depth_to_cloud(rendered), depth_to_cloud(observed) -- gcc's
+              // right-to-left argument order -- then full_log_likelihood
+      require(rendered->width == k->width && rendered->height == k->height,
               ErrorCode::invalid, "depth_to_cloud: image dimensions do not match intrinsics");
+      require(observed->width == k->width && observed->height == k->height,
+              ErrorCode::invalid, "depth_to_cloud: image dimensions do not match intrinsics");
+      validate_noise();
+      require(rend_valid > 0, ErrorCode::invalid, "full_log_likelihood: empty rendered cloud");
     }
     int dev = 0;
     cuda_check(cudaGetDevice(&dev), "cudaGetDevice");

@@ -604,9 +604,12 @@ b3d_status b3d_render(const b3d_scene* scene, const b3d_pose* camera, const b3d_
                       b3d_depth_image** out) {
   return guarded([&] {  // render_depth (renderer.cpp:176-179) on the device
     check(scene && camera && k && out, "bad arguments");
+    // render_depth(scene, from_c(*camera), from_c(*k)) (b3d_capi.cpp:271):
+    // the reference's build (gcc) evaluates the arguments right to left --
+    // intrinsics, then the camera -- and scene_instances' contacts
+    // (renderer.cpp:153-162) come inside
+    b3d200_validate_intrinsics(*k);
     const b3d_pose cam = normalized_pose(*camera);
-    // scene_instances (renderer.cpp:153-162) first -- contact errors come
-    // before the intrinsics check of render_instances (renderer.cpp:176)
     std::vector<b3d_pose> poses{b3d_pose{1, 0, 0, 0, 0, 0, 0}};
     for (const auto& c : scene->children) {
       b3d_pose p;
@@ -614,7 +617,6 @@ b3d_status b3d_render(const b3d_scene* scene, const b3d_pose* camera, const b3d_
                              c.face, c.dx, c.dy, c.dtheta, &p));
       poses.push_back(p);
     }
-    b3d200_validate_intrinsics(*k);
     b3d_gpu_context* g = g_gpu.get();
     std::vector<int32_t> ids{g_gpu.table(scene->table_w, scene->table_h, scene->thickness)};
     for (const auto& c : scene->children) ids.push_back(g_gpu.mesh(*c.obj));
@@ -707,6 +709,10 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     const int n_particles = r.int_or("particles", 1000);
     cfg.resample_threshold = r.num_or("resample_threshold", 0.5);
     r.finish();
+    // make_inference_context(observed, from_c(*camera), ...) (b3d_capi.cpp:368-370):
+    // the camera is converted (unit quaternion check) as an argument, before
+    // the context's own checks
+    const b3d_pose cam = normalized_pose(*camera);
     // make_inference_context (inference.cpp:140-157), then run_smc / smc_init
     // (inference.cpp:495, 400): the reference's checks in its order, all
     // before any device work
@@ -731,7 +737,6 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
       refine.push_back({(uint32_t)st.n_dx, (uint32_t)st.n_dy, (uint32_t)st.n_dtheta});
     cfg.n_objects = (uint32_t)n_objects;
     cfg.n_particles = (uint32_t)n_particles;
-    const b3d_pose cam = normalized_pose(*camera);
     b3d_gpu_context* g = g_gpu.get();
     ok(b3d_gpu_set_camera(g, &ik, &cam));
     ok(b3d_gpu_set_observation(g, b3d_depth_image_data(observed)));

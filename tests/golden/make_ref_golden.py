@@ -400,6 +400,14 @@ def sec_fuzz():
         json.dump([{"kind": k, "bytes": base64.b64encode(b).decode(), "result": r}
                    for (k, b), r in zip(files, res)], f, indent=0)
     print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
+    for name, gen, run in (("loglik", infer_fuzz.loglik_cases, infer_fuzz.run_loglik),
+                           ("render", infer_fuzz.render_cases, infer_fuzz.run_render)):
+        cases = gen()
+        res = run(R.lib(), cases)
+        path = os.path.join(HERE, f"ref_{name}_fuzz.json")
+        with open(path, "w") as f:
+            json.dump([{"case": c, "result": r} for c, r in zip(cases, res)], f, indent=0)
+        print(f"  wrote {os.path.relpath(path, ROOT)} ({len(res)} cases)")
     mans = infer_fuzz.manifest_texts()
     res = infer_fuzz.run_manifests(R.lib(), mans)
     path = os.path.join(HERE, "ref_manifest_fuzz.json")

@@ -336,3 +336,114 @@ def run_manifests(L, texts):
         else:
             out.append([int(st), L.b3d_last_error().decode().replace(tmp, "<tmp>")])
     return out
+
+
+def loglik_cases(seed: int = 13, n: int = 160) -> list:
+    """Seeded random b3d_log_likelihood calls (b3d.h:110-115): image pairs
+    with random sentinel fractions and sizes, intrinsics, noise, window."""
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        w, h = rng.choice([(8, 6), (8, 6), (8, 6), (6, 8), (1, 1)])  # noqa: E501
+        rw, rh = (w, h) if rng.random() < 0.85 else rng.choice([(6, 8), (8, 5)])
+        fill_o, fill_r = rng.choice([0.0, 0.3, 0.9, 1.0]), rng.choice([0.0, 0.3, 0.9, 1.0])
+        far = rng.choice([4.0, 4.0, 2.0])
+        seed_img = rng.randrange(1 << 30)
+        k = [rng.choice([10.0, 10.0, 0.0, -5.0]), 10.0,
+             rng.choice([(w - 1) / 2, (w - 1) / 2, w + 3.0]), (h - 1) / 2, w, h,
+             rng.choice([0.05, 0.05, 5.0]), far]
+        if rng.random() < 0.05:
+            k[4] = 0
+        out.append({"obs": [w, h, fill_o], "rend": [rw, rh, fill_r], "seed": seed_img, "k": k,
+                    "p": rng.choice([-0.1, 0.0, 1e-9, 0.05, 0.3, 1.0, 1.5]),
+                    "sigma": rng.choice([0.0, -0.01, 1e-4, 0.01, 0.05, 0.2]),
+                    "sigma_max": rng.choice([0.0, 0.1, 0.1, 1e-3]),
+                    "window": rng.choice([-1, 0, 1, 2, 3, 100])})
+    return out
+
+
+def _img(w, h, fill, far, seed):
+    g = np.random.Generator(np.random.PCG64(seed))
+    d = g.uniform(0.5, far * 0.9, size=(h, w)).astype(np.float32)
+    d[g.random((h, w)) < fill] = np.float32(far)
+    return d
+
+
+def run_loglik(L, cases):
+    """[status, message] or [0, value] per call."""
+    _sig(L)
+    out = []
+    for c in cases:
+        k = Intr(*c["k"])
+        o = _img(*c["obs"], c["k"][7], c["seed"])
+        r = _img(*c["rend"], c["k"][7], c["seed"] + 1)
+        ho, hr = C.c_void_p(), C.c_void_p()
+        assert L.b3d_depth_image_create(o.shape[1], o.shape[0], o.ctypes.data, C.byref(ho)) == 0
+        assert L.b3d_depth_image_create(r.shape[1], r.shape[0], r.ctypes.data, C.byref(hr)) == 0
+        v = C.c_double()
+        st = L.b3d_log_likelihood(ho, hr, C.byref(k), c["p"], c["sigma"], c["sigma_max"],
+                                  c["window"], C.byref(v))
+        out.append([0, v.value] if st == 0 else [int(st), L.b3d_last_error().decode()])
+        L.b3d_depth_image_destroy(ho)
+        L.b3d_depth_image_destroy(hr)
+    return out
+
+
+def render_cases(seed: int = 17, n: int = 120) -> list:
+    """Seeded random b3d_render calls: scenes of 0-18 children (some with
+    invalid contacts), cameras around / inside / behind the table,
+    intrinsics (some invalid)."""
+    rng = random.Random(seed)
+    out = []
+    for _ in range(n):
+        nch = rng.choice([0, 1, 2, 5, 18])
+        ch = []
+        for i in range(nch):
+            ch.append({"object_id": rng.randrange(2), "face": rng.choice([1, 2, 3, 4, 5, 6, 6, 7]),
+                       "dx": rng.choice([0.01, 0.05, 0.1, 0.2, -0.01, 0.35]),
+                       "dy": rng.choice([0.01, 0.05, 0.1, 0.15]),
+                       "dtheta": rng.choice([0.0, 1.0, 3.0, 6.0, 6.3])})
+        cam = rng.choice([[0, 1, 0, 0, 0.15, 0.12, 0.5], [0, 1, 0, 0, 0.15, 0.12, 0.05],
+                          [0, 1.001, 0, 0, 0.15, 0.12, 0.5], [0, 0.9999999, 0, 0, 0.15, 0.12, 0.5],
+                          [1, 0, 0, 0, 0.1, 0.1, -0.4], [0.9238795, 0.3826834, 0, 0, 0.1, -0.2, 0.4],
+                          [0, 1, 0, 0, 0.15, 0.12, 0.01], [0, 1, 0, 0, 3.0, 0.12, 0.5]])
+        k = [20.0, 20.0, 7.5, 5.5, 16, 12, rng.choice([0.05, 0.05, 0.3]), 4.0]
+        if rng.random() < 0.1:
+            k[2] = 40.0
+        out.append({"scene": {"table": {"width": 0.3, "height": 0.25}, "children": ch},
+                    "camera": cam, "k": k})
+    return out
+
+
+def run_render(L, cases):
+    """[status, message] or [0, sha256 of the depth image] per call."""
+    import hashlib
+    _sig(L)
+    L.b3d_depth_image_data.argtypes = [C.c_void_p]
+    L.b3d_depth_image_data.restype = C.POINTER(C.c_float)
+    tmp = tempfile.mkdtemp()
+    _svox(os.path.join(tmp, "a.svox"), [[0, 0, 0], [1, 0, 0]], res=0.01)
+    _svox(os.path.join(tmp, "b.svox"), [[0, 0, 0], [0, 1, 0], [0, 0, 1]], res=0.01)
+    man = os.path.join(tmp, "m.json")
+    with open(man, "w") as f:
+        json.dump({"models": [{"id": 0, "path": "a.svox"}, {"id": 1, "path": "b.svox"}]}, f)
+    lib = C.c_void_p()
+    assert L.b3d_library_open(man.encode(), C.byref(lib)) == 0, L.b3d_last_error()
+    out = []
+    for c in cases:
+        sc = C.c_void_p()
+        st = L.b3d_scene_from_json(json.dumps(c["scene"]).encode(), lib, C.byref(sc))
+        if st != 0:
+            out.append([int(st), L.b3d_last_error().decode()])
+            continue
+        img = C.c_void_p()
+        st = L.b3d_render(sc, C.byref(Pose(*c["camera"])), C.byref(Intr(*c["k"])), C.byref(img))
+        if st == 0:
+            a = np.ctypeslib.as_array(L.b3d_depth_image_data(img), shape=(c["k"][4] * c["k"][5],))
+            out.append([0, hashlib.sha256(a.tobytes()).hexdigest()])
+            L.b3d_depth_image_destroy(img)
+        else:
+            out.append([int(st), L.b3d_last_error().decode()])
+        L.b3d_scene_destroy(sc)
+    L.b3d_library_destroy(lib)
+    return out

@@ -155,3 +155,41 @@ def test_manifest_fuzz():
     got = infer_fuzz.run_manifests(_lib(), [c["manifest"] for c in cases])
     for c, g in zip(cases, got):
         assert g == c["result"], (c["manifest"], g, c["result"])
+
+
+def _check_calls(name, gpu):
+    import infer_fuzz
+    with open(os.path.join(HERE, "golden", f"ref_{name}_fuzz.json")) as f:
+        cases = json.load(f)
+    run = infer_fuzz.run_loglik if name == "loglik" else infer_fuzz.run_render
+    got = run(_lib(), [c["case"] for c in cases])
+    compared = 0
+    for c, g in zip(cases, got):
+        want = c["result"]
+        if not gpu and _device_error(g):
+            continue
+        compared += 1
+        if name == "loglik" and want[0] == 0 and g[0] == 0 and g[1] != want[1]:
+            # the windowed / full likelihood on the device in fp64 (equal
+            # infinities compare equal above)
+            assert abs(g[1] - want[1]) <= 1e-9 * abs(want[1]), (c["case"], g, want)
+        else:
+            assert g == want, (c["case"], g, want)
+    return compared
+
+
+def test_loglik_and_render_fuzz_cpu():
+    """160 random b3d_log_likelihood calls (sizes, sentinel fractions,
+    intrinsics, noise, windows) and 120 random b3d_render calls (scenes of up
+    to 18 children, invalid contacts and faces, non-unit cameras, invalid
+    intrinsics): every error the product raises before the device equals the
+    reference's, in the reference's order of checks."""
+    assert _check_calls("loglik", False) >= 140
+    assert _check_calls("render", False) >= 90
+
+
+@pytest.mark.gpu
+def test_loglik_and_render_fuzz_gpu():
+    """All of them: values within 1e-9 relative, renders bitwise (sha256)."""
+    assert _check_calls("loglik", True) == 160
+    assert _check_calls("render", True) == 120
