@@ -199,18 +199,14 @@ std::shared_ptr<b3d_object_model> load_svox(const std::string& path, int id) {  
 // cvttsd2si) or 0 (uint32_t, through the 64-bit conversion).
 int json_int(const J::Value& x) {
   if (x.kind == J::Value::Bool) return x.b ? 1 : 0;  // nlohmann converts booleans too
-  if (x.integral) {
-    if (x.num >= 9223372036854775808.0) return (int)(uint32_t)(uint64_t)x.num;
-    return (int)(uint32_t)(uint64_t)(int64_t)x.num;
-  }
+  if (x.int_kind == 1) return (int)(uint32_t)(uint64_t)x.i;
+  if (x.int_kind == 2) return (int)(uint32_t)x.u;
   return (x.num > -2147483649.0 && x.num < 2147483648.0) ? (int)x.num : INT_MIN;
 }
 uint32_t json_u32(const J::Value& x) {
   if (x.kind == J::Value::Bool) return x.b ? 1u : 0u;
-  if (x.integral) {
-    if (x.num >= 9223372036854775808.0) return (uint32_t)(uint64_t)x.num;
-    return (uint32_t)(uint64_t)(int64_t)x.num;
-  }
+  if (x.int_kind == 1) return (uint32_t)(uint64_t)x.i;
+  if (x.int_kind == 2) return (uint32_t)x.u;
   return (x.num > -9223372036854775809.0 && x.num < 9223372036854775808.0)
              ? (uint32_t)(uint64_t)(int64_t)x.num
              : 0u;

@@ -1,11 +1,15 @@
 // json_mini.hpp -- a small strict JSON reader for the reference's
 // configuration objects (b3d_scene_from_json, b3d_infer config, library
 // manifests) and a compact writer; the reference uses nlohmann::json, which
-// this image does not ship.  Numbers are parsed with strtod and written as
-// nlohmann's dump writes them (shortest round-trip digits); object keys keep
-// their order.
+// this image does not ship, and the reader accepts exactly what its parser
+// accepts (RFC 8259; objects keyed like its std::map, in byte order, the last
+// of repeated keys kept).  Numbers keep their integer literal (int64 /
+// uint64) or strtod value and are written as nlohmann's dump writes them
+// (shortest round-trip digits).
 #pragma once
 
+#include <algorithm>
+#include <cerrno>
 #include <charconv>
 #include <cmath>
 #include <cstdio>
@@ -24,7 +28,11 @@ struct Value {
   enum Kind { Null, Bool, Number, String, Array, Object } kind = Null;
   bool b = false;
   double num = 0;
-  bool integral = false;  // written without fraction / exponent
+  // an integer literal that fits (nlohmann: number_integer if negative,
+  // number_unsigned otherwise); any other number is a float
+  int int_kind = 0;  // 0 float, 1 int64 (i), 2 uint64 (u)
+  long long i = 0;
+  unsigned long long u = 0;
   std::string str;
   std::vector<Value> arr;
   std::vector<std::pair<std::string, Value>> obj;
@@ -46,6 +54,7 @@ class Parser {
  public:
   explicit Parser(const std::string& s) : s_(s) {}
   Value parse() {
+    if (s_.compare(0, 3, "\xEF\xBB\xBF") == 0) i_ = 3;  // a leading UTF-8 BOM is skipped
     Value v = value();
     ws();
     if (i_ != s_.size()) throw ParseError("trailing characters");
@@ -86,6 +95,18 @@ class Parser {
         v.obj.emplace_back(std::move(k), value());
       } while (eat(','));
       expect('}');
+      // nlohmann's object is a std::map: keys in byte order, a repeated key
+      // keeps its last value
+      std::stable_sort(v.obj.begin(), v.obj.end(),
+                       [](const auto& a, const auto& b) { return a.first < b.first; });
+      std::vector<std::pair<std::string, Value>> uniq;
+      for (auto& kv : v.obj) {
+        if (!uniq.empty() && uniq.back().first == kv.first)
+          uniq.back().second = std::move(kv.second);
+        else
+          uniq.push_back(std::move(kv));
+      }
+      v.obj = std::move(uniq);
     } else if (c == '[') {
       ++i_;
       v.kind = Value::Array;
@@ -105,58 +126,148 @@ class Parser {
       v.kind = Value::Bool;
     } else if (s_.compare(i_, 4, "null") == 0) {
       i_ += 4;
-    } else {
-      const char* b = s_.c_str() + i_;
-      char* e = nullptr;
-      v.num = std::strtod(b, &e);
-      if (e == b) throw ParseError("invalid value");
+    } else {  // JSON number grammar: -?(0|[1-9]d*)(.d+)?([eE][+-]?d+)?
+      const size_t b0 = i_;
+      size_t q = i_;
+      auto digit = [&](size_t k) { return k < s_.size() && s_[k] >= '0' && s_[k] <= '9'; };
+      if (q < s_.size() && s_[q] == '-') ++q;
+      if (!digit(q)) throw ParseError("invalid value");
+      if (s_[q] == '0') ++q;
+      else
+        while (digit(q)) ++q;
+      bool is_int = true;
+      if (q < s_.size() && s_[q] == '.') {
+        is_int = false;
+        ++q;
+        if (!digit(q)) throw ParseError("invalid number");
+        while (digit(q)) ++q;
+      }
+      if (q < s_.size() && (s_[q] == 'e' || s_[q] == 'E')) {
+        is_int = false;
+        ++q;
+        if (q < s_.size() && (s_[q] == '+' || s_[q] == '-')) ++q;
+        if (!digit(q)) throw ParseError("invalid number");
+        while (digit(q)) ++q;
+      }
+      const std::string lit = s_.substr(b0, q - b0);
       v.kind = Value::Number;
-      v.integral = true;
-      for (const char* q = b; q < e; ++q)
-        if (*q == '.' || *q == 'e' || *q == 'E') v.integral = false;
-      i_ += (size_t)(e - b);
+      v.num = std::strtod(lit.c_str(), nullptr);
+      if (is_int) {
+        errno = 0;
+        if (lit[0] == '-') {
+          const long long x = std::strtoll(lit.c_str(), nullptr, 10);
+          if (errno == 0) {
+            v.int_kind = 1;
+            v.i = x;
+          }
+        } else {
+          const unsigned long long x = std::strtoull(lit.c_str(), nullptr, 10);
+          if (errno == 0) {
+            v.int_kind = 2;
+            v.u = x;
+          }
+        }
+      }
+      i_ = q;
     }
     return v;
   }
   std::string string() {
+    // RFC 8259 strings as nlohmann's lexer reads them: no raw control
+    // characters, the eight escapes and \uXXXX (surrogate pairs combined,
+    // lone surrogates rejected), well-formed UTF-8 otherwise
     if (i_ >= s_.size() || s_[i_] != '"') throw ParseError("expected a string");
     ++i_;
     std::string out;
-    while (i_ < s_.size() && s_[i_] != '"') {
-      char c = s_[i_++];
+    auto put_utf8 = [&](unsigned cp) {
+      if (cp < 0x80) {
+        out += (char)cp;
+      } else if (cp < 0x800) {
+        out += (char)(0xC0 | (cp >> 6));
+        out += (char)(0x80 | (cp & 0x3F));
+      } else if (cp < 0x10000) {
+        out += (char)(0xE0 | (cp >> 12));
+        out += (char)(0x80 | ((cp >> 6) & 0x3F));
+        out += (char)(0x80 | (cp & 0x3F));
+      } else {
+        out += (char)(0xF0 | (cp >> 18));
+        out += (char)(0x80 | ((cp >> 12) & 0x3F));
+        out += (char)(0x80 | ((cp >> 6) & 0x3F));
+        out += (char)(0x80 | (cp & 0x3F));
+      }
+    };
+    auto hex4 = [&]() -> unsigned {
+      if (i_ + 4 > s_.size()) throw ParseError("bad escape");
+      unsigned v = 0;
+      for (int k = 0; k < 4; ++k) {
+        const char h = s_[i_++];
+        v <<= 4;
+        if (h >= '0' && h <= '9') v |= (unsigned)(h - '0');
+        else if (h >= 'a' && h <= 'f') v |= (unsigned)(h - 'a' + 10);
+        else if (h >= 'A' && h <= 'F') v |= (unsigned)(h - 'A' + 10);
+        else throw ParseError("bad escape");
+      }
+      return v;
+    };
+    for (;;) {
+      if (i_ >= s_.size()) throw ParseError("unterminated string");
+      const unsigned char c = (unsigned char)s_[i_++];
+      if (c == '"') break;
+      if (c < 0x20) throw ParseError("control character in string");
       if (c == '\\') {
-        if (i_ >= s_.size()) break;
+        if (i_ >= s_.size()) throw ParseError("bad escape");
         const char e = s_[i_++];
         switch (e) {
-          case 'n': c = '\n'; break;
-          case 't': c = '\t'; break;
-          case 'r': c = '\r'; break;
-          case 'b': c = '\b'; break;
-          case 'f': c = '\f'; break;
+          case '"': out += '"'; break;
+          case '\\': out += '\\'; break;
+          case '/': out += '/'; break;
+          case 'b': out += '\b'; break;
+          case 'f': out += '\f'; break;
+          case 'n': out += '\n'; break;
+          case 'r': out += '\r'; break;
+          case 't': out += '\t'; break;
           case 'u': {
-            if (i_ + 4 > s_.size()) throw ParseError("bad escape");
-            const unsigned cp = (unsigned)std::strtoul(s_.substr(i_, 4).c_str(), nullptr, 16);
-            i_ += 4;
-            if (cp < 0x80) {
-              c = (char)cp;
-            } else {  // UTF-8 (BMP only)
-              if (cp < 0x800) {
-                out += (char)(0xC0 | (cp >> 6));
-              } else {
-                out += (char)(0xE0 | (cp >> 12));
-                out += (char)(0x80 | ((cp >> 6) & 0x3F));
-              }
-              c = (char)(0x80 | (cp & 0x3F));
+            unsigned cp = hex4();
+            if (cp >= 0xD800 && cp <= 0xDBFF) {  // a high surrogate needs its low half
+              if (i_ + 2 > s_.size() || s_[i_] != '\\' || s_[i_ + 1] != 'u')
+                throw ParseError("lone surrogate");
+              i_ += 2;
+              const unsigned lo = hex4();
+              if (lo < 0xDC00 || lo > 0xDFFF) throw ParseError("lone surrogate");
+              cp = 0x10000 + ((cp - 0xD800) << 10) + (lo - 0xDC00);
+            } else if (cp >= 0xDC00 && cp <= 0xDFFF) {
+              throw ParseError("lone surrogate");
             }
+            put_utf8(cp);
             break;
           }
-          default: c = e;
+          default: throw ParseError("bad escape");
         }
+        continue;
       }
-      out += c;
+      if (c < 0x80) {
+        out += (char)c;
+        continue;
+      }
+      // a multi-byte UTF-8 sequence, checked (shortest form, no surrogates)
+      int n = 0;
+      unsigned cp = 0;
+      if ((c & 0xE0) == 0xC0) n = 1, cp = c & 0x1F;
+      else if ((c & 0xF0) == 0xE0) n = 2, cp = c & 0x0F;
+      else if ((c & 0xF8) == 0xF0) n = 3, cp = c & 0x07;
+      else throw ParseError("ill-formed UTF-8");
+      if (i_ + n > s_.size()) throw ParseError("ill-formed UTF-8");
+      for (int k = 0; k < n; ++k) {
+        const unsigned char d = (unsigned char)s_[i_ + k];
+        if ((d & 0xC0) != 0x80) throw ParseError("ill-formed UTF-8");
+        cp = (cp << 6) | (d & 0x3F);
+      }
+      if ((n == 1 && cp < 0x80) || (n == 2 && cp < 0x800) || (n == 3 && cp < 0x10000) ||
+          cp > 0x10FFFF || (cp >= 0xD800 && cp <= 0xDFFF))
+        throw ParseError("ill-formed UTF-8");
+      out.append(s_, i_ - 1, (size_t)n + 1);
+      i_ += (size_t)n;
     }
-    if (i_ >= s_.size()) throw ParseError("unterminated string");
-    ++i_;
     return out;
   }
 };

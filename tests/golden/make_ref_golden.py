@@ -373,13 +373,14 @@ def sec_capi():
 
 
 def sec_fuzz():
-    """The reference's b3d_infer on 240 seeded random configurations and its
+    """The reference's b3d_infer on 240 seeded random configurations (and 200
+    character-level edits of one, for the JSON parser's verdicts) and its
     b3d_scene_from_json / b3d_scene_to_json on 200 random scene documents
     (tests/infer_fuzz.py): status + message, or the result."""
     import json
     sys.path.insert(0, os.path.join(ROOT, "tests"))
     import infer_fuzz
-    texts = infer_fuzz.configs()
+    texts = infer_fuzz.configs() + infer_fuzz.syntax_texts()
     res = infer_fuzz.run(R.lib(), texts, True)
     path = os.path.join(HERE, "ref_infer_fuzz.json")
     with open(path, "w") as f:

@@ -104,9 +104,10 @@ def run(L, texts, allow_device: bool):
     out = []
     for text in texts:
         part = vp()
-        st = L.b3d_infer(obs, C.byref(CAMERA), lib, text.encode(), 3, C.byref(part))
+        st = L.b3d_infer(obs, C.byref(CAMERA), lib, text.encode("utf-8", "surrogatepass"), 3,
+                         C.byref(part))
         if st != 0:
-            out.append([int(st), L.b3d_last_error().decode()])
+            out.append([int(st), L.b3d_last_error().decode("utf-8", "backslashreplace")])
             continue
         le, txt = C.c_double(), C.c_void_p()
         assert L.b3d_particles_log_evidence(part, C.byref(le)) == 0
@@ -446,4 +447,30 @@ def run_render(L, cases):
             out.append([int(st), L.b3d_last_error().decode()])
         L.b3d_scene_destroy(sc)
     L.b3d_library_destroy(lib)
+    return out
+
+
+def syntax_texts(seed: int = 19, n: int = 200) -> list:
+    """The base infer config's JSON text with random character edits:
+    brackets, quotes, commas, escapes (\\u, \\n, bad ones), control
+    characters, duplicate keys, whitespace -- for the parser's verdicts."""
+    rng = random.Random(seed)
+    base = json.dumps(BASE)
+    pieces = ['{', '}', '[', ']', '"', ',', ':', '\\\\', '\\\\u0041', '\\\\uD83D\\\\uDE00', '\\\\x',
+              '\\t', '\\n', ' ', '\\u0001', 'true', 'null', '-', '0', '1e5', '"threads": 1, ',
+              '"window": 1, ', '/**/', '\\ufeff', 'é', '"s\\\\"t"']
+    out = []
+    for _ in range(n):
+        t = base
+        for _ in range(rng.randint(1, 2)):
+            i = rng.randrange(len(t))
+            op = rng.random()
+            p = rng.choice(pieces).encode().decode("unicode_escape")
+            if op < 0.4:
+                t = t[:i] + p + t[i:]
+            elif op < 0.7:
+                t = t[:i] + t[i + 1:]
+            else:
+                t = t[:i] + p + t[i + 1:]
+        out.append(t)
     return out

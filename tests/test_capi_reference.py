@@ -92,7 +92,9 @@ def _device_error(res):
 
 
 def test_infer_config_fuzz_cpu():
-    """240 seeded random b3d_infer configurations (tests/infer_fuzz.py): every
+    """240 seeded random b3d_infer configurations plus 200 character-level
+    edits of one (tests/infer_fuzz.py; strings, escapes, surrogates, control
+    characters, numbers, BOM, repeated keys -- the JSON parser's verdicts): every
     one the product settles on the host -- JSON and schema errors, nlohmann's
     number conversions (booleans and floats into integers, wrapping, gcc's
     right-to-left argument order), make_inference_context / run_smc checks
@@ -106,7 +108,7 @@ def test_infer_config_fuzz_cpu():
             continue  # needs the device: the GPU test covers it
         compared += 1
         assert _same(g, c["result"]), (c["config"], g, c["result"])
-    assert compared >= 200
+    assert compared >= 380
 
 
 @pytest.mark.gpu
