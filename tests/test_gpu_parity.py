@@ -1151,3 +1151,33 @@ def test_c_abi_is_thread_safe_like_the_reference():
     for i in range(8):
         np.testing.assert_array_equal(got[i].view(np.uint32), serial[i].view(np.uint32))
         assert got_ll[i] == serial_ll[i]
+
+
+@pytest.mark.parametrize("wh", [(1, 1), (3, 2), (2, 3), (1920, 1080)])
+def test_extreme_image_sizes(gpu_ctx, oracle, wh):
+    """1x1, 3x2, 2x3 and 1920x1080 images: depth / ids bitwise, scores within
+    1e-4 of the oracle (= the reference, bitwise on every fixture)."""
+    w_px, h_px = wh
+    f = 0.9 * max(w_px, h_px)
+    k = configs.Intr(f, f, (w_px - 1) / 2, (h_px - 1) / 2, w_px, h_px, 0.01, 10.0)
+    vox = synth.eden_blob(500, 21)
+    verts, tris = configs.make_mesh(vox, oracle.voxel_to_mesh)
+    rng = np.random.Generator(np.random.PCG64(9))
+    poses = np.array([[*synth.uniform_quaternion(rng), rng.uniform(-0.02, 0.02),
+                       rng.uniform(-0.02, 0.02), rng.uniform(0.3, 0.6)] for _ in range(4)])
+    _render_parity(gpu_ctx, oracle, k, verts, tris, poses)
+    obs = np.array(oracle.render(k, [(verts, tris, poses[0])]), dtype=np.float32)
+    if (obs < k.far).sum() == 0:
+        return  # nothing visible at this size: the renders above are the check
+    gpu_ctx.set_camera(b3d_intr(k))
+    mid = gpu_ctx.upload_mesh(verts, tris)
+    gpu_ctx.set_likelihood([(0.1, 0.01)], 0.1, 1)
+    gpu_ctx.set_observation(obs)
+    s, st = gpu_ctx.score_poses(mid, poses)
+    for i in range(poses.shape[0]):
+        d = oracle.render(k, [(verts, tris, poses[i])])
+        if (d < k.far).sum() == 0:
+            assert st[i] == 1
+            continue
+        want = oracle.windowed_loglik_multi(obs, d, k, [(0.1, 0.01)], 0.1, 1)[0]
+        assert rel_err(s[i, 0], want) <= 1e-4, (wh, i, s[i, 0], want)
