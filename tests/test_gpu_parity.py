@@ -1181,3 +1181,33 @@ def test_extreme_image_sizes(gpu_ctx, oracle, wh):
             continue
         want = oracle.windowed_loglik_multi(obs, d, k, [(0.1, 0.01)], 0.1, 1)[0]
         assert rel_err(s[i, 0], want) <= 1e-4, (wh, i, s[i, 0], want)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_adversarial_triangle_soup(gpu_ctx, oracle, seed):
+    """Triangle soups built to hit the rasterizer's corner cases: vertices
+    placed on pixel centres and half-pixels (edges through centres, the
+    top-left tie rule), shared edges, zero-area and sliver triangles, equal
+    depths (the draw-index tie), vertices behind / on / just in front of
+    z = near (the clipped fan), and triangles far outside the image --
+    depth and ids bitwise equal to the oracle."""
+    rng = np.random.Generator(np.random.PCG64(100 + seed))
+    k = configs.Intr(40.0, 40.0, 15.5, 11.5, 32, 24, 0.1, 5.0)
+    pts = []
+    for _ in range(300):
+        u = rng.integers(-8, 40) + rng.choice([0.0, 0.5, 0.25])
+        v = rng.integers(-8, 32) + rng.choice([0.0, 0.5])
+        z = rng.choice([0.1, 0.1 * (1 - 1e-13), 0.09, 0.05, 0.5, 1.0, 1.0, 2.0, 4.99, 6.0])
+        pts.append([(u - k.cx) * z / k.fx, (v - k.cy) * z / k.fy, z])
+    pts = np.array(pts)
+    tris = []
+    for _ in range(400):
+        a, b, c = rng.integers(0, len(pts), 3)
+        tris.append([a, b, c])
+        if rng.random() < 0.2:  # a neighbour sharing the edge (a, b)
+            tris.append([b, a, rng.integers(0, len(pts))])
+        if rng.random() < 0.05:
+            tris.append([a, a, b])  # zero area
+    tris = np.array(tris, dtype=np.uint32)
+    poses = np.array([[1.0, 0, 0, 0, 0, 0, 0], [1.0, 0, 0, 0, 0.01, -0.02, 0.3]])
+    _render_parity(gpu_ctx, oracle, k, pts, tris, poses)
