@@ -432,9 +432,12 @@ B3D_API b3d_status b3d_gpu_score_grid_range(b3d_gpu_context* ctx, int32_t mesh_i
                                             uint64_t n, double* scores, uint8_t* status);
 
 /* ---- camera mode: a scene of mesh instances under camera hypotheses ----
- * render_instances (renderer.cpp:153-189) of up to 16 instances in draw
+ * render_instances (renderer.cpp:153-189) of any number of instances in draw
  * order (draw indices continue across instances); model_to_world[i] is used
- * verbatim, as scene_instances (inference.cpp:172-184) produces it. */
+ * verbatim, as scene_instances (inference.cpp:172-184) produces it.  Up to
+ * B3D_MAX_INSTANCES instances render and score in one fused launch; larger
+ * scenes render per group of B3D_MAX_INSTANCES, merged per pixel (the same
+ * depth and ids), and score through the fp64 image likelihood. */
 enum { B3D_MAX_INSTANCES = 16 };
 B3D_API b3d_status b3d_gpu_set_camera_scene(b3d_gpu_context* ctx, const int32_t* mesh_ids,
                                             const b3d_pose* model_to_world, uint32_t n);

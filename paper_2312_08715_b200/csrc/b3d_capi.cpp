@@ -54,6 +54,11 @@ cudaError_t launch_obs_prepare(const float* depth, int W, int H, float far_f, fl
                                float fcy, float inv_fx, float inv_fy, float4* out,
                                int* count, cudaStream_t st);
 cudaError_t launch_exact_score(const KExactArgs& a, int ctas, cudaStream_t st);
+cudaError_t launch_min_merge_f32(float* dst, const float* src, size_t n, cudaStream_t st);
+cudaError_t launch_min_merge_u64(unsigned long long* dst, const unsigned long long* src,
+                                 size_t n, cudaStream_t st);
+cudaError_t launch_keys_to_depth_ids(const unsigned long long* keys, size_t n, float far_f,
+                                     float* depth, int32_t* ids, cudaStream_t st);
 cudaError_t launch_shard_barrier(const KBarrier& b, cudaStream_t st);
 cudaError_t launch_exchange_emulation(unsigned long long* sig, double* arr, int n_ranks,
                                       int rounds, int double_buffered,
@@ -424,10 +429,19 @@ struct b3d_gpu_context {
   long long score_peer_offset = 0;
   long long score_peer_cap = 0;
   // camera mode scene (b3d_gpu_set_camera_scene): concatenated instances
-  std::unique_ptr<Mesh> cam_mesh;
-  int cam_n = 0;
-  int cam_v0[kMaxInst + 1] = {0};
-  KPose cam_pose[kMaxInst];
+  // camera scene (b3d_gpu_set_camera_scene): instances in draw order, in
+  // groups of up to kMaxInst (one concatenated mesh each; draw indices
+  // continue across groups).  One group: the fused camera-mode kernels; more:
+  // per-group renders merged per pixel, then the fp64 image likelihood.
+  struct CamGroup {
+    std::unique_ptr<Mesh> mesh;
+    int n = 0;
+    int v0[kMaxInst + 1] = {0};
+    KPose pose[kMaxInst];
+    uint32_t draw_base = 0;
+  };
+  std::vector<CamGroup> cam_groups;
+  DevBuf cam_tmp, cam_keys;
   long long obs_version = 0, base_version = 0;
   std::string base_terms_key;
 };
@@ -1409,13 +1423,76 @@ double lattice_at(double center, double extent, int n, int i) {
   return center - extent + 2.0 * extent * i / (n - 1);
 }
 
-void cam_params(b3d_gpu_context* ctx, KParams& p) {
+void cam_params(b3d_gpu_context* ctx, KParams& p, const b3d_gpu_context::CamGroup& g) {
+  (void)ctx;
   p.cams = nullptr;
-  p.n_inst = ctx->cam_n;
-  for (int i = 0; i <= kMaxInst; ++i) p.inst_v0[i] = ctx->cam_v0[i];
-  for (int i = 0; i < kMaxInst; ++i) p.inst_pose[i] = ctx->cam_pose[i];
-  p.draw_base = 0;
+  p.n_inst = g.n;
+  for (int i = 0; i <= kMaxInst; ++i) p.inst_v0[i] = g.v0[i];
+  for (int i = 0; i < kMaxInst; ++i) p.inst_pose[i] = g.pose[i];
+  p.draw_base = g.draw_base;
   p.base_keys = nullptr;
+}
+
+// Render-many of hypotheses cams[0..n) over every camera group: depth (or,
+// with keys, 64-bit (depth, draw) keys) of group 0 into out, each further
+// group into a scratch image set merged per pixel (the z-test's minimum is
+// the same whatever the instance order; ties keep the lower draw index).
+void render_camera_groups(b3d_gpu_context* ctx, const KPose* cams, long long n, float* depth,
+                          unsigned long long* keys) {
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  for (size_t gi = 0; gi < ctx->cam_groups.size(); ++gi) {
+    const auto& g = ctx->cam_groups[gi];
+    const Mesh& m = *g.mesh;
+    KParams q = base_params(ctx, m);
+    cam_params(ctx, q, g);
+    q.cams = cams;
+    q.n_hyp = n;
+    q.lik.n_noise = 0;
+    q.scores = nullptr;
+    q.status = nullptr;
+    q.rng_dst = nullptr;
+    q.n_score_peers = 0;
+    float* od = nullptr;
+    unsigned long long* ok = nullptr;
+    if (gi == 0) {
+      od = depth;
+      ok = keys;
+    } else if (keys) {
+      ctx->cam_tmp.ensure(8 * npx * (size_t)n);
+      ok = ctx->cam_tmp.as<unsigned long long>();
+    } else {
+      ctx->cam_tmp.ensure(4 * npx * (size_t)n);
+      od = ctx->cam_tmp.as<float>();
+    }
+    q.out_depth = keys ? nullptr : od;
+    q.out_ids = nullptr;
+    q.out_keys = ok;
+    if (keys) {
+      LaunchPlan lp = plan_launch<true, false, true>(ctx, m, n);
+      q.zscratch = ctx->zscratch.as<unsigned long long>();
+      q.vscratch = ctx->vscratch.as<double>();
+      q.vcap = lp.vcap;
+      q.zcap = lp.zcap;
+      q.zstride = lp.zstride;
+      cuda_check(launch_render_score<true, false, true>(q, lp.grid, lp.smem, ctx->stream),
+                 "render launch (camera groups)");
+    } else {
+      LaunchPlan lp = plan_launch<false, false, true>(ctx, m, n);
+      q.zscratch = ctx->zscratch.as<unsigned long long>();
+      q.vscratch = ctx->vscratch.as<double>();
+      q.vcap = lp.vcap;
+      q.zcap = lp.zcap;
+      q.zstride = lp.zstride;
+      cuda_check(launch_render_score<false, false, true>(q, lp.grid, lp.smem, ctx->stream),
+                 "render launch (camera groups)");
+    }
+    if (gi > 0) {
+      if (keys)
+        cuda_check(launch_min_merge_u64(keys, ok, npx * (size_t)n, ctx->stream), "merge keys");
+      else
+        cuda_check(launch_min_merge_f32(depth, od, npx * (size_t)n, ctx->stream), "merge depth");
+    }
+  }
 }
 
 // score-many over camera poses (device-resident `cams` of n entries) into
@@ -1423,12 +1500,51 @@ void cam_params(b3d_gpu_context* ctx, KParams& p) {
 void launch_score_cameras(b3d_gpu_context* ctx, const KPose* cams, long long n, double* scores,
                           uint8_t* status, bool pdl = false) {
   require(ctx->cam_spec_err.empty(), ErrorCode::invalid, ctx->cam_spec_err);
-  const Mesh& m = *ctx->cam_mesh;
-  KParams p = base_params(ctx, m);
-  cam_params(ctx, p);
-  p.cams = cams;
-  p.n_hyp = n;
-  run_scores(ctx, m, p, ctx->cam_spec, n, scores, status, true, 0, pdl);
+  if (ctx->cam_groups.size() == 1) {  // the fused camera-mode kernel
+    const auto& g = ctx->cam_groups.front();
+    const Mesh& m = *g.mesh;
+    KParams p = base_params(ctx, m);
+    cam_params(ctx, p, g);
+    p.cams = cams;
+    p.n_hyp = n;
+    run_scores(ctx, m, p, ctx->cam_spec, n, scores, status, true, 0, pdl);
+    return;
+  }
+  // more instances than one launch holds: merged group renders, then the
+  // fp64 image likelihood (exact_score.cu) of each hypothesis
+  const LikSpec& spec = ctx->cam_spec;
+  const size_t npx = (size_t)ctx->k.width * ctx->k.height;
+  const long long chunk =
+      std::max<long long>(1, std::min<long long>(n, (256ll << 20) / (4 * (long long)npx)));
+  ctx->ex_depth.ensure(4 * npx * (size_t)chunk);
+  const int ctas = (int)std::min<long long>(chunk, 4ll * ctx->sm_count);
+  if (spec.window < 0)
+    ctx->ex_pts.ensure(exact_score_pts_bytes((int)ctx->k.width, (int)ctx->k.height, ctas));
+  for (long long h0 = 0; h0 < n; h0 += chunk) {
+    const long long c = std::min(chunk, n - h0);
+    render_camera_groups(ctx, cams + h0, c, ctx->ex_depth.as<float>(), nullptr);
+    for (const LikChunk& ch : spec.chunks) {
+      KExactArgs a{};
+      a.obs = ctx->obs_pts.as<float4>();
+      a.rend = ctx->ex_depth.as<float>();
+      a.W = (int)ctx->k.width;
+      a.H = (int)ctx->k.height;
+      a.fx = ctx->k.fx;
+      a.fy = ctx->k.fy;
+      a.cx = ctx->k.cx;
+      a.cy = ctx->k.cy;
+      a.far_f = static_cast<float>(ctx->k.far_m);
+      a.n = c;
+      a.scores = scores + (size_t)h0 * spec.n_cols;
+      a.ld = spec.n_cols;
+      a.col0 = ch.col0;
+      a.status = status ? status + h0 : nullptr;
+      a.pts = spec.window < 0 ? ctx->ex_pts.as<double>() : nullptr;
+      a.lik = ch.ex;
+      cuda_check(launch_exact_score(a, (int)std::min<long long>(c, ctas), ctx->stream),
+                 "exact_score launch (camera groups)");
+    }
+  }
 }
 }  // namespace
 
@@ -2054,46 +2170,58 @@ b3d_status b3d_gpu_set_camera_scene(b3d_gpu_context* ctx, const int32_t* mesh_id
   return guarded([&] {
     if (ctx) ++ctx->gen;
     check(ctx && mesh_ids && model_to_world, "bad arguments");
-    require(n >= 1 && n <= (uint32_t)kMaxInst, ErrorCode::invalid,
-            "camera scene: 1 to 16 instances");
+    require(n >= 1, ErrorCode::invalid, "camera scene: at least one instance");
+    for (uint32_t i = 0; i < n; ++i) get_mesh(ctx, mesh_ids[i]);  // ids valid
     DeviceGuard dg(ctx->device);
-    auto sm = std::make_unique<Mesh>();
-    long long nv = 0, nt = 0;
-    int sign = 2;
-    for (uint32_t i = 0; i < n; ++i) {
-      const Mesh& m = get_mesh(ctx, mesh_ids[i]);
-      ctx->cam_v0[i] = (int)nv;
-      nv += m.nv;
-      nt += m.nt;
-      sign = (sign == 2 || sign == m.cull) ? m.cull : 0;
-    }
-    require(nv < (1ll << 30) && nt < (1ll << 30), ErrorCode::invalid, "camera scene: too large");
-    for (uint32_t i = n; i <= (uint32_t)kMaxInst; ++i) ctx->cam_v0[i] = (int)nv;
-    sm->nv = (int)nv;
-    sm->nt = (int)nt;
-    sm->cull = sign == 2 ? 0 : sign;  // per-triangle culling only if every mesh shares a sign
-    sm->verts.ensure(24 * nv);
-    sm->tris.ensure(16 * nt);
-    std::vector<uint32_t> tri(4 * nt);
-    long long vo = 0, to = 0;
-    for (uint32_t i = 0; i < n; ++i) {
-      const Mesh& m = get_mesh(ctx, mesh_ids[i]);
-      cuda_check(cudaMemcpy(sm->verts.as<char>() + 24 * vo, m.verts.p, 24ull * m.nv,
-                            cudaMemcpyDeviceToDevice),
+    std::vector<b3d_gpu_context::CamGroup> groups;
+    long long draw = 0;
+    for (uint32_t g0 = 0; g0 < n; g0 += (uint32_t)kMaxInst) {
+      const uint32_t gn = std::min<uint32_t>((uint32_t)kMaxInst, n - g0);
+      b3d_gpu_context::CamGroup grp;
+      grp.n = (int)gn;
+      grp.draw_base = (uint32_t)draw;
+      auto sm = std::make_unique<Mesh>();
+      long long nv = 0, nt = 0;
+      int sign = 2;
+      for (uint32_t i = 0; i < gn; ++i) {
+        const Mesh& m = get_mesh(ctx, mesh_ids[g0 + i]);
+        grp.v0[i] = (int)nv;
+        nv += m.nv;
+        nt += m.nt;
+        sign = (sign == 2 || sign == m.cull) ? m.cull : 0;
+      }
+      require(nv < (1ll << 30) && nt < (1ll << 30) && draw + nt < (1ll << 31),
+              ErrorCode::invalid, "camera scene: too large");
+      for (uint32_t i = gn; i <= (uint32_t)kMaxInst; ++i) grp.v0[i] = (int)nv;
+      sm->nv = (int)nv;
+      sm->nt = (int)nt;
+      sm->cull = sign == 2 ? 0 : sign;  // per-triangle culling only if every mesh shares a sign
+      sm->verts.ensure(24 * nv);
+      sm->tris.ensure(16 * nt);
+      std::vector<uint32_t> tri(4 * nt);
+      long long vo = 0, to = 0;
+      for (uint32_t i = 0; i < gn; ++i) {
+        const Mesh& m = get_mesh(ctx, mesh_ids[g0 + i]);
+        cuda_check(cudaMemcpy(sm->verts.as<char>() + 24 * vo, m.verts.p, 24ull * m.nv,
+                              cudaMemcpyDeviceToDevice),
+                   "cudaMemcpy");
+        cuda_check(cudaMemcpy(tri.data() + 4 * to, m.tris.p, 16ull * m.nt,
+                              cudaMemcpyDeviceToHost),
+                   "cudaMemcpy");
+        for (long long k = 0; k < m.nt; ++k)
+          for (int j = 0; j < 3; ++j) tri[4 * (to + k) + j] += (uint32_t)vo;
+        vo += m.nv;
+        to += m.nt;
+        const b3d_pose& q = model_to_world[g0 + i];
+        grp.pose[i] = KPose{q.qw, q.qx, q.qy, q.qz, q.tx, q.ty, q.tz};
+      }
+      cuda_check(cudaMemcpy(sm->tris.p, tri.data(), 16ull * nt, cudaMemcpyHostToDevice),
                  "cudaMemcpy");
-      cuda_check(cudaMemcpy(tri.data() + 4 * to, m.tris.p, 16ull * m.nt, cudaMemcpyDeviceToHost),
-                 "cudaMemcpy");
-      for (long long k = 0; k < m.nt; ++k)
-        for (int j = 0; j < 3; ++j) tri[4 * (to + k) + j] += (uint32_t)vo;
-      vo += m.nv;
-      to += m.nt;
-      const b3d_pose& q = model_to_world[i];
-      ctx->cam_pose[i] = KPose{q.qw, q.qx, q.qy, q.qz, q.tx, q.ty, q.tz};
+      grp.mesh = std::move(sm);
+      draw += nt;
+      groups.push_back(std::move(grp));
     }
-    cuda_check(cudaMemcpy(sm->tris.p, tri.data(), 16ull * nt, cudaMemcpyHostToDevice),
-               "cudaMemcpy");
-    ctx->cam_mesh = std::move(sm);
-    ctx->cam_n = (int)n;
+    ctx->cam_groups = std::move(groups);
   });
 }
 
@@ -2102,11 +2230,11 @@ b3d_status b3d_gpu_render_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras,
   return guarded([&] {
     require_ready(ctx, false, false);
     check(cameras && depth && n > 0, "bad arguments");
-    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    require(!ctx->cam_groups.empty(), ErrorCode::invalid, "gpu context: camera scene not set");
     DeviceGuard dg(ctx->device);
-    const Mesh& m = *ctx->cam_mesh;
+    const Mesh& m = *ctx->cam_groups.front().mesh;
     KParams p = base_params(ctx, m);
-    cam_params(ctx, p);
+    cam_params(ctx, p, ctx->cam_groups.front());
     bool host_in = false;
     p.cams = static_cast<const KPose*>(
         stage_in(ctx, ctx->in_stage, cameras, sizeof(b3d_pose) * n, &host_in));
@@ -2129,7 +2257,19 @@ b3d_status b3d_gpu_render_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras,
         p.out_ids = ctx->out_stage2.as<int32_t>();
       }
     }
-    if (draw_index) {
+    if (ctx->cam_groups.size() > 1) {  // merged per-group renders
+      if (draw_index) {
+        ctx->cam_keys.ensure(8 * npx * n);
+        render_camera_groups(ctx, p.cams, (long long)n, nullptr,
+                             ctx->cam_keys.as<unsigned long long>());
+        cuda_check(launch_keys_to_depth_ids(ctx->cam_keys.as<unsigned long long>(), npx * n,
+                                            static_cast<float>(ctx->k.far_m), p.out_depth,
+                                            p.out_ids, ctx->stream),
+                   "keys_to_depth_ids launch");
+      } else {
+        render_camera_groups(ctx, p.cams, (long long)n, p.out_depth, nullptr);
+      }
+    } else if (draw_index) {
       LaunchPlan lp = plan_launch<true, false, true>(ctx, m, (long long)n);
       p.zscratch = ctx->zscratch.as<unsigned long long>();
       p.vscratch = ctx->vscratch.as<double>();
@@ -2166,7 +2306,7 @@ b3d_status b3d_gpu_score_cameras(b3d_gpu_context* ctx, const b3d_pose* cameras, 
   return guarded([&] {
     require_ready(ctx, true, true);
     check(cameras && scores && n > 0, "bad arguments");
-    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    require(!ctx->cam_groups.empty(), ErrorCode::invalid, "gpu context: camera scene not set");
     DeviceGuard dg(ctx->device);
     bool host_in = false;
     const KPose* cams = static_cast<const KPose*>(
@@ -2206,7 +2346,7 @@ b3d_status b3d_gpu_track_camera(b3d_gpu_context* ctx, const float* frames, uint3
     check(ctx && frames && initial && search && out_poses, "bad arguments");
     require(n_frames >= 1, ErrorCode::invalid, "track_camera: empty frame list");
     require_ready(ctx, false, true);
-    require(ctx->cam_mesh != nullptr, ErrorCode::invalid, "gpu context: camera scene not set");
+    require(!ctx->cam_groups.empty(), ErrorCode::invalid, "gpu context: camera scene not set");
     require(ctx->cam_spec_err.empty(), ErrorCode::invalid, ctx->cam_spec_err);
     require(ctx->cam_spec.n_cols == 1, ErrorCode::invalid, "track_camera: one noise setting");
     const b3d_track_search& s = *search;

@@ -168,6 +168,57 @@ cudaError_t launch_exact_score(const KExactArgs& a, int ctas, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+namespace {
+// per-pixel merges of renders of disjoint instance groups (camera scenes of
+// more than one launch's instances): the z-test's minimum; keys are
+// (depth bits << 32 | draw index), so a depth tie keeps the lower index
+__global__ void min_merge_f32_kernel(float* dst, const float* src, size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (src[i] < dst[i]) dst[i] = src[i];
+}
+__global__ void min_merge_u64_kernel(unsigned long long* dst, const unsigned long long* src,
+                                     size_t n) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x)
+    if (src[i] < dst[i]) dst[i] = src[i];
+}
+// render-many's output convention (render_score.cuh, kOut): far sentinel,
+// id -1 for the background
+__global__ void keys_to_depth_ids_kernel(const unsigned long long* keys, size_t n, float far_f,
+                                         float* depth, int32_t* ids) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const float z = __uint_as_float((unsigned int)(k >> 32));
+    depth[i] = z < far_f ? z : far_f;
+    if (ids) {
+      const unsigned int d = (unsigned int)(k & 0xffffffffull);
+      ids[i] = d == 0xffffffffu ? -1 : (int32_t)d;
+    }
+  }
+}
+unsigned grid_for(size_t n) {
+  const size_t b = (n + 255) / 256;
+  return (unsigned)(b < 4096 ? (b > 0 ? b : 1) : 4096);
+}
+}  // namespace
+
+cudaError_t launch_min_merge_f32(float* dst, const float* src, size_t n, cudaStream_t st) {
+  min_merge_f32_kernel<<<grid_for(n), 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_min_merge_u64(unsigned long long* dst, const unsigned long long* src,
+                                 size_t n, cudaStream_t st) {
+  min_merge_u64_kernel<<<grid_for(n), 256, 0, st>>>(dst, src, n);
+  return cudaGetLastError();
+}
+cudaError_t launch_keys_to_depth_ids(const unsigned long long* keys, size_t n, float far_f,
+                                     float* depth, int32_t* ids, cudaStream_t st) {
+  keys_to_depth_ids_kernel<<<grid_for(n), 256, 0, st>>>(keys, n, far_f, depth, ids);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fill_column(double* s, long long n, int ld, int col, double v,
                                cudaStream_t st) {
   const int blocks = (int)((n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024);

@@ -1211,3 +1211,73 @@ def test_adversarial_triangle_soup(gpu_ctx, oracle, seed):
     tris = np.array(tris, dtype=np.uint32)
     poses = np.array([[1.0, 0, 0, 0, 0, 0, 0], [1.0, 0, 0, 0, 0.01, -0.02, 0.3]])
     _render_parity(gpu_ctx, oracle, k, pts, tris, poses)
+
+
+def _crowded_scene(oracle, n_objects=23):
+    """Table + n_objects blobs on a grid: more instances than one camera-mode
+    launch holds (B3D_MAX_INSTANCES = 16)."""
+    seq = _orbit(oracle, 64, n_frames=3)
+    (tv, tt, tp) = seq["instances"][0]
+    inst = [(tv, tt, tp)]
+    for i in range(n_objects):
+        vox = synth.eden_blob(60 + 7 * i, 500 + i)
+        v, t = configs.make_mesh(vox, oracle.voxel_to_mesh)
+        lo, hi = v.min(axis=0), v.max(axis=0)
+        pose = oracle.contact_to_pose(0.5, 0.5, lo, hi, 1 + i % 6, 0.02 + 0.06 * (i % 6),
+                                      0.02 + 0.07 * (i // 6), (0.3 * i) % 6.0)
+        inst.append((v, t, pose))
+    return dict(seq, instances=inst)
+
+
+def test_camera_scene_beyond_one_launch(gpu_ctx, oracle):
+    """24 instances (table + 23 objects): per-group renders merged per pixel
+    -- depth and global draw indices bitwise equal to the oracle's
+    render_instances -- and scores through the fp64 image likelihood within
+    the tolerance; the same scene split below the limit gives the same renders."""
+    seq = _crowded_scene(oracle)
+    _camera_scene(gpu_ctx, seq)
+    rng = np.random.Generator(np.random.PCG64(31))
+    cams = [oracle.camera_pose_from_spherical(rng.uniform(0.4, 1.2), rng.uniform(0, 6.28),
+                                              rng.uniform(0.3, 1.3)) for _ in range(6)]
+    cams.append(oracle.camera_pose_from_spherical(0.1, 0.5, 0.3))  # near-plane clipping
+    cams = np.array(cams)
+    d, ids = gpu_ctx.render_cameras(cams)
+    d_only = gpu_ctx.render_cameras(cams, with_ids=False)[0]
+    for i, c in enumerate(cams):
+        od, oi = oracle.render(seq["k"], seq["instances"], camera=c, with_ids=True)
+        np.testing.assert_array_equal(d[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(d_only[i].view(np.uint32), od.view(np.uint32))
+        np.testing.assert_array_equal(ids[i], oi)
+    n_table = seq["instances"][0][1].shape[0]
+    assert (ids[:-1] > n_table + 16 * 40).any()  # pixels of the later groups' objects
+    obs = d[0].copy()
+    gpu_ctx.set_observation(obs)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    s_gpu, st = gpu_ctx.score_cameras(cams)
+    s_orc = np.array([oracle.windowed_loglik_multi(
+        obs, oracle.render(seq["k"], seq["instances"], camera=c), seq["k"], [seq["noise"]],
+        seq["sigma_max"], seq["window"])[0] for c in cams])
+    assert (st == 0).all()
+    assert rel_err(s_gpu[:, 0], s_orc).max() <= SCORE_RTOL
+
+
+def test_track_camera_crowded_scene(gpu_ctx, oracle):
+    """track_camera over the 24-instance scene (merged group renders, fp64
+    image likelihood) picks the oracle's lattice points (a differing pick
+    must tie within the score tolerance)."""
+    seq = _crowded_scene(oracle)
+    _camera_scene(gpu_ctx, seq)
+    gpu_ctx.set_likelihood([seq["noise"]], seq["sigma_max"], seq["window"])
+    cams = [oracle.camera_pose_from_spherical(seq["distance"], a, seq["altitude"])
+            for a in seq["azimuths"][:3]]
+    frames = np.stack([oracle.render(seq["k"], seq["instances"], camera=c) for c in cams])
+    est, ms = gpu_ctx.track_camera(frames, cams[0])
+    log = []
+    ref = oracle.track_camera(frames, seq["k"], seq["instances"], cams[0], seq["noise"],
+                              seq["sigma_max"], seq["window"], stage_log=log)
+    assert len(cams) == 3
+    for f in range(len(cams)):
+        if not np.array_equal(est[f], ref[f]):
+            _, _, grid, scores = [e for e in log if e[0] == f][-1]
+            s = np.array(scores)
+            assert np.sort(s)[-1] - np.sort(s)[-2] <= SCORE_RTOL * abs(np.max(s))
