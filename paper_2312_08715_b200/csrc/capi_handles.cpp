@@ -192,7 +192,6 @@ std::shared_ptr<b3d_object_model> load_svox(const std::string& path, int id) {  
   return model_from_grid(id, res, origin, std::move(vox));
 }
 
-// ConfigReader (config.cpp): strict object view, unknown keys are errors
 // nlohmann's number -> int / uint32_t conversions as the reference's build
 // performs them (static_cast under gcc on x86-64): integers wrap modulo
 // 2^32; a float truncates toward zero, out of range giving INT_MIN (int,
@@ -217,6 +216,7 @@ uint32_t json_u32(const J::Value& x) {
 // get_arithmetic_value, numbers only
 bool is_arith(const J::Value& x) { return x.kind == J::Value::Number || x.kind == J::Value::Bool; }
 
+// ConfigReader (config.cpp): strict object view, unknown keys are errors
 struct Reader {
   const J::Value& v;
   std::string ctx;
