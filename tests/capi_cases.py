@@ -234,6 +234,29 @@ def run_cases(L, gpu: bool):
             L.b3d_particles_destroy(part)
             out[name] = [0, res]
         L.b3d_depth_image_destroy(seen)
+    # io.cpp:60-102 / 118-130: saved bytes (golden layout), atomic writes that
+    # leave nothing behind when the target directory is missing
+    L.b3d_depth_image_save.argtypes = [vp, C.c_char_p]
+    L.b3d_model_save.argtypes = [vp, C.c_char_p]
+    L.b3d_model_load.argtypes = [C.c_char_p, C.c_int, C.POINTER(vp)]
+    L.b3d_model_destroy.argtypes = [vp]
+    for name, fn in (("depth_save", lambda p: L.b3d_depth_image_save(obs, p)),):
+        good = os.path.join(tmp, "saved.sdpt")
+        st = fn(good.encode())
+        out[name] = [st, hashlib.sha256(open(good, "rb").read()).hexdigest() if st == 0 else
+                     L.b3d_last_error().decode()]
+        bad = os.path.join(tmp, "no_such_dir", "x.sdpt")
+        out[name + "_bad_dir"] = _res(L, fn(bad.encode()))
+        out[name + "_bad_dir_leftovers"] = [0, str(sorted(os.listdir(tmp)))]
+    mh = vp()
+    assert L.b3d_model_load(os.path.join(tmp, "a.svox").encode(), 4, C.byref(mh)) == 0
+    good = os.path.join(tmp, "saved.svox")
+    st = L.b3d_model_save(mh, good.encode())
+    out["model_save"] = [st, hashlib.sha256(open(good, "rb").read()).hexdigest() if st == 0
+                         else L.b3d_last_error().decode()]
+    out["model_save_bad_dir"] = _res(L, L.b3d_model_save(
+        mh, os.path.join(tmp, "no_such_dir", "m.svox").encode()))
+    L.b3d_model_destroy(mh)
     # b3d_infer config schema (b3d_capi.cpp:297-379)
     kk = {"fx": 60.0, "fy": 60.0, "cx": 31.5, "cy": 23.5, "width": 64, "height": 48,
           "near": 0.05, "far": 4.0}
