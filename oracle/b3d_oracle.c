@@ -969,6 +969,8 @@ typedef struct score_job {
   const orc_intrinsics* k;
   orc_pose w2c;
   obs_cache oc;
+  double* obs_pts; /* window < 0: the observed cloud (depth_to_cloud) */
+  size_t n_obs;
   const float* base;
   const double* verts;
   uint64_t nv;
@@ -998,6 +1000,26 @@ static void score_one(score_job* J, size_t i, float* img, orc_counters* c) {
   orc_pose m2c;
   orc_compose(&J->w2c, &J->poses[i], &m2c);
   orc_raster_mesh(img, 0, J->k, J->verts, J->nv, J->tris, J->nt, &m2c, 0, c);
+  if (J->window < 0) {
+    /* ModelConfig::windowed = false: observation_loglik_cached
+       (inference.cpp:40-56) per entry -- -inf outside the noise support,
+       the full likelihood of the two clouds otherwise; an empty render is
+       flagged like the windowed path's */
+    double* rp = (double*)malloc(npx * 3 * sizeof(double));
+    size_t nr = 0;
+    orc_depth_to_cloud(img, J->k, rp, &nr);
+    J->status[i] = (uint8_t)(nr == 0);
+    for (size_t e = 0; e < J->n_noise; ++e) {
+      double v = -INFINITY;
+      if (nr > 0 && noise_ok(&J->noise[e], J->sigma_max) &&
+          orc_full_loglik_points(J->obs_pts, J->n_obs, rp, nr, &J->noise[e], J->volume,
+                                 J->sigma_max, J->prefactor, &v) != 0)
+        v = -INFINITY;
+      J->scores[i * J->n_noise + e] = v;
+    }
+    free(rp);
+    return;
+  }
   const int rc =
       windowed_loglik_cached(&J->oc, img, J->k, J->noise, J->n_noise, J->volume,
                              J->sigma_max, J->window, J->prefactor,
@@ -1043,6 +1065,10 @@ int orc_score_poses(const orc_intrinsics* k, const orc_pose* camera, const float
   J.k = k;
   orc_inverse(camera, &J.w2c);
   obs_cache_build(&J.oc, obs, k); /* once per observation (inference.cpp:158) */
+  if (window < 0) {
+    J.obs_pts = (double*)malloc((size_t)k->width * k->height * 3 * sizeof(double));
+    orc_depth_to_cloud(obs, k, J.obs_pts, &J.n_obs);
+  }
   J.base = base;
   J.verts = verts;
   J.nv = nv;
@@ -1068,6 +1094,7 @@ int orc_score_poses(const orc_intrinsics* k, const orc_pose* camera, const float
   free(th);
   pthread_mutex_destroy(&J.mu);
   obs_cache_free(&J.oc);
+  free(J.obs_pts);
   if (counters) *counters = J.cnt;
   return 0;
 }

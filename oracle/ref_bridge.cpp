@@ -264,8 +264,9 @@ REFB_API int refb_score_poses(const RefIntr* k, const float* obs, const double* 
       b3d::DepthImage img = base;
       b3d::raster_mesh(img, kk, mesh, b3d::compose(world_to_camera, pose_in(poses + 7 * h)));
       status[h] = 0;
-      if (window < 0) {
+      if (window < 0) {  // observation_loglik_cached: an empty render scores -inf
         const b3d::PointCloud rc = b3d::depth_to_cloud(img, kk);
+        status[h] = rc.points.empty() ? 1 : 0;  // flagged like the windowed path
         for (int e = 0; e < n_noise; ++e)
           out[h * n_noise + e] = rc.points.empty()
               ? -INFINITY

@@ -244,11 +244,12 @@ needs_ref = pytest.mark.skipif(
 @needs_ref
 def test_oracle_equals_reference_random_cases(oracle):
     """Fresh random cases, oracle vs the reference library, bitwise: poses
-    straddling the near plane, random meshes, windows 0..4, multi-noise."""
+    straddling the near plane, random meshes, windows 0..4 and the
+    untruncated likelihood (window < 0), multi-noise."""
     from oracle import pyref as R
     rng = np.random.Generator(np.random.PCG64(2024))
     k = configs.Intr(120.0, 110.0, 40.5, 30.25, 80, 60, 0.05, 3.0)
-    for trial in range(6):
+    for trial in range(7):
         vox = synth.random_walk_blob(int(rng.integers(20, 200)), int(rng.integers(0, 1000)))
         org = synth.centered_origin(vox, 0.01)
         v, t = oracle.voxel_to_mesh(vox, 0.01, org)
@@ -263,7 +264,7 @@ def test_oracle_equals_reference_random_cases(oracle):
         for p in poses:
             _eq(oracle.render(k, [(v, t, p)]), R.render(k, [(v, t, p)]))
         noise = [(0.01, 0.01), (0.3, 0.01), (0.1, 0.04)]
-        wi = trial % 5
+        wi = trial % 5 if trial < 6 else -1
         so, sto = oracle.score_poses(k, obs, v, t, poses, noise, 0.1, wi)
         sr, str_ = R.score_poses(k, obs, v, t, poses, noise, 0.1, wi)
         np.testing.assert_array_equal(sto, str_)
