@@ -83,3 +83,64 @@ def test_score_sweep(gpu_ctx, oracle, case):
     scale = w * h * 60.0  # |log-term| per observed pixel is bounded by ~60
     assert rel.max(initial=0) <= RTOL, (case, rel.max())
     assert d.max(initial=0) <= RTOL * scale, (case, d.max())
+
+
+def test_stage_draw_sweep(gpu_ctx, oracle):
+    """300 random stages: flat, two-level, peaked and sparse (-inf) score
+    arrays of 1 to 70,000 entries, each drawn with its own seed -- argmax,
+    the categorical draw and the advanced Rng state equal the oracle's
+    (sample_categorical's sequential CDF, inference.cpp:345-353)."""
+    rng = np.random.Generator(np.random.PCG64(77))
+    for t in range(300):
+        n = int(rng.choice([1, 2, 3, 10, 97, 1024, 4097, 16384, 16385, 70000]))
+        kind = t % 4
+        if kind == 0:
+            x = np.full(n, -3.25)
+        elif kind == 1:
+            x = np.where(rng.random(n) < 0.5, 0.0, -np.log(3.0))
+        elif kind == 2:
+            x = rng.normal(0.0, 40.0, n)
+        else:
+            x = np.where(rng.random(n) < 0.9, -np.inf, rng.normal(0.0, 1.0, n))
+            x[int(rng.integers(0, n))] = 0.0
+        st_g = b3d.rng_seed(900 + t)
+        st_o = oracle.rng_seed(900 + t)
+        r = gpu_ctx.stage_reduce(x, rng_state=st_g)
+        probs_o, _ = oracle.normalize(x)
+        assert r.argmax == oracle.argmax(x), t
+        assert r.sample == oracle.sample_categorical(probs_o, st_o), (t, n, kind)
+        np.testing.assert_array_equal(st_g, st_o)
+
+
+def test_stage_draw_on_cdf_boundaries(gpu_ctx, oracle):
+    """Draws placed on a CDF boundary on purpose: the stage's uniform u is
+    known from its seed, and the scores put the running sum at index j to
+    within an ulp of u -- the parallel CDF must hand these to the sequential
+    fallback (the reference's index-order total and running sum) and agree
+    with the oracle's pick and Rng state -- except where the device's exp and
+    the host libm's differ in the last ulp and u sits within those ulps of
+    the boundary: then the pick is the neighbouring index."""
+    fallbacks = ulp_band = 0
+    for seed in range(40):
+        st = oracle.rng_seed(5000 + seed)
+        u = oracle.rng_uniform(st.copy())
+        n = 2 + seed % 7
+        j = seed % (n - 1)
+        # probabilities: j + 1 entries summing to u, the rest to 1 - u
+        p = np.concatenate([np.full(j + 1, u / (j + 1)), np.full(n - j - 1, (1 - u) / (n - j - 1))])
+        x = np.log(p) + (seed % 5) * 3.0
+        st_g, st_o = b3d.rng_seed(5000 + seed), oracle.rng_seed(5000 + seed)
+        r = gpu_ctx.stage_reduce(x, rng_state=st_g)
+        probs_o, _ = oracle.normalize(x)
+        pick = oracle.sample_categorical(probs_o, st_o)
+        np.testing.assert_array_equal(st_g, st_o)
+        fallbacks += int(r.sample_fallback)
+        if r.sample != pick:
+            acc = 0.0
+            for i in range(min(r.sample, pick) + 1):
+                acc += probs_o[i]
+            assert r.sample_fallback and abs(r.sample - pick) == 1, seed
+            assert abs(acc - u) <= 4 * np.spacing(u), (seed, acc, u)
+            ulp_band += 1
+    assert fallbacks >= 30  # the boundary cases took the sequential path
+    assert ulp_band <= 8
