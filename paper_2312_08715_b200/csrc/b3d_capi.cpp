@@ -85,8 +85,9 @@ cudaError_t launch_image_loglik(const float* obs, const float* rend, int W, int 
                                 double fx, double fy, double cx, double cy, float far_f,
                                 double p_outlier, double sigma, double sigma_max,
                                 double volume, int window, int prefactor,
-                                unsigned long long* d_acc, double* d_out, int* d_count,
+                                double* d_partial, double* d_out, int* d_count,
                                 cudaStream_t st);
+int image_loglik_partials(int n);
 
 // ------------------------------------------------------------------ errors
 enum class ErrorCode { invalid = 1, config = 2, io = 3, numeric = 4 };
@@ -1629,6 +1630,37 @@ const float* b3d_depth_image_data(const b3d_depth_image* img) {
 }
 void b3d_depth_image_destroy(b3d_depth_image* img) { delete img; }
 
+}  // extern "C"
+namespace {
+struct LoglikScratch {
+  int device = -1;
+  cudaStream_t st = nullptr;
+  DevBuf img, res;
+  PinnedBuf pin;
+  ~LoglikScratch() {
+    if (st) cudaStreamDestroy(st);  // thread exit: errors at teardown are moot
+  }
+};
+LoglikScratch& loglik_scratch() {
+  thread_local LoglikScratch s;
+  int dev = 0;
+  cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+  if (s.device != dev) {  // first use on this thread, or the device changed
+    if (s.st) cudaStreamDestroy(s.st);
+    s.st = nullptr;
+    for (DevBuf* b : {&s.img, &s.res}) {
+      if (b->p) cudaFree(b->p);
+      b->p = nullptr;
+      b->bytes = 0;
+    }
+    cuda_check(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking), "cudaStreamCreate");
+    s.device = dev;
+  }
+  return s;
+}
+}  // namespace
+extern "C" {
+
 b3d_status b3d_log_likelihood(const b3d_depth_image* observed, const b3d_depth_image* rendered,
                               const b3d_intrinsics* k, double p_outlier, double sigma_noise,
                               double sigma_max, int window, double* out) {
@@ -1660,30 +1692,36 @@ b3d_status b3d_log_likelihood(const b3d_depth_image* observed, const b3d_depth_i
       validate_noise();
       require(rend_valid > 0, ErrorCode::invalid, "full_log_likelihood: empty rendered cloud");
     }
-    int dev = 0;
-    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    // the calling thread's device state, kept across calls: buffers that
+    // only grow, page-locked staging, a private stream (one copy in, one
+    // launch, one copy out, one synchronisation per call)
+    LoglikScratch& s = loglik_scratch();
     const size_t npx = (size_t)k->width * k->height;
-    DevBuf d_obs, d_rend, d_acc, d_out, d_cnt;
-    d_obs.ensure(npx * 4);
-    d_rend.ensure(npx * 4);
-    d_acc.ensure(16);
-    d_out.ensure(8);
-    d_cnt.ensure(8);
-    cuda_check(cudaMemcpy(d_obs.p, observed->depth.data(), npx * 4, cudaMemcpyHostToDevice),
-               "cudaMemcpy");
-    cuda_check(cudaMemcpy(d_rend.p, rendered->depth.data(), npx * 4, cudaMemcpyHostToDevice),
-               "cudaMemcpy");
-    cuda_check(launch_image_loglik(d_obs.as<float>(), d_rend.as<float>(), (int)k->width,
+    s.img.ensure(npx * 8);
+    s.res.ensure(32 + 8 * (size_t)image_loglik_partials((int)npx));
+    s.pin.ensure(npx * 8 + 32);
+    float* h_img = s.pin.as<float>();
+    std::memcpy(h_img, observed->depth.data(), npx * 4);
+    std::memcpy(h_img + npx, rendered->depth.data(), npx * 4);
+    cuda_check(cudaMemcpyAsync(s.img.p, h_img, npx * 8, cudaMemcpyHostToDevice, s.st),
+               "cudaMemcpyAsync");
+    char* d_res = s.res.as<char>();
+    cuda_check(launch_image_loglik(s.img.as<float>(), s.img.as<float>() + npx, (int)k->width,
                                    (int)k->height, k->fx, k->fy, k->cx, k->cy,
                                    static_cast<float>(k->far_m), p_outlier, sigma_noise,
                                    sigma_max, visible_volume(*k), window, 0,
-                                   d_acc.as<unsigned long long>(), d_out.as<double>(),
-                                   d_cnt.as<int>(), nullptr),
+                                   reinterpret_cast<double*>(d_res + 32),
+                                   reinterpret_cast<double*>(d_res + 16),
+                                   reinterpret_cast<int*>(d_res + 24), s.st),
                "image_loglik launch");
-    int cnt = 0;
+    char* h_res = s.pin.as<char>() + npx * 8;
+    cuda_check(cudaMemcpyAsync(h_res, d_res + 16, 16, cudaMemcpyDeviceToHost, s.st),
+               "cudaMemcpyAsync");
+    cuda_check(cudaStreamSynchronize(s.st), "b3d_log_likelihood");
     double v = 0;
-    cuda_check(cudaMemcpy(&cnt, d_cnt.p, 4, cudaMemcpyDeviceToHost), "cudaMemcpy");
-    cuda_check(cudaMemcpy(&v, d_out.p, 8, cudaMemcpyDeviceToHost), "cudaMemcpy");
+    int cnt = 0;
+    std::memcpy(&v, h_res, 8);
+    std::memcpy(&cnt, h_res + 8, 4);
     if (window >= 0)
       require(cnt > 0, ErrorCode::invalid, "windowed likelihood: empty rendered cloud");
     else

@@ -289,6 +289,9 @@ struct Gpu {
   b3d_gpu_context* ctx = nullptr;
   std::map<uint64_t, int32_t> meshes;
   std::map<std::tuple<double, double, double>, int32_t> tables;
+  // what the context holds now (b3d_render reuses it call after call); any
+  // other setter of the camera clears cam_key
+  std::string cam_key, scene_key;
   ~Gpu() {
     if (ctx) b3d_gpu_context_destroy(ctx);
   }
@@ -306,6 +309,24 @@ struct Gpu {
     ok(b3d_gpu_upload_mesh(get(), m.verts.data(), m.verts.size() / 3, m.tris.data(),
                            m.tris.size() / 3, &id));
     return meshes[m.serial] = id;
+  }
+  template <class T>
+  static std::string bytes(const T* p, size_t n) {
+    return std::string(reinterpret_cast<const char*>(p), sizeof(T) * n);
+  }
+  void camera(const b3d_intrinsics* k) {  // intrinsics only (camera-mode renders)
+    const std::string key = bytes(k, 1);
+    if (key == cam_key) return;
+    cam_key.clear();
+    ok(b3d_gpu_set_camera(get(), k, nullptr));
+    cam_key = key;
+  }
+  void camera_scene(const std::vector<int32_t>& ids, const std::vector<b3d_pose>& poses) {
+    const std::string key = bytes(ids.data(), ids.size()) + bytes(poses.data(), poses.size());
+    if (key == scene_key) return;
+    scene_key.clear();
+    ok(b3d_gpu_set_camera_scene(get(), ids.data(), poses.data(), (uint32_t)ids.size()));
+    scene_key = key;
   }
   int32_t table(double w, double h, double thickness) {  // ObjectModel::table
     const auto key = std::make_tuple(w, h, thickness);
@@ -618,10 +639,11 @@ b3d_status b3d_render(const b3d_scene* scene, const b3d_pose* camera, const b3d_
     for (const auto& c : scene->children) ids.push_back(g_gpu.mesh(*c.obj));
     std::vector<float> depth((size_t)k->width * k->height);
     if (ids.size() <= B3D_MAX_INSTANCES) {  // camera mode: one launch
-      ok(b3d_gpu_set_camera(g, k, nullptr));
-      ok(b3d_gpu_set_camera_scene(g, ids.data(), poses.data(), (uint32_t)ids.size()));
+      g_gpu.camera(k);  // both kept from the previous call when unchanged
+      g_gpu.camera_scene(ids, poses);
       ok(b3d_gpu_render_cameras(g, &cam, 1, depth.data(), nullptr));
     } else {  // any number of children: instance after instance
+      g_gpu.cam_key.clear();  // sets the camera itself
       b3d200_render_scene_keys(g, k, &cam, ids.data(), poses.data(), (uint32_t)ids.size(),
                                depth.data());
     }
@@ -734,6 +756,7 @@ b3d_status b3d_infer(const b3d_depth_image* observed, const b3d_pose* camera,
     cfg.n_objects = (uint32_t)n_objects;
     cfg.n_particles = (uint32_t)n_particles;
     b3d_gpu_context* g = g_gpu.get();
+    g_gpu.cam_key.clear();
     ok(b3d_gpu_set_camera(g, &ik, &cam));
     ok(b3d_gpu_set_observation(g, b3d_depth_image_data(observed)));
     std::vector<b3d_smc_object> objs;

@@ -101,24 +101,18 @@ cudaError_t launch_image_loglik(const float* obs, const float* rend, int W, int 
                                 double fy, double cx, double cy, float far_f,
                                 double p_outlier, double sigma, double sigma_max,
                                 double volume, int window, int prefactor,
-                                unsigned long long* d_scratch, double* d_out, int* d_count,
+                                double* d_partial, double* d_out, int* d_count,
                                 cudaStream_t st) {
-  (void)d_scratch;
+  // asynchronous: the caller checked for an empty render on the host (the
+  // reference's error) and reads d_out / d_count after its one sync;
+  // d_partial holds image_loglik_partials(W * H) doubles
   const int n = W * H;
   cudaError_t e = cudaMemsetAsync(d_count, 0, sizeof(int), st);
   if (e != cudaSuccess) return e;
   int nb = (n + kB - 1) / kB;
   if (nb > kMaxBlocks) nb = kMaxBlocks;
   count_kernel<<<nb, kB, 0, st>>>(rend, n, far_f, d_count);
-  int cnt = 0;
-  e = cudaMemcpyAsync(&cnt, d_count, sizeof(int), cudaMemcpyDeviceToHost, st);
-  if (e != cudaSuccess) return e;
-  e = cudaStreamSynchronize(st);
-  if (e != cudaSuccess) return e;
-  if (cnt == 0) return cudaSuccess;  // caller raises the reference's error
-  double* partial = nullptr;
-  e = cudaMallocAsync(&partial, sizeof(double) * nb, st);
-  if (e != cudaSuccess) return e;
+  double* partial = d_partial;
   ImgArgs a;
   a.obs = obs;
   a.rend = rend;
@@ -138,9 +132,12 @@ cudaError_t launch_image_loglik(const float* obs, const float* rend, int W, int 
   a.window = window;
   terms_kernel<<<nb, kB, 0, st>>>(a, d_count, partial);
   final_kernel<<<1, 32, 0, st>>>(partial, nb, a.prefactor, d_out);
-  e = cudaFreeAsync(partial, st);
-  if (e != cudaSuccess) return e;
   return cudaGetLastError();
+}
+
+int image_loglik_partials(int n) {
+  const int nb = (n + kB - 1) / kB;
+  return nb > kMaxBlocks ? kMaxBlocks : nb;
 }
 
 }  // namespace b3d200
