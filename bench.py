@@ -931,6 +931,11 @@ def main():
     torch.cuda.synchronize()
     clocks.start()
     time.sleep(0.3)
+    # the device idles ~20 ms first (outside every event) while the host
+    # queues all the timed steps, so a host-side stall (an nvidia-smi sample
+    # holding the driver, a context switch) cannot open a gap between a
+    # step's start event and its kernels: the events time device work only
+    torch.cuda._sleep(40_000_000)
     for i in range(args.steps):
         flush.fill_(float(i))  # L2 flush between timed steps (outside the events)
         e0, ek, e1 = evs[i]
@@ -946,6 +951,7 @@ def main():
     kern_ms = []
     for i in range(10):
         flush.fill_(float(i))
+        torch.cuda._sleep(2_000_000)  # the launch is queued before the device gets to it
         ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ka.record(stream)
         ctx.score_grid(mid, grid, d_scores, d_status)
