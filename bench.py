@@ -47,7 +47,8 @@ def _ncu_traffic():
     files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_render_score_details.txt")),
                    key=lambda f: (len(os.path.basename(f)), os.path.basename(f)))
     # round 2 on: one capture per leg, the cfg1 one is the headline kernel's
-    files += sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9]_cfg1_score_details.txt")))
+    files += sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9]*_cfg1_score_details.txt")),
+                    key=lambda f: (len(os.path.basename(f)), os.path.basename(f)))
     if not files:
         return None
     text = open(files[-1]).read()
