@@ -289,8 +289,12 @@ def _ptr(a) -> int:
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
     if isinstance(a, np.ndarray):
-        if not a.flags["C_CONTIGUOUS"]:
+        if not a.flags.c_contiguous:
             raise ValueError("arrays must be C-contiguous")
+        if a.flags.writeable and a.size:
+            # ~0.4 us instead of ~1.3 us for a.ctypes.data (a per-call cost on
+            # the end-to-end path, four pointers per stage)
+            return C.addressof(C.c_char.from_buffer(a))
         return a.ctypes.data
     raise TypeError(f"unsupported buffer type {type(a)}")
 
