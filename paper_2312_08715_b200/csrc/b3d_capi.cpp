@@ -602,14 +602,19 @@ LaunchPlan plan_launch(b3d_gpu_context* ctx, const Mesh& m, long long n, int win
     return e ? std::atoi(e) : 2;
   }();
   static const bool no_vcache = std::getenv("B3D_PLAN_VCAP0") != nullptr;  // A/B only
-  for (int b = 2; b >= min_b; --b) {
+  static const int max_b = [] {
+    const char* e = std::getenv("B3D_PLAN_MAXB");  // A/B only: plan for up to N CTAs/SM
+    const int v = e ? std::atoi(e) : 2;
+    return v >= 2 && v <= 8 ? v : 2;
+  }();
+  for (int b = max_b; b >= min_b; --b) {
     budget = budget_for(b);
     if (!no_vcache && vbytes + stage + zmin <= budget) {
       lp.vcap = m.nv;
       break;
     }
   }
-  if (lp.vcap == 0) budget = budget_for(2);
+  if (lp.vcap == 0) budget = budget_for(max_b);
   if (full_frame && (budget - 32ull * lp.vcap - stage) / key < padded) {
     if (vbytes + stage + padded * key <= budget_for(1)) {
       budget = budget_for(1);

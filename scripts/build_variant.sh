@@ -15,5 +15,5 @@ grep -h "spill" $T/rs_score_w1.log | head -1
 O=build/obj
 mkdir -p _ab
 /usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -cudart static -o _ab/lib_$NAME.so \
-  $T/*.o $O/stage.cu.o $O/image_score.cu.o $O/mesh_build.cu.o $O/track.cu.o $O/b3d_capi.cpp.o $O/smc.cpp.o $O/capi_handles.cpp.o -Xlinker --no-undefined -lpthread -ldl -lrt || cat $T/*.log
+  $T/*.o $O/stage.cu.o $O/image_score.cu.o $O/exact_score.cu.o $O/exchange.cu.o $O/mesh_build.cu.o $O/track.cu.o $O/b3d_capi.cpp.o $O/smc.cpp.o $O/capi_handles.cpp.o -Xlinker --no-undefined -lpthread -ldl -lrt || cat $T/*.log
 rm -rf $T
