@@ -95,3 +95,21 @@ def test_box_mesh_and_contact_to_pose_match_oracle_bitwise():
                                           O.contact_to_pose(0.5, 0.5, amin, amax, face, dx, dy, th))
     with pytest.raises(b3d.B3DError):
         b3d.contact_to_pose(0.5, 0.5, amin, amax, 1, 0.49, 0.1, 0.0)
+
+
+def test_buffer_pointers_match_numpy():
+    """b3d._ptr (the wrapper's per-call pointer path) returns the array's data
+    address for writable, read-only, sliced, empty and non-float arrays."""
+    a = np.arange(12.0).reshape(3, 4)
+    assert b3d._ptr(a) == a.ctypes.data
+    assert b3d._ptr(a[1:]) == a[1:].ctypes.data
+    r = np.zeros(4, dtype=np.uint64)
+    r.flags.writeable = False
+    assert b3d._ptr(r) == r.ctypes.data
+    e = np.zeros(0)
+    assert b3d._ptr(e) == e.ctypes.data
+    u8 = np.zeros(5, dtype=np.uint8)
+    assert b3d._ptr(u8) == u8.ctypes.data
+    assert b3d._ptr(None) is None
+    with pytest.raises(ValueError):
+        b3d._ptr(a[:, ::2])
