@@ -337,6 +337,24 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
+#ifndef B3D_EX2_FTZ
+#define B3D_EX2_FTZ 1
+#endif
+// One window tap's exp2.  exp2f keeps subnormal results (a compare and two
+// predicated multiplies around MUFU.EX2 per tap); a tap below 2^-126 adds
+// nothing an fp32 window sum or the log(floor + coef*S) term can register
+// (the fp64 image path takes the settings where the floor vanishes, §5.5),
+// so the flush-to-zero form is one instruction.
+__device__ __forceinline__ float ex2_tap(float x) {
+#if B3D_EX2_FTZ
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+#else
+  return exp2f(x);
+#endif
+}
+
 // sum over the (2w+1)^2 window of exp(-|o - r|^2 / (2 sigma^2)) per distinct
 // sigma (likelihood.cpp:198-214) in fp32: rendered points back-projected on
 // the fly from the region buffer, exp as ex2 with the scale pre-multiplied
@@ -366,7 +384,7 @@ __device__ __forceinline__ void window_sums_w(const KParams& p,
       const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
 #pragma unroll
       for (int s = 0; s < (kS1 ? 1 : kMaxSlots); ++s)
-        if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+        if (kS1 || s < p.lik.n_slots) S[s] += ex2_tap(-d2 * p.lik.slot_scale[s]);
     }
   }
 }
@@ -392,7 +410,7 @@ __device__ __forceinline__ void window_sums_any(const KParams& p,
       const float d2 = __fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz));
 #pragma unroll
       for (int s = 0; s < (kS1 ? 1 : kMaxSlots); ++s)
-        if (kS1 || s < p.lik.n_slots) S[s] += exp2f(-d2 * p.lik.slot_scale[s]);
+        if (kS1 || s < p.lik.n_slots) S[s] += ex2_tap(-d2 * p.lik.slot_scale[s]);
     }
   }
 }
