@@ -801,8 +801,10 @@ KLik make_lik(const b3d_intrinsics& k, const b3d_noise* noise, uint32_t n_noise,
     L.slot_of[e] = (int)s;
   }
   L.n_slots = (int)slots.size();
-  for (size_t s = 0; s < slots.size(); ++s)
+  for (size_t s = 0; s < slots.size(); ++s) {
     L.slot_scale[s] = (float)(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
+    L.slot_root[s] = (float)std::sqrt(1.4426950408889634 / (2.0 * slots[s] * slots[s]));
+  }
   return L;
 }
 

@@ -55,6 +55,7 @@ struct KLik {
   int window;
   int slot_of[kMaxNoise];
   float slot_scale[kMaxSlots];   // log2(e)/(2 sigma^2) per distinct sigma (exp2 form)
+  float slot_root[kMaxSlots];    // sqrt(slot_scale): single-sigma taps scale the points
   double one_minus_p[kMaxNoise]; // 1 - p_outlier
   double norm3[kMaxNoise];       // pow(2 pi sigma^2, -1.5)
   double floor_term[kMaxNoise];  // p_outlier / V

@@ -337,6 +337,9 @@ __device__ __forceinline__ int warp_sum_i(int v) {
   return v;
 }
 
+#ifndef B3D_TAP_ROOT
+#define B3D_TAP_ROOT 1
+#endif
 #ifndef B3D_EX2_FTZ
 #define B3D_EX2_FTZ 1
 #endif
@@ -369,6 +372,31 @@ __device__ __forceinline__ void window_sums_w(const KParams& p,
   const float cu0 = ((float)(u - kW) - p.fcx) * p.inv_fx;
   const float cv0 = ((float)(v - kW) - p.fcy) * p.inv_fy;
   const typename KeyT<kIds>::T* row0 = zb + (v - kW - rg.oy) * rg.rw + (u - kW - rg.ox);
+#if B3D_TAP_ROOT
+  if constexpr (kS1) {
+    // one sigma: scale both points by k = sqrt(log2(e)/(2 sigma^2)) so a tap
+    // is three FFMAs, the squared norm and one ex2 (no dz subtraction and no
+    // scale multiply per tap); the base-image sums use the same form
+    const float k = p.lik.slot_root[0];
+    const float kox = k * o.x, koy = k * o.y, koz = k * o.z;
+#pragma unroll
+    for (int j = 0; j < 2 * kW + 1; ++j) {
+      const float kcv = k * (cv0 + (float)j * p.inv_fy);
+#pragma unroll
+      for (int c = 0; c < 2 * kW + 1; ++c) {
+        const typename KeyT<kIds>::T key = row0[j * rg.rw + c];
+        const float z = __uint_as_float(
+            kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+        const float kcu = k * (cu0 + (float)c * p.inv_fx);
+        const float dx = __fmaf_rn(-kcu, z, kox);
+        const float dy = __fmaf_rn(-kcv, z, koy);
+        const float dz = __fmaf_rn(-k, z, koz);
+        S[0] += ex2_tap(-__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz)));
+      }
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < 2 * kW + 1; ++j) {
     const float cv = cv0 + (float)j * p.inv_fy;
@@ -397,6 +425,26 @@ __device__ __forceinline__ void window_sums_any(const KParams& p,
 #pragma unroll
   for (int s = 0; s < kMaxSlots; ++s) S[s] = 0.f;
   const int w = p.lik.window;
+#if B3D_TAP_ROOT
+  if constexpr (kS1) {  // the single-sigma form of window_sums_w
+    const float k = p.lik.slot_root[0];
+    const float kox = k * o.x, koy = k * o.y, koz = k * o.z;
+    for (int rv = v - w; rv <= v + w; ++rv) {
+      const float kcv = k * (((float)rv - p.fcy) * p.inv_fy);
+      for (int ru = u - w; ru <= u + w; ++ru) {
+        const typename KeyT<kIds>::T key = zb[(rv - rg.oy) * rg.rw + (ru - rg.ox)];
+        const float z = __uint_as_float(
+            kIds ? (unsigned int)((unsigned long long)key >> 32) : (unsigned int)key);
+        const float kcu = k * (((float)ru - p.fcx) * p.inv_fx);
+        const float dx = __fmaf_rn(-kcu, z, kox);
+        const float dy = __fmaf_rn(-kcv, z, koy);
+        const float dz = __fmaf_rn(-k, z, koz);
+        S[0] += ex2_tap(-__fmaf_rn(dx, dx, __fmaf_rn(dy, dy, dz * dz)));
+      }
+    }
+    return;
+  }
+#endif
   for (int rv = v - w; rv <= v + w; ++rv) {
     const float cv = ((float)rv - p.fcy) * p.inv_fy;
     for (int ru = u - w; ru <= u + w; ++ru) {
@@ -432,6 +480,18 @@ template <bool kIds>
 __device__ __forceinline__ void window_sums_rt(const KParams& p, const typename KeyT<kIds>::T* zb,
                                                const Region& rg, int u, int v, float4 o,
                                                float S[kMaxSlots]) {
+  // the score kernels take their single-sigma form when n_noise == 1
+  // (pick_kernel): the same taps here, so S and S_base agree bitwise
+  if (p.lik.n_noise == 1) {
+    switch (p.lik.window) {
+      case 0: window_sums_w<kIds, 0, true>(p, zb, rg, u, v, o, S); break;
+      case 1: window_sums_w<kIds, 1, true>(p, zb, rg, u, v, o, S); break;
+      case 2: window_sums_w<kIds, 2, true>(p, zb, rg, u, v, o, S); break;
+      case 3: window_sums_w<kIds, 3, true>(p, zb, rg, u, v, o, S); break;
+      default: window_sums_any<kIds, true>(p, zb, rg, u, v, o, S); break;
+    }
+    return;
+  }
   switch (p.lik.window) {
     case 0: window_sums_w<kIds, 0, false>(p, zb, rg, u, v, o, S); break;
     case 1: window_sums_w<kIds, 1, false>(p, zb, rg, u, v, o, S); break;
